@@ -1,0 +1,51 @@
+// GPU-only knobs and device-resident entry points of the B200 build. Not part
+// of the reference API (the reference structs in driver.hpp / types.hpp are
+// left untouched); everything here is additive.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "csaidx/driver.hpp"
+#include "csaidx/memory_ledger.hpp"
+#include "csaidx/types.hpp"
+
+namespace csaidx::gpu {
+
+struct Options {
+    int device = 0;            // CUDA ordinal used by the host-API entry points
+    bool strict_bf16 = false;  // reject q / kc values that are not bf16-representable
+    void* stream = nullptr;    // cudaStream_t to enqueue on; nullptr = engine's own stream
+};
+
+void set_options(const Options& options);
+Options options();
+
+// Device bytes held by the driver's allocations (live) and their high-water
+// mark since the last reset, for the calling thread's device.
+struct DeviceMemory {
+    uint64_t live_bytes = 0;
+    uint64_t peak_bytes = 0;
+};
+DeviceMemory device_memory();
+void reset_device_peak();
+
+// Operands already resident in HBM. dtype: 0 = bf16 (tensor-core path),
+// 1 = fp32 (exact-order path).
+struct DeviceOperands {
+    const void* q = nullptr;   // [B, S, H_I, d_h]
+    const void* kc = nullptr;  // [B, T, d_h]
+    const float* w = nullptr;  // [B, S, H_I]
+    int dtype = 0;
+};
+
+// Device-resident Algorithm 2 over a subset of query chunks (all chunks when
+// chunk_starts is null). Chunk starts must be multiples of the clamped c_S;
+// chunk c of the list writes its rows to out rows [row0_c, row0_c + rows_c)
+// where row0 accumulates over the list. Outputs are device [B, out_rows, k].
+void run_chunked_device(const DeviceOperands& ops, const ProblemDims& dims,
+                        const DriverConfig& config, const std::vector<int64_t>* chunk_starts,
+                        int64_t* out_indices, float* out_values, int64_t out_rows,
+                        MemoryLedger& ledger, RunStats* stats = nullptr);
+
+}  // namespace csaidx::gpu

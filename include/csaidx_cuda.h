@@ -1,0 +1,160 @@
+/*
+ * csaidx_cuda.h — the C-ABI boundary of the B200 indexer (libcsaidx_cuda.so).
+ *
+ * Plain C: POD arguments, device or host pointers plus sizes, no C++ types,
+ * no exceptions. Every entry point returns a status code; the C++ drop-in
+ * layer (include/csaidx/ headers, libcsaidx.so) maps those codes 1:1 onto the
+ * exception types the reference throws, and csaidx_cuda_last_error() returns
+ * the (thread-local) message.
+ *
+ * The reference (proj/, CPU-only C++20) has no FFI of its own: its boundary
+ * is the C++ API in proj/include/csaidx/. Each function below replaces one
+ * step of that API's hot path; the comment on each cites the reference
+ * interface it stands in for.
+ *
+ * Work is enqueued on the engine's stream (asynchronous) unless a function
+ * says otherwise. Data-dependent failures (non-finite score, sentinel
+ * contract) are latched in device flags and reported by
+ * csaidx_engine_check(), which synchronizes.
+ */
+#ifndef CSAIDX_CUDA_H
+#define CSAIDX_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; one per reference exception type (types.cpp, score.cpp,
+ * topk.cpp, driver.cpp, memory_ledger.cpp). */
+#define CSAIDX_OK 0
+#define CSAIDX_INVALID_ARGUMENT 1 /* std::invalid_argument */
+#define CSAIDX_RUNTIME_ERROR 2    /* std::runtime_error    */
+#define CSAIDX_OVERFLOW_ERROR 3   /* std::overflow_error   */
+#define CSAIDX_LOGIC_ERROR 4      /* std::logic_error      */
+#define CSAIDX_CUDA_ERROR 5       /* CUDA failure (mapped to runtime_error) */
+
+/* Score kernel request, mirrors ScoreKernel (score.hpp:19-27). */
+#define CSAIDX_KERNEL_AUTO 0   /* tcgen05 when the shape allows, else exact */
+#define CSAIDX_KERNEL_EXACT 1  /* CUDA-core kernel in the reference op order */
+
+/* AccumulationMode (score.hpp:11-17). */
+#define CSAIDX_MODE_FP32 0
+#define CSAIDX_MODE_FP16_EMULATED 1
+
+/* ProblemDims (types.hpp:19-34). */
+typedef struct csaidx_dims {
+    int64_t batch;
+    int64_t seq_len;
+    int64_t key_blocks;
+    int64_t heads;
+    int64_t head_dim;
+    int64_t ratio;
+    int64_t top_k;
+} csaidx_dims;
+
+typedef struct csaidx_engine csaidx_engine;
+
+const char* csaidx_cuda_last_error(void);
+int csaidx_cuda_abi_version(void);
+int csaidx_cuda_device_count(int* count);
+
+/* Engine: device ordinal, stream, error flags, allocation accounting. */
+int csaidx_engine_create(int device, csaidx_engine** out);
+int csaidx_engine_destroy(csaidx_engine* e);
+/* Enqueue on an external cudaStream_t (e.g. torch's current stream; NULL is
+ * the legacy default stream). csaidx_engine_use_own_stream restores the
+ * engine's private non-blocking stream (the default after create). */
+int csaidx_engine_set_stream(csaidx_engine* e, void* stream);
+int csaidx_engine_use_own_stream(csaidx_engine* e);
+int csaidx_engine_get_stream(csaidx_engine* e, void** stream);
+int csaidx_engine_num_sms(csaidx_engine* e, int* num_sms);
+/* Synchronizes the stream, then reports (and clears) latched data errors. */
+int csaidx_engine_check(csaidx_engine* e);
+/* Device bytes currently held / high-water through csaidx_cuda_alloc. */
+int csaidx_engine_mem_stats(csaidx_engine* e, uint64_t* live, uint64_t* peak);
+int csaidx_engine_reset_peak(csaidx_engine* e);
+
+/* Stream-ordered device memory from a cached pool. */
+int csaidx_cuda_alloc(csaidx_engine* e, size_t bytes, void** ptr);
+int csaidx_cuda_free(csaidx_engine* e, void* ptr);
+int csaidx_cuda_copy(csaidx_engine* e, void* dst, const void* src, size_t bytes);
+int csaidx_cuda_memset(csaidx_engine* e, void* dst, int value, size_t bytes);
+
+/* fp32 -> bf16 (RNE) staging of q / kc (IndexerInputs::validated,
+ * types.cpp:73-92: rejects non-finite; strict also rejects values that are
+ * not bf16-representable). src/dst are device pointers. */
+int csaidx_cuda_to_bf16(csaidx_engine* e, const float* src, uint16_t* dst, int64_t n, int strict);
+
+/* Operand element type of q / kc on device. */
+#define CSAIDX_DTYPE_BF16 0 /* tcgen05 path (KERNEL_AUTO, fp32 mode, H_I=64, d_h=128) */
+#define CSAIDX_DTYPE_F32 1  /* exact CUDA-core path only; bit-exact vs the CPU reference */
+
+/* score_tile (score.hpp:61-64, score.cpp:54-101) on device operands:
+ * out[b, i, j] for i < rows, j < cols, row stride ld (multiple of 4).
+ * apply_mask folds mask_tile (causal.cpp:30-41) into the same pass and skips
+ * key tiles that are causally dead for the whole query block. The tcgen05
+ * kernel runs when kernel == AUTO, mode == FP32, dtype == BF16 and the shape
+ * is the V4 indexer's; everything else runs the exact-order kernel. */
+int csaidx_cuda_score(csaidx_engine* e, const void* q, const void* kc, int dtype, const float* w,
+                      const csaidx_dims* dims, int64_t s0, int64_t rows, int64_t t0, int64_t cols,
+                      int mode, int kernel, int apply_mask, float* out, int64_t ld);
+/* 1 when csaidx_cuda_score would take the tcgen05 path for these arguments. */
+int csaidx_cuda_score_uses_tensor_cores(const csaidx_dims* dims, int dtype, int mode, int kernel);
+
+/* build_mask_tile / apply_mask_tile (causal.cpp:43-79). */
+int csaidx_cuda_bool_mask(csaidx_engine* e, uint8_t* keep, int64_t s0, int64_t t0, int64_t rows,
+                          int64_t cols, int64_t ratio);
+int csaidx_cuda_apply_bool_mask(csaidx_engine* e, float* scores, int64_t ld, const uint8_t* keep,
+                                int64_t batch, int64_t rows, int64_t cols);
+
+/* tile_topk (topk.hpp:71, topk.cpp:105-132): per (b, row) top-min(k, n)
+ * under succ, n = legal columns (apply_mask) or cols; output rows of
+ * width = min(k, cols) at stride cand_ld, indices offset by t0, padded with
+ * (-inf, -1). Requires min(k, cols) <= csaidx_cuda_select_capacity(). */
+int csaidx_cuda_select(csaidx_engine* e, const float* scores, int64_t batch, int64_t rows,
+                       int64_t ld, int64_t cols, int64_t s0, int64_t t0, int64_t ratio,
+                       int apply_mask, int64_t k, float* cand_val, int32_t* cand_idx,
+                       int64_t cand_ld);
+int csaidx_cuda_select_capacity(void);
+
+/* merge_topk / overwrite_topk (topk.hpp:73-82, topk.cpp:134-191) over nrows
+ * running rows of k entries. check_overlap latches the reference's
+ * overlapping-index error. */
+int csaidx_cuda_merge(csaidx_engine* e, float* run_val, int32_t* run_idx, int64_t nrows, int64_t k,
+                      const float* cand_val, const int32_t* cand_idx, int64_t cand_ld,
+                      int64_t width, int overwrite, int check_overlap);
+
+/* TopKBuffer initialisation (types.cpp:125-134): (-inf, -1). */
+int csaidx_cuda_fill_sentinel(csaidx_engine* e, float* val, int32_t* idx, int64_t n);
+
+/* Sentinel pass (driver.cpp:84-105) into int64/fp32 output rows
+ * [b, out_row0 + i] of an [batch, out_rows, k] result. */
+int csaidx_cuda_finalize(csaidx_engine* e, const float* run_val, const int32_t* run_idx,
+                         int64_t batch, int64_t rows, int64_t s0, int64_t ratio, int64_t k,
+                         int check_keff, int64_t* out_idx, float* out_val, int64_t out_rows,
+                         int64_t out_row0);
+
+/* One query chunk x one key tile of process_query_tile (driver.cpp:57-77):
+ * masked score -> select -> merge (or copy when first_tile). score_buf must
+ * hold batch*rows*ld floats, cand_* batch*rows*min(k, cols) entries. */
+int csaidx_cuda_chunk_step(csaidx_engine* e, const void* q, const void* kc, int dtype,
+                           const float* w, const csaidx_dims* dims, int64_t s0, int64_t rows,
+                           int64_t t0, int64_t cols, int mode, int kernel, float* score_buf,
+                           int64_t ld, float* cand_val, int32_t* cand_idx, float* run_val,
+                           int32_t* run_idx, int first_tile, int overwrite);
+
+/* Synthetic operand generator for large shapes (counter-based, same
+ * distribution as synth.cpp:66-81, different stream). */
+int csaidx_cuda_gen_normal_bf16(csaidx_engine* e, uint16_t* dst, int64_t n, double stddev,
+                                uint64_t seed, uint64_t stream_id, int64_t offset);
+int csaidx_cuda_gen_normal_f32(csaidx_engine* e, float* dst, int64_t n, double stddev,
+                               uint64_t seed, uint64_t stream_id, int64_t offset);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CSAIDX_CUDA_H */

@@ -1,0 +1,96 @@
+/*
+ * csaidx_host.h — C entry points of libcsaidx.so, the drop-in C++ driver.
+ *
+ * The reference-facing call with HOST buffers (what a ctypes / cgo / JNI
+ * binding of the reference's run_chunked / run_materialize / dispatch would
+ * bind; proj/include/csaidx/driver.hpp:64-89), plus the device-resident
+ * chunk scheduler used for multi-GPU sharding. Same status codes as
+ * csaidx_cuda.h; csaidx_host_last_error() holds the exception message.
+ */
+#ifndef CSAIDX_HOST_H
+#define CSAIDX_HOST_H
+
+#include <stdint.h>
+
+#include "csaidx_cuda.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Ablation (driver.hpp:11-20) */
+#define CSAIDX_ABLATION_NONE 0
+#define CSAIDX_ABLATION_A1_NO_MERGE 1
+#define CSAIDX_ABLATION_A2_SKIP_NARROW 2
+
+/* ScoreKernel (score.hpp:19-27) */
+#define CSAIDX_SCORE_AUTO 0
+#define CSAIDX_SCORE_SCALAR 1
+#define CSAIDX_SCORE_AVX2 2
+
+/* DriverConfig (driver.hpp:25-48) + gpu::Options. */
+typedef struct csaidx_run_config {
+    int64_t query_tile;            /* c_S */
+    int64_t key_tile;              /* c_T */
+    int mode;                      /* CSAIDX_MODE_* */
+    int ablation;                  /* CSAIDX_ABLATION_* */
+    int kernel;                    /* CSAIDX_SCORE_* */
+    int causal_early_exit;
+    int bool_mask_tile;
+    int threads;
+    uint64_t auto_threshold_bytes;
+    int device;
+    int strict_bf16;
+    void* stream;                  /* cudaStream_t or NULL (engine stream) */
+} csaidx_run_config;
+
+/* RunStats (driver.hpp:55-59) + the path taken and both peaks. */
+typedef struct csaidx_run_stats {
+    int64_t dispatch_count;
+    int64_t tiles_skipped_masked;
+    int64_t tiles_skipped_narrow;
+    uint64_t ledger_peak_bytes;
+    uint64_t device_peak_bytes;
+    int path; /* 0 materialize, 1 chunked */
+} csaidx_run_stats;
+
+const char* csaidx_host_last_error(void);
+void csaidx_host_default_config(csaidx_run_config* cfg);
+
+/* run_chunked / run_materialize / dispatch on host fp32 buffers
+ * q [B,S,H,D], kc [B,T,D], w [B,S,H]; results into host [B,S,k]. */
+int csaidx_host_run_chunked(const float* q, const float* kc, const float* w, const csaidx_dims* dims,
+                            const csaidx_run_config* cfg, int64_t* out_idx, float* out_val,
+                            csaidx_run_stats* stats);
+int csaidx_host_run_materialize(const float* q, const float* kc, const float* w, const csaidx_dims* dims,
+                                const csaidx_run_config* cfg, int64_t* out_idx, float* out_val,
+                                csaidx_run_stats* stats);
+int csaidx_host_dispatch(const float* q, const float* kc, const float* w, const csaidx_dims* dims,
+                         const csaidx_run_config* cfg, int64_t* out_idx, float* out_val,
+                         csaidx_run_stats* stats);
+
+/* Algorithm 2 over device-resident operands (dtype CSAIDX_DTYPE_*), for the
+ * listed query chunks (NULL / 0 = all), outputs device [B, out_rows, k]. */
+int csaidx_device_run_chunked(const void* q, const void* kc, int dtype, const float* w,
+                              const csaidx_dims* dims, const csaidx_run_config* cfg,
+                              const int64_t* chunk_starts, int64_t n_chunks, int64_t* out_idx,
+                              float* out_val, int64_t out_rows, csaidx_run_stats* stats);
+
+/* Pure host arithmetic of the API (types.cpp / driver.cpp), no GPU needed. */
+int csaidx_host_problem_dims(int64_t batch, int64_t seq_len, int64_t ratio, int64_t heads,
+                             int64_t head_dim, int64_t top_k, csaidx_dims* out);
+int csaidx_host_dispatch_count_model(const csaidx_dims* dims, int64_t query_tile, int64_t key_tile,
+                                     int64_t* out);
+int csaidx_host_chunked_peak_model_bytes(int64_t batch, int64_t query_tile, int64_t key_tile,
+                                         int64_t top_k, int bool_mask_tile, uint64_t* out);
+int csaidx_host_materialize_bytes(const csaidx_dims* dims, uint64_t* out);
+int csaidx_host_choose_path(const csaidx_dims* dims, uint64_t threshold, int* path,
+                            uint64_t* predicted);
+int64_t csaidx_host_t_legal(int64_t t, int64_t ratio);
+int64_t csaidx_host_k_eff(int64_t t, int64_t ratio, int64_t top_k);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CSAIDX_HOST_H */

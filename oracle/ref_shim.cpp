@@ -1,0 +1,229 @@
+// ref_shim.cpp — TEST / BASELINE INFRASTRUCTURE ONLY.
+//
+// extern "C" entry points over the *unmodified* reference library, compiled
+// from the sources under /root/reference/proj/src by oracle/Makefile into
+// oracle/_ref/libcsaidx_ref.so (namespace renamed csaidx -> csaidx_ref by
+// -Dcsaidx=csaidx_ref so it can never collide with the GPU library). Used to
+// pin the C oracle (golden fixtures) and to time the reference CPU path for
+// bench.py's cpu_baseline / --impl reference leg. No reference source is
+// copied into this repository; this file only calls the reference's public
+// API (proj/include/csaidx/*.hpp).
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <thread>
+#include <vector>
+
+#include "csaidx/causal.hpp"
+#include "csaidx/driver.hpp"
+#include "csaidx/half.hpp"
+#include "csaidx/memory_ledger.hpp"
+#include "csaidx/score.hpp"
+#include "csaidx/synth.hpp"
+#include "csaidx/topk.hpp"
+#include "csaidx/types.hpp"
+
+using namespace csaidx;
+
+namespace {
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return 1;
+    } catch (const std::overflow_error&) {
+        return 3;
+    } catch (const std::logic_error&) {
+        return 4;
+    } catch (const std::runtime_error&) {
+        return 2;
+    } catch (...) {
+        return 5;
+    }
+}
+
+IndexerInputs wrap(const float* q, const float* kc, const float* w, const ProblemDims& d) {
+    IndexerInputs in;
+    in.q.assign(q, q + d.q_elems());
+    in.kc.assign(kc, kc + d.kc_elems());
+    in.w.assign(w, w + d.w_elems());
+    return in;
+}
+
+void unwrap(const TopKResult& r, int64_t* idx, float* val) {
+    std::memcpy(idx, r.indices.data(), r.indices.size() * sizeof(int64_t));
+    std::memcpy(val, r.values.data(), r.values.size() * sizeof(float));
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_generate(int64_t B, int64_t S, int64_t m, int64_t H, int64_t D, int64_t k, uint64_t seed, float* q,
+                 float* kc, float* w) {
+    return guarded([&] {
+        const ProblemDims d = ProblemDims::create(B, S, m, H, D, k);
+        const IndexerInputs in = generate_inputs({d, seed, 7168});
+        std::memcpy(q, in.q.data(), in.q.size() * sizeof(float));
+        std::memcpy(kc, in.kc.data(), in.kc.size() * sizeof(float));
+        std::memcpy(w, in.w.data(), in.w.size() * sizeof(float));
+    });
+}
+
+int ref_splitmix_first(uint64_t state, int n, uint64_t* out) {
+    // Xoshiro256pp seeded with (seed=state, stream=0) exposes splitmix64 only
+    // indirectly; reproduce the published-vector check through the stream.
+    return guarded([&] {
+        Xoshiro256pp g(state, 0);
+        for (int i = 0; i < n; ++i) out[i] = g.next();
+    });
+}
+
+int ref_xoshiro(uint64_t seed, uint64_t stream, int n, uint64_t* out) {
+    return guarded([&] {
+        Xoshiro256pp g(seed, stream);
+        for (int i = 0; i < n; ++i) out[i] = g.next();
+    });
+}
+
+int ref_half_round(const float* x, int64_t n, float* out) {
+    return guarded([&] {
+        for (int64_t i = 0; i < n; ++i) out[i] = half_round(x[i]);
+    });
+}
+
+int ref_score_tile(const float* q, const float* kc, const float* w, int64_t B, int64_t S, int64_t m, int64_t H,
+                   int64_t D, int64_t s0, int64_t t0, int64_t rows, int64_t cols, int fp16, int scalar, float* out) {
+    return guarded([&] {
+        const ProblemDims d = ProblemDims::create(B, S, m, H, D, 1);
+        const IndexerInputs in = wrap(q, kc, w, d);
+        MemoryLedger ledger;
+        const ScoreTile t = score_tile(in, d, s0, t0, rows, cols,
+                                       fp16 ? AccumulationMode::fp16_emulated : AccumulationMode::fp32, ledger,
+                                       scalar ? ScoreKernel::scalar : ScoreKernel::auto_detect);
+        std::memcpy(out, t.scores.data(), t.scores.size() * sizeof(float));
+    });
+}
+
+int ref_run_materialize(const float* q, const float* kc, const float* w, int64_t B, int64_t S, int64_t m, int64_t H,
+                        int64_t D, int64_t k, int fp16, int64_t* idx, float* val, uint64_t* peak) {
+    return guarded([&] {
+        const ProblemDims d = ProblemDims::create(B, S, m, H, D, k);
+        const IndexerInputs in = wrap(q, kc, w, d);
+        MemoryLedger ledger;
+        const TopKResult r =
+            run_materialize(in, d, fp16 ? AccumulationMode::fp16_emulated : AccumulationMode::fp32, ledger);
+        unwrap(r, idx, val);
+        if (peak) *peak = ledger.peak_bytes();
+    });
+}
+
+int ref_run_chunked(const float* q, const float* kc, const float* w, int64_t B, int64_t S, int64_t m, int64_t H,
+                    int64_t D, int64_t k, int64_t cs, int64_t ct, int fp16, int ablation, int early_exit,
+                    int bool_mask, int threads, int64_t* idx, float* val, int64_t* stats3, uint64_t* peak) {
+    return guarded([&] {
+        const ProblemDims d = ProblemDims::create(B, S, m, H, D, k);
+        const IndexerInputs in = wrap(q, kc, w, d);
+        MemoryLedger ledger;
+        DriverConfig cfg;
+        cfg.tile = TileConfig{cs, ct};
+        cfg.mode = fp16 ? AccumulationMode::fp16_emulated : AccumulationMode::fp32;
+        cfg.ablation = ablation == 1 ? Ablation::a1_no_merge
+                                     : (ablation == 2 ? Ablation::a2_skip_narrow : Ablation::none);
+        cfg.causal_early_exit = early_exit != 0;
+        cfg.bool_mask_tile = bool_mask != 0;
+        cfg.threads = threads;
+        RunStats st;
+        const TopKResult r = run_chunked(in, d, cfg, ledger, &st);
+        unwrap(r, idx, val);
+        if (stats3) {
+            stats3[0] = st.dispatch_count;
+            stats3[1] = st.tiles_skipped_masked;
+            stats3[2] = st.tiles_skipped_narrow;
+        }
+        if (peak) *peak = ledger.peak_bytes();
+    });
+}
+
+int64_t ref_dispatch_count_model(int64_t S, int64_t m, int64_t cs, int64_t ct) {
+    int64_t out = -1;
+    guarded([&] { out = dispatch_count_model(ProblemDims::create(1, S, m, 1, 1, 1), TileConfig{cs, ct}); });
+    return out;
+}
+
+uint64_t ref_chunked_peak_model_bytes(int64_t B, int64_t cs, int64_t ct, int64_t k, int bool_mask) {
+    uint64_t out = 0;
+    guarded([&] { out = chunked_peak_model_bytes(B, TileConfig{cs, ct}, k, bool_mask != 0); });
+    return out;
+}
+
+// CPU baseline: the body of process_query_tile (driver.cpp:36-106) executed
+// through the reference's public engine API (score_tile -> mask_tile ->
+// tile_topk -> merge_topk) over a deterministic sample of n_tiles query tiles
+// of an (S, m, H, D, k) instance spread evenly over t, each with its full
+// causal key range, on `threads` std::threads. q rows of the sampled tiles
+// and the full kc come from the reference generator. Reports wall seconds
+// and causal-legal pairs scored.
+int ref_sample_chunked(int64_t S, int64_t m, int64_t H, int64_t D, int64_t k, int64_t cs, int64_t ct,
+                       int64_t n_tiles, int threads, uint64_t seed, double* seconds, double* pairs) {
+    return guarded([&] {
+        const int64_t T = S / m;
+        ProblemDims d;  // compact instance: only the sampled rows, every key block
+        d.batch = 1;
+        d.seq_len = n_tiles * cs;
+        d.key_blocks = T;
+        d.heads = H;
+        d.head_dim = D;
+        d.ratio = m;
+        d.top_k = k;
+        IndexerInputs in;
+        in.q.resize(static_cast<size_t>(d.q_elems()));
+        in.kc.resize(static_cast<size_t>(d.kc_elems()));
+        in.w.resize(static_cast<size_t>(d.w_elems()));
+        const double unit = 1.0 / std::sqrt(static_cast<double>(D));
+        fill_gaussian(in.q, unit, seed, kStreamQueries);
+        fill_gaussian(in.kc, unit, seed, kStreamKeys);
+        fill_gaussian(in.w, 1.0 / std::sqrt(static_cast<double>(D * H)), seed, kStreamWeights);
+        std::vector<int64_t> starts(static_cast<size_t>(n_tiles));
+        double legal_pairs = 0.0;
+        for (int64_t i = 0; i < n_tiles; ++i) {
+            int64_t s0 = (2 * i + 1) * S / (2 * n_tiles);
+            s0 = std::min(S - cs, s0 / cs * cs);
+            starts[static_cast<size_t>(i)] = s0;
+            for (int64_t r = 0; r < cs; ++r) legal_pairs += static_cast<double>(std::min(T, t_legal(s0 + r, m)));
+        }
+        std::atomic<int64_t> next{0};
+        MemoryLedger ledger;
+        auto worker = [&] {
+            for (int64_t i = next.fetch_add(1); i < n_tiles; i = next.fetch_add(1)) {
+                const int64_t s0 = starts[static_cast<size_t>(i)];
+                const int64_t local = i * cs;
+                TopKBuffer buf(1, cs, k, ledger);
+                for (int64_t t0 = 0; t0 < T; t0 += ct) {
+                    const int64_t cols = std::min(ct, T - t0);
+                    if (tile_fully_masked(s0, cs, t0, m)) break;
+                    ScoreTile tile = score_tile(in, d, local, t0, cs, cols, AccumulationMode::fp32, ledger);
+                    tile.s0 = s0;  // causal position of these rows in the full instance
+                    mask_tile(tile, m);
+                    TileTopK sel = tile_topk(tile, k, ledger);
+                    for (int64_t r = 0; r < cs; ++r) merge_topk(buf, 0, r, sel.row(0, r));
+                }
+            }
+        };
+        const auto t_start = std::chrono::steady_clock::now();
+        std::vector<std::thread> pool;
+        for (int t = 0; t < std::max(1, threads); ++t) pool.emplace_back(worker);
+        for (auto& t : pool) t.join();
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+        *pairs = legal_pairs;
+    });
+}
+
+}  // extern "C"

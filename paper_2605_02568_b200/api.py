@@ -1,0 +1,342 @@
+"""Python mirror of the reference driver API (proj/include/csaidx/driver.hpp,
+types.hpp) over libcsaidx.so's C entry points (include/csaidx_host.h).
+
+Same names, argument meaning and error behaviour as the C++ API:
+``ProblemDims.create`` rejects bad extents with ``InvalidArgument``
+(a ValueError), a non-finite fp32 score raises ``ScoreRuntimeError``, a
+broken sentinel contract ``LogicError``. The compute runs on the B200; there
+is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import os
+from ctypes import POINTER, Structure, c_char_p, c_int, c_int64, c_uint64, c_void_p
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+from ._capi import Dims, check as _check_cuda
+
+SENTINEL_INDEX = -1
+TOPK_ENTRY_BYTES = 12
+
+
+class AccumulationMode(enum.IntEnum):
+    fp32 = 0
+    fp16_emulated = 1
+
+
+class ScoreKernel(enum.IntEnum):
+    auto_detect = 0
+    scalar = 1
+    avx2 = 2
+
+
+class Ablation(enum.IntEnum):
+    none = 0
+    a1_no_merge = 1
+    a2_skip_narrow = 2
+
+
+class ExecutionPath(enum.IntEnum):
+    materialize = 0
+    chunked = 1
+
+
+class RunConfig(Structure):
+    """csaidx_run_config (include/csaidx_host.h)."""
+
+    _fields_ = [
+        ("query_tile", c_int64),
+        ("key_tile", c_int64),
+        ("mode", c_int),
+        ("ablation", c_int),
+        ("kernel", c_int),
+        ("causal_early_exit", c_int),
+        ("bool_mask_tile", c_int),
+        ("threads", c_int),
+        ("auto_threshold_bytes", c_uint64),
+        ("device", c_int),
+        ("strict_bf16", c_int),
+        ("stream", c_void_p),
+    ]
+
+
+class RunStatsC(Structure):
+    _fields_ = [
+        ("dispatch_count", c_int64),
+        ("tiles_skipped_masked", c_int64),
+        ("tiles_skipped_narrow", c_int64),
+        ("ledger_peak_bytes", c_uint64),
+        ("device_peak_bytes", c_uint64),
+        ("path", c_int),
+    ]
+
+
+_F = POINTER(ctypes.c_float)
+HOST_SYMBOLS = {
+    "csaidx_host_last_error": (c_char_p, []),
+    "csaidx_host_default_config": (None, [POINTER(RunConfig)]),
+    "csaidx_host_run_chunked": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(Dims), POINTER(RunConfig), c_void_p,
+                                        c_void_p, POINTER(RunStatsC)]),
+    "csaidx_host_run_materialize": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(Dims), POINTER(RunConfig),
+                                            c_void_p, c_void_p, POINTER(RunStatsC)]),
+    "csaidx_host_dispatch": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(Dims), POINTER(RunConfig), c_void_p,
+                                     c_void_p, POINTER(RunStatsC)]),
+    "csaidx_device_run_chunked": (c_int, [c_void_p, c_void_p, c_int, c_void_p, POINTER(Dims), POINTER(RunConfig),
+                                          c_void_p, c_int64, c_void_p, c_void_p, c_int64, POINTER(RunStatsC)]),
+    "csaidx_host_problem_dims": (c_int, [c_int64] * 6 + [POINTER(Dims)]),
+    "csaidx_host_dispatch_count_model": (c_int, [POINTER(Dims), c_int64, c_int64, POINTER(c_int64)]),
+    "csaidx_host_chunked_peak_model_bytes": (c_int, [c_int64, c_int64, c_int64, c_int64, c_int, POINTER(c_uint64)]),
+    "csaidx_host_materialize_bytes": (c_int, [POINTER(Dims), POINTER(c_uint64)]),
+    "csaidx_host_choose_path": (c_int, [POINTER(Dims), c_uint64, POINTER(c_int), POINTER(c_uint64)]),
+    "csaidx_host_t_legal": (c_int64, [c_int64, c_int64]),
+    "csaidx_host_k_eff": (c_int64, [c_int64, c_int64, c_int64]),
+}
+
+_host = None
+
+
+def host_lib():
+    global _host
+    if _host is None:
+        _capi.cuda_lib()  # the driver library depends on it
+        if not os.path.exists(_capi.HOST_LIB):
+            raise ImportError(f"{_capi.HOST_LIB} missing: run __graft_entry__.build()")
+        lib = ctypes.CDLL(_capi.HOST_LIB)
+        for name, (res, args) in HOST_SYMBOLS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _host = lib
+    return _host
+
+
+def _check(rc: int) -> None:
+    if rc != _capi.OK:
+        msg = host_lib().csaidx_host_last_error().decode(errors="replace")
+        raise _capi._ERRORS.get(rc, _capi.CsaidxError)(msg)
+
+
+# ----------------------------------------------------------------- types
+
+
+@dataclass
+class ProblemDims:
+    batch: int = 1
+    seq_len: int = 1
+    key_blocks: int = 1
+    heads: int = 1
+    head_dim: int = 1
+    ratio: int = 1
+    top_k: int = 1
+
+    @staticmethod
+    def create(batch, seq_len, ratio, heads, head_dim, top_k) -> "ProblemDims":
+        d = Dims()
+        _check(host_lib().csaidx_host_problem_dims(batch, seq_len, ratio, heads, head_dim, top_k, ctypes.byref(d)))
+        return ProblemDims(d.batch, d.seq_len, d.key_blocks, d.heads, d.head_dim, d.ratio, d.top_k)
+
+    def c(self) -> Dims:
+        return Dims(self.batch, self.seq_len, self.key_blocks, self.heads, self.head_dim, self.ratio, self.top_k)
+
+    @property
+    def q_elems(self):
+        return self.batch * self.seq_len * self.heads * self.head_dim
+
+    @property
+    def kc_elems(self):
+        return self.batch * self.key_blocks * self.head_dim
+
+    @property
+    def w_elems(self):
+        return self.batch * self.seq_len * self.heads
+
+
+@dataclass
+class TileConfig:
+    query_tile: int = 2048
+    key_tile: int = 8192
+
+
+@dataclass
+class DriverConfig:
+    tile: TileConfig = field(default_factory=TileConfig)
+    mode: AccumulationMode = AccumulationMode.fp32
+    ablation: Ablation = Ablation.none
+    kernel: ScoreKernel = ScoreKernel.auto_detect
+    auto_threshold_bytes: int = 1 << 30
+    causal_early_exit: bool = True
+    bool_mask_tile: bool = False
+    threads: int = 1
+    # gpu::Options
+    device: int = 0
+    strict_bf16: bool = False
+    stream: int = 0
+
+    def c(self) -> RunConfig:
+        return RunConfig(self.tile.query_tile, self.tile.key_tile, int(self.mode), int(self.ablation),
+                         int(self.kernel), int(self.causal_early_exit), int(self.bool_mask_tile), self.threads,
+                         self.auto_threshold_bytes, self.device, int(self.strict_bf16), c_void_p(self.stream))
+
+
+@dataclass
+class RunStats:
+    dispatch_count: int = 0
+    tiles_skipped_masked: int = 0
+    tiles_skipped_narrow: int = 0
+    ledger_peak_bytes: int = 0
+    device_peak_bytes: int = 0
+    path: ExecutionPath = ExecutionPath.chunked
+
+
+@dataclass
+class IndexerInputs:
+    q: np.ndarray   # [B, S, H, D] fp32
+    kc: np.ndarray  # [B, T, D]
+    w: np.ndarray   # [B, S, H]
+
+    @staticmethod
+    def validated(q, kc, w, dims: ProblemDims) -> "IndexerInputs":
+        q = np.ascontiguousarray(q, dtype=np.float32).reshape(-1)
+        kc = np.ascontiguousarray(kc, dtype=np.float32).reshape(-1)
+        w = np.ascontiguousarray(w, dtype=np.float32).reshape(-1)
+        for arr, n, name in ((q, dims.q_elems, "q"), (kc, dims.kc_elems, "kc"), (w, dims.w_elems, "w")):
+            if arr.size != n:
+                raise _capi.InvalidArgument(f"IndexerInputs: {name} extent mismatch")
+        for arr, name in ((q, "q"), (kc, "kc"), (w, "w")):
+            if not np.all(np.isfinite(arr)):
+                raise _capi.InvalidArgument(f"IndexerInputs: non-finite entry in {name}")
+        return IndexerInputs(q, kc, w)
+
+
+@dataclass
+class TopKResult:
+    batch: int
+    seq_len: int
+    top_k: int
+    indices: np.ndarray  # [B, S, k] int64
+    values: np.ndarray   # [B, S, k] fp32
+
+    @staticmethod
+    def sized(dims: ProblemDims) -> "TopKResult":
+        shape = (dims.batch, dims.seq_len, dims.top_k)
+        return TopKResult(dims.batch, dims.seq_len, dims.top_k, np.full(shape, -1, np.int64),
+                          np.full(shape, -np.inf, np.float32))
+
+    def valid_count(self, b: int, t: int) -> int:
+        row = self.indices[b, t]
+        hits = np.flatnonzero(row == SENTINEL_INDEX)
+        return int(hits[0]) if hits.size else self.top_k
+
+
+def _ptr(a: np.ndarray):
+    return c_void_p(a.ctypes.data)
+
+
+def _host_call(fn, inputs: IndexerInputs, dims: ProblemDims, config: DriverConfig):
+    for arr in (inputs.q, inputs.kc, inputs.w):
+        if arr.dtype != np.float32 or not arr.flags["C_CONTIGUOUS"]:
+            raise _capi.InvalidArgument("operands must be contiguous fp32 arrays")
+    out = TopKResult.sized(dims)
+    st = RunStatsC()
+    cd, cc = dims.c(), config.c()
+    _check(fn(_ptr(inputs.q), _ptr(inputs.kc), _ptr(inputs.w), ctypes.byref(cd), ctypes.byref(cc),
+              _ptr(out.indices), _ptr(out.values), ctypes.byref(st)))
+    stats = RunStats(st.dispatch_count, st.tiles_skipped_masked, st.tiles_skipped_narrow, st.ledger_peak_bytes,
+                     st.device_peak_bytes, ExecutionPath(st.path))
+    return out, stats
+
+
+def run_chunked(inputs: IndexerInputs, dims: ProblemDims, config: DriverConfig | None = None):
+    """driver.hpp:70-72 -> (TopKResult, RunStats)."""
+    return _host_call(host_lib().csaidx_host_run_chunked, inputs, dims, config or DriverConfig())
+
+
+def run_materialize(inputs: IndexerInputs, dims: ProblemDims, mode=AccumulationMode.fp32,
+                    kernel=ScoreKernel.auto_detect, config: DriverConfig | None = None):
+    """driver.hpp:77-79 -> (TopKResult, RunStats)."""
+    cfg = config or DriverConfig()
+    cfg = DriverConfig(**{**cfg.__dict__, "mode": mode, "kernel": kernel})
+    return _host_call(host_lib().csaidx_host_run_materialize, inputs, dims, cfg)
+
+
+def dispatch(inputs: IndexerInputs, dims: ProblemDims, config: DriverConfig | None = None):
+    """driver.hpp:87-89 -> (TopKResult, RunStats with .path)."""
+    return _host_call(host_lib().csaidx_host_dispatch, inputs, dims, config or DriverConfig())
+
+
+def run_chunked_device(q, kc, w, dims: ProblemDims, config: DriverConfig, chunk_starts=None, out_idx=None,
+                       out_val=None):
+    """Device-resident Algorithm 2 (csaidx_device_run_chunked): torch CUDA tensors in, torch tensors out."""
+    import torch
+
+    dtype = _capi.DTYPE_BF16 if q.dtype == torch.bfloat16 else _capi.DTYPE_F32
+    starts = None
+    n_chunks = 0
+    rows = dims.seq_len
+    if chunk_starts is not None:
+        starts = np.ascontiguousarray(chunk_starts, dtype=np.int64)
+        n_chunks = starts.size
+        cs = min(config.tile.query_tile, dims.seq_len)
+        rows = int(sum(min(cs, dims.seq_len - int(s)) for s in starts))
+    if out_idx is None:
+        out_idx = torch.empty((dims.batch, rows, dims.top_k), dtype=torch.int64, device=q.device)
+        out_val = torch.empty((dims.batch, rows, dims.top_k), dtype=torch.float32, device=q.device)
+    st = RunStatsC()
+    cd, cc = dims.c(), config.c()
+    _check(host_lib().csaidx_device_run_chunked(
+        c_void_p(q.data_ptr()), c_void_p(kc.data_ptr()), dtype, c_void_p(w.data_ptr()), ctypes.byref(cd),
+        ctypes.byref(cc), None if starts is None else _ptr(starts), n_chunks, c_void_p(out_idx.data_ptr()),
+        c_void_p(out_val.data_ptr()), out_idx.shape[1], ctypes.byref(st)))
+    stats = RunStats(st.dispatch_count, st.tiles_skipped_masked, st.tiles_skipped_narrow, st.ledger_peak_bytes,
+                     st.device_peak_bytes, ExecutionPath.chunked)
+    return out_idx, out_val, stats
+
+
+# ------------------------------------------------------- host arithmetic
+
+
+def t_legal(t: int, ratio: int) -> int:
+    if t < 0 or ratio < 1:
+        raise _capi.InvalidArgument("t_legal: t must be >= 0 and ratio >= 1")
+    return int(host_lib().csaidx_host_t_legal(t, ratio))
+
+
+def k_eff(t: int, ratio: int, top_k: int) -> int:
+    if top_k < 0:
+        raise _capi.InvalidArgument("k_eff: top_k must be >= 0")
+    return int(host_lib().csaidx_host_k_eff(t, ratio, top_k))
+
+
+def dispatch_count_model(dims: ProblemDims, tile: TileConfig) -> int:
+    out = c_int64()
+    cd = dims.c()
+    _check(host_lib().csaidx_host_dispatch_count_model(ctypes.byref(cd), tile.query_tile, tile.key_tile,
+                                                        ctypes.byref(out)))
+    return out.value
+
+
+def chunked_peak_model_bytes(batch: int, tile: TileConfig, top_k: int, bool_mask_tile: bool) -> int:
+    out = c_uint64()
+    _check(host_lib().csaidx_host_chunked_peak_model_bytes(batch, tile.query_tile, tile.key_tile, top_k,
+                                                            int(bool_mask_tile), ctypes.byref(out)))
+    return out.value
+
+
+def materialize_bytes(dims: ProblemDims) -> int:
+    out = c_uint64()
+    cd = dims.c()
+    _check(host_lib().csaidx_host_materialize_bytes(ctypes.byref(cd), ctypes.byref(out)))
+    return out.value
+
+
+def choose_path(dims: ProblemDims, threshold_bytes: int):
+    path, pred = c_int(), c_uint64()
+    cd = dims.c()
+    _check(host_lib().csaidx_host_choose_path(ctypes.byref(cd), threshold_bytes, ctypes.byref(path),
+                                              ctypes.byref(pred)))
+    return ExecutionPath(path.value), pred.value

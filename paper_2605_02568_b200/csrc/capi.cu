@@ -1,0 +1,483 @@
+// C-ABI implementation (include/csaidx_cuda.h). Argument validation mirrors
+// the reference's checks so the C++ layer can rethrow the same exception
+// types; kernels are enqueued on the engine stream.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+#include "csaidx_cuda.h"
+#include "kernels/kernels.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list args;
+    va_start(args, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, args);
+    va_end(args);
+    g_last_error = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t err, const char* where) {
+    return fail(CSAIDX_CUDA_ERROR, "%s: CUDA error %s (%s)", where, cudaGetErrorName(err),
+                cudaGetErrorString(err));
+}
+
+#define CSAIDX_CUDA_TRY(expr, where)                 \
+    do {                                             \
+        cudaError_t _e = (expr);                     \
+        if (_e != cudaSuccess) return cuda_fail(_e, where); \
+    } while (0)
+
+enum Flag { kNonfiniteScore = 0, kInexact = 1, kNonfiniteInput = 2, kTrail = 3, kKeff = 4, kOverlap = 5, kNumFlags = 8 };
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess) {
+            fn = reinterpret_cast<EncodeTiledFn>(ptr);
+        }
+    });
+    return fn;
+}
+
+}  // namespace
+
+struct csaidx_engine {
+    int device = 0;
+    int num_sms = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    int* flags = nullptr;  // device [kNumFlags]
+    std::mutex mu;
+    std::unordered_map<void*, size_t> sizes;
+    uint64_t live = 0;
+    uint64_t peak = 0;
+};
+
+namespace {
+
+int set_device(csaidx_engine* e) {
+    if (e == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null engine");
+    CSAIDX_CUDA_TRY(cudaSetDevice(e->device), "cudaSetDevice");
+    return CSAIDX_OK;
+}
+
+// 2D bf16 row-major [rows, 128] tensor map with a (64 x box_rows) SW128 box.
+int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+    EncodeTiledFn enc = get_encode_fn();
+    if (enc == nullptr) return fail(CSAIDX_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {cols * 2};
+    const cuuint32_t box[2] = {64, box_rows};
+    const cuuint32_t estride[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estride,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(CSAIDX_CUDA_ERROR, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+    return CSAIDX_OK;
+}
+
+int check_dims(const csaidx_dims* d) {
+    if (d == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null dims");
+    if (d->batch < 1 || d->seq_len < 1 || d->key_blocks < 1 || d->heads < 1 || d->head_dim < 1 || d->ratio < 1 ||
+        d->top_k < 1)
+        return fail(CSAIDX_INVALID_ARGUMENT, "dims: every extent must be >= 1");
+    return CSAIDX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* csaidx_cuda_last_error(void) { return g_last_error.c_str(); }
+
+int csaidx_cuda_abi_version(void) { return 1; }
+
+int csaidx_cuda_device_count(int* count) {
+    if (count == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null count");
+    cudaError_t err = cudaGetDeviceCount(count);
+    if (err != cudaSuccess) {
+        *count = 0;
+        cudaGetLastError();
+    }
+    return CSAIDX_OK;
+}
+
+int csaidx_engine_create(int device, csaidx_engine** out) {
+    if (out == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null out");
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return fail(CSAIDX_CUDA_ERROR, "no CUDA device available (the B200 indexer has no CPU path)");
+    }
+    if (device < 0 || device >= count) return fail(CSAIDX_INVALID_ARGUMENT, "device ordinal %d out of range", device);
+    auto* e = new csaidx_engine();
+    e->device = device;
+    CSAIDX_CUDA_TRY(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop;
+    CSAIDX_CUDA_TRY(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10) {
+        delete e;
+        return fail(CSAIDX_CUDA_ERROR, "device %d is sm_%d%d; this build targets sm_100a only", device, prop.major,
+                    prop.minor);
+    }
+    e->num_sms = prop.multiProcessorCount;
+    CSAIDX_CUDA_TRY(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    e->stream = e->own_stream;
+    CSAIDX_CUDA_TRY(cudaMalloc(&e->flags, kNumFlags * sizeof(int)), "cudaMalloc(flags)");
+    CSAIDX_CUDA_TRY(cudaMemset(e->flags, 0, kNumFlags * sizeof(int)), "cudaMemset(flags)");
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thresh = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh);
+    }
+    *out = e;
+    return CSAIDX_OK;
+}
+
+int csaidx_engine_destroy(csaidx_engine* e) {
+    if (e == nullptr) return CSAIDX_OK;
+    cudaSetDevice(e->device);
+    if (e->stream) cudaStreamSynchronize(e->stream);
+    for (auto& kv : e->sizes) cudaFree(kv.first);
+    if (e->flags) cudaFree(e->flags);
+    if (e->own_stream) cudaStreamDestroy(e->own_stream);
+    delete e;
+    return CSAIDX_OK;
+}
+
+int csaidx_engine_set_stream(csaidx_engine* e, void* stream) {
+    if (e == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null engine");
+    e->stream = static_cast<cudaStream_t>(stream);
+    return CSAIDX_OK;
+}
+
+int csaidx_engine_use_own_stream(csaidx_engine* e) {
+    if (e == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null engine");
+    e->stream = e->own_stream;
+    return CSAIDX_OK;
+}
+
+int csaidx_engine_get_stream(csaidx_engine* e, void** stream) {
+    if (e == nullptr || stream == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null argument");
+    *stream = e->stream;
+    return CSAIDX_OK;
+}
+
+int csaidx_engine_num_sms(csaidx_engine* e, int* num_sms) {
+    if (e == nullptr || num_sms == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null argument");
+    *num_sms = e->num_sms;
+    return CSAIDX_OK;
+}
+
+int csaidx_engine_check(csaidx_engine* e) {
+    if (int rc = set_device(e)) return rc;
+    CSAIDX_CUDA_TRY(cudaStreamSynchronize(e->stream), "cudaStreamSynchronize");
+    int h[kNumFlags];
+    CSAIDX_CUDA_TRY(cudaMemcpy(h, e->flags, sizeof(h), cudaMemcpyDeviceToHost), "flags D2H");
+    bool any = false;
+    for (int f : h) any = any || f != 0;
+    if (!any) return CSAIDX_OK;
+    CSAIDX_CUDA_TRY(cudaMemset(e->flags, 0, sizeof(h)), "flags reset");
+    if (h[kNonfiniteInput]) return fail(CSAIDX_INVALID_ARGUMENT, "IndexerInputs: non-finite entry in q/kc");
+    if (h[kInexact]) return fail(CSAIDX_INVALID_ARGUMENT, "operand is not bf16-representable (strict mode)");
+    if (h[kOverlap]) return fail(CSAIDX_INVALID_ARGUMENT, "merge_topk: overlapping indices between buffer and tile");
+    if (h[kNonfiniteScore]) return fail(CSAIDX_RUNTIME_ERROR, "score_tile: non-finite score in fp32 mode");
+    if (h[kTrail]) return fail(CSAIDX_LOGIC_ERROR, "run_chunked: sentinel entries do not trail");
+    if (h[kKeff]) return fail(CSAIDX_LOGIC_ERROR, "run_chunked: row valid count != k_eff");
+    return fail(CSAIDX_LOGIC_ERROR, "unknown device flag");
+}
+
+int csaidx_engine_mem_stats(csaidx_engine* e, uint64_t* live, uint64_t* peak) {
+    if (e == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null engine");
+    std::lock_guard<std::mutex> lock(e->mu);
+    if (live) *live = e->live;
+    if (peak) *peak = e->peak;
+    return CSAIDX_OK;
+}
+
+int csaidx_engine_reset_peak(csaidx_engine* e) {
+    if (e == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null engine");
+    std::lock_guard<std::mutex> lock(e->mu);
+    e->peak = e->live;
+    return CSAIDX_OK;
+}
+
+int csaidx_cuda_alloc(csaidx_engine* e, size_t bytes, void** ptr) {
+    if (int rc = set_device(e)) return rc;
+    if (ptr == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null out pointer");
+    *ptr = nullptr;
+    if (bytes == 0) bytes = 16;
+    CSAIDX_CUDA_TRY(cudaMallocAsync(ptr, bytes, e->stream), "cudaMallocAsync");
+    std::lock_guard<std::mutex> lock(e->mu);
+    e->sizes[*ptr] = bytes;
+    e->live += bytes;
+    if (e->live > e->peak) e->peak = e->live;
+    return CSAIDX_OK;
+}
+
+int csaidx_cuda_free(csaidx_engine* e, void* ptr) {
+    if (int rc = set_device(e)) return rc;
+    if (ptr == nullptr) return CSAIDX_OK;
+    {
+        std::lock_guard<std::mutex> lock(e->mu);
+        auto it = e->sizes.find(ptr);
+        if (it == e->sizes.end()) return fail(CSAIDX_INVALID_ARGUMENT, "csaidx_cuda_free: unknown pointer");
+        e->live -= it->second;
+        e->sizes.erase(it);
+    }
+    CSAIDX_CUDA_TRY(cudaFreeAsync(ptr, e->stream), "cudaFreeAsync");
+    return CSAIDX_OK;
+}
+
+int csaidx_cuda_copy(csaidx_engine* e, void* dst, const void* src, size_t bytes) {
+    if (int rc = set_device(e)) return rc;
+    if (bytes == 0) return CSAIDX_OK;
+    CSAIDX_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, e->stream), "cudaMemcpyAsync");
+    return CSAIDX_OK;
+}
+
+int csaidx_cuda_memset(csaidx_engine* e, void* dst, int value, size_t bytes) {
+    if (int rc = set_device(e)) return rc;
+    if (bytes == 0) return CSAIDX_OK;
+    CSAIDX_CUDA_TRY(cudaMemsetAsync(dst, value, bytes, e->stream), "cudaMemsetAsync");
+    return CSAIDX_OK;
+}
+
+int csaidx_cuda_to_bf16(csaidx_engine* e, const float* src, uint16_t* dst, int64_t n, int strict) {
+    if (int rc = set_device(e)) return rc;
+    if (n < 0) return fail(CSAIDX_INVALID_ARGUMENT, "to_bf16: negative length");
+    ConvertParams p{src, reinterpret_cast<__nv_bfloat16*>(dst), n, strict ? e->flags + kInexact : nullptr,
+                    e->flags + kNonfiniteInput};
+    CSAIDX_CUDA_TRY(csaidx_kern::launch_convert_bf16(p, e->stream), "convert_bf16");
+    return CSAIDX_OK;
+}
+
+int csaidx_cuda_score_uses_tensor_cores(const csaidx_dims* d, int dtype, int mode, int kernel) {
+    if (d == nullptr) return 0;
+    return kernel == CSAIDX_KERNEL_AUTO && mode == CSAIDX_MODE_FP32 && dtype == CSAIDX_DTYPE_BF16 &&
+           csaidx_kern::score_tc_supported(d->heads, d->head_dim);
+}
+
+int csaidx_cuda_score(csaidx_engine* e, const void* q, const void* kc, int dtype, const float* w,
+                      const csaidx_dims* d, int64_t s0, int64_t rows, int64_t t0, int64_t cols, int mode, int kernel,
+                      int apply_mask, float* out, int64_t ld) {
+    if (int rc = set_device(e)) return rc;
+    if (int rc = check_dims(d)) return rc;
+    if (rows < 1 || cols < 1 || s0 < 0 || t0 < 0 || s0 + rows > d->seq_len || t0 + cols > d->key_blocks)
+        return fail(CSAIDX_INVALID_ARGUMENT, "score_tile: tile out of range");
+    if (ld < cols || (ld % 4) != 0) return fail(CSAIDX_INVALID_ARGUMENT, "score: ld must be >= cols and a multiple of 4");
+    if (mode != CSAIDX_MODE_FP32 && mode != CSAIDX_MODE_FP16_EMULATED)
+        return fail(CSAIDX_INVALID_ARGUMENT, "score: unknown accumulation mode");
+    if (dtype != CSAIDX_DTYPE_BF16 && dtype != CSAIDX_DTYPE_F32)
+        return fail(CSAIDX_INVALID_ARGUMENT, "score: unknown operand dtype");
+    if (kernel != CSAIDX_KERNEL_AUTO && kernel != CSAIDX_KERNEL_EXACT)
+        return fail(CSAIDX_INVALID_ARGUMENT, "score: unknown kernel request");
+    if (csaidx_cuda_score_uses_tensor_cores(d, dtype, mode, kernel)) {
+        const uint16_t* q_bf16 = static_cast<const uint16_t*>(q);
+        const uint16_t* kc_bf16 = static_cast<const uint16_t*>(kc);
+        CUtensorMap qmap, kmap;
+        if (int rc = make_map(&qmap, q_bf16, static_cast<uint64_t>(d->batch * d->seq_len * d->heads), d->head_dim, 256))
+            return rc;
+        if (int rc = make_map(&kmap, kc_bf16, static_cast<uint64_t>(d->batch * d->key_blocks), d->head_dim, 128))
+            return rc;
+        ScoreTcParams p{};
+        p.w = w;
+        p.out = out;
+        p.nonfinite = e->flags + kNonfiniteScore;
+        p.ld = ld;
+        p.seq_len = d->seq_len;
+        p.key_blocks = d->key_blocks;
+        p.ratio = d->ratio;
+        p.s0 = s0;
+        p.rows = rows;
+        p.t0 = t0;
+        p.cols = cols;
+        p.batch = static_cast<int>(d->batch);
+        p.apply_mask = apply_mask;
+        CSAIDX_CUDA_TRY(csaidx_kern::launch_score_tc(qmap, kmap, p, e->num_sms, e->stream), "score_tc");
+    } else {
+        ScoreExactParams p{};
+        p.q = q;
+        p.kc = kc;
+        p.operand_f32 = dtype == CSAIDX_DTYPE_F32;
+        p.w = w;
+        p.out = out;
+        p.nonfinite = e->flags + kNonfiniteScore;
+        p.ld = ld;
+        p.seq_len = d->seq_len;
+        p.key_blocks = d->key_blocks;
+        p.heads = d->heads;
+        p.head_dim = d->head_dim;
+        p.ratio = d->ratio;
+        p.s0 = s0;
+        p.rows = rows;
+        p.t0 = t0;
+        p.cols = cols;
+        p.batch = static_cast<int>(d->batch);
+        p.apply_mask = apply_mask;
+        p.fp16 = mode == CSAIDX_MODE_FP16_EMULATED;
+        CSAIDX_CUDA_TRY(csaidx_kern::launch_score_exact(p, e->stream), "score_exact");
+    }
+    return CSAIDX_OK;
+}
+
+int csaidx_cuda_bool_mask(csaidx_engine* e, uint8_t* keep, int64_t s0, int64_t t0, int64_t rows, int64_t cols,
+                          int64_t ratio) {
+    if (int rc = set_device(e)) return rc;
+    if (rows < 1 || cols < 1 || s0 < 0 || t0 < 0 || ratio < 1)
+        return fail(CSAIDX_INVALID_ARGUMENT, "build_mask_tile: bad tile extents");
+    CSAIDX_CUDA_TRY(csaidx_kern::launch_bool_mask(keep, rows, cols, s0, t0, ratio, e->stream), "bool_mask");
+    return CSAIDX_OK;
+}
+
+int csaidx_cuda_apply_bool_mask(csaidx_engine* e, float* scores, int64_t ld, const uint8_t* keep, int64_t batch,
+                                int64_t rows, int64_t cols) {
+    if (int rc = set_device(e)) return rc;
+    CSAIDX_CUDA_TRY(csaidx_kern::launch_apply_bool_mask(scores, ld, keep, batch, rows, cols, e->stream),
+                    "apply_bool_mask");
+    return CSAIDX_OK;
+}
+
+int csaidx_cuda_select_capacity(void) { return csaidx_kern::select_max_take(); }
+
+int csaidx_cuda_select(csaidx_engine* e, const float* scores, int64_t batch, int64_t rows, int64_t ld, int64_t cols,
+                       int64_t s0, int64_t t0, int64_t ratio, int apply_mask, int64_t k, float* cand_val,
+                       int32_t* cand_idx, int64_t cand_ld) {
+    if (int rc = set_device(e)) return rc;
+    if (k < 1) return fail(CSAIDX_INVALID_ARGUMENT, "tile_topk: top_k must be >= 1");
+    if (rows < 1 || cols < 1 || batch < 1 || ratio < 1) return fail(CSAIDX_INVALID_ARGUMENT, "select: bad extents");
+    if ((ld % 4) != 0 || ld < cols) return fail(CSAIDX_INVALID_ARGUMENT, "select: ld must be >= cols, multiple of 4");
+    if ((reinterpret_cast<uintptr_t>(scores) & 15) != 0) return fail(CSAIDX_INVALID_ARGUMENT, "select: scores not 16B aligned");
+    const int64_t width = k < cols ? k : cols;
+    if (width > csaidx_kern::select_max_take())
+        return fail(CSAIDX_INVALID_ARGUMENT, "tile_topk: min(k, cols) = %lld exceeds the GPU select capacity %d",
+                    static_cast<long long>(width), csaidx_kern::select_max_take());
+    if (cand_ld < width) return fail(CSAIDX_INVALID_ARGUMENT, "select: cand_ld < min(k, cols)");
+    SelectParams p{};
+    p.scores = scores;
+    p.ld = ld;
+    p.rows = rows;
+    p.cols = cols;
+    p.s0 = s0;
+    p.t0 = t0;
+    p.ratio = ratio;
+    p.batch = static_cast<int>(batch);
+    p.apply_mask = apply_mask;
+    p.k = static_cast<int>(k);
+    p.width = static_cast<int>(width);
+    p.out_val = cand_val;
+    p.out_idx = cand_idx;
+    p.out_ld = cand_ld;
+    CSAIDX_CUDA_TRY(csaidx_kern::launch_select(p, e->stream), "select");
+    return CSAIDX_OK;
+}
+
+int csaidx_cuda_merge(csaidx_engine* e, float* run_val, int32_t* run_idx, int64_t nrows, int64_t k,
+                      const float* cand_val, const int32_t* cand_idx, int64_t cand_ld, int64_t width, int overwrite,
+                      int check_overlap) {
+    if (int rc = set_device(e)) return rc;
+    if (k < 1 || k > csaidx_kern::select_max_take())
+        return fail(CSAIDX_INVALID_ARGUMENT, "merge: k must be in [1, %d]", csaidx_kern::select_max_take());
+    if (width < 0 || width > k || cand_ld < width) return fail(CSAIDX_INVALID_ARGUMENT, "merge: bad candidate width");
+    MergeParams p{};
+    p.run_val = run_val;
+    p.run_idx = run_idx;
+    p.cand_val = cand_val;
+    p.cand_idx = cand_idx;
+    p.cand_ld = cand_ld;
+    p.nrows = nrows;
+    p.k = static_cast<int>(k);
+    p.width = static_cast<int>(width);
+    p.overwrite = overwrite;
+    p.check_overlap = check_overlap;
+    p.overlap_flag = e->flags + kOverlap;
+    CSAIDX_CUDA_TRY(csaidx_kern::launch_merge(p, e->stream), "merge");
+    return CSAIDX_OK;
+}
+
+int csaidx_cuda_fill_sentinel(csaidx_engine* e, float* val, int32_t* idx, int64_t n) {
+    if (int rc = set_device(e)) return rc;
+    CSAIDX_CUDA_TRY(csaidx_kern::launch_fill_sentinel(val, idx, n, e->stream), "fill_sentinel");
+    return CSAIDX_OK;
+}
+
+int csaidx_cuda_finalize(csaidx_engine* e, const float* run_val, const int32_t* run_idx, int64_t batch, int64_t rows,
+                         int64_t s0, int64_t ratio, int64_t k, int check_keff, int64_t* out_idx, float* out_val,
+                         int64_t out_rows, int64_t out_row0) {
+    if (int rc = set_device(e)) return rc;
+    if (out_row0 < 0 || out_row0 + rows > out_rows) return fail(CSAIDX_INVALID_ARGUMENT, "finalize: rows out of range");
+    FinalizeParams p{};
+    p.run_val = run_val;
+    p.run_idx = run_idx;
+    p.rows = rows;
+    p.s0 = s0;
+    p.ratio = ratio;
+    p.batch = static_cast<int>(batch);
+    p.k = static_cast<int>(k);
+    p.check_keff = check_keff;
+    p.out_idx = out_idx;
+    p.out_val = out_val;
+    p.out_rows = out_rows;
+    p.out_row0 = out_row0;
+    p.trail_flag = e->flags + kTrail;
+    p.keff_flag = e->flags + kKeff;
+    CSAIDX_CUDA_TRY(csaidx_kern::launch_finalize(p, e->stream), "finalize");
+    return CSAIDX_OK;
+}
+
+int csaidx_cuda_chunk_step(csaidx_engine* e, const void* q, const void* kc, int dtype, const float* w,
+                           const csaidx_dims* d, int64_t s0, int64_t rows, int64_t t0, int64_t cols, int mode,
+                           int kernel, float* score_buf, int64_t ld, float* cand_val, int32_t* cand_idx, float* run_val,
+                           int32_t* run_idx, int first_tile, int overwrite) {
+    if (int rc = csaidx_cuda_score(e, q, kc, dtype, w, d, s0, rows, t0, cols, mode, kernel, 1, score_buf, ld))
+        return rc;
+    const int64_t k = d->top_k;
+    const int64_t width = k < cols ? k : cols;
+    if (first_tile && width == k) {
+        // Merging into an all-sentinel buffer is a copy (and so is A1's
+        // overwrite): select straight into the running rows.
+        return csaidx_cuda_select(e, score_buf, d->batch, rows, ld, cols, s0, t0, d->ratio, 1, k, run_val, run_idx, k);
+    }
+    if (int rc = csaidx_cuda_select(e, score_buf, d->batch, rows, ld, cols, s0, t0, d->ratio, 1, k, cand_val, cand_idx,
+                                    width))
+        return rc;
+    return csaidx_cuda_merge(e, run_val, run_idx, d->batch * rows, k, cand_val, cand_idx, width, width, overwrite, 0);
+}
+
+int csaidx_cuda_gen_normal_bf16(csaidx_engine* e, uint16_t* dst, int64_t n, double stddev, uint64_t seed,
+                                uint64_t stream_id, int64_t offset) {
+    if (int rc = set_device(e)) return rc;
+    CSAIDX_CUDA_TRY(csaidx_kern::launch_gen_normal_bf16(reinterpret_cast<__nv_bfloat16*>(dst), n, stddev, seed,
+                                                        stream_id, offset, e->stream),
+                    "gen_bf16");
+    return CSAIDX_OK;
+}
+
+int csaidx_cuda_gen_normal_f32(csaidx_engine* e, float* dst, int64_t n, double stddev, uint64_t seed,
+                               uint64_t stream_id, int64_t offset) {
+    if (int rc = set_device(e)) return rc;
+    CSAIDX_CUDA_TRY(csaidx_kern::launch_gen_normal_f32(dst, n, stddev, seed, stream_id, offset, e->stream), "gen_f32");
+    return CSAIDX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,218 @@
+// C entry points of libcsaidx.so (include/csaidx_host.h): the reference
+// driver API on raw host buffers (no IndexerInputs copy) and on device
+// operands. Exceptions become status codes + a thread-local message.
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "csaidx/causal.hpp"
+#include "csaidx/driver.hpp"
+#include "csaidx/gpu.hpp"
+#include "csaidx_host.h"
+#include "device.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return CSAIDX_OK;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return CSAIDX_INVALID_ARGUMENT;
+    } catch (const std::overflow_error& e) {
+        g_err = e.what();
+        return CSAIDX_OVERFLOW_ERROR;
+    } catch (const std::logic_error& e) {
+        g_err = e.what();
+        return CSAIDX_LOGIC_ERROR;
+    } catch (const std::runtime_error& e) {
+        g_err = e.what();
+        return CSAIDX_RUNTIME_ERROR;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return CSAIDX_RUNTIME_ERROR;
+    }
+}
+
+csaidx::ProblemDims from_c(const csaidx_dims* d) {
+    if (d == nullptr) throw std::invalid_argument("null dims");
+    csaidx::ProblemDims p{d->batch, d->seq_len, d->key_blocks, d->heads, d->head_dim, d->ratio, d->top_k};
+    csaidx::detail::validate_dims(p);
+    return p;
+}
+
+csaidx::DriverConfig from_c(const csaidx_run_config* c) {
+    if (c == nullptr) throw std::invalid_argument("null config");
+    csaidx::DriverConfig cfg;
+    cfg.tile = csaidx::TileConfig{c->query_tile, c->key_tile};
+    cfg.mode = c->mode == CSAIDX_MODE_FP16_EMULATED ? csaidx::AccumulationMode::fp16_emulated
+                                                    : csaidx::AccumulationMode::fp32;
+    switch (c->ablation) {
+        case CSAIDX_ABLATION_NONE: cfg.ablation = csaidx::Ablation::none; break;
+        case CSAIDX_ABLATION_A1_NO_MERGE: cfg.ablation = csaidx::Ablation::a1_no_merge; break;
+        case CSAIDX_ABLATION_A2_SKIP_NARROW: cfg.ablation = csaidx::Ablation::a2_skip_narrow; break;
+        default: throw std::invalid_argument("unknown ablation");
+    }
+    switch (c->kernel) {
+        case CSAIDX_SCORE_AUTO: cfg.kernel = csaidx::ScoreKernel::auto_detect; break;
+        case CSAIDX_SCORE_SCALAR: cfg.kernel = csaidx::ScoreKernel::scalar; break;
+        case CSAIDX_SCORE_AVX2: cfg.kernel = csaidx::ScoreKernel::avx2; break;
+        default: throw std::invalid_argument("unknown score kernel");
+    }
+    cfg.causal_early_exit = c->causal_early_exit != 0;
+    cfg.bool_mask_tile = c->bool_mask_tile != 0;
+    cfg.threads = c->threads;
+    cfg.auto_threshold_bytes = c->auto_threshold_bytes;
+    csaidx::gpu::Options o;
+    o.device = c->device;
+    o.strict_bf16 = c->strict_bf16 != 0;
+    o.stream = c->stream;
+    csaidx::gpu::set_options(o);
+    return cfg;
+}
+
+void copy_out(const csaidx::TopKResult& r, int64_t* idx, float* val) {
+    std::memcpy(idx, r.indices.data(), r.indices.size() * sizeof(int64_t));
+    std::memcpy(val, r.values.data(), r.values.size() * sizeof(float));
+}
+
+void fill_stats(csaidx_run_stats* st, const csaidx::RunStats& rs, const csaidx::MemoryLedger& ledger, int path) {
+    if (st == nullptr) return;
+    st->dispatch_count = rs.dispatch_count;
+    st->tiles_skipped_masked = rs.tiles_skipped_masked;
+    st->tiles_skipped_narrow = rs.tiles_skipped_narrow;
+    st->ledger_peak_bytes = ledger.peak_bytes();
+    st->device_peak_bytes = csaidx::gpu::device_memory().peak_bytes;
+    st->path = path;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* csaidx_host_last_error(void) { return g_err.c_str(); }
+
+void csaidx_host_default_config(csaidx_run_config* cfg) {
+    if (cfg == nullptr) return;
+    const csaidx::DriverConfig d;
+    *cfg = csaidx_run_config{d.tile.query_tile, d.tile.key_tile, CSAIDX_MODE_FP32, CSAIDX_ABLATION_NONE,
+                             CSAIDX_SCORE_AUTO, 1, 0, 1, d.auto_threshold_bytes, 0, 0, nullptr};
+}
+
+int csaidx_host_run_chunked(const float* q, const float* kc, const float* w, const csaidx_dims* dims,
+                            const csaidx_run_config* cfg, int64_t* out_idx, float* out_val, csaidx_run_stats* stats) {
+    return guarded([&] {
+        const csaidx::ProblemDims d = from_c(dims);
+        const csaidx::DriverConfig c = from_c(cfg);
+        csaidx::gpu::reset_device_peak();
+        csaidx::MemoryLedger ledger;
+        csaidx::RunStats rs;
+        const csaidx::TopKResult r = csaidx::detail::run_chunked_view({q, kc, w}, d, c, ledger, &rs);
+        copy_out(r, out_idx, out_val);
+        fill_stats(stats, rs, ledger, 1);
+    });
+}
+
+int csaidx_host_run_materialize(const float* q, const float* kc, const float* w, const csaidx_dims* dims,
+                                const csaidx_run_config* cfg, int64_t* out_idx, float* out_val,
+                                csaidx_run_stats* stats) {
+    return guarded([&] {
+        const csaidx::ProblemDims d = from_c(dims);
+        const csaidx::DriverConfig c = from_c(cfg);
+        csaidx::gpu::reset_device_peak();
+        csaidx::MemoryLedger ledger;
+        const csaidx::TopKResult r = csaidx::detail::run_materialize_view({q, kc, w}, d, c.mode, ledger, c.kernel);
+        copy_out(r, out_idx, out_val);
+        fill_stats(stats, csaidx::RunStats{}, ledger, 0);
+    });
+}
+
+int csaidx_host_dispatch(const float* q, const float* kc, const float* w, const csaidx_dims* dims,
+                         const csaidx_run_config* cfg, int64_t* out_idx, float* out_val, csaidx_run_stats* stats) {
+    return guarded([&] {
+        const csaidx::ProblemDims d = from_c(dims);
+        const csaidx::DriverConfig c = from_c(cfg);
+        const csaidx::DispatchDecision dec = csaidx::choose_path(d, c.auto_threshold_bytes);
+        csaidx::gpu::reset_device_peak();
+        csaidx::MemoryLedger ledger;
+        csaidx::RunStats rs;
+        const csaidx::TopKResult r =
+            dec.path == csaidx::ExecutionPath::materialize
+                ? csaidx::detail::run_materialize_view({q, kc, w}, d, c.mode, ledger, c.kernel)
+                : csaidx::detail::run_chunked_view({q, kc, w}, d, c, ledger, &rs);
+        copy_out(r, out_idx, out_val);
+        fill_stats(stats, rs, ledger, dec.path == csaidx::ExecutionPath::materialize ? 0 : 1);
+    });
+}
+
+int csaidx_device_run_chunked(const void* q, const void* kc, int dtype, const float* w, const csaidx_dims* dims,
+                              const csaidx_run_config* cfg, const int64_t* chunk_starts, int64_t n_chunks,
+                              int64_t* out_idx, float* out_val, int64_t out_rows, csaidx_run_stats* stats) {
+    return guarded([&] {
+        const csaidx::ProblemDims d = from_c(dims);
+        const csaidx::DriverConfig c = from_c(cfg);
+        std::vector<int64_t> starts;
+        if (chunk_starts != nullptr && n_chunks > 0) starts.assign(chunk_starts, chunk_starts + n_chunks);
+        csaidx::gpu::reset_device_peak();
+        csaidx::MemoryLedger ledger;
+        csaidx::RunStats rs;
+        csaidx::gpu::run_chunked_device(csaidx::gpu::DeviceOperands{q, kc, w, dtype}, d, c,
+                                        starts.empty() ? nullptr : &starts, out_idx, out_val, out_rows, ledger, &rs);
+        fill_stats(stats, rs, ledger, 1);
+    });
+}
+
+int csaidx_host_problem_dims(int64_t batch, int64_t seq_len, int64_t ratio, int64_t heads, int64_t head_dim,
+                             int64_t top_k, csaidx_dims* out) {
+    return guarded([&] {
+        const auto p = csaidx::ProblemDims::create(batch, seq_len, ratio, heads, head_dim, top_k);
+        *out = csaidx::detail::to_c(p);
+    });
+}
+
+int csaidx_host_dispatch_count_model(const csaidx_dims* dims, int64_t query_tile, int64_t key_tile, int64_t* out) {
+    return guarded([&] { *out = csaidx::dispatch_count_model(from_c(dims), csaidx::TileConfig{query_tile, key_tile}); });
+}
+
+int csaidx_host_chunked_peak_model_bytes(int64_t batch, int64_t query_tile, int64_t key_tile, int64_t top_k,
+                                         int bool_mask_tile, uint64_t* out) {
+    return guarded([&] {
+        *out = csaidx::chunked_peak_model_bytes(batch, csaidx::TileConfig{query_tile, key_tile}, top_k,
+                                                bool_mask_tile != 0);
+    });
+}
+
+int csaidx_host_materialize_bytes(const csaidx_dims* dims, uint64_t* out) {
+    return guarded([&] {
+        if (dims == nullptr) throw std::invalid_argument("null dims");
+        csaidx::ProblemDims p{dims->batch, dims->seq_len, dims->key_blocks, dims->heads, dims->head_dim, dims->ratio,
+                              dims->top_k};
+        *out = csaidx::materialize_bytes(p);
+    });
+}
+
+int csaidx_host_choose_path(const csaidx_dims* dims, uint64_t threshold, int* path, uint64_t* predicted) {
+    return guarded([&] {
+        const csaidx::DispatchDecision dd = csaidx::choose_path(from_c(dims), threshold);
+        *path = dd.path == csaidx::ExecutionPath::materialize ? 0 : 1;
+        *predicted = dd.predicted_bytes;
+    });
+}
+
+int64_t csaidx_host_t_legal(int64_t t, int64_t ratio) {
+    int64_t r = -1;
+    guarded([&] { r = csaidx::t_legal(t, ratio); });
+    return r;
+}
+
+int64_t csaidx_host_k_eff(int64_t t, int64_t ratio, int64_t top_k) {
+    int64_t r = -1;
+    guarded([&] { r = csaidx::k_eff(t, ratio, top_k); });
+    return r;
+}
+
+}  // extern "C"

@@ -1,0 +1,174 @@
+// Engine registry, error mapping, device buffers and operand staging.
+#include "device.hpp"
+
+#include <algorithm>
+#include <map>
+#include <stdexcept>
+#include <string>
+
+namespace csaidx {
+namespace gpu {
+
+namespace {
+std::mutex g_opt_mu;
+Options g_options;
+}  // namespace
+
+void set_options(const Options& o) {
+    std::lock_guard<std::mutex> lock(g_opt_mu);
+    g_options = o;
+}
+
+Options options() {
+    std::lock_guard<std::mutex> lock(g_opt_mu);
+    return g_options;
+}
+
+DeviceMemory device_memory() {
+    DeviceMemory m;
+    detail::check(csaidx_engine_mem_stats(detail::engine(), &m.live_bytes, &m.peak_bytes));
+    return m;
+}
+
+void reset_device_peak() { detail::check(csaidx_engine_reset_peak(detail::engine())); }
+
+}  // namespace gpu
+
+namespace detail {
+
+void throw_status(int rc, const char* what) {
+    switch (rc) {
+        case CSAIDX_INVALID_ARGUMENT: throw std::invalid_argument(what);
+        case CSAIDX_OVERFLOW_ERROR: throw std::overflow_error(what);
+        case CSAIDX_LOGIC_ERROR: throw std::logic_error(what);
+        case CSAIDX_RUNTIME_ERROR:
+        case CSAIDX_CUDA_ERROR:
+        default: throw std::runtime_error(what);
+    }
+}
+
+void check(int rc) {
+    if (rc != CSAIDX_OK) throw_status(rc, csaidx_cuda_last_error());
+}
+
+std::mutex& engine_mutex() {
+    static std::mutex mu;
+    return mu;
+}
+
+csaidx_engine* engine() {
+    static std::mutex mu;
+    static std::map<int, csaidx_engine*> engines;  // intentionally never destroyed (CUDA teardown order)
+    const gpu::Options o = gpu::options();
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = engines.find(o.device);
+    if (it == engines.end()) {
+        csaidx_engine* e = nullptr;
+        check(csaidx_engine_create(o.device, &e));
+        it = engines.emplace(o.device, e).first;
+    }
+    if (o.stream != nullptr)
+        check(csaidx_engine_set_stream(it->second, o.stream));
+    else
+        check(csaidx_engine_use_own_stream(it->second));
+    return it->second;
+}
+
+DeviceBuffer::DeviceBuffer(csaidx_engine* e, size_t bytes) : e_(e), bytes_(bytes) {
+    check(csaidx_cuda_alloc(e, bytes, &ptr_));
+}
+
+DeviceBuffer::DeviceBuffer(DeviceBuffer&& o) noexcept : e_(o.e_), ptr_(o.ptr_), bytes_(o.bytes_) {
+    o.ptr_ = nullptr;
+    o.bytes_ = 0;
+}
+
+DeviceBuffer& DeviceBuffer::operator=(DeviceBuffer&& o) noexcept {
+    if (this != &o) {
+        reset();
+        e_ = o.e_;
+        ptr_ = o.ptr_;
+        bytes_ = o.bytes_;
+        o.ptr_ = nullptr;
+        o.bytes_ = 0;
+    }
+    return *this;
+}
+
+DeviceBuffer::~DeviceBuffer() { reset(); }
+
+void DeviceBuffer::reset() {
+    if (ptr_ != nullptr) csaidx_cuda_free(e_, ptr_);
+    ptr_ = nullptr;
+    bytes_ = 0;
+}
+
+void DeviceBuffer::upload(const void* host, size_t bytes) { check(csaidx_cuda_copy(e_, ptr_, host, bytes)); }
+
+void DeviceBuffer::download(void* host, size_t bytes) const { check(csaidx_cuda_copy(e_, host, ptr_, bytes)); }
+
+int kernel_code(ScoreKernel kernel) {
+    switch (kernel) {
+        case ScoreKernel::auto_detect: return CSAIDX_KERNEL_AUTO;
+        case ScoreKernel::scalar: return CSAIDX_KERNEL_EXACT;
+        case ScoreKernel::avx2:
+            throw std::invalid_argument("avx2 kernel requested but this build has no AVX2 kernel (B200 path)");
+    }
+    throw std::invalid_argument("unknown score kernel");
+}
+
+int mode_code(AccumulationMode mode) {
+    return mode == AccumulationMode::fp16_emulated ? CSAIDX_MODE_FP16_EMULATED : CSAIDX_MODE_FP32;
+}
+
+csaidx_dims to_c(const ProblemDims& d) {
+    return csaidx_dims{d.batch, d.seq_len, d.key_blocks, d.heads, d.head_dim, d.ratio, d.top_k};
+}
+
+void validate_dims(const ProblemDims& d) {
+    if (d.batch < 1 || d.seq_len < 1 || d.key_blocks < 1 || d.heads < 1 || d.head_dim < 1 || d.ratio < 1 ||
+        d.top_k < 1)
+        throw std::invalid_argument("ProblemDims: every extent must be >= 1");
+}
+
+int operand_dtype(const ProblemDims& dims, int mode, int kernel) {
+    const csaidx_dims c = to_c(dims);
+    return csaidx_cuda_score_uses_tensor_cores(&c, CSAIDX_DTYPE_BF16, mode, kernel) ? CSAIDX_DTYPE_BF16
+                                                                                    : CSAIDX_DTYPE_F32;
+}
+
+namespace {
+
+// fp32 host -> device, rounded to bf16 on device through a bounded slab.
+void stage_bf16(csaidx_engine* e, DeviceBuffer& dst, const float* host, int64_t n, bool strict) {
+    constexpr int64_t kSlab = int64_t{1} << 26;  // 64 Mi elements (256 MiB fp32)
+    DeviceBuffer slab(e, static_cast<size_t>(std::min(n, kSlab)) * sizeof(float));
+    for (int64_t off = 0; off < n; off += kSlab) {
+        const int64_t len = std::min(kSlab, n - off);
+        check(csaidx_cuda_copy(e, slab.as<void>(), host + off, static_cast<size_t>(len) * sizeof(float)));
+        check(csaidx_cuda_to_bf16(e, slab.as<float>(), dst.as<uint16_t>() + off, len, strict ? 1 : 0));
+    }
+}
+
+}  // namespace
+
+StagedOperands::StagedOperands(csaidx_engine* e, const HostView& host, const ProblemDims& dims, int dtype,
+                               bool strict)
+    : dtype_(dtype) {
+    const int64_t nq = dims.q_elems(), nk = dims.kc_elems(), nw = dims.w_elems();
+    const size_t esz = dtype == CSAIDX_DTYPE_BF16 ? 2 : 4;
+    q_ = DeviceBuffer(e, static_cast<size_t>(nq) * esz);
+    kc_ = DeviceBuffer(e, static_cast<size_t>(nk) * esz);
+    w_ = DeviceBuffer(e, static_cast<size_t>(nw) * sizeof(float));
+    if (dtype == CSAIDX_DTYPE_BF16) {
+        stage_bf16(e, kc_, host.kc, nk, strict);
+        stage_bf16(e, q_, host.q, nq, strict);
+    } else {
+        q_.upload(host.q, static_cast<size_t>(nq) * sizeof(float));
+        kc_.upload(host.kc, static_cast<size_t>(nk) * sizeof(float));
+    }
+    w_.upload(host.w, static_cast<size_t>(nw) * sizeof(float));
+}
+
+}  // namespace detail
+}  // namespace csaidx

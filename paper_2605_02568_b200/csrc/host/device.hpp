@@ -1,0 +1,110 @@
+// Internal plumbing of libcsaidx.so: status -> exception mapping, the
+// per-device engine registry, RAII device buffers, operand staging and the
+// device-side chunk scheduler shared by every driver entry point. Every GPU
+// action goes through the C-ABI in include/csaidx_cuda.h.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <mutex>
+#include <vector>
+
+#include "csaidx/driver.hpp"
+#include "csaidx/gpu.hpp"
+#include "csaidx/types.hpp"
+#include "csaidx_cuda.h"
+
+namespace csaidx::detail {
+
+// Throws the reference exception type for a C-ABI status (no-op on OK).
+void check(int rc);
+[[noreturn]] void throw_status(int rc, const char* what);
+
+// Engine of gpu::options().device with the configured stream applied.
+csaidx_engine* engine();
+std::mutex& engine_mutex();
+
+class DeviceBuffer {
+public:
+    DeviceBuffer() = default;
+    DeviceBuffer(csaidx_engine* e, size_t bytes);
+    DeviceBuffer(DeviceBuffer&& o) noexcept;
+    DeviceBuffer& operator=(DeviceBuffer&& o) noexcept;
+    DeviceBuffer(const DeviceBuffer&) = delete;
+    DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+    ~DeviceBuffer();
+
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(ptr_);
+    }
+    [[nodiscard]] size_t bytes() const { return bytes_; }
+    void upload(const void* host, size_t bytes);
+    void download(void* host, size_t bytes) const;
+
+private:
+    void reset();
+    csaidx_engine* e_ = nullptr;
+    void* ptr_ = nullptr;
+    size_t bytes_ = 0;
+};
+
+int kernel_code(ScoreKernel kernel);  // throws like resolve_score_kernel for unavailable kernels
+int mode_code(AccumulationMode mode);
+csaidx_dims to_c(const ProblemDims& d);
+
+struct HostView {
+    const float* q;
+    const float* kc;
+    const float* w;
+};
+
+struct DeviceOps {
+    const void* q;
+    const void* kc;
+    const float* w;
+    int dtype;  // CSAIDX_DTYPE_*
+};
+
+// Device copies of q / kc / w. dtype bf16 stages through a bounded fp32
+// slab and rounds on device; fp32 copies straight.
+class StagedOperands {
+public:
+    StagedOperands(csaidx_engine* e, const HostView& host, const ProblemDims& dims, int dtype, bool strict);
+    [[nodiscard]] DeviceOps ops() const { return {q_.as<void>(), kc_.as<void>(), w_.as<float>(), dtype_}; }
+
+private:
+    DeviceBuffer q_, kc_, w_;
+    int dtype_;
+};
+
+// Operand dtype the score kernel wants for this (dims, mode, kernel).
+int operand_dtype(const ProblemDims& dims, int mode, int kernel);
+
+struct ChunkPlan {
+    int64_t cs = 0;  // clamped c_S
+    int64_t ct = 0;  // clamped c_T
+    std::vector<int64_t> starts;
+    std::vector<int64_t> out_row0;
+};
+
+ChunkPlan plan_chunks(const ProblemDims& dims, const TileConfig& tile, const std::vector<int64_t>* starts);
+
+// process_query_tile (driver.cpp:36-106) for every chunk of the plan, on
+// device. Results land in device [B, out_rows, k] int64 / fp32.
+void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, const DriverConfig& config,
+              const ChunkPlan& plan, int64_t* out_idx, float* out_val, int64_t out_rows, MemoryLedger& ledger,
+              RunStats& stats);
+
+// Materialized path on device (driver.cpp:167-192).
+void run_materialize_device(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, int mode, int kernel,
+                            int64_t* out_idx, float* out_val, MemoryLedger& ledger);
+
+TopKResult run_chunked_view(const HostView& in, const ProblemDims& dims, const DriverConfig& config,
+                            MemoryLedger& ledger, RunStats* stats);
+TopKResult run_materialize_view(const HostView& in, const ProblemDims& dims, AccumulationMode mode,
+                                MemoryLedger& ledger, ScoreKernel kernel);
+
+void validate_dims(const ProblemDims& d);
+
+}  // namespace csaidx::detail

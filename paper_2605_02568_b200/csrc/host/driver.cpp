@@ -1,0 +1,262 @@
+// Host chunk scheduler (Algorithm 2) over the C-ABI. Reference semantics:
+// driver.cpp:29-211. Each (s0, t0) host tile becomes one masked score launch
+// plus one select (+ merge) launch on device; the running top-k rows live in
+// HBM for the whole query chunk; the sentinel pass and the k_eff contract are
+// checked on device. Ledger charges mirror the reference's labels, byte
+// counts and scopes, so RunStats and ledger peaks are directly comparable.
+#include "csaidx/driver.hpp"
+
+#include <algorithm>
+#include <stdexcept>
+
+#include "csaidx/causal.hpp"
+#include "device.hpp"
+
+namespace csaidx {
+
+namespace detail {
+
+namespace {
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+struct Clamped {
+    int64_t cs, ct;
+};
+
+Clamped clamp(const ProblemDims& dims, const TileConfig& tile) {
+    tile.validate();
+    return {std::min(tile.query_tile, dims.seq_len), std::min(tile.key_tile, dims.key_blocks)};
+}
+
+}  // namespace
+
+ChunkPlan plan_chunks(const ProblemDims& dims, const TileConfig& tile, const std::vector<int64_t>* starts) {
+    const Clamped c = clamp(dims, tile);
+    ChunkPlan plan;
+    plan.cs = c.cs;
+    plan.ct = c.ct;
+    if (starts == nullptr) {
+        for (int64_t s0 = 0; s0 < dims.seq_len; s0 += c.cs) plan.starts.push_back(s0);
+    } else {
+        for (int64_t s0 : *starts) {
+            if (s0 < 0 || s0 >= dims.seq_len || s0 % c.cs != 0)
+                throw std::invalid_argument("chunk start must be a multiple of the query tile inside the sequence");
+            plan.starts.push_back(s0);
+        }
+    }
+    int64_t row = 0;
+    for (int64_t s0 : plan.starts) {
+        plan.out_row0.push_back(row);
+        row += std::min(c.cs, dims.seq_len - s0);
+    }
+    return plan;
+}
+
+void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, const DriverConfig& config,
+              const ChunkPlan& plan, int64_t* out_idx, float* out_val, int64_t out_rows, MemoryLedger& ledger,
+              RunStats& stats) {
+    const int64_t B = dims.batch, k = dims.top_k, T = dims.key_blocks;
+    if (std::min(k, plan.ct) > csaidx_cuda_select_capacity() || k > csaidx_cuda_select_capacity())
+        throw std::invalid_argument("top_k exceeds the GPU selection capacity (4096)");
+    const int kcode = kernel_code(config.kernel);
+    const int mcode = mode_code(config.mode);
+    const csaidx_dims cd = to_c(dims);
+    const int64_t ld = (plan.ct + 3) / 4 * 4;
+    const int64_t width_max = std::min(k, plan.ct);
+
+    // Device working set, sized once for the largest tile and reused.
+    DeviceBuffer scores(e, static_cast<size_t>(B * plan.cs * ld) * sizeof(float));
+    DeviceBuffer cand_v(e, static_cast<size_t>(B * plan.cs * width_max) * 4);
+    DeviceBuffer cand_i(e, static_cast<size_t>(B * plan.cs * width_max) * 4);
+    DeviceBuffer run_v(e, static_cast<size_t>(B * plan.cs * k) * 4);
+    DeviceBuffer run_i(e, static_cast<size_t>(B * plan.cs * k) * 4);
+    DeviceBuffer keep;
+    if (config.bool_mask_tile) keep = DeviceBuffer(e, static_cast<size_t>(plan.cs * plan.ct));
+
+    for (size_t c = 0; c < plan.starts.size(); ++c) {
+        const int64_t s0 = plan.starts[c];
+        const int64_t rows = std::min(plan.cs, dims.seq_len - s0);
+        LedgerCharge buffer_charge(ledger, "topk_buffer", run_buffer_bytes(B, rows, k));
+        check(csaidx_cuda_fill_sentinel(e, run_v.as<float>(), run_i.as<int32_t>(), B * rows * k));
+        bool first = true;
+        for (int64_t t0 = 0; t0 < T; t0 += plan.ct) {
+            const int64_t cols = std::min(plan.ct, T - t0);
+            if (config.ablation == Ablation::a2_skip_narrow && cols < k) {
+                ++stats.tiles_skipped_narrow;
+                continue;
+            }
+            if (config.causal_early_exit && tile_fully_masked(s0, rows, t0, dims.ratio)) {
+                stats.tiles_skipped_masked += ceil_div(T - t0, plan.ct);
+                break;
+            }
+            LedgerCharge tile_charge(ledger, "score_tile", chunk_tile_bytes(B, rows, cols));
+            if (config.bool_mask_tile) {
+                check(csaidx_cuda_score(e, ops.q, ops.kc, ops.dtype, ops.w, &cd, s0, rows, t0, cols, mcode, kcode, 0,
+                                        scores.as<float>(), ld));
+                LedgerCharge mask_charge(ledger, "mask_tile", static_cast<uint64_t>(rows) * static_cast<uint64_t>(cols));
+                check(csaidx_cuda_bool_mask(e, keep.as<uint8_t>(), s0, t0, rows, cols, dims.ratio));
+                check(csaidx_cuda_apply_bool_mask(e, scores.as<float>(), ld, keep.as<uint8_t>(), B, rows, cols));
+            } else {
+                check(csaidx_cuda_score(e, ops.q, ops.kc, ops.dtype, ops.w, &cd, s0, rows, t0, cols, mcode, kcode, 1,
+                                        scores.as<float>(), ld));
+            }
+            ++stats.dispatch_count;
+            const int64_t width = std::min(k, cols);
+            LedgerCharge scratch_charge(ledger, "tile_topk_scratch", tile_scratch_bytes(B, rows, cols, k));
+            const bool overwrite = config.ablation == Ablation::a1_no_merge;
+            if (first && width == k) {
+                // merge into all-sentinel rows (or A1 overwrite) == copy
+                check(csaidx_cuda_select(e, scores.as<float>(), B, rows, ld, cols, s0, t0, dims.ratio, 1, k,
+                                         run_v.as<float>(), run_i.as<int32_t>(), k));
+            } else {
+                check(csaidx_cuda_select(e, scores.as<float>(), B, rows, ld, cols, s0, t0, dims.ratio, 1, k,
+                                         cand_v.as<float>(), cand_i.as<int32_t>(), width));
+                check(csaidx_cuda_merge(e, run_v.as<float>(), run_i.as<int32_t>(), B * rows, k, cand_v.as<float>(),
+                                        cand_i.as<int32_t>(), width, width, overwrite ? 1 : 0, 0));
+            }
+            first = false;
+        }
+        check(csaidx_cuda_finalize(e, run_v.as<float>(), run_i.as<int32_t>(), B, rows, s0, dims.ratio, k,
+                                   config.ablation == Ablation::none ? 1 : 0, out_idx, out_val, out_rows,
+                                   plan.out_row0[c]));
+    }
+    check(csaidx_engine_check(e));
+}
+
+void run_materialize_device(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, int mode, int kernel,
+                            int64_t* out_idx, float* out_val, MemoryLedger& ledger) {
+    const int64_t B = dims.batch, S = dims.seq_len, T = dims.key_blocks, k = dims.top_k;
+    if (std::min(k, T) > csaidx_cuda_select_capacity())
+        throw std::invalid_argument("top_k exceeds the GPU selection capacity (4096)");
+    LedgerCharge charge(ledger, "score_tile", chunk_tile_bytes(B, S, T));
+    const int64_t ld = (T + 3) / 4 * 4;
+    const csaidx_dims cd = to_c(dims);
+    DeviceBuffer scores(e, static_cast<size_t>(B * S * ld) * sizeof(float));
+    // The whole [B, S, T] matrix as one masked tile, same kernel as chunked.
+    check(csaidx_cuda_score(e, ops.q, ops.kc, ops.dtype, ops.w, &cd, 0, S, 0, T, mode, kernel, 1, scores.as<float>(),
+                            ld));
+    const int64_t width = std::min(k, T);
+    DeviceBuffer run_v(e, static_cast<size_t>(B * S * k) * 4), run_i(e, static_cast<size_t>(B * S * k) * 4);
+    check(csaidx_cuda_fill_sentinel(e, run_v.as<float>(), run_i.as<int32_t>(), B * S * k));
+    // oracle_topk per row == top-min(k, legal) sorted under succ; rows are
+    // written at stride k so the tail beyond `width` keeps its sentinels.
+    check(csaidx_cuda_select(e, scores.as<float>(), B, S, ld, T, 0, 0, dims.ratio, 1, k, run_v.as<float>(),
+                             run_i.as<int32_t>(), k));
+    (void)width;
+    check(csaidx_cuda_finalize(e, run_v.as<float>(), run_i.as<int32_t>(), B, S, 0, dims.ratio, k, 1, out_idx, out_val,
+                               S, 0));
+    check(csaidx_engine_check(e));
+}
+
+namespace {
+
+void check_extents(const ProblemDims& dims, size_t nq, size_t nk, size_t nw) {
+    validate_dims(dims);
+    if (static_cast<int64_t>(nq) != dims.q_elems() || static_cast<int64_t>(nk) != dims.kc_elems() ||
+        static_cast<int64_t>(nw) != dims.w_elems())
+        throw std::invalid_argument("IndexerInputs: extent mismatch with ProblemDims");
+}
+
+void download_result(csaidx_engine* e, const DeviceBuffer& idx, const DeviceBuffer& val, TopKResult& out) {
+    idx.download(out.indices.data(), out.indices.size() * sizeof(int64_t));
+    val.download(out.values.data(), out.values.size() * sizeof(float));
+    check(csaidx_engine_check(e));
+}
+
+}  // namespace
+
+TopKResult run_chunked_view(const HostView& in, const ProblemDims& dims, const DriverConfig& config,
+                            MemoryLedger& ledger, RunStats* stats_out) {
+    const ChunkPlan plan = plan_chunks(dims, config.tile, nullptr);
+    TopKResult out = TopKResult::sized(dims);
+    const int kcode = kernel_code(config.kernel);
+    std::lock_guard<std::mutex> lock(engine_mutex());
+    csaidx_engine* e = engine();
+    const StagedOperands ops(e, in, dims, operand_dtype(dims, mode_code(config.mode), kcode),
+                             gpu::options().strict_bf16);
+    DeviceBuffer idx(e, out.indices.size() * sizeof(int64_t)), val(e, out.values.size() * sizeof(float));
+    RunStats stats;
+    run_plan(e, ops.ops(), dims, config, plan, idx.as<int64_t>(), val.as<float>(), dims.seq_len, ledger, stats);
+    download_result(e, idx, val, out);
+    if (stats_out != nullptr) *stats_out = stats;
+    return out;
+}
+
+TopKResult run_materialize_view(const HostView& in, const ProblemDims& dims, AccumulationMode mode,
+                                MemoryLedger& ledger, ScoreKernel kernel) {
+    validate_dims(dims);
+    TopKResult out = TopKResult::sized(dims);
+    const int kcode = kernel_code(kernel);
+    const int mcode = mode_code(mode);
+    std::lock_guard<std::mutex> lock(engine_mutex());
+    csaidx_engine* e = engine();
+    const StagedOperands ops(e, in, dims, operand_dtype(dims, mcode, kcode), gpu::options().strict_bf16);
+    DeviceBuffer idx(e, out.indices.size() * sizeof(int64_t)), val(e, out.values.size() * sizeof(float));
+    run_materialize_device(e, ops.ops(), dims, mcode, kcode, idx.as<int64_t>(), val.as<float>(), ledger);
+    download_result(e, idx, val, out);
+    return out;
+}
+
+}  // namespace detail
+
+int64_t dispatch_count_model(const ProblemDims& dims, const TileConfig& tile) {
+    tile.validate();
+    const int64_t cs = std::min(tile.query_tile, dims.seq_len), ct = std::min(tile.key_tile, dims.key_blocks);
+    return (dims.seq_len + cs - 1) / cs * ((dims.key_blocks + ct - 1) / ct);
+}
+
+TopKResult run_chunked(const IndexerInputs& inputs, const ProblemDims& dims, const DriverConfig& config,
+                       MemoryLedger& ledger, RunStats* stats) {
+    detail::check_extents(dims, inputs.q.size(), inputs.kc.size(), inputs.w.size());
+    return detail::run_chunked_view({inputs.q.data(), inputs.kc.data(), inputs.w.data()}, dims, config, ledger,
+                                    stats);
+}
+
+TopKResult run_materialize(const IndexerInputs& inputs, const ProblemDims& dims, AccumulationMode mode,
+                           MemoryLedger& ledger, ScoreKernel kernel) {
+    detail::check_extents(dims, inputs.q.size(), inputs.kc.size(), inputs.w.size());
+    return detail::run_materialize_view({inputs.q.data(), inputs.kc.data(), inputs.w.data()}, dims, mode, ledger,
+                                        kernel);
+}
+
+DispatchDecision choose_path(const ProblemDims& dims, uint64_t threshold_bytes) {
+    const uint64_t predicted = materialize_bytes(dims);
+    return {predicted <= threshold_bytes ? ExecutionPath::materialize : ExecutionPath::chunked, predicted};
+}
+
+TopKResult dispatch(const IndexerInputs& inputs, const ProblemDims& dims, const DriverConfig& config,
+                    MemoryLedger& ledger, DispatchDecision* decision_out, RunStats* stats_out) {
+    const DispatchDecision decision = choose_path(dims, config.auto_threshold_bytes);
+    if (decision_out != nullptr) *decision_out = decision;
+    if (decision.path == ExecutionPath::materialize) {
+        if (stats_out != nullptr) *stats_out = RunStats{};
+        return run_materialize(inputs, dims, config.mode, ledger, config.kernel);
+    }
+    return run_chunked(inputs, dims, config, ledger, stats_out);
+}
+
+namespace gpu {
+
+void run_chunked_device(const DeviceOperands& ops, const ProblemDims& dims, const DriverConfig& config,
+                        const std::vector<int64_t>* chunk_starts, int64_t* out_indices, float* out_values,
+                        int64_t out_rows, MemoryLedger& ledger, RunStats* stats_out) {
+    detail::validate_dims(dims);
+    const detail::ChunkPlan plan = detail::plan_chunks(dims, config.tile, chunk_starts);
+    int64_t need = 0;
+    for (size_t c = 0; c < plan.starts.size(); ++c) need = plan.out_row0[c] + std::min(plan.cs, dims.seq_len - plan.starts[c]);
+    if (out_rows < need) throw std::invalid_argument("run_chunked_device: out_rows too small for the chunk list");
+    const int kcode = detail::kernel_code(config.kernel);
+    if (ops.dtype != detail::operand_dtype(dims, detail::mode_code(config.mode), kcode))
+        throw std::invalid_argument("run_chunked_device: operand dtype does not match the selected score kernel");
+    std::lock_guard<std::mutex> lock(detail::engine_mutex());
+    csaidx_engine* e = detail::engine();
+    RunStats stats;
+    detail::run_plan(e, detail::DeviceOps{ops.q, ops.kc, ops.w, ops.dtype}, dims, config, plan, out_indices,
+                     out_values, out_rows, ledger, stats);
+    if (stats_out != nullptr) *stats_out = stats;
+}
+
+}  // namespace gpu
+
+}  // namespace csaidx

@@ -1,0 +1,127 @@
+// Kernel-side parameter blocks and launchers. Internal to libcsaidx_cuda;
+// the public boundary is include/csaidx_cuda.h.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+// ------------------------------------------------------------------ score
+struct ScoreTcParams {
+    const float* w;     // [B, S, 64] fp32 mixing weights
+    float* out;         // [B, rows, ld] fp32 scores
+    int* nonfinite;     // set to 1 when an unmasked score is not finite
+    int64_t ld;
+    int64_t seq_len, key_blocks, ratio;
+    int64_t s0, rows, t0, cols;
+    int batch;
+    int apply_mask;
+    // filled by the launcher
+    int nqb, npieces, nitems;
+};
+
+struct ScoreExactParams {
+    const void* q;            // [B, S, H, D], bf16 or fp32 (operand_f32)
+    const void* kc;           // [B, T, D]
+    const float* w;           // [B, S, H]
+    float* out;               // [B, rows, ld]
+    int* nonfinite;
+    int64_t ld;
+    int64_t seq_len, key_blocks, heads, head_dim, ratio;
+    int64_t s0, rows, t0, cols;
+    int batch;
+    int apply_mask;
+    int fp16;  // emulate binary16 rounding points (score_scalar.cpp:29-32)
+    int operand_f32;  // 1: q/kc are fp32 (bit-exact vs the CPU reference on any input)
+};
+
+// ------------------------------------------------------------------ select
+// Per (b, row): exact top-min(k, n) of the row's first n columns under the
+// reference order (score desc, index asc), n = legal columns of that row
+// (or all cols when apply_mask == 0). Output rows are `width` wide, sorted,
+// padded with (-inf, -1).
+struct SelectParams {
+    const float* scores;  // [B, rows, ld]
+    int64_t ld;
+    int64_t rows, cols, s0, t0, ratio;
+    int batch;
+    int apply_mask;
+    int k;
+    int width;
+    float* out_val;       // [B, rows, out_ld]
+    int32_t* out_idx;
+    int64_t out_ld;
+};
+
+// ------------------------------------------------------------------ merge
+// Per row: run := top-k(run U cand) (merge) or run := cand (overwrite, A1).
+struct MergeParams {
+    float* run_val;        // [nrows, k], sorted
+    int32_t* run_idx;
+    const float* cand_val; // [nrows, cand_ld], sorted, width valid
+    const int32_t* cand_idx;
+    int64_t cand_ld;
+    int64_t nrows;
+    int k;
+    int width;
+    int overwrite;
+    int check_overlap;
+    int* overlap_flag;
+};
+
+// ------------------------------------------------------------------ finalize
+// Sentinel pass (driver.cpp:84-105): -inf -> index -1, trailing check,
+// valid == k_eff check; widen to int64 into the output rows.
+struct FinalizeParams {
+    const float* run_val;   // [B, rows, k]
+    const int32_t* run_idx;
+    int64_t rows, s0, ratio;
+    int batch;
+    int k;
+    int check_keff;
+    int64_t* out_idx;       // [B, out_rows, k] at row offset out_row0
+    float* out_val;
+    int64_t out_rows, out_row0;
+    int* trail_flag;        // sentinel entries do not trail
+    int* keff_flag;         // valid != k_eff
+};
+
+// ------------------------------------------------------------------ prep
+struct ConvertParams {
+    const float* src;
+    __nv_bfloat16* dst;
+    int64_t n;
+    int* inexact_flag;  // set when an element is not bf16-representable
+    int* nonfinite_flag;
+};
+
+namespace csaidx_kern {
+
+bool score_tc_supported(int64_t heads, int64_t head_dim);
+size_t score_tc_smem_bytes();
+cudaError_t launch_score_tc(const CUtensorMap& qmap, const CUtensorMap& kmap, ScoreTcParams p,
+                            int num_sms, cudaStream_t stream);
+cudaError_t launch_score_exact(const ScoreExactParams& p, cudaStream_t stream);
+
+int select_max_take();
+cudaError_t launch_select(const SelectParams& p, cudaStream_t stream);
+cudaError_t launch_merge(const MergeParams& p, cudaStream_t stream);
+cudaError_t launch_finalize(const FinalizeParams& p, cudaStream_t stream);
+
+cudaError_t launch_convert_bf16(const ConvertParams& p, cudaStream_t stream);
+cudaError_t launch_fill_sentinel(float* val, int32_t* idx, int64_t n, cudaStream_t stream);
+cudaError_t launch_bool_mask(uint8_t* keep, int64_t rows, int64_t cols, int64_t s0, int64_t t0,
+                             int64_t ratio, cudaStream_t stream);
+cudaError_t launch_apply_bool_mask(float* scores, int64_t ld, const uint8_t* keep, int64_t batch,
+                                   int64_t rows, int64_t cols, cudaStream_t stream);
+// Counter-based synthetic normal generator (splitmix64 hash of the element
+// index + Box-Muller), rounded to bf16 or kept fp32.
+cudaError_t launch_gen_normal_bf16(__nv_bfloat16* dst, int64_t n, double stddev, uint64_t seed,
+                                   uint64_t stream_id, int64_t offset, cudaStream_t stream);
+cudaError_t launch_gen_normal_f32(float* dst, int64_t n, double stddev, uint64_t seed,
+                                  uint64_t stream_id, int64_t offset, cudaStream_t stream);
+
+}  // namespace csaidx_kern

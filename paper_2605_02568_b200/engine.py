@@ -1,0 +1,140 @@
+"""Device-level handle over the C-ABI: one engine per GPU.
+
+Tensors are torch CUDA tensors (PyTorch is used for device memory and
+streams only); every compute call goes through libcsaidx_cuda.so.
+"""
+from __future__ import annotations
+
+import ctypes
+from ctypes import byref, c_int, c_uint64, c_void_p
+
+import torch
+
+from . import _capi
+from ._capi import Dims, check
+
+NEG_INF = float("-inf")
+
+
+def dims_struct(batch, seq_len, heads, head_dim, ratio, top_k, key_blocks=None) -> Dims:
+    if key_blocks is None:
+        key_blocks = seq_len // ratio
+    return Dims(batch, seq_len, key_blocks, heads, head_dim, ratio, top_k)
+
+
+def _dtype(t):
+    if t.dtype == torch.bfloat16:
+        return _capi.DTYPE_BF16
+    if t.dtype == torch.float32:
+        return _capi.DTYPE_F32
+    raise TypeError(f"q/kc must be bf16 or fp32, got {t.dtype}")
+
+
+def _p(t):
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+class Engine:
+    """Wraps csaidx_engine (include/csaidx_cuda.h)."""
+
+    def __init__(self, device: int = 0, use_torch_stream: bool = True):
+        self.lib = _capi.cuda_lib()
+        self.device = device
+        h = c_void_p()
+        check(self.lib.csaidx_engine_create(device, byref(h)))
+        self.handle = h
+        if use_torch_stream:
+            self.use_stream(torch.cuda.current_stream(device))
+
+    def close(self):
+        if self.handle:
+            self.lib.csaidx_engine_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - interpreter teardown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def use_stream(self, stream: torch.cuda.Stream | None):
+        """Enqueue on a torch stream (None: the engine's own stream)."""
+        if stream is None:
+            check(self.lib.csaidx_engine_use_own_stream(self.handle))
+        else:
+            check(self.lib.csaidx_engine_set_stream(self.handle, c_void_p(stream.cuda_stream)))
+
+    @property
+    def num_sms(self) -> int:
+        n = c_int()
+        check(self.lib.csaidx_engine_num_sms(self.handle, byref(n)))
+        return n.value
+
+    def check(self):
+        check(self.lib.csaidx_engine_check(self.handle))
+
+    def mem_stats(self):
+        live, peak = c_uint64(), c_uint64()
+        check(self.lib.csaidx_engine_mem_stats(self.handle, byref(live), byref(peak)))
+        return live.value, peak.value
+
+    # ------------------------------------------------------------ operands
+    def to_bf16(self, src: torch.Tensor, strict: bool = False) -> torch.Tensor:
+        assert src.dtype == torch.float32 and src.is_cuda and src.is_contiguous()
+        dst = torch.empty(src.shape, dtype=torch.bfloat16, device=src.device)
+        check(self.lib.csaidx_cuda_to_bf16(self.handle, _p(src), _p(dst), src.numel(), int(strict)))
+        return dst
+
+    def gen_normal_bf16(self, n: int, stddev: float, seed: int, stream_id: int, offset: int = 0) -> torch.Tensor:
+        out = torch.empty(n, dtype=torch.bfloat16, device=f"cuda:{self.device}")
+        check(self.lib.csaidx_cuda_gen_normal_bf16(self.handle, _p(out), n, stddev, seed, stream_id, offset))
+        return out
+
+    def gen_normal_f32(self, n: int, stddev: float, seed: int, stream_id: int, offset: int = 0) -> torch.Tensor:
+        out = torch.empty(n, dtype=torch.float32, device=f"cuda:{self.device}")
+        check(self.lib.csaidx_cuda_gen_normal_f32(self.handle, _p(out), n, stddev, seed, stream_id, offset))
+        return out
+
+    # ------------------------------------------------------------ hot path
+    def score(self, q, kc, w, dims: Dims, s0, rows, t0, cols, mode=0, kernel=0, apply_mask=False, out=None):
+        ld = (cols + 3) // 4 * 4
+        if out is None:
+            out = torch.empty((dims.batch, rows, ld), dtype=torch.float32, device=q.device)
+        else:
+            ld = out.shape[-1]
+        check(self.lib.csaidx_cuda_score(self.handle, _p(q), _p(kc), _dtype(q), _p(w), byref(dims), s0, rows, t0,
+                                         cols, mode,
+                                         kernel, int(apply_mask), _p(out), ld))
+        return out
+
+    def select(self, scores, batch, rows, cols, s0, t0, ratio, k, apply_mask=True):
+        ld = scores.shape[-1]
+        width = min(k, cols)
+        val = torch.empty((batch, rows, width), dtype=torch.float32, device=scores.device)
+        idx = torch.empty((batch, rows, width), dtype=torch.int32, device=scores.device)
+        check(self.lib.csaidx_cuda_select(self.handle, _p(scores), batch, rows, ld, cols, s0, t0, ratio,
+                                          int(apply_mask), k, _p(val), _p(idx), width))
+        return val, idx
+
+    def merge(self, run_val, run_idx, cand_val, cand_idx, overwrite=False, check_overlap=False):
+        k = run_val.shape[-1]
+        nrows = run_val.numel() // k
+        width = cand_val.shape[-1]
+        check(self.lib.csaidx_cuda_merge(self.handle, _p(run_val), _p(run_idx), nrows, k, _p(cand_val),
+                                         _p(cand_idx), width, width, int(overwrite), int(check_overlap)))
+
+    def fill_sentinel(self, val, idx):
+        check(self.lib.csaidx_cuda_fill_sentinel(self.handle, _p(val), _p(idx), val.numel()))
+
+    def finalize(self, run_val, run_idx, batch, rows, s0, ratio, k, out_idx, out_val, out_row0, check_keff=True):
+        out_rows = out_idx.shape[1]
+        check(self.lib.csaidx_cuda_finalize(self.handle, _p(run_val), _p(run_idx), batch, rows, s0, ratio, k,
+                                            int(check_keff), _p(out_idx), _p(out_val), out_rows, out_row0))
+
+    def chunk_step(self, q, kc, w, dims, s0, rows, t0, cols, score_buf, cand_val, cand_idx, run_val, run_idx,
+                   first_tile, mode=0, kernel=0, overwrite=False):
+        check(self.lib.csaidx_cuda_chunk_step(self.handle, _p(q), _p(kc), _dtype(q), _p(w), byref(dims), s0, rows,
+                                              t0, cols,
+                                              mode, kernel, _p(score_buf), score_buf.shape[-1], _p(cand_val),
+                                              _p(cand_idx), _p(run_val), _p(run_idx), int(first_tile),
+                                              int(overwrite)))

@@ -1,0 +1,229 @@
+"""Kernel-level parity through the C-ABI (device pointers).
+
+score_tc (tcgen05) is compared with a float64 restatement of the score
+definition (tolerance below); score_exact with the reference's fp32 op order
+(bit-exact); select / merge / finalize with sort-based selection under the
+reference order (bit-exact, ties included).
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+NEG_INF = np.float32(-np.inf)
+
+
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(torch.bfloat16).float().numpy()
+
+
+def make_inputs(B, S, H, D, m, seed=0):
+    rng = np.random.default_rng(seed)
+    T = S // m
+    q = bf16_round(rng.normal(0, D ** -0.5, (B, S, H, D)))
+    kc = bf16_round(rng.normal(0, D ** -0.5, (B, T, D)))
+    w = rng.normal(0, (D * H) ** -0.5, (B, S, H)).astype(np.float32)
+    return q, kc, w
+
+
+def ref_scores_f64(q, kc, w, s0, rows, t0, cols):
+    qq = q[:, s0:s0 + rows].astype(np.float64)           # B,rows,H,D
+    kk = kc[:, t0:t0 + cols].astype(np.float64)          # B,cols,D
+    dots = np.einsum("brhd,bcd->brhc", qq, kk)
+    return np.einsum("brh,brhc->brc", w[:, s0:s0 + rows].astype(np.float64), np.maximum(dots, 0.0))
+
+
+def ref_scores_exact_f32(q, kc, w, s0, rows, t0, cols):
+    """score_scalar.cpp:20-34 op order in float32 numpy (one rounding per op)."""
+    B, _, H, D = q.shape
+    out = np.zeros((B, rows, cols), np.float32)
+    for b in range(B):
+        qq = q[b, s0:s0 + rows]
+        kk = kc[b, t0:t0 + cols]
+        acc = np.zeros((rows, cols), np.float32)
+        for h in range(H):
+            dot = np.zeros((rows, cols), np.float32)
+            for d in range(D):
+                dot = dot + qq[:, h, d][:, None] * kk[:, d][None, :]
+            rect = np.where(dot < 0, np.float32(0), dot)
+            acc = acc + w[b, s0:s0 + rows, h][:, None] * rect
+        out[b] = acc
+    return out
+
+
+def legal(s, m):
+    return (s + 1) // m
+
+
+def ref_select(scores, s0, t0, m, k, apply_mask=True):
+    """tile_topk over legal columns, sorted by (score desc, index asc)."""
+    B, rows, cols = scores.shape
+    width = min(k, cols)
+    val = np.full((B, rows, width), NEG_INF, np.float32)
+    idx = np.full((B, rows, width), -1, np.int32)
+    for b in range(B):
+        for i in range(rows):
+            n = cols if not apply_mask else int(np.clip(legal(s0 + i, m) - t0, 0, cols))
+            row = scores[b, i, :n]
+            order = np.lexsort((np.arange(n), -row.astype(np.float64)))[: min(k, n)]
+            val[b, i, : len(order)] = row[order]
+            idx[b, i, : len(order)] = order + t0
+    return val, idx
+
+
+def to_dev(x, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    return t.to(dtype) if dtype is not None else t
+
+
+@pytest.mark.parametrize(
+    "B,S,s0,rows,t0,cols",
+    [(1, 512, 0, 512, 0, 128), (1, 1024, 40, 77, 3, 250), (2, 2048, 1000, 300, 100, 412)],
+)
+def test_score_tc_matches_definition(engine, B, S, s0, rows, t0, cols):
+    from paper_2605_02568_b200.engine import dims_struct
+
+    H, D, m = 64, 128, 4
+    q, kc, w = make_inputs(B, S, H, D, m, seed=S + rows)
+    dims = dims_struct(B, S, H, D, m, 16)
+    out = engine.score(to_dev(q, torch.bfloat16), to_dev(kc, torch.bfloat16), to_dev(w), dims, s0, rows, t0, cols)
+    engine.check()
+    got = out[:, :, :cols].cpu().numpy()
+    want = ref_scores_f64(q, kc, w, s0, rows, t0, cols)
+    scale = np.abs(want).max()
+    err = np.abs(got - want).max()
+    assert err <= 1e-5 * scale, (err, scale)
+
+
+def test_score_tc_mask_and_causal_skip(engine):
+    from paper_2605_02568_b200.engine import dims_struct
+
+    B, S, H, D, m = 1, 4096, 64, 128, 4
+    q, kc, w = make_inputs(B, S, H, D, m, seed=7)
+    dims = dims_struct(B, S, H, D, m, 16)
+    s0, rows, t0, cols = 1536, 512, 128, 768
+    out = engine.score(to_dev(q, torch.bfloat16), to_dev(kc, torch.bfloat16), to_dev(w), dims, s0, rows, t0, cols,
+                       apply_mask=True)
+    engine.check()
+    got = out[:, :, :cols].cpu().numpy()
+    want = ref_scores_f64(q, kc, w, s0, rows, t0, cols)
+    scale = np.abs(want).max()
+    for i in range(rows):
+        n = int(np.clip(legal(s0 + i, m) - t0, 0, cols))
+        assert np.abs(got[0, i, :n] - want[0, i, :n]).max(initial=0) <= 1e-5 * scale
+        # causally dead columns inside a computed key tile are -inf
+        tail = got[0, i, n:min(cols, (n + 127) // 128 * 128)]
+        assert np.all(tail == NEG_INF) or n == 0
+
+
+def test_score_tc_is_tiling_invariant(engine):
+    """Each score must not depend on which tile computed it (chunked == materialize)."""
+    from paper_2605_02568_b200.engine import dims_struct
+
+    B, S, H, D, m = 1, 2048, 64, 128, 4
+    q, kc, w = make_inputs(B, S, H, D, m, seed=11)
+    dims = dims_struct(B, S, H, D, m, 16)
+    qd, kd, wd = to_dev(q, torch.bfloat16), to_dev(kc, torch.bfloat16), to_dev(w)
+    full = engine.score(qd, kd, wd, dims, 0, S, 0, S // m)[:, :, : S // m].cpu().numpy()
+    for (s0, rows, t0, cols) in [(5, 33, 7, 100), (1000, 1, 0, 512), (2040, 8, 300, 212)]:
+        part = engine.score(qd, kd, wd, dims, s0, rows, t0, cols)[:, :, :cols].cpu().numpy()
+        assert np.array_equal(part, full[:, s0:s0 + rows, t0:t0 + cols])
+
+
+@pytest.mark.parametrize("H,D,fp16", [(1, 1, False), (3, 5, False), (8, 24, False), (2, 7, True)])
+def test_score_exact_is_bit_exact(engine, H, D, fp16):
+    from paper_2605_02568_b200.engine import dims_struct
+
+    B, S, m = 2, 48, 4
+    q, kc, w = make_inputs(B, S, H, D, m, seed=H * 100 + D)
+    dims = dims_struct(B, S, H, D, m, 4)
+    out = engine.score(to_dev(q, torch.bfloat16), to_dev(kc, torch.bfloat16), to_dev(w), dims, 0, S, 0, S // m,
+                       mode=1 if fp16 else 0, kernel=1)
+    engine.check()
+    got = out[:, :, : S // m].cpu().numpy()
+    if not fp16:
+        want = ref_scores_exact_f32(q, kc, w, 0, S, 0, S // m)
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    else:
+        assert np.all(np.isfinite(got))
+
+
+@pytest.mark.parametrize("cols,k,quant", [(300, 16, False), (5000, 512, False), (20000, 1024, True), (9000, 2048, True), (7, 10, False)])
+def test_select_matches_sorted_reference(engine, cols, k, quant):
+    rng = np.random.default_rng(cols + k)
+    B, rows, m = 2, 9, 1
+    s0, t0 = cols - 5, 0
+    scores = rng.normal(0, 1, (B, rows, cols)).astype(np.float32)
+    if quant:
+        scores = np.round(scores * 4) / 4  # heavy ties
+    ld = (cols + 3) // 4 * 4
+    pad = np.zeros((B, rows, ld), np.float32)
+    pad[:, :, :cols] = scores
+    val, idx = engine.select(to_dev(pad), B, rows, cols, s0, t0, m, k)
+    engine.check()
+    wv, wi = ref_select(scores, s0, t0, m, k)
+    assert np.array_equal(idx.cpu().numpy(), wi)
+    assert np.array_equal(val.cpu().numpy().view(np.uint32), wv.view(np.uint32))
+
+
+def test_select_all_equal_scores_take_smallest_indices(engine):
+    B, rows, cols, k = 1, 3, 10000, 100
+    scores = np.zeros((B, rows, cols), np.float32)
+    val, idx = engine.select(to_dev(scores), B, rows, cols, 10 ** 6, 0, 1, k)
+    engine.check()
+    assert np.array_equal(idx.cpu().numpy()[0, 0], np.arange(k, dtype=np.int32))
+
+
+def test_merge_equals_union_topk(engine):
+    rng = np.random.default_rng(3)
+    rows, k = 50, 64
+    run = np.sort(rng.integers(0, 20, (rows, k)).astype(np.float32))[:, ::-1]
+    run_i = np.stack([rng.permutation(1000)[:k] for _ in range(rows)]).astype(np.int32)
+    cand = np.sort(rng.integers(0, 20, (rows, 40)).astype(np.float32))[:, ::-1]
+    cand_i = (1000 + np.stack([rng.permutation(1000)[:40] for _ in range(rows)])).astype(np.int32)
+    # make each list sorted under (score desc, index asc)
+    for arr_v, arr_i in ((run, run_i), (cand, cand_i)):
+        for r in range(rows):
+            o = np.lexsort((arr_i[r], -arr_v[r]))
+            arr_v[r], arr_i[r] = arr_v[r][o].copy(), arr_i[r][o].copy()
+    rv, ri = to_dev(run.copy()), to_dev(run_i.copy())
+    engine.merge(rv, ri, to_dev(cand.copy()), to_dev(cand_i.copy()))
+    engine.check()
+    for r in range(rows):
+        v = np.concatenate([run[r], cand[r]])
+        i = np.concatenate([run_i[r], cand_i[r]])
+        o = np.lexsort((i, -v))[:k]
+        assert np.array_equal(ri.cpu().numpy()[r], i[o])
+        assert np.array_equal(rv.cpu().numpy()[r], v[o])
+
+
+def test_chunked_pipeline_small_v4(engine):
+    """score -> select -> merge over several key tiles == one-shot selection."""
+    from paper_2605_02568_b200.engine import dims_struct
+
+    B, S, H, D, m, k = 1, 4096, 64, 128, 4, 512
+    q, kc, w = make_inputs(B, S, H, D, m, seed=99)
+    dims = dims_struct(B, S, H, D, m, k)
+    qd, kd, wd = to_dev(q, torch.bfloat16), to_dev(kc, torch.bfloat16), to_dev(w)
+    T = S // m
+    full = engine.score(qd, kd, wd, dims, 0, S, 0, T, apply_mask=True)
+    fv, fi = engine.select(full, B, S, T, 0, 0, m, k)
+    s0, rows, ct = 2048, 1024, 200
+    rv = torch.empty((B, rows, k), dtype=torch.float32, device="cuda")
+    ri = torch.empty((B, rows, k), dtype=torch.int32, device="cuda")
+    engine.fill_sentinel(rv, ri)
+    ld = (ct + 3) // 4 * 4
+    sb = torch.empty((B, rows, ld), dtype=torch.float32, device="cuda")
+    cv = torch.empty((B, rows, k), dtype=torch.float32, device="cuda")
+    ci = torch.empty((B, rows, k), dtype=torch.int32, device="cuda")
+    first = True
+    for t0 in range(0, T, ct):
+        cols = min(ct, T - t0)
+        if t0 >= legal(s0 + rows - 1, m):
+            break
+        engine.chunk_step(qd, kd, wd, dims, s0, rows, t0, cols, sb, cv, ci, rv, ri, first)
+        first = False
+    engine.check()
+    assert np.array_equal(ri.cpu().numpy(), fi[:, s0:s0 + rows].cpu().numpy())
+    assert np.array_equal(rv.cpu().numpy(), fv[:, s0:s0 + rows].cpu().numpy())
