@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark of the CSA lightning-indexer step on B200 (one JSON line).
+
+Metric (BASELINE.json): indexer query·key pairs/sec (+ peak HBM), V4-Flash.
+Default workload = C3: B=1, S=262,144 (T=65,536), H_I=64, d_h=128, m=4,
+k=1024, c_S=2048, query-sharded over the N GPUs of one node (strong scaling:
+the same problem at every N). One "step" = the full indexer step over the
+whole instance: K broadcast (N>1) -> score/mask/select/merge for every
+query chunk -> gather of the [S, k] index output to rank 0 (N>1).
+
+* value  — legal (causal) query·key pairs per second, whole job, operands
+           resident in HBM (bf16 q/kc generated on device), max over ranks.
+* e2e    — the same metric through the reference-facing host API
+           (csaidx_host_run_chunked_rows) from pinned fp32 host buffers, H2D
+           of q/kc/w and D2H of indices+values inside the timed region.
+* roofline — score kernel (tcgen05): algorithmic FLOPs (16,384 per legal
+           pair) / event-timed kernel ms, vs MEASURED_PEAKS.json.
+* cpu_baseline — the reference C++ library (oracle/_ref, compiled from the
+           reference sources) on this host's cores, bounded sample.
+
+`--impl reference` times that reference CPU path alone (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (B, S, H, D, m, k, c_S, c_T or None=T)
+    "c1": (1, 4096, 64, 128, 4, 512, 2048, None),
+    "c2": (1, 65536, 64, 128, 4, 512, 2048, None),
+    "c3": (1, 262144, 64, 128, 4, 1024, 2048, None),
+    "c4": (1, 1048576, 64, 128, 4, 1024, 2048, None),
+    "c5": (2, 131072, 64, 128, 4, 1024, 2048, None),
+}
+FLOPS_PER_PAIR = 2 * 64 * 128
+
+
+def legal_pairs_rows(S, m, starts, cs, T):
+    tot = 0
+    for s0 in starts:
+        t = np.arange(s0, min(s0 + cs, S), dtype=np.int64)
+        tot += int(np.minimum((t + 1) // m, T).sum())
+    return tot
+
+
+def shard_chunks(S, m, cs, world, rank):
+    """LPT assignment of c_S chunks by causal work (balanced query sharding)."""
+    starts = list(range(0, S, cs))
+    cost = [(legal_pairs_rows(S, m, [s], cs, S // m), s) for s in starts]
+    cost.sort(reverse=True)
+    loads = [0] * world
+    owner = {}
+    for c, s in cost:
+        r = min(range(world), key=lambda i: (loads[i], i))
+        loads[r] += c
+        owner[s] = r
+    mine = sorted(s for s in starts if owner[s] == rank)
+    return mine, loads
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_baseline(S, m, H, D, k, budget_s=15.0):
+    """The reference library (oracle/_ref) on this host: process_query_tile's
+    engine sequence over a deterministic sample of query tiles."""
+    from oracle.oracle import Reference
+
+    ref = Reference()
+    threads = os.cpu_count() or 1
+    cs, ct = 64, 1024
+    sec, pairs = ref.sample_chunked(S, m, H, D, k, cs, ct, threads, threads)
+    rate = pairs / max(sec, 1e-9)
+    avg_tile = pairs / threads
+    n_tiles = int(max(threads, min(threads * 64, budget_s * rate / max(avg_tile, 1.0))))
+    sec, pairs = ref.sample_chunked(S, m, H, D, k, cs, ct, n_tiles, threads)
+    return {"value": pairs / sec, "unit": "legal pairs/s", "cores": threads, "kind": "reference",
+            "sample": f"{n_tiles} query tiles of c_S={cs} (c_T={ct}) spread evenly over t of S={S}, full causal "
+                      f"key range each; {pairs:.3e} legal pairs in {sec:.1f} s (reference run_chunked engine "
+                      f"sequence, std::thread x{threads})"}
+
+
+def run_reference_arm(args, wl):
+    B, S, H, D, m, k, cs, ct = wl
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle.oracle import Reference
+
+    ref = Reference()
+    threads = os.cpu_count() or 1
+    n_tiles = threads * 2
+    samples = []
+    for i in range(args.warmup + args.steps):
+        sec, pairs = ref.sample_chunked(S, m, H, D, k, 64, 1024, n_tiles, threads, seed=1 + i)
+        if i >= args.warmup:
+            samples.append((sec, pairs))
+    sec = sum(s for s, _ in samples)
+    pairs = sum(p for _, p in samples)
+    value = pairs / sec
+    line = {
+        "impl": "reference", "metric": "indexer query·key pairs/sec (legal causal pairs)", "value": value,
+        "unit": "legal pairs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * sec / max(len(samples), 1), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference generator)",
+        "config": {"workload": args.workload, "B": B, "S": S, "H_I": H, "d_h": D, "m": m, "k": k},
+        "cpu_baseline": {"value": value, "unit": "legal pairs/s", "cores": threads, "kind": "reference",
+                         "sample": f"per step {n_tiles} query tiles of c_S=64 (c_T=1024) spread over t of S={S}"},
+        "e2e": {"value": value, "unit": "legal pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--cs", type=int, default=None)
+    ap.add_argument("--ct", type=int, default=None)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no e2e/baseline)")
+    args = ap.parse_args()
+    wl = list(WORKLOADS[args.workload])
+    if args.cs:
+        wl[6] = args.cs
+    if args.ct:
+        wl[7] = args.ct
+    if args.impl == "reference":
+        return run_reference_arm(args, wl)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_02568_b200 import _capi, api
+    from paper_2605_02568_b200.engine import Engine
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.Stream()  # all timed work and its events live on this stream
+    torch.cuda.set_stream(stream)
+
+    B, S, H, D, m, k, cs, ct = wl
+    T = S // m
+    ct = ct or T
+    cfg = api.DriverConfig(tile=api.TileConfig(cs, ct), device=local, stream=stream.cuda_stream)
+    dims = api.ProblemDims.create(B, S, m, H, D, k)
+    mine, loads = shard_chunks(S, m, cs, world, rank)
+    rows = api.chunk_rows(dims, cfg, mine)
+    pairs_total = B * legal_pairs_rows(S, m, range(0, S, cs), cs, T)
+    pairs_mine = B * legal_pairs_rows(S, m, mine, cs, T)
+
+    # ---------------------------------------------------------- operands in HBM
+    eng = Engine(local)
+    q = eng.gen_normal_bf16(B * S * H * D, D ** -0.5, 1, 1)
+    w = eng.gen_normal_f32(B * S * H, (D * H) ** -0.5, 1, 3)
+    if rank == 0:
+        kc = eng.gen_normal_bf16(B * T * D, D ** -0.5, 1, 2)
+    else:
+        kc = torch.empty(B * T * D, dtype=torch.bfloat16, device="cuda")
+    out_idx = torch.empty((B, rows, k), dtype=torch.int64, device="cuda")
+    out_val = torch.empty((B, rows, k), dtype=torch.float32, device="cuda")
+    max_rows = rows
+    if world > 1:
+        t = torch.tensor([rows], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        max_rows = int(t.item())
+        send = torch.zeros((B, max_rows, k), dtype=torch.int64, device="cuda")
+        gather_list = [torch.empty_like(send) for _ in range(world)] if rank == 0 else None
+    torch.cuda.synchronize()
+
+    stats_box = {}
+
+    def step():
+        if world > 1:
+            dist.broadcast(kc, src=0)  # keys once over NVLink
+        st = api.run_chunked_device(q, kc, w, dims, cfg, mine, out_idx, out_val)[2]
+        stats_box["st"] = st
+        if world > 1:
+            send[:, :rows].copy_(out_idx)
+            dist.gather(send, gather_list, dst=0)  # only the [S, k] indices travel
+
+    drv = api.KernelStats(api.driver_engine(local))
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.reset_peak_memory_stats()
+    drv.reset()
+    drv.profiling(True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    drv.profiling(False)
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    kinds = {"score": _capi.KIND_SCORE, "select": _capi.KIND_SELECT, "merge": _capi.KIND_MERGE,
+             "finalize": _capi.KIND_FINALIZE, "prep": _capi.KIND_PREP}
+    kstats = {name: drv.get(kd) for name, kd in kinds.items()}
+    launches = sum(n for n, _ in kstats.values())
+    score_n, score_ms = kstats["score"]
+    peaks, peak_src = load_peaks()
+    score_flops = pairs_mine * FLOPS_PER_PAIR * args.steps
+    achieved_tflops = score_flops / (score_ms / 1000.0) / 1e12 if score_ms > 0 else None
+    peak_tflops = peaks["bf16_tflops_sustained"]
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(args.workload, {}).get("score_dram_bytes_per_launch")
+    sel_n, sel_ms = kstats["select"]
+    select_gbs = (pairs_mine * 4 * args.steps) / (sel_ms / 1000.0) / 1e9 if sel_ms > 0 else None
+    _, drv_peak = drv.mem()
+    hbm_peak = torch.cuda.max_memory_allocated() + drv_peak
+    st = stats_box["st"]
+
+    # ---------------------------------------------------------- e2e (host API)
+    e2e = None
+    if not args.no_e2e and not args.profile_only:
+        qh = torch.empty((B, S, H, D), dtype=torch.float32, pin_memory=True)
+        qh.view(-1).copy_(q.float())
+        kch = torch.empty((B, T, D), dtype=torch.float32, pin_memory=True)
+        if world > 1:
+            dist.broadcast(kc, src=0)
+        kch.view(-1).copy_(kc.float())
+        wh = torch.empty((B, S, H), dtype=torch.float32, pin_memory=True)
+        wh.view(-1).copy_(w)
+        oi = torch.empty((B, rows, k), dtype=torch.int64, pin_memory=True)
+        ov = torch.empty((B, rows, k), dtype=torch.float32, pin_memory=True)
+        ecfg = api.DriverConfig(tile=api.TileConfig(cs, ct), device=local, stream=0)
+        torch.cuda.synchronize()
+        api.run_chunked_rows(qh, kch, wh, dims, ecfg, mine, oi, ov)  # warm-up
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            api.run_chunked_rows(qh, kch, wh, dims, ecfg, mine, oi, ov)
+        torch.cuda.synchronize()
+        e2e_ms = (time.perf_counter() - t0) * 1000 / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        h2d = B * rows * H * D * 4 + B * T * D * 4 + B * rows * H * 4
+        d2h = B * rows * k * 12
+        e2e = {"value": pairs_total / (e2e_ms / 1000.0), "unit": "legal pairs/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "path": "csaidx_host_run_chunked_rows (libcsaidx.so C entry of csaidx::run_chunked), pinned fp32 "
+                       "host operands"}
+        # cheap end-to-end correctness guard: the host API must agree with the resident run
+        assert torch.equal(oi, out_idx.cpu()), "host-API result differs from the device-resident run"
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_only:
+        try:
+            cpu = cpu_baseline(S, m, H, D, k)
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"value": None, "unit": "legal pairs/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": "indexer query·key pairs/sec (legal causal pairs)",
+            "value": pairs_total / (ms / 1000.0),
+            "unit": "legal pairs/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic: counter-based N(0,1/d_h) q/kc rounded to bf16, w ~ N(0,1/(d_h*H_I)) fp32, on device",
+            "config": {"workload": f"{args.workload}: V4-Flash B={B} S={S} T={T} H_I={H} d_h={D} m={m} k={k}",
+                       "query_tile": cs, "key_tile": ct, "parallelism": f"query-sharded x{world} (LPT by causal work)",
+                       "l2": "inputs (q 4.3 GB bf16 at C3) exceed L2; no flush needed",
+                       "dense_pairs_per_s": B * S * T / (ms / 1000.0)},
+            "hbm_peak_gb": hbm_peak / 1e9,
+            "ledger_peak_bytes": st.ledger_peak_bytes,
+            "roofline": {"bound": "tensor", "kernel": "score_tc_kernel (tcgen05 kind::f16, M=128 keys x N=256 q-heads)",
+                         "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
+                         "frac": (achieved_tflops / peak_tflops) if achieved_tflops else None,
+                         "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
+                         "traffic": traffic, "algorithmic": f"{FLOPS_PER_PAIR} FLOP per legal pair",
+                         "launches": score_n, "avg_launch_ms": score_ms / max(score_n, 1)},
+            "kernels_ms_per_step": {n: v[1] / args.steps for n, v in kstats.items()},
+            "select_gbs_one_pass": select_gbs,
+            "gpu_launches": launches,
+            "clocks": clk,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "run_stats": {"dispatch_count": st.dispatch_count, "tiles_skipped_masked": st.tiles_skipped_masked},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

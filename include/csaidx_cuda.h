@@ -77,6 +77,19 @@ int csaidx_engine_check(csaidx_engine* e);
 int csaidx_engine_mem_stats(csaidx_engine* e, uint64_t* live, uint64_t* peak);
 int csaidx_engine_reset_peak(csaidx_engine* e);
 
+/* Kernel accounting: every launch is counted per class; with profiling on,
+ * CUDA events on the launching stream bracket each launch and
+ * csaidx_engine_kernel_stats resolves them into summed device milliseconds. */
+#define CSAIDX_KIND_SCORE 0
+#define CSAIDX_KIND_SELECT 1
+#define CSAIDX_KIND_MERGE 2
+#define CSAIDX_KIND_FINALIZE 3
+#define CSAIDX_KIND_PREP 4
+#define CSAIDX_NUM_KINDS 5
+int csaidx_engine_set_profiling(csaidx_engine* e, int enabled);
+int csaidx_engine_kernel_stats(csaidx_engine* e, int kind, int64_t* launches, double* total_ms);
+int csaidx_engine_reset_stats(csaidx_engine* e);
+
 /* Stream-ordered device memory from a cached pool. */
 int csaidx_cuda_alloc(csaidx_engine* e, size_t bytes, void** ptr);
 int csaidx_cuda_free(csaidx_engine* e, void* ptr);

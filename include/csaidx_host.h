@@ -56,6 +56,8 @@ typedef struct csaidx_run_stats {
 
 const char* csaidx_host_last_error(void);
 void csaidx_host_default_config(csaidx_run_config* cfg);
+/* The engine the driver uses for `device` (for profiling / memory stats). */
+int csaidx_host_engine(int device, csaidx_engine** out);
 
 /* run_chunked / run_materialize / dispatch on host fp32 buffers
  * q [B,S,H,D], kc [B,T,D], w [B,S,H]; results into host [B,S,k]. */
@@ -68,6 +70,14 @@ int csaidx_host_run_materialize(const float* q, const float* kc, const float* w,
 int csaidx_host_dispatch(const float* q, const float* kc, const float* w, const csaidx_dims* dims,
                          const csaidx_run_config* cfg, int64_t* out_idx, float* out_val,
                          csaidx_run_stats* stats);
+
+/* run_chunked on host buffers for a subset of query chunks (starts must be
+ * multiples of the clamped c_S; NULL / 0 = all): only those q / w rows
+ * cross PCIe; results packed into host [B, out_rows, k]. The per-rank entry
+ * of a query-sharded multi-GPU run. */
+int csaidx_host_run_chunked_rows(const float* q, const float* kc, const float* w, const csaidx_dims* dims,
+                                 const csaidx_run_config* cfg, const int64_t* chunk_starts, int64_t n_chunks,
+                                 int64_t* out_idx, float* out_val, int64_t out_rows, csaidx_run_stats* stats);
 
 /* Algorithm 2 over device-resident operands (dtype CSAIDX_DTYPE_*), for the
  * listed query chunks (NULL / 0 = all), outputs device [B, out_rows, k]. */

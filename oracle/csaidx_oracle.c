@@ -160,20 +160,52 @@ int64_t orc_k_eff(int64_t t, int64_t ratio, int64_t top_k) {
 
 /* ------------------------------------------------------------ score */
 
-/* score_scalar.cpp:20-34 */
-static float score_pair(const float* qrow, const float* krow, const float* wrow, int64_t heads, int64_t head_dim,
-                        int fp16) {
-    float acc = 0.0f;
-    for (int64_t h = 0; h < heads; ++h) {
-        const float* qh = qrow + h * head_dim;
-        float dot = 0.0f;
-        for (int64_t d = 0; d < head_dim; ++d) dot = dot + qh[d] * krow[d];
-        if (fp16) dot = orc_half_round(dot);
-        const float rect = (dot < 0.0f) ? 0.0f : dot;
-        acc = acc + wrow[h] * rect;
-        if (fp16) acc = orc_half_round(acc);
+/* score_scalar.cpp:20-34 for one query row against ncols consecutive key
+ * rows. Keys are processed in panels of ORC_PANEL lanes (transposed once per
+ * panel) so the compiler can vectorise ACROSS keys; every lane still runs the
+ * reference's exact per-score sequence: ascending-d dot as mul then add,
+ * x<0?0:x, ascending-h acc = acc + w*r (contraction is off for this TU). */
+#define ORC_PANEL 16
+typedef float orc_v8 __attribute__((vector_size(32)));
+static void score_span(const float* qrow, const float* wrow, const float* krows, int64_t ncols, int64_t heads,
+                       int64_t head_dim, int fp16, float* out) {
+    float* kt = (float*)malloc((size_t)(head_dim * ORC_PANEL) * sizeof(float));
+    for (int64_t j0 = 0; j0 < ncols; j0 += ORC_PANEL) {
+        const int64_t nb = ncols - j0 < ORC_PANEL ? ncols - j0 : ORC_PANEL;
+        for (int64_t d = 0; d < head_dim; ++d)
+            for (int64_t jj = 0; jj < ORC_PANEL; ++jj)
+                kt[d * ORC_PANEL + jj] = jj < nb ? krows[(j0 + jj) * head_dim + d] : 0.0f;
+        float acc[ORC_PANEL];
+        for (int jj = 0; jj < ORC_PANEL; ++jj) acc[jj] = 0.0f;
+        for (int64_t h = 0; h < heads; ++h) {
+            const float* qh = qrow + h * head_dim;
+            /* 2 x 8 independent lanes; separate mul and add (no contraction). */
+            orc_v8 d0 = {0, 0, 0, 0, 0, 0, 0, 0}, d1 = d0;
+            for (int64_t d = 0; d < head_dim; ++d) {
+                const float qv = qh[d];
+                const orc_v8 qb = {qv, qv, qv, qv, qv, qv, qv, qv};
+                orc_v8 k0, k1;
+                memcpy(&k0, kt + d * ORC_PANEL, sizeof(k0));
+                memcpy(&k1, kt + d * ORC_PANEL + 8, sizeof(k1));
+                d0 = d0 + qb * k0;
+                d1 = d1 + qb * k1;
+            }
+            float dot[ORC_PANEL];
+            memcpy(dot, &d0, sizeof(d0));
+            memcpy(dot + 8, &d1, sizeof(d1));
+            const float wh = wrow[h];
+            for (int jj = 0; jj < ORC_PANEL; ++jj) {
+                float dv = dot[jj];
+                if (fp16) dv = orc_half_round(dv);
+                const float rect = (dv < 0.0f) ? 0.0f : dv;
+                float a = acc[jj] + wh * rect;
+                if (fp16) a = orc_half_round(a);
+                acc[jj] = a;
+            }
+        }
+        for (int64_t jj = 0; jj < nb; ++jj) out[j0 + jj] = acc[jj];
     }
-    return acc;
+    free(kt);
 }
 
 void orc_score_tile(const float* q, const float* kc, const float* w, int64_t batch, int64_t seq_len,
@@ -182,12 +214,9 @@ void orc_score_tile(const float* q, const float* kc, const float* w, int64_t bat
     for (int64_t b = 0; b < batch; ++b) {
         for (int64_t i = 0; i < rows; ++i) {
             const int64_t s = s0 + i;
-            const float* qrow = q + ((b * seq_len + s) * heads) * head_dim;
-            const float* wrow = w + (b * seq_len + s) * heads;
-            for (int64_t j = 0; j < cols; ++j) {
-                const float* krow = kc + (b * key_blocks + t0 + j) * head_dim;
-                out[(b * rows + i) * cols + j] = score_pair(qrow, krow, wrow, heads, head_dim, fp16);
-            }
+            score_span(q + ((b * seq_len + s) * heads) * head_dim, w + (b * seq_len + s) * heads,
+                       kc + (b * key_blocks + t0) * head_dim, cols, heads, head_dim, fp16,
+                       out + (b * rows + i) * cols);
         }
     }
 }
@@ -246,8 +275,7 @@ void orc_run_materialize(const float* q, const float* kc, const float* w, int64_
             const int64_t legal = orc_t_legal(t, ratio);
             const float* qrow = q + ((b * seq_len + t) * heads) * head_dim;
             const float* wrow = w + (b * seq_len + t) * heads;
-            for (int64_t j = 0; j < legal; ++j)
-                row[j] = score_pair(qrow, kc + (b * T + j) * head_dim, wrow, heads, head_dim, fp16);
+            score_span(qrow, wrow, kc + b * T * head_dim, legal, heads, head_dim, fp16, row);
             orc_oracle_topk(row, legal, top_k, out_val + (b * seq_len + t) * top_k,
                             out_idx + (b * seq_len + t) * top_k);
         }
@@ -380,7 +408,7 @@ int64_t orc_row_topk(const float* q_row, const float* w_row, const float* kc, in
     if (legal > key_blocks) legal = key_blocks;
     if (legal <= 0) return 0;
     float* row = (float*)malloc((size_t)legal * sizeof(float));
-    for (int64_t j = 0; j < legal; ++j) row[j] = score_pair(q_row, kc + j * head_dim, w_row, heads, head_dim, 0);
+    score_span(q_row, w_row, kc, legal, heads, head_dim, 0, row);
     const int64_t n = orc_oracle_topk(row, legal, k, out_v, out_i);
     free(row);
     return n;

@@ -18,6 +18,7 @@ OK, INVALID_ARGUMENT, RUNTIME_ERROR, OVERFLOW_ERROR, LOGIC_ERROR, CUDA_ERROR = r
 KERNEL_AUTO, KERNEL_EXACT = 0, 1
 DTYPE_BF16, DTYPE_F32 = 0, 1
 MODE_FP32, MODE_FP16_EMULATED = 0, 1
+KIND_SCORE, KIND_SELECT, KIND_MERGE, KIND_FINALIZE, KIND_PREP = range(5)
 
 
 class CsaidxError(RuntimeError):
@@ -81,6 +82,9 @@ CUDA_SYMBOLS = {
     "csaidx_engine_check": (c_int, [c_void_p]),
     "csaidx_engine_mem_stats": (c_int, [c_void_p, POINTER(c_uint64), POINTER(c_uint64)]),
     "csaidx_engine_reset_peak": (c_int, [c_void_p]),
+    "csaidx_engine_set_profiling": (c_int, [c_void_p, c_int]),
+    "csaidx_engine_kernel_stats": (c_int, [c_void_p, c_int, POINTER(c_int64), POINTER(ctypes.c_double)]),
+    "csaidx_engine_reset_stats": (c_int, [c_void_p]),
     "csaidx_cuda_alloc": (c_int, [c_void_p, c_size_t, POINTER(c_void_p)]),
     "csaidx_cuda_free": (c_int, [c_void_p, c_void_p]),
     "csaidx_cuda_copy": (c_int, [c_void_p, c_void_p, c_void_p, c_size_t]),

@@ -80,12 +80,15 @@ _F = POINTER(ctypes.c_float)
 HOST_SYMBOLS = {
     "csaidx_host_last_error": (c_char_p, []),
     "csaidx_host_default_config": (None, [POINTER(RunConfig)]),
+    "csaidx_host_engine": (c_int, [c_int, POINTER(c_void_p)]),
     "csaidx_host_run_chunked": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(Dims), POINTER(RunConfig), c_void_p,
                                         c_void_p, POINTER(RunStatsC)]),
     "csaidx_host_run_materialize": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(Dims), POINTER(RunConfig),
                                             c_void_p, c_void_p, POINTER(RunStatsC)]),
     "csaidx_host_dispatch": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(Dims), POINTER(RunConfig), c_void_p,
                                      c_void_p, POINTER(RunStatsC)]),
+    "csaidx_host_run_chunked_rows": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(Dims), POINTER(RunConfig),
+                                             c_void_p, c_int64, c_void_p, c_void_p, c_int64, POINTER(RunStatsC)]),
     "csaidx_device_run_chunked": (c_int, [c_void_p, c_void_p, c_int, c_void_p, POINTER(Dims), POINTER(RunConfig),
                                           c_void_p, c_int64, c_void_p, c_void_p, c_int64, POINTER(RunStatsC)]),
     "csaidx_host_problem_dims": (c_int, [c_int64] * 6 + [POINTER(Dims)]),
@@ -269,6 +272,30 @@ def dispatch(inputs: IndexerInputs, dims: ProblemDims, config: DriverConfig | No
     return _host_call(host_lib().csaidx_host_dispatch, inputs, dims, config or DriverConfig())
 
 
+def chunk_rows(dims: ProblemDims, config: DriverConfig, chunk_starts) -> int:
+    cs = min(config.tile.query_tile, dims.seq_len)
+    return int(sum(min(cs, dims.seq_len - int(s)) for s in chunk_starts))
+
+
+def run_chunked_rows(q, kc, w, dims: ProblemDims, config: DriverConfig, chunk_starts, out_idx, out_val):
+    """Host-buffer run over a chunk subset (csaidx_host_run_chunked_rows).
+
+    q/kc/w/out_* are contiguous host arrays (numpy, or pinned torch CPU
+    tensors); only the chunk rows of q/w are copied to the device."""
+    starts = np.ascontiguousarray(chunk_starts, dtype=np.int64)
+    st = RunStatsC()
+    cd, cc = dims.c(), config.c()
+
+    def ptr(a):
+        return c_void_p(a.data_ptr()) if hasattr(a, "data_ptr") else _ptr(a)
+
+    _check(host_lib().csaidx_host_run_chunked_rows(ptr(q), ptr(kc), ptr(w), ctypes.byref(cd), ctypes.byref(cc),
+                                                   _ptr(starts), starts.size, ptr(out_idx), ptr(out_val),
+                                                   out_idx.shape[1], ctypes.byref(st)))
+    return RunStats(st.dispatch_count, st.tiles_skipped_masked, st.tiles_skipped_narrow, st.ledger_peak_bytes,
+                    st.device_peak_bytes, ExecutionPath.chunked)
+
+
 def run_chunked_device(q, kc, w, dims: ProblemDims, config: DriverConfig, chunk_starts=None, out_idx=None,
                        out_val=None):
     """Device-resident Algorithm 2 (csaidx_device_run_chunked): torch CUDA tensors in, torch tensors out."""
@@ -295,6 +322,37 @@ def run_chunked_device(q, kc, w, dims: ProblemDims, config: DriverConfig, chunk_
     stats = RunStats(st.dispatch_count, st.tiles_skipped_masked, st.tiles_skipped_narrow, st.ledger_peak_bytes,
                      st.device_peak_bytes, ExecutionPath.chunked)
     return out_idx, out_val, stats
+
+
+def driver_engine(device: int = 0):
+    """Handle of the engine libcsaidx.so's driver uses on `device`."""
+    h = c_void_p()
+    _check(host_lib().csaidx_host_engine(device, ctypes.byref(h)))
+    return h
+
+
+class KernelStats:
+    """Launch counts / event-timed device ms per kernel class of an engine."""
+
+    def __init__(self, handle):
+        self.h = handle
+        self.lib = _capi.cuda_lib()
+
+    def profiling(self, on: bool):
+        _check_cuda(self.lib.csaidx_engine_set_profiling(self.h, int(on)))
+
+    def reset(self):
+        _check_cuda(self.lib.csaidx_engine_reset_stats(self.h))
+
+    def get(self, kind: int):
+        n, ms = c_int64(), ctypes.c_double()
+        _check_cuda(self.lib.csaidx_engine_kernel_stats(self.h, kind, ctypes.byref(n), ctypes.byref(ms)))
+        return n.value, ms.value
+
+    def mem(self):
+        live, peak = c_uint64(), c_uint64()
+        _check_cuda(self.lib.csaidx_engine_mem_stats(self.h, ctypes.byref(live), ctypes.byref(peak)))
+        return live.value, peak.value
 
 
 # ------------------------------------------------------- host arithmetic

@@ -10,6 +10,7 @@
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <vector>
 
 #include "csaidx_cuda.h"
 #include "kernels/kernels.h"
@@ -71,6 +72,16 @@ struct csaidx_engine {
     std::unordered_map<void*, size_t> sizes;
     uint64_t live = 0;
     uint64_t peak = 0;
+    // per-kernel-class accounting (CSAIDX_KIND_*)
+    int64_t launches[CSAIDX_NUM_KINDS] = {};
+    double total_ms[CSAIDX_NUM_KINDS] = {};
+    bool profiling = false;
+    struct Pending {
+        int kind;
+        cudaEvent_t start, stop;
+    };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> event_pool;
 };
 
 namespace {
@@ -80,6 +91,39 @@ int set_device(csaidx_engine* e) {
     CSAIDX_CUDA_TRY(cudaSetDevice(e->device), "cudaSetDevice");
     return CSAIDX_OK;
 }
+
+cudaEvent_t take_event(csaidx_engine* e) {
+    if (!e->event_pool.empty()) {
+        cudaEvent_t ev = e->event_pool.back();
+        e->event_pool.pop_back();
+        return ev;
+    }
+    cudaEvent_t ev = nullptr;
+    cudaEventCreate(&ev);
+    return ev;
+}
+
+// Brackets one kernel launch: counts it and, when profiling, records CUDA
+// events on the launching stream (resolved lazily by kernel_stats).
+struct LaunchScope {
+    csaidx_engine* e;
+    int kind;
+    cudaEvent_t start = nullptr;
+    LaunchScope(csaidx_engine* e_, int kind_) : e(e_), kind(kind_) {
+        ++e->launches[kind];
+        if (e->profiling) {
+            start = take_event(e);
+            cudaEventRecord(start, e->stream);
+        }
+    }
+    ~LaunchScope() {
+        if (start != nullptr) {
+            cudaEvent_t stop = take_event(e);
+            cudaEventRecord(stop, e->stream);
+            e->pending.push_back({kind, start, stop});
+        }
+    }
+};
 
 // 2D bf16 row-major [rows, 128] tensor map with a (64 x box_rows) SW128 box.
 int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
@@ -159,6 +203,11 @@ int csaidx_engine_destroy(csaidx_engine* e) {
     cudaSetDevice(e->device);
     if (e->stream) cudaStreamSynchronize(e->stream);
     for (auto& kv : e->sizes) cudaFree(kv.first);
+    for (const auto& pd : e->pending) {
+        cudaEventDestroy(pd.start);
+        cudaEventDestroy(pd.stop);
+    }
+    for (cudaEvent_t ev : e->event_pool) cudaEventDestroy(ev);
     if (e->flags) cudaFree(e->flags);
     if (e->own_stream) cudaStreamDestroy(e->own_stream);
     delete e;
@@ -215,6 +264,44 @@ int csaidx_engine_mem_stats(csaidx_engine* e, uint64_t* live, uint64_t* peak) {
     return CSAIDX_OK;
 }
 
+int csaidx_engine_set_profiling(csaidx_engine* e, int enabled) {
+    if (e == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null engine");
+    e->profiling = enabled != 0;
+    return CSAIDX_OK;
+}
+
+int csaidx_engine_kernel_stats(csaidx_engine* e, int kind, int64_t* launches, double* total_ms) {
+    if (int rc = set_device(e)) return rc;
+    if (kind < 0 || kind >= CSAIDX_NUM_KINDS) return fail(CSAIDX_INVALID_ARGUMENT, "unknown kernel kind");
+    for (const auto& pd : e->pending) {
+        float ms = 0.0f;
+        CSAIDX_CUDA_TRY(cudaEventSynchronize(pd.stop), "cudaEventSynchronize");
+        CSAIDX_CUDA_TRY(cudaEventElapsedTime(&ms, pd.start, pd.stop), "cudaEventElapsedTime");
+        e->total_ms[pd.kind] += ms;
+        e->event_pool.push_back(pd.start);
+        e->event_pool.push_back(pd.stop);
+    }
+    e->pending.clear();
+    if (launches) *launches = e->launches[kind];
+    if (total_ms) *total_ms = e->total_ms[kind];
+    return CSAIDX_OK;
+}
+
+int csaidx_engine_reset_stats(csaidx_engine* e) {
+    if (int rc = set_device(e)) return rc;
+    for (const auto& pd : e->pending) {
+        cudaEventSynchronize(pd.stop);
+        e->event_pool.push_back(pd.start);
+        e->event_pool.push_back(pd.stop);
+    }
+    e->pending.clear();
+    for (int k = 0; k < CSAIDX_NUM_KINDS; ++k) {
+        e->launches[k] = 0;
+        e->total_ms[k] = 0.0;
+    }
+    return CSAIDX_OK;
+}
+
 int csaidx_engine_reset_peak(csaidx_engine* e) {
     if (e == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null engine");
     std::lock_guard<std::mutex> lock(e->mu);
@@ -268,6 +355,7 @@ int csaidx_cuda_to_bf16(csaidx_engine* e, const float* src, uint16_t* dst, int64
     if (n < 0) return fail(CSAIDX_INVALID_ARGUMENT, "to_bf16: negative length");
     ConvertParams p{src, reinterpret_cast<__nv_bfloat16*>(dst), n, strict ? e->flags + kInexact : nullptr,
                     e->flags + kNonfiniteInput};
+    LaunchScope ls(e, CSAIDX_KIND_PREP);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_convert_bf16(p, e->stream), "convert_bf16");
     return CSAIDX_OK;
 }
@@ -314,6 +402,7 @@ int csaidx_cuda_score(csaidx_engine* e, const void* q, const void* kc, int dtype
         p.cols = cols;
         p.batch = static_cast<int>(d->batch);
         p.apply_mask = apply_mask;
+        LaunchScope ls(e, CSAIDX_KIND_SCORE);
         CSAIDX_CUDA_TRY(csaidx_kern::launch_score_tc(qmap, kmap, p, e->num_sms, e->stream), "score_tc");
     } else {
         ScoreExactParams p{};
@@ -336,6 +425,7 @@ int csaidx_cuda_score(csaidx_engine* e, const void* q, const void* kc, int dtype
         p.batch = static_cast<int>(d->batch);
         p.apply_mask = apply_mask;
         p.fp16 = mode == CSAIDX_MODE_FP16_EMULATED;
+        LaunchScope ls(e, CSAIDX_KIND_SCORE);
         CSAIDX_CUDA_TRY(csaidx_kern::launch_score_exact(p, e->stream), "score_exact");
     }
     return CSAIDX_OK;
@@ -346,6 +436,7 @@ int csaidx_cuda_bool_mask(csaidx_engine* e, uint8_t* keep, int64_t s0, int64_t t
     if (int rc = set_device(e)) return rc;
     if (rows < 1 || cols < 1 || s0 < 0 || t0 < 0 || ratio < 1)
         return fail(CSAIDX_INVALID_ARGUMENT, "build_mask_tile: bad tile extents");
+    LaunchScope ls(e, CSAIDX_KIND_PREP);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_bool_mask(keep, rows, cols, s0, t0, ratio, e->stream), "bool_mask");
     return CSAIDX_OK;
 }
@@ -353,6 +444,7 @@ int csaidx_cuda_bool_mask(csaidx_engine* e, uint8_t* keep, int64_t s0, int64_t t
 int csaidx_cuda_apply_bool_mask(csaidx_engine* e, float* scores, int64_t ld, const uint8_t* keep, int64_t batch,
                                 int64_t rows, int64_t cols) {
     if (int rc = set_device(e)) return rc;
+    LaunchScope ls(e, CSAIDX_KIND_PREP);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_apply_bool_mask(scores, ld, keep, batch, rows, cols, e->stream),
                     "apply_bool_mask");
     return CSAIDX_OK;
@@ -388,6 +480,7 @@ int csaidx_cuda_select(csaidx_engine* e, const float* scores, int64_t batch, int
     p.out_val = cand_val;
     p.out_idx = cand_idx;
     p.out_ld = cand_ld;
+    LaunchScope ls(e, CSAIDX_KIND_SELECT);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_select(p, e->stream), "select");
     return CSAIDX_OK;
 }
@@ -411,12 +504,14 @@ int csaidx_cuda_merge(csaidx_engine* e, float* run_val, int32_t* run_idx, int64_
     p.overwrite = overwrite;
     p.check_overlap = check_overlap;
     p.overlap_flag = e->flags + kOverlap;
+    LaunchScope ls(e, CSAIDX_KIND_MERGE);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_merge(p, e->stream), "merge");
     return CSAIDX_OK;
 }
 
 int csaidx_cuda_fill_sentinel(csaidx_engine* e, float* val, int32_t* idx, int64_t n) {
     if (int rc = set_device(e)) return rc;
+    LaunchScope ls(e, CSAIDX_KIND_PREP);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_fill_sentinel(val, idx, n, e->stream), "fill_sentinel");
     return CSAIDX_OK;
 }
@@ -441,6 +536,7 @@ int csaidx_cuda_finalize(csaidx_engine* e, const float* run_val, const int32_t* 
     p.out_row0 = out_row0;
     p.trail_flag = e->flags + kTrail;
     p.keff_flag = e->flags + kKeff;
+    LaunchScope ls(e, CSAIDX_KIND_FINALIZE);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_finalize(p, e->stream), "finalize");
     return CSAIDX_OK;
 }
@@ -467,6 +563,7 @@ int csaidx_cuda_chunk_step(csaidx_engine* e, const void* q, const void* kc, int 
 int csaidx_cuda_gen_normal_bf16(csaidx_engine* e, uint16_t* dst, int64_t n, double stddev, uint64_t seed,
                                 uint64_t stream_id, int64_t offset) {
     if (int rc = set_device(e)) return rc;
+    LaunchScope ls(e, CSAIDX_KIND_PREP);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_gen_normal_bf16(reinterpret_cast<__nv_bfloat16*>(dst), n, stddev, seed,
                                                         stream_id, offset, e->stream),
                     "gen_bf16");
@@ -476,6 +573,7 @@ int csaidx_cuda_gen_normal_bf16(csaidx_engine* e, uint16_t* dst, int64_t n, doub
 int csaidx_cuda_gen_normal_f32(csaidx_engine* e, float* dst, int64_t n, double stddev, uint64_t seed,
                                uint64_t stream_id, int64_t offset) {
     if (int rc = set_device(e)) return rc;
+    LaunchScope ls(e, CSAIDX_KIND_PREP);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_gen_normal_f32(dst, n, stddev, seed, stream_id, offset, e->stream), "gen_f32");
     return CSAIDX_OK;
 }

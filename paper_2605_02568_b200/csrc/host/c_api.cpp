@@ -103,6 +103,16 @@ void csaidx_host_default_config(csaidx_run_config* cfg) {
                              CSAIDX_SCORE_AUTO, 1, 0, 1, d.auto_threshold_bytes, 0, 0, nullptr};
 }
 
+int csaidx_host_engine(int device, csaidx_engine** out) {
+    return guarded([&] {
+        if (out == nullptr) throw std::invalid_argument("null out");
+        csaidx::gpu::Options o = csaidx::gpu::options();
+        o.device = device;
+        csaidx::gpu::set_options(o);
+        *out = csaidx::detail::engine();
+    });
+}
+
 int csaidx_host_run_chunked(const float* q, const float* kc, const float* w, const csaidx_dims* dims,
                             const csaidx_run_config* cfg, int64_t* out_idx, float* out_val, csaidx_run_stats* stats) {
     return guarded([&] {
@@ -113,6 +123,23 @@ int csaidx_host_run_chunked(const float* q, const float* kc, const float* w, con
         csaidx::RunStats rs;
         const csaidx::TopKResult r = csaidx::detail::run_chunked_view({q, kc, w}, d, c, ledger, &rs);
         copy_out(r, out_idx, out_val);
+        fill_stats(stats, rs, ledger, 1);
+    });
+}
+
+int csaidx_host_run_chunked_rows(const float* q, const float* kc, const float* w, const csaidx_dims* dims,
+                                 const csaidx_run_config* cfg, const int64_t* chunk_starts, int64_t n_chunks,
+                                 int64_t* out_idx, float* out_val, int64_t out_rows, csaidx_run_stats* stats) {
+    return guarded([&] {
+        const csaidx::ProblemDims d = from_c(dims);
+        const csaidx::DriverConfig c = from_c(cfg);
+        std::vector<int64_t> starts;
+        if (chunk_starts != nullptr && n_chunks > 0) starts.assign(chunk_starts, chunk_starts + n_chunks);
+        csaidx::gpu::reset_device_peak();
+        csaidx::MemoryLedger ledger;
+        csaidx::RunStats rs;
+        csaidx::detail::run_chunked_rows_view({q, kc, w}, d, c, starts.empty() ? nullptr : &starts, out_idx, out_val,
+                                              out_rows, ledger, &rs);
         fill_stats(stats, rs, ledger, 1);
     });
 }

@@ -140,20 +140,21 @@ int operand_dtype(const ProblemDims& dims, int mode, int kernel) {
 namespace {
 
 // fp32 host -> device, rounded to bf16 on device through a bounded slab.
-void stage_bf16(csaidx_engine* e, DeviceBuffer& dst, const float* host, int64_t n, bool strict) {
+void stage_bf16(csaidx_engine* e, DeviceBuffer& dst, int64_t dst_off, const float* host, int64_t n, bool strict) {
     constexpr int64_t kSlab = int64_t{1} << 26;  // 64 Mi elements (256 MiB fp32)
+    if (n <= 0) return;
     DeviceBuffer slab(e, static_cast<size_t>(std::min(n, kSlab)) * sizeof(float));
     for (int64_t off = 0; off < n; off += kSlab) {
         const int64_t len = std::min(kSlab, n - off);
         check(csaidx_cuda_copy(e, slab.as<void>(), host + off, static_cast<size_t>(len) * sizeof(float)));
-        check(csaidx_cuda_to_bf16(e, slab.as<float>(), dst.as<uint16_t>() + off, len, strict ? 1 : 0));
+        check(csaidx_cuda_to_bf16(e, slab.as<float>(), dst.as<uint16_t>() + dst_off + off, len, strict ? 1 : 0));
     }
 }
 
 }  // namespace
 
 StagedOperands::StagedOperands(csaidx_engine* e, const HostView& host, const ProblemDims& dims, int dtype,
-                               bool strict)
+                               bool strict, const std::vector<std::pair<int64_t, int64_t>>* row_ranges)
     : dtype_(dtype) {
     const int64_t nq = dims.q_elems(), nk = dims.kc_elems(), nw = dims.w_elems();
     const size_t esz = dtype == CSAIDX_DTYPE_BF16 ? 2 : 4;
@@ -161,13 +162,26 @@ StagedOperands::StagedOperands(csaidx_engine* e, const HostView& host, const Pro
     kc_ = DeviceBuffer(e, static_cast<size_t>(nk) * esz);
     w_ = DeviceBuffer(e, static_cast<size_t>(nw) * sizeof(float));
     if (dtype == CSAIDX_DTYPE_BF16) {
-        stage_bf16(e, kc_, host.kc, nk, strict);
-        stage_bf16(e, q_, host.q, nq, strict);
+        stage_bf16(e, kc_, 0, host.kc, nk, strict);
     } else {
-        q_.upload(host.q, static_cast<size_t>(nq) * sizeof(float));
         kc_.upload(host.kc, static_cast<size_t>(nk) * sizeof(float));
     }
-    w_.upload(host.w, static_cast<size_t>(nw) * sizeof(float));
+    std::vector<std::pair<int64_t, int64_t>> all{{0, dims.seq_len}};
+    const auto& ranges = row_ranges != nullptr ? *row_ranges : all;
+    const int64_t qrow = dims.heads * dims.head_dim;
+    for (int64_t b = 0; b < dims.batch; ++b) {
+        for (const auto& [s0, rows] : ranges) {
+            const int64_t qoff = (b * dims.seq_len + s0) * qrow, woff = (b * dims.seq_len + s0) * dims.heads;
+            if (dtype == CSAIDX_DTYPE_BF16) {
+                stage_bf16(e, q_, qoff, host.q + qoff, rows * qrow, strict);
+            } else {
+                check(csaidx_cuda_copy(e, q_.as<float>() + qoff, host.q + qoff,
+                                       static_cast<size_t>(rows * qrow) * sizeof(float)));
+            }
+            check(csaidx_cuda_copy(e, w_.as<float>() + woff, host.w + woff,
+                                   static_cast<size_t>(rows * dims.heads) * sizeof(float)));
+        }
+    }
 }
 
 }  // namespace detail

@@ -70,7 +70,10 @@ struct DeviceOps {
 // slab and rounds on device; fp32 copies straight.
 class StagedOperands {
 public:
-    StagedOperands(csaidx_engine* e, const HostView& host, const ProblemDims& dims, int dtype, bool strict);
+    // row_ranges (s0, rows): only these query rows of q / w are staged (all
+    // when null); the device arrays keep the full [B, S, ...] layout.
+    StagedOperands(csaidx_engine* e, const HostView& host, const ProblemDims& dims, int dtype, bool strict,
+                   const std::vector<std::pair<int64_t, int64_t>>* row_ranges = nullptr);
     [[nodiscard]] DeviceOps ops() const { return {q_.as<void>(), kc_.as<void>(), w_.as<float>(), dtype_}; }
 
 private:
@@ -102,6 +105,11 @@ void run_materialize_device(csaidx_engine* e, const DeviceOps& ops, const Proble
 
 TopKResult run_chunked_view(const HostView& in, const ProblemDims& dims, const DriverConfig& config,
                             MemoryLedger& ledger, RunStats* stats);
+// Host-buffer Algorithm 2 over a chunk subset (all when starts is null);
+// results into host [B, out_rows, k] with the plan's row packing.
+void run_chunked_rows_view(const HostView& in, const ProblemDims& dims, const DriverConfig& config,
+                           const std::vector<int64_t>* starts, int64_t* host_idx, float* host_val, int64_t out_rows,
+                           MemoryLedger& ledger, RunStats* stats);
 TopKResult run_materialize_view(const HostView& in, const ProblemDims& dims, AccumulationMode mode,
                                 MemoryLedger& ledger, ScoreKernel kernel);
 

@@ -166,20 +166,38 @@ void download_result(csaidx_engine* e, const DeviceBuffer& idx, const DeviceBuff
 
 }  // namespace
 
-TopKResult run_chunked_view(const HostView& in, const ProblemDims& dims, const DriverConfig& config,
-                            MemoryLedger& ledger, RunStats* stats_out) {
-    const ChunkPlan plan = plan_chunks(dims, config.tile, nullptr);
-    TopKResult out = TopKResult::sized(dims);
+void run_chunked_rows_view(const HostView& in, const ProblemDims& dims, const DriverConfig& config,
+                           const std::vector<int64_t>* starts, int64_t* host_idx, float* host_val, int64_t out_rows,
+                           MemoryLedger& ledger, RunStats* stats_out) {
+    const ChunkPlan plan = plan_chunks(dims, config.tile, starts);
+    int64_t need = 0;
+    std::vector<std::pair<int64_t, int64_t>> ranges;
+    for (size_t c = 0; c < plan.starts.size(); ++c) {
+        const int64_t rows = std::min(plan.cs, dims.seq_len - plan.starts[c]);
+        ranges.emplace_back(plan.starts[c], rows);
+        need = plan.out_row0[c] + rows;
+    }
+    if (out_rows < need) throw std::invalid_argument("run_chunked: out_rows too small for the chunk list");
     const int kcode = kernel_code(config.kernel);
     std::lock_guard<std::mutex> lock(engine_mutex());
     csaidx_engine* e = engine();
     const StagedOperands ops(e, in, dims, operand_dtype(dims, mode_code(config.mode), kcode),
-                             gpu::options().strict_bf16);
-    DeviceBuffer idx(e, out.indices.size() * sizeof(int64_t)), val(e, out.values.size() * sizeof(float));
+                             gpu::options().strict_bf16, starts != nullptr ? &ranges : nullptr);
+    const size_t n = static_cast<size_t>(dims.batch * out_rows * dims.top_k);
+    DeviceBuffer idx(e, n * sizeof(int64_t)), val(e, n * sizeof(float));
     RunStats stats;
-    run_plan(e, ops.ops(), dims, config, plan, idx.as<int64_t>(), val.as<float>(), dims.seq_len, ledger, stats);
-    download_result(e, idx, val, out);
+    run_plan(e, ops.ops(), dims, config, plan, idx.as<int64_t>(), val.as<float>(), out_rows, ledger, stats);
+    idx.download(host_idx, n * sizeof(int64_t));
+    val.download(host_val, n * sizeof(float));
+    check(csaidx_engine_check(e));
     if (stats_out != nullptr) *stats_out = stats;
+}
+
+TopKResult run_chunked_view(const HostView& in, const ProblemDims& dims, const DriverConfig& config,
+                            MemoryLedger& ledger, RunStats* stats_out) {
+    TopKResult out = TopKResult::sized(dims);
+    run_chunked_rows_view(in, dims, config, nullptr, out.indices.data(), out.values.data(), dims.seq_len, ledger,
+                          stats_out);
     return out;
 }
 

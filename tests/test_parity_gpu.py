@@ -1,0 +1,170 @@
+"""Parity of the B200 path, called through the reference-facing API
+(libcsaidx.so's C entry points = csaidx::run_chunked / run_materialize /
+dispatch), against the pinned oracle and the reference's own golden fixtures.
+
+* Shapes off the tensor-core path (tiny H_I / d_h, fp16 mode, scalar kernel)
+  run the exact-order kernel: bit-exact indices, values and RunStats.
+* The V4 indexer shape runs tcgen05: the north-star tolerance rule
+  (tests/parity.py) at C1 (S=4096, k=512) against the full oracle.
+* chunked == materialize bit-for-bit on the GPU under any tiling.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle.oracle import Oracle
+from paper_2605_02568_b200 import api
+from paper_2605_02568_b200._capi import InvalidArgument, LogicError, ScoreRuntimeError
+
+from .parity import check_rows
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden.npz")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return Oracle()
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return np.load(GOLDEN)
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def inputs_for(orc, B, S, m, H, D, k, seed, bf16=False):
+    q, kc, w = orc.generate_inputs(B, S, m, H, D, seed, bf16=bf16)
+    dims = api.ProblemDims.create(B, S, m, H, D, k)
+    return api.IndexerInputs.validated(q, kc, w, dims), dims, (q, kc, w)
+
+
+def test_golden_driver_cases_bit_exact(orc, gold):
+    for n, (B, S, m, H, D, k, seed, cs, ct, fp16, abl, ee, bm) in enumerate(gold["drv_cases"]):
+        inputs, dims, _ = inputs_for(orc, int(B), int(S), int(m), int(H), int(D), int(k), int(seed))
+        cfg = api.DriverConfig(tile=api.TileConfig(int(cs), int(ct)), mode=api.AccumulationMode(int(fp16)),
+                               ablation=api.Ablation(int(abl)), causal_early_exit=bool(ee), bool_mask_tile=bool(bm))
+        res, stats = api.run_chunked(inputs, dims, cfg)
+        assert np.array_equal(res.indices, gold[f"drv{n}_idx"]), n
+        assert np.array_equal(bits(res.values), bits(gold[f"drv{n}_val"])), n
+        assert [stats.dispatch_count, stats.tiles_skipped_masked, stats.tiles_skipped_narrow] == \
+            list(gold[f"drv{n}_stats"]), n
+        assert stats.ledger_peak_bytes == int(gold[f"drv{n}_peak"][0]), n
+        mres, _ = api.run_materialize(inputs, dims, mode=api.AccumulationMode(int(fp16)))
+        assert np.array_equal(mres.indices, gold[f"drv{n}_midx"]), n
+        assert np.array_equal(bits(mres.values), bits(gold[f"drv{n}_mval"])), n
+
+
+def test_scalar_kernel_is_bit_exact_at_v4_shape(orc, gold):
+    # ScoreKernel::scalar keeps fp32 operands and the reference op order.
+    inputs, dims, _ = inputs_for(orc, 1, 512, 4, 64, 128, 64, 1, bf16=True)
+    res, _ = api.run_materialize(inputs, dims, kernel=api.ScoreKernel.scalar)
+    assert np.array_equal(res.indices.astype(np.int16), gold["v4_idx"])
+    assert np.array_equal(bits(res.values), bits(gold["v4_val"]))
+
+
+def test_tensor_core_path_v4_small_matches_reference_rule(orc, gold):
+    inputs, dims, (q, kc, w) = inputs_for(orc, 1, 512, 4, 64, 128, 64, 1, bf16=True)
+    res, st = api.run_chunked(inputs, dims, api.DriverConfig(tile=api.TileConfig(128, 64)))
+    full = orc.score_tile(q, kc, w, 0, 0, 512, 128)[0]
+    legal = (np.arange(512) + 1) // 4
+    rep = check_rows(res.indices[0], res.values[0], full, legal, 64)
+    assert rep["rows"] == 509
+
+
+@pytest.fixture(scope="module")
+def c1(orc):
+    """C1: B=1, S=4096, H_I=64, d_h=128, m=4, k=512, bf16-representable inputs."""
+    inputs, dims, (q, kc, w) = inputs_for(orc, 1, 4096, 4, 64, 128, 512, 1, bf16=True)
+    full = orc.score_tile(q, kc, w, 0, 0, 4096, 1024)[0]  # oracle scores, reference op order
+    return inputs, dims, full
+
+
+@pytest.mark.parametrize("cs,ct", [(256, 256), (2048, 8192), (4096, 1024), (100, 300)])
+def test_c1_parity_against_oracle(c1, cs, ct):
+    inputs, dims, full = c1
+    res, st = api.run_chunked(inputs, dims, api.DriverConfig(tile=api.TileConfig(cs, ct)))
+    legal = (np.arange(4096) + 1) // 4
+    rep = check_rows(res.indices[0], res.values[0], full, legal, 512)
+    assert rep["rows"] == 4093  # rows 0..2 have no legal block
+    assert st.dispatch_count == sum(
+        1 for s0 in range(0, 4096, cs) for t0 in range(0, 1024, min(ct, 1024))
+        if t0 < (min(s0 + cs, 4096)) // 4)
+
+
+def test_c1_chunked_equals_materialize_bitwise(c1):
+    inputs, dims, _ = c1
+    ref, st = api.run_materialize(inputs, dims)
+    for cs, ct in [(256, 256), (4096, 1024), (333, 77)]:
+        got, _ = api.run_chunked(inputs, dims, api.DriverConfig(tile=api.TileConfig(cs, ct)))
+        assert np.array_equal(got.indices, ref.indices)
+        assert np.array_equal(bits(got.values), bits(ref.values))
+    via, stats = api.dispatch(inputs, dims)
+    assert stats.path == api.ExecutionPath.materialize  # 4096*64*1024*4 = 2^30 <= threshold
+    assert np.array_equal(via.indices, ref.indices)
+
+
+def test_ablations_follow_reference_semantics(orc):
+    # acceptance.cpp:339-380 directions at a small V4-like shape
+    inputs, dims, (q, kc, w) = inputs_for(orc, 1, 2048, 4, 8, 64, 64, 1)
+    prod, _ = api.run_chunked(inputs, dims, api.DriverConfig(tile=api.TileConfig(256, 128)))
+    rc, oidx, _, _ = orc.run_chunked(q, kc, w, 4, 64, 256, 128, ablation=0)
+    assert rc == 0 and np.array_equal(prod.indices, oidx)
+    a2, st2 = api.run_chunked(inputs, dims, api.DriverConfig(tile=api.TileConfig(256, 32),
+                                                               ablation=api.Ablation.a2_skip_narrow))
+    assert st2.dispatch_count == 0 and np.all(a2.indices == -1)
+    a1, _ = api.run_chunked(inputs, dims, api.DriverConfig(tile=api.TileConfig(256, 128),
+                                                             ablation=api.Ablation.a1_no_merge))
+    rc, a1o, _, _ = orc.run_chunked(q, kc, w, 4, 64, 256, 128, ablation=1)
+    assert np.array_equal(a1.indices, a1o)
+    r = orc.recall(prod.indices, a1.indices)
+    assert 0.0 < r["mean"] < 1.0
+
+
+def test_fp16_mode_matches_reference_bits(orc):
+    inputs, dims, (q, kc, w) = inputs_for(orc, 1, 512, 4, 8, 64, 32, 5)
+    got, _ = api.run_chunked(inputs, dims, api.DriverConfig(tile=api.TileConfig(64, 32),
+                                                              mode=api.AccumulationMode.fp16_emulated))
+    idx, val = orc.run_materialize(q, kc, w, 4, 32, fp16=True)
+    assert np.array_equal(got.indices, idx)
+    assert np.array_equal(bits(got.values), bits(val))
+
+
+def test_error_behaviour_matches_reference():
+    d = api.ProblemDims.create(1, 1, 1, 1, 2, 1)
+    big = api.IndexerInputs.validated([3.0e38, 3.0e38], [3.0e38, 3.0e38], [1.0], d)
+    with pytest.raises(ScoreRuntimeError):  # score.cpp:96
+        api.run_chunked(big, d)
+    with pytest.raises(InvalidArgument):  # TileConfig::validate
+        api.run_chunked(big, d, api.DriverConfig(tile=api.TileConfig(0, 1)))
+    with pytest.raises(InvalidArgument):  # no AVX2 kernel in this build
+        api.run_chunked(big, d, api.DriverConfig(kernel=api.ScoreKernel.avx2))
+    ok = api.IndexerInputs.validated([1.0, 1.0], [1.0, 1.0], [0.5], d)
+    res, _ = api.run_chunked(ok, d)
+    # t=0, m=1: t_legal = 1 -> block 0 legal; score = 0.5 * relu(1*1 + 1*1) = 1
+    assert res.indices[0, 0, 0] == 0 and res.values[0, 0, 0] == 1.0
+    assert issubclass(LogicError, RuntimeError)
+
+
+def test_sentinel_contract_exhaustive(orc):
+    for m in (1, 2, 4):
+        for k in (1, 2, 1000):
+            S = 4 * m
+            inputs, dims, (q, kc, w) = inputs_for(orc, 1, S, m, 2, 3, k, m * 1000 + k)
+            for cs, ct in ((S, S // m), (1, 1), (3, 2)):
+                res, _ = api.run_chunked(inputs, dims, api.DriverConfig(tile=api.TileConfig(cs, ct)))
+                rc, idx, val, _ = orc.run_chunked(q, kc, w, m, k, cs, ct)
+                assert np.array_equal(res.indices, idx) and np.array_equal(bits(res.values), bits(val))
