@@ -187,8 +187,9 @@ int csaidx_engine_create(int device, csaidx_engine** out) {
     e->num_sms = prop.multiProcessorCount;
     CSAIDX_CUDA_TRY(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     e->stream = e->own_stream;
-    CSAIDX_CUDA_TRY(cudaMalloc(&e->flags, kNumFlags * sizeof(int)), "cudaMalloc(flags)");
-    CSAIDX_CUDA_TRY(cudaMemset(e->flags, 0, kNumFlags * sizeof(int)), "cudaMemset(flags)");
+    // flags [0, kNumFlags) + the score kernel's self-resetting work counters
+    CSAIDX_CUDA_TRY(cudaMalloc(&e->flags, 2 * kNumFlags * sizeof(int)), "cudaMalloc(flags)");
+    CSAIDX_CUDA_TRY(cudaMemset(e->flags, 0, 2 * kNumFlags * sizeof(int)), "cudaMemset(flags)");
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
         uint64_t thresh = UINT64_MAX;
@@ -392,6 +393,7 @@ int csaidx_cuda_score(csaidx_engine* e, const void* q, const void* kc, int dtype
         p.w = w;
         p.out = out;
         p.nonfinite = e->flags + kNonfiniteScore;
+        p.sched = e->flags + kNumFlags;
         p.ld = ld;
         p.seq_len = d->seq_len;
         p.key_blocks = d->key_blocks;

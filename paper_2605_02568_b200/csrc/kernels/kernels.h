@@ -10,17 +10,23 @@
 #include <cstdint>
 
 // ------------------------------------------------------------------ score
+constexpr int kScoreMaxPieces = 256;
+
 struct ScoreTcParams {
     const float* w;     // [B, S, 64] fp32 mixing weights
     float* out;         // [B, rows, ld] fp32 scores
     int* nonfinite;     // set to 1 when an unmasked score is not finite
+    int* sched;         // [2] work counter + exit counter (zero between launches)
     int64_t ld;
     int64_t seq_len, key_blocks, ratio;
     int64_t s0, rows, t0, cols;
     int batch;
     int apply_mask;
-    // filled by the launcher
-    int nqb, npieces, nitems;
+    // filled by the launcher: dense piece-major work list. Piece p (key tiles
+    // [p*tpp, (p+1)*tpp)) is live for the query blocks qb >= nqb - count_p,
+    // count_p = (piece_start[p+1] - piece_start[p]) / batch.
+    int nqb, tpp, npieces, nitems;
+    int piece_start[kScoreMaxPieces + 1];
 };
 
 struct ScoreExactParams {

@@ -6,23 +6,27 @@
 // causal.cpp:30-41 (mask). Two kernels:
 //
 //  * score_tc_kernel — the production path for the V4 indexer shape
-//    (H_I = 64, d_h = 128). A warp-specialised tcgen05 GEMM with keys as M
-//    (128 TMEM lanes) and (query x head) as N (4 queries x 64 heads = 256
-//    columns). q and kc tiles are staged by TMA with 128-byte swizzle; the
-//    fp32 accumulator lives in TMEM (2 x 256 columns, double buffered); the
-//    epilogue warps read one key row per thread with tcgen05.ld and fold
-//    ReLU, the w-weighted head reduction and the causal mask before the only
-//    store, so the [B,S,H_I,T] per-head intermediate never exists.
+//    (H_I = 64, d_h = 128). A warp-specialised, persistent tcgen05 GEMM with
+//    keys as M (128 TMEM lanes) and (query x head) as N (4 queries x 64 heads
+//    = 256 columns). q and kc tiles are staged by TMA with 128-byte swizzle,
+//    w rows by a bulk copy; the fp32 accumulator lives in TMEM (2 x 256
+//    columns, double buffered); the epilogue warps read one key row per
+//    thread with tcgen05.ld and fold ReLU, the w-weighted head reduction and
+//    the causal mask before the only store, so the [B,S,H_I,T] per-head
+//    intermediate never exists. Work items (8 queries x <= tpp key tiles)
+//    form a dense piece-major list (causally dead tiles are never listed)
+//    handed out by an atomic counter, so every SM stays busy to the end.
 //
 //  * score_exact_kernel — any shape, CUDA cores, the reference's fp32 op
 //    order exactly (ascending-d dot as mul-then-add, ReLU as x<0?0:x,
 //    ascending-h acc = acc + w*r, optional binary16 rounding points). Given
-//    bf16-representable inputs it is bit-identical to the CPU reference.
+//    the same operands it is bit-identical to the CPU reference.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "kernels.h"
 #include "sm100_ptx.cuh"
@@ -39,8 +43,9 @@ constexpr int kUmmaN = kQPerGroup * kHeads;     // 256
 constexpr int kGroups = 2;                      // query groups per work item
 constexpr int kQPerItem = kQPerGroup * kGroups; // 8
 constexpr int kStages = 2;
-constexpr int kKTilesPerPiece = 32;             // 4096 keys per work item
+constexpr int kMinTilesPerPiece = 32;           // >= 4096 keys per work item
 constexpr int kKSteps = kDim / 16;              // UMMA_K = 16 for bf16
+constexpr int kItemSlots = 4;
 
 constexpr uint32_t kHalfRowBytes = 128;                          // 64 bf16
 constexpr uint32_t kQHalfBytes = kUmmaN * kHalfRowBytes;         // 32 KiB
@@ -48,8 +53,11 @@ constexpr uint32_t kQGroupBytes = 2 * kQHalfBytes;               // 64 KiB
 constexpr uint32_t kKHalfBytes = kBlockKeys * kHalfRowBytes;     // 16 KiB
 constexpr uint32_t kKStageBytes = 2 * kKHalfBytes;               // 32 KiB
 constexpr uint32_t kQBytes = kGroups * kQGroupBytes;             // 128 KiB
-constexpr uint32_t kSmemData = kQBytes + kStages * kKStageBytes; // 192 KiB
-constexpr uint32_t kSmemBytes = kSmemData + 256 + 1024;          // + barriers + align slack
+constexpr uint32_t kWRowBytes = kHeads * 4;                      // 256 B per query
+constexpr uint32_t kWBufBytes = kQPerItem * kWRowBytes;          // 2 KiB
+constexpr uint32_t kWOffset = kQBytes + kStages * kKStageBytes;  // 192 KiB
+constexpr uint32_t kBarOffset = kWOffset + 2 * kWBufBytes;       // + 4 KiB
+constexpr uint32_t kSmemBytes = kBarOffset + 512 + 1024;         // barriers, items, align slack
 
 constexpr int kNumThreads = 384;  // 4 control warps + 8 epilogue warps
 constexpr int kEpiWarps = 8;
@@ -57,50 +65,83 @@ constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kIdesc = idesc_bf16_f32(kBlockKeys, kUmmaN);
 
 struct Item {
-    int b, r0, nrows, kt_begin, kt_end;
+    int b, r0, nrows, kt_begin, kt_end;  // kt_begin < 0: no more work
 };
 
 __device__ __forceinline__ int64_t t_legal_dev(int64_t t, int64_t ratio) { return (t + 1) / ratio; }
 
-// Work item enumeration shared by every role. Items run heaviest-first: query
-// blocks from the end of the chunk (longest causal prefix) downwards, each
-// split into pieces of kKTilesPerPiece key tiles.
-__device__ __forceinline__ bool decode_item(const ScoreTcParams& p, int idx, Item& it) {
-    const int piece = idx % p.npieces;
-    const int rest = idx / p.npieces;
-    const int b = rest % p.batch;
-    const int qb = p.nqb - 1 - rest / p.batch;
-    it.b = b;
+// Dense piece-major decode: idx -> (piece p, batch b, query block qb).
+__device__ __forceinline__ void decode_item(const ScoreTcParams& p, int idx, Item& it) {
+    int lo = 0, hi = p.npieces;  // largest piece with piece_start <= idx
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (p.piece_start[mid] <= idx) lo = mid; else hi = mid;
+    }
+    const int local = idx - p.piece_start[lo];
+    it.b = local % p.batch;
+    const int qb = p.nqb - 1 - local / p.batch;
     it.r0 = qb * kQPerItem;
     it.nrows = min(kQPerItem, static_cast<int>(p.rows) - it.r0);
     int64_t kend = p.cols;
     if (p.apply_mask) {
-        const int64_t s_last = p.s0 + it.r0 + it.nrows - 1;
-        kend = t_legal_dev(s_last, p.ratio) - p.t0;
+        kend = t_legal_dev(p.s0 + it.r0 + it.nrows - 1, p.ratio) - p.t0;
         kend = kend < 0 ? 0 : (kend > p.cols ? p.cols : kend);
     }
     const int ntiles = static_cast<int>((kend + kBlockKeys - 1) / kBlockKeys);
-    it.kt_begin = piece * kKTilesPerPiece;
-    it.kt_end = min(it.kt_begin + kKTilesPerPiece, ntiles);
-    return it.kt_begin < it.kt_end;
+    it.kt_begin = lo * p.tpp;
+    it.kt_end = min(it.kt_begin + p.tpp, ntiles);
+}
+
+// Epilogue math for one query of one accumulator: 64 head partials of one
+// key row -> sum_h w_h * relu(x_h). 48 heads take ReLU on the ALU pipe
+// (FMNMX), 16 heads as x + |x| = 2 relu(x) on the FMA pipe (scaled back by
+// an exact 0.5 at the end), and all products go through packed FFMA2 into
+// five independent chains, balancing the two pipes.
+__device__ __forceinline__ float head_reduce(const float (&v)[64], const float* __restrict__ wq) {
+    float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, d0 = a0, d1 = a0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const float4 w4 = *reinterpret_cast<const float4*>(wq + 4 * j);
+        const float x0 = v[4 * j], x1 = v[4 * j + 1], x2 = v[4 * j + 2], x3 = v[4 * j + 3];
+        if ((j & 3) == 3) {
+            const float2 r01 = make_float2(x0 + fabsf(x0), x1 + fabsf(x1));
+            const float2 r23 = make_float2(x2 + fabsf(x2), x3 + fabsf(x3));
+            d0 = __ffma2_rn(r01, make_float2(w4.x, w4.y), d0);
+            d1 = __ffma2_rn(r23, make_float2(w4.z, w4.w), d1);
+        } else {
+            const float2 r01 = make_float2(fmaxf(x0, 0.f), fmaxf(x1, 0.f));
+            const float2 r23 = make_float2(fmaxf(x2, 0.f), fmaxf(x3, 0.f));
+            float2& acc = (j & 3) == 0 ? a0 : ((j & 3) == 1 ? a1 : a2);
+            acc = __ffma2_rn(r01, make_float2(w4.x, w4.y), acc);
+            acc = __ffma2_rn(r23, make_float2(w4.z, w4.w), acc);
+        }
+    }
+    const float main = ((a0.x + a0.y) + (a1.x + a1.y)) + (a2.x + a2.y);
+    const float dbl = (d0.x + d0.y) + (d1.x + d1.y);
+    return fmaf(0.5f, dbl, main);
 }
 
 __global__ void __launch_bounds__(kNumThreads, 1)
     score_tc_kernel(const __grid_constant__ CUtensorMap qmap,
-                    const __grid_constant__ CUtensorMap kmap, const ScoreTcParams p) {
+                    const __grid_constant__ CUtensorMap kmap, const __grid_constant__ ScoreTcParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint8_t* q_smem = smem;
     uint8_t* k_smem = smem + kQBytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemData);
+    float* w_smem = reinterpret_cast<float*>(smem + kWOffset);  // [2][8][64]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOffset);
     uint64_t* k_full = bars + 0;
     uint64_t* k_empty = bars + 2;
     uint64_t* q_full = bars + 4;
     uint64_t* q_empty = bars + 5;
     uint64_t* acc_full = bars + 6;
     uint64_t* acc_empty = bars + 8;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+    uint64_t* item_full = bars + 10;               // [kItemSlots]
+    uint64_t* item_empty = bars + 10 + kItemSlots;  // [kItemSlots]
+    uint64_t* w_full = bars + 10 + 2 * kItemSlots;  // [2] one per w buffer
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12 + 2 * kItemSlots);
+    Item* items = reinterpret_cast<Item*>(bars + 14 + 2 * kItemSlots);  // [kItemSlots]
 
     const int warp = threadIdx.x / 32;
 
@@ -117,6 +158,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             mbar_init(&acc_full[a], 1);
             mbar_init(&acc_empty[a], kEpiWarps);
         }
+        for (int s = 0; s < kItemSlots; ++s) {
+            mbar_init(&item_full[s], 1);
+            mbar_init(&item_empty[s], 1 + kEpiWarps);  // MMA thread + epilogue warps
+        }
+        mbar_init(&w_full[0], 1);
+        mbar_init(&w_full[1], 1);
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
@@ -126,21 +173,39 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ------------------------------------------------ TMA producer
+        // ------------------------------------------------ scheduler + TMA producer
         if (elect_one()) {
             const uint64_t keep = policy_evict_last();  // keys are re-read by every query block
             uint32_t kiter = 0, qiter = 0;
-            for (int idx = blockIdx.x; idx < p.nitems; idx += gridDim.x) {
+            for (uint32_t it_iter = 0;; ++it_iter) {
+                const uint32_t slot = it_iter % kItemSlots;
+                mbar_wait(&item_empty[slot], ((it_iter / kItemSlots) & 1) ^ 1);
+                const int idx = atomicAdd(p.sched, 1);
                 Item it;
-                if (!decode_item(p, idx, it)) continue;
+                if (idx >= p.nitems) {
+                    it.kt_begin = -1;
+                    items[slot] = it;
+                    mbar_arrive(&item_full[slot]);
+                    break;
+                }
+                decode_item(p, idx, it);
+                items[slot] = it;
+                mbar_arrive(&item_full[slot]);
+
                 mbar_wait(q_empty, (qiter & 1) ^ 1);
+                // q_empty(i-1) also proves the epilogue finished item i-2, the
+                // previous user of this w buffer (its MMAs needed acc_empty).
+                mbar_expect_tx(&w_full[qiter & 1], it.nrows * kWRowBytes);
+                bulk_copy_g2s(w_smem + (qiter & 1) * (kQPerItem * kHeads),
+                              p.w + (static_cast<int64_t>(it.b) * p.seq_len + p.s0 + it.r0) * kHeads,
+                              it.nrows * kWRowBytes, &w_full[qiter & 1]);
                 mbar_expect_tx(q_full, kQBytes);
-                const int32_t qrow =
-                    static_cast<int32_t>((static_cast<int64_t>(it.b) * p.seq_len + p.s0 + it.r0) * kHeads);
+                const int64_t qrow64 = static_cast<int64_t>(it.b) * p.seq_len + p.s0 + it.r0;
+                const int32_t qrow = static_cast<int32_t>(qrow64 * kHeads);
                 for (int g = 0; g < kGroups; ++g) {
                     for (int hf = 0; hf < 2; ++hf) {
-                        tma_load_2d(q_smem + g * kQGroupBytes + hf * kQHalfBytes, &qmap, q_full,
-                                    hf * 64, qrow + g * kUmmaN);
+                        tma_load_2d(q_smem + g * kQGroupBytes + hf * kQHalfBytes, &qmap, q_full, hf * 64,
+                                    qrow + g * kUmmaN);
                     }
                 }
                 ++qiter;
@@ -151,8 +216,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                     mbar_expect_tx(&k_full[s], kKStageBytes);
                     const int32_t krow = static_cast<int32_t>(krow0 + kt * kBlockKeys);
                     for (int hf = 0; hf < 2; ++hf) {
-                        tma_load_2d_hint(k_smem + s * kKStageBytes + hf * kKHalfBytes, &kmap,
-                                         &k_full[s], hf * 64, krow, keep);
+                        tma_load_2d_hint(k_smem + s * kKStageBytes + hf * kKHalfBytes, &kmap, &k_full[s], hf * 64,
+                                         krow, keep);
                     }
                     ++kiter;
                 }
@@ -164,9 +229,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             uint32_t kiter = 0, qiter = 0, aiter = 0;
             const uint32_t q_base = smem_u32(q_smem);
             const uint32_t k_base = smem_u32(k_smem);
-            for (int idx = blockIdx.x; idx < p.nitems; idx += gridDim.x) {
-                Item it;
-                if (!decode_item(p, idx, it)) continue;
+            for (uint32_t it_iter = 0;; ++it_iter) {
+                const uint32_t slot = it_iter % kItemSlots;
+                mbar_wait(&item_full[slot], (it_iter / kItemSlots) & 1);
+                const Item it = items[slot];
+                mbar_arrive(&item_empty[slot]);
+                if (it.kt_begin < 0) break;
                 mbar_wait(q_full, qiter & 1);
                 ++qiter;
                 tc_fence_after();
@@ -198,14 +266,21 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue
         const int quarter = warp & 3;           // TMEM lane quarter this warp may touch
-        const int qpair = (warp - 4) >> 2;      // which two queries of the group
+        const int qpair = (warp - 4) >> 2;      // which two queries of each group
         const uint32_t lane = lane_id();
         const uint32_t row_taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
-        uint32_t aiter = 0;
+        uint32_t aiter = 0, qiter = 0;
         const float neg_inf = -__int_as_float(0x7f800000);
-        for (int idx = blockIdx.x; idx < p.nitems; idx += gridDim.x) {
-            Item it;
-            if (!decode_item(p, idx, it)) continue;
+        for (uint32_t it_iter = 0;; ++it_iter) {
+            const uint32_t slot = it_iter % kItemSlots;
+            mbar_wait(&item_full[slot], (it_iter / kItemSlots) & 1);
+            const Item it = items[slot];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&item_empty[slot]);
+            if (it.kt_begin < 0) break;
+            const float* w_item = w_smem + (qiter & 1) * (kQPerItem * kHeads);
+            mbar_wait(&w_full[qiter & 1], (qiter >> 1) & 1);
+            ++qiter;
             for (int kt = it.kt_begin; kt < it.kt_end; ++kt) {
                 const int64_t j = static_cast<int64_t>(kt) * kBlockKeys + quarter * 32 + lane;
                 for (int g = 0; g < kGroups; ++g) {
@@ -216,27 +291,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                     for (int qq = 0; qq < 2; ++qq) {
                         const int qi = g * kQPerGroup + qpair * 2 + qq;   // query within item
                         if (qi >= it.nrows) continue;                      // warp-uniform
-                        const int64_t r = it.r0 + qi;
-                        const int64_t s = p.s0 + r;
-                        const float* wrow = p.w + (static_cast<int64_t>(it.b) * p.seq_len + s) * kHeads;
-                        const uint32_t col = a * kUmmaN + (qpair * 2 + qq) * kHeads;
-                        float acc = 0.0f;
-#pragma unroll
-                        for (int half = 0; half < 2; ++half) {
-                            float v[32];
-                            tmem_ld32(row_taddr + col + half * 32, v);
-                            tmem_ld_wait();
-                            const float4* w4 = reinterpret_cast<const float4*>(wrow + half * 32);
-#pragma unroll
-                            for (int h4 = 0; h4 < 8; ++h4) {
-                                const float4 wv = __ldg(w4 + h4);
-                                acc = fmaf(wv.x, fmaxf(v[4 * h4 + 0], 0.0f), acc);
-                                acc = fmaf(wv.y, fmaxf(v[4 * h4 + 1], 0.0f), acc);
-                                acc = fmaf(wv.z, fmaxf(v[4 * h4 + 2], 0.0f), acc);
-                                acc = fmaf(wv.w, fmaxf(v[4 * h4 + 3], 0.0f), acc);
-                            }
-                        }
+                        float v[64];
+                        tmem_ld64(row_taddr + a * kUmmaN + (qpair * 2 + qq) * kHeads, v);
+                        tmem_ld_wait();
+                        const float acc = head_reduce(v, w_item + qi * kHeads);
                         if (j < p.cols) {
+                            const int64_t r = it.r0 + qi;
+                            const int64_t s = p.s0 + r;
                             float outv = acc;
                             const bool legal = !p.apply_mask || (p.t0 + j) < t_legal_dev(s, p.ratio);
                             if (!legal) {
@@ -261,6 +322,15 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<kTmemCols>(tmem_base);
+    }
+    if (threadIdx.x == 0) {
+        // The last CTA out re-arms the work counter for the next launch.
+        __threadfence();
+        if (atomicAdd(p.sched + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+            p.sched[0] = 0;
+            p.sched[1] = 0;
+            __threadfence();
+        }
     }
 }
 
@@ -328,11 +398,37 @@ size_t score_tc_smem_bytes() { return kSmemBytes; }
 
 cudaError_t launch_score_tc(const CUtensorMap& qmap, const CUtensorMap& kmap, ScoreTcParams p,
                             int num_sms, cudaStream_t stream) {
+    // Dense piece-major work list: piece pc covers key tiles [pc*tpp,
+    // (pc+1)*tpp); the query blocks for which it is causally live form a
+    // suffix qb >= nqb - count[pc] because the live extent grows with qb.
     p.nqb = static_cast<int>((p.rows + kQPerItem - 1) / kQPerItem);
     const int64_t max_tiles = (p.cols + kBlockKeys - 1) / kBlockKeys;
-    p.npieces = static_cast<int>((max_tiles + kKTilesPerPiece - 1) / kKTilesPerPiece);
-    if (p.npieces < 1) p.npieces = 1;
-    p.nitems = p.nqb * p.batch * p.npieces;
+    int64_t tpp = kMinTilesPerPiece;
+    while ((max_tiles + tpp - 1) / tpp > kScoreMaxPieces) tpp *= 2;
+    p.tpp = static_cast<int>(tpp);
+    p.npieces = static_cast<int>((max_tiles + tpp - 1) / tpp);
+    std::vector<int> live(static_cast<size_t>(p.npieces) + 1, 0);  // live[n] = #qb with exactly n pieces
+    for (int qb = 0; qb < p.nqb; ++qb) {
+        const int64_t r0 = static_cast<int64_t>(qb) * kQPerItem;
+        const int64_t nrows = (p.rows - r0) < kQPerItem ? (p.rows - r0) : kQPerItem;
+        int64_t kend = p.cols;
+        if (p.apply_mask) {
+            kend = (p.s0 + r0 + nrows) / p.ratio - p.t0;
+            kend = kend < 0 ? 0 : (kend > p.cols ? p.cols : kend);
+        }
+        const int64_t ntiles = (kend + kBlockKeys - 1) / kBlockKeys;
+        ++live[static_cast<size_t>((ntiles + tpp - 1) / tpp)];
+    }
+    int above = 0;  // #qb with more than pc pieces, built from the top
+    std::vector<int> count(static_cast<size_t>(p.npieces), 0);
+    for (int pc = p.npieces - 1; pc >= 0; --pc) {
+        above += live[static_cast<size_t>(pc) + 1];
+        count[static_cast<size_t>(pc)] = above;
+    }
+    p.piece_start[0] = 0;
+    for (int pc = 0; pc < p.npieces; ++pc) p.piece_start[pc + 1] = p.piece_start[pc] + count[pc] * p.batch;
+    p.nitems = p.piece_start[p.npieces];
+    if (p.nitems <= 0) return cudaSuccess;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(score_tc_kernel,
@@ -342,7 +438,6 @@ cudaError_t launch_score_tc(const CUtensorMap& qmap, const CUtensorMap& kmap, Sc
         attr_set = true;
     }
     const int grid = p.nitems < num_sms ? p.nitems : num_sms;
-    if (grid <= 0) return cudaSuccess;
     score_tc_kernel<<<grid, kNumThreads, kSmemBytes, stream>>>(qmap, kmap, p);
     return cudaGetLastError();
 }

@@ -1,0 +1,10 @@
+#!/bin/bash
+# GPU-box profiling pass (run under gpurun): kernel launch list + one full
+# ncu capture of the score and select kernels at a late C3 chunk.
+set -x
+mkdir -p gpurun_out
+B="python bench.py --profile-only --steps 1 --warmup 1"
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/launches.log 2>&1
+timeout 400 ncu --set full --clock-control none --import-source on -k regex:score_tc_kernel -s 200 -c 1 -f -o gpurun_out/score_full $B > gpurun_out/score_full.log 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:select_kernel -s 200 -c 1 -f -o gpurun_out/select_full $B > gpurun_out/select_full.log 2>&1
+ls -la gpurun_out

@@ -167,6 +167,27 @@ def test_select_matches_sorted_reference(engine, cols, k, quant):
     assert np.array_equal(val.cpu().numpy().view(np.uint32), wv.view(np.uint32))
 
 
+@pytest.mark.parametrize("mode", ["sampled_low", "sampled_high", "two_levels"])
+def test_select_survives_adversarial_samples(engine, mode):
+    """Rows built so the sector sample mispredicts the threshold: the kernel
+    must fall back to the exact radix path and still match the reference."""
+    rng = np.random.default_rng(7)
+    B, rows, cols, k = 1, 4, 65536, 1024
+    scores = rng.normal(0, 1, (B, rows, cols)).astype(np.float32)
+    sampled = (np.arange(cols) // 8) % 16 == 0  # every 16th 32-byte sector
+    if mode == "sampled_low":
+        scores[..., sampled] = -10.0           # threshold too low -> overflow
+    elif mode == "sampled_high":
+        scores[..., sampled] = 10.0            # threshold at the sampled plateau
+    else:
+        scores[..., ~sampled] = 5.0            # ties everywhere off-sample
+    val, idx = engine.select(to_dev(scores), B, rows, cols, 10 ** 7, 0, 1, k)
+    engine.check()
+    wv, wi = ref_select(scores, 10 ** 7, 0, 1, k)
+    assert np.array_equal(idx.cpu().numpy(), wi)
+    assert np.array_equal(val.cpu().numpy().view(np.uint32), wv.view(np.uint32))
+
+
 def test_select_all_equal_scores_take_smallest_indices(engine):
     B, rows, cols, k = 1, 3, 10000, 100
     scores = np.zeros((B, rows, cols), np.float32)
