@@ -261,6 +261,7 @@ def main():
         dist.barrier()
     torch.cuda.reset_peak_memory_stats()
     drv.reset()
+    drv.select_fallbacks(reset=True)
     drv.profiling(True)
     clocks = ClockSampler(local)
     clocks.start()
@@ -296,6 +297,7 @@ def main():
     sel_n, sel_ms = kstats["select"]
     select_gbs = (pairs_mine * 4 * args.steps) / (sel_ms / 1000.0) / 1e9 if sel_ms > 0 else None
     _, drv_peak = drv.mem()
+    fallbacks = drv.select_fallbacks()
     hbm_peak = torch.cuda.max_memory_allocated() + drv_peak
     st = stats_box["st"]
 
@@ -371,6 +373,7 @@ def main():
                          "launches": score_n, "avg_launch_ms": score_ms / max(score_n, 1)},
             "kernels_ms_per_step": {n: v[1] / args.steps for n, v in kstats.items()},
             "select_gbs_one_pass": select_gbs,
+            "select_fallback_rows": fallbacks,
             "gpu_launches": launches,
             "clocks": clk,
             "cpu_baseline": cpu,

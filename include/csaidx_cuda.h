@@ -89,6 +89,9 @@ int csaidx_engine_reset_peak(csaidx_engine* e);
 int csaidx_engine_set_profiling(csaidx_engine* e, int enabled);
 int csaidx_engine_kernel_stats(csaidx_engine* e, int kind, int64_t* launches, double* total_ms);
 int csaidx_engine_reset_stats(csaidx_engine* e);
+/* Rows whose select took the exact global-memory fallback (the sampled
+ * threshold mispredicted) since the last reset; synchronizes. */
+int csaidx_engine_select_fallbacks(csaidx_engine* e, int64_t* rows, int reset);
 
 /* Stream-ordered device memory from a cached pool. */
 int csaidx_cuda_alloc(csaidx_engine* e, size_t bytes, void** ptr);

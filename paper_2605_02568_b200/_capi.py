@@ -85,6 +85,7 @@ CUDA_SYMBOLS = {
     "csaidx_engine_set_profiling": (c_int, [c_void_p, c_int]),
     "csaidx_engine_kernel_stats": (c_int, [c_void_p, c_int, POINTER(c_int64), POINTER(ctypes.c_double)]),
     "csaidx_engine_reset_stats": (c_int, [c_void_p]),
+    "csaidx_engine_select_fallbacks": (c_int, [c_void_p, POINTER(c_int64), c_int]),
     "csaidx_cuda_alloc": (c_int, [c_void_p, c_size_t, POINTER(c_void_p)]),
     "csaidx_cuda_free": (c_int, [c_void_p, c_void_p]),
     "csaidx_cuda_copy": (c_int, [c_void_p, c_void_p, c_void_p, c_size_t]),

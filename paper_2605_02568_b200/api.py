@@ -349,6 +349,11 @@ class KernelStats:
         _check_cuda(self.lib.csaidx_engine_kernel_stats(self.h, kind, ctypes.byref(n), ctypes.byref(ms)))
         return n.value, ms.value
 
+    def select_fallbacks(self, reset: bool = False) -> int:
+        n = c_int64()
+        _check_cuda(self.lib.csaidx_engine_select_fallbacks(self.h, ctypes.byref(n), int(reset)))
+        return n.value
+
     def mem(self):
         live, peak = c_uint64(), c_uint64()
         _check_cuda(self.lib.csaidx_engine_mem_stats(self.h, ctypes.byref(live), ctypes.byref(peak)))

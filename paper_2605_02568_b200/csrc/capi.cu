@@ -288,6 +288,16 @@ int csaidx_engine_kernel_stats(csaidx_engine* e, int kind, int64_t* launches, do
     return CSAIDX_OK;
 }
 
+int csaidx_engine_select_fallbacks(csaidx_engine* e, int64_t* rows, int reset) {
+    if (int rc = set_device(e)) return rc;
+    int h = 0;
+    CSAIDX_CUDA_TRY(cudaStreamSynchronize(e->stream), "cudaStreamSynchronize");
+    CSAIDX_CUDA_TRY(cudaMemcpy(&h, e->flags + kNumFlags + 2, sizeof(int), cudaMemcpyDeviceToHost), "counter D2H");
+    if (rows) *rows = h;
+    if (reset) CSAIDX_CUDA_TRY(cudaMemset(e->flags + kNumFlags + 2, 0, sizeof(int)), "counter reset");
+    return CSAIDX_OK;
+}
+
 int csaidx_engine_reset_stats(csaidx_engine* e) {
     if (int rc = set_device(e)) return rc;
     for (const auto& pd : e->pending) {
@@ -482,6 +492,7 @@ int csaidx_cuda_select(csaidx_engine* e, const float* scores, int64_t batch, int
     p.out_val = cand_val;
     p.out_idx = cand_idx;
     p.out_ld = cand_ld;
+    p.fallbacks = e->flags + kNumFlags + 2;
     LaunchScope ls(e, CSAIDX_KIND_SELECT);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_select(p, e->stream), "select");
     return CSAIDX_OK;

@@ -60,6 +60,7 @@ struct SelectParams {
     float* out_val;       // [B, rows, out_ld]
     int32_t* out_idx;
     int64_t out_ld;
+    int* fallbacks;       // rows that took the exact global fallback (telemetry)
 };
 
 // ------------------------------------------------------------------ merge

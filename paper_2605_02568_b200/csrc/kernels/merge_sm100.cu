@@ -101,39 +101,63 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
     }
 }
 
-__global__ void finalize_kernel(const FinalizeParams p) {
-    const int lane = threadIdx.x & 31;
-    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nrows = static_cast<int64_t>(p.batch) * p.rows;
-    if (gw >= nrows) return;
-    const int b = static_cast<int>(gw / p.rows);
-    const int64_t i = gw % p.rows;
-    const float* rv = p.run_val + gw * p.k;
-    const int32_t* ri = p.run_idx + gw * p.k;
+// One CTA per row; 4 entries per thread per step (16 B loads, 2 x 16 B
+// int64 stores) when k is a multiple of 4.
+__global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
+    __shared__ int s_first, s_real;
+    const int64_t row = blockIdx.x;
+    const int b = static_cast<int>(row / p.rows);
+    const int64_t i = row % p.rows;
+    const float* rv = p.run_val + row * p.k;
+    const int32_t* ri = p.run_idx + row * p.k;
     const float neg_inf = -__int_as_float(0x7f800000);
     int64_t* oi = p.out_idx + (static_cast<int64_t>(b) * p.out_rows + p.out_row0 + i) * p.k;
     float* ov = p.out_val + (static_cast<int64_t>(b) * p.out_rows + p.out_row0 + i) * p.k;
+    if (threadIdx.x == 0) {
+        s_first = p.k;
+        s_real = 0;
+    }
+    __syncthreads();
     int first_inf = p.k;
     int real = 0;
-    for (int e = lane; e < p.k; e += 32) {
-        const float v = rv[e];
-        const bool inf = (v == neg_inf);
-        if (inf && e < first_inf) first_inf = e;
-        real += inf ? 0 : 1;
-        ov[e] = v;
-        oi[e] = inf ? -1 : static_cast<int64_t>(ri[e]);
-    }
+    if ((p.k & 3) == 0) {
+        for (int e = 4 * threadIdx.x; e < p.k; e += 4 * blockDim.x) {
+            const float4 v = *reinterpret_cast<const float4*>(rv + e);
+            const int4 x = *reinterpret_cast<const int4*>(ri + e);
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+            const int xx[4] = {x.x, x.y, x.z, x.w};
+            long long o[4];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        first_inf = min(first_inf, __shfl_xor_sync(0xffffffffu, first_inf, o));
-        real += __shfl_xor_sync(0xffffffffu, real, o);
+            for (int u = 0; u < 4; ++u) {
+                const bool inf = vv[u] == neg_inf;
+                if (inf && e + u < first_inf) first_inf = e + u;
+                real += inf ? 0 : 1;
+                o[u] = inf ? -1ll : static_cast<long long>(xx[u]);
+            }
+            *reinterpret_cast<float4*>(ov + e) = v;
+            *reinterpret_cast<longlong2*>(oi + e) = make_longlong2(o[0], o[1]);
+            *reinterpret_cast<longlong2*>(oi + e + 2) = make_longlong2(o[2], o[3]);
+        }
+    } else {
+        for (int e = threadIdx.x; e < p.k; e += blockDim.x) {
+            const float v = rv[e];
+            const bool inf = v == neg_inf;
+            if (inf && e < first_inf) first_inf = e;
+            real += inf ? 0 : 1;
+            ov[e] = v;
+            oi[e] = inf ? -1 : static_cast<int64_t>(ri[e]);
+        }
     }
-    if (lane == 0) {
-        if (real != first_inf) atomicOr(p.trail_flag, 1);
+    if (first_inf < p.k) atomicMin(&s_first, first_inf);
+    if (real != 0) atomicAdd(&s_real, real);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int first = s_first;
+        if (s_real != first) atomicOr(p.trail_flag, 1);
         if (p.check_keff) {
             const int64_t legal = (p.s0 + i + 1) / p.ratio;
             const int64_t want = legal < p.k ? legal : p.k;
-            if (first_inf != want) atomicOr(p.keff_flag, 1);
+            if (first != want) atomicOr(p.keff_flag, 1);
         }
     }
 }
@@ -162,9 +186,7 @@ cudaError_t launch_merge(const MergeParams& p, cudaStream_t stream) {
 cudaError_t launch_finalize(const FinalizeParams& p, cudaStream_t stream) {
     const int64_t nrows = static_cast<int64_t>(p.batch) * p.rows;
     if (nrows <= 0) return cudaSuccess;
-    const int threads = 256;
-    const int64_t blocks = (nrows * 32 + threads - 1) / threads;
-    finalize_kernel<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(p);
+    finalize_kernel<<<static_cast<unsigned>(nrows), 256, 0, stream>>>(p);
     return cudaGetLastError();
 }
 

@@ -56,7 +56,8 @@ constexpr uint32_t kQBytes = kGroups * kQGroupBytes;             // 128 KiB
 constexpr uint32_t kWRowBytes = kHeads * 4;                      // 256 B per query
 constexpr uint32_t kWBufBytes = kQPerItem * kWRowBytes;          // 2 KiB
 constexpr uint32_t kWOffset = kQBytes + kStages * kKStageBytes;  // 192 KiB
-constexpr uint32_t kBarOffset = kWOffset + 2 * kWBufBytes;       // + 4 KiB
+constexpr int kWBufs = 3;                                        // see the producer's reuse proof
+constexpr uint32_t kBarOffset = kWOffset + kWBufs * kWBufBytes;  // + 6 KiB
 constexpr uint32_t kSmemBytes = kBarOffset + 512 + 1024;         // barriers, items, align slack
 
 constexpr int kNumThreads = 384;  // 4 control warps + 8 epilogue warps
@@ -129,19 +130,19 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint8_t* q_smem = smem;
     uint8_t* k_smem = smem + kQBytes;
-    float* w_smem = reinterpret_cast<float*>(smem + kWOffset);  // [2][8][64]
+    float* w_smem = reinterpret_cast<float*>(smem + kWOffset);  // [kWBufs][8][64]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOffset);
-    uint64_t* k_full = bars + 0;
-    uint64_t* k_empty = bars + 2;
-    uint64_t* q_full = bars + 4;
-    uint64_t* q_empty = bars + 5;
-    uint64_t* acc_full = bars + 6;
-    uint64_t* acc_empty = bars + 8;
-    uint64_t* item_full = bars + 10;               // [kItemSlots]
-    uint64_t* item_empty = bars + 10 + kItemSlots;  // [kItemSlots]
-    uint64_t* w_full = bars + 10 + 2 * kItemSlots;  // [2] one per w buffer
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12 + 2 * kItemSlots);
-    Item* items = reinterpret_cast<Item*>(bars + 14 + 2 * kItemSlots);  // [kItemSlots]
+    uint64_t* k_full = bars + 0;      // [kStages]
+    uint64_t* k_empty = bars + 2;     // [kStages]
+    uint64_t* q_full = bars + 4;      // [kGroups] one per query-group buffer
+    uint64_t* q_empty = bars + 6;     // [kGroups]
+    uint64_t* acc_full = bars + 8;    // [2]
+    uint64_t* acc_empty = bars + 10;  // [2]
+    uint64_t* item_full = bars + 12;                // [kItemSlots]
+    uint64_t* item_empty = bars + 12 + kItemSlots;  // [kItemSlots]
+    uint64_t* w_full = bars + 12 + 2 * kItemSlots;  // [kWBufs]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12 + 2 * kItemSlots + kWBufs);
+    Item* items = reinterpret_cast<Item*>(bars + 14 + 2 * kItemSlots + kWBufs);  // [kItemSlots]
 
     const int warp = threadIdx.x / 32;
 
@@ -152,8 +153,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             mbar_init(&k_full[s], 1);
             mbar_init(&k_empty[s], 1);
         }
-        mbar_init(q_full, 1);
-        mbar_init(q_empty, 1);
+        for (int g = 0; g < kGroups; ++g) {
+            mbar_init(&q_full[g], 1);
+            mbar_init(&q_empty[g], 1);
+        }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&acc_full[a], 1);
             mbar_init(&acc_empty[a], kEpiWarps);
@@ -162,8 +165,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             mbar_init(&item_full[s], 1);
             mbar_init(&item_empty[s], 1 + kEpiWarps);  // MMA thread + epilogue warps
         }
-        mbar_init(&w_full[0], 1);
-        mbar_init(&w_full[1], 1);
+        for (int wb = 0; wb < kWBufs; ++wb) mbar_init(&w_full[wb], 1);
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
@@ -192,23 +194,29 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                 items[slot] = it;
                 mbar_arrive(&item_full[slot]);
 
-                mbar_wait(q_empty, (qiter & 1) ^ 1);
-                // q_empty(i-1) also proves the epilogue finished item i-2, the
-                // previous user of this w buffer (its MMAs needed acc_empty).
-                mbar_expect_tx(&w_full[qiter & 1], it.nrows * kWRowBytes);
-                bulk_copy_g2s(w_smem + (qiter & 1) * (kQPerItem * kHeads),
-                              p.w + (static_cast<int64_t>(it.b) * p.seq_len + p.s0 + it.r0) * kHeads,
-                              it.nrows * kWRowBytes, &w_full[qiter & 1]);
-                mbar_expect_tx(q_full, kQBytes);
+                // Query groups refill independently: group g of item i is
+                // reloaded as soon as item i-1's last group-g MMA retires,
+                // overlapping the other group's MMAs; group 1 is issued after
+                // the item's first key tile so that tile is never delayed.
                 const int64_t qrow64 = static_cast<int64_t>(it.b) * p.seq_len + p.s0 + it.r0;
                 const int32_t qrow = static_cast<int32_t>(qrow64 * kHeads);
-                for (int g = 0; g < kGroups; ++g) {
+                const uint32_t qpar = (qiter & 1) ^ 1;
+                auto load_group = [&](int g) {
+                    mbar_wait(&q_empty[g], qpar);
+                    mbar_expect_tx(&q_full[g], kQGroupBytes);
                     for (int hf = 0; hf < 2; ++hf) {
-                        tma_load_2d(q_smem + g * kQGroupBytes + hf * kQHalfBytes, &qmap, q_full, hf * 64,
+                        tma_load_2d(q_smem + g * kQGroupBytes + hf * kQHalfBytes, &qmap, &q_full[g], hf * 64,
                                     qrow + g * kUmmaN);
                     }
-                }
-                ++qiter;
+                };
+                load_group(0);
+                // q_empty[0] of item i-1 retires after item i-1's first group-1
+                // MMA, which waited for the epilogue to release item i-2's last
+                // accumulator: so with 3 w buffers, buffer (i % 3) is free.
+                const uint32_t wb = qiter % kWBufs;
+                mbar_expect_tx(&w_full[wb], it.nrows * kWRowBytes);
+                bulk_copy_g2s(w_smem + wb * (kQPerItem * kHeads), p.w + qrow64 * kHeads, it.nrows * kWRowBytes,
+                              &w_full[wb]);
                 const int64_t krow0 = static_cast<int64_t>(it.b) * p.key_blocks + p.t0;
                 for (int kt = it.kt_begin; kt < it.kt_end; ++kt) {
                     const uint32_t s = kiter % kStages;
@@ -220,7 +228,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                                          krow, keep);
                     }
                     ++kiter;
+                    if (kt == it.kt_begin) load_group(1);
                 }
+                ++qiter;
             }
         }
     } else if (warp == 1) {
@@ -235,14 +245,17 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                 const Item it = items[slot];
                 mbar_arrive(&item_empty[slot]);
                 if (it.kt_begin < 0) break;
-                mbar_wait(q_full, qiter & 1);
+                const uint32_t qpar = qiter & 1;
                 ++qiter;
-                tc_fence_after();
                 for (int kt = it.kt_begin; kt < it.kt_end; ++kt) {
                     const uint32_t s = kiter % kStages;
                     mbar_wait(&k_full[s], (kiter / kStages) & 1);
                     tc_fence_after();
                     for (int g = 0; g < kGroups; ++g) {
+                        if (kt == it.kt_begin) {
+                            mbar_wait(&q_full[g], qpar);
+                            tc_fence_after();
+                        }
                         const uint32_t a = aiter & 1;
                         mbar_wait(&acc_empty[a], ((aiter >> 1) & 1) ^ 1);
                         tc_fence_after();
@@ -255,12 +268,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                                       sw128_kmajor_desc(q_base + qoff), kIdesc, kk > 0 ? 1u : 0u);
                         }
                         umma_commit(&acc_full[a]);
+                        if (kt == it.kt_end - 1) umma_commit(&q_empty[g]);  // group g of this item retired
                         ++aiter;
                     }
                     umma_commit(&k_empty[s]);
                     ++kiter;
                 }
-                umma_commit(q_empty);
             }
         }
     } else if (warp >= 4) {
@@ -278,8 +291,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&item_empty[slot]);
             if (it.kt_begin < 0) break;
-            const float* w_item = w_smem + (qiter & 1) * (kQPerItem * kHeads);
-            mbar_wait(&w_full[qiter & 1], (qiter >> 1) & 1);
+            const uint32_t wb = qiter % kWBufs;
+            const float* w_item = w_smem + wb * (kQPerItem * kHeads);
+            mbar_wait(&w_full[wb], (qiter / kWBufs) & 1);
             ++qiter;
             for (int kt = it.kt_begin; kt < it.kt_end; ++kt) {
                 const int64_t j = static_cast<int64_t>(kt) * kBlockKeys + quarter * 32 + lane;

@@ -1,23 +1,24 @@
 // Per-row exact top-k selection over one score tile (the GPU tile_topk,
 // reference topk.cpp:105-132 + causal.cpp:30-41).
 //
-// One CTA per (batch, query row); n = the row's legal columns. Every entry is
-// packed into a unique 64-bit composite (ord_key(score) << 32 | ~(col + 1)):
-// ord_key is monotone in the float order with -0.0 folded onto +0.0, and the
-// low word makes ties go to the smaller index, so descending composite order
-// is exactly the reference's succ() order (topk.hpp:23-26).
+// One 256-thread CTA per (batch, query row), several rows per SM; n = the
+// row's legal columns. Every entry is packed into a unique 64-bit composite
+// (ord_key(score) << 32 | ~(col + 1)): ord_key is monotone in the float order
+// with -0.0 folded onto +0.0, and the low word makes ties go to the smaller
+// index, so descending composite order is exactly the reference's succ()
+// order (topk.hpp:23-26).
 //
-// Fast path (one streaming pass over HBM/L2):
-//   1. sample: every stride-th 32-byte sector of the row (1/16 of the row or
-//      less) goes to shared memory; a shared-memory radix select finds the
-//      sample key whose rank predicts ~2k survivors in the whole row;
-//   2. filter: the row is streamed once (2 x float4 per thread in flight);
-//      entries at or above that key are appended to a shared candidate list
-//      with warp-aggregated atomics;
+// Fast path (one streaming pass over the row):
+//   1. sample: evenly spaced 128-byte lines (<= 1/16 of the row); one
+//      histogram below the sample's common key prefix picks a threshold
+//      expected to keep ~2k entries of the row;
+//   2. filter: the row is streamed once (4 x float4 per thread in flight);
+//      survivors are appended to a shared candidate list with one warp scan
+//      and one shared atomic per warp;
 //   3. if the list holds between k and its capacity, the exact k-th largest
-//      composite is found by shared-memory radix select (unique keys, so no
-//      tie bookkeeping), the k survivors are bitonic-sorted and written.
-// If the sample mispredicts (fewer than k or more than capacity survivors)
+//      composite is found by shared-memory radix select (unique keys, no tie
+//      bookkeeping); the k survivors are bitonic-sorted and written.
+// When the sample mispredicts (fewer than k or more than capacity survivors)
 // the row falls back to an exact MSB-first radix select over global memory
 // with index-ordered tie collection. Rows with n <= capacity skip sampling.
 #include <cuda_runtime.h>
@@ -31,14 +32,37 @@ using namespace csaidx_dev;
 
 namespace {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kBins = 2048;
 constexpr int kMaxTake = 4096;    // largest min(k, n) a row may select
-constexpr int kCandCap = 8192;    // shared candidate list (u64)
-constexpr int kSampleSectors = 1024;
-constexpr size_t kSmemBytes = kCandCap * sizeof(uint64_t) + kMaxTake * sizeof(uint64_t) + kBins * sizeof(uint32_t) +
-                              4 * kWarps * sizeof(uint32_t) + 64;
+constexpr int kMaxCand = 8192;    // largest shared candidate list
+constexpr int kSampleLines = 256;  // <= 8192 sampled keys per row
+
+struct Layout {
+    int cand_cap;  // power of two, >= 2k
+    int buf_cap;   // power of two, >= k
+};
+
+__host__ __device__ inline int pow2_at_least(int x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+__host__ __device__ inline Layout layout_for(int k) {
+    Layout l;
+    int c = pow2_at_least(4 * k);
+    l.cand_cap = c < 2048 ? 2048 : (c > kMaxCand ? kMaxCand : c);
+    l.buf_cap = pow2_at_least(k);
+    return l;
+}
+
+__host__ __device__ inline size_t smem_bytes_for(int k) {
+    const Layout l = layout_for(k);
+    return static_cast<size_t>(l.cand_cap + l.buf_cap) * sizeof(uint64_t) + kBins * sizeof(uint32_t) +
+           (4 * kWarps + 16) * sizeof(uint32_t);
+}
 
 __device__ __forceinline__ uint64_t composite(uint32_t key, int64_t col) {
     return (static_cast<uint64_t>(key) << 32) | static_cast<uint32_t>(~static_cast<uint32_t>(col + 1));
@@ -46,12 +70,6 @@ __device__ __forceinline__ uint64_t composite(uint32_t key, int64_t col) {
 
 __device__ __forceinline__ int64_t composite_col(uint64_t c) {
     return static_cast<int64_t>(~static_cast<uint32_t>(c)) - 1;
-}
-
-__device__ __forceinline__ int pow2_ceil(int x) {
-    int p = 1;
-    while (p < x) p <<= 1;
-    return p;
 }
 
 // Descending bitonic sort of a[0, P), P a power of two, whole block.
@@ -73,49 +91,74 @@ __device__ void bitonic_sort_desc(uint64_t* a, int P) {
     }
 }
 
-// Finds the bin (scanning from the top) holding the kk-th largest element.
-// out3 = {bin, count strictly above it, the bin's own count}.
-__device__ void find_bin(const uint32_t* hist, int nbins, uint32_t kk, uint32_t* out3) {
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        const int per = nbins / 32;
-        const int hi = nbins - lane * per;  // lane 0 owns the highest bins
-        uint32_t sum = 0;
-        for (int b = hi - 1; b >= hi - per; --b) sum += hist[b];
-        uint32_t incl = sum;
+// Block-parallel search of the bin (counting from the top) holding the
+// kk-th largest element: every thread sums a run of bins, a block scan
+// locates the run, its owner walks it. out3 = {bin, count above, bin count}.
+__device__ void find_bin(const uint32_t* hist, int nbins, uint32_t kk, uint32_t* out3, uint32_t* wsum) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int per = nbins >= static_cast<int>(blockDim.x) ? nbins / blockDim.x : 1;
+    const int hi = nbins - static_cast<int>(threadIdx.x) * per;  // thread 0 owns the highest bins
+    uint32_t sum = 0;
+    for (int b = hi - 1; b >= hi - per && b >= 0; --b) sum += hist[b];
+    uint32_t incl = sum;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += v;
-        }
-        const uint32_t excl = incl - sum;
-        if (excl < kk && kk <= incl) {
-            uint32_t cum = excl;
-            for (int b = hi - 1; b >= hi - per; --b) {
-                const uint32_t c = hist[b];
-                if (cum + c >= kk) {
-                    out3[0] = static_cast<uint32_t>(b);
-                    out3[1] = cum;
-                    out3[2] = c;
-                    break;
-                }
-                cum += c;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    uint32_t before = 0;
+    for (int w = 0; w < warp; ++w) before += wsum[w];
+    const uint32_t excl = before + incl - sum;
+    if (sum > 0 && excl < kk && kk <= excl + sum) {
+        uint32_t cum = excl;
+        for (int b = hi - 1; b >= hi - per && b >= 0; --b) {
+            const uint32_t c = hist[b];
+            if (cum + c >= kk) {
+                out3[0] = static_cast<uint32_t>(b);
+                out3[1] = cum;
+                out3[2] = c;
+                break;
             }
+            cum += c;
         }
     }
     __syncthreads();
 }
 
-// kk-th largest of the unique 64-bit values a[0, n) in shared memory: returns
-// (prefix, pbits) such that exactly kk values have their top pbits >= prefix.
+// kk-th largest of the unique 64-bit values a[0, n) in shared memory:
+// returns (prefix, pbits) such that exactly kk values have top pbits >= prefix.
 __device__ void smem_radix_u64(const uint64_t* a, int n, uint32_t kk, uint32_t* hist, uint32_t* res,
-                               uint64_t& prefix_out, int& pbits_out) {
-    uint64_t prefix = 0;
-    int pbits = 0;
-    const int widths[6] = {11, 11, 10, 11, 11, 10};
+                               uint32_t* wsum, uint64_t& prefix_out, int& pbits_out) {
+    // Start below the common prefix of min and max: candidates are the top
+    // few percent of a row and share their leading key bits.
+    __shared__ unsigned long long s_mm[2];
+    if (threadIdx.x == 0) {
+        s_mm[0] = ~0ull;
+        s_mm[1] = 0ull;
+    }
+    __syncthreads();
+    unsigned long long mn = ~0ull, mx = 0ull;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        mn = min(mn, static_cast<unsigned long long>(a[i]));
+        mx = max(mx, static_cast<unsigned long long>(a[i]));
+    }
 #pragma unroll
-    for (int pass = 0; pass < 6; ++pass) {
-        const int wbits = widths[pass];
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&s_mm[0], mn);
+        atomicMax(&s_mm[1], mx);
+    }
+    __syncthreads();
+    const uint64_t lo = s_mm[0], hi = s_mm[1];
+    int pbits = lo == hi ? 64 : __clzll(static_cast<long long>(lo ^ hi));
+    uint64_t prefix = pbits == 0 ? 0ull : (pbits == 64 ? lo : (lo >> (64 - pbits)));
+    while (pbits < 64) {
+        const int wbits = 64 - pbits < 11 ? 64 - pbits : 11;
         const int shift = 64 - pbits - wbits;
         for (int i = threadIdx.x; i < kBins; i += blockDim.x) hist[i] = 0;
         __syncthreads();
@@ -125,7 +168,7 @@ __device__ void smem_radix_u64(const uint64_t* a, int n, uint32_t kk, uint32_t* 
                 atomicAdd(&hist[static_cast<uint32_t>(v >> shift) & ((1u << wbits) - 1u)], 1u);
         }
         __syncthreads();
-        find_bin(hist, 1 << wbits, kk, res);
+        find_bin(hist, 1 << wbits, kk, res, wsum);
         const uint32_t bin = res[0], above = res[1], cnt = res[2];
         __syncthreads();
         kk -= above;
@@ -139,32 +182,6 @@ __device__ void smem_radix_u64(const uint64_t* a, int n, uint32_t kk, uint32_t* 
 
 __device__ __forceinline__ bool top_ge(uint64_t v, uint64_t prefix, int pbits) {
     return pbits >= 64 ? v >= prefix : (v >> (64 - pbits)) >= prefix;
-}
-
-// kk-th largest of the u32 sample s[0, n) (shared memory).
-__device__ uint32_t smem_kth_u32(const uint32_t* s, int n, uint32_t kk, uint32_t* hist, uint32_t* res) {
-    uint32_t prefix = 0;
-    int pbits = 0;
-    const int widths[3] = {11, 11, 10};
-#pragma unroll
-    for (int pass = 0; pass < 3; ++pass) {
-        const int wbits = widths[pass];
-        const int shift = 32 - pbits - wbits;
-        for (int i = threadIdx.x; i < kBins; i += blockDim.x) hist[i] = 0;
-        __syncthreads();
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const uint32_t v = s[i];
-            if (pbits == 0 || (v >> (32 - pbits)) == prefix) atomicAdd(&hist[(v >> shift) & ((1u << wbits) - 1u)], 1u);
-        }
-        __syncthreads();
-        find_bin(hist, 1 << wbits, kk, res);
-        const uint32_t bin = res[0], above = res[1];
-        __syncthreads();
-        kk -= above;
-        prefix = (pbits == 0 ? 0u : (prefix << wbits)) | bin;
-        pbits += wbits;
-    }
-    return prefix;  // full 32-bit key of the kk-th largest sample
 }
 
 // ------------------------------------------------------------------ fallback
@@ -234,32 +251,31 @@ __device__ void collect_pass(const float* row, int64_t n, uint32_t prefix, int p
     __syncthreads();
 }
 
-__device__ void exact_global_select(const float* row, int64_t n, int k, uint64_t* buf, uint64_t* cand,
-                                    uint32_t* hist, uint32_t* wtot, uint32_t* res) {
+__device__ void exact_global_select(const float* row, int64_t n, int k, uint64_t* buf, uint64_t* cand, int cand_cap,
+                                    uint32_t* hist, uint32_t* wtot, uint32_t* res, uint32_t* wsum) {
     uint32_t prefix = 0;
     int pbits = 0;
     uint32_t kk = static_cast<uint32_t>(k);
     uint32_t bin_count = 0;
-    const int widths[3] = {11, 11, 10};
-#pragma unroll
+#pragma unroll 1
     for (int pass = 0; pass < 3; ++pass) {
-        const int wbits = widths[pass];
+        const int wbits = pass == 2 ? 10 : 11;
         histogram_pass(row, n, prefix, pbits, wbits, hist);
-        find_bin(hist, 1 << wbits, kk, res);
+        find_bin(hist, 1 << wbits, kk, res, wsum);
         kk -= res[1];
         bin_count = res[2];
         prefix = (pbits == 0 ? 0u : (prefix << wbits)) | res[0];
         pbits += wbits;
         __syncthreads();
-        if (bin_count <= static_cast<uint32_t>(kCandCap)) break;
+        if (bin_count <= static_cast<uint32_t>(cand_cap)) break;
     }
     const uint32_t above = static_cast<uint32_t>(k) - kk;
     if (pbits == 32) {
         // a single key value: its first kk entries in index order
         collect_pass(row, n, prefix, pbits, buf, buf + above, kk, wtot);
     } else {
-        collect_pass(row, n, prefix, pbits, buf, cand, static_cast<uint32_t>(kCandCap), wtot);
-        const int P = pow2_ceil(static_cast<int>(bin_count));
+        collect_pass(row, n, prefix, pbits, buf, cand, static_cast<uint32_t>(cand_cap), wtot);
+        const int P = pow2_at_least(static_cast<int>(bin_count));
         for (int i = static_cast<int>(bin_count) + threadIdx.x; i < P; i += blockDim.x) cand[i] = 0;
         __syncthreads();
         bitonic_sort_desc(cand, P);
@@ -270,13 +286,16 @@ __device__ void exact_global_select(const float* row, int64_t n, int k, uint64_t
 
 // ------------------------------------------------------------------ kernel
 
-__global__ void __launch_bounds__(kThreads, 2) select_kernel(const SelectParams p) {
+__global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams p) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    uint64_t* cand = reinterpret_cast<uint64_t*>(smem_raw);  // [kCandCap]
-    uint64_t* buf = cand + kCandCap;                         // [kMaxTake]
-    uint32_t* hist = reinterpret_cast<uint32_t*>(buf + kMaxTake);
+    const int k = p.k;
+    const Layout L = layout_for(k);
+    uint64_t* cand = reinterpret_cast<uint64_t*>(smem_raw);  // [cand_cap]
+    uint64_t* buf = cand + L.cand_cap;                       // [buf_cap]
+    uint32_t* hist = reinterpret_cast<uint32_t*>(buf + L.buf_cap);
     uint32_t* wtot = hist + kBins;                           // [2][2*kWarps]
-    uint32_t* res = wtot + 4 * kWarps;                       // find_bin result (3) + counter
+    uint32_t* wsum = wtot + 4 * kWarps;                      // [kWarps] (find_bin)
+    uint32_t* res = wsum + kWarps;                           // [8]
     uint32_t* counter = res + 4;
     uint32_t* sample = reinterpret_cast<uint32_t*>(cand);    // aliases cand during sampling
 
@@ -288,47 +307,99 @@ __global__ void __launch_bounds__(kThreads, 2) select_kernel(const SelectParams 
         n = n < 0 ? 0 : (n > p.cols ? p.cols : n);
     }
     const float* row = p.scores + (static_cast<int64_t>(b) * p.rows + row_id) * p.ld;
-    const int k = p.k;
     const int take = static_cast<int>(n < k ? n : k);
     const int lane = threadIdx.x & 31;
 
     if (take > 0) {
         int count = -1;  // candidates in cand[], or -1 -> fallback
-        if (n <= kCandCap) {
+        if (n <= L.cand_cap) {
             for (int64_t i = threadIdx.x; i < n; i += blockDim.x) cand[i] = composite(ord_key(__ldg(row + i)), i);
             count = static_cast<int>(n);
             __syncthreads();
         } else {
-            // 1. sample every stride-th 32-byte sector
-            const int64_t sectors = n >> 3;
-            int64_t stride = (sectors + kSampleSectors - 1) / kSampleSectors;
-            if (stride < 16) stride = 16;
-            const int nss = static_cast<int>((sectors + stride - 1) / stride);
-            const float4* row4 = reinterpret_cast<const float4*>(row);
-            for (int s = threadIdx.x; s < nss; s += blockDim.x) {
-                const int64_t sec = static_cast<int64_t>(s) * stride;
-                const float4 a = __ldg(row4 + 2 * sec), c = __ldg(row4 + 2 * sec + 1);
-                uint32_t* dst = sample + 8 * s;
-                dst[0] = ord_key(a.x); dst[1] = ord_key(a.y); dst[2] = ord_key(a.z); dst[3] = ord_key(a.w);
-                dst[4] = ord_key(c.x); dst[5] = ord_key(c.y); dst[6] = ord_key(c.z); dst[7] = ord_key(c.w);
+            // 1. sample evenly spaced 128-byte lines; each warp issues all
+            //    of its line loads before consuming them
+            int nseg = static_cast<int>(n / 512);
+            if (nseg > kSampleLines) nseg = kSampleLines;
+            if (nseg > L.cand_cap / 16) nseg = L.cand_cap / 16;  // 32 keys per line must fit in cand
+            const int64_t seg_stride = n / nseg;
+            constexpr int kLinesPerWarp = kSampleLines / kWarps;  // 32
+            const int w = threadIdx.x >> 5;
+            float sv[kLinesPerWarp];
+#pragma unroll
+            for (int u = 0; u < kLinesPerWarp; ++u) {
+                const int s = w + u * kWarps;
+                sv[u] = s < nseg ? __ldg(row + static_cast<int64_t>(s) * seg_stride + lane) : 0.f;
             }
-            if (threadIdx.x == 0) *counter = 0;
+            uint32_t kmin = 0xffffffffu, kmax = 0u;
+#pragma unroll
+            for (int u = 0; u < kLinesPerWarp; ++u) {
+                const int s = w + u * kWarps;
+                if (s < nseg) {
+                    const uint32_t key = ord_key(sv[u]);
+                    sample[32 * s + lane] = key;
+                    kmin = min(kmin, key);
+                    kmax = max(kmax, key);
+                }
+            }
+            if (threadIdx.x == 0) {
+                *counter = 0;
+                res[6] = 0xffffffffu;
+                res[7] = 0u;
+            }
+            for (int i = threadIdx.x; i < kBins; i += blockDim.x) hist[i] = 0;
             __syncthreads();
-            const int ns = 8 * nss;
-            const int target = (2 * k < (kCandCap * 3) / 4) ? 2 * k : (kCandCap * 3) / 4;
+            kmin = __reduce_min_sync(0xffffffffu, kmin);
+            kmax = __reduce_max_sync(0xffffffffu, kmax);
+            if (lane == 0) {
+                atomicMin(&res[6], kmin);
+                atomicMax(&res[7], kmax);
+            }
+            __syncthreads();
+            const int ns = 32 * nseg;
+            const int target = (2 * k < (L.cand_cap * 3) / 4) ? 2 * k : (L.cand_cap * 3) / 4;
             int r = static_cast<int>((static_cast<int64_t>(target) * ns) / n);
             if (r < 1) r = 1;
-            if (r > ns) r = ns;
-            const uint32_t tau = smem_kth_u32(sample, ns, static_cast<uint32_t>(r), hist, res);
-            // 2. stream the row once; keep entries with key >= tau. The test
-            //    is a plain float compare (ord_key is monotone and maps -0.0
-            //    onto +0.0, like the float order); survivors (~2k of n) are
-            //    appended with one warp scan + one shared atomic per warp.
+            // Two 11-bit histogram passes below the sample's common key
+            // prefix locate the sample's rank-r key to 22 bits; the threshold
+            // is the lower edge of that fine bin.
+            const uint32_t lo = res[6], hi_k = res[7];
+            uint32_t prefix = 0;
+            int pbits = lo == hi_k ? 32 : __clz(lo ^ hi_k);
+            if (pbits > 0) prefix = pbits == 32 ? lo : (lo >> (32 - pbits));
+            uint32_t rr = static_cast<uint32_t>(r);
+#pragma unroll 1
+            for (int pass = 0; pass < 2 && pbits < 32; ++pass) {
+                const int wbits = 32 - pbits < 11 ? 32 - pbits : 11;
+                const int shift = 32 - pbits - wbits;
+                if (pass > 0) {
+                    for (int i = threadIdx.x; i < kBins; i += blockDim.x) hist[i] = 0;
+                    __syncthreads();
+                }
+                for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+                    const uint32_t v = sample[i];
+                    if (pbits == 0 || (v >> (32 - pbits)) == prefix)
+                        atomicAdd(&hist[(v >> shift) & ((1u << wbits) - 1u)], 1u);
+                }
+                __syncthreads();
+                find_bin(hist, 1 << wbits, rr, res, wsum);
+                rr -= res[1];
+                prefix = (pbits == 0 ? 0u : (prefix << wbits)) | res[0];
+                pbits += wbits;
+                __syncthreads();
+            }
+            const uint32_t tau = pbits >= 32 ? prefix : (prefix << (32 - pbits));
+
+            // 2. stream the row once; keep entries with key >= tau (a plain
+            //    float compare: ord_key is monotone and folds -0.0 onto +0.0
+            //    like the float order)
             const float tau_f = ord_key_to_float(tau);
+            const float4* row4 = reinterpret_cast<const float4*>(row);
             const int64_t n4 = n >> 2;
             constexpr int kUnroll = 4;
             const int64_t step = kUnroll * static_cast<int64_t>(blockDim.x);
             const int64_t n4r = (n4 + step - 1) / step * step;
+            const uint32_t cap = static_cast<uint32_t>(L.cand_cap);
             for (int64_t it = threadIdx.x; it < n4r; it += step) {
                 float4 v[kUnroll];
 #pragma unroll
@@ -362,8 +433,7 @@ __global__ void __launch_bounds__(kThreads, 2) select_kernel(const SelectParams 
 #pragma unroll
                     for (int x = 0; x < 4; ++x) {
                         if (m & (1u << (4 * u + x))) {
-                            if (pos < static_cast<uint32_t>(kCandCap))
-                                cand[pos] = composite(ord_key(e[x]), 4 * (it + u * blockDim.x) + x);
+                            if (pos < cap) cand[pos] = composite(ord_key(e[x]), 4 * (it + u * blockDim.x) + x);
                             ++pos;
                         }
                     }
@@ -374,20 +444,18 @@ __global__ void __launch_bounds__(kThreads, 2) select_kernel(const SelectParams 
                 const bool inb = i < n;
                 const uint32_t key = inb ? ord_key(__ldg(row + i)) : 0u;
                 const bool pass = inb && key >= tau;
-                const uint32_t m = __ballot_sync(0xffffffffu, pass);
-                if (m != 0) {
+                const uint32_t mm = __ballot_sync(0xffffffffu, pass);
+                if (mm != 0) {
                     uint32_t base = 0;
-                    if (lane == 0) base = atomicAdd(counter, __popc(m));
+                    if (lane == 0) base = atomicAdd(counter, __popc(mm));
                     base = __shfl_sync(0xffffffffu, base, 0);
-                    const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
-                    if (pass && pos < static_cast<uint32_t>(kCandCap)) cand[pos] = composite(key, i);
+                    const uint32_t pos = base + __popc(mm & ((1u << lane) - 1u));
+                    if (pass && pos < cap) cand[pos] = composite(key, i);
                 }
             }
             __syncthreads();
             const uint32_t total = *counter;
-            count = (total >= static_cast<uint32_t>(k) && total <= static_cast<uint32_t>(kCandCap))
-                        ? static_cast<int>(total)
-                        : -1;
+            count = (total >= static_cast<uint32_t>(k) && total <= cap) ? static_cast<int>(total) : -1;
             __syncthreads();
         }
 
@@ -396,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 2) select_kernel(const SelectParams 
             if (count > take) {
                 uint64_t prefix;
                 int pbits;
-                smem_radix_u64(cand, count, static_cast<uint32_t>(take), hist, res, prefix, pbits);
+                smem_radix_u64(cand, count, static_cast<uint32_t>(take), hist, res, wsum, prefix, pbits);
                 if (threadIdx.x == 0) *counter = 0;
                 __syncthreads();
                 for (int i = threadIdx.x; i < count; i += blockDim.x) {
@@ -408,9 +476,10 @@ __global__ void __launch_bounds__(kThreads, 2) select_kernel(const SelectParams 
             }
             __syncthreads();
         } else {
-            exact_global_select(row, n, take, buf, cand, hist, wtot, res);
+            if (threadIdx.x == 0 && p.fallbacks != nullptr) atomicAdd(p.fallbacks, 1);
+            exact_global_select(row, n, take, buf, cand, L.cand_cap, hist, wtot, res, wsum);
         }
-        const int P = pow2_ceil(take);
+        const int P = pow2_at_least(take);
         for (int i = take + threadIdx.x; i < P; i += blockDim.x) buf[i] = 0;
         __syncthreads();
         bitonic_sort_desc(buf, P);
@@ -442,12 +511,12 @@ cudaError_t launch_select(const SelectParams& p, cudaStream_t stream) {
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(kSmemBytes));
+                                             static_cast<int>(smem_bytes_for(kMaxTake)));
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     const dim3 grid(static_cast<unsigned>(p.rows), static_cast<unsigned>(p.batch));
-    select_kernel<<<grid, kThreads, kSmemBytes, stream>>>(p);
+    select_kernel<<<grid, kThreads, smem_bytes_for(p.k), stream>>>(p);
     return cudaGetLastError();
 }
 
