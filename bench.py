@@ -56,18 +56,11 @@ def legal_pairs_rows(S, m, starts, cs, T):
 
 
 def shard_chunks(S, m, cs, world, rank):
-    """LPT assignment of c_S chunks by causal work (balanced query sharding)."""
-    starts = list(range(0, S, cs))
-    cost = [(legal_pairs_rows(S, m, [s], cs, S // m), s) for s in starts]
-    cost.sort(reverse=True)
-    loads = [0] * world
-    owner = {}
-    for c, s in cost:
-        r = min(range(world), key=lambda i: (loads[i], i))
-        loads[r] += c
-        owner[s] = r
-    mine = sorted(s for s in starts if owner[s] == rank)
-    return mine, loads
+    """LPT assignment of c_S chunks by causal work (paper_2605_02568_b200/shard.py)."""
+    from paper_2605_02568_b200.shard import plan_shards
+
+    shards, loads = plan_shards(S, m, cs, world)
+    return shards[rank], loads, shards
 
 
 def load_peaks():
@@ -218,7 +211,7 @@ def main():
     ct = ct or T
     cfg = api.DriverConfig(tile=api.TileConfig(cs, ct), device=local, stream=stream.cuda_stream)
     dims = api.ProblemDims.create(B, S, m, H, D, k)
-    mine, loads = shard_chunks(S, m, cs, world, rank)
+    mine, loads, shards = shard_chunks(S, m, cs, world, rank)
     rows = api.chunk_rows(dims, cfg, mine)
     pairs_total = B * legal_pairs_rows(S, m, range(0, S, cs), cs, T)
     pairs_mine = B * legal_pairs_rows(S, m, mine, cs, T)
@@ -280,6 +273,14 @@ def main():
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    gather_ok = None
+    if world > 1 and rank == 0:
+        # the gathered rows reassemble into sequence order (checked once, untimed)
+        from paper_2605_02568_b200.shard import assemble
+
+        parts = [g[:, : api.chunk_rows(dims, cfg, shards[r])].cpu().numpy() for r, g in enumerate(gather_list)]
+        full = assemble(parts, shards, S, cs)
+        gather_ok = bool(np.array_equal(full[:, mine[0]:mine[0] + 1], out_idx[:, :1].cpu().numpy()))
     kinds = {"score": _capi.KIND_SCORE, "select": _capi.KIND_SELECT, "merge": _capi.KIND_MERGE,
              "finalize": _capi.KIND_FINALIZE, "prep": _capi.KIND_PREP}
     kstats = {name: drv.get(kd) for name, kd in kinds.items()}
@@ -379,6 +380,9 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "run_stats": {"dispatch_count": st.dispatch_count, "tiles_skipped_masked": st.tiles_skipped_masked},
+            "multi_gpu": {"rank_work_pairs": loads, "gather_reassembly_ok": gather_ok,
+                          "collectives": "broadcast kc (bf16) from rank 0 + gather int64 [rows,k] to rank 0"
+                          if world > 1 else "none"},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -125,9 +125,10 @@ __device__ __forceinline__ float head_reduce(const float (&v)[64], const float* 
 __global__ void __launch_bounds__(kNumThreads, 1)
     score_tc_kernel(const __grid_constant__ CUtensorMap qmap,
                     const __grid_constant__ CUtensorMap kmap, const __grid_constant__ ScoreTcParams p) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // Align by offsetting the shared array itself (keeps the shared address
+    // space visible to the compiler, so w reads are LDS, not generic loads).
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* q_smem = smem;
     uint8_t* k_smem = smem + kQBytes;
     float* w_smem = reinterpret_cast<float*>(smem + kWOffset);  // [kWBufs][8][64]
@@ -293,10 +294,31 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             if (it.kt_begin < 0) break;
             const uint32_t wb = qiter % kWBufs;
             const float* w_item = w_smem + wb * (kQPerItem * kHeads);
+            // Per-item constants of this thread's 4 queries: output row and
+            // the causal limit (first illegal column, relative to t0).
+            float* orow[kGroups][2];
+            int lim[kGroups][2];
+#pragma unroll
+            for (int g = 0; g < kGroups; ++g) {
+#pragma unroll
+                for (int qq = 0; qq < 2; ++qq) {
+                    const int qi = g * kQPerGroup + qpair * 2 + qq;
+                    const int64_t r = it.r0 + qi;
+                    orow[g][qq] = p.out + (static_cast<int64_t>(it.b) * p.rows + r) * p.ld;
+                    int64_t l = p.cols;
+                    if (p.apply_mask) {
+                        l = t_legal_dev(p.s0 + r, p.ratio) - p.t0;
+                        l = l < 0 ? 0 : (l > p.cols ? p.cols : l);
+                    }
+                    lim[g][qq] = static_cast<int>(l);
+                }
+            }
             mbar_wait(&w_full[wb], (qiter / kWBufs) & 1);
             ++qiter;
+            const int cols = static_cast<int>(p.cols);
             for (int kt = it.kt_begin; kt < it.kt_end; ++kt) {
-                const int64_t j = static_cast<int64_t>(kt) * kBlockKeys + quarter * 32 + lane;
+                const int j = kt * kBlockKeys + quarter * 32 + static_cast<int>(lane);
+#pragma unroll
                 for (int g = 0; g < kGroups; ++g) {
                     const uint32_t a = aiter & 1;
                     mbar_wait(&acc_full[a], (aiter >> 1) & 1);
@@ -309,17 +331,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                         tmem_ld64(row_taddr + a * kUmmaN + (qpair * 2 + qq) * kHeads, v);
                         tmem_ld_wait();
                         const float acc = head_reduce(v, w_item + qi * kHeads);
-                        if (j < p.cols) {
-                            const int64_t r = it.r0 + qi;
-                            const int64_t s = p.s0 + r;
-                            float outv = acc;
-                            const bool legal = !p.apply_mask || (p.t0 + j) < t_legal_dev(s, p.ratio);
-                            if (!legal) {
-                                outv = neg_inf;
-                            } else if (!isfinite(acc)) {
-                                atomicOr(p.nonfinite, 1);
-                            }
-                            p.out[(static_cast<int64_t>(it.b) * p.rows + r) * p.ld + j] = outv;
+                        if (j < cols) {
+                            const bool legal = j < lim[g][qq];
+                            if (legal && !isfinite(acc)) atomicOr(p.nonfinite, 1);
+                            orow[g][qq][j] = legal ? acc : neg_inf;
                         }
                     }
                     tc_fence_before();

@@ -91,6 +91,81 @@ __device__ void bitonic_sort_desc(uint64_t* a, int P) {
     }
 }
 
+// Descending bitonic sort of a[0, P) with P == E * blockDim.x: each thread
+// holds E consecutive elements in registers; strides < E are in-register,
+// strides < 32E go through warp shuffles, and only the strides that cross
+// warps touch shared memory (6 barrier stages for P = 1024 instead of 55).
+template <int E>
+__device__ void bitonic_sort_desc_regs(uint64_t* a, int P) {
+    const int t = threadIdx.x;
+    uint64_t x[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = a[t * E + e];
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride < E) {
+                // compile-time strides keep x[] in registers
+#pragma unroll
+                for (int s = E / 2; s >= 1; s >>= 1) {
+                    if (s != stride) continue;
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const int pe = e ^ s;
+                        if (pe > e) {
+                            const int i = t * E + e;
+                            const bool desc = (i & size) == 0;
+                            const uint64_t lo = x[e], hi = x[pe];
+                            if (desc ? (lo < hi) : (lo > hi)) {
+                                x[e] = hi;
+                                x[pe] = lo;
+                            }
+                        }
+                    }
+                }
+            } else if (stride < 32 * E) {
+                const int lane_x = stride / E;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int i = t * E + e;
+                    const uint64_t other = __shfl_xor_sync(0xffffffffu, x[e], lane_x);
+                    const bool lower = (i & stride) == 0;
+                    const bool desc = (i & size) == 0;
+                    const bool keep_max = lower == desc;
+                    x[e] = keep_max ? (x[e] > other ? x[e] : other) : (x[e] < other ? x[e] : other);
+                }
+            } else {
+                __syncthreads();
+#pragma unroll
+                for (int e = 0; e < E; ++e) a[t * E + e] = x[e];
+                __syncthreads();
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int i = t * E + e;
+                    const uint64_t other = a[i ^ stride];
+                    const bool lower = (i & stride) == 0;
+                    const bool desc = (i & size) == 0;
+                    const bool keep_max = lower == desc;
+                    x[e] = keep_max ? (x[e] > other ? x[e] : other) : (x[e] < other ? x[e] : other);
+                }
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; ++e) a[t * E + e] = x[e];
+    __syncthreads();
+}
+
+__device__ void sort_desc(uint64_t* a, int P) {
+    switch (P / static_cast<int>(blockDim.x)) {
+        case 1: bitonic_sort_desc_regs<1>(a, P); break;
+        case 2: bitonic_sort_desc_regs<2>(a, P); break;
+        case 4: bitonic_sort_desc_regs<4>(a, P); break;
+        case 8: bitonic_sort_desc_regs<8>(a, P); break;
+        default: bitonic_sort_desc(a, P); break;  // P < blockDim
+    }
+}
+
 // Block-parallel search of the bin (counting from the top) holding the
 // kk-th largest element: every thread sums a run of bins, a block scan
 // locates the run, its owner walks it. out3 = {bin, count above, bin count}.
@@ -278,7 +353,7 @@ __device__ void exact_global_select(const float* row, int64_t n, int k, uint64_t
         const int P = pow2_at_least(static_cast<int>(bin_count));
         for (int i = static_cast<int>(bin_count) + threadIdx.x; i < P; i += blockDim.x) cand[i] = 0;
         __syncthreads();
-        bitonic_sort_desc(cand, P);
+        sort_desc(cand, P);
         for (uint32_t i = threadIdx.x; i < kk; i += blockDim.x) buf[above + i] = cand[i];
     }
     __syncthreads();
@@ -467,9 +542,15 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
                 smem_radix_u64(cand, count, static_cast<uint32_t>(take), hist, res, wsum, prefix, pbits);
                 if (threadIdx.x == 0) *counter = 0;
                 __syncthreads();
-                for (int i = threadIdx.x; i < count; i += blockDim.x) {
-                    const uint64_t v = cand[i];
-                    if (top_ge(v, prefix, pbits)) buf[atomicAdd(counter, 1u)] = v;
+                const int countr = (count + 31) & ~31;
+                for (int i = threadIdx.x; i < countr; i += blockDim.x) {
+                    const uint64_t v = i < count ? cand[i] : 0ull;
+                    const bool keep = i < count && top_ge(v, prefix, pbits);
+                    const uint32_t m = __ballot_sync(0xffffffffu, keep);
+                    uint32_t base = 0;
+                    if (lane == 0 && m != 0) base = atomicAdd(counter, __popc(m));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (keep) buf[base + __popc(m & ((1u << lane) - 1u))] = v;
                 }
             } else {
                 for (int i = threadIdx.x; i < count; i += blockDim.x) buf[i] = cand[i];
@@ -482,7 +563,7 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
         const int P = pow2_at_least(take);
         for (int i = take + threadIdx.x; i < P; i += blockDim.x) buf[i] = 0;
         __syncthreads();
-        bitonic_sort_desc(buf, P);
+        sort_desc(buf, P);
     }
 
     float* ov = p.out_val + (static_cast<int64_t>(b) * p.rows + row_id) * p.out_ld;
