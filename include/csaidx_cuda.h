@@ -70,6 +70,13 @@ int csaidx_engine_destroy(csaidx_engine* e);
 int csaidx_engine_set_stream(csaidx_engine* e, void* stream);
 int csaidx_engine_use_own_stream(csaidx_engine* e);
 int csaidx_engine_get_stream(csaidx_engine* e, void** stream);
+/* Copy lanes for overlapping host transfers with compute: subsequent calls
+ * enqueue on lane 0 (the main stream set above), 1 (copy-in) or 2
+ * (copy-out). signal records event `slot` (0..63) on the current lane;
+ * await makes the current lane wait for the slot's latest signal. */
+int csaidx_engine_use_lane(csaidx_engine* e, int lane);
+int csaidx_engine_signal(csaidx_engine* e, int slot);
+int csaidx_engine_await(csaidx_engine* e, int slot);
 int csaidx_engine_num_sms(csaidx_engine* e, int* num_sms);
 /* Synchronizes the stream, then reports (and clears) latched data errors. */
 int csaidx_engine_check(csaidx_engine* e);
@@ -92,6 +99,10 @@ int csaidx_engine_reset_stats(csaidx_engine* e);
 /* Rows whose select took the exact global-memory fallback (the sampled
  * threshold mispredicted) since the last reset; synchronizes. */
 int csaidx_engine_select_fallbacks(csaidx_engine* e, int64_t* rows, int reset);
+/* Profiling hook: when non-NULL, select launches of batch 0 write per-row
+ * clock64 stamps [rows][8] = {start, threshold, filtered, sorted, n} into
+ * this device buffer. */
+int csaidx_engine_set_select_probe(csaidx_engine* e, long long* device_clocks);
 
 /* Stream-ordered device memory from a cached pool. */
 int csaidx_cuda_alloc(csaidx_engine* e, size_t bytes, void** ptr);

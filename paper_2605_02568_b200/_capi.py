@@ -86,6 +86,10 @@ CUDA_SYMBOLS = {
     "csaidx_engine_kernel_stats": (c_int, [c_void_p, c_int, POINTER(c_int64), POINTER(ctypes.c_double)]),
     "csaidx_engine_reset_stats": (c_int, [c_void_p]),
     "csaidx_engine_select_fallbacks": (c_int, [c_void_p, POINTER(c_int64), c_int]),
+    "csaidx_engine_set_select_probe": (c_int, [c_void_p, c_void_p]),
+    "csaidx_engine_use_lane": (c_int, [c_void_p, c_int]),
+    "csaidx_engine_signal": (c_int, [c_void_p, c_int]),
+    "csaidx_engine_await": (c_int, [c_void_p, c_int]),
     "csaidx_cuda_alloc": (c_int, [c_void_p, c_size_t, POINTER(c_void_p)]),
     "csaidx_cuda_free": (c_int, [c_void_p, c_void_p]),
     "csaidx_cuda_copy": (c_int, [c_void_p, c_void_p, c_void_p, c_size_t]),

@@ -82,6 +82,12 @@ struct csaidx_engine {
     };
     std::vector<Pending> pending;
     std::vector<cudaEvent_t> event_pool;
+    // copy lanes for overlapping host transfers with compute (created lazily)
+    cudaStream_t lanes[3] = {nullptr, nullptr, nullptr};  // [0] = main (== stream when lane 0 active)
+    cudaStream_t main_stream = nullptr;
+    int lane = 0;
+    cudaEvent_t slots[64] = {};
+    long long* select_probe = nullptr;  // optional per-row phase clocks (profiling)
 };
 
 namespace {
@@ -187,6 +193,7 @@ int csaidx_engine_create(int device, csaidx_engine** out) {
     e->num_sms = prop.multiProcessorCount;
     CSAIDX_CUDA_TRY(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     e->stream = e->own_stream;
+    e->main_stream = e->stream;
     // flags [0, kNumFlags) + the score kernel's self-resetting work counters
     CSAIDX_CUDA_TRY(cudaMalloc(&e->flags, 2 * kNumFlags * sizeof(int)), "cudaMalloc(flags)");
     CSAIDX_CUDA_TRY(cudaMemset(e->flags, 0, 2 * kNumFlags * sizeof(int)), "cudaMemset(flags)");
@@ -210,6 +217,10 @@ int csaidx_engine_destroy(csaidx_engine* e) {
     }
     for (cudaEvent_t ev : e->event_pool) cudaEventDestroy(ev);
     if (e->flags) cudaFree(e->flags);
+    for (int i = 1; i < 3; ++i)
+        if (e->lanes[i]) cudaStreamDestroy(e->lanes[i]);
+    for (cudaEvent_t ev : e->slots)
+        if (ev) cudaEventDestroy(ev);
     if (e->own_stream) cudaStreamDestroy(e->own_stream);
     delete e;
     return CSAIDX_OK;
@@ -218,12 +229,44 @@ int csaidx_engine_destroy(csaidx_engine* e) {
 int csaidx_engine_set_stream(csaidx_engine* e, void* stream) {
     if (e == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null engine");
     e->stream = static_cast<cudaStream_t>(stream);
+    e->main_stream = e->stream;
+    e->lane = 0;
+    return CSAIDX_OK;
+}
+
+int csaidx_engine_use_lane(csaidx_engine* e, int lane) {
+    if (int rc = set_device(e)) return rc;
+    if (lane < 0 || lane > 2) return fail(CSAIDX_INVALID_ARGUMENT, "lane must be 0 (main), 1 (copy-in) or 2 (copy-out)");
+    if (e->lane == 0) e->main_stream = e->stream;
+    if (lane > 0 && e->lanes[lane] == nullptr)
+        CSAIDX_CUDA_TRY(cudaStreamCreateWithFlags(&e->lanes[lane], cudaStreamNonBlocking), "cudaStreamCreate(lane)");
+    e->stream = lane == 0 ? e->main_stream : e->lanes[lane];
+    e->lane = lane;
+    return CSAIDX_OK;
+}
+
+int csaidx_engine_signal(csaidx_engine* e, int slot) {
+    if (int rc = set_device(e)) return rc;
+    if (slot < 0 || slot >= 64) return fail(CSAIDX_INVALID_ARGUMENT, "event slot out of range");
+    if (e->slots[slot] == nullptr)
+        CSAIDX_CUDA_TRY(cudaEventCreateWithFlags(&e->slots[slot], cudaEventDisableTiming), "cudaEventCreate");
+    CSAIDX_CUDA_TRY(cudaEventRecord(e->slots[slot], e->stream), "cudaEventRecord");
+    return CSAIDX_OK;
+}
+
+int csaidx_engine_await(csaidx_engine* e, int slot) {
+    if (int rc = set_device(e)) return rc;
+    if (slot < 0 || slot >= 64) return fail(CSAIDX_INVALID_ARGUMENT, "event slot out of range");
+    if (e->slots[slot] == nullptr) return CSAIDX_OK;  // never signalled: nothing to wait for
+    CSAIDX_CUDA_TRY(cudaStreamWaitEvent(e->stream, e->slots[slot], 0), "cudaStreamWaitEvent");
     return CSAIDX_OK;
 }
 
 int csaidx_engine_use_own_stream(csaidx_engine* e) {
     if (e == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null engine");
     e->stream = e->own_stream;
+    e->main_stream = e->stream;
+    e->lane = 0;
     return CSAIDX_OK;
 }
 
@@ -242,6 +285,10 @@ int csaidx_engine_num_sms(csaidx_engine* e, int* num_sms) {
 int csaidx_engine_check(csaidx_engine* e) {
     if (int rc = set_device(e)) return rc;
     CSAIDX_CUDA_TRY(cudaStreamSynchronize(e->stream), "cudaStreamSynchronize");
+    for (int i = 0; i < 3; ++i) {
+        cudaStream_t s = i == 0 ? e->main_stream : e->lanes[i];
+        if (s != nullptr && s != e->stream) CSAIDX_CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize(lane)");
+    }
     int h[kNumFlags];
     CSAIDX_CUDA_TRY(cudaMemcpy(h, e->flags, sizeof(h), cudaMemcpyDeviceToHost), "flags D2H");
     bool any = false;
@@ -285,6 +332,12 @@ int csaidx_engine_kernel_stats(csaidx_engine* e, int kind, int64_t* launches, do
     e->pending.clear();
     if (launches) *launches = e->launches[kind];
     if (total_ms) *total_ms = e->total_ms[kind];
+    return CSAIDX_OK;
+}
+
+int csaidx_engine_set_select_probe(csaidx_engine* e, long long* device_clocks) {
+    if (e == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null engine");
+    e->select_probe = device_clocks;
     return CSAIDX_OK;
 }
 
@@ -493,6 +546,7 @@ int csaidx_cuda_select(csaidx_engine* e, const float* scores, int64_t batch, int
     p.out_idx = cand_idx;
     p.out_ld = cand_ld;
     p.fallbacks = e->flags + kNumFlags + 2;
+    p.phase_clk = e->select_probe;
     LaunchScope ls(e, CSAIDX_KIND_SELECT);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_select(p, e->stream), "select");
     return CSAIDX_OK;

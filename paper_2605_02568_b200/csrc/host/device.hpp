@@ -6,6 +6,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <mutex>
 #include <vector>
 
@@ -93,11 +94,18 @@ struct ChunkPlan {
 
 ChunkPlan plan_chunks(const ProblemDims& dims, const TileConfig& tile, const std::vector<int64_t>* starts);
 
+// Per-chunk callbacks around run_plan's main-lane work (used to overlap host
+// transfers of neighbouring chunks on the engine's copy lanes).
+struct ChunkHooks {
+    std::function<void(size_t)> before;  // before chunk c's first kernel
+    std::function<void(size_t)> after;   // after chunk c's finalize
+};
+
 // process_query_tile (driver.cpp:36-106) for every chunk of the plan, on
 // device. Results land in device [B, out_rows, k] int64 / fp32.
 void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, const DriverConfig& config,
               const ChunkPlan& plan, int64_t* out_idx, float* out_val, int64_t out_rows, MemoryLedger& ledger,
-              RunStats& stats);
+              RunStats& stats, const ChunkHooks& hooks = {});
 
 // Materialized path on device (driver.cpp:167-192).
 void run_materialize_device(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, int mode, int kernel,

@@ -55,7 +55,7 @@ ChunkPlan plan_chunks(const ProblemDims& dims, const TileConfig& tile, const std
 
 void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, const DriverConfig& config,
               const ChunkPlan& plan, int64_t* out_idx, float* out_val, int64_t out_rows, MemoryLedger& ledger,
-              RunStats& stats) {
+              RunStats& stats, const ChunkHooks& hooks) {
     const int64_t B = dims.batch, k = dims.top_k, T = dims.key_blocks;
     if (std::min(k, plan.ct) > csaidx_cuda_select_capacity() || k > csaidx_cuda_select_capacity())
         throw std::invalid_argument("top_k exceeds the GPU selection capacity (4096)");
@@ -77,6 +77,7 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
     for (size_t c = 0; c < plan.starts.size(); ++c) {
         const int64_t s0 = plan.starts[c];
         const int64_t rows = std::min(plan.cs, dims.seq_len - s0);
+        if (hooks.before) hooks.before(c);
         LedgerCharge buffer_charge(ledger, "topk_buffer", run_buffer_bytes(B, rows, k));
         check(csaidx_cuda_fill_sentinel(e, run_v.as<float>(), run_i.as<int32_t>(), B * rows * k));
         bool first = true;
@@ -120,6 +121,7 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
         check(csaidx_cuda_finalize(e, run_v.as<float>(), run_i.as<int32_t>(), B, rows, s0, dims.ratio, k,
                                    config.ablation == Ablation::none ? 1 : 0, out_idx, out_val, out_rows,
                                    plan.out_row0[c]));
+        if (hooks.after) hooks.after(c);
     }
     check(csaidx_engine_check(e));
 }
@@ -179,17 +181,81 @@ void run_chunked_rows_view(const HostView& in, const ProblemDims& dims, const Dr
     }
     if (out_rows < need) throw std::invalid_argument("run_chunked: out_rows too small for the chunk list");
     const int kcode = kernel_code(config.kernel);
+    const int dtype = operand_dtype(dims, mode_code(config.mode), kcode);
+    const bool strict = gpu::options().strict_bf16;
     std::lock_guard<std::mutex> lock(engine_mutex());
     csaidx_engine* e = engine();
-    const StagedOperands ops(e, in, dims, operand_dtype(dims, mode_code(config.mode), kcode),
-                             gpu::options().strict_bf16, starts != nullptr ? &ranges : nullptr);
-    const size_t n = static_cast<size_t>(dims.batch * out_rows * dims.top_k);
+
+    // Three-lane pipeline: lane 1 copies chunk c+1's q / w rows in (and rounds
+    // q to bf16) while lane 0 computes chunk c and lane 2 copies chunk c-1's
+    // indices / values out. With pinned host buffers the PCIe traffic hides
+    // behind the kernels; pageable buffers still work (copies then block).
+    const int64_t B = dims.batch, k = dims.top_k, qrow = dims.heads * dims.head_dim;
+    const size_t esz = dtype == CSAIDX_DTYPE_BF16 ? 2 : 4;
+    DeviceBuffer q(e, static_cast<size_t>(dims.q_elems()) * esz), kc(e, static_cast<size_t>(dims.kc_elems()) * esz),
+        w(e, static_cast<size_t>(dims.w_elems()) * sizeof(float));
+    DeviceBuffer slab[2];
+    if (dtype == CSAIDX_DTYPE_BF16) {
+        for (auto& sb : slab) sb = DeviceBuffer(e, static_cast<size_t>(plan.cs * qrow) * sizeof(float));
+    }
+    const size_t n = static_cast<size_t>(B * out_rows * k);
     DeviceBuffer idx(e, n * sizeof(int64_t)), val(e, n * sizeof(float));
+    const DeviceOps ops{q.as<void>(), kc.as<void>(), w.as<float>(), dtype};
+    constexpr int kMainLane = 0, kInLane = 1, kOutLane = 2;
+    auto upload_chunk = [&](size_t c) {
+        const int64_t s0 = plan.starts[c], rows = std::min(plan.cs, dims.seq_len - s0);
+        for (int64_t b = 0; b < B; ++b) {
+            const int64_t qoff = (b * dims.seq_len + s0) * qrow, woff = (b * dims.seq_len + s0) * dims.heads;
+            if (dtype == CSAIDX_DTYPE_BF16) {
+                DeviceBuffer& sb = slab[c % 2];
+                check(csaidx_cuda_copy(e, sb.as<void>(), in.q + qoff, static_cast<size_t>(rows * qrow) * sizeof(float)));
+                check(csaidx_cuda_to_bf16(e, sb.as<float>(), q.as<uint16_t>() + qoff, rows * qrow, strict ? 1 : 0));
+            } else {
+                check(csaidx_cuda_copy(e, q.as<float>() + qoff, in.q + qoff,
+                                       static_cast<size_t>(rows * qrow) * sizeof(float)));
+            }
+            check(csaidx_cuda_copy(e, w.as<float>() + woff, in.w + woff,
+                                   static_cast<size_t>(rows * dims.heads) * sizeof(float)));
+        }
+        check(csaidx_engine_signal(e, static_cast<int>(c % 32)));
+    };
+    ChunkHooks hooks;
+    hooks.before = [&](size_t c) {
+        check(csaidx_engine_use_lane(e, kInLane));
+        if (c == 0) {
+            if (dtype == CSAIDX_DTYPE_BF16) {
+                DeviceBuffer tmp(e, static_cast<size_t>(dims.kc_elems()) * sizeof(float));
+                tmp.upload(in.kc, static_cast<size_t>(dims.kc_elems()) * sizeof(float));
+                check(csaidx_cuda_to_bf16(e, tmp.as<float>(), kc.as<uint16_t>(), dims.kc_elems(), strict ? 1 : 0));
+            } else {
+                kc.upload(in.kc, static_cast<size_t>(dims.kc_elems()) * sizeof(float));
+            }
+            upload_chunk(0);
+        }
+        if (c + 1 < plan.starts.size()) upload_chunk(c + 1);
+        check(csaidx_engine_use_lane(e, kMainLane));
+        check(csaidx_engine_await(e, static_cast<int>(c % 32)));
+    };
+    hooks.after = [&](size_t c) {
+        check(csaidx_engine_signal(e, static_cast<int>(32 + c % 32)));
+        check(csaidx_engine_use_lane(e, kOutLane));
+        check(csaidx_engine_await(e, static_cast<int>(32 + c % 32)));
+        const int64_t rows = std::min(plan.cs, dims.seq_len - plan.starts[c]);
+        for (int64_t b = 0; b < B; ++b) {
+            const int64_t off = (b * out_rows + plan.out_row0[c]) * k;
+            check(csaidx_cuda_copy(e, host_idx + off, idx.as<int64_t>() + off, static_cast<size_t>(rows * k) * 8));
+            check(csaidx_cuda_copy(e, host_val + off, val.as<float>() + off, static_cast<size_t>(rows * k) * 4));
+        }
+        check(csaidx_engine_use_lane(e, kMainLane));
+    };
     RunStats stats;
-    run_plan(e, ops.ops(), dims, config, plan, idx.as<int64_t>(), val.as<float>(), out_rows, ledger, stats);
-    idx.download(host_idx, n * sizeof(int64_t));
-    val.download(host_val, n * sizeof(float));
-    check(csaidx_engine_check(e));
+    try {
+        run_plan(e, ops, dims, config, plan, idx.as<int64_t>(), val.as<float>(), out_rows, ledger, stats, hooks);
+    } catch (...) {
+        csaidx_engine_use_lane(e, kMainLane);
+        csaidx_engine_check(e);  // drain every lane before the buffers go away
+        throw;
+    }
     if (stats_out != nullptr) *stats_out = stats;
 }
 

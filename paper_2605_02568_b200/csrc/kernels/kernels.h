@@ -61,6 +61,7 @@ struct SelectParams {
     int32_t* out_idx;
     int64_t out_ld;
     int* fallbacks;       // rows that took the exact global fallback (telemetry)
+    long long* phase_clk; // optional [rows * 8] clock64 stamps per phase (profiling)
 };
 
 // ------------------------------------------------------------------ merge

@@ -9,15 +9,15 @@
 // order (topk.hpp:23-26).
 //
 // Fast path (one streaming pass over the row):
-//   1. sample: evenly spaced 128-byte lines (<= 1/16 of the row); one
-//      histogram below the sample's common key prefix picks a threshold
-//      expected to keep ~2k entries of the row;
+//   1. sample: evenly spaced 128-byte lines (<= 1/16 of the row); two
+//      histogram passes below the sample's common key prefix pick a
+//      threshold expected to keep ~1.5k entries of the row;
 //   2. filter: the row is streamed once (4 x float4 per thread in flight);
 //      survivors are appended to a shared candidate list with one warp scan
 //      and one shared atomic per warp;
-//   3. if the list holds between k and its capacity, the exact k-th largest
-//      composite is found by shared-memory radix select (unique keys, no tie
-//      bookkeeping); the k survivors are bitonic-sorted and written.
+//   3. if the list holds between k and its capacity, every candidate is
+//      sorted (unique composites: a total order) by a register/shuffle
+//      bitonic sort and the first k are written.
 // When the sample mispredicts (fewer than k or more than capacity survivors)
 // the row falls back to an exact MSB-first radix select over global memory
 // with index-ordered tie collection. Rows with n <= capacity skip sampling.
@@ -52,7 +52,7 @@ __host__ __device__ inline int pow2_at_least(int x) {
 
 __host__ __device__ inline Layout layout_for(int k) {
     Layout l;
-    int c = pow2_at_least(4 * k);
+    int c = pow2_at_least(3 * k);
     l.cand_cap = c < 2048 ? 2048 : (c > kMaxCand ? kMaxCand : c);
     l.buf_cap = pow2_at_least(k);
     return l;
@@ -202,63 +202,6 @@ __device__ void find_bin(const uint32_t* hist, int nbins, uint32_t kk, uint32_t*
     __syncthreads();
 }
 
-// kk-th largest of the unique 64-bit values a[0, n) in shared memory:
-// returns (prefix, pbits) such that exactly kk values have top pbits >= prefix.
-__device__ void smem_radix_u64(const uint64_t* a, int n, uint32_t kk, uint32_t* hist, uint32_t* res,
-                               uint32_t* wsum, uint64_t& prefix_out, int& pbits_out) {
-    // Start below the common prefix of min and max: candidates are the top
-    // few percent of a row and share their leading key bits.
-    __shared__ unsigned long long s_mm[2];
-    if (threadIdx.x == 0) {
-        s_mm[0] = ~0ull;
-        s_mm[1] = 0ull;
-    }
-    __syncthreads();
-    unsigned long long mn = ~0ull, mx = 0ull;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        mn = min(mn, static_cast<unsigned long long>(a[i]));
-        mx = max(mx, static_cast<unsigned long long>(a[i]));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    }
-    if ((threadIdx.x & 31) == 0) {
-        atomicMin(&s_mm[0], mn);
-        atomicMax(&s_mm[1], mx);
-    }
-    __syncthreads();
-    const uint64_t lo = s_mm[0], hi = s_mm[1];
-    int pbits = lo == hi ? 64 : __clzll(static_cast<long long>(lo ^ hi));
-    uint64_t prefix = pbits == 0 ? 0ull : (pbits == 64 ? lo : (lo >> (64 - pbits)));
-    while (pbits < 64) {
-        const int wbits = 64 - pbits < 11 ? 64 - pbits : 11;
-        const int shift = 64 - pbits - wbits;
-        for (int i = threadIdx.x; i < kBins; i += blockDim.x) hist[i] = 0;
-        __syncthreads();
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const uint64_t v = a[i];
-            if (pbits == 0 || (v >> (64 - pbits)) == prefix)
-                atomicAdd(&hist[static_cast<uint32_t>(v >> shift) & ((1u << wbits) - 1u)], 1u);
-        }
-        __syncthreads();
-        find_bin(hist, 1 << wbits, kk, res, wsum);
-        const uint32_t bin = res[0], above = res[1], cnt = res[2];
-        __syncthreads();
-        kk -= above;
-        prefix = (pbits == 0 ? 0ull : (prefix << wbits)) | bin;
-        pbits += wbits;
-        if (cnt == kk) break;  // the whole bucket is in; exactly kk remain
-    }
-    prefix_out = prefix;
-    pbits_out = pbits;
-}
-
-__device__ __forceinline__ bool top_ge(uint64_t v, uint64_t prefix, int pbits) {
-    return pbits >= 64 ? v >= prefix : (v >> (64 - pbits)) >= prefix;
-}
-
 // ------------------------------------------------------------------ fallback
 // Exact MSB-first radix select over global memory (any n, any ties): the
 // selected composites (unsorted) land in buf[0, k).
@@ -385,6 +328,9 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
     const int take = static_cast<int>(n < k ? n : k);
     const int lane = threadIdx.x & 31;
 
+    const uint64_t* result = buf;  // sorted selection, best first
+    long long* clk = p.phase_clk != nullptr && threadIdx.x == 0 && b == 0 ? p.phase_clk + row_id * 8 : nullptr;
+    if (clk) clk[0] = clock64();
     if (take > 0) {
         int count = -1;  // candidates in cand[], or -1 -> fallback
         if (n <= L.cand_cap) {
@@ -431,8 +377,11 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
                 atomicMax(&res[7], kmax);
             }
             __syncthreads();
+            if (clk) clk[5] = clock64();
             const int ns = 32 * nseg;
-            const int target = (2 * k < (L.cand_cap * 3) / 4) ? 2 * k : (L.cand_cap * 3) / 4;
+            // ~1.5k survivors: enough margin that < k is a rare miss, few
+            // enough that k = 1024 rows finish in a 2048-entry register sort
+            const int target = (3 * k / 2 < (L.cand_cap * 3) / 4) ? 3 * k / 2 : (L.cand_cap * 3) / 4;
             int r = static_cast<int>((static_cast<int64_t>(target) * ns) / n);
             if (r < 1) r = 1;
             // Two 11-bit histogram passes below the sample's common key
@@ -465,6 +414,7 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
             }
             const uint32_t tau = pbits >= 32 ? prefix : (prefix << (32 - pbits));
 
+            if (clk) clk[1] = clock64();
             // 2. stream the row once; keep entries with key >= tau (a plain
             //    float compare: ord_key is monotone and folds -0.0 onto +0.0
             //    like the float order)
@@ -534,44 +484,40 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
             __syncthreads();
         }
 
+        if (clk) clk[2] = clock64();
         if (count >= 0) {
-            // 3. exact k-th largest composite among the candidates
-            if (count > take) {
-                uint64_t prefix;
-                int pbits;
-                smem_radix_u64(cand, count, static_cast<uint32_t>(take), hist, res, wsum, prefix, pbits);
-                if (threadIdx.x == 0) *counter = 0;
-                __syncthreads();
-                const int countr = (count + 31) & ~31;
-                for (int i = threadIdx.x; i < countr; i += blockDim.x) {
-                    const uint64_t v = i < count ? cand[i] : 0ull;
-                    const bool keep = i < count && top_ge(v, prefix, pbits);
-                    const uint32_t m = __ballot_sync(0xffffffffu, keep);
-                    uint32_t base = 0;
-                    if (lane == 0 && m != 0) base = atomicAdd(counter, __popc(m));
-                    base = __shfl_sync(0xffffffffu, base, 0);
-                    if (keep) buf[base + __popc(m & ((1u << lane) - 1u))] = v;
-                }
-            } else {
-                for (int i = threadIdx.x; i < count; i += blockDim.x) buf[i] = cand[i];
-            }
+            // 3. sort every candidate (unique composites, so the order is
+            //    total) and keep the first `take`: ~1.5k entries, one
+            //    register/shuffle bitonic sort with a handful of barriers
+            const int P = pow2_at_least(count);
+            for (int i = count + threadIdx.x; i < P; i += blockDim.x) cand[i] = 0;
             __syncthreads();
+            if (clk) {
+                clk[6] = count;
+                clk[7] = clock64();
+            }
+            sort_desc(cand, P);
+            result = cand;
         } else {
             if (threadIdx.x == 0 && p.fallbacks != nullptr) atomicAdd(p.fallbacks, 1);
             exact_global_select(row, n, take, buf, cand, L.cand_cap, hist, wtot, res, wsum);
+            const int P = pow2_at_least(take);
+            for (int i = take + threadIdx.x; i < P; i += blockDim.x) buf[i] = 0;
+            __syncthreads();
+            sort_desc(buf, P);
         }
-        const int P = pow2_at_least(take);
-        for (int i = take + threadIdx.x; i < P; i += blockDim.x) buf[i] = 0;
-        __syncthreads();
-        sort_desc(buf, P);
     }
 
+    if (clk) {
+        clk[3] = clock64();
+        clk[4] = n;
+    }
     float* ov = p.out_val + (static_cast<int64_t>(b) * p.rows + row_id) * p.out_ld;
     int32_t* oi = p.out_idx + (static_cast<int64_t>(b) * p.rows + row_id) * p.out_ld;
     const float neg_inf = -__int_as_float(0x7f800000);
     for (int e = threadIdx.x; e < p.width; e += blockDim.x) {
         if (e < take) {
-            const uint64_t c = buf[e];
+            const uint64_t c = result[e];
             ov[e] = ord_key_to_float(static_cast<uint32_t>(c >> 32));
             oi[e] = static_cast<int32_t>(composite_col(c) + p.t0);
         } else {

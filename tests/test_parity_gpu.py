@@ -117,6 +117,31 @@ def test_c1_chunked_equals_materialize_bitwise(c1):
     assert np.array_equal(via.indices, ref.indices)
 
 
+def test_chunk_subset_entry_matches_full_run(c1):
+    """csaidx_host_run_chunked_rows (pinned buffers, copy lanes overlapped
+    with compute) and csaidx_device_run_chunked on a shard of chunks give the
+    full run's rows."""
+    import torch
+
+    inputs, dims, _ = c1
+    cfg = api.DriverConfig(tile=api.TileConfig(512, 1024))
+    full, _ = api.run_chunked(inputs, dims, cfg)
+    starts = [3584, 0, 2048]
+    rows = api.chunk_rows(dims, cfg, starts)
+    q = torch.from_numpy(inputs.q).pin_memory()
+    kc = torch.from_numpy(inputs.kc).pin_memory()
+    w = torch.from_numpy(inputs.w).pin_memory()
+    oi = torch.empty((1, rows, dims.top_k), dtype=torch.int64).pin_memory()
+    ov = torch.empty((1, rows, dims.top_k), dtype=torch.float32).pin_memory()
+    api.run_chunked_rows(q, kc, w, dims, cfg, starts, oi, ov)
+    expect = np.concatenate([full.indices[:, s:s + 512] for s in starts], axis=1)
+    assert np.array_equal(oi.numpy(), expect)
+    qd = q.cuda().to(torch.bfloat16)
+    kd = kc.cuda().to(torch.bfloat16)
+    di, dv, _ = api.run_chunked_device(qd, kd, w.cuda(), dims, cfg, starts)
+    assert np.array_equal(di.cpu().numpy(), expect)
+
+
 def test_ablations_follow_reference_semantics(orc):
     # acceptance.cpp:339-380 directions at a small V4-like shape
     inputs, dims, (q, kc, w) = inputs_for(orc, 1, 2048, 4, 8, 64, 64, 1)
