@@ -202,6 +202,71 @@ __device__ void find_bin(const uint32_t* hist, int nbins, uint32_t kk, uint32_t*
     __syncthreads();
 }
 
+// Exactly the kk largest of the unique 64-bit values a[0, n) (shared memory)
+// into dst[0, kk), unordered. MSB-first radix select starting below the
+// common prefix of the list's min and max (candidates are the top few percent
+// of a row and share their leading bits); usually two 11-bit passes.
+__device__ void smem_take_top(const uint64_t* a, int n, uint32_t kk, uint64_t* dst, uint32_t* hist, uint32_t* res,
+                              uint32_t* wsum, uint32_t* counter) {
+    __shared__ unsigned long long s_mm[2];
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        s_mm[0] = ~0ull;
+        s_mm[1] = 0ull;
+        *counter = 0;
+    }
+    __syncthreads();
+    unsigned long long mn = ~0ull, mx = 0ull;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        mn = min(mn, static_cast<unsigned long long>(a[i]));
+        mx = max(mx, static_cast<unsigned long long>(a[i]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) {
+        atomicMin(&s_mm[0], mn);
+        atomicMax(&s_mm[1], mx);
+    }
+    __syncthreads();
+    const uint64_t lo = s_mm[0], hi = s_mm[1];
+    int pbits = lo == hi ? 64 : __clzll(static_cast<long long>(lo ^ hi));
+    uint64_t prefix = pbits == 0 ? 0ull : (pbits == 64 ? lo : (lo >> (64 - pbits)));
+    while (pbits < 64) {
+        const int wbits = 64 - pbits < 11 ? 64 - pbits : 11;
+        const int shift = 64 - pbits - wbits;
+        for (int i = threadIdx.x; i < kBins; i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const uint64_t v = a[i];
+            if (pbits == 0 || (v >> (64 - pbits)) == prefix)
+                atomicAdd(&hist[static_cast<uint32_t>(v >> shift) & ((1u << wbits) - 1u)], 1u);
+        }
+        __syncthreads();
+        find_bin(hist, 1 << wbits, kk, res, wsum);
+        const uint32_t bin = res[0], above = res[1], cnt = res[2];
+        __syncthreads();
+        kk -= above;
+        prefix = (pbits == 0 ? 0ull : (prefix << wbits)) | bin;
+        pbits += wbits;
+        if (cnt == kk) break;  // the whole bucket is in: exactly kk remain
+    }
+    // keep the values whose top pbits are >= prefix (exactly the requested count)
+    const int nr = (n + 31) & ~31;
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+        const uint64_t v = i < n ? a[i] : 0ull;
+        const bool keep = i < n && (pbits >= 64 ? v >= prefix : (v >> (64 - pbits)) >= prefix);
+        const uint32_t m = __ballot_sync(0xffffffffu, keep);
+        uint32_t base = 0;
+        if (lane == 0 && m != 0) base = atomicAdd(counter, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) dst[base + __popc(m & ((1u << lane) - 1u))] = v;
+    }
+    __syncthreads();
+}
+
 // ------------------------------------------------------------------ fallback
 // Exact MSB-first radix select over global memory (any n, any ties): the
 // selected composites (unsorted) land in buf[0, k).
@@ -379,9 +444,9 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
             __syncthreads();
             if (clk) clk[5] = clock64();
             const int ns = 32 * nseg;
-            // ~1.5k survivors: enough margin that < k is a rare miss, few
-            // enough that k = 1024 rows finish in a 2048-entry register sort
-            const int target = (3 * k / 2 < (L.cand_cap * 3) / 4) ? 3 * k / 2 : (L.cand_cap * 3) / 4;
+            // ~2k survivors: a comfortable margin over k (misses -> the slow
+            // exact fallback) while the shared list stays at <= 4k entries
+            const int target = (2 * k < (L.cand_cap * 3) / 4) ? 2 * k : (L.cand_cap * 3) / 4;
             int r = static_cast<int>((static_cast<int64_t>(target) * ns) / n);
             if (r < 1) r = 1;
             // Two 11-bit histogram passes below the sample's common key
@@ -452,16 +517,17 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
                 if (lane == 31) base = atomicAdd(counter, incl);
                 base = __shfl_sync(0xffffffffu, base, 31);
                 uint32_t pos = base + incl - c;
-#pragma unroll
-                for (int u = 0; u < kUnroll; ++u) {
-                    const float e[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-                    for (int x = 0; x < 4; ++x) {
-                        if (m & (1u << (4 * u + x))) {
-                            if (pos < cap) cand[pos] = composite(ord_key(e[x]), 4 * (it + u * blockDim.x) + x);
-                            ++pos;
-                        }
-                    }
+                // Survivors are ~2% of entries: walk only the set bits (the
+                // warp iterates max-popc times, usually once or twice) and
+                // pick the element with selects, not an unrolled 16-way body.
+                while (m != 0) {
+                    const int bit = __ffs(m) - 1;
+                    m &= m - 1;
+                    const int u = bit >> 2, x = bit & 3;
+                    const float4 vv = u == 0 ? v[0] : (u == 1 ? v[1] : (u == 2 ? v[2] : v[3]));
+                    const float e = x == 0 ? vv.x : (x == 1 ? vv.y : (x == 2 ? vv.z : vv.w));
+                    if (pos < cap) cand[pos] = composite(ord_key(e), 4 * (it + u * blockDim.x) + x);
+                    ++pos;
                 }
             }
             if (threadIdx.x < 32) {  // the < 4 entries past the last float4
@@ -486,18 +552,21 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
 
         if (clk) clk[2] = clock64();
         if (count >= 0) {
-            // 3. sort every candidate (unique composites, so the order is
-            //    total) and keep the first `take`: ~1.5k entries, one
-            //    register/shuffle bitonic sort with a handful of barriers
-            const int P = pow2_at_least(count);
-            for (int i = count + threadIdx.x; i < P; i += blockDim.x) cand[i] = 0;
+            // 3. exactly `take` of the (unique) candidates by shared-memory
+            //    radix select, then one register/shuffle bitonic sort
+            if (count > take) {
+                smem_take_top(cand, count, static_cast<uint32_t>(take), buf, hist, res, wsum, counter);
+            } else {
+                for (int i = threadIdx.x; i < count; i += blockDim.x) buf[i] = cand[i];
+            }
+            const int P = pow2_at_least(take);
+            for (int i = take + threadIdx.x; i < P; i += blockDim.x) buf[i] = 0;
             __syncthreads();
             if (clk) {
                 clk[6] = count;
                 clk[7] = clock64();
             }
-            sort_desc(cand, P);
-            result = cand;
+            sort_desc(buf, P);
         } else {
             if (threadIdx.x == 0 && p.fallbacks != nullptr) atomicAdd(p.fallbacks, 1);
             exact_global_select(row, n, take, buf, cand, L.cand_cap, hist, wtot, res, wsum);
