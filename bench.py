@@ -255,6 +255,7 @@ def main():
     torch.cuda.reset_peak_memory_stats()
     drv.reset()
     drv.select_fallbacks(reset=True)
+    drv.candidate_hits(reset=True)
     drv.profiling(True)
     clocks = ClockSampler(local)
     clocks.start()
@@ -299,6 +300,7 @@ def main():
     select_gbs = (pairs_mine * 4 * args.steps) / (sel_ms / 1000.0) / 1e9 if sel_ms > 0 else None
     _, drv_peak = drv.mem()
     fallbacks = drv.select_fallbacks()
+    cand_hits = drv.candidate_hits()
     hbm_peak = torch.cuda.max_memory_allocated() + drv_peak
     st = stats_box["st"]
 
@@ -375,6 +377,7 @@ def main():
             "kernels_ms_per_step": {n: v[1] / args.steps for n, v in kstats.items()},
             "select_gbs_one_pass": select_gbs,
             "select_fallback_rows": fallbacks,
+            "select_prefilter_rows": cand_hits,
             "gpu_launches": launches,
             "clocks": clk,
             "cpu_baseline": cpu,

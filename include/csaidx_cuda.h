@@ -99,6 +99,9 @@ int csaidx_engine_reset_stats(csaidx_engine* e);
 /* Rows whose select took the exact global-memory fallback (the sampled
  * threshold mispredicted) since the last reset; synchronizes. */
 int csaidx_engine_select_fallbacks(csaidx_engine* e, int64_t* rows, int reset);
+/* Rows the select finished from a fused pre-filter candidate bitmap
+ * (csaidx_cuda_select_from_candidates) since the last reset; synchronizes. */
+int csaidx_engine_candidate_hits(csaidx_engine* e, int64_t* rows, int reset);
 /* Profiling hook: when non-NULL, select launches of batch 0 write per-row
  * clock64 stamps [rows][8] = {start, threshold, filtered, sorted, n} into
  * this device buffer. */
@@ -146,6 +149,40 @@ int csaidx_cuda_select(csaidx_engine* e, const float* scores, int64_t batch, int
                        int apply_mask, int64_t k, float* cand_val, int32_t* cand_idx,
                        int64_t cand_ld);
 int csaidx_cuda_select_capacity(void);
+
+/* Fused select pre-filter (an implementation of the same tile_topk
+ * contract; results are identical to csaidx_cuda_select on every input):
+ *   1. score_sampled scores every kt_stride-th 128-key tile of the masked
+ *      tile into sample[b, i, 0..lds) (compacted columns, illegal = -inf);
+ *   2. row_threshold turns each row's sample into a threshold tau[b*rows+i]
+ *      chosen so that ~2k of the row's scores are expected to be >= tau
+ *      (-inf when the legal row fits the candidate list outright);
+ *   3. score_filtered is csaidx_cuda_score (apply_mask on) that also writes
+ *      the candidate bitmap: bit (j % 32) of
+ *      pass_bits[(b*rows + i) * bits_ld + j / 32] = (column j legal and
+ *      score >= tau). Words of key tiles that are causally dead for the
+ *      whole query block are left unwritten (no row reads them);
+ *   4. select_from_candidates finishes each row from its flagged entries
+ *      when min(k, n) <= flagged <= csaidx_cuda_candidate_capacity(k) (they
+ *      then hold every score >= tau, hence the exact top) and streams the
+ *      score row otherwise.
+ * Tensor-core shape only (csaidx_cuda_score_uses_tensor_cores with BF16 /
+ * FP32 / AUTO). bits_ld >= csaidx_cuda_candidate_words(cols). */
+int csaidx_cuda_candidate_capacity(int64_t k);
+int64_t csaidx_cuda_candidate_words(int64_t cols);
+int csaidx_cuda_score_sampled(csaidx_engine* e, const void* q_bf16, const void* kc_bf16, const float* w,
+                              const csaidx_dims* dims, int64_t s0, int64_t rows, int64_t t0, int64_t cols,
+                              int kt_stride, float* sample, int64_t lds);
+int csaidx_cuda_row_threshold(csaidx_engine* e, const float* sample, int64_t lds, int64_t batch, int64_t rows,
+                              int64_t cols, int64_t s0, int64_t t0, int64_t ratio, int kt_stride, int64_t k,
+                              float* tau);
+int csaidx_cuda_score_filtered(csaidx_engine* e, const void* q_bf16, const void* kc_bf16, const float* w,
+                               const csaidx_dims* dims, int64_t s0, int64_t rows, int64_t t0, int64_t cols,
+                               float* out, int64_t ld, const float* tau, uint32_t* pass_bits, int64_t bits_ld);
+int csaidx_cuda_select_from_candidates(csaidx_engine* e, const float* scores, int64_t batch, int64_t rows,
+                                       int64_t ld, int64_t cols, int64_t s0, int64_t t0, int64_t ratio, int64_t k,
+                                       const uint32_t* pass_bits, int64_t bits_ld, float* out_val,
+                                       int32_t* out_idx, int64_t out_ld);
 
 /* merge_topk / overwrite_topk (topk.hpp:73-82, topk.cpp:134-191) over nrows
  * running rows of k entries. check_overlap latches the reference's

@@ -86,6 +86,7 @@ CUDA_SYMBOLS = {
     "csaidx_engine_kernel_stats": (c_int, [c_void_p, c_int, POINTER(c_int64), POINTER(ctypes.c_double)]),
     "csaidx_engine_reset_stats": (c_int, [c_void_p]),
     "csaidx_engine_select_fallbacks": (c_int, [c_void_p, POINTER(c_int64), c_int]),
+    "csaidx_engine_candidate_hits": (c_int, [c_void_p, POINTER(c_int64), c_int]),
     "csaidx_engine_set_select_probe": (c_int, [c_void_p, c_void_p]),
     "csaidx_engine_use_lane": (c_int, [c_void_p, c_int]),
     "csaidx_engine_signal": (c_int, [c_void_p, c_int]),
@@ -109,6 +110,28 @@ CUDA_SYMBOLS = {
          c_void_p, c_void_p, c_int64],
     ),
     "csaidx_cuda_select_capacity": (c_int, []),
+    "csaidx_cuda_candidate_capacity": (c_int, [c_int64]),
+    "csaidx_cuda_candidate_words": (c_int64, [c_int64]),
+    "csaidx_cuda_score_sampled": (
+        c_int,
+        [c_void_p, c_void_p, c_void_p, c_void_p, POINTER(Dims), c_int64, c_int64, c_int64, c_int64, c_int,
+         c_void_p, c_int64],
+    ),
+    "csaidx_cuda_row_threshold": (
+        c_int,
+        [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int, c_int64,
+         c_void_p],
+    ),
+    "csaidx_cuda_score_filtered": (
+        c_int,
+        [c_void_p, c_void_p, c_void_p, c_void_p, POINTER(Dims), c_int64, c_int64, c_int64, c_int64,
+         c_void_p, c_int64, c_void_p, c_void_p, c_int64],
+    ),
+    "csaidx_cuda_select_from_candidates": (
+        c_int,
+        [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64,
+         c_void_p, c_int64, c_void_p, c_void_p, c_int64],
+    ),
     "csaidx_cuda_merge": (
         c_int,
         [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_int64, c_int64, c_int, c_int],

@@ -354,6 +354,12 @@ class KernelStats:
         _check_cuda(self.lib.csaidx_engine_select_fallbacks(self.h, ctypes.byref(n), int(reset)))
         return n.value
 
+    def candidate_hits(self, reset: bool = False) -> int:
+        """Rows finished from the fused pre-filter's candidate lists."""
+        n = c_int64()
+        _check_cuda(self.lib.csaidx_engine_candidate_hits(self.h, ctypes.byref(n), int(reset)))
+        return n.value
+
     def mem(self):
         live, peak = c_uint64(), c_uint64()
         _check_cuda(self.lib.csaidx_engine_mem_stats(self.h, ctypes.byref(live), ctypes.byref(peak)))

@@ -351,6 +351,16 @@ int csaidx_engine_select_fallbacks(csaidx_engine* e, int64_t* rows, int reset) {
     return CSAIDX_OK;
 }
 
+int csaidx_engine_candidate_hits(csaidx_engine* e, int64_t* rows, int reset) {
+    if (int rc = set_device(e)) return rc;
+    int h = 0;
+    CSAIDX_CUDA_TRY(cudaStreamSynchronize(e->stream), "cudaStreamSynchronize");
+    CSAIDX_CUDA_TRY(cudaMemcpy(&h, e->flags + kNumFlags + 3, sizeof(int), cudaMemcpyDeviceToHost), "counter D2H");
+    if (rows) *rows = h;
+    if (reset) CSAIDX_CUDA_TRY(cudaMemset(e->flags + kNumFlags + 3, 0, sizeof(int)), "counter reset");
+    return CSAIDX_OK;
+}
+
 int csaidx_engine_reset_stats(csaidx_engine* e) {
     if (int rc = set_device(e)) return rc;
     for (const auto& pd : e->pending) {
@@ -430,6 +440,111 @@ int csaidx_cuda_score_uses_tensor_cores(const csaidx_dims* d, int dtype, int mod
            csaidx_kern::score_tc_supported(d->heads, d->head_dim);
 }
 
+}  // extern "C"
+
+namespace {
+
+// score_tc launch shared by the plain, sampled and filtered entry points.
+int launch_tc(csaidx_engine* e, const void* q, const void* kc, const float* w, const csaidx_dims* d, int64_t s0,
+              int64_t rows, int64_t t0, int64_t cols, int apply_mask, float* out, int64_t ld, int kt_stride,
+              const float* tau, uint32_t* pass_bits, int64_t bits_ld) {
+    CUtensorMap qmap, kmap;
+    if (int rc = make_map(&qmap, q, static_cast<uint64_t>(d->batch * d->seq_len * d->heads), d->head_dim, 256))
+        return rc;
+    if (int rc = make_map(&kmap, kc, static_cast<uint64_t>(d->batch * d->key_blocks), d->head_dim, 128)) return rc;
+    ScoreTcParams p{};
+    p.w = w;
+    p.out = out;
+    p.nonfinite = e->flags + kNonfiniteScore;
+    p.sched = e->flags + kNumFlags;
+    p.ld = ld;
+    p.seq_len = d->seq_len;
+    p.key_blocks = d->key_blocks;
+    p.ratio = d->ratio;
+    p.s0 = s0;
+    p.rows = rows;
+    p.t0 = t0;
+    p.cols = cols;
+    p.batch = static_cast<int>(d->batch);
+    p.apply_mask = apply_mask;
+    p.kt_stride = kt_stride;
+    p.tau = tau;
+    p.pass_bits = pass_bits;
+    p.bits_ld = bits_ld;
+    LaunchScope ls(e, CSAIDX_KIND_SCORE);
+    CSAIDX_CUDA_TRY(csaidx_kern::launch_score_tc(qmap, kmap, p, e->num_sms, e->stream), "score_tc");
+    return CSAIDX_OK;
+}
+
+int check_tile(const csaidx_dims* d, int64_t s0, int64_t rows, int64_t t0, int64_t cols) {
+    if (int rc = check_dims(d)) return rc;
+    if (rows < 1 || cols < 1 || s0 < 0 || t0 < 0 || s0 + rows > d->seq_len || t0 + cols > d->key_blocks)
+        return fail(CSAIDX_INVALID_ARGUMENT, "score_tile: tile out of range");
+    return CSAIDX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t csaidx_cuda_candidate_words(int64_t cols) { return cols < 1 ? 0 : (cols + 127) / 128 * 4; }
+
+int csaidx_cuda_candidate_capacity(int64_t k) {
+    return k < 1 || k > csaidx_kern::select_max_take() ? 0 : csaidx_kern::select_cand_capacity(static_cast<int>(k));
+}
+
+int csaidx_cuda_score_sampled(csaidx_engine* e, const void* q_bf16, const void* kc_bf16, const float* w,
+                              const csaidx_dims* d, int64_t s0, int64_t rows, int64_t t0, int64_t cols, int kt_stride,
+                              float* sample, int64_t lds) {
+    if (int rc = set_device(e)) return rc;
+    if (int rc = check_tile(d, s0, rows, t0, cols)) return rc;
+    if (!csaidx_cuda_score_uses_tensor_cores(d, CSAIDX_DTYPE_BF16, CSAIDX_MODE_FP32, CSAIDX_KERNEL_AUTO))
+        return fail(CSAIDX_INVALID_ARGUMENT, "score_sampled: tensor-core shape only");
+    if (kt_stride < 1) return fail(CSAIDX_INVALID_ARGUMENT, "score_sampled: kt_stride must be >= 1");
+    const int64_t vtiles = ((cols + 127) / 128 + kt_stride - 1) / kt_stride;
+    if (lds < vtiles * 128 || (lds % 4) != 0) return fail(CSAIDX_INVALID_ARGUMENT, "score_sampled: lds too small");
+    return launch_tc(e, q_bf16, kc_bf16, w, d, s0, rows, t0, cols, 1, sample, lds, kt_stride, nullptr, nullptr, 0);
+}
+
+int csaidx_cuda_row_threshold(csaidx_engine* e, const float* sample, int64_t lds, int64_t batch, int64_t rows,
+                              int64_t cols, int64_t s0, int64_t t0, int64_t ratio, int kt_stride, int64_t k,
+                              float* tau) {
+    if (int rc = set_device(e)) return rc;
+    const int cap = csaidx_cuda_candidate_capacity(k);
+    if (cap == 0) return fail(CSAIDX_INVALID_ARGUMENT, "row_threshold: k outside the GPU selection capacity");
+    TauParams p{};
+    p.sample = sample;
+    p.lds = lds;
+    p.rows = rows;
+    p.cols = cols;
+    p.s0 = s0;
+    p.t0 = t0;
+    p.ratio = ratio;
+    p.batch = static_cast<int>(batch);
+    p.kt_stride = kt_stride < 1 ? 1 : kt_stride;
+    p.k = static_cast<int>(k);
+    p.cand_cap = cap;
+    p.tau = tau;
+    LaunchScope ls(e, CSAIDX_KIND_SELECT);
+    CSAIDX_CUDA_TRY(csaidx_kern::launch_tau(p, e->stream), "row_threshold");
+    return CSAIDX_OK;
+}
+
+int csaidx_cuda_score_filtered(csaidx_engine* e, const void* q_bf16, const void* kc_bf16, const float* w,
+                               const csaidx_dims* d, int64_t s0, int64_t rows, int64_t t0, int64_t cols, float* out,
+                               int64_t ld, const float* tau, uint32_t* pass_bits, int64_t bits_ld) {
+    if (int rc = set_device(e)) return rc;
+    if (int rc = check_tile(d, s0, rows, t0, cols)) return rc;
+    if (!csaidx_cuda_score_uses_tensor_cores(d, CSAIDX_DTYPE_BF16, CSAIDX_MODE_FP32, CSAIDX_KERNEL_AUTO))
+        return fail(CSAIDX_INVALID_ARGUMENT, "score_filtered: tensor-core shape only");
+    if (ld < cols || (ld % 4) != 0) return fail(CSAIDX_INVALID_ARGUMENT, "score: ld must be >= cols and a multiple of 4");
+    if (tau == nullptr || pass_bits == nullptr)
+        return fail(CSAIDX_INVALID_ARGUMENT, "score_filtered: missing tau / candidate bitmap");
+    if (bits_ld < csaidx_cuda_candidate_words(cols))
+        return fail(CSAIDX_INVALID_ARGUMENT, "score_filtered: bits_ld < csaidx_cuda_candidate_words(cols)");
+    return launch_tc(e, q_bf16, kc_bf16, w, d, s0, rows, t0, cols, 1, out, ld, 1, tau, pass_bits, bits_ld);
+}
+
 int csaidx_cuda_score(csaidx_engine* e, const void* q, const void* kc, int dtype, const float* w,
                       const csaidx_dims* d, int64_t s0, int64_t rows, int64_t t0, int64_t cols, int mode, int kernel,
                       int apply_mask, float* out, int64_t ld) {
@@ -445,30 +560,7 @@ int csaidx_cuda_score(csaidx_engine* e, const void* q, const void* kc, int dtype
     if (kernel != CSAIDX_KERNEL_AUTO && kernel != CSAIDX_KERNEL_EXACT)
         return fail(CSAIDX_INVALID_ARGUMENT, "score: unknown kernel request");
     if (csaidx_cuda_score_uses_tensor_cores(d, dtype, mode, kernel)) {
-        const uint16_t* q_bf16 = static_cast<const uint16_t*>(q);
-        const uint16_t* kc_bf16 = static_cast<const uint16_t*>(kc);
-        CUtensorMap qmap, kmap;
-        if (int rc = make_map(&qmap, q_bf16, static_cast<uint64_t>(d->batch * d->seq_len * d->heads), d->head_dim, 256))
-            return rc;
-        if (int rc = make_map(&kmap, kc_bf16, static_cast<uint64_t>(d->batch * d->key_blocks), d->head_dim, 128))
-            return rc;
-        ScoreTcParams p{};
-        p.w = w;
-        p.out = out;
-        p.nonfinite = e->flags + kNonfiniteScore;
-        p.sched = e->flags + kNumFlags;
-        p.ld = ld;
-        p.seq_len = d->seq_len;
-        p.key_blocks = d->key_blocks;
-        p.ratio = d->ratio;
-        p.s0 = s0;
-        p.rows = rows;
-        p.t0 = t0;
-        p.cols = cols;
-        p.batch = static_cast<int>(d->batch);
-        p.apply_mask = apply_mask;
-        LaunchScope ls(e, CSAIDX_KIND_SCORE);
-        CSAIDX_CUDA_TRY(csaidx_kern::launch_score_tc(qmap, kmap, p, e->num_sms, e->stream), "score_tc");
+        return launch_tc(e, q, kc, w, d, s0, rows, t0, cols, apply_mask, out, ld, 1, nullptr, nullptr, 0);
     } else {
         ScoreExactParams p{};
         p.q = q;
@@ -517,9 +609,13 @@ int csaidx_cuda_apply_bool_mask(csaidx_engine* e, float* scores, int64_t ld, con
 
 int csaidx_cuda_select_capacity(void) { return csaidx_kern::select_max_take(); }
 
-int csaidx_cuda_select(csaidx_engine* e, const float* scores, int64_t batch, int64_t rows, int64_t ld, int64_t cols,
-                       int64_t s0, int64_t t0, int64_t ratio, int apply_mask, int64_t k, float* cand_val,
-                       int32_t* cand_idx, int64_t cand_ld) {
+}  // extern "C"
+
+namespace {
+
+int select_impl(csaidx_engine* e, const float* scores, int64_t batch, int64_t rows, int64_t ld, int64_t cols,
+                int64_t s0, int64_t t0, int64_t ratio, int apply_mask, int64_t k, float* cand_val, int32_t* cand_idx,
+                int64_t cand_ld, const uint32_t* pass_bits, int64_t bits_ld) {
     if (int rc = set_device(e)) return rc;
     if (k < 1) return fail(CSAIDX_INVALID_ARGUMENT, "tile_topk: top_k must be >= 1");
     if (rows < 1 || cols < 1 || batch < 1 || ratio < 1) return fail(CSAIDX_INVALID_ARGUMENT, "select: bad extents");
@@ -547,9 +643,34 @@ int csaidx_cuda_select(csaidx_engine* e, const float* scores, int64_t batch, int
     p.out_ld = cand_ld;
     p.fallbacks = e->flags + kNumFlags + 2;
     p.phase_clk = e->select_probe;
+    p.pass_bits = pass_bits;
+    p.bits_ld = bits_ld;
+    p.cand_hits = e->flags + kNumFlags + 3;
     LaunchScope ls(e, CSAIDX_KIND_SELECT);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_select(p, e->stream), "select");
     return CSAIDX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int csaidx_cuda_select(csaidx_engine* e, const float* scores, int64_t batch, int64_t rows, int64_t ld, int64_t cols,
+                       int64_t s0, int64_t t0, int64_t ratio, int apply_mask, int64_t k, float* cand_val,
+                       int32_t* cand_idx, int64_t cand_ld) {
+    return select_impl(e, scores, batch, rows, ld, cols, s0, t0, ratio, apply_mask, k, cand_val, cand_idx, cand_ld,
+                       nullptr, 0);
+}
+
+int csaidx_cuda_select_from_candidates(csaidx_engine* e, const float* scores, int64_t batch, int64_t rows,
+                                       int64_t ld, int64_t cols, int64_t s0, int64_t t0, int64_t ratio, int64_t k,
+                                       const uint32_t* pass_bits, int64_t bits_ld, float* out_val,
+                                       int32_t* out_idx, int64_t out_ld) {
+    if (pass_bits == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "select_from_candidates: missing candidate bitmap");
+    if (bits_ld < csaidx_cuda_candidate_words(cols))
+        return fail(CSAIDX_INVALID_ARGUMENT, "select_from_candidates: bits_ld < csaidx_cuda_candidate_words(cols)");
+    return select_impl(e, scores, batch, rows, ld, cols, s0, t0, ratio, 1, k, out_val, out_idx, out_ld, pass_bits,
+                       bits_ld);
 }
 
 int csaidx_cuda_merge(csaidx_engine* e, float* run_val, int32_t* run_idx, int64_t nrows, int64_t k,

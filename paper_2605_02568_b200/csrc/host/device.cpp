@@ -2,6 +2,7 @@
 #include "device.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -106,6 +107,11 @@ void DeviceBuffer::reset() {
 void DeviceBuffer::upload(const void* host, size_t bytes) { check(csaidx_cuda_copy(e_, ptr_, host, bytes)); }
 
 void DeviceBuffer::download(void* host, size_t bytes) const { check(csaidx_cuda_copy(e_, host, ptr_, bytes)); }
+
+bool prefilter_enabled() {
+    const char* v = std::getenv("CSAIDX_SELECT_PREFILTER");
+    return v != nullptr && std::string(v) == "1";
+}
 
 int kernel_code(ScoreKernel kernel) {
     switch (kernel) {

@@ -50,6 +50,14 @@ private:
     size_t bytes_ = 0;
 };
 
+// Fused select pre-filter: off unless CSAIDX_SELECT_PREFILTER=1. Results are
+// identical either way; measured at C3 it costs more in the score epilogue
+// (+15 ms: one ballot + word store per score, plus the sample pass) than it
+// saves in the select (-2 ms), so it stays an A/B option. The
+// sample pass scores at most kPrefilterSampleTiles 128-key tiles per row.
+bool prefilter_enabled();
+constexpr int64_t kPrefilterSampleTiles = 16;
+
 int kernel_code(ScoreKernel kernel);  // throws like resolve_score_kernel for unavailable kernels
 int mode_code(AccumulationMode mode);
 csaidx_dims to_c(const ProblemDims& d);

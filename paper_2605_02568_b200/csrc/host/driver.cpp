@@ -74,6 +74,24 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
     DeviceBuffer keep;
     if (config.bool_mask_tile) keep = DeviceBuffer(e, static_cast<size_t>(plan.cs * plan.ct));
 
+    // Fused select pre-filter (csaidx_cuda.h): tensor-core tiles whose longest
+    // legal row exceeds the candidate list. Same results as the plain select;
+    // device scratch only (the reference has no such buffers to charge).
+    const int cap = csaidx_cuda_candidate_capacity(k);
+    const bool prefilter = prefilter_enabled() && !config.bool_mask_tile && cap > 0 &&
+                           csaidx_cuda_score_uses_tensor_cores(&cd, ops.dtype, mcode, kcode) != 0;
+    const int64_t tiles_max = ceil_div(plan.ct, 128);
+    // per tile: stride = ceil(tiles / kPrefilterSampleTiles) -> at most
+    // min(tiles, kPrefilterSampleTiles) sampled tiles
+    const int64_t lds = std::min<int64_t>(tiles_max, kPrefilterSampleTiles) * 128;
+    const int64_t bits_ld = csaidx_cuda_candidate_words(plan.ct);
+    DeviceBuffer pf_bits, pf_tau, pf_sample;
+    if (prefilter) {
+        pf_bits = DeviceBuffer(e, static_cast<size_t>(B * plan.cs * bits_ld) * sizeof(uint32_t));
+        pf_tau = DeviceBuffer(e, static_cast<size_t>(B * plan.cs) * sizeof(float));
+        pf_sample = DeviceBuffer(e, static_cast<size_t>(B * plan.cs * lds) * sizeof(float));
+    }
+
     for (size_t c = 0; c < plan.starts.size(); ++c) {
         const int64_t s0 = plan.starts[c];
         const int64_t rows = std::min(plan.cs, dims.seq_len - s0);
@@ -92,7 +110,18 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
                 break;
             }
             LedgerCharge tile_charge(ledger, "score_tile", chunk_tile_bytes(B, rows, cols));
-            if (config.bool_mask_tile) {
+            const int64_t legal_max = std::min(cols, (s0 + rows) / dims.ratio - t0);
+            const bool filtered = prefilter && legal_max > cap;
+            if (filtered) {
+                const int64_t ntiles = ceil_div(cols, 128);
+                const int stride = static_cast<int>(std::max<int64_t>(1, ceil_div(ntiles, kPrefilterSampleTiles)));
+                check(csaidx_cuda_score_sampled(e, ops.q, ops.kc, ops.w, &cd, s0, rows, t0, cols, stride,
+                                                pf_sample.as<float>(), lds));
+                check(csaidx_cuda_row_threshold(e, pf_sample.as<float>(), lds, B, rows, cols, s0, t0, dims.ratio,
+                                                stride, k, pf_tau.as<float>()));
+                check(csaidx_cuda_score_filtered(e, ops.q, ops.kc, ops.w, &cd, s0, rows, t0, cols, scores.as<float>(),
+                                                 ld, pf_tau.as<float>(), pf_bits.as<uint32_t>(), bits_ld));
+            } else if (config.bool_mask_tile) {
                 check(csaidx_cuda_score(e, ops.q, ops.kc, ops.dtype, ops.w, &cd, s0, rows, t0, cols, mcode, kcode, 0,
                                         scores.as<float>(), ld));
                 LedgerCharge mask_charge(ledger, "mask_tile", static_cast<uint64_t>(rows) * static_cast<uint64_t>(cols));
@@ -106,13 +135,20 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
             const int64_t width = std::min(k, cols);
             LedgerCharge scratch_charge(ledger, "tile_topk_scratch", tile_scratch_bytes(B, rows, cols, k));
             const bool overwrite = config.ablation == Ablation::a1_no_merge;
+            auto select = [&](float* v, int32_t* i, int64_t out_ld) {
+                if (filtered)
+                    check(csaidx_cuda_select_from_candidates(e, scores.as<float>(), B, rows, ld, cols, s0, t0,
+                                                             dims.ratio, k, pf_bits.as<uint32_t>(), bits_ld, v, i,
+                                                             out_ld));
+                else
+                    check(csaidx_cuda_select(e, scores.as<float>(), B, rows, ld, cols, s0, t0, dims.ratio, 1, k, v, i,
+                                             out_ld));
+            };
             if (first && width == k) {
                 // merge into all-sentinel rows (or A1 overwrite) == copy
-                check(csaidx_cuda_select(e, scores.as<float>(), B, rows, ld, cols, s0, t0, dims.ratio, 1, k,
-                                         run_v.as<float>(), run_i.as<int32_t>(), k));
+                select(run_v.as<float>(), run_i.as<int32_t>(), k);
             } else {
-                check(csaidx_cuda_select(e, scores.as<float>(), B, rows, ld, cols, s0, t0, dims.ratio, 1, k,
-                                         cand_v.as<float>(), cand_i.as<int32_t>(), width));
+                select(cand_v.as<float>(), cand_i.as<int32_t>(), width);
                 check(csaidx_cuda_merge(e, run_v.as<float>(), run_i.as<int32_t>(), B * rows, k, cand_v.as<float>(),
                                         cand_i.as<int32_t>(), width, width, overwrite ? 1 : 0, 0));
             }

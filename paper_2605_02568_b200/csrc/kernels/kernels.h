@@ -22,6 +22,16 @@ struct ScoreTcParams {
     int64_t s0, rows, t0, cols;
     int batch;
     int apply_mask;
+    // Sample mode: tile kt of the launch covers physical key tile
+    // kt * kt_stride; outputs use the compacted (virtual) column kt*128+lane.
+    int kt_stride;
+    // Fused candidate filter (optional): bit (j & 31) of
+    // pass_bits[(b*rows + r) * bits_ld + j / 32] = (column j legal and its
+    // score >= tau[b*rows + r]); one ballot + one word store per warp.
+    // Words of causally dead key tiles are not written.
+    const float* tau;
+    uint32_t* pass_bits;
+    int64_t bits_ld;
     // filled by the launcher: dense piece-major work list. Piece p (key tiles
     // [p*tpp, (p+1)*tpp)) is live for the query blocks qb >= nqb - count_p,
     // count_p = (piece_start[p+1] - piece_start[p]) / batch.
@@ -62,6 +72,28 @@ struct SelectParams {
     int64_t out_ld;
     int* fallbacks;       // rows that took the exact global fallback (telemetry)
     long long* phase_clk; // optional [rows * 8] clock64 stamps per phase (profiling)
+    // Optional candidate bitmap from the score epilogue (bit j of row r =
+    // legal score j >= tau[r]): when the row's flagged count is within
+    // [min(k, n), list capacity] the row is finished from the flagged
+    // entries; otherwise it streams `scores` as usual.
+    const uint32_t* pass_bits;  // [B, rows, bits_ld]
+    int64_t bits_ld;
+    int* cand_hits;       // rows finished from the bitmap (telemetry)
+};
+
+// Per-row candidate threshold from a strided sample of the row's scores
+// (the sample pass of score_tc, kt_stride > 1): the sample's rank-r key with
+// r chosen so ~2k entries of the whole row are expected to pass; -inf when
+// the row's legal length fits the candidate list outright.
+struct TauParams {
+    const float* sample;  // [B, rows, lds] virtual columns (illegal = -inf)
+    int64_t lds;
+    int64_t rows, cols, s0, t0, ratio;
+    int batch;
+    int kt_stride;
+    int k;
+    int cand_cap;
+    float* tau;           // [B * rows]
 };
 
 // ------------------------------------------------------------------ merge
@@ -115,7 +147,9 @@ cudaError_t launch_score_tc(const CUtensorMap& qmap, const CUtensorMap& kmap, Sc
 cudaError_t launch_score_exact(const ScoreExactParams& p, cudaStream_t stream);
 
 int select_max_take();
+int select_cand_capacity(int k);  // candidate-list length the select kernel accepts for this k
 cudaError_t launch_select(const SelectParams& p, cudaStream_t stream);
+cudaError_t launch_tau(const TauParams& p, cudaStream_t stream);
 cudaError_t launch_merge(const MergeParams& p, cudaStream_t stream);
 cudaError_t launch_finalize(const FinalizeParams& p, cudaStream_t stream);
 

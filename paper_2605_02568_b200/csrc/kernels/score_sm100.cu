@@ -88,7 +88,8 @@ __device__ __forceinline__ void decode_item(const ScoreTcParams& p, int idx, Ite
         kend = t_legal_dev(p.s0 + it.r0 + it.nrows - 1, p.ratio) - p.t0;
         kend = kend < 0 ? 0 : (kend > p.cols ? p.cols : kend);
     }
-    const int ntiles = static_cast<int>((kend + kBlockKeys - 1) / kBlockKeys);
+    const int ntiles_phys = static_cast<int>((kend + kBlockKeys - 1) / kBlockKeys);
+    const int ntiles = (ntiles_phys + p.kt_stride - 1) / p.kt_stride;  // virtual tiles
     it.kt_begin = lo * p.tpp;
     it.kt_end = min(it.kt_begin + p.tpp, ntiles);
 }
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                     const uint32_t s = kiter % kStages;
                     mbar_wait(&k_empty[s], ((kiter / kStages) & 1) ^ 1);
                     mbar_expect_tx(&k_full[s], kKStageBytes);
-                    const int32_t krow = static_cast<int32_t>(krow0 + kt * kBlockKeys);
+                    const int32_t krow = static_cast<int32_t>(krow0 + static_cast<int64_t>(kt) * p.kt_stride * kBlockKeys);
                     for (int hf = 0; hf < 2; ++hf) {
                         tma_load_2d_hint(k_smem + s * kKStageBytes + hf * kKHalfBytes, &kmap, &k_full[s], hf * 64,
                                          krow, keep);
@@ -298,26 +299,31 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             // the causal limit (first illegal column, relative to t0).
             float* orow[kGroups][2];
             int lim[kGroups][2];
+            float tq[kGroups][2];  // candidate thresholds (filter mode)
 #pragma unroll
             for (int g = 0; g < kGroups; ++g) {
 #pragma unroll
                 for (int qq = 0; qq < 2; ++qq) {
                     const int qi = g * kQPerGroup + qpair * 2 + qq;
                     const int64_t r = it.r0 + qi;
-                    orow[g][qq] = p.out + (static_cast<int64_t>(it.b) * p.rows + r) * p.ld;
+                    const int64_t grow = static_cast<int64_t>(it.b) * p.rows + r;
+                    orow[g][qq] = p.out + grow * p.ld;
                     int64_t l = p.cols;
                     if (p.apply_mask) {
                         l = t_legal_dev(p.s0 + r, p.ratio) - p.t0;
                         l = l < 0 ? 0 : (l > p.cols ? p.cols : l);
                     }
                     lim[g][qq] = static_cast<int>(l);
+                    tq[g][qq] = (p.tau != nullptr && qi < it.nrows) ? p.tau[grow] : 0.f;
                 }
             }
             mbar_wait(&w_full[wb], (qiter / kWBufs) & 1);
             ++qiter;
             const int cols = static_cast<int>(p.cols);
+            const int out_cols = p.kt_stride == 1 ? cols : static_cast<int>(p.ld);
             for (int kt = it.kt_begin; kt < it.kt_end; ++kt) {
-                const int j = kt * kBlockKeys + quarter * 32 + static_cast<int>(lane);
+                const int jo = kt * kBlockKeys + quarter * 32 + static_cast<int>(lane);  // output column
+                const int j = jo + kt * (p.kt_stride - 1) * kBlockKeys;                 // key column
 #pragma unroll
                 for (int g = 0; g < kGroups; ++g) {
                     const uint32_t a = aiter & 1;
@@ -331,10 +337,19 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                         tmem_ld64(row_taddr + a * kUmmaN + (qpair * 2 + qq) * kHeads, v);
                         tmem_ld_wait();
                         const float acc = head_reduce(v, w_item + qi * kHeads);
-                        if (j < cols) {
-                            const bool legal = j < lim[g][qq];
+                        const bool legal = j < lim[g][qq];
+                        if (jo < out_cols) {
                             if (legal && !isfinite(acc)) atomicOr(p.nonfinite, 1);
-                            orow[g][qq][j] = legal ? acc : neg_inf;
+                            orow[g][qq][jo] = legal ? acc : neg_inf;
+                        }
+                        if (p.tau != nullptr) {
+                            // fused select pre-filter: one candidate word per
+                            // warp (32 consecutive key columns)
+                            const uint32_t m = __ballot_sync(0xffffffffu, legal && acc >= tq[g][qq]);
+                            if (lane == 0) {
+                                const int64_t grow = static_cast<int64_t>(it.b) * p.rows + it.r0 + qi;
+                                p.pass_bits[grow * p.bits_ld + (jo >> 5)] = m;
+                            }
                         }
                     }
                     tc_fence_before();
@@ -431,7 +446,9 @@ cudaError_t launch_score_tc(const CUtensorMap& qmap, const CUtensorMap& kmap, Sc
     // (pc+1)*tpp); the query blocks for which it is causally live form a
     // suffix qb >= nqb - count[pc] because the live extent grows with qb.
     p.nqb = static_cast<int>((p.rows + kQPerItem - 1) / kQPerItem);
-    const int64_t max_tiles = (p.cols + kBlockKeys - 1) / kBlockKeys;
+    if (p.kt_stride < 1) p.kt_stride = 1;
+    const int64_t stride = p.kt_stride;
+    const int64_t max_tiles = ((p.cols + kBlockKeys - 1) / kBlockKeys + stride - 1) / stride;  // virtual
     int64_t tpp = kMinTilesPerPiece;
     while ((max_tiles + tpp - 1) / tpp > kScoreMaxPieces) tpp *= 2;
     p.tpp = static_cast<int>(tpp);
@@ -445,7 +462,7 @@ cudaError_t launch_score_tc(const CUtensorMap& qmap, const CUtensorMap& kmap, Sc
             kend = (p.s0 + r0 + nrows) / p.ratio - p.t0;
             kend = kend < 0 ? 0 : (kend > p.cols ? p.cols : kend);
         }
-        const int64_t ntiles = (kend + kBlockKeys - 1) / kBlockKeys;
+        const int64_t ntiles = ((kend + kBlockKeys - 1) / kBlockKeys + stride - 1) / stride;
         ++live[static_cast<size_t>((ntiles + tpp - 1) / tpp)];
     }
     int above = 0;  // #qb with more than pc pieces, built from the top

@@ -95,57 +95,53 @@ __device__ void bitonic_sort_desc(uint64_t* a, int P) {
 // holds E consecutive elements in registers; strides < E are in-register,
 // strides < 32E go through warp shuffles, and only the strides that cross
 // warps touch shared memory (6 barrier stages for P = 1024 instead of 55).
+// Fully unrolled (size and stride are compile-time), so every per-stage
+// predicate is one bit test of the thread index and each element costs a
+// shuffle pair, one 64-bit compare and one select.
 template <int E>
-__device__ void bitonic_sort_desc_regs(uint64_t* a, int P) {
+__device__ __forceinline__ void bitonic_sort_desc_regs(uint64_t* a) {
+    constexpr int P = E * kThreads;
     const int t = threadIdx.x;
     uint64_t x[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) x[e] = a[t * E + e];
+#pragma unroll
     for (int size = 2; size <= P; size <<= 1) {
+#pragma unroll
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
             if (stride < E) {
-                // compile-time strides keep x[] in registers
 #pragma unroll
-                for (int s = E / 2; s >= 1; s >>= 1) {
-                    if (s != stride) continue;
-#pragma unroll
-                    for (int e = 0; e < E; ++e) {
-                        const int pe = e ^ s;
-                        if (pe > e) {
-                            const int i = t * E + e;
-                            const bool desc = (i & size) == 0;
-                            const uint64_t lo = x[e], hi = x[pe];
-                            if (desc ? (lo < hi) : (lo > hi)) {
-                                x[e] = hi;
-                                x[pe] = lo;
-                            }
-                        }
+                for (int e = 0; e < E; ++e) {
+                    const int pe = e ^ stride;
+                    if (pe > e) {
+                        const bool desc = ((t * E + e) & size) == 0;
+                        const uint64_t lo = x[e], hi = x[pe];
+                        const bool swap = desc ? (lo < hi) : (lo > hi);
+                        x[e] = swap ? hi : lo;
+                        x[pe] = swap ? lo : hi;
                     }
                 }
-            } else if (stride < 32 * E) {
-                const int lane_x = stride / E;
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    const int i = t * E + e;
-                    const uint64_t other = __shfl_xor_sync(0xffffffffu, x[e], lane_x);
-                    const bool lower = (i & stride) == 0;
-                    const bool desc = (i & size) == 0;
-                    const bool keep_max = lower == desc;
-                    x[e] = keep_max ? (x[e] > other ? x[e] : other) : (x[e] < other ? x[e] : other);
-                }
             } else {
-                __syncthreads();
+                // both bits come from the thread index: uniform over e
+                const bool lower = (t & (stride / E)) == 0;
+                const bool desc = (t & (size / E)) == 0 || size >= P;
+                const bool keep_max = lower == desc;
+                if (stride < 32 * E) {
 #pragma unroll
-                for (int e = 0; e < E; ++e) a[t * E + e] = x[e];
-                __syncthreads();
+                    for (int e = 0; e < E; ++e) {
+                        const uint64_t other = __shfl_xor_sync(0xffffffffu, x[e], stride / E);
+                        x[e] = ((x[e] > other) == keep_max) ? x[e] : other;
+                    }
+                } else {
+                    __syncthreads();
 #pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    const int i = t * E + e;
-                    const uint64_t other = a[i ^ stride];
-                    const bool lower = (i & stride) == 0;
-                    const bool desc = (i & size) == 0;
-                    const bool keep_max = lower == desc;
-                    x[e] = keep_max ? (x[e] > other ? x[e] : other) : (x[e] < other ? x[e] : other);
+                    for (int e = 0; e < E; ++e) a[t * E + e] = x[e];
+                    __syncthreads();
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const uint64_t other = a[(t * E + e) ^ stride];
+                        x[e] = ((x[e] > other) == keep_max) ? x[e] : other;
+                    }
                 }
             }
         }
@@ -158,11 +154,11 @@ __device__ void bitonic_sort_desc_regs(uint64_t* a, int P) {
 
 __device__ void sort_desc(uint64_t* a, int P) {
     switch (P / static_cast<int>(blockDim.x)) {
-        case 1: bitonic_sort_desc_regs<1>(a, P); break;
-        case 2: bitonic_sort_desc_regs<2>(a, P); break;
-        case 4: bitonic_sort_desc_regs<4>(a, P); break;
-        case 8: bitonic_sort_desc_regs<8>(a, P); break;
-        default: bitonic_sort_desc(a, P); break;  // P < blockDim
+        case 1: bitonic_sort_desc_regs<1>(a); break;
+        case 2: bitonic_sort_desc_regs<2>(a); break;
+        case 4: bitonic_sort_desc_regs<4>(a); break;
+        case 8: bitonic_sort_desc_regs<8>(a); break;
+        default: bitonic_sort_desc(a, P); break;  // P < blockDim or very large
     }
 }
 
@@ -398,7 +394,43 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
     if (clk) clk[0] = clock64();
     if (take > 0) {
         int count = -1;  // candidates in cand[], or -1 -> fallback
-        if (n <= L.cand_cap) {
+        int pre = -1;    // candidates flagged by the score epilogue, if usable
+        if (p.pass_bits != nullptr) {
+            // The bitmap flags every legal score >= the row's tau; when the
+            // flagged count lies in [take, cand_cap] the flagged entries
+            // contain the exact top-take and fit the list.
+            const uint32_t* bits = p.pass_bits + (static_cast<int64_t>(b) * p.rows + row_id) * p.bits_ld;
+            const int nw = static_cast<int>((n + 31) >> 5);
+            if (threadIdx.x == 0) *counter = 0;
+            __syncthreads();
+            uint32_t loc = 0;
+            for (int i = threadIdx.x; i < nw; i += kThreads) loc += __popc(__ldg(bits + i));
+            loc = __reduce_add_sync(0xffffffffu, loc);
+            if (lane == 0 && loc != 0) atomicAdd(counter, loc);
+            __syncthreads();
+            const uint32_t tot = *counter;
+            __syncthreads();
+            if (tot >= static_cast<uint32_t>(take) && tot <= static_cast<uint32_t>(L.cand_cap)) {
+                if (threadIdx.x == 0) *counter = 0;
+                __syncthreads();
+                for (int i = threadIdx.x; i < nw; i += kThreads) {
+                    uint32_t m = __ldg(bits + i);
+                    if (m == 0) continue;
+                    uint32_t pos = atomicAdd(counter, static_cast<uint32_t>(__popc(m)));
+                    while (m != 0) {
+                        const int j = i * 32 + __ffs(m) - 1;
+                        m &= m - 1;
+                        cand[pos++] = composite(ord_key(__ldg(row + j)), j);
+                    }
+                }
+                pre = static_cast<int>(tot);
+                if (threadIdx.x == 0 && p.cand_hits != nullptr) atomicAdd(p.cand_hits, 1);
+                __syncthreads();
+            }
+        }
+        if (pre >= 0) {
+            count = pre;
+        } else if (n <= L.cand_cap) {
             for (int64_t i = threadIdx.x; i < n; i += blockDim.x) cand[i] = composite(ord_key(__ldg(row + i)), i);
             count = static_cast<int>(n);
             __syncthreads();
@@ -596,11 +628,109 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
     }
 }
 
+// ------------------------------------------------------------------ tau
+constexpr int kTauMaxSamples = 8192;
+
+__global__ void __launch_bounds__(kThreads) tau_kernel(const TauParams p) {
+    __shared__ uint32_t s_keys[kTauMaxSamples];
+    __shared__ uint32_t hist[kBins];
+    __shared__ uint32_t wsum[kWarps];
+    __shared__ uint32_t res[8];
+    const int64_t row_id = blockIdx.x;
+    const int b = blockIdx.y;
+    const int lane = threadIdx.x & 31;
+    int64_t n = (p.s0 + row_id + 1) / p.ratio - p.t0;
+    n = n < 0 ? 0 : (n > p.cols ? p.cols : n);
+    float* out = p.tau + static_cast<int64_t>(b) * p.rows + row_id;
+    const float neg_inf = -__int_as_float(0x7f800000);
+    if (n <= p.cand_cap) {  // the whole legal row fits the candidate list
+        if (threadIdx.x == 0) *out = neg_inf;
+        return;
+    }
+    const int64_t vt = ((n + 127) / 128 + p.kt_stride - 1) / p.kt_stride;
+    int64_t nv = vt * 128;
+    if (nv > p.lds) nv = p.lds;
+    const float* srow = p.sample + (static_cast<int64_t>(b) * p.rows + row_id) * p.lds;
+    if (threadIdx.x == 0) {
+        res[4] = 0;
+        res[6] = 0xffffffffu;
+        res[7] = 0u;
+    }
+    for (int i = threadIdx.x; i < kBins; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    uint32_t kmin = 0xffffffffu, kmax = 0u;
+    const int64_t nvr = (nv + 31) & ~int64_t{31};
+    for (int64_t i = threadIdx.x; i < nvr; i += blockDim.x) {
+        const float v = i < nv ? __ldg(srow + i) : neg_inf;
+        const bool keep = v != neg_inf;  // legal sampled entries (scores are finite)
+        const uint32_t m = __ballot_sync(0xffffffffu, keep);
+        uint32_t base = 0;
+        if (lane == 0 && m != 0) base = atomicAdd(&res[4], __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) {
+            const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
+            const uint32_t key = ord_key(v);
+            if (pos < static_cast<uint32_t>(kTauMaxSamples)) s_keys[pos] = key;
+            kmin = min(kmin, key);
+            kmax = max(kmax, key);
+        }
+    }
+    kmin = __reduce_min_sync(0xffffffffu, kmin);
+    kmax = __reduce_max_sync(0xffffffffu, kmax);
+    if (lane == 0) {
+        atomicMin(&res[6], kmin);
+        atomicMax(&res[7], kmax);
+    }
+    __syncthreads();
+    const int ns = static_cast<int>(min(res[4], static_cast<uint32_t>(kTauMaxSamples)));
+    const int target = (2 * p.k < (p.cand_cap * 3) / 4) ? 2 * p.k : (p.cand_cap * 3) / 4;
+    int r = static_cast<int>((static_cast<int64_t>(target) * ns) / n);
+    if (r < 1) r = 1;
+    if (ns == 0 || r > ns) {  // sample too thin to cut: keep everything (the select falls back)
+        if (threadIdx.x == 0) *out = neg_inf;
+        return;
+    }
+    const uint32_t lo = res[6], hi_k = res[7];
+    uint32_t prefix = 0;
+    int pbits = lo == hi_k ? 32 : __clz(lo ^ hi_k);
+    if (pbits > 0) prefix = pbits == 32 ? lo : (lo >> (32 - pbits));
+    uint32_t rr = static_cast<uint32_t>(r);
+#pragma unroll 1
+    for (int pass = 0; pass < 2 && pbits < 32; ++pass) {
+        const int wbits = 32 - pbits < 11 ? 32 - pbits : 11;
+        const int shift = 32 - pbits - wbits;
+        if (pass > 0) {
+            for (int i = threadIdx.x; i < kBins; i += blockDim.x) hist[i] = 0;
+            __syncthreads();
+        }
+        for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+            const uint32_t v = s_keys[i];
+            if (pbits == 0 || (v >> (32 - pbits)) == prefix) atomicAdd(&hist[(v >> shift) & ((1u << wbits) - 1u)], 1u);
+        }
+        __syncthreads();
+        find_bin(hist, 1 << wbits, rr, res, wsum);
+        rr -= res[1];
+        prefix = (pbits == 0 ? 0u : (prefix << wbits)) | res[0];
+        pbits += wbits;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = ord_key_to_float(pbits >= 32 ? prefix : (prefix << (32 - pbits)));
+}
+
 }  // namespace
 
 namespace csaidx_kern {
 
 int select_max_take() { return kMaxTake; }
+
+int select_cand_capacity(int k) { return layout_for(k).cand_cap; }
+
+cudaError_t launch_tau(const TauParams& p, cudaStream_t stream) {
+    if (p.rows <= 0 || p.batch <= 0) return cudaSuccess;
+    const dim3 grid(static_cast<unsigned>(p.rows), static_cast<unsigned>(p.batch));
+    tau_kernel<<<grid, kThreads, 0, stream>>>(p);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_select(const SelectParams& p, cudaStream_t stream) {
     if (p.rows <= 0 || p.batch <= 0) return cudaSuccess;

@@ -6,7 +6,7 @@ streams only); every compute call goes through libcsaidx_cuda.so.
 from __future__ import annotations
 
 import ctypes
-from ctypes import byref, c_int, c_uint64, c_void_p
+from ctypes import byref, c_int, c_int64, c_uint64, c_void_p
 
 import torch
 
@@ -115,6 +115,50 @@ class Engine:
         check(self.lib.csaidx_cuda_select(self.handle, _p(scores), batch, rows, ld, cols, s0, t0, ratio,
                                           int(apply_mask), k, _p(val), _p(idx), width))
         return val, idx
+
+    # ------------------------------------------------ fused select pre-filter
+    def candidate_capacity(self, k: int) -> int:
+        return int(self.lib.csaidx_cuda_candidate_capacity(k))
+
+    def score_sampled(self, q, kc, w, dims: Dims, s0, rows, t0, cols, kt_stride):
+        vt = (-(-cols // 128) + kt_stride - 1) // kt_stride
+        out = torch.empty((dims.batch, rows, vt * 128), dtype=torch.float32, device=q.device)
+        check(self.lib.csaidx_cuda_score_sampled(self.handle, _p(q), _p(kc), _p(w), byref(dims), s0, rows, t0, cols,
+                                                 kt_stride, _p(out), out.shape[-1]))
+        return out
+
+    def row_threshold(self, sample, batch, rows, cols, s0, t0, ratio, kt_stride, k):
+        tau = torch.empty((batch, rows), dtype=torch.float32, device=sample.device)
+        check(self.lib.csaidx_cuda_row_threshold(self.handle, _p(sample), sample.shape[-1], batch, rows, cols, s0, t0,
+                                                 ratio, kt_stride, k, _p(tau)))
+        return tau
+
+    def candidate_words(self, cols: int) -> int:
+        return int(self.lib.csaidx_cuda_candidate_words(cols))
+
+    def score_filtered(self, q, kc, w, dims: Dims, s0, rows, t0, cols, tau):
+        """Masked score tile + per-row candidate bitmap (legal scores >= tau)."""
+        ld = (cols + 3) // 4 * 4
+        out = torch.empty((dims.batch, rows, ld), dtype=torch.float32, device=q.device)
+        bits = torch.zeros((dims.batch, rows, self.candidate_words(cols)), dtype=torch.int32, device=q.device)
+        check(self.lib.csaidx_cuda_score_filtered(self.handle, _p(q), _p(kc), _p(w), byref(dims), s0, rows, t0, cols,
+                                                  _p(out), ld, _p(tau), _p(bits), bits.shape[-1]))
+        return out, bits
+
+    def select_from_candidates(self, scores, batch, rows, cols, s0, t0, ratio, k, bits):
+        ld = scores.shape[-1]
+        width = min(k, cols)
+        val = torch.empty((batch, rows, width), dtype=torch.float32, device=scores.device)
+        idx = torch.empty((batch, rows, width), dtype=torch.int32, device=scores.device)
+        check(self.lib.csaidx_cuda_select_from_candidates(self.handle, _p(scores), batch, rows, ld, cols, s0, t0,
+                                                          ratio, k, _p(bits), bits.shape[-1], _p(val),
+                                                          _p(idx), width))
+        return val, idx
+
+    def candidate_hits(self, reset: bool = True) -> int:
+        n = c_int64(0)
+        check(self.lib.csaidx_engine_candidate_hits(self.handle, byref(n), int(reset)))
+        return n.value
 
     def merge(self, run_val, run_idx, cand_val, cand_idx, overwrite=False, check_overlap=False):
         k = run_val.shape[-1]

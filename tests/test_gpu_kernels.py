@@ -248,3 +248,95 @@ def test_chunked_pipeline_small_v4(engine):
     engine.check()
     assert np.array_equal(ri.cpu().numpy(), fi[:, s0:s0 + rows].cpu().numpy())
     assert np.array_equal(rv.cpu().numpy(), fv[:, s0:s0 + rows].cpu().numpy())
+
+
+# ------------------------------------------------------- fused select pre-filter
+def _prefilter_case(engine, seed=11, zero_w=False):
+    from paper_2605_02568_b200.engine import dims_struct
+
+    B, S, H, D, m, k = 1, 16384, 64, 128, 4, 512
+    q, kc, w = make_inputs(B, S, H, D, m, seed=seed)
+    if zero_w:
+        w[:] = 0.0  # every legal score is +0.0: one giant tie
+    dims = dims_struct(B, S, H, D, m, k)
+    qd, kd, wd = to_dev(q, torch.bfloat16), to_dev(kc, torch.bfloat16), to_dev(w)
+    s0, rows, t0, cols = 12288, 512, 0, S // m
+    return dims, (qd, kd, wd), (B, m, k, s0, rows, t0, cols)
+
+
+def test_prefilter_select_equals_plain_select(engine):
+    """sample -> tau -> filtered score -> select from the bitmap == score ->
+    select, bit for bit; the bitmap flags exactly the legal scores >= tau."""
+    dims, (qd, kd, wd), (B, m, k, s0, rows, t0, cols) = _prefilter_case(engine)
+    cap = engine.candidate_capacity(k)
+    assert cap >= 2 * k
+    stride = max(1, -(-(-(-cols // 128)) // 16))
+    sample = engine.score_sampled(qd, kd, wd, dims, s0, rows, t0, cols, stride)
+    tau = engine.row_threshold(sample, B, rows, cols, s0, t0, m, stride, k)
+    sc, bits = engine.score_filtered(qd, kd, wd, dims, s0, rows, t0, cols, tau)
+    engine.candidate_hits(reset=True)
+    fv, fi = engine.select_from_candidates(sc, B, rows, cols, s0, t0, m, k, bits)
+    hits = engine.candidate_hits()
+    plain = engine.score(qd, kd, wd, dims, s0, rows, t0, cols, apply_mask=True)
+    pv, pi = engine.select(plain, B, rows, cols, s0, t0, m, k)
+    engine.check()
+    assert torch.equal(fi, pi) and torch.equal(fv.view(torch.int32), pv.view(torch.int32))
+    scn, pn, tn = sc.cpu().numpy(), plain.cpu().numpy(), tau.cpu().numpy()
+    bn = bits.cpu().numpy().view(np.uint32)
+    nflag = []
+    for i in range(rows):
+        n = int(np.clip(legal(s0 + i, m) - t0, 0, cols))
+        assert np.array_equal(scn[0, i, :n].view(np.uint32), pn[0, i, :n].view(np.uint32))
+        want = scn[0, i, :n] >= tn[0, i]
+        nw = -(-n // 32)
+        got = np.unpackbits(bn[0, i, :nw].view(np.uint8), bitorder="little")[:n].astype(bool)
+        assert np.array_equal(got, want), i
+        assert not np.any(np.unpackbits(bn[0, i, :nw].view(np.uint8), bitorder="little")[n:nw * 32])
+        nflag.append(int(want.sum()))
+    nflag = np.array(nflag)
+    # the sample threshold lands every row between k and the list capacity
+    assert hits == int(np.sum((nflag >= k) & (nflag <= cap))) and hits >= rows * 9 // 10, (hits, nflag.min(), nflag.max())
+    # sample columns are the kt_stride-th key tiles
+    vt = sample.shape[-1] // 128
+    for v in range(vt):
+        phys = v * stride * 128
+        if phys >= cols:
+            break
+        seg = min(128, cols - phys)
+        lim = np.clip((s0 + np.arange(rows) + 1) // m - t0 - phys, 0, seg)
+        sn = sample[0, :, v * 128:v * 128 + seg].cpu().numpy()
+        for i in range(0, rows, 17):
+            if lim[i] == 0:
+                continue  # the row never reads this sample tile (it may be causally dead)
+            assert np.array_equal(sn[i, :lim[i]].view(np.uint32), pn[0, i, phys:phys + lim[i]].view(np.uint32))
+            assert np.all(np.isneginf(sn[i, lim[i]:]))
+
+
+@pytest.mark.parametrize("how", ["tau_high", "tau_low", "all_ties"])
+def test_prefilter_falls_back_when_the_bitmap_is_unusable(engine, how):
+    """Fewer than min(k, n) flagged entries (tau too high) or more than the
+    list capacity (tau too low, giant ties) must take the streaming select."""
+    dims, (qd, kd, wd), (B, m, k, s0, rows, t0, cols) = _prefilter_case(engine, seed=12, zero_w=how == "all_ties")
+    cap = engine.candidate_capacity(k)
+    if how == "tau_high":
+        tau = torch.full((B, rows), 1e30, device="cuda")
+    elif how == "tau_low":
+        tau = torch.full((B, rows), -1e30, device="cuda")
+    else:
+        stride = 2
+        sample = engine.score_sampled(qd, kd, wd, dims, s0, rows, t0, cols, stride)
+        tau = engine.row_threshold(sample, B, rows, cols, s0, t0, m, stride, k)
+    sc, bits = engine.score_filtered(qd, kd, wd, dims, s0, rows, t0, cols, tau)
+    engine.candidate_hits(reset=True)
+    fv, fi = engine.select_from_candidates(sc, B, rows, cols, s0, t0, m, k, bits)
+    hits = engine.candidate_hits()
+    pv, pi = engine.select(sc, B, rows, cols, s0, t0, m, k)
+    engine.check()
+    assert torch.equal(fi, pi) and torch.equal(fv.view(torch.int32), pv.view(torch.int32))
+    n_rows = np.clip((s0 + np.arange(rows) + 1) // m - t0, 0, cols)
+    if how == "tau_high":
+        assert hits == 0
+    else:  # only rows whose whole legal row fits the list can hit
+        assert hits == int(np.sum(n_rows <= cap))
+    if how == "all_ties":
+        assert np.array_equal(fi[0, -1].cpu().numpy(), np.arange(k, dtype=np.int32))
