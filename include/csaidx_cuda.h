@@ -106,6 +106,11 @@ int csaidx_engine_candidate_hits(csaidx_engine* e, int64_t* rows, int reset);
  * clock64 stamps [rows][8] = {start, threshold, filtered, sorted, n} into
  * this device buffer. */
 int csaidx_engine_set_select_probe(csaidx_engine* e, long long* device_clocks);
+/* Profiling hook: when non-NULL, tcgen05 score launches write per-CTA
+ * clock64 wait counters [grid][8] = {MMA wait k_full, MMA wait acc_empty,
+ * MMA wait q_full, MMA span, epilogue wait acc_full, epilogue span,
+ * producer wait k_empty, producer wait q_empty} (grid = SM count). */
+int csaidx_engine_set_score_probe(csaidx_engine* e, long long* device_counters);
 
 /* Stream-ordered device memory from a cached pool. */
 int csaidx_cuda_alloc(csaidx_engine* e, size_t bytes, void** ptr);

@@ -88,6 +88,7 @@ CUDA_SYMBOLS = {
     "csaidx_engine_select_fallbacks": (c_int, [c_void_p, POINTER(c_int64), c_int]),
     "csaidx_engine_candidate_hits": (c_int, [c_void_p, POINTER(c_int64), c_int]),
     "csaidx_engine_set_select_probe": (c_int, [c_void_p, c_void_p]),
+    "csaidx_engine_set_score_probe": (c_int, [c_void_p, c_void_p]),
     "csaidx_engine_use_lane": (c_int, [c_void_p, c_int]),
     "csaidx_engine_signal": (c_int, [c_void_p, c_int]),
     "csaidx_engine_await": (c_int, [c_void_p, c_int]),

@@ -88,6 +88,7 @@ struct csaidx_engine {
     int lane = 0;
     cudaEvent_t slots[64] = {};
     long long* select_probe = nullptr;  // optional per-row phase clocks (profiling)
+    long long* score_probe = nullptr;   // optional per-CTA wait counters (profiling)
 };
 
 namespace {
@@ -335,6 +336,12 @@ int csaidx_engine_kernel_stats(csaidx_engine* e, int kind, int64_t* launches, do
     return CSAIDX_OK;
 }
 
+int csaidx_engine_set_score_probe(csaidx_engine* e, long long* device_counters) {
+    if (e == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null engine");
+    e->score_probe = device_counters;
+    return CSAIDX_OK;
+}
+
 int csaidx_engine_set_select_probe(csaidx_engine* e, long long* device_clocks) {
     if (e == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null engine");
     e->select_probe = device_clocks;
@@ -471,6 +478,7 @@ int launch_tc(csaidx_engine* e, const void* q, const void* kc, const float* w, c
     p.tau = tau;
     p.pass_bits = pass_bits;
     p.bits_ld = bits_ld;
+    p.probe = e->score_probe;
     LaunchScope ls(e, CSAIDX_KIND_SCORE);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_score_tc(qmap, kmap, p, e->num_sms, e->stream), "score_tc");
     return CSAIDX_OK;

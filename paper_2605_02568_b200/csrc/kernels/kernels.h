@@ -32,6 +32,10 @@ struct ScoreTcParams {
     const float* tau;
     uint32_t* pass_bits;
     int64_t bits_ld;
+    // Optional profiling counters, [grid][8] clock64 cycles: MMA waits on
+    // k_full / acc_empty / q_full, MMA span, epilogue (warp 4) wait on
+    // acc_full, epilogue span, producer waits on k_empty / q_empty.
+    long long* probe;
     // filled by the launcher: dense piece-major work list. Piece p (key tiles
     // [p*tpp, (p+1)*tpp)) is live for the query blocks qb >= nqb - count_p,
     // count_p = (piece_start[p+1] - piece_start[p]) / batch.

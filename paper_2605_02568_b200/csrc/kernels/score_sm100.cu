@@ -60,8 +60,8 @@ constexpr int kWBufs = 3;                                        // see the prod
 constexpr uint32_t kBarOffset = kWOffset + kWBufs * kWBufBytes;  // + 6 KiB
 constexpr uint32_t kSmemBytes = kBarOffset + 512 + 1024;         // barriers, items, align slack
 
-constexpr int kNumThreads = 384;  // 4 control warps + 8 epilogue warps
-constexpr int kEpiWarps = 8;
+constexpr int kNumThreads = 640;  // 4 control warps + 16 epilogue warps
+constexpr int kEpiWarps = 16;     // 4 per TMEM lane quarter, one query of each group each
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kIdesc = idesc_bf16_f32(kBlockKeys, kUmmaN);
 
@@ -99,23 +99,35 @@ __device__ __forceinline__ void decode_item(const ScoreTcParams& p, int idx, Ite
 // (FMNMX), 16 heads as x + |x| = 2 relu(x) on the FMA pipe (scaled back by
 // an exact 0.5 at the end), and all products go through packed FFMA2 into
 // five independent chains, balancing the two pipes.
-__device__ __forceinline__ float head_reduce(const float (&v)[64], const float* __restrict__ wq) {
+//
+// The 64 columns are read from TMEM in four 16-column slices so the whole
+// epilogue fits the 96 registers a 640-thread CTA allows; four epilogue
+// warps per sub-partition hide the extra load latency. Chain assignment and
+// order do not depend on the slicing.
+__device__ __forceinline__ float head_reduce_tmem(uint32_t taddr, const float* __restrict__ wq) {
     float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, d0 = a0, d1 = a0;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        const float4 w4 = *reinterpret_cast<const float4*>(wq + 4 * j);
-        const float x0 = v[4 * j], x1 = v[4 * j + 1], x2 = v[4 * j + 2], x3 = v[4 * j + 3];
-        if ((j & 3) == 3) {
-            const float2 r01 = make_float2(x0 + fabsf(x0), x1 + fabsf(x1));
-            const float2 r23 = make_float2(x2 + fabsf(x2), x3 + fabsf(x3));
-            d0 = __ffma2_rn(r01, make_float2(w4.x, w4.y), d0);
-            d1 = __ffma2_rn(r23, make_float2(w4.z, w4.w), d1);
-        } else {
-            const float2 r01 = make_float2(fmaxf(x0, 0.f), fmaxf(x1, 0.f));
-            const float2 r23 = make_float2(fmaxf(x2, 0.f), fmaxf(x3, 0.f));
-            float2& acc = (j & 3) == 0 ? a0 : ((j & 3) == 1 ? a1 : a2);
-            acc = __ffma2_rn(r01, make_float2(w4.x, w4.y), acc);
-            acc = __ffma2_rn(r23, make_float2(w4.z, w4.w), acc);
+    for (int part = 0; part < 4; ++part) {
+        float v[16];
+        tmem_ld16(taddr + part * 16, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+            const int j = part * 4 + jj;
+            const float4 w4 = *reinterpret_cast<const float4*>(wq + 4 * j);
+            const float x0 = v[4 * jj], x1 = v[4 * jj + 1], x2 = v[4 * jj + 2], x3 = v[4 * jj + 3];
+            if ((j & 3) == 3) {
+                const float2 r01 = make_float2(x0 + fabsf(x0), x1 + fabsf(x1));
+                const float2 r23 = make_float2(x2 + fabsf(x2), x3 + fabsf(x3));
+                d0 = __ffma2_rn(r01, make_float2(w4.x, w4.y), d0);
+                d1 = __ffma2_rn(r23, make_float2(w4.z, w4.w), d1);
+            } else {
+                const float2 r01 = make_float2(fmaxf(x0, 0.f), fmaxf(x1, 0.f));
+                const float2 r23 = make_float2(fmaxf(x2, 0.f), fmaxf(x3, 0.f));
+                float2& acc = (j & 3) == 0 ? a0 : ((j & 3) == 1 ? a1 : a2);
+                acc = __ffma2_rn(r01, make_float2(w4.x, w4.y), acc);
+                acc = __ffma2_rn(r23, make_float2(w4.z, w4.w), acc);
+            }
         }
     }
     const float main = ((a0.x + a0.y) + (a1.x + a1.y)) + (a2.x + a2.y);
@@ -147,6 +159,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     Item* items = reinterpret_cast<Item*>(bars + 14 + 2 * kItemSlots + kWBufs);  // [kItemSlots]
 
     const int warp = threadIdx.x / 32;
+    long long* const probe = p.probe;  // optional per-CTA wait-cycle counters (profiling)
 
     if (warp == 0 && elect_one()) {
         tma_prefetch(&qmap);
@@ -181,6 +194,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         if (elect_one()) {
             const uint64_t keep = policy_evict_last();  // keys are re-read by every query block
             uint32_t kiter = 0, qiter = 0;
+            long long pw_k = 0, pw_q = 0;
             for (uint32_t it_iter = 0;; ++it_iter) {
                 const uint32_t slot = it_iter % kItemSlots;
                 mbar_wait(&item_empty[slot], ((it_iter / kItemSlots) & 1) ^ 1);
@@ -190,6 +204,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                     it.kt_begin = -1;
                     items[slot] = it;
                     mbar_arrive(&item_full[slot]);
+                    if (probe) {
+                        probe[blockIdx.x * 8 + 6] = pw_k;
+                        probe[blockIdx.x * 8 + 7] = pw_q;
+                    }
                     break;
                 }
                 decode_item(p, idx, it);
@@ -204,7 +222,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                 const int32_t qrow = static_cast<int32_t>(qrow64 * kHeads);
                 const uint32_t qpar = (qiter & 1) ^ 1;
                 auto load_group = [&](int g) {
+                    const long long c0 = probe ? clock64() : 0;
                     mbar_wait(&q_empty[g], qpar);
+                    if (probe) pw_q += clock64() - c0;
                     mbar_expect_tx(&q_full[g], kQGroupBytes);
                     for (int hf = 0; hf < 2; ++hf) {
                         tma_load_2d(q_smem + g * kQGroupBytes + hf * kQHalfBytes, &qmap, &q_full[g], hf * 64,
@@ -222,7 +242,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                 const int64_t krow0 = static_cast<int64_t>(it.b) * p.key_blocks + p.t0;
                 for (int kt = it.kt_begin; kt < it.kt_end; ++kt) {
                     const uint32_t s = kiter % kStages;
+                    const long long c0 = probe ? clock64() : 0;
                     mbar_wait(&k_empty[s], ((kiter / kStages) & 1) ^ 1);
+                    if (probe) pw_k += clock64() - c0;
                     mbar_expect_tx(&k_full[s], kKStageBytes);
                     const int32_t krow = static_cast<int32_t>(krow0 + static_cast<int64_t>(kt) * p.kt_stride * kBlockKeys);
                     for (int hf = 0; hf < 2; ++hf) {
@@ -239,6 +261,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         // ------------------------------------------------ MMA issuer
         if (elect_one()) {
             uint32_t kiter = 0, qiter = 0, aiter = 0;
+            long long mw_k = 0, mw_acc = 0, mw_q = 0;
+            const long long m_start = probe ? clock64() : 0;
             const uint32_t q_base = smem_u32(q_smem);
             const uint32_t k_base = smem_u32(k_smem);
             for (uint32_t it_iter = 0;; ++it_iter) {
@@ -246,20 +270,34 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                 mbar_wait(&item_full[slot], (it_iter / kItemSlots) & 1);
                 const Item it = items[slot];
                 mbar_arrive(&item_empty[slot]);
-                if (it.kt_begin < 0) break;
+                if (it.kt_begin < 0) {
+                    if (probe) {
+                        probe[blockIdx.x * 8 + 0] = mw_k;
+                        probe[blockIdx.x * 8 + 1] = mw_acc;
+                        probe[blockIdx.x * 8 + 2] = mw_q;
+                        probe[blockIdx.x * 8 + 3] = clock64() - m_start;
+                    }
+                    break;
+                }
                 const uint32_t qpar = qiter & 1;
                 ++qiter;
                 for (int kt = it.kt_begin; kt < it.kt_end; ++kt) {
                     const uint32_t s = kiter % kStages;
+                    long long c0 = probe ? clock64() : 0;
                     mbar_wait(&k_full[s], (kiter / kStages) & 1);
+                    if (probe) mw_k += clock64() - c0;
                     tc_fence_after();
                     for (int g = 0; g < kGroups; ++g) {
                         if (kt == it.kt_begin) {
+                            if (probe) c0 = clock64();
                             mbar_wait(&q_full[g], qpar);
+                            if (probe) mw_q += clock64() - c0;
                             tc_fence_after();
                         }
                         const uint32_t a = aiter & 1;
+                        if (probe) c0 = clock64();
                         mbar_wait(&acc_empty[a], ((aiter >> 1) & 1) ^ 1);
+                        if (probe) mw_acc += clock64() - c0;
                         tc_fence_after();
                         const uint32_t d_tmem = tmem_base + a * kUmmaN;
 #pragma unroll
@@ -280,11 +318,16 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue
-        const int quarter = warp & 3;           // TMEM lane quarter this warp may touch
-        const int qpair = (warp - 4) >> 2;      // which two queries of each group
+        // 16 warps: warp w reads TMEM lanes 32*(w % 4).. (its key quarter)
+        // and owns query qsel = (w - 4) / 4 of every 4-query group, so each
+        // accumulator is drained by 4 warps per SM sub-partition.
+        const int quarter = warp & 3;
+        const int qsel = (warp - 4) >> 2;
         const uint32_t lane = lane_id();
-        const uint32_t row_taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
+        const uint32_t row_taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + qsel * kHeads;
         uint32_t aiter = 0, qiter = 0;
+        long long ew_acc = 0;
+        const long long e_start = probe ? clock64() : 0;
         const float neg_inf = -__int_as_float(0x7f800000);
         for (uint32_t it_iter = 0;; ++it_iter) {
             const uint32_t slot = it_iter % kItemSlots;
@@ -292,30 +335,33 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             const Item it = items[slot];
             __syncwarp();
             if (lane == 0) mbar_arrive(&item_empty[slot]);
-            if (it.kt_begin < 0) break;
+            if (it.kt_begin < 0) {
+                if (probe && warp == 4 && lane == 0) {
+                    probe[blockIdx.x * 8 + 4] = ew_acc;
+                    probe[blockIdx.x * 8 + 5] = clock64() - e_start;
+                }
+                break;
+            }
             const uint32_t wb = qiter % kWBufs;
             const float* w_item = w_smem + wb * (kQPerItem * kHeads);
-            // Per-item constants of this thread's 4 queries: output row and
-            // the causal limit (first illegal column, relative to t0).
-            float* orow[kGroups][2];
-            int lim[kGroups][2];
-            float tq[kGroups][2];  // candidate thresholds (filter mode)
+            // Per-item constants of this warp's 2 queries (one per group):
+            // output row and the causal limit (first illegal column, t0-relative).
+            float* orow[kGroups];
+            int lim[kGroups];
+            float tq[kGroups];  // candidate thresholds (filter mode)
 #pragma unroll
             for (int g = 0; g < kGroups; ++g) {
-#pragma unroll
-                for (int qq = 0; qq < 2; ++qq) {
-                    const int qi = g * kQPerGroup + qpair * 2 + qq;
-                    const int64_t r = it.r0 + qi;
-                    const int64_t grow = static_cast<int64_t>(it.b) * p.rows + r;
-                    orow[g][qq] = p.out + grow * p.ld;
-                    int64_t l = p.cols;
-                    if (p.apply_mask) {
-                        l = t_legal_dev(p.s0 + r, p.ratio) - p.t0;
-                        l = l < 0 ? 0 : (l > p.cols ? p.cols : l);
-                    }
-                    lim[g][qq] = static_cast<int>(l);
-                    tq[g][qq] = (p.tau != nullptr && qi < it.nrows) ? p.tau[grow] : 0.f;
+                const int qi = g * kQPerGroup + qsel;
+                const int64_t r = it.r0 + qi;
+                const int64_t grow = static_cast<int64_t>(it.b) * p.rows + r;
+                orow[g] = p.out + grow * p.ld;
+                int64_t l = p.cols;
+                if (p.apply_mask) {
+                    l = t_legal_dev(p.s0 + r, p.ratio) - p.t0;
+                    l = l < 0 ? 0 : (l > p.cols ? p.cols : l);
                 }
+                lim[g] = static_cast<int>(l);
+                tq[g] = (p.tau != nullptr && qi < it.nrows) ? p.tau[grow] : 0.f;
             }
             mbar_wait(&w_full[wb], (qiter / kWBufs) & 1);
             ++qiter;
@@ -327,25 +373,22 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 #pragma unroll
                 for (int g = 0; g < kGroups; ++g) {
                     const uint32_t a = aiter & 1;
+                    const long long c0 = probe ? clock64() : 0;
                     mbar_wait(&acc_full[a], (aiter >> 1) & 1);
+                    if (probe) ew_acc += clock64() - c0;
                     tc_fence_after();
-#pragma unroll
-                    for (int qq = 0; qq < 2; ++qq) {
-                        const int qi = g * kQPerGroup + qpair * 2 + qq;   // query within item
-                        if (qi >= it.nrows) continue;                      // warp-uniform
-                        float v[64];
-                        tmem_ld64(row_taddr + a * kUmmaN + (qpair * 2 + qq) * kHeads, v);
-                        tmem_ld_wait();
-                        const float acc = head_reduce(v, w_item + qi * kHeads);
-                        const bool legal = j < lim[g][qq];
+                    const int qi = g * kQPerGroup + qsel;  // query within item
+                    if (qi < it.nrows) {                   // warp-uniform
+                        const float acc = head_reduce_tmem(row_taddr + a * kUmmaN, w_item + qi * kHeads);
+                        const bool legal = j < lim[g];
                         if (jo < out_cols) {
                             if (legal && !isfinite(acc)) atomicOr(p.nonfinite, 1);
-                            orow[g][qq][jo] = legal ? acc : neg_inf;
+                            orow[g][jo] = legal ? acc : neg_inf;
                         }
                         if (p.tau != nullptr) {
                             // fused select pre-filter: one candidate word per
                             // warp (32 consecutive key columns)
-                            const uint32_t m = __ballot_sync(0xffffffffu, legal && acc >= tq[g][qq]);
+                            const uint32_t m = __ballot_sync(0xffffffffu, legal && acc >= tq[g]);
                             if (lane == 0) {
                                 const int64_t grow = static_cast<int64_t>(it.b) * p.rows + it.r0 + qi;
                                 p.pass_bits[grow * p.bits_ld + (jo >> 5)] = m;
