@@ -189,6 +189,19 @@ int csaidx_cuda_select_from_candidates(csaidx_engine* e, const float* scores, in
                                        const uint32_t* pass_bits, int64_t bits_ld, float* out_val,
                                        int32_t* out_idx, int64_t out_ld);
 
+/* tile_topk (topk.cpp:105-132) fused with the sentinel pass of
+ * process_query_tile (driver.cpp:84-105), for query tiles whose single key
+ * tile covers every key (t0 = 0, cols = T): with one tile the merge into the
+ * all-sentinel TopKBuffer is a copy, so each row's exact top-min(k, n) goes
+ * straight to out_idx/out_val[b, out_row0 + i, 0..k) (int64, fp32), sorted
+ * under succ, the rest (-inf, -1). pass_bits: optional candidate bitmap of
+ * csaidx_cuda_score_filtered (NULL = stream the scores). Replaces
+ * select + finalize (two launches and the int32 run buffer round trip). */
+int csaidx_cuda_select_final(csaidx_engine* e, const float* scores, int64_t batch, int64_t rows,
+                             int64_t ld, int64_t cols, int64_t s0, int64_t t0, int64_t ratio,
+                             int64_t k, const uint32_t* pass_bits, int64_t bits_ld,
+                             int64_t* out_idx, float* out_val, int64_t out_rows, int64_t out_row0);
+
 /* merge_topk / overwrite_topk (topk.hpp:73-82, topk.cpp:134-191) over nrows
  * running rows of k entries. check_overlap latches the reference's
  * overlapping-index error. */

@@ -133,6 +133,11 @@ CUDA_SYMBOLS = {
         [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64,
          c_void_p, c_int64, c_void_p, c_void_p, c_int64],
     ),
+    "csaidx_cuda_select_final": (
+        c_int,
+        [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64,
+         c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int64],
+    ),
     "csaidx_cuda_merge": (
         c_int,
         [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_int64, c_int64, c_int, c_int],

@@ -623,13 +623,14 @@ namespace {
 
 int select_impl(csaidx_engine* e, const float* scores, int64_t batch, int64_t rows, int64_t ld, int64_t cols,
                 int64_t s0, int64_t t0, int64_t ratio, int apply_mask, int64_t k, float* cand_val, int32_t* cand_idx,
-                int64_t cand_ld, const uint32_t* pass_bits, int64_t bits_ld) {
+                int64_t cand_ld, const uint32_t* pass_bits, int64_t bits_ld, int64_t* final_idx = nullptr,
+                int64_t final_rows = 0, int64_t final_row0 = 0) {
     if (int rc = set_device(e)) return rc;
     if (k < 1) return fail(CSAIDX_INVALID_ARGUMENT, "tile_topk: top_k must be >= 1");
     if (rows < 1 || cols < 1 || batch < 1 || ratio < 1) return fail(CSAIDX_INVALID_ARGUMENT, "select: bad extents");
     if ((ld % 4) != 0 || ld < cols) return fail(CSAIDX_INVALID_ARGUMENT, "select: ld must be >= cols, multiple of 4");
     if ((reinterpret_cast<uintptr_t>(scores) & 15) != 0) return fail(CSAIDX_INVALID_ARGUMENT, "select: scores not 16B aligned");
-    const int64_t width = k < cols ? k : cols;
+    const int64_t width = final_idx != nullptr ? k : (k < cols ? k : cols);
     if (width > csaidx_kern::select_max_take())
         return fail(CSAIDX_INVALID_ARGUMENT, "tile_topk: min(k, cols) = %lld exceeds the GPU select capacity %d",
                     static_cast<long long>(width), csaidx_kern::select_max_take());
@@ -654,6 +655,9 @@ int select_impl(csaidx_engine* e, const float* scores, int64_t batch, int64_t ro
     p.pass_bits = pass_bits;
     p.bits_ld = bits_ld;
     p.cand_hits = e->flags + kNumFlags + 3;
+    p.final_idx = final_idx;
+    p.final_rows = final_rows;
+    p.final_row0 = final_row0;
     LaunchScope ls(e, CSAIDX_KIND_SELECT);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_select(p, e->stream), "select");
     return CSAIDX_OK;
@@ -679,6 +683,18 @@ int csaidx_cuda_select_from_candidates(csaidx_engine* e, const float* scores, in
         return fail(CSAIDX_INVALID_ARGUMENT, "select_from_candidates: bits_ld < csaidx_cuda_candidate_words(cols)");
     return select_impl(e, scores, batch, rows, ld, cols, s0, t0, ratio, 1, k, out_val, out_idx, out_ld, pass_bits,
                        bits_ld);
+}
+
+int csaidx_cuda_select_final(csaidx_engine* e, const float* scores, int64_t batch, int64_t rows, int64_t ld,
+                             int64_t cols, int64_t s0, int64_t t0, int64_t ratio, int64_t k, const uint32_t* pass_bits,
+                             int64_t bits_ld, int64_t* out_idx, float* out_val, int64_t out_rows, int64_t out_row0) {
+    if (out_idx == nullptr || out_val == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "select_final: null output");
+    if (out_row0 < 0 || out_row0 + rows > out_rows)
+        return fail(CSAIDX_INVALID_ARGUMENT, "select_final: rows out of range");
+    if (pass_bits != nullptr && bits_ld < csaidx_cuda_candidate_words(cols))
+        return fail(CSAIDX_INVALID_ARGUMENT, "select_final: bits_ld < csaidx_cuda_candidate_words(cols)");
+    return select_impl(e, scores, batch, rows, ld, cols, s0, t0, ratio, 1, k, out_val, nullptr, k, pass_bits, bits_ld,
+                       out_idx, out_rows, out_row0);
 }
 
 int csaidx_cuda_merge(csaidx_engine* e, float* run_val, int32_t* run_idx, int64_t nrows, int64_t k,

@@ -97,7 +97,13 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
         const int64_t rows = std::min(plan.cs, dims.seq_len - s0);
         if (hooks.before) hooks.before(c);
         LedgerCharge buffer_charge(ledger, "topk_buffer", run_buffer_bytes(B, rows, k));
-        check(csaidx_cuda_fill_sentinel(e, run_v.as<float>(), run_i.as<int32_t>(), B * rows * k));
+        // One key tile covering all T keys: its select is a copy into the
+        // all-sentinel buffer followed by the sentinel pass, so it writes the
+        // output rows directly (csaidx_cuda_select_final) and the buffer is
+        // only initialised if the tile ends up skipped.
+        const bool one_tile = plan.ct >= T;
+        bool finalized = false;
+        if (!one_tile) check(csaidx_cuda_fill_sentinel(e, run_v.as<float>(), run_i.as<int32_t>(), B * rows * k));
         bool first = true;
         for (int64_t t0 = 0; t0 < T; t0 += plan.ct) {
             const int64_t cols = std::min(plan.ct, T - t0);
@@ -144,7 +150,12 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
                     check(csaidx_cuda_select(e, scores.as<float>(), B, rows, ld, cols, s0, t0, dims.ratio, 1, k, v, i,
                                              out_ld));
             };
-            if (first && width == k) {
+            if (one_tile) {
+                check(csaidx_cuda_select_final(e, scores.as<float>(), B, rows, ld, cols, s0, t0, dims.ratio, k,
+                                               filtered ? pf_bits.as<uint32_t>() : nullptr, bits_ld, out_idx, out_val,
+                                               out_rows, plan.out_row0[c]));
+                finalized = true;
+            } else if (first && width == k) {
                 // merge into all-sentinel rows (or A1 overwrite) == copy
                 select(run_v.as<float>(), run_i.as<int32_t>(), k);
             } else {
@@ -154,9 +165,12 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
             }
             first = false;
         }
-        check(csaidx_cuda_finalize(e, run_v.as<float>(), run_i.as<int32_t>(), B, rows, s0, dims.ratio, k,
-                                   config.ablation == Ablation::none ? 1 : 0, out_idx, out_val, out_rows,
-                                   plan.out_row0[c]));
+        if (!finalized) {
+            if (one_tile) check(csaidx_cuda_fill_sentinel(e, run_v.as<float>(), run_i.as<int32_t>(), B * rows * k));
+            check(csaidx_cuda_finalize(e, run_v.as<float>(), run_i.as<int32_t>(), B, rows, s0, dims.ratio, k,
+                                       config.ablation == Ablation::none ? 1 : 0, out_idx, out_val, out_rows,
+                                       plan.out_row0[c]));
+        }
         if (hooks.after) hooks.after(c);
     }
     check(csaidx_engine_check(e));

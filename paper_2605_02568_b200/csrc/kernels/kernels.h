@@ -83,6 +83,12 @@ struct SelectParams {
     const uint32_t* pass_bits;  // [B, rows, bits_ld]
     int64_t bits_ld;
     int* cand_hits;       // rows finished from the bitmap (telemetry)
+    // Optional fused sentinel pass (the finalize_kernel contract, for plans
+    // whose one key tile covers every key): row r of batch b is written to
+    // out_val / final_idx + (b * final_rows + final_row0 + r) * out_ld with
+    // int64 indices; entries past min(k, n) are (-inf, -1).
+    int64_t* final_idx;
+    int64_t final_rows, final_row0;
 };
 
 // Per-row candidate threshold from a strided sample of the row's scores

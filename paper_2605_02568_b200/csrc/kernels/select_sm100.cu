@@ -9,15 +9,18 @@
 // order (topk.hpp:23-26).
 //
 // Fast path (one streaming pass over the row):
-//   1. sample: evenly spaced 128-byte lines (<= 1/16 of the row); two
-//      histogram passes below the sample's common key prefix pick a
-//      threshold expected to keep ~1.5k entries of the row;
+//   1. sample: evenly spaced 128-byte lines (<= 1/16 of the row), held in
+//      registers; a value-linear histogram over the sample's range (plus a
+//      refinement pass inside a coarse rank bin) picks a threshold expected
+//      to keep ~2k entries of the row;
 //   2. filter: the row is streamed once (4 x float4 per thread in flight);
 //      survivors are appended to a shared candidate list with one warp scan
-//      and one shared atomic per warp;
-//   3. if the list holds between k and its capacity, every candidate is
-//      sorted (unique composites: a total order) by a register/shuffle
-//      bitonic sort and the first k are written.
+//      and one shared atomic per warp, and counted into value-linear
+//      buckets over [threshold, sample max];
+//   3. if the list holds between k and its capacity, the bucket finish
+//      (descending scan, scatter of the buckets above rank k, rank inside
+//      each small bucket) writes the top k sorted. Degenerate buckets (heavy
+//      ties) take a shared-memory radix select + bitonic sort instead.
 // When the sample mispredicts (fewer than k or more than capacity survivors)
 // the row falls back to an exact MSB-first radix select over global memory
 // with index-ordered tie collection. Rows with n <= capacity skip sampling.
@@ -39,9 +42,12 @@ constexpr int kMaxTake = 4096;    // largest min(k, n) a row may select
 constexpr int kMaxCand = 8192;    // largest shared candidate list
 constexpr int kSampleLines = 256;  // <= 8192 sampled keys per row
 
+constexpr int kFinBins = 1024;   // value-linear buckets of the bucket finish
+constexpr int kMaxBucket = 128;  // largest bucket the finish ranks pairwise
+
 struct Layout {
     int cand_cap;  // power of two, >= 2k
-    int buf_cap;   // power of two, >= k
+    int buf_cap;   // >= pow2(k) (radix path) and >= k + kMaxBucket (bucket finish)
 };
 
 __host__ __device__ inline int pow2_at_least(int x) {
@@ -55,6 +61,7 @@ __host__ __device__ inline Layout layout_for(int k) {
     int c = pow2_at_least(3 * k);
     l.cand_cap = c < 2048 ? 2048 : (c > kMaxCand ? kMaxCand : c);
     l.buf_cap = pow2_at_least(k);
+    if (l.buf_cap < k + kMaxBucket) l.buf_cap = k + kMaxBucket;
     return l;
 }
 
@@ -263,6 +270,114 @@ __device__ void smem_take_top(const uint64_t* a, int n, uint32_t kk, uint64_t* d
     __syncthreads();
 }
 
+// Value-linear bucket of a composite between the list's min (lo) and max.
+__device__ __forceinline__ int fin_bin(uint64_t c, float lo, float scale) {
+    const float v = ord_key_to_float(static_cast<uint32_t>(c >> 32));
+    return static_cast<int>(fminf(fmaxf((v - lo) * scale, 0.f), static_cast<float>(kFinBins - 1)));
+}
+
+// The top `take` of the unique composites a[0, n), sorted best first, into
+// a[0, take): one histogram over kFinBins buckets linear in the score value
+// (monotone, so bucket order is score order), a descending scan, a scatter
+// of only the buckets that start above rank `take` into tmp[], and each
+// scattered element's rank inside its bucket by pairwise comparison (buckets
+// hold a few entries). Replaces a radix select + a k-wide bitonic sort.
+// Returns false with a[] untouched when a needed bucket exceeds kMaxBucket
+// or tmp[] (heavy ties, degenerate ranges); the caller then takes the radix
+// path. start/cur: kFinBins words each; sc: 4 scratch words.
+__device__ bool bucket_finish(uint64_t* a, int n, int take, uint64_t* tmp, int tmp_cap, uint32_t* start,
+                              uint32_t* cur, uint32_t* wsum, uint32_t* sc, bool prebuilt, float pb_lo,
+                              float pb_scale) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        sc[0] = 0xffffffffu;  // min key
+        sc[1] = 0u;           // max key
+        sc[2] = 0u;           // overflow flag
+        sc[3] = 0u;           // scattered extent
+    }
+    float lo = pb_lo, scale = pb_scale;
+    if (!prebuilt) {
+        for (int i = threadIdx.x; i < kFinBins; i += blockDim.x) start[i] = 0;
+        uint32_t kmin = 0xffffffffu, kmax = 0u;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const uint32_t key = static_cast<uint32_t>(a[i] >> 32);
+            kmin = min(kmin, key);
+            kmax = max(kmax, key);
+        }
+        kmin = __reduce_min_sync(0xffffffffu, kmin);
+        kmax = __reduce_max_sync(0xffffffffu, kmax);
+        __syncthreads();
+        if (lane == 0) {
+            atomicMin(&sc[0], kmin);
+            atomicMax(&sc[1], kmax);
+        }
+        __syncthreads();
+        lo = ord_key_to_float(sc[0]);
+        const float hi = ord_key_to_float(sc[1]);
+        scale = static_cast<float>(kFinBins) / (hi - lo);
+        if (!(hi > lo) || !isfinite(scale)) scale = 0.f;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&start[fin_bin(a[i], lo, scale)], 1u);
+    }
+    __syncthreads();
+    // descending exclusive scan: thread t owns bins [NB-4t-4, NB-4t), highest first
+    constexpr int kPer = kFinBins / 256;
+    static_assert(kFinBins % 256 == 0, "bins per thread");
+    uint32_t c[kPer];
+    uint32_t sum = 0;
+    const int top = kFinBins - 1 - kPer * static_cast<int>(threadIdx.x);
+    if (threadIdx.x < 256) {
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            c[u] = start[top - u];
+            sum += c[u];
+        }
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    uint32_t before = 0;
+    for (int w = 0; w < warp; ++w) before += wsum[w];
+    if (threadIdx.x < 256) {
+        uint32_t run = before + incl - sum;
+        const uint32_t tk = static_cast<uint32_t>(take);
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int b = top - u;
+            start[b] = run;
+            cur[b] = run;
+            if (run < tk) {
+                if (c[u] > static_cast<uint32_t>(kMaxBucket) || run + c[u] > static_cast<uint32_t>(tmp_cap)) sc[2] = 1u;
+                if (run + c[u] >= tk) sc[3] = run + c[u];  // the bucket holding rank `take`
+            }
+            run += c[u];
+        }
+    }
+    __syncthreads();
+    if (sc[2] != 0u) return false;
+    const uint32_t extent = sc[3];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint64_t v = a[i];
+        const int b = fin_bin(v, lo, scale);
+        if (start[b] < static_cast<uint32_t>(take)) tmp[atomicAdd(&cur[b], 1u)] = v;
+    }
+    __syncthreads();
+    for (uint32_t s = threadIdx.x; s < extent; s += blockDim.x) {
+        const uint64_t v = tmp[s];
+        const int b = fin_bin(v, lo, scale);
+        const uint32_t b0 = start[b], b1 = cur[b];
+        uint32_t r = 0;
+        for (uint32_t j = b0; j < b1; ++j) r += tmp[j] > v ? 1u : 0u;
+        if (b0 + r < static_cast<uint32_t>(take)) a[b0 + r] = v;
+    }
+    __syncthreads();
+    return true;
+}
+
 // ------------------------------------------------------------------ fallback
 // Exact MSB-first radix select over global memory (any n, any ties): the
 // selected composites (unsorted) land in buf[0, k).
@@ -376,7 +491,6 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
     uint32_t* wsum = wtot + 4 * kWarps;                      // [kWarps] (find_bin)
     uint32_t* res = wsum + kWarps;                           // [8]
     uint32_t* counter = res + 4;
-    uint32_t* sample = reinterpret_cast<uint32_t*>(cand);    // aliases cand during sampling
 
     const int64_t row_id = blockIdx.x;
     const int b = blockIdx.y;
@@ -389,12 +503,14 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
     const int take = static_cast<int>(n < k ? n : k);
     const int lane = threadIdx.x & 31;
 
-    const uint64_t* result = buf;  // sorted selection, best first
+    const uint64_t* result = buf;  // sorted selection, best first (buf or cand)
     long long* clk = p.phase_clk != nullptr && threadIdx.x == 0 && b == 0 ? p.phase_clk + row_id * 8 : nullptr;
     if (clk) clk[0] = clock64();
     if (take > 0) {
         int count = -1;  // candidates in cand[], or -1 -> fallback
         int pre = -1;    // candidates flagged by the score epilogue, if usable
+        bool prebuilt = false;  // bucket-finish histogram built while streaming
+        float pb_lo = 0.f, pb_scale = 0.f;
         if (p.pass_bits != nullptr) {
             // The bitmap flags every legal score >= the row's tau; when the
             // flagged count lies in [take, cand_cap] the flagged entries
@@ -435,11 +551,10 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
             count = static_cast<int>(n);
             __syncthreads();
         } else {
-            // 1. sample evenly spaced 128-byte lines; each warp issues all
-            //    of its line loads before consuming them
+            // 1. sample evenly spaced 128-byte lines (kept in registers);
+            //    each warp issues all of its line loads before consuming them
             int nseg = static_cast<int>(n / 512);
             if (nseg > kSampleLines) nseg = kSampleLines;
-            if (nseg > L.cand_cap / 16) nseg = L.cand_cap / 16;  // 32 keys per line must fit in cand
             const int64_t seg_stride = n / nseg;
             constexpr int kLinesPerWarp = kSampleLines / kWarps;  // 32
             const int w = threadIdx.x >> 5;
@@ -452,16 +567,15 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
             uint32_t kmin = 0xffffffffu, kmax = 0u;
 #pragma unroll
             for (int u = 0; u < kLinesPerWarp; ++u) {
-                const int s = w + u * kWarps;
-                if (s < nseg) {
+                if (w + u * kWarps < nseg) {
                     const uint32_t key = ord_key(sv[u]);
-                    sample[32 * s + lane] = key;
                     kmin = min(kmin, key);
                     kmax = max(kmax, key);
                 }
             }
             if (threadIdx.x == 0) {
                 *counter = 0;
+                res[0] = res[1] = res[2] = 0u;  // find_bin leaves them when the rank is out of range
                 res[6] = 0xffffffffu;
                 res[7] = 0u;
             }
@@ -481,41 +595,56 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
             const int target = (2 * k < (L.cand_cap * 3) / 4) ? 2 * k : (L.cand_cap * 3) / 4;
             int r = static_cast<int>((static_cast<int64_t>(target) * ns) / n);
             if (r < 1) r = 1;
-            // Two 11-bit histogram passes below the sample's common key
-            // prefix locate the sample's rank-r key to 22 bits; the threshold
-            // is the lower edge of that fine bin.
-            const uint32_t lo = res[6], hi_k = res[7];
-            uint32_t prefix = 0;
-            int pbits = lo == hi_k ? 32 : __clz(lo ^ hi_k);
-            if (pbits > 0) prefix = pbits == 32 ? lo : (lo >> (32 - pbits));
+            // The sample's rank-r value by value-linear histograms over
+            // [sample min, sample max]: one pass, plus a refinement pass
+            // inside the rank-r bin when that bin is coarse (outliers,
+            // heavy tails). tau = the lower edge of the final bin.
+            const float smin = ord_key_to_float(res[6]), smax = ord_key_to_float(res[7]);
+            float lo = smin, hi = smax;
             uint32_t rr = static_cast<uint32_t>(r);
+            float tau_f = smin;
 #pragma unroll 1
-            for (int pass = 0; pass < 2 && pbits < 32; ++pass) {
-                const int wbits = 32 - pbits < 11 ? 32 - pbits : 11;
-                const int shift = 32 - pbits - wbits;
+            for (int pass = 0; pass < 2; ++pass) {
+                float scale = static_cast<float>(kBins) / (hi - lo);
+                if (!(hi > lo) || !isfinite(scale)) break;  // degenerate: keep tau = lo
                 if (pass > 0) {
                     for (int i = threadIdx.x; i < kBins; i += blockDim.x) hist[i] = 0;
+                    if (threadIdx.x == 0) res[0] = res[1] = res[2] = 0u;
                     __syncthreads();
                 }
-                for (int i = threadIdx.x; i < ns; i += blockDim.x) {
-                    const uint32_t v = sample[i];
-                    if (pbits == 0 || (v >> (32 - pbits)) == prefix)
-                        atomicAdd(&hist[(v >> shift) & ((1u << wbits) - 1u)], 1u);
+#pragma unroll
+                for (int u = 0; u < kLinesPerWarp; ++u) {
+                    const float v = sv[u];
+                    if (w + u * kWarps < nseg && v >= lo && v <= hi)
+                        atomicAdd(&hist[static_cast<int>(fminf((v - lo) * scale, static_cast<float>(kBins - 1)))], 1u);
                 }
                 __syncthreads();
-                find_bin(hist, 1 << wbits, rr, res, wsum);
-                rr -= res[1];
-                prefix = (pbits == 0 ? 0u : (prefix << wbits)) | res[0];
-                pbits += wbits;
+                find_bin(hist, kBins, rr, res, wsum);
+                const uint32_t bin = res[0], above = res[1], cnt = res[2];
                 __syncthreads();
+                const float width = (hi - lo) / static_cast<float>(kBins);
+                const float blo = lo + static_cast<float>(bin) * width;
+                tau_f = blo > lo ? blo : lo;
+                if (cnt * 8u <= rr || cnt <= 4u) break;  // fine enough
+                rr -= above;
+                hi = fminf(hi, blo + width);
+                lo = tau_f;
             }
-            const uint32_t tau = pbits >= 32 ? prefix : (prefix << (32 - pbits));
+            // scores are compared as floats: ord_key is monotone and folds
+            // -0.0 onto +0.0 exactly like the float order
+            if (tau_f == 0.f) tau_f = 0.f;  // -0.0 -> +0.0
+            const uint32_t tau = ord_key(tau_f);
+            // the finish histogram (value-linear over [tau, sample max]) is
+            // built while streaming
+            const float fin_lo = tau_f;
+            float fin_scale = static_cast<float>(kFinBins) / (smax - tau_f);
+            if (!(smax > tau_f) || !isfinite(fin_scale)) fin_scale = 0.f;
+            uint32_t* fin_hist = hist;
+            for (int i = threadIdx.x; i < kFinBins; i += blockDim.x) fin_hist[i] = 0;
+            __syncthreads();
 
             if (clk) clk[1] = clock64();
-            // 2. stream the row once; keep entries with key >= tau (a plain
-            //    float compare: ord_key is monotone and folds -0.0 onto +0.0
-            //    like the float order)
-            const float tau_f = ord_key_to_float(tau);
+            // 2. stream the row once; keep entries >= tau
             const float4* row4 = reinterpret_cast<const float4*>(row);
             const int64_t n4 = n >> 2;
             constexpr int kUnroll = 4;
@@ -549,7 +678,7 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
                 if (lane == 31) base = atomicAdd(counter, incl);
                 base = __shfl_sync(0xffffffffu, base, 31);
                 uint32_t pos = base + incl - c;
-                // Survivors are ~2% of entries: walk only the set bits (the
+                // Survivors are ~6% of entries: walk only the set bits (the
                 // warp iterates max-popc times, usually once or twice) and
                 // pick the element with selects, not an unrolled 16-way body.
                 while (m != 0) {
@@ -558,7 +687,11 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
                     const int u = bit >> 2, x = bit & 3;
                     const float4 vv = u == 0 ? v[0] : (u == 1 ? v[1] : (u == 2 ? v[2] : v[3]));
                     const float e = x == 0 ? vv.x : (x == 1 ? vv.y : (x == 2 ? vv.z : vv.w));
-                    if (pos < cap) cand[pos] = composite(ord_key(e), 4 * (it + u * blockDim.x) + x);
+                    if (pos < cap) {
+                        const uint64_t cc = composite(ord_key(e), 4 * (it + u * blockDim.x) + x);
+                        cand[pos] = cc;
+                        atomicAdd(&fin_hist[fin_bin(cc, fin_lo, fin_scale)], 1u);
+                    }
                     ++pos;
                 }
             }
@@ -573,32 +706,45 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
                     if (lane == 0) base = atomicAdd(counter, __popc(mm));
                     base = __shfl_sync(0xffffffffu, base, 0);
                     const uint32_t pos = base + __popc(mm & ((1u << lane) - 1u));
-                    if (pass && pos < cap) cand[pos] = composite(key, i);
+                    if (pass && pos < cap) {
+                        const uint64_t cc = composite(key, i);
+                        cand[pos] = cc;
+                        atomicAdd(&fin_hist[fin_bin(cc, fin_lo, fin_scale)], 1u);
+                    }
                 }
             }
             __syncthreads();
             const uint32_t total = *counter;
             count = (total >= static_cast<uint32_t>(k) && total <= cap) ? static_cast<int>(total) : -1;
+            prebuilt = true;
+            pb_lo = fin_lo;
+            pb_scale = fin_scale;
             __syncthreads();
         }
 
         if (clk) clk[2] = clock64();
         if (count >= 0) {
-            // 3. exactly `take` of the (unique) candidates by shared-memory
-            //    radix select, then one register/shuffle bitonic sort
-            if (count > take) {
-                smem_take_top(cand, count, static_cast<uint32_t>(take), buf, hist, res, wsum, counter);
-            } else {
-                for (int i = threadIdx.x; i < count; i += blockDim.x) buf[i] = cand[i];
-            }
-            const int P = pow2_at_least(take);
-            for (int i = take + threadIdx.x; i < P; i += blockDim.x) buf[i] = 0;
-            __syncthreads();
             if (clk) {
                 clk[6] = count;
                 clk[7] = clock64();
             }
-            sort_desc(buf, P);
+            // 3. the sorted top `take` of the (unique) candidates: bucket
+            //    finish, or (heavy ties) a shared-memory radix select + one
+            //    register/shuffle bitonic sort
+            if (bucket_finish(cand, count, take, buf, L.buf_cap, hist, hist + kFinBins, wsum, res, prebuilt, pb_lo,
+                              pb_scale)) {
+                result = cand;
+            } else {
+                if (count > take) {
+                    smem_take_top(cand, count, static_cast<uint32_t>(take), buf, hist, res, wsum, counter);
+                } else {
+                    for (int i = threadIdx.x; i < count; i += blockDim.x) buf[i] = cand[i];
+                }
+                const int P = pow2_at_least(take);
+                for (int i = take + threadIdx.x; i < P; i += blockDim.x) buf[i] = 0;
+                __syncthreads();
+                sort_desc(buf, P);
+            }
         } else {
             if (threadIdx.x == 0 && p.fallbacks != nullptr) atomicAdd(p.fallbacks, 1);
             exact_global_select(row, n, take, buf, cand, L.cand_cap, hist, wtot, res, wsum);
@@ -613,9 +759,28 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
         clk[3] = clock64();
         clk[4] = n;
     }
-    float* ov = p.out_val + (static_cast<int64_t>(b) * p.rows + row_id) * p.out_ld;
-    int32_t* oi = p.out_idx + (static_cast<int64_t>(b) * p.rows + row_id) * p.out_ld;
+    const bool final_out = p.final_idx != nullptr;
+    const int64_t orow = final_out ? static_cast<int64_t>(b) * p.final_rows + p.final_row0 + row_id
+                                   : static_cast<int64_t>(b) * p.rows + row_id;
+    float* ov = p.out_val + orow * p.out_ld;
     const float neg_inf = -__int_as_float(0x7f800000);
+    if (final_out) {
+        // fused sentinel pass (finalize_kernel): int64 indices, (-inf, -1) tail
+        int64_t* oi = p.final_idx + orow * p.out_ld;
+        for (int e = threadIdx.x; e < p.width; e += blockDim.x) {
+            if (e < take) {
+                const uint64_t c = result[e];
+                const float v = ord_key_to_float(static_cast<uint32_t>(c >> 32));
+                ov[e] = v;
+                oi[e] = v == neg_inf ? -1 : composite_col(c) + p.t0;
+            } else {
+                ov[e] = neg_inf;
+                oi[e] = -1;
+            }
+        }
+        return;
+    }
+    int32_t* oi = p.out_idx + orow * p.out_ld;
     for (int e = threadIdx.x; e < p.width; e += blockDim.x) {
         if (e < take) {
             const uint64_t c = result[e];

@@ -155,6 +155,14 @@ class Engine:
                                                           _p(idx), width))
         return val, idx
 
+    def select_final(self, scores, batch, rows, cols, s0, t0, ratio, k, out_idx, out_val, out_row0, bits=None):
+        """tile_topk + sentinel pass straight into int64/fp32 output rows [b, out_row0 + i, :k]."""
+        ld = scores.shape[-1]
+        check(self.lib.csaidx_cuda_select_final(self.handle, _p(scores), batch, rows, ld, cols, s0, t0, ratio, k,
+                                                _p(bits) if bits is not None else None,
+                                                bits.shape[-1] if bits is not None else 0, _p(out_idx), _p(out_val),
+                                                out_idx.shape[1], out_row0))
+
     def candidate_hits(self, reset: bool = True) -> int:
         n = c_int64(0)
         check(self.lib.csaidx_engine_candidate_hits(self.handle, byref(n), int(reset)))

@@ -188,6 +188,79 @@ def test_select_survives_adversarial_samples(engine, mode):
     assert np.array_equal(val.cpu().numpy().view(np.uint32), wv.view(np.uint32))
 
 
+@pytest.mark.parametrize("dist", ["lognormal_tail", "far_outlier", "signed_zeros", "ulp_range", "near_cut_dups",
+                                  "short_rows_mixed_sign"])
+def test_select_bucket_finish_distributions(engine, dist):
+    """Distributions aimed at the value-linear bucket finish: long tails,
+    one far outlier (nearly every candidate in one bucket -> radix path),
+    +0.0/-0.0 folding, ranges a few ulps wide, ties straddling rank k."""
+    rng = np.random.default_rng(11)
+    B, rows, cols, k = 1, 6, 40000, 1024
+    x = rng.normal(0, 1, (B, rows, cols)).astype(np.float32)
+    if dist == "lognormal_tail":
+        x = np.exp(2.5 * x).astype(np.float32)
+    elif dist == "far_outlier":
+        x[..., 123] = 3e30
+    elif dist == "signed_zeros":
+        x = np.where(x > 1.5, x, np.where(rng.random(x.shape) < 0.5, np.float32(0.0), np.float32(-0.0)))
+        x = x.astype(np.float32)
+    elif dist == "ulp_range":
+        base = np.float32(1.0)
+        x = (base + rng.integers(0, 6, x.shape).astype(np.float32) * np.finfo(np.float32).eps).astype(np.float32)
+    elif dist == "near_cut_dups":
+        x = np.round(x * 64) / 64
+    else:  # short rows: every legal row fits the candidate list outright
+        cols = 3000
+        x = x[..., :cols] - 0.5
+    x = np.ascontiguousarray(x.astype(np.float32))
+    ld = (cols + 3) // 4 * 4
+    pad = np.zeros((B, rows, ld), np.float32)
+    pad[:, :, :cols] = x
+    val, idx = engine.select(to_dev(pad), B, rows, cols, 10 ** 7, 0, 1, k)
+    engine.check()
+    wv, wi = ref_select(x, 10 ** 7, 0, 1, k)
+    assert np.array_equal(idx.cpu().numpy(), wi)
+    got = val.cpu().numpy()
+    assert np.array_equal(np.where(got == 0, 0, got), np.where(wv == 0, 0, wv))  # -0.0 is reported as +0.0
+
+
+@pytest.mark.parametrize("S,cols,k,m", [(4096, 1024, 512, 4), (6000, 1500, 100, 4), (700, 700, 1024, 1)])
+def test_select_final_equals_select_then_finalize(engine, S, cols, k, m):
+    """select_final (one key tile) == fill_sentinel + select + finalize, into
+    the caller's int64 rows at an offset, neighbouring rows untouched."""
+    rng = np.random.default_rng(S + k)
+    B, rows, s0 = 2, 37, S - 40
+    scores = rng.normal(0, 1, (B, rows, cols)).astype(np.float32)
+    ld = (cols + 3) // 4 * 4
+    pad = np.zeros((B, rows, ld), np.float32)
+    pad[:, :, :cols] = scores
+    dev = to_dev(pad)
+    out_rows, row0 = rows + 10, 4
+    oi = torch.full((B, out_rows, k), 77, dtype=torch.int64, device="cuda")
+    ov = torch.full((B, out_rows, k), 5.0, dtype=torch.float32, device="cuda")
+    engine.select_final(dev, B, rows, cols, s0, 0, m, k, oi, ov, row0)
+    engine.check()
+    run_v = torch.empty((B, rows, k), dtype=torch.float32, device="cuda")
+    run_i = torch.empty((B, rows, k), dtype=torch.int32, device="cuda")
+    engine.fill_sentinel(run_v, run_i)
+    if min(k, cols) == k:
+        v, i = engine.select(dev, B, rows, cols, s0, 0, m, k)
+        run_v.copy_(v)
+        run_i.copy_(i)
+    else:
+        v, i = engine.select(dev, B, rows, cols, s0, 0, m, k)
+        engine.merge(run_v, run_i, v, i)
+    wi = torch.full((B, out_rows, k), 77, dtype=torch.int64, device="cuda")
+    wv = torch.full((B, out_rows, k), 5.0, dtype=torch.float32, device="cuda")
+    engine.finalize(run_v, run_i, B, rows, s0, m, k, wi, wv, row0)
+    engine.check()
+    assert torch.equal(oi, wi)
+    assert torch.equal(ov.view(torch.int32), wv.view(torch.int32))
+    rv, ri = ref_select(scores, s0, 0, m, k)
+    got = oi[:, row0:row0 + rows, : rv.shape[-1]].cpu().numpy()
+    assert np.array_equal(got, ri.astype(np.int64))
+
+
 def test_select_all_equal_scores_take_smallest_indices(engine):
     B, rows, cols, k = 1, 3, 10000, 100
     scores = np.zeros((B, rows, cols), np.float32)
