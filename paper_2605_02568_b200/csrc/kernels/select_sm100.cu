@@ -9,14 +9,14 @@
 // order (topk.hpp:23-26).
 //
 // Fast path (one streaming pass over the row):
-//   1. sample: evenly spaced 128-byte lines (<= 1/16 of the row), held in
+//   1. sample: evenly spaced 512-byte segments (~1/16 of the row), held in
 //      registers; a value-linear histogram over the sample's range (plus a
 //      refinement pass inside a coarse rank bin) picks a threshold expected
 //      to keep ~2k entries of the row;
 //   2. filter: the row is streamed once (4 x float4 per thread in flight);
-//      survivors are appended to a shared candidate list with one warp scan
-//      and one shared atomic per warp, and counted into value-linear
-//      buckets over [threshold, sample max];
+//      survivors' columns are appended to a shared list with one warp scan
+//      and one shared atomic per warp; their scores are then gathered back
+//      (L2 hits) into 64-bit composites;
 //   3. if the list holds between k and its capacity, the bucket finish
 //      (descending scan, scatter of the buckets above rank k, rank inside
 //      each small bucket) writes the top k sorted. Degenerate buckets (heavy
@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "sm100_ptx.cuh"
@@ -40,7 +41,8 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kBins = 2048;
 constexpr int kMaxTake = 4096;    // largest min(k, n) a row may select
 constexpr int kMaxCand = 8192;    // largest shared candidate list
-constexpr int kSampleLines = 256;  // <= 8192 sampled keys per row
+constexpr int kGatherPer = 16;     // survivors per thread the fused gather handles (4096)
+constexpr int kSampleSegs = 64;    // 512-byte segments: <= 8192 sampled keys per row
 
 constexpr int kFinBins = 1024;   // value-linear buckets of the bucket finish
 constexpr int kMaxBucket = 128;  // largest bucket the finish ranks pairwise
@@ -284,10 +286,11 @@ __device__ __forceinline__ int fin_bin(uint64_t c, float lo, float scale) {
 // hold a few entries). Replaces a radix select + a k-wide bitonic sort.
 // Returns false with a[] untouched when a needed bucket exceeds kMaxBucket
 // or tmp[] (heavy ties, degenerate ranges); the caller then takes the radix
-// path. start/cur: kFinBins words each; sc: 4 scratch words.
+// path. start/cur: kFinBins words each; sc: 4 scratch words. With
+// `prebuilt` the caller has already counted a[] into start[] over the bins
+// (plo, pscale).
 __device__ bool bucket_finish(uint64_t* a, int n, int take, uint64_t* tmp, int tmp_cap, uint32_t* start,
-                              uint32_t* cur, uint32_t* wsum, uint32_t* sc, bool prebuilt, float pb_lo,
-                              float pb_scale) {
+                              uint32_t* cur, uint32_t* wsum, uint32_t* sc, bool prebuilt, float plo, float pscale) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
         sc[0] = 0xffffffffu;  // min key
@@ -295,7 +298,7 @@ __device__ bool bucket_finish(uint64_t* a, int n, int take, uint64_t* tmp, int t
         sc[2] = 0u;           // overflow flag
         sc[3] = 0u;           // scattered extent
     }
-    float lo = pb_lo, scale = pb_scale;
+    float lo = plo, scale = pscale;  // prebuilt: start[] already holds the histogram over (plo, pscale)
     if (!prebuilt) {
         for (int i = threadIdx.x; i < kFinBins; i += blockDim.x) start[i] = 0;
         uint32_t kmin = 0xffffffffu, kmax = 0u;
@@ -480,7 +483,8 @@ __device__ void exact_global_select(const float* row, int64_t n, int k, uint64_t
 
 // ------------------------------------------------------------------ kernel
 
-__global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams p) {
+template <int kUnroll, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const SelectParams p) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     const int k = p.k;
     const Layout L = layout_for(k);
@@ -509,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
     if (take > 0) {
         int count = -1;  // candidates in cand[], or -1 -> fallback
         int pre = -1;    // candidates flagged by the score epilogue, if usable
-        bool prebuilt = false;  // bucket-finish histogram built while streaming
+        bool prebuilt = false;  // finish histogram built by the gather
         float pb_lo = 0.f, pb_scale = 0.f;
         if (p.pass_bits != nullptr) {
             // The bitmap flags every legal score >= the row's tau; when the
@@ -551,26 +555,30 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
             count = static_cast<int>(n);
             __syncthreads();
         } else {
-            // 1. sample evenly spaced 128-byte lines (kept in registers);
-            //    each warp issues all of its line loads before consuming them
-            int nseg = static_cast<int>(n / 512);
-            if (nseg > kSampleLines) nseg = kSampleLines;
-            const int64_t seg_stride = n / nseg;
-            constexpr int kLinesPerWarp = kSampleLines / kWarps;  // 32
+            // 1. sample evenly spaced 512-byte segments (one float4 per lane,
+            //    ~1/16 of the row, <= 8192 values), held in registers; each
+            //    warp issues all of its loads before consuming them
+            int nseg = static_cast<int>(n / 2048);
+            if (nseg > kSampleSegs) nseg = kSampleSegs;
+            if (nseg < 1) nseg = 1;
+            const int64_t seg_stride = (n / nseg) & ~int64_t{3};
+            constexpr int kSegsPerWarp = kSampleSegs / kWarps;  // 8
             const int w = threadIdx.x >> 5;
-            float sv[kLinesPerWarp];
+            float4 sv[kSegsPerWarp];
 #pragma unroll
-            for (int u = 0; u < kLinesPerWarp; ++u) {
-                const int s = w + u * kWarps;
-                sv[u] = s < nseg ? __ldg(row + static_cast<int64_t>(s) * seg_stride + lane) : 0.f;
+            for (int u = 0; u < kSegsPerWarp; ++u) {
+                const int sg = w + u * kWarps;
+                sv[u] = sg < nseg ? __ldg(reinterpret_cast<const float4*>(row + sg * seg_stride) + lane)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
             }
             uint32_t kmin = 0xffffffffu, kmax = 0u;
 #pragma unroll
-            for (int u = 0; u < kLinesPerWarp; ++u) {
+            for (int u = 0; u < kSegsPerWarp; ++u) {
                 if (w + u * kWarps < nseg) {
-                    const uint32_t key = ord_key(sv[u]);
-                    kmin = min(kmin, key);
-                    kmax = max(kmax, key);
+                    const uint32_t k0 = ord_key(sv[u].x), k1 = ord_key(sv[u].y);
+                    const uint32_t k2 = ord_key(sv[u].z), k3 = ord_key(sv[u].w);
+                    kmin = min(kmin, min(min(k0, k1), min(k2, k3)));
+                    kmax = max(kmax, max(max(k0, k1), max(k2, k3)));
                 }
             }
             if (threadIdx.x == 0) {
@@ -589,7 +597,7 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
             }
             __syncthreads();
             if (clk) clk[5] = clock64();
-            const int ns = 32 * nseg;
+            const int ns = 128 * nseg;
             // ~2k survivors: a comfortable margin over k (misses -> the slow
             // exact fallback) while the shared list stays at <= 4k entries
             const int target = (2 * k < (L.cand_cap * 3) / 4) ? 2 * k : (L.cand_cap * 3) / 4;
@@ -613,10 +621,17 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
                     __syncthreads();
                 }
 #pragma unroll
-                for (int u = 0; u < kLinesPerWarp; ++u) {
-                    const float v = sv[u];
-                    if (w + u * kWarps < nseg && v >= lo && v <= hi)
-                        atomicAdd(&hist[static_cast<int>(fminf((v - lo) * scale, static_cast<float>(kBins - 1)))], 1u);
+                for (int u = 0; u < kSegsPerWarp; ++u) {
+                    if (w + u * kWarps < nseg) {
+                        const float vs[4] = {sv[u].x, sv[u].y, sv[u].z, sv[u].w};
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const float v = vs[c];
+                            if (v >= lo && v <= hi)
+                                atomicAdd(&hist[static_cast<int>(fminf((v - lo) * scale, static_cast<float>(kBins - 1)))],
+                                          1u);
+                        }
+                    }
                 }
                 __syncthreads();
                 find_bin(hist, kBins, rr, res, wsum);
@@ -634,23 +649,18 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
             // -0.0 onto +0.0 exactly like the float order
             if (tau_f == 0.f) tau_f = 0.f;  // -0.0 -> +0.0
             const uint32_t tau = ord_key(tau_f);
-            // the finish histogram (value-linear over [tau, sample max]) is
-            // built while streaming
-            const float fin_lo = tau_f;
-            float fin_scale = static_cast<float>(kFinBins) / (smax - tau_f);
-            if (!(smax > tau_f) || !isfinite(fin_scale)) fin_scale = 0.f;
-            uint32_t* fin_hist = hist;
-            for (int i = threadIdx.x; i < kFinBins; i += blockDim.x) fin_hist[i] = 0;
-            __syncthreads();
+            // survivors are recorded as column indices only (the composites
+            // are gathered after the pass); the list aliases buf + hist
+            uint32_t* idx_list = reinterpret_cast<uint32_t*>(buf);
 
             if (clk) clk[1] = clock64();
             // 2. stream the row once; keep entries >= tau
             const float4* row4 = reinterpret_cast<const float4*>(row);
             const int64_t n4 = n >> 2;
-            constexpr int kUnroll = 4;
             const int64_t step = kUnroll * static_cast<int64_t>(blockDim.x);
             const int64_t n4r = (n4 + step - 1) / step * step;
-            const uint32_t cap = static_cast<uint32_t>(L.cand_cap);
+            const uint32_t cap = static_cast<uint32_t>(
+                min(L.cand_cap, 2 * L.buf_cap + kBins));  // idx list capacity
             for (int64_t it = threadIdx.x; it < n4r; it += step) {
                 float4 v[kUnroll];
 #pragma unroll
@@ -679,19 +689,14 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
                 base = __shfl_sync(0xffffffffu, base, 31);
                 uint32_t pos = base + incl - c;
                 // Survivors are ~6% of entries: walk only the set bits (the
-                // warp iterates max-popc times, usually once or twice) and
-                // pick the element with selects, not an unrolled 16-way body.
+                // warp iterates max-popc times, usually 2-4) and record the
+                // column only: the divergent body stays a handful of
+                // instructions.
                 while (m != 0) {
                     const int bit = __ffs(m) - 1;
                     m &= m - 1;
-                    const int u = bit >> 2, x = bit & 3;
-                    const float4 vv = u == 0 ? v[0] : (u == 1 ? v[1] : (u == 2 ? v[2] : v[3]));
-                    const float e = x == 0 ? vv.x : (x == 1 ? vv.y : (x == 2 ? vv.z : vv.w));
-                    if (pos < cap) {
-                        const uint64_t cc = composite(ord_key(e), 4 * (it + u * blockDim.x) + x);
-                        cand[pos] = cc;
-                        atomicAdd(&fin_hist[fin_bin(cc, fin_lo, fin_scale)], 1u);
-                    }
+                    if (pos < cap)
+                        idx_list[pos] = static_cast<uint32_t>(4 * (it + (bit >> 2) * kThreads) + (bit & 3));
                     ++pos;
                 }
             }
@@ -706,19 +711,65 @@ __global__ void __launch_bounds__(kThreads, 4) select_kernel(const SelectParams 
                     if (lane == 0) base = atomicAdd(counter, __popc(mm));
                     base = __shfl_sync(0xffffffffu, base, 0);
                     const uint32_t pos = base + __popc(mm & ((1u << lane) - 1u));
-                    if (pass && pos < cap) {
-                        const uint64_t cc = composite(key, i);
-                        cand[pos] = cc;
-                        atomicAdd(&fin_hist[fin_bin(cc, fin_lo, fin_scale)], 1u);
-                    }
+                    if (pass && pos < cap) idx_list[pos] = static_cast<uint32_t>(i);
                 }
             }
             __syncthreads();
             const uint32_t total = *counter;
             count = (total >= static_cast<uint32_t>(k) && total <= cap) ? static_cast<int>(total) : -1;
-            prebuilt = true;
-            pb_lo = fin_lo;
-            pb_scale = fin_scale;
+            if (count >= 0 && count <= kGatherPer * kThreads) {
+                // gather the survivors' scores (just streamed: L2 hits) into
+                // composites and count them into the finish buckets over
+                // [tau, sample max] (entries above the sample max clamp into
+                // the top bucket)
+                uint32_t cc[kGatherPer];
+#pragma unroll
+                for (int g = 0; g < kGatherPer; ++g) {
+                    const int i = threadIdx.x + g * kThreads;
+                    cc[g] = i < count ? idx_list[i] : 0u;
+                }
+                __syncthreads();  // the list (aliasing hist) is consumed
+                for (int i = threadIdx.x; i < kFinBins; i += blockDim.x) hist[i] = 0;
+                pb_lo = tau_f;
+                pb_scale = static_cast<float>(kFinBins) / (smax - tau_f);
+                if (!(smax > tau_f) || !isfinite(pb_scale)) pb_scale = 0.f;
+                __syncthreads();
+#pragma unroll
+                for (int h = 0; h < kGatherPer; h += 8) {
+                    float vv[8];
+#pragma unroll
+                    for (int g = 0; g < 8; ++g)
+                        vv[g] = threadIdx.x + (h + g) * kThreads < count ? __ldg(row + cc[h + g]) : 0.f;
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) {
+                        const int i = threadIdx.x + (h + g) * kThreads;
+                        if (i < count) {
+                            const uint64_t c = composite(ord_key(vv[g]), cc[h + g]);
+                            cand[i] = c;
+                            atomicAdd(&hist[fin_bin(c, pb_lo, pb_scale)], 1u);
+                        }
+                    }
+                }
+                prebuilt = true;
+            } else if (count >= 0) {
+                constexpr int G = 8;
+                for (int base = threadIdx.x; base < count; base += G * kThreads) {
+                    uint32_t cc[G];
+                    float vv[G];
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        const int i = base + g * kThreads;
+                        cc[g] = i < count ? idx_list[i] : 0u;
+                    }
+#pragma unroll
+                    for (int g = 0; g < G; ++g) vv[g] = base + g * kThreads < count ? __ldg(row + cc[g]) : 0.f;
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        const int i = base + g * kThreads;
+                        if (i < count) cand[i] = composite(ord_key(vv[g]), cc[g]);
+                    }
+                }
+            }
             __syncthreads();
         }
 
@@ -897,18 +948,36 @@ cudaError_t launch_tau(const TauParams& p, cudaStream_t stream) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_select(const SelectParams& p, cudaStream_t stream) {
-    if (p.rows <= 0 || p.batch <= 0) return cudaSuccess;
+namespace {
+template <int U, int MB>
+cudaError_t launch_select_variant(const SelectParams& p, cudaStream_t stream) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(select_kernel<U, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem_bytes_for(kMaxTake)));
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     const dim3 grid(static_cast<unsigned>(p.rows), static_cast<unsigned>(p.batch));
-    select_kernel<<<grid, kThreads, smem_bytes_for(p.k), stream>>>(p);
+    select_kernel<U, MB><<<grid, kThreads, smem_bytes_for(p.k), stream>>>(p);
     return cudaGetLastError();
+}
+
+int select_variant() {
+    static int v = [] {
+        const char* s = getenv("CSAIDX_SELECT_VARIANT");  // A/B knob (dev): 0 = 8 x float4 / 3 CTAs, 1 = 4 x float4 / 4 CTAs
+        return s != nullptr ? atoi(s) : 0;
+    }();
+    return v;
+}
+}  // namespace
+
+cudaError_t launch_select(const SelectParams& p, cudaStream_t stream) {
+    if (p.rows <= 0 || p.batch <= 0) return cudaSuccess;
+    // 8 float4 in flight per thread, 3 CTAs per SM (measured faster than
+    // 4 x float4 at 4 CTAs per SM: scripts/probe_select.py)
+    if (select_variant() == 1) return launch_select_variant<4, 4>(p, stream);
+    return launch_select_variant<8, 3>(p, stream);
 }
 
 }  // namespace csaidx_kern
