@@ -41,7 +41,7 @@ WORKLOADS = {
     "c1": (1, 4096, 64, 128, 4, 512, 2048, None),
     "c2": (1, 65536, 64, 128, 4, 512, 2048, None),
     "c3": (1, 262144, 64, 128, 4, 1024, 2048, None),
-    "c4": (1, 1048576, 64, 128, 4, 1024, 2048, None),
+    "c4": (1, 1048576, 64, 128, 4, 1024, 1024, None),  # c_S=1024: rank 0 stays < 10 GB with the gathered [S,k]
     "c5": (2, 131072, 64, 128, 4, 1024, 2048, None),
 }
 FLOPS_PER_PAIR = 2 * 64 * 128
@@ -182,6 +182,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no e2e/baseline)")
+    ap.add_argument("--simulate-rank", default=None, metavar="R/N",
+                    help="measure rank R's shard of an N-GPU run on this one GPU (per-rank numbers)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: logic check of the N>1 path with several ranks on one GPU")
     args = ap.parse_args()
     wl = list(WORKLOADS[args.workload])
     if args.cs:
@@ -199,10 +203,14 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())  # gloo check: ranks share GPU 0
     torch.cuda.set_device(local)
+    backend = args.backend
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:  # logic check of the N>1 path on one GPU (collectives staged through host memory)
+            dist.init_process_group("gloo")
     stream = torch.cuda.Stream()  # all timed work and its events live on this stream
     torch.cuda.set_stream(stream)
 
@@ -211,40 +219,89 @@ def main():
     ct = ct or T
     cfg = api.DriverConfig(tile=api.TileConfig(cs, ct), device=local, stream=stream.cuda_stream)
     dims = api.ProblemDims.create(B, S, m, H, D, k)
-    mine, loads, shards = shard_chunks(S, m, cs, world, rank)
+    # --simulate-rank R/N: one process measures rank R's shard of an N-way run
+    plan_world, plan_rank = world, rank
+    if args.simulate_rank:
+        plan_rank, plan_world = (int(x) for x in args.simulate_rank.split("/"))
+        assert world == 1 and 0 <= plan_rank < plan_world
+    mine, loads, shards = shard_chunks(S, m, cs, plan_world, plan_rank)
     rows = api.chunk_rows(dims, cfg, mine)
     pairs_total = B * legal_pairs_rows(S, m, range(0, S, cs), cs, T)
     pairs_mine = B * legal_pairs_rows(S, m, mine, cs, T)
 
-    # ---------------------------------------------------------- operands in HBM
+    # ------------------------------------------------- operands in HBM (rank-local)
+    # Each rank generates only its own chunks' q / w rows (the counter-based
+    # generator is indexed by the global element, so the values equal those
+    # of a full-size draw) and keeps them as a local stack in chunk order.
     eng = Engine(local)
-    q = eng.gen_normal_bf16(B * S * H * D, D ** -0.5, 1, 1)
-    w = eng.gen_normal_f32(B * S * H, (D * H) ** -0.5, 1, 3)
+
+    def local_stack(per_row, stddev, stream_id, bf16):
+        gen = eng.gen_normal_bf16 if bf16 else eng.gen_normal_f32
+        parts = []
+        for b in range(B):
+            for s0 in mine:
+                n = min(cs, S - s0)
+                parts.append(gen(n * per_row, stddev, 1, stream_id, (b * S + s0) * per_row))
+        return torch.cat(parts)
+
+    q = local_stack(H * D, D ** -0.5, 1, True)
+    w = local_stack(H, (D * H) ** -0.5, 3, False)
     if rank == 0:
         kc = eng.gen_normal_bf16(B * T * D, D ** -0.5, 1, 2)
     else:
         kc = torch.empty(B * T * D, dtype=torch.bfloat16, device="cuda")
     out_idx = torch.empty((B, rows, k), dtype=torch.int64, device="cuda")
     out_val = torch.empty((B, rows, k), dtype=torch.float32, device="cuda")
-    max_rows = rows
-    if world > 1:
-        t = torch.tensor([rows], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        max_rows = int(t.item())
-        send = torch.zeros((B, max_rows, k), dtype=torch.int64, device="cuda")
-        gather_list = [torch.empty_like(send) for _ in range(world)] if rank == 0 else None
+    # Gather of the int32 index rows to rank 0, in slices of <= 256 MB per
+    # rank so the staging stays bounded; rank 0 holds the [world, B, rows, k]
+    # int32 result (allocated in --simulate-rank 0/N too, for peak HBM).
+    max_rows = max(api.chunk_rows(dims, cfg, sh) for sh in shards)
+    slice_rows = max(1, min(max_rows, (256 << 20) // (B * k * 4)))
+    gathered = None
+    if plan_rank == 0 and plan_world > 1:
+        gathered = torch.empty((plan_world, B, max_rows, k), dtype=torch.int32, device="cuda")
+    send = torch.zeros((B, max_rows, k), dtype=torch.int32, device="cuda") if world > 1 else None
     torch.cuda.synchronize()
+
+    def bcast(t):
+        if backend == "nccl":
+            dist.broadcast(t, src=0)
+        else:
+            h = t.cpu()
+            dist.broadcast(h, src=0)
+            t.copy_(h)
+
+    def gather_rows():
+        send[:, :rows].copy_(out_idx)  # int64 -> int32 (indices < T)
+        for r0 in range(0, max_rows, slice_rows):
+            n = min(slice_rows, max_rows - r0)
+            part = send[:, r0:r0 + n].contiguous()
+            if backend == "nccl":
+                dst = [gathered[r, :, r0:r0 + n] for r in range(world)] if rank == 0 else None
+                if rank == 0:
+                    bufs = [torch.empty_like(part) for _ in range(world)]
+                    dist.gather(part, bufs, dst=0)
+                    for r in range(world):
+                        dst[r].copy_(bufs[r])
+                else:
+                    dist.gather(part, None, dst=0)
+            else:
+                h = part.cpu()
+                bufs = [torch.empty_like(h) for _ in range(world)] if rank == 0 else None
+                dist.gather(h, bufs, dst=0)
+                if rank == 0:
+                    for r in range(world):
+                        gathered[r, :, r0:r0 + n].copy_(bufs[r])
 
     stats_box = {}
 
     def step():
         if world > 1:
-            dist.broadcast(kc, src=0)  # keys once over NVLink
-        st = api.run_chunked_device(q, kc, w, dims, cfg, mine, out_idx, out_val)[2]
+            bcast(kc)  # keys once over NVLink
+        st = api.run_chunked_device(q, kc, w, dims, cfg, mine, out_idx, out_val, local_rows=True)[2]
         stats_box["st"] = st
         if world > 1:
-            send[:, :rows].copy_(out_idx)
-            dist.gather(send, gather_list, dst=0)  # only the [S, k] indices travel
+            gather_rows()  # only the [S, k] indices travel
 
     drv = api.KernelStats(api.driver_engine(local))
     for _ in range(args.warmup):
@@ -272,14 +329,19 @@ def main():
     if world > 1:
         dist.barrier()
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if backend == "nccl":
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        else:
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.MAX)
+            t = h
         ms = float(t.item())
     gather_ok = None
     if world > 1 and rank == 0:
         # the gathered rows reassemble into sequence order (checked once, untimed)
         from paper_2605_02568_b200.shard import assemble
 
-        parts = [g[:, : api.chunk_rows(dims, cfg, shards[r])].cpu().numpy() for r, g in enumerate(gather_list)]
+        parts = [gathered[r][:, : api.chunk_rows(dims, cfg, shards[r])].cpu().numpy() for r in range(world)]
         full = assemble(parts, shards, S, cs)
         gather_ok = bool(np.array_equal(full[:, mine[0]:mine[0] + 1], out_idx[:, :1].cpu().numpy()))
     kinds = {"score": _capi.KIND_SCORE, "select": _capi.KIND_SELECT, "merge": _capi.KIND_MERGE,
@@ -291,11 +353,13 @@ def main():
     score_flops = pairs_mine * FLOPS_PER_PAIR * args.steps
     achieved_tflops = score_flops / (score_ms / 1000.0) / 1e12 if score_ms > 0 else None
     peak_tflops = peaks["bf16_tflops_sustained"]
-    traffic = None
+    traffic = sel_traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(args.workload, {}).get("score_dram_bytes_per_launch")
+            tj = json.load(f).get(args.workload, {})
+            traffic = tj.get("score_dram_bytes_per_launch")
+            sel_traffic = tj.get("select_dram_bytes_per_launch")
     sel_n, sel_ms = kstats["select"]
     select_gbs = (pairs_mine * 4 * args.steps) / (sel_ms / 1000.0) / 1e9 if sel_ms > 0 else None
     _, drv_peak = drv.mem()
@@ -307,36 +371,44 @@ def main():
     # ---------------------------------------------------------- e2e (host API)
     e2e = None
     if not args.no_e2e and not args.profile_only:
-        qh = torch.empty((B, S, H, D), dtype=torch.float32, pin_memory=True)
+        # the reference-facing host API with pinned fp32 host operands; each
+        # rank holds only its own q / w rows (csaidx_host_run_chunked_local)
+        qh = torch.empty((B, rows, H, D), dtype=torch.float32, pin_memory=True)
         qh.view(-1).copy_(q.float())
         kch = torch.empty((B, T, D), dtype=torch.float32, pin_memory=True)
         if world > 1:
-            dist.broadcast(kc, src=0)
+            bcast(kc)
         kch.view(-1).copy_(kc.float())
-        wh = torch.empty((B, S, H), dtype=torch.float32, pin_memory=True)
+        wh = torch.empty((B, rows, H), dtype=torch.float32, pin_memory=True)
         wh.view(-1).copy_(w)
         oi = torch.empty((B, rows, k), dtype=torch.int64, pin_memory=True)
         ov = torch.empty((B, rows, k), dtype=torch.float32, pin_memory=True)
         ecfg = api.DriverConfig(tile=api.TileConfig(cs, ct), device=local, stream=0)
         torch.cuda.synchronize()
-        api.run_chunked_rows(qh, kch, wh, dims, ecfg, mine, oi, ov)  # warm-up
+        api.run_chunked_rows(qh, kch, wh, dims, ecfg, mine, oi, ov, local_rows=True)  # warm-up
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            api.run_chunked_rows(qh, kch, wh, dims, ecfg, mine, oi, ov)
+            api.run_chunked_rows(qh, kch, wh, dims, ecfg, mine, oi, ov, local_rows=True)
         torch.cuda.synchronize()
         e2e_ms = (time.perf_counter() - t0) * 1000 / args.e2e_steps
         if world > 1:
-            t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+            h = torch.tensor([e2e_ms], dtype=torch.float64)
+            if backend == "nccl":
+                t = h.cuda()
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                h = t.cpu()
+            else:
+                dist.all_reduce(h, op=dist.ReduceOp.MAX)
+            e2e_ms = float(h.item())
         h2d = B * rows * H * D * 4 + B * T * D * 4 + B * rows * H * 4
         d2h = B * rows * k * 12
-        e2e = {"value": pairs_total / (e2e_ms / 1000.0), "unit": "legal pairs/s", "ms_per_step": e2e_ms,
+        e2e = {"value": (pairs_mine if args.simulate_rank else pairs_total) / (e2e_ms / 1000.0),
+               "unit": "legal pairs/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "path": "csaidx_host_run_chunked_rows (libcsaidx.so C entry of csaidx::run_chunked), pinned fp32 "
-                       "host operands"}
+               "path": "csaidx_host_run_chunked_local (libcsaidx.so C entry of csaidx::run_chunked over this "
+                       "rank's rows), pinned fp32 host operands, H2D/D2H inside the timed region"}
         # cheap end-to-end correctness guard: the host API must agree with the resident run
         assert torch.equal(oi, out_idx.cpu()), "host-API result differs from the device-resident run"
 
@@ -351,7 +423,7 @@ def main():
     if rank == 0:
         line = {
             "metric": "indexer query·key pairs/sec (legal causal pairs)",
-            "value": pairs_total / (ms / 1000.0),
+            "value": (pairs_mine if args.simulate_rank else pairs_total) / (ms / 1000.0),
             "unit": "legal pairs/s",
             "n_gpus": world,
             "steps": args.steps,
@@ -363,8 +435,11 @@ def main():
             "dtype": "bf16",
             "data": "synthetic: counter-based N(0,1/d_h) q/kc rounded to bf16, w ~ N(0,1/(d_h*H_I)) fp32, on device",
             "config": {"workload": f"{args.workload}: V4-Flash B={B} S={S} T={T} H_I={H} d_h={D} m={m} k={k}",
-                       "query_tile": cs, "key_tile": ct, "parallelism": f"query-sharded x{world} (LPT by causal work)",
-                       "l2": "inputs (q 4.3 GB bf16 at C3) exceed L2; no flush needed",
+                       "query_tile": cs, "key_tile": ct,
+                       "parallelism": (f"rank {plan_rank} of a query-sharded x{plan_world} run, measured alone on one "
+                                       f"GPU (value = this rank's legal pairs / its step time)" if args.simulate_rank
+                                       else f"query-sharded x{world} (LPT by causal work)"),
+                       "l2": f"inputs (q {q.numel() * 2 / 1e9:.1f} GB bf16 per rank) exceed L2; no flush needed",
                        "dense_pairs_per_s": B * S * T / (ms / 1000.0)},
             "hbm_peak_gb": hbm_peak / 1e9,
             "ledger_peak_bytes": st.ledger_peak_bytes,
@@ -375,7 +450,12 @@ def main():
                          "traffic": traffic, "algorithmic": f"{FLOPS_PER_PAIR} FLOP per legal pair",
                          "launches": score_n, "avg_launch_ms": score_ms / max(score_n, 1)},
             "kernels_ms_per_step": {n: v[1] / args.steps for n, v in kstats.items()},
-            "select_gbs_one_pass": select_gbs,
+            "select_roofline": {"bound": "hbm", "kernel": "select_kernel (per-row exact top-k over the fp32 tile)",
+                                "achieved": select_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                                "frac": (select_gbs / peaks["hbm_gbs"]) if select_gbs else None,
+                                "traffic": sel_traffic,
+                                "algorithmic": "4 B per legal pair (one read of each legal fp32 score)",
+                                "launches": sel_n, "avg_launch_ms": sel_ms / max(sel_n, 1)},
             "select_fallback_rows": fallbacks,
             "select_prefilter_rows": cand_hits,
             "gpu_launches": launches,
@@ -384,8 +464,9 @@ def main():
             "e2e": e2e,
             "run_stats": {"dispatch_count": st.dispatch_count, "tiles_skipped_masked": st.tiles_skipped_masked},
             "multi_gpu": {"rank_work_pairs": loads, "gather_reassembly_ok": gather_ok,
-                          "collectives": "broadcast kc (bf16) from rank 0 + gather int64 [rows,k] to rank 0"
-                          if world > 1 else "none"},
+                          "collectives": (f"broadcast kc (bf16) from rank 0 + gather of int32 [rows,k] index rows to "
+                                          f"rank 0 in {slice_rows}-row slices ({backend})") if world > 1 else "none",
+                          "rank_rows": rows, "rank_pairs": pairs_mine},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -33,10 +33,13 @@ void reset_device_peak();
 // Operands already resident in HBM. dtype: 0 = bf16 (tensor-core path),
 // 1 = fp32 (exact-order path).
 struct DeviceOperands {
-    const void* q = nullptr;   // [B, S, H_I, d_h]
+    const void* q = nullptr;   // [B, S, H_I, d_h]  (local_rows: [B, out_rows, H_I, d_h])
     const void* kc = nullptr;  // [B, T, d_h]
-    const float* w = nullptr;  // [B, S, H_I]
+    const float* w = nullptr;  // [B, S, H_I]        (local_rows: [B, out_rows, H_I])
     int dtype = 0;
+    // Query-sharded ranks: q / w hold only the listed chunks' rows, stacked
+    // in list order exactly like the output rows (chunk c at row row0_c).
+    bool local_rows = false;
 };
 
 // Device-resident Algorithm 2 over a subset of query chunks (all chunks when

@@ -136,6 +136,14 @@ int csaidx_cuda_to_bf16(csaidx_engine* e, const float* src, uint16_t* dst, int64
 int csaidx_cuda_score(csaidx_engine* e, const void* q, const void* kc, int dtype, const float* w,
                       const csaidx_dims* dims, int64_t s0, int64_t rows, int64_t t0, int64_t cols,
                       int mode, int kernel, int apply_mask, float* out, int64_t ld);
+/* Same tile over rank-local operands: q / w hold op_rows query rows per
+ * batch ([B, op_rows, H_I, d_h] / [B, op_rows, H_I]) and query s0 + i lives
+ * at operand row op_row0 + i. csaidx_cuda_score == op_rows = S,
+ * op_row0 = s0. Lets a query-sharded rank keep only its own q / w rows. */
+int csaidx_cuda_score_rows(csaidx_engine* e, const void* q, const void* kc, int dtype, const float* w,
+                           const csaidx_dims* dims, int64_t s0, int64_t rows, int64_t t0, int64_t cols,
+                           int mode, int kernel, int apply_mask, float* out, int64_t ld,
+                           int64_t op_rows, int64_t op_row0);
 /* 1 when csaidx_cuda_score would take the tcgen05 path for these arguments. */
 int csaidx_cuda_score_uses_tensor_cores(const csaidx_dims* dims, int dtype, int mode, int kernel);
 

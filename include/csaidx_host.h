@@ -79,12 +79,28 @@ int csaidx_host_run_chunked_rows(const float* q, const float* kc, const float* w
                                  const csaidx_run_config* cfg, const int64_t* chunk_starts, int64_t n_chunks,
                                  int64_t* out_idx, float* out_val, int64_t out_rows, csaidx_run_stats* stats);
 
+/* Same with rank-local host operands: q / w hold only the listed chunks'
+ * rows, stacked in list order like the outputs ([B, out_rows, H_I, d_h],
+ * [B, out_rows, H_I]); kc is the full [B, T, d_h]. */
+int csaidx_host_run_chunked_local(const float* q, const float* kc, const float* w, const csaidx_dims* dims,
+                                  const csaidx_run_config* cfg, const int64_t* chunk_starts, int64_t n_chunks,
+                                  int64_t* out_idx, float* out_val, int64_t out_rows, csaidx_run_stats* stats);
+
 /* Algorithm 2 over device-resident operands (dtype CSAIDX_DTYPE_*), for the
  * listed query chunks (NULL / 0 = all), outputs device [B, out_rows, k]. */
 int csaidx_device_run_chunked(const void* q, const void* kc, int dtype, const float* w,
                               const csaidx_dims* dims, const csaidx_run_config* cfg,
                               const int64_t* chunk_starts, int64_t n_chunks, int64_t* out_idx,
                               float* out_val, int64_t out_rows, csaidx_run_stats* stats);
+
+/* Same over rank-local operands: q / w hold only the listed chunks' rows,
+ * stacked in list order like the outputs ([B, out_rows, H_I, d_h] and
+ * [B, out_rows, H_I]); kc is the full [B, T, d_h]. A query-sharded rank's
+ * HBM then scales with its share of S. */
+int csaidx_device_run_chunked_local(const void* q, const void* kc, int dtype, const float* w,
+                                    const csaidx_dims* dims, const csaidx_run_config* cfg,
+                                    const int64_t* chunk_starts, int64_t n_chunks, int64_t* out_idx,
+                                    float* out_val, int64_t out_rows, csaidx_run_stats* stats);
 
 /* Pure host arithmetic of the API (types.cpp / driver.cpp), no GPU needed. */
 int csaidx_host_problem_dims(int64_t batch, int64_t seq_len, int64_t ratio, int64_t heads,

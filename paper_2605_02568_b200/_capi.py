@@ -102,6 +102,11 @@ CUDA_SYMBOLS = {
         [c_void_p, c_void_p, c_void_p, c_int, c_void_p, POINTER(Dims), c_int64, c_int64, c_int64, c_int64,
          c_int, c_int, c_int, c_void_p, c_int64],
     ),
+    "csaidx_cuda_score_rows": (
+        c_int,
+        [c_void_p, c_void_p, c_void_p, c_int, c_void_p, POINTER(Dims), c_int64, c_int64, c_int64, c_int64,
+         c_int, c_int, c_int, c_void_p, c_int64, c_int64, c_int64],
+    ),
     "csaidx_cuda_score_uses_tensor_cores": (c_int, [POINTER(Dims), c_int, c_int, c_int]),
     "csaidx_cuda_bool_mask": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64]),
     "csaidx_cuda_apply_bool_mask": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64]),

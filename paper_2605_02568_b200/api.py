@@ -89,8 +89,13 @@ HOST_SYMBOLS = {
                                      c_void_p, POINTER(RunStatsC)]),
     "csaidx_host_run_chunked_rows": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(Dims), POINTER(RunConfig),
                                              c_void_p, c_int64, c_void_p, c_void_p, c_int64, POINTER(RunStatsC)]),
+    "csaidx_host_run_chunked_local": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(Dims), POINTER(RunConfig),
+                                              c_void_p, c_int64, c_void_p, c_void_p, c_int64, POINTER(RunStatsC)]),
     "csaidx_device_run_chunked": (c_int, [c_void_p, c_void_p, c_int, c_void_p, POINTER(Dims), POINTER(RunConfig),
                                           c_void_p, c_int64, c_void_p, c_void_p, c_int64, POINTER(RunStatsC)]),
+    "csaidx_device_run_chunked_local": (c_int, [c_void_p, c_void_p, c_int, c_void_p, POINTER(Dims),
+                                                POINTER(RunConfig), c_void_p, c_int64, c_void_p, c_void_p, c_int64,
+                                                POINTER(RunStatsC)]),
     "csaidx_host_problem_dims": (c_int, [c_int64] * 6 + [POINTER(Dims)]),
     "csaidx_host_dispatch_count_model": (c_int, [POINTER(Dims), c_int64, c_int64, POINTER(c_int64)]),
     "csaidx_host_chunked_peak_model_bytes": (c_int, [c_int64, c_int64, c_int64, c_int64, c_int, POINTER(c_uint64)]),
@@ -277,11 +282,14 @@ def chunk_rows(dims: ProblemDims, config: DriverConfig, chunk_starts) -> int:
     return int(sum(min(cs, dims.seq_len - int(s)) for s in chunk_starts))
 
 
-def run_chunked_rows(q, kc, w, dims: ProblemDims, config: DriverConfig, chunk_starts, out_idx, out_val):
+def run_chunked_rows(q, kc, w, dims: ProblemDims, config: DriverConfig, chunk_starts, out_idx, out_val,
+                     local_rows=False):
     """Host-buffer run over a chunk subset (csaidx_host_run_chunked_rows).
 
     q/kc/w/out_* are contiguous host arrays (numpy, or pinned torch CPU
-    tensors); only the chunk rows of q/w are copied to the device."""
+    tensors); only the chunk rows of q/w are copied to the device.
+    local_rows: q / w hold only those rows, stacked in chunk-list order
+    (csaidx_host_run_chunked_local)."""
     starts = np.ascontiguousarray(chunk_starts, dtype=np.int64)
     st = RunStatsC()
     cd, cc = dims.c(), config.c()
@@ -289,16 +297,19 @@ def run_chunked_rows(q, kc, w, dims: ProblemDims, config: DriverConfig, chunk_st
     def ptr(a):
         return c_void_p(a.data_ptr()) if hasattr(a, "data_ptr") else _ptr(a)
 
-    _check(host_lib().csaidx_host_run_chunked_rows(ptr(q), ptr(kc), ptr(w), ctypes.byref(cd), ctypes.byref(cc),
-                                                   _ptr(starts), starts.size, ptr(out_idx), ptr(out_val),
-                                                   out_idx.shape[1], ctypes.byref(st)))
+    entry = host_lib().csaidx_host_run_chunked_local if local_rows else host_lib().csaidx_host_run_chunked_rows
+    _check(entry(ptr(q), ptr(kc), ptr(w), ctypes.byref(cd), ctypes.byref(cc), _ptr(starts), starts.size,
+                 ptr(out_idx), ptr(out_val), out_idx.shape[1], ctypes.byref(st)))
     return RunStats(st.dispatch_count, st.tiles_skipped_masked, st.tiles_skipped_narrow, st.ledger_peak_bytes,
                     st.device_peak_bytes, ExecutionPath.chunked)
 
 
 def run_chunked_device(q, kc, w, dims: ProblemDims, config: DriverConfig, chunk_starts=None, out_idx=None,
-                       out_val=None):
-    """Device-resident Algorithm 2 (csaidx_device_run_chunked): torch CUDA tensors in, torch tensors out."""
+                       out_val=None, local_rows=False):
+    """Device-resident Algorithm 2 (csaidx_device_run_chunked): torch CUDA tensors in, torch tensors out.
+
+    local_rows: q / w hold only the listed chunks' rows, stacked in list order
+    (csaidx_device_run_chunked_local), as a query-sharded rank keeps them."""
     import torch
 
     dtype = _capi.DTYPE_BF16 if q.dtype == torch.bfloat16 else _capi.DTYPE_F32
@@ -315,7 +326,11 @@ def run_chunked_device(q, kc, w, dims: ProblemDims, config: DriverConfig, chunk_
         out_val = torch.empty((dims.batch, rows, dims.top_k), dtype=torch.float32, device=q.device)
     st = RunStatsC()
     cd, cc = dims.c(), config.c()
-    _check(host_lib().csaidx_device_run_chunked(
+    entry = host_lib().csaidx_device_run_chunked_local if local_rows else host_lib().csaidx_device_run_chunked
+    if local_rows and (q.numel() != dims.batch * rows * dims.heads * dims.head_dim or
+                       w.numel() != dims.batch * rows * dims.heads):
+        raise ValueError("local_rows: q / w must hold exactly the listed chunks' rows")
+    _check(entry(
         c_void_p(q.data_ptr()), c_void_p(kc.data_ptr()), dtype, c_void_p(w.data_ptr()), ctypes.byref(cd),
         ctypes.byref(cc), None if starts is None else _ptr(starts), n_chunks, c_void_p(out_idx.data_ptr()),
         c_void_p(out_val.data_ptr()), out_idx.shape[1], ctypes.byref(st)))

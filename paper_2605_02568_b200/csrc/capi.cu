@@ -454,9 +454,13 @@ namespace {
 // score_tc launch shared by the plain, sampled and filtered entry points.
 int launch_tc(csaidx_engine* e, const void* q, const void* kc, const float* w, const csaidx_dims* d, int64_t s0,
               int64_t rows, int64_t t0, int64_t cols, int apply_mask, float* out, int64_t ld, int kt_stride,
-              const float* tau, uint32_t* pass_bits, int64_t bits_ld) {
+              const float* tau, uint32_t* pass_bits, int64_t bits_ld, int64_t op_rows = -1, int64_t op_row0 = -1) {
+    if (op_rows < 0) {
+        op_rows = d->seq_len;
+        op_row0 = s0;
+    }
     CUtensorMap qmap, kmap;
-    if (int rc = make_map(&qmap, q, static_cast<uint64_t>(d->batch * d->seq_len * d->heads), d->head_dim, 256))
+    if (int rc = make_map(&qmap, q, static_cast<uint64_t>(d->batch * op_rows * d->heads), d->head_dim, 256))
         return rc;
     if (int rc = make_map(&kmap, kc, static_cast<uint64_t>(d->batch * d->key_blocks), d->head_dim, 128)) return rc;
     ScoreTcParams p{};
@@ -472,6 +476,8 @@ int launch_tc(csaidx_engine* e, const void* q, const void* kc, const float* w, c
     p.rows = rows;
     p.t0 = t0;
     p.cols = cols;
+    p.op_rows = op_rows;
+    p.op_shift = op_row0 - s0;
     p.batch = static_cast<int>(d->batch);
     p.apply_mask = apply_mask;
     p.kt_stride = kt_stride;
@@ -556,10 +562,20 @@ int csaidx_cuda_score_filtered(csaidx_engine* e, const void* q_bf16, const void*
 int csaidx_cuda_score(csaidx_engine* e, const void* q, const void* kc, int dtype, const float* w,
                       const csaidx_dims* d, int64_t s0, int64_t rows, int64_t t0, int64_t cols, int mode, int kernel,
                       int apply_mask, float* out, int64_t ld) {
+    if (int rc = check_dims(d)) return rc;
+    return csaidx_cuda_score_rows(e, q, kc, dtype, w, d, s0, rows, t0, cols, mode, kernel, apply_mask, out, ld,
+                                  d->seq_len, s0);
+}
+
+int csaidx_cuda_score_rows(csaidx_engine* e, const void* q, const void* kc, int dtype, const float* w,
+                           const csaidx_dims* d, int64_t s0, int64_t rows, int64_t t0, int64_t cols, int mode,
+                           int kernel, int apply_mask, float* out, int64_t ld, int64_t op_rows, int64_t op_row0) {
     if (int rc = set_device(e)) return rc;
     if (int rc = check_dims(d)) return rc;
     if (rows < 1 || cols < 1 || s0 < 0 || t0 < 0 || s0 + rows > d->seq_len || t0 + cols > d->key_blocks)
         return fail(CSAIDX_INVALID_ARGUMENT, "score_tile: tile out of range");
+    if (op_rows < 1 || op_row0 < 0 || op_row0 + rows > op_rows)
+        return fail(CSAIDX_INVALID_ARGUMENT, "score: operand rows [op_row0, op_row0 + rows) outside op_rows");
     if (ld < cols || (ld % 4) != 0) return fail(CSAIDX_INVALID_ARGUMENT, "score: ld must be >= cols and a multiple of 4");
     if (mode != CSAIDX_MODE_FP32 && mode != CSAIDX_MODE_FP16_EMULATED)
         return fail(CSAIDX_INVALID_ARGUMENT, "score: unknown accumulation mode");
@@ -568,7 +584,8 @@ int csaidx_cuda_score(csaidx_engine* e, const void* q, const void* kc, int dtype
     if (kernel != CSAIDX_KERNEL_AUTO && kernel != CSAIDX_KERNEL_EXACT)
         return fail(CSAIDX_INVALID_ARGUMENT, "score: unknown kernel request");
     if (csaidx_cuda_score_uses_tensor_cores(d, dtype, mode, kernel)) {
-        return launch_tc(e, q, kc, w, d, s0, rows, t0, cols, apply_mask, out, ld, 1, nullptr, nullptr, 0);
+        return launch_tc(e, q, kc, w, d, s0, rows, t0, cols, apply_mask, out, ld, 1, nullptr, nullptr, 0, op_rows,
+                         op_row0);
     } else {
         ScoreExactParams p{};
         p.q = q;
@@ -587,6 +604,8 @@ int csaidx_cuda_score(csaidx_engine* e, const void* q, const void* kc, int dtype
         p.rows = rows;
         p.t0 = t0;
         p.cols = cols;
+        p.op_rows = op_rows;
+        p.op_shift = op_row0 - s0;
         p.batch = static_cast<int>(d->batch);
         p.apply_mask = apply_mask;
         p.fp16 = mode == CSAIDX_MODE_FP16_EMULATED;

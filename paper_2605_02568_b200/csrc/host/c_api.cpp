@@ -144,6 +144,23 @@ int csaidx_host_run_chunked_rows(const float* q, const float* kc, const float* w
     });
 }
 
+int csaidx_host_run_chunked_local(const float* q, const float* kc, const float* w, const csaidx_dims* dims,
+                                  const csaidx_run_config* cfg, const int64_t* chunk_starts, int64_t n_chunks,
+                                  int64_t* out_idx, float* out_val, int64_t out_rows, csaidx_run_stats* stats) {
+    return guarded([&] {
+        const csaidx::ProblemDims d = from_c(dims);
+        const csaidx::DriverConfig c = from_c(cfg);
+        std::vector<int64_t> starts;
+        if (chunk_starts != nullptr && n_chunks > 0) starts.assign(chunk_starts, chunk_starts + n_chunks);
+        csaidx::gpu::reset_device_peak();
+        csaidx::MemoryLedger ledger;
+        csaidx::RunStats rs;
+        csaidx::detail::run_chunked_rows_view({q, kc, w, true}, d, c, starts.empty() ? nullptr : &starts, out_idx, out_val,
+                                              out_rows, ledger, &rs);
+        fill_stats(stats, rs, ledger, 1);
+    });
+}
+
 int csaidx_host_run_materialize(const float* q, const float* kc, const float* w, const csaidx_dims* dims,
                                 const csaidx_run_config* cfg, int64_t* out_idx, float* out_val,
                                 csaidx_run_stats* stats) {
@@ -188,6 +205,23 @@ int csaidx_device_run_chunked(const void* q, const void* kc, int dtype, const fl
         csaidx::MemoryLedger ledger;
         csaidx::RunStats rs;
         csaidx::gpu::run_chunked_device(csaidx::gpu::DeviceOperands{q, kc, w, dtype}, d, c,
+                                        starts.empty() ? nullptr : &starts, out_idx, out_val, out_rows, ledger, &rs);
+        fill_stats(stats, rs, ledger, 1);
+    });
+}
+
+int csaidx_device_run_chunked_local(const void* q, const void* kc, int dtype, const float* w, const csaidx_dims* dims,
+                                    const csaidx_run_config* cfg, const int64_t* chunk_starts, int64_t n_chunks,
+                                    int64_t* out_idx, float* out_val, int64_t out_rows, csaidx_run_stats* stats) {
+    return guarded([&] {
+        const csaidx::ProblemDims d = from_c(dims);
+        const csaidx::DriverConfig c = from_c(cfg);
+        std::vector<int64_t> starts;
+        if (chunk_starts != nullptr && n_chunks > 0) starts.assign(chunk_starts, chunk_starts + n_chunks);
+        csaidx::gpu::reset_device_peak();
+        csaidx::MemoryLedger ledger;
+        csaidx::RunStats rs;
+        csaidx::gpu::run_chunked_device(csaidx::gpu::DeviceOperands{q, kc, w, dtype, true}, d, c,
                                         starts.empty() ? nullptr : &starts, out_idx, out_val, out_rows, ledger, &rs);
         fill_stats(stats, rs, ledger, 1);
     });

@@ -66,6 +66,9 @@ struct HostView {
     const float* q;
     const float* kc;
     const float* w;
+    // q / w hold only the call's chunks, stacked like the output rows
+    // ([B, out_rows, ...]) instead of the full [B, S, ...] tensors.
+    bool local_rows = false;
 };
 
 struct DeviceOps {
@@ -73,6 +76,10 @@ struct DeviceOps {
     const void* kc;
     const float* w;
     int dtype;  // CSAIDX_DTYPE_*
+    // 0: q / w are the full [B, S, ...] tensors. > 0: rank-local stacks of
+    // the plan's chunks in plan order, op_rows rows per batch (chunk c at
+    // operand row plan.out_row0[c]).
+    int64_t op_rows = 0;
 };
 
 // Device copies of q / kc / w. dtype bf16 stages through a bounded fp32

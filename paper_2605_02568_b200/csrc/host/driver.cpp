@@ -78,7 +78,7 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
     // legal row exceeds the candidate list. Same results as the plain select;
     // device scratch only (the reference has no such buffers to charge).
     const int cap = csaidx_cuda_candidate_capacity(k);
-    const bool prefilter = prefilter_enabled() && !config.bool_mask_tile && cap > 0 &&
+    const bool prefilter = prefilter_enabled() && !config.bool_mask_tile && cap > 0 && ops.op_rows == 0 &&
                            csaidx_cuda_score_uses_tensor_cores(&cd, ops.dtype, mcode, kcode) != 0;
     const int64_t tiles_max = ceil_div(plan.ct, 128);
     // per tile: stride = ceil(tiles / kPrefilterSampleTiles) -> at most
@@ -95,6 +95,8 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
     for (size_t c = 0; c < plan.starts.size(); ++c) {
         const int64_t s0 = plan.starts[c];
         const int64_t rows = std::min(plan.cs, dims.seq_len - s0);
+        const int64_t op_rows = ops.op_rows > 0 ? ops.op_rows : dims.seq_len;
+        const int64_t op_row0 = ops.op_rows > 0 ? plan.out_row0[c] : s0;
         if (hooks.before) hooks.before(c);
         LedgerCharge buffer_charge(ledger, "topk_buffer", run_buffer_bytes(B, rows, k));
         // One key tile covering all T keys: its select is a copy into the
@@ -128,14 +130,14 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
                 check(csaidx_cuda_score_filtered(e, ops.q, ops.kc, ops.w, &cd, s0, rows, t0, cols, scores.as<float>(),
                                                  ld, pf_tau.as<float>(), pf_bits.as<uint32_t>(), bits_ld));
             } else if (config.bool_mask_tile) {
-                check(csaidx_cuda_score(e, ops.q, ops.kc, ops.dtype, ops.w, &cd, s0, rows, t0, cols, mcode, kcode, 0,
-                                        scores.as<float>(), ld));
+                check(csaidx_cuda_score_rows(e, ops.q, ops.kc, ops.dtype, ops.w, &cd, s0, rows, t0, cols, mcode, kcode,
+                                             0, scores.as<float>(), ld, op_rows, op_row0));
                 LedgerCharge mask_charge(ledger, "mask_tile", static_cast<uint64_t>(rows) * static_cast<uint64_t>(cols));
                 check(csaidx_cuda_bool_mask(e, keep.as<uint8_t>(), s0, t0, rows, cols, dims.ratio));
                 check(csaidx_cuda_apply_bool_mask(e, scores.as<float>(), ld, keep.as<uint8_t>(), B, rows, cols));
             } else {
-                check(csaidx_cuda_score(e, ops.q, ops.kc, ops.dtype, ops.w, &cd, s0, rows, t0, cols, mcode, kcode, 1,
-                                        scores.as<float>(), ld));
+                check(csaidx_cuda_score_rows(e, ops.q, ops.kc, ops.dtype, ops.w, &cd, s0, rows, t0, cols, mcode, kcode,
+                                             1, scores.as<float>(), ld, op_rows, op_row0));
             }
             ++stats.dispatch_count;
             const int64_t width = std::min(k, cols);
@@ -242,29 +244,33 @@ void run_chunked_rows_view(const HostView& in, const ProblemDims& dims, const Dr
     // behind the kernels; pageable buffers still work (copies then block).
     const int64_t B = dims.batch, k = dims.top_k, qrow = dims.heads * dims.head_dim;
     const size_t esz = dtype == CSAIDX_DTYPE_BF16 ? 2 : 4;
-    DeviceBuffer q(e, static_cast<size_t>(dims.q_elems()) * esz), kc(e, static_cast<size_t>(dims.kc_elems()) * esz),
-        w(e, static_cast<size_t>(dims.w_elems()) * sizeof(float));
+    // q / w on device hold only this call's chunks (rank-local stacks in plan
+    // order, the same row layout as the outputs)
+    DeviceBuffer q(e, static_cast<size_t>(B * out_rows * qrow) * esz), kc(e, static_cast<size_t>(dims.kc_elems()) * esz),
+        w(e, static_cast<size_t>(B * out_rows * dims.heads) * sizeof(float));
     DeviceBuffer slab[2];
     if (dtype == CSAIDX_DTYPE_BF16) {
         for (auto& sb : slab) sb = DeviceBuffer(e, static_cast<size_t>(plan.cs * qrow) * sizeof(float));
     }
     const size_t n = static_cast<size_t>(B * out_rows * k);
     DeviceBuffer idx(e, n * sizeof(int64_t)), val(e, n * sizeof(float));
-    const DeviceOps ops{q.as<void>(), kc.as<void>(), w.as<float>(), dtype};
+    const DeviceOps ops{q.as<void>(), kc.as<void>(), w.as<float>(), dtype, out_rows};
     constexpr int kMainLane = 0, kInLane = 1, kOutLane = 2;
     auto upload_chunk = [&](size_t c) {
         const int64_t s0 = plan.starts[c], rows = std::min(plan.cs, dims.seq_len - s0);
         for (int64_t b = 0; b < B; ++b) {
-            const int64_t qoff = (b * dims.seq_len + s0) * qrow, woff = (b * dims.seq_len + s0) * dims.heads;
+            const int64_t lrow = b * out_rows + plan.out_row0[c];  // operand row on device
+            const int64_t hrow = in.local_rows ? lrow : b * dims.seq_len + s0;  // ... and on the host
+            const int64_t qoff = hrow * qrow, woff = hrow * dims.heads;
             if (dtype == CSAIDX_DTYPE_BF16) {
                 DeviceBuffer& sb = slab[c % 2];
                 check(csaidx_cuda_copy(e, sb.as<void>(), in.q + qoff, static_cast<size_t>(rows * qrow) * sizeof(float)));
-                check(csaidx_cuda_to_bf16(e, sb.as<float>(), q.as<uint16_t>() + qoff, rows * qrow, strict ? 1 : 0));
+                check(csaidx_cuda_to_bf16(e, sb.as<float>(), q.as<uint16_t>() + lrow * qrow, rows * qrow, strict ? 1 : 0));
             } else {
-                check(csaidx_cuda_copy(e, q.as<float>() + qoff, in.q + qoff,
+                check(csaidx_cuda_copy(e, q.as<float>() + lrow * qrow, in.q + qoff,
                                        static_cast<size_t>(rows * qrow) * sizeof(float)));
             }
-            check(csaidx_cuda_copy(e, w.as<float>() + woff, in.w + woff,
+            check(csaidx_cuda_copy(e, w.as<float>() + lrow * dims.heads, in.w + woff,
                                    static_cast<size_t>(rows * dims.heads) * sizeof(float)));
         }
         check(csaidx_engine_signal(e, static_cast<int>(c % 32)));
@@ -386,8 +392,8 @@ void run_chunked_device(const DeviceOperands& ops, const ProblemDims& dims, cons
     std::lock_guard<std::mutex> lock(detail::engine_mutex());
     csaidx_engine* e = detail::engine();
     RunStats stats;
-    detail::run_plan(e, detail::DeviceOps{ops.q, ops.kc, ops.w, ops.dtype}, dims, config, plan, out_indices,
-                     out_values, out_rows, ledger, stats);
+    detail::run_plan(e, detail::DeviceOps{ops.q, ops.kc, ops.w, ops.dtype, ops.local_rows ? out_rows : 0}, dims,
+                     config, plan, out_indices, out_values, out_rows, ledger, stats);
     if (stats_out != nullptr) *stats_out = stats;
 }
 

@@ -20,6 +20,10 @@ struct ScoreTcParams {
     int64_t ld;
     int64_t seq_len, key_blocks, ratio;
     int64_t s0, rows, t0, cols;
+    // Operand row layout: q / w hold op_rows query rows per batch and query
+    // s lives at operand row s + op_shift (op_rows = seq_len, op_shift = 0
+    // for the full [B, S, ...] tensors; rank-local stacks otherwise).
+    int64_t op_rows, op_shift;
     int batch;
     int apply_mask;
     // Sample mode: tile kt of the launch covers physical key tile
@@ -52,6 +56,7 @@ struct ScoreExactParams {
     int64_t ld;
     int64_t seq_len, key_blocks, heads, head_dim, ratio;
     int64_t s0, rows, t0, cols;
+    int64_t op_rows, op_shift;  // operand row layout (see ScoreTcParams)
     int batch;
     int apply_mask;
     int fp16;  // emulate binary16 rounding points (score_scalar.cpp:29-32)

@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                 // reloaded as soon as item i-1's last group-g MMA retires,
                 // overlapping the other group's MMAs; group 1 is issued after
                 // the item's first key tile so that tile is never delayed.
-                const int64_t qrow64 = static_cast<int64_t>(it.b) * p.seq_len + p.s0 + it.r0;
+                const int64_t qrow64 = static_cast<int64_t>(it.b) * p.op_rows + p.s0 + p.op_shift + it.r0;
                 const int32_t qrow = static_cast<int32_t>(qrow64 * kHeads);
                 const uint32_t qpar = (qiter & 1) ^ 1;
                 auto load_group = [&](int g) {
@@ -445,9 +445,10 @@ __device__ __forceinline__ void score_exact_one(const ScoreExactParams& p, int b
         return;
     }
     const bool f32 = p.operand_f32 != 0;
-    const int64_t qbase = ((static_cast<int64_t>(b) * p.seq_len + s) * p.heads) * p.head_dim;
+    const int64_t orow = static_cast<int64_t>(b) * p.op_rows + s + p.op_shift;
+    const int64_t qbase = (orow * p.heads) * p.head_dim;
     const int64_t kbase = (static_cast<int64_t>(b) * p.key_blocks + t) * p.head_dim;
-    const float* wrow = p.w + (static_cast<int64_t>(b) * p.seq_len + s) * p.heads;
+    const float* wrow = p.w + orow * p.heads;
     float acc = 0.0f;
     for (int64_t h = 0; h < p.heads; ++h) {
         float dot = 0.0f;

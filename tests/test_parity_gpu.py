@@ -142,6 +142,40 @@ def test_chunk_subset_entry_matches_full_run(c1):
     assert np.array_equal(di.cpu().numpy(), expect)
 
 
+@pytest.mark.parametrize("B", [1, 2])
+def test_rank_local_operands_match_full_tensors(orc, B):
+    """A query-sharded rank keeps only its chunks' q / w rows
+    (csaidx_device_run_chunked_local / csaidx_host_run_chunked_local): the
+    result equals the run over the full tensors, for the tcgen05 shape and
+    for the exact-order kernel."""
+    import torch
+
+    for (H, D, S, k, cs) in [(64, 128, 2048, 128, 256), (3, 5, 96, 7, 16)]:
+        q, kc, w = orc.generate_inputs(B, S, 4, H, D, 5, bf16=(H == 64))
+        dims = api.ProblemDims.create(B, S, 4, H, D, k)
+        cfg = api.DriverConfig(tile=api.TileConfig(cs, 10 ** 6))
+        starts = [S - cs, cs, 0] if S > 2 * cs else [0]
+        rows = api.chunk_rows(dims, cfg, starts)
+        dt = torch.bfloat16 if H == 64 else torch.float32
+        qd, kd, wd = torch.from_numpy(q).cuda().to(dt), torch.from_numpy(kc).cuda().to(dt), torch.from_numpy(w).cuda()
+        fi, fv, _ = api.run_chunked_device(qd, kd, wd, dims, cfg, starts)
+        ql = torch.cat([torch.cat([qd[b, s0:s0 + cs] for s0 in starts]) for b in range(B)]).contiguous()
+        wl = torch.cat([torch.cat([wd[b, s0:s0 + cs] for s0 in starts]) for b in range(B)]).contiguous()
+        li, lv, _ = api.run_chunked_device(ql, kd, wl, dims, cfg, starts, local_rows=True)
+        assert torch.equal(li, fi) and torch.equal(lv.view(torch.int32), fv.view(torch.int32))
+        # host entry with rank-local host rows
+        qh = np.ascontiguousarray(np.concatenate([np.concatenate([q[b, s0:s0 + cs] for s0 in starts])[None]
+                                                  for b in range(B)]))
+        wh = np.ascontiguousarray(np.concatenate([np.concatenate([w[b, s0:s0 + cs] for s0 in starts])[None]
+                                                  for b in range(B)]))
+        oi = np.empty((B, rows, k), np.int64)
+        ov = np.empty((B, rows, k), np.float32)
+        api.run_chunked_rows(qh, kc, wh, dims, cfg, starts, oi, ov, local_rows=True)
+        assert np.array_equal(oi, fi.cpu().numpy())
+        with pytest.raises(ValueError):
+            api.run_chunked_device(qd, kd, wd, dims, cfg, starts, local_rows=True)
+
+
 def test_ablations_follow_reference_semantics(orc):
     # acceptance.cpp:339-380 directions at a small V4-like shape
     inputs, dims, (q, kc, w) = inputs_for(orc, 1, 2048, 4, 8, 64, 64, 1)
