@@ -95,17 +95,22 @@ __device__ __forceinline__ void decode_item(const ScoreTcParams& p, int idx, Ite
 }
 
 // Epilogue math for one query of one accumulator: 64 head partials of one
-// key row -> sum_h w_h * relu(x_h). 48 heads take ReLU on the ALU pipe
-// (FMNMX), 16 heads as x + |x| = 2 relu(x) on the FMA pipe (scaled back by
-// an exact 0.5 at the end), and all products go through packed FFMA2 into
-// five independent chains, balancing the two pipes.
+// key row -> sum_h w_h * relu(x_h): ReLU on the ALU pipe (FMNMX), products
+// as packed FFMA2 on the FMA pipe into four independent chains.
+//
+// The epilogue paces the MMA: with the head math removed the kernel runs
+// ~21% faster at C3 (energy/pacing probe, profiles/r01_ncu_history.md).
+// Measured alternatives that shift ReLU onto the FMA pipe — 2 relu(x) =
+// x + |x| as an FADD, or folded into a second FFMA2 with the |x| operand
+// modifier — were equal (16 heads) or slower (16/32 heads as |x|-FFMA2):
+// FFMA2 does not double the FMA pipe's rate, so the ALU pipe taking every
+// ReLU is the balanced split.
 //
 // The 64 columns are read from TMEM in four 16-column slices so the whole
-// epilogue fits the 96 registers a 640-thread CTA allows; four epilogue
-// warps per sub-partition hide the extra load latency. Chain assignment and
-// order do not depend on the slicing.
+// epilogue fits the 96 registers a 640-thread CTA allows; chain assignment
+// and order do not depend on the slicing.
 __device__ __forceinline__ float head_reduce_tmem(uint32_t taddr, const float* __restrict__ wq) {
-    float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, d0 = a0, d1 = a0;
+    float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
 #pragma unroll
     for (int part = 0; part < 4; ++part) {
         float v[16];
@@ -115,24 +120,15 @@ __device__ __forceinline__ float head_reduce_tmem(uint32_t taddr, const float* _
         for (int jj = 0; jj < 4; ++jj) {
             const int j = part * 4 + jj;
             const float4 w4 = *reinterpret_cast<const float4*>(wq + 4 * j);
-            const float x0 = v[4 * jj], x1 = v[4 * jj + 1], x2 = v[4 * jj + 2], x3 = v[4 * jj + 3];
-            if ((j & 3) == 3) {
-                const float2 r01 = make_float2(x0 + fabsf(x0), x1 + fabsf(x1));
-                const float2 r23 = make_float2(x2 + fabsf(x2), x3 + fabsf(x3));
-                d0 = __ffma2_rn(r01, make_float2(w4.x, w4.y), d0);
-                d1 = __ffma2_rn(r23, make_float2(w4.z, w4.w), d1);
-            } else {
-                const float2 r01 = make_float2(fmaxf(x0, 0.f), fmaxf(x1, 0.f));
-                const float2 r23 = make_float2(fmaxf(x2, 0.f), fmaxf(x3, 0.f));
-                float2& acc = (j & 3) == 0 ? a0 : ((j & 3) == 1 ? a1 : a2);
-                acc = __ffma2_rn(r01, make_float2(w4.x, w4.y), acc);
-                acc = __ffma2_rn(r23, make_float2(w4.z, w4.w), acc);
-            }
+            const float2 r01 = make_float2(fmaxf(v[4 * jj], 0.f), fmaxf(v[4 * jj + 1], 0.f));
+            const float2 r23 = make_float2(fmaxf(v[4 * jj + 2], 0.f), fmaxf(v[4 * jj + 3], 0.f));
+            float2& x = (j & 1) ? a1 : a0;
+            float2& y = (j & 1) ? a3 : a2;
+            x = __ffma2_rn(r01, make_float2(w4.x, w4.y), x);
+            y = __ffma2_rn(r23, make_float2(w4.z, w4.w), y);
         }
     }
-    const float main = ((a0.x + a0.y) + (a1.x + a1.y)) + (a2.x + a2.y);
-    const float dbl = (d0.x + d0.y) + (d1.x + d1.y);
-    return fmaf(0.5f, dbl, main);
+    return ((a0.x + a0.y) + (a1.x + a1.y)) + ((a2.x + a2.y) + (a3.x + a3.y));
 }
 
 __global__ void __launch_bounds__(kNumThreads, 1)

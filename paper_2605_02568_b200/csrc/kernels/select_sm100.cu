@@ -38,6 +38,11 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+
+// All selection code runs on one group of kThreads threads synchronised by
+// named barrier 1 (the whole CTA of select_kernel / tau_kernel), so the row
+// stages can also serve a CTA with extra, non-participating warps.
+__device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory"); }
 constexpr int kBins = 2048;
 constexpr int kMaxTake = 4096;    // largest min(k, n) a row may select
 constexpr int kMaxCand = 8192;    // largest shared candidate list
@@ -85,7 +90,7 @@ __device__ __forceinline__ int64_t composite_col(uint64_t c) {
 __device__ void bitonic_sort_desc(uint64_t* a, int P) {
     for (int size = 2; size <= P; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int i = threadIdx.x; i < P / 2; i += blockDim.x) {
+            for (int i = threadIdx.x; i < P / 2; i += kThreads) {
                 const int lo = 2 * i - (i & (stride - 1));
                 const int hi = lo + stride;
                 const bool desc = (lo & size) == 0;
@@ -95,12 +100,12 @@ __device__ void bitonic_sort_desc(uint64_t* a, int P) {
                     a[hi] = x;
                 }
             }
-            __syncthreads();
+            csync();
         }
     }
 }
 
-// Descending bitonic sort of a[0, P) with P == E * blockDim.x: each thread
+// Descending bitonic sort of a[0, P) with P == E * kThreads: each thread
 // holds E consecutive elements in registers; strides < E are in-register,
 // strides < 32E go through warp shuffles, and only the strides that cross
 // warps touch shared memory (6 barrier stages for P = 1024 instead of 55).
@@ -142,10 +147,10 @@ __device__ __forceinline__ void bitonic_sort_desc_regs(uint64_t* a) {
                         x[e] = ((x[e] > other) == keep_max) ? x[e] : other;
                     }
                 } else {
-                    __syncthreads();
+                    csync();
 #pragma unroll
                     for (int e = 0; e < E; ++e) a[t * E + e] = x[e];
-                    __syncthreads();
+                    csync();
 #pragma unroll
                     for (int e = 0; e < E; ++e) {
                         const uint64_t other = a[(t * E + e) ^ stride];
@@ -155,14 +160,14 @@ __device__ __forceinline__ void bitonic_sort_desc_regs(uint64_t* a) {
             }
         }
     }
-    __syncthreads();
+    csync();
 #pragma unroll
     for (int e = 0; e < E; ++e) a[t * E + e] = x[e];
-    __syncthreads();
+    csync();
 }
 
 __device__ void sort_desc(uint64_t* a, int P) {
-    switch (P / static_cast<int>(blockDim.x)) {
+    switch (P / kThreads) {
         case 1: bitonic_sort_desc_regs<1>(a); break;
         case 2: bitonic_sort_desc_regs<2>(a); break;
         case 4: bitonic_sort_desc_regs<4>(a); break;
@@ -176,7 +181,7 @@ __device__ void sort_desc(uint64_t* a, int P) {
 // locates the run, its owner walks it. out3 = {bin, count above, bin count}.
 __device__ void find_bin(const uint32_t* hist, int nbins, uint32_t kk, uint32_t* out3, uint32_t* wsum) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int per = nbins >= static_cast<int>(blockDim.x) ? nbins / blockDim.x : 1;
+    const int per = nbins >= kThreads ? nbins / kThreads : 1;
     const int hi = nbins - static_cast<int>(threadIdx.x) * per;  // thread 0 owns the highest bins
     uint32_t sum = 0;
     for (int b = hi - 1; b >= hi - per && b >= 0; --b) sum += hist[b];
@@ -187,7 +192,7 @@ __device__ void find_bin(const uint32_t* hist, int nbins, uint32_t kk, uint32_t*
         if (lane >= o) incl += v;
     }
     if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
+    csync();
     uint32_t before = 0;
     for (int w = 0; w < warp; ++w) before += wsum[w];
     const uint32_t excl = before + incl - sum;
@@ -204,7 +209,7 @@ __device__ void find_bin(const uint32_t* hist, int nbins, uint32_t kk, uint32_t*
             cum += c;
         }
     }
-    __syncthreads();
+    csync();
 }
 
 // Exactly the kk largest of the unique 64-bit values a[0, n) (shared memory)
@@ -220,9 +225,9 @@ __device__ void smem_take_top(const uint64_t* a, int n, uint32_t kk, uint64_t* d
         s_mm[1] = 0ull;
         *counter = 0;
     }
-    __syncthreads();
+    csync();
     unsigned long long mn = ~0ull, mx = 0ull;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    for (int i = threadIdx.x; i < n; i += kThreads) {
         mn = min(mn, static_cast<unsigned long long>(a[i]));
         mx = max(mx, static_cast<unsigned long long>(a[i]));
     }
@@ -235,24 +240,24 @@ __device__ void smem_take_top(const uint64_t* a, int n, uint32_t kk, uint64_t* d
         atomicMin(&s_mm[0], mn);
         atomicMax(&s_mm[1], mx);
     }
-    __syncthreads();
+    csync();
     const uint64_t lo = s_mm[0], hi = s_mm[1];
     int pbits = lo == hi ? 64 : __clzll(static_cast<long long>(lo ^ hi));
     uint64_t prefix = pbits == 0 ? 0ull : (pbits == 64 ? lo : (lo >> (64 - pbits)));
     while (pbits < 64) {
         const int wbits = 64 - pbits < 11 ? 64 - pbits : 11;
         const int shift = 64 - pbits - wbits;
-        for (int i = threadIdx.x; i < kBins; i += blockDim.x) hist[i] = 0;
-        __syncthreads();
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        for (int i = threadIdx.x; i < kBins; i += kThreads) hist[i] = 0;
+        csync();
+        for (int i = threadIdx.x; i < n; i += kThreads) {
             const uint64_t v = a[i];
             if (pbits == 0 || (v >> (64 - pbits)) == prefix)
                 atomicAdd(&hist[static_cast<uint32_t>(v >> shift) & ((1u << wbits) - 1u)], 1u);
         }
-        __syncthreads();
+        csync();
         find_bin(hist, 1 << wbits, kk, res, wsum);
         const uint32_t bin = res[0], above = res[1], cnt = res[2];
-        __syncthreads();
+        csync();
         kk -= above;
         prefix = (pbits == 0 ? 0ull : (prefix << wbits)) | bin;
         pbits += wbits;
@@ -260,7 +265,7 @@ __device__ void smem_take_top(const uint64_t* a, int n, uint32_t kk, uint64_t* d
     }
     // keep the values whose top pbits are >= prefix (exactly the requested count)
     const int nr = (n + 31) & ~31;
-    for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+    for (int i = threadIdx.x; i < nr; i += kThreads) {
         const uint64_t v = i < n ? a[i] : 0ull;
         const bool keep = i < n && (pbits >= 64 ? v >= prefix : (v >> (64 - pbits)) >= prefix);
         const uint32_t m = __ballot_sync(0xffffffffu, keep);
@@ -269,7 +274,7 @@ __device__ void smem_take_top(const uint64_t* a, int n, uint32_t kk, uint64_t* d
         base = __shfl_sync(0xffffffffu, base, 0);
         if (keep) dst[base + __popc(m & ((1u << lane) - 1u))] = v;
     }
-    __syncthreads();
+    csync();
 }
 
 // Value-linear bucket of a composite between the list's min (lo) and max.
@@ -300,28 +305,28 @@ __device__ bool bucket_finish(uint64_t* a, int n, int take, uint64_t* tmp, int t
     }
     float lo = plo, scale = pscale;  // prebuilt: start[] already holds the histogram over (plo, pscale)
     if (!prebuilt) {
-        for (int i = threadIdx.x; i < kFinBins; i += blockDim.x) start[i] = 0;
+        for (int i = threadIdx.x; i < kFinBins; i += kThreads) start[i] = 0;
         uint32_t kmin = 0xffffffffu, kmax = 0u;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        for (int i = threadIdx.x; i < n; i += kThreads) {
             const uint32_t key = static_cast<uint32_t>(a[i] >> 32);
             kmin = min(kmin, key);
             kmax = max(kmax, key);
         }
         kmin = __reduce_min_sync(0xffffffffu, kmin);
         kmax = __reduce_max_sync(0xffffffffu, kmax);
-        __syncthreads();
+        csync();
         if (lane == 0) {
             atomicMin(&sc[0], kmin);
             atomicMax(&sc[1], kmax);
         }
-        __syncthreads();
+        csync();
         lo = ord_key_to_float(sc[0]);
         const float hi = ord_key_to_float(sc[1]);
         scale = static_cast<float>(kFinBins) / (hi - lo);
         if (!(hi > lo) || !isfinite(scale)) scale = 0.f;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&start[fin_bin(a[i], lo, scale)], 1u);
+        for (int i = threadIdx.x; i < n; i += kThreads) atomicAdd(&start[fin_bin(a[i], lo, scale)], 1u);
     }
-    __syncthreads();
+    csync();
     // descending exclusive scan: thread t owns bins [NB-4t-4, NB-4t), highest first
     constexpr int kPer = kFinBins / 256;
     static_assert(kFinBins % 256 == 0, "bins per thread");
@@ -342,7 +347,7 @@ __device__ bool bucket_finish(uint64_t* a, int n, int take, uint64_t* tmp, int t
         if (lane >= o) incl += v;
     }
     if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
+    csync();
     uint32_t before = 0;
     for (int w = 0; w < warp; ++w) before += wsum[w];
     if (threadIdx.x < 256) {
@@ -360,16 +365,16 @@ __device__ bool bucket_finish(uint64_t* a, int n, int take, uint64_t* tmp, int t
             run += c[u];
         }
     }
-    __syncthreads();
+    csync();
     if (sc[2] != 0u) return false;
     const uint32_t extent = sc[3];
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    for (int i = threadIdx.x; i < n; i += kThreads) {
         const uint64_t v = a[i];
         const int b = fin_bin(v, lo, scale);
         if (start[b] < static_cast<uint32_t>(take)) tmp[atomicAdd(&cur[b], 1u)] = v;
     }
-    __syncthreads();
-    for (uint32_t s = threadIdx.x; s < extent; s += blockDim.x) {
+    csync();
+    for (uint32_t s = threadIdx.x; s < extent; s += kThreads) {
         const uint64_t v = tmp[s];
         const int b = fin_bin(v, lo, scale);
         const uint32_t b0 = start[b], b1 = cur[b];
@@ -377,7 +382,7 @@ __device__ bool bucket_finish(uint64_t* a, int n, int take, uint64_t* tmp, int t
         for (uint32_t j = b0; j < b1; ++j) r += tmp[j] > v ? 1u : 0u;
         if (b0 + r < static_cast<uint32_t>(take)) a[b0 + r] = v;
     }
-    __syncthreads();
+    csync();
     return true;
 }
 
@@ -390,15 +395,15 @@ __device__ __forceinline__ bool prefix_match(uint32_t key, uint32_t prefix, int 
 }
 
 __device__ void histogram_pass(const float* row, int64_t n, uint32_t prefix, int pbits, int wbits, uint32_t* hist) {
-    for (int i = threadIdx.x; i < kBins; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
+    for (int i = threadIdx.x; i < kBins; i += kThreads) hist[i] = 0;
+    csync();
     const int shift = 32 - pbits - wbits;
     const uint32_t mask = (1u << wbits) - 1u;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    for (int64_t i = threadIdx.x; i < n; i += kThreads) {
         const uint32_t key = ord_key(__ldg(row + i));
         if (prefix_match(key, prefix, pbits)) atomicAdd(&hist[(key >> shift) & mask], 1u);
     }
-    __syncthreads();
+    csync();
 }
 
 // Ordered (index-ascending) block compaction: entries above the prefix go to
@@ -409,7 +414,7 @@ __device__ void collect_pass(const float* row, int64_t n, uint32_t prefix, int p
     const int warp = threadIdx.x >> 5;
     uint32_t run_above = 0, run_eq = 0;
     int parity = 0;
-    for (int64_t base = 0; base < n; base += blockDim.x) {
+    for (int64_t base = 0; base < n; base += kThreads) {
         const int64_t i = base + threadIdx.x;
         uint32_t key = 0;
         int cls = 0;
@@ -425,7 +430,7 @@ __device__ void collect_pass(const float* row, int64_t n, uint32_t prefix, int p
             wt[warp] = __popc(ma);
             wt[kWarps + warp] = __popc(me);
         }
-        __syncthreads();
+        csync();
         uint32_t off_a = 0, off_e = 0, tot_a = 0, tot_e = 0;
         for (int w = 0; w < kWarps; ++w) {
             if (w < warp) {
@@ -445,7 +450,7 @@ __device__ void collect_pass(const float* row, int64_t n, uint32_t prefix, int p
         run_eq += tot_e;
         parity ^= 1;
     }
-    __syncthreads();
+    csync();
 }
 
 __device__ void exact_global_select(const float* row, int64_t n, int k, uint64_t* buf, uint64_t* cand, int cand_cap,
@@ -463,7 +468,7 @@ __device__ void exact_global_select(const float* row, int64_t n, int k, uint64_t
         bin_count = res[2];
         prefix = (pbits == 0 ? 0u : (prefix << wbits)) | res[0];
         pbits += wbits;
-        __syncthreads();
+        csync();
         if (bin_count <= static_cast<uint32_t>(cand_cap)) break;
     }
     const uint32_t above = static_cast<uint32_t>(k) - kk;
@@ -473,15 +478,144 @@ __device__ void exact_global_select(const float* row, int64_t n, int k, uint64_t
     } else {
         collect_pass(row, n, prefix, pbits, buf, cand, static_cast<uint32_t>(cand_cap), wtot);
         const int P = pow2_at_least(static_cast<int>(bin_count));
-        for (int i = static_cast<int>(bin_count) + threadIdx.x; i < P; i += blockDim.x) cand[i] = 0;
-        __syncthreads();
+        for (int i = static_cast<int>(bin_count) + threadIdx.x; i < P; i += kThreads) cand[i] = 0;
+        csync();
         sort_desc(cand, P);
-        for (uint32_t i = threadIdx.x; i < kk; i += blockDim.x) buf[above + i] = cand[i];
+        for (uint32_t i = threadIdx.x; i < kk; i += kThreads) buf[above + i] = cand[i];
     }
-    __syncthreads();
+    csync();
+}
+
+// ------------------------------------------------------------------ shared row stages
+
+// Survivor columns idx_list[0, count) of `row` -> 64-bit composites in
+// cand[0, count) (their scores were just streamed: L2 hits; each thread's
+// loads are all in flight at once). When count fits the fused form the
+// finish buckets over [lo_f, hi_f] (threshold, sample max) are counted into
+// hist[0, kFinBins) on the way (prebuilt). count < 0: nothing to do.
+__device__ void gather_candidates(const float* row, const uint32_t* idx_list, int count, uint64_t* cand,
+                                  uint32_t* hist, float lo_f, float hi_f, bool& prebuilt, float& pb_lo,
+                                  float& pb_scale, bool build_hist = true) {
+    if (build_hist && count >= 0 && count <= kGatherPer * kThreads) {
+        uint32_t cc[kGatherPer];
+#pragma unroll
+        for (int g = 0; g < kGatherPer; ++g) {
+            const int i = threadIdx.x + g * kThreads;
+            cc[g] = i < count ? idx_list[i] : 0u;
+        }
+        csync();  // the list (it may alias hist) is consumed
+        for (int i = threadIdx.x; i < kFinBins; i += kThreads) hist[i] = 0;
+        pb_lo = lo_f;
+        pb_scale = static_cast<float>(kFinBins) / (hi_f - lo_f);
+        if (!(hi_f > lo_f) || !isfinite(pb_scale)) pb_scale = 0.f;
+        csync();
+#pragma unroll
+        for (int h = 0; h < kGatherPer; h += 8) {
+            float vv[8];
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+                vv[g] = threadIdx.x + (h + g) * kThreads < count ? __ldg(row + cc[h + g]) : 0.f;
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                const int i = threadIdx.x + (h + g) * kThreads;
+                if (i < count) {
+                    const uint64_t c = composite(ord_key(vv[g]), cc[h + g]);
+                    cand[i] = c;
+                    atomicAdd(&hist[fin_bin(c, pb_lo, pb_scale)], 1u);
+                }
+            }
+        }
+        prebuilt = true;
+    } else if (count >= 0) {
+        constexpr int G = 8;
+        for (int base = threadIdx.x; base < count; base += G * kThreads) {
+            uint32_t cc[G];
+            float vv[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const int i = base + g * kThreads;
+                cc[g] = i < count ? idx_list[i] : 0u;
+            }
+#pragma unroll
+            for (int g = 0; g < G; ++g) vv[g] = base + g * kThreads < count ? __ldg(row + cc[g]) : 0.f;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const int i = base + g * kThreads;
+                if (i < count) cand[i] = composite(ord_key(vv[g]), cc[g]);
+            }
+        }
+    }
+    csync();
+}
+
+// The sorted top `take` of a row. count >= 0: from the unique candidates
+// cand[0, count) (bucket finish, or for heavy ties a shared-memory radix
+// select + register bitonic sort); count < 0 (the threshold mispredicted):
+// exact radix select over the row in global memory. Returns the array that
+// holds the result (cand or buf).
+__device__ const uint64_t* finish_row(const float* row, int64_t n, int take, int count, const Layout& L,
+                                      uint64_t* cand, uint64_t* buf, uint32_t* hist, uint32_t* wtot,
+                                      uint32_t* wsum, uint32_t* res, uint32_t* counter, bool prebuilt, float pb_lo,
+                                      float pb_scale, int* fallbacks) {
+    if (count >= 0) {
+        if (bucket_finish(cand, count, take, buf, L.buf_cap, hist, hist + kFinBins, wsum, res, prebuilt, pb_lo,
+                          pb_scale))
+            return cand;
+        if (count > take) {
+            smem_take_top(cand, count, static_cast<uint32_t>(take), buf, hist, res, wsum, counter);
+        } else {
+            for (int i = threadIdx.x; i < count; i += kThreads) buf[i] = cand[i];
+        }
+    } else {
+        if (threadIdx.x == 0 && fallbacks != nullptr) atomicAdd(fallbacks, 1);
+        exact_global_select(row, n, take, buf, cand, L.cand_cap, hist, wtot, res, wsum);
+    }
+    const int P = pow2_at_least(take);
+    for (int i = take + threadIdx.x; i < P; i += kThreads) buf[i] = 0;
+    csync();
+    sort_desc(buf, P);
+    return buf;
+}
+
+// Output row: the first `take` entries of result (best first), the rest
+// (-inf, -1); int32 candidate rows, or with final_idx the int64 output rows
+// of the fused sentinel pass (finalize_kernel semantics).
+__device__ void write_row(const SelectParams& p, int b, int64_t row_id, int take, const uint64_t* result) {
+    const bool final_out = p.final_idx != nullptr;
+    const int64_t orow = final_out ? static_cast<int64_t>(b) * p.final_rows + p.final_row0 + row_id
+                                   : static_cast<int64_t>(b) * p.rows + row_id;
+    float* ov = p.out_val + orow * p.out_ld;
+    const float neg_inf = -__int_as_float(0x7f800000);
+    if (final_out) {
+        int64_t* oi = p.final_idx + orow * p.out_ld;
+        for (int e = threadIdx.x; e < p.width; e += kThreads) {
+            if (e < take) {
+                const uint64_t c = result[e];
+                const float v = ord_key_to_float(static_cast<uint32_t>(c >> 32));
+                ov[e] = v;
+                oi[e] = v == neg_inf ? -1 : composite_col(c) + p.t0;
+            } else {
+                ov[e] = neg_inf;
+                oi[e] = -1;
+            }
+        }
+        return;
+    }
+    int32_t* oi = p.out_idx + orow * p.out_ld;
+    for (int e = threadIdx.x; e < p.width; e += kThreads) {
+        if (e < take) {
+            const uint64_t c = result[e];
+            ov[e] = ord_key_to_float(static_cast<uint32_t>(c >> 32));
+            oi[e] = static_cast<int32_t>(composite_col(c) + p.t0);
+        } else {
+            ov[e] = neg_inf;
+            oi[e] = -1;
+        }
+    }
 }
 
 // ------------------------------------------------------------------ kernel
+
 
 template <int kUnroll, int kMinBlocks>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const SelectParams p) {
@@ -522,17 +656,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const Sele
             const uint32_t* bits = p.pass_bits + (static_cast<int64_t>(b) * p.rows + row_id) * p.bits_ld;
             const int nw = static_cast<int>((n + 31) >> 5);
             if (threadIdx.x == 0) *counter = 0;
-            __syncthreads();
+            csync();
             uint32_t loc = 0;
             for (int i = threadIdx.x; i < nw; i += kThreads) loc += __popc(__ldg(bits + i));
             loc = __reduce_add_sync(0xffffffffu, loc);
             if (lane == 0 && loc != 0) atomicAdd(counter, loc);
-            __syncthreads();
+            csync();
             const uint32_t tot = *counter;
-            __syncthreads();
+            csync();
             if (tot >= static_cast<uint32_t>(take) && tot <= static_cast<uint32_t>(L.cand_cap)) {
                 if (threadIdx.x == 0) *counter = 0;
-                __syncthreads();
+                csync();
                 for (int i = threadIdx.x; i < nw; i += kThreads) {
                     uint32_t m = __ldg(bits + i);
                     if (m == 0) continue;
@@ -545,15 +679,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const Sele
                 }
                 pre = static_cast<int>(tot);
                 if (threadIdx.x == 0 && p.cand_hits != nullptr) atomicAdd(p.cand_hits, 1);
-                __syncthreads();
+                csync();
             }
         }
         if (pre >= 0) {
             count = pre;
         } else if (n <= L.cand_cap) {
-            for (int64_t i = threadIdx.x; i < n; i += blockDim.x) cand[i] = composite(ord_key(__ldg(row + i)), i);
+            for (int64_t i = threadIdx.x; i < n; i += kThreads) cand[i] = composite(ord_key(__ldg(row + i)), i);
             count = static_cast<int>(n);
-            __syncthreads();
+            csync();
         } else {
             // 1. sample evenly spaced 512-byte segments (one float4 per lane,
             //    ~1/16 of the row, <= 8192 values), held in registers; each
@@ -587,15 +721,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const Sele
                 res[6] = 0xffffffffu;
                 res[7] = 0u;
             }
-            for (int i = threadIdx.x; i < kBins; i += blockDim.x) hist[i] = 0;
-            __syncthreads();
+            for (int i = threadIdx.x; i < kBins; i += kThreads) hist[i] = 0;
+            csync();
             kmin = __reduce_min_sync(0xffffffffu, kmin);
             kmax = __reduce_max_sync(0xffffffffu, kmax);
             if (lane == 0) {
                 atomicMin(&res[6], kmin);
                 atomicMax(&res[7], kmax);
             }
-            __syncthreads();
+            csync();
             if (clk) clk[5] = clock64();
             const int ns = 128 * nseg;
             // ~2k survivors: a comfortable margin over k (misses -> the slow
@@ -616,9 +750,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const Sele
                 float scale = static_cast<float>(kBins) / (hi - lo);
                 if (!(hi > lo) || !isfinite(scale)) break;  // degenerate: keep tau = lo
                 if (pass > 0) {
-                    for (int i = threadIdx.x; i < kBins; i += blockDim.x) hist[i] = 0;
+                    for (int i = threadIdx.x; i < kBins; i += kThreads) hist[i] = 0;
                     if (threadIdx.x == 0) res[0] = res[1] = res[2] = 0u;
-                    __syncthreads();
+                    csync();
                 }
 #pragma unroll
                 for (int u = 0; u < kSegsPerWarp; ++u) {
@@ -633,10 +767,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const Sele
                         }
                     }
                 }
-                __syncthreads();
+                csync();
                 find_bin(hist, kBins, rr, res, wsum);
                 const uint32_t bin = res[0], above = res[1], cnt = res[2];
-                __syncthreads();
+                csync();
                 const float width = (hi - lo) / static_cast<float>(kBins);
                 const float blo = lo + static_cast<float>(bin) * width;
                 tau_f = blo > lo ? blo : lo;
@@ -657,7 +791,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const Sele
             // 2. stream the row once; keep entries >= tau
             const float4* row4 = reinterpret_cast<const float4*>(row);
             const int64_t n4 = n >> 2;
-            const int64_t step = kUnroll * static_cast<int64_t>(blockDim.x);
+            const int64_t step = kUnroll * static_cast<int64_t>(kThreads);
             const int64_t n4r = (n4 + step - 1) / step * step;
             const uint32_t cap = static_cast<uint32_t>(
                 min(L.cand_cap, 2 * L.buf_cap + kBins));  // idx list capacity
@@ -665,7 +799,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const Sele
                 float4 v[kUnroll];
 #pragma unroll
                 for (int u = 0; u < kUnroll; ++u) {
-                    const int64_t i4 = it + u * blockDim.x;
+                    const int64_t i4 = it + u * kThreads;
                     v[u] = i4 < n4 ? __ldg(row4 + i4) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
                 }
                 uint32_t m = 0;
@@ -714,134 +848,26 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const Sele
                     if (pass && pos < cap) idx_list[pos] = static_cast<uint32_t>(i);
                 }
             }
-            __syncthreads();
+            csync();
             const uint32_t total = *counter;
             count = (total >= static_cast<uint32_t>(k) && total <= cap) ? static_cast<int>(total) : -1;
-            if (count >= 0 && count <= kGatherPer * kThreads) {
-                // gather the survivors' scores (just streamed: L2 hits) into
-                // composites and count them into the finish buckets over
-                // [tau, sample max] (entries above the sample max clamp into
-                // the top bucket)
-                uint32_t cc[kGatherPer];
-#pragma unroll
-                for (int g = 0; g < kGatherPer; ++g) {
-                    const int i = threadIdx.x + g * kThreads;
-                    cc[g] = i < count ? idx_list[i] : 0u;
-                }
-                __syncthreads();  // the list (aliasing hist) is consumed
-                for (int i = threadIdx.x; i < kFinBins; i += blockDim.x) hist[i] = 0;
-                pb_lo = tau_f;
-                pb_scale = static_cast<float>(kFinBins) / (smax - tau_f);
-                if (!(smax > tau_f) || !isfinite(pb_scale)) pb_scale = 0.f;
-                __syncthreads();
-#pragma unroll
-                for (int h = 0; h < kGatherPer; h += 8) {
-                    float vv[8];
-#pragma unroll
-                    for (int g = 0; g < 8; ++g)
-                        vv[g] = threadIdx.x + (h + g) * kThreads < count ? __ldg(row + cc[h + g]) : 0.f;
-#pragma unroll
-                    for (int g = 0; g < 8; ++g) {
-                        const int i = threadIdx.x + (h + g) * kThreads;
-                        if (i < count) {
-                            const uint64_t c = composite(ord_key(vv[g]), cc[h + g]);
-                            cand[i] = c;
-                            atomicAdd(&hist[fin_bin(c, pb_lo, pb_scale)], 1u);
-                        }
-                    }
-                }
-                prebuilt = true;
-            } else if (count >= 0) {
-                constexpr int G = 8;
-                for (int base = threadIdx.x; base < count; base += G * kThreads) {
-                    uint32_t cc[G];
-                    float vv[G];
-#pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        const int i = base + g * kThreads;
-                        cc[g] = i < count ? idx_list[i] : 0u;
-                    }
-#pragma unroll
-                    for (int g = 0; g < G; ++g) vv[g] = base + g * kThreads < count ? __ldg(row + cc[g]) : 0.f;
-#pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        const int i = base + g * kThreads;
-                        if (i < count) cand[i] = composite(ord_key(vv[g]), cc[g]);
-                    }
-                }
-            }
-            __syncthreads();
+            gather_candidates(row, idx_list, count, cand, hist, tau_f, smax, prebuilt, pb_lo, pb_scale);
         }
 
         if (clk) clk[2] = clock64();
-        if (count >= 0) {
-            if (clk) {
-                clk[6] = count;
-                clk[7] = clock64();
-            }
-            // 3. the sorted top `take` of the (unique) candidates: bucket
-            //    finish, or (heavy ties) a shared-memory radix select + one
-            //    register/shuffle bitonic sort
-            if (bucket_finish(cand, count, take, buf, L.buf_cap, hist, hist + kFinBins, wsum, res, prebuilt, pb_lo,
-                              pb_scale)) {
-                result = cand;
-            } else {
-                if (count > take) {
-                    smem_take_top(cand, count, static_cast<uint32_t>(take), buf, hist, res, wsum, counter);
-                } else {
-                    for (int i = threadIdx.x; i < count; i += blockDim.x) buf[i] = cand[i];
-                }
-                const int P = pow2_at_least(take);
-                for (int i = take + threadIdx.x; i < P; i += blockDim.x) buf[i] = 0;
-                __syncthreads();
-                sort_desc(buf, P);
-            }
-        } else {
-            if (threadIdx.x == 0 && p.fallbacks != nullptr) atomicAdd(p.fallbacks, 1);
-            exact_global_select(row, n, take, buf, cand, L.cand_cap, hist, wtot, res, wsum);
-            const int P = pow2_at_least(take);
-            for (int i = take + threadIdx.x; i < P; i += blockDim.x) buf[i] = 0;
-            __syncthreads();
-            sort_desc(buf, P);
+        if (clk) {
+            clk[6] = count;
+            clk[7] = clock64();
         }
+        result = finish_row(row, n, take, count, L, cand, buf, hist, wtot, wsum, res, counter, prebuilt, pb_lo,
+                            pb_scale, p.fallbacks);
     }
 
     if (clk) {
         clk[3] = clock64();
         clk[4] = n;
     }
-    const bool final_out = p.final_idx != nullptr;
-    const int64_t orow = final_out ? static_cast<int64_t>(b) * p.final_rows + p.final_row0 + row_id
-                                   : static_cast<int64_t>(b) * p.rows + row_id;
-    float* ov = p.out_val + orow * p.out_ld;
-    const float neg_inf = -__int_as_float(0x7f800000);
-    if (final_out) {
-        // fused sentinel pass (finalize_kernel): int64 indices, (-inf, -1) tail
-        int64_t* oi = p.final_idx + orow * p.out_ld;
-        for (int e = threadIdx.x; e < p.width; e += blockDim.x) {
-            if (e < take) {
-                const uint64_t c = result[e];
-                const float v = ord_key_to_float(static_cast<uint32_t>(c >> 32));
-                ov[e] = v;
-                oi[e] = v == neg_inf ? -1 : composite_col(c) + p.t0;
-            } else {
-                ov[e] = neg_inf;
-                oi[e] = -1;
-            }
-        }
-        return;
-    }
-    int32_t* oi = p.out_idx + orow * p.out_ld;
-    for (int e = threadIdx.x; e < p.width; e += blockDim.x) {
-        if (e < take) {
-            const uint64_t c = result[e];
-            ov[e] = ord_key_to_float(static_cast<uint32_t>(c >> 32));
-            oi[e] = static_cast<int32_t>(composite_col(c) + p.t0);
-        } else {
-            ov[e] = neg_inf;
-            oi[e] = -1;
-        }
-    }
+    write_row(p, b, row_id, take, result);
 }
 
 // ------------------------------------------------------------------ tau
@@ -872,11 +898,11 @@ __global__ void __launch_bounds__(kThreads) tau_kernel(const TauParams p) {
         res[6] = 0xffffffffu;
         res[7] = 0u;
     }
-    for (int i = threadIdx.x; i < kBins; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
+    for (int i = threadIdx.x; i < kBins; i += kThreads) hist[i] = 0;
+    csync();
     uint32_t kmin = 0xffffffffu, kmax = 0u;
     const int64_t nvr = (nv + 31) & ~int64_t{31};
-    for (int64_t i = threadIdx.x; i < nvr; i += blockDim.x) {
+    for (int64_t i = threadIdx.x; i < nvr; i += kThreads) {
         const float v = i < nv ? __ldg(srow + i) : neg_inf;
         const bool keep = v != neg_inf;  // legal sampled entries (scores are finite)
         const uint32_t m = __ballot_sync(0xffffffffu, keep);
@@ -897,7 +923,7 @@ __global__ void __launch_bounds__(kThreads) tau_kernel(const TauParams p) {
         atomicMin(&res[6], kmin);
         atomicMax(&res[7], kmax);
     }
-    __syncthreads();
+    csync();
     const int ns = static_cast<int>(min(res[4], static_cast<uint32_t>(kTauMaxSamples)));
     const int target = (2 * p.k < (p.cand_cap * 3) / 4) ? 2 * p.k : (p.cand_cap * 3) / 4;
     int r = static_cast<int>((static_cast<int64_t>(target) * ns) / n);
@@ -916,19 +942,19 @@ __global__ void __launch_bounds__(kThreads) tau_kernel(const TauParams p) {
         const int wbits = 32 - pbits < 11 ? 32 - pbits : 11;
         const int shift = 32 - pbits - wbits;
         if (pass > 0) {
-            for (int i = threadIdx.x; i < kBins; i += blockDim.x) hist[i] = 0;
-            __syncthreads();
+            for (int i = threadIdx.x; i < kBins; i += kThreads) hist[i] = 0;
+            csync();
         }
-        for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+        for (int i = threadIdx.x; i < ns; i += kThreads) {
             const uint32_t v = s_keys[i];
             if (pbits == 0 || (v >> (32 - pbits)) == prefix) atomicAdd(&hist[(v >> shift) & ((1u << wbits) - 1u)], 1u);
         }
-        __syncthreads();
+        csync();
         find_bin(hist, 1 << wbits, rr, res, wsum);
         rr -= res[1];
         prefix = (pbits == 0 ? 0u : (prefix << wbits)) | res[0];
         pbits += wbits;
-        __syncthreads();
+        csync();
     }
     if (threadIdx.x == 0) *out = ord_key_to_float(pbits >= 32 ? prefix : (prefix << (32 - pbits)));
 }
@@ -976,6 +1002,12 @@ cudaError_t launch_select(const SelectParams& p, cudaStream_t stream) {
     if (p.rows <= 0 || p.batch <= 0) return cudaSuccess;
     // 8 float4 in flight per thread, 3 CTAs per SM (measured faster than
     // 4 x float4 at 4 CTAs per SM: scripts/probe_select.py)
+    // 8 float4 in flight per thread at 3 CTAs per SM measured faster than
+    // 4 x float4 at 4 CTAs per SM (scripts/time_select.py). Also measured
+    // slower and dropped: building the composites inside the filter loop
+    // (re-reading the score from L1) instead of the L2 gather, and a
+    // persistent warp-specialised form streaming rows through a TMA
+    // bulk-copy ring (2 CTAs/SM; 3.7 vs 5.3 TB/s on long rows).
     if (select_variant() == 1) return launch_select_variant<4, 4>(p, stream);
     return launch_select_variant<8, 3>(p, stream);
 }
