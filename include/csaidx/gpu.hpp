@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "csaidx/driver.hpp"
@@ -50,5 +51,17 @@ void run_chunked_device(const DeviceOperands& ops, const ProblemDims& dims,
                         const DriverConfig& config, const std::vector<int64_t>* chunk_starts,
                         int64_t* out_indices, float* out_values, int64_t out_rows,
                         MemoryLedger& ledger, RunStats* stats = nullptr);
+
+// Streams a CSAT input dump (tensor_io.hpp) into caller-owned device
+// buffers: q / kc as dtype (CSAIDX_DTYPE_BF16: rounded to bf16 on device,
+// strict rejects non-representable values; CSAIDX_DTYPE_F32: as stored),
+// w as fp32. With chunk_starts only those query chunks' q / w rows are read,
+// stacked like the output rows ([B, out_rows, ...], the local_rows layout);
+// kc is always whole. Throws runtime_error on a malformed file (the
+// reference's read_sections cases) and invalid_argument when the sections
+// do not match dims.
+void load_inputs_device(const std::string& path, const ProblemDims& dims, const TileConfig& tile,
+                        const std::vector<int64_t>* chunk_starts, int dtype, bool strict, void* q, void* kc,
+                        float* w);
 
 }  // namespace csaidx::gpu

@@ -77,6 +77,9 @@ int csaidx_engine_get_stream(csaidx_engine* e, void** stream);
 int csaidx_engine_use_lane(csaidx_engine* e, int lane);
 int csaidx_engine_signal(csaidx_engine* e, int slot);
 int csaidx_engine_await(csaidx_engine* e, int slot);
+/* Host-side wait for the slot's latest signal (e.g. before reusing a pinned
+ * staging buffer whose copy was enqueued before the signal). */
+int csaidx_engine_sync_slot(csaidx_engine* e, int slot);
 int csaidx_engine_num_sms(csaidx_engine* e, int* num_sms);
 /* Synchronizes the stream, then reports (and clears) latched data errors. */
 int csaidx_engine_check(csaidx_engine* e);
@@ -117,6 +120,9 @@ int csaidx_cuda_alloc(csaidx_engine* e, size_t bytes, void** ptr);
 int csaidx_cuda_free(csaidx_engine* e, void* ptr);
 int csaidx_cuda_copy(csaidx_engine* e, void* dst, const void* src, size_t bytes);
 int csaidx_cuda_memset(csaidx_engine* e, void* dst, int value, size_t bytes);
+/* Page-locked host staging memory (cudaHostAlloc) for asynchronous copies. */
+int csaidx_cuda_host_alloc(csaidx_engine* e, size_t bytes, void** ptr);
+int csaidx_cuda_host_free(csaidx_engine* e, void* ptr);
 
 /* fp32 -> bf16 (RNE) staging of q / kc (IndexerInputs::validated,
  * types.cpp:73-92: rejects non-finite; strict also rejects values that are

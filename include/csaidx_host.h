@@ -102,6 +102,30 @@ int csaidx_device_run_chunked_local(const void* q, const void* kc, int dtype, co
                                     const int64_t* chunk_starts, int64_t n_chunks, int64_t* out_idx,
                                     float* out_val, int64_t out_rows, csaidx_run_stats* stats);
 
+/* CSAT input dump (tensor_io.hpp:10-41, tensor_io.cpp:28-140). */
+typedef struct csaidx_section_info {
+    uint8_t tag;      /* 0 q, 1 kc, 2 w */
+    uint8_t rank;
+    uint32_t dims[4];
+    uint64_t elems;
+    uint64_t offset;  /* payload byte offset in the file */
+} csaidx_section_info;
+/* write_inputs_file: q / kc / w host fp32 arrays of `dims`. */
+int csaidx_host_write_inputs_file(const char* path, const float* q, const float* kc, const float* w,
+                                  const csaidx_dims* dims, uint64_t* bytes);
+/* Header scan (read_sections' checks and error messages, without loading
+ * payloads): up to max_sections infos, *n_sections = sections in the file. */
+int csaidx_host_scan_sections(const char* path, csaidx_section_info* out, int max_sections, int* n_sections);
+/* read_sections + shape check against dims into host fp32 arrays. */
+int csaidx_host_read_inputs(const char* path, const csaidx_dims* dims, float* q, float* kc, float* w);
+/* CSAT dump -> device buffers (gpu.hpp load_inputs_device): q / kc as dtype
+ * (CSAIDX_DTYPE_BF16 rounds on device; strict rejects non-representable),
+ * w fp32; only the listed query chunks' q / w rows (NULL / 0 = all), stacked
+ * in list order ([B, out_rows, ...]), for the *_run_chunked_local entries. */
+int csaidx_host_load_inputs_device(const char* path, const csaidx_dims* dims, int64_t query_tile,
+                                   const int64_t* chunk_starts, int64_t n_chunks, int dtype, int strict,
+                                   int device, void* q, void* kc, float* w);
+
 /* Pure host arithmetic of the API (types.cpp / driver.cpp), no GPU needed. */
 int csaidx_host_problem_dims(int64_t batch, int64_t seq_len, int64_t ratio, int64_t heads,
                              int64_t head_dim, int64_t top_k, csaidx_dims* out);

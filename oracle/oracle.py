@@ -164,6 +164,8 @@ class Reference:
         L.ref_chunked_peak_model_bytes.restype = c_uint64
         L.ref_chunked_peak_model_bytes.argtypes = [c_int64] * 4 + [c_int]
         L.ref_sample_chunked.argtypes = [c_int64] * 8 + [c_int, c_uint64, POINTER(c_double), POINTER(c_double)]
+        L.ref_write_inputs_file.argtypes = [ctypes.c_char_p] + [c_void_p] * 3 + [c_int64] * 6 + [POINTER(c_uint64)]
+        L.ref_read_sections_file.argtypes = [ctypes.c_char_p, POINTER(c_int), ctypes.c_char_p, c_int]
 
     def generate(self, B, S, m, H, D, k, seed):
         T = S // m
@@ -212,6 +214,20 @@ class Reference:
                                     int(early_exit), int(bool_mask), threads, _p(idx), _p(val), _p(stats),
                                     _p(peak))
         return rc, idx, val, stats, int(peak[0])
+
+    def write_inputs_file(self, path, q, kc, w, m, k):
+        """tensor_io.cpp write_inputs_file: the reference's CSAT dump of (q, kc, w)."""
+        B, S, H, D = q.shape
+        n = c_uint64(0)
+        rc = self.L.ref_write_inputs_file(path.encode(), _p(q), _p(kc), _p(w), B, S, m, H, D, k, ctypes.byref(n))
+        return rc, n.value
+
+    def read_sections_file(self, path):
+        """tensor_io.cpp read_sections on a file -> (rc, n_sections, runtime_error message)."""
+        n = c_int(0)
+        msg = ctypes.create_string_buffer(256)
+        rc = self.L.ref_read_sections_file(os.fsencode(path), ctypes.byref(n), msg, 256)
+        return rc, n.value, msg.value.decode()
 
     def sample_chunked(self, S, m, H, D, k, cs, ct, n_tiles, threads, seed=1):
         sec, pairs = c_double(), c_double()

@@ -13,7 +13,9 @@
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <stdexcept>
 #include <thread>
 #include <vector>
@@ -24,6 +26,7 @@
 #include "csaidx/memory_ledger.hpp"
 #include "csaidx/score.hpp"
 #include "csaidx/synth.hpp"
+#include "csaidx/tensor_io.hpp"
 #include "csaidx/topk.hpp"
 #include "csaidx/types.hpp"
 
@@ -226,4 +229,24 @@ int ref_sample_chunked(int64_t S, int64_t m, int64_t H, int64_t D, int64_t k, in
     });
 }
 
+// tensor_io.cpp: the CSAT input dump (write_inputs_file) and its reader.
+int ref_write_inputs_file(const char* path, const float* q, const float* kc, const float* w, int64_t B, int64_t S,
+                          int64_t m, int64_t H, int64_t D, int64_t k, uint64_t* bytes) {
+    return guarded([&] {
+        const auto d = ProblemDims::create(B, S, m, H, D, k);
+        *bytes = write_inputs_file(path, wrap(q, kc, w, d), d);
+    });
+}
+// tensor_io.cpp read_sections on a file: section count, or the exception
+// message (runtime_error -> rc 2).
+int ref_read_sections_file(const char* path, int* n_sections, char* msg, int msg_len) {
+    try {
+        std::ifstream is(path, std::ios::binary);
+        *n_sections = static_cast<int>(read_sections(is).size());
+        return 0;
+    } catch (const std::runtime_error& e) {
+        std::snprintf(msg, static_cast<size_t>(msg_len), "%s", e.what());
+        return 2;
+    }
+}
 }  // extern "C"

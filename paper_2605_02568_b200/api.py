@@ -76,8 +76,19 @@ class RunStatsC(Structure):
     ]
 
 
+class SectionInfoC(Structure):
+    _fields_ = [("tag", ctypes.c_uint8), ("rank", ctypes.c_uint8), ("dims", ctypes.c_uint32 * 4),
+                ("elems", c_uint64), ("offset", c_uint64)]
+
+
 _F = POINTER(ctypes.c_float)
 HOST_SYMBOLS = {
+    "csaidx_host_write_inputs_file": (c_int, [ctypes.c_char_p, c_void_p, c_void_p, c_void_p, POINTER(Dims),
+                                              POINTER(c_uint64)]),
+    "csaidx_host_scan_sections": (c_int, [ctypes.c_char_p, POINTER(SectionInfoC), c_int, POINTER(c_int)]),
+    "csaidx_host_read_inputs": (c_int, [ctypes.c_char_p, POINTER(Dims), c_void_p, c_void_p, c_void_p]),
+    "csaidx_host_load_inputs_device": (c_int, [ctypes.c_char_p, POINTER(Dims), c_int64, c_void_p, c_int64, c_int,
+                                               c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "csaidx_host_last_error": (c_char_p, []),
     "csaidx_host_default_config": (None, [POINTER(RunConfig)]),
     "csaidx_host_engine": (c_int, [c_int, POINTER(c_void_p)]),
@@ -302,6 +313,69 @@ def run_chunked_rows(q, kc, w, dims: ProblemDims, config: DriverConfig, chunk_st
                  ptr(out_idx), ptr(out_val), out_idx.shape[1], ctypes.byref(st)))
     return RunStats(st.dispatch_count, st.tiles_skipped_masked, st.tiles_skipped_narrow, st.ledger_peak_bytes,
                     st.device_peak_bytes, ExecutionPath.chunked)
+
+
+# ---------------------------------------------------------------- CSAT input dump
+def write_inputs_file(path, inputs: "IndexerInputs", dims: ProblemDims) -> int:
+    """tensor_io.hpp write_inputs_file (csaidx_host_write_inputs_file); returns bytes written."""
+    n = c_uint64(0)
+    cd = dims.c()
+    q, kc, w = (np.ascontiguousarray(a, np.float32) for a in (inputs.q, inputs.kc, inputs.w))
+    _check(host_lib().csaidx_host_write_inputs_file(os.fsencode(path), _ptr(q), _ptr(kc), _ptr(w),
+                                                    ctypes.byref(cd), ctypes.byref(n)))
+    return n.value
+
+
+def scan_sections(path):
+    """Header scan with read_sections' checks: [(tag, rank, dims, elems, payload_offset)]."""
+    buf = (SectionInfoC * 8)()
+    n = c_int(0)
+    _check(host_lib().csaidx_host_scan_sections(os.fsencode(path), buf, 8, ctypes.byref(n)))
+    return [(s.tag, s.rank, tuple(s.dims[:s.rank]), s.elems, s.offset) for s in buf[:min(n.value, 8)]]
+
+
+def read_inputs(path, dims: ProblemDims):
+    """read_sections + shape check -> IndexerInputs-shaped host arrays (q, kc, w)."""
+    q = np.empty((dims.batch, dims.seq_len, dims.heads, dims.head_dim), np.float32)
+    kc = np.empty((dims.batch, dims.key_blocks, dims.head_dim), np.float32)
+    w = np.empty((dims.batch, dims.seq_len, dims.heads), np.float32)
+    cd = dims.c()
+    _check(host_lib().csaidx_host_read_inputs(os.fsencode(path), ctypes.byref(cd), _ptr(q), _ptr(kc), _ptr(w)))
+    return q, kc, w
+
+
+def load_inputs_device(path, dims: ProblemDims, config: DriverConfig, chunk_starts=None, strict=False, device=0,
+                       dtype=None):
+    """CSAT dump -> torch CUDA tensors (csaidx_host_load_inputs_device): q / kc in the score
+    kernel's operand type (bf16 for the tensor-core shape), w fp32; with chunk_starts only
+    those query chunks' q / w rows, stacked for run_chunked_device(..., local_rows=True)."""
+    import torch
+
+    if dtype is None:
+        cd0 = dims.c()
+        kern = 0 if int(config.kernel) == 0 else 1  # ScoreKernel.auto_detect -> tcgen05 when the shape allows
+        tc = _capi.cuda_lib().csaidx_cuda_score_uses_tensor_cores(ctypes.byref(cd0), _capi.DTYPE_BF16,
+                                                                   int(config.mode), kern)
+        dtype = _capi.DTYPE_BF16 if tc else _capi.DTYPE_F32
+    rows = dims.seq_len
+    starts = None
+    n_chunks = 0
+    if chunk_starts is not None:
+        starts = np.ascontiguousarray(chunk_starts, dtype=np.int64)
+        n_chunks = starts.size
+        rows = chunk_rows(dims, config, chunk_starts)
+    tdt = torch.bfloat16 if dtype == _capi.DTYPE_BF16 else torch.float32
+    dev = torch.device("cuda", device)
+    q = torch.empty((dims.batch, rows, dims.heads, dims.head_dim), dtype=tdt, device=dev)
+    kc = torch.empty((dims.batch, dims.key_blocks, dims.head_dim), dtype=tdt, device=dev)
+    w = torch.empty((dims.batch, rows, dims.heads), dtype=torch.float32, device=dev)
+    torch.cuda.synchronize(dev)
+    cd = dims.c()
+    _check(host_lib().csaidx_host_load_inputs_device(
+        os.fsencode(path), ctypes.byref(cd), config.tile.query_tile, None if starts is None else _ptr(starts),
+        n_chunks, dtype, int(strict), device, c_void_p(q.data_ptr()), c_void_p(kc.data_ptr()),
+        c_void_p(w.data_ptr())))
+    return q, kc, w
 
 
 def run_chunked_device(q, kc, w, dims: ProblemDims, config: DriverConfig, chunk_starts=None, out_idx=None,

@@ -263,6 +263,14 @@ int csaidx_engine_await(csaidx_engine* e, int slot) {
     return CSAIDX_OK;
 }
 
+int csaidx_engine_sync_slot(csaidx_engine* e, int slot) {
+    if (int rc = set_device(e)) return rc;
+    if (slot < 0 || slot >= 64) return fail(CSAIDX_INVALID_ARGUMENT, "event slot out of range");
+    if (e->slots[slot] == nullptr) return CSAIDX_OK;
+    CSAIDX_CUDA_TRY(cudaEventSynchronize(e->slots[slot]), "cudaEventSynchronize");
+    return CSAIDX_OK;
+}
+
 int csaidx_engine_use_own_stream(csaidx_engine* e) {
     if (e == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null engine");
     e->stream = e->own_stream;
@@ -421,6 +429,21 @@ int csaidx_cuda_copy(csaidx_engine* e, void* dst, const void* src, size_t bytes)
     if (int rc = set_device(e)) return rc;
     if (bytes == 0) return CSAIDX_OK;
     CSAIDX_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, e->stream), "cudaMemcpyAsync");
+    return CSAIDX_OK;
+}
+
+int csaidx_cuda_host_alloc(csaidx_engine* e, size_t bytes, void** ptr) {
+    if (int rc = set_device(e)) return rc;
+    if (ptr == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "host_alloc: null out pointer");
+    *ptr = nullptr;
+    if (bytes == 0) return CSAIDX_OK;
+    CSAIDX_CUDA_TRY(cudaHostAlloc(ptr, bytes, cudaHostAllocDefault), "cudaHostAlloc");
+    return CSAIDX_OK;
+}
+
+int csaidx_cuda_host_free(csaidx_engine* e, void* ptr) {
+    if (int rc = set_device(e)) return rc;
+    if (ptr != nullptr) CSAIDX_CUDA_TRY(cudaFreeHost(ptr), "cudaFreeHost");
     return CSAIDX_OK;
 }
 

@@ -2,12 +2,14 @@
 // driver API on raw host buffers (no IndexerInputs copy) and on device
 // operands. Exceptions become status codes + a thread-local message.
 #include <cstring>
+#include <fstream>
 #include <stdexcept>
 #include <string>
 
 #include "csaidx/causal.hpp"
 #include "csaidx/driver.hpp"
 #include "csaidx/gpu.hpp"
+#include "csaidx/tensor_io.hpp"
 #include "csaidx_host.h"
 #include "device.hpp"
 
@@ -224,6 +226,65 @@ int csaidx_device_run_chunked_local(const void* q, const void* kc, int dtype, co
         csaidx::gpu::run_chunked_device(csaidx::gpu::DeviceOperands{q, kc, w, dtype, true}, d, c,
                                         starts.empty() ? nullptr : &starts, out_idx, out_val, out_rows, ledger, &rs);
         fill_stats(stats, rs, ledger, 1);
+    });
+}
+
+int csaidx_host_write_inputs_file(const char* path, const float* q, const float* kc, const float* w,
+                                  const csaidx_dims* dims, uint64_t* bytes) {
+    return guarded([&] {
+        const csaidx::ProblemDims d = from_c(dims);
+        csaidx::IndexerInputs in;
+        in.q.assign(q, q + d.q_elems());
+        in.kc.assign(kc, kc + d.kc_elems());
+        in.w.assign(w, w + d.w_elems());
+        const uint64_t n = csaidx::write_inputs_file(path, in, d);
+        if (bytes != nullptr) *bytes = n;
+    });
+}
+
+int csaidx_host_scan_sections(const char* path, csaidx_section_info* out, int max_sections, int* n_sections) {
+    return guarded([&] {
+        const auto secs = csaidx::detail::scan_sections_file(path);
+        for (size_t i = 0; i < secs.size() && static_cast<int>(i) < max_sections; ++i) {
+            out[i].tag = secs[i].tag;
+            out[i].rank = secs[i].rank;
+            for (int j = 0; j < 4; ++j) out[i].dims[j] = secs[i].dims[j];
+            out[i].elems = secs[i].elems;
+            out[i].offset = secs[i].offset;
+        }
+        *n_sections = static_cast<int>(secs.size());
+    });
+}
+
+int csaidx_host_read_inputs(const char* path, const csaidx_dims* dims, float* q, float* kc, float* w) {
+    return guarded([&] {
+        const csaidx::ProblemDims d = from_c(dims);
+        std::ifstream is(path, std::ios::binary);
+        if (!is) throw std::runtime_error(std::string("read_sections: cannot open ") + path);
+        const auto secs = csaidx::read_sections(is);
+        const int64_t want[3] = {d.q_elems(), d.kc_elems(), d.w_elems()};
+        float* dst[3] = {q, kc, w};
+        if (secs.size() != 3) throw std::invalid_argument("read_inputs: expected 3 sections (q, kc, w)");
+        for (int i = 0; i < 3; ++i) {
+            if (secs[i].tag != i || static_cast<int64_t>(secs[i].data.size()) != want[i])
+                throw std::invalid_argument("read_inputs: section " + std::to_string(i) + " does not match dims");
+            std::memcpy(dst[i], secs[i].data.data(), secs[i].data.size() * sizeof(float));
+        }
+    });
+}
+
+int csaidx_host_load_inputs_device(const char* path, const csaidx_dims* dims, int64_t query_tile,
+                                   const int64_t* chunk_starts, int64_t n_chunks, int dtype, int strict,
+                                   int device, void* q, void* kc, float* w) {
+    return guarded([&] {
+        csaidx::gpu::Options o = csaidx::gpu::options();
+        o.device = device;
+        csaidx::gpu::set_options(o);
+        std::vector<int64_t> starts;
+        if (chunk_starts != nullptr && n_chunks > 0) starts.assign(chunk_starts, chunk_starts + n_chunks);
+        const csaidx::ProblemDims d = from_c(dims);
+        csaidx::gpu::load_inputs_device(path, d, csaidx::TileConfig{query_tile, d.key_blocks},
+                                        starts.empty() ? nullptr : &starts, dtype, strict != 0, q, kc, w);
     });
 }
 

@@ -176,6 +176,38 @@ def test_rank_local_operands_match_full_tensors(orc, B):
             api.run_chunked_device(qd, kd, wd, dims, cfg, starts, local_rows=True)
 
 
+def test_csat_dump_loads_into_hbm_rank_local(orc, tmp_path):
+    """CSAT dump -> device (csaidx_host_load_inputs_device): a chunk subset's
+    q / w rows stacked rank-locally + the full kc, rounded to bf16 on device
+    for the tcgen05 shape (fp32 for the exact kernel); the run over them
+    equals the host-API run on the same file's arrays."""
+    import torch
+
+    for (H, D, S, k, cs) in [(64, 128, 2048, 64, 256), (3, 5, 96, 7, 16)]:
+        B = 2
+        q, kc, w = orc.generate_inputs(B, S, 4, H, D, 21, bf16=(H == 64))
+        dims = api.ProblemDims.create(B, S, 4, H, D, k)
+        cfg = api.DriverConfig(tile=api.TileConfig(cs, 10 ** 6))
+        path = tmp_path / f"in_{H}.csat"
+        api.write_inputs_file(path, api.IndexerInputs(q, kc, w), dims)
+        starts = [S - cs, 0, cs]
+        ql, kd, wl = api.load_inputs_device(path, dims, cfg, starts)
+        assert ql.dtype == (torch.bfloat16 if H == 64 else torch.float32)
+        assert torch.equal(kd.float().cpu(), torch.from_numpy(kc))
+        exp_q = np.concatenate([np.concatenate([q[b, s0:s0 + cs] for s0 in starts])[None] for b in range(B)])
+        assert np.array_equal(ql.float().cpu().numpy(), exp_q)
+        li, lv, _ = api.run_chunked_device(ql, kd, wl, dims, cfg, starts, local_rows=True)
+        full, _ = api.run_chunked(api.IndexerInputs.validated(q, kc, w, dims), dims, cfg)
+        exp = np.concatenate([full.indices[:, s0:s0 + cs] for s0 in starts], axis=1)
+        assert np.array_equal(li.cpu().numpy(), exp)
+    # strict bf16: a value that bf16 cannot hold is rejected, as on the host path
+    q[0, 5, 0, 0] = np.float32(1.0 + 2 ** -12)
+    api.write_inputs_file(tmp_path / "bad.csat", api.IndexerInputs(q, kc, w), dims)
+    dims64 = api.ProblemDims.create(2, 96, 4, 3, 5, 7)
+    with pytest.raises(InvalidArgument):
+        api.load_inputs_device(tmp_path / "bad.csat", dims64, cfg, strict=True, dtype=0)
+
+
 def test_ablations_follow_reference_semantics(orc):
     # acceptance.cpp:339-380 directions at a small V4-like shape
     inputs, dims, (q, kc, w) = inputs_for(orc, 1, 2048, 4, 8, 64, 64, 1)
