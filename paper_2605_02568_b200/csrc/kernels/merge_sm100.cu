@@ -3,10 +3,11 @@
 //
 // merge_kernel: one CTA per query row. The running row (k entries, sorted
 // under succ) and the candidate row (width entries, sorted) are packed to the
-// 64-bit composite key (ord_key(score) << 32 | ~(index + 1)); the candidate
-// row is laid down reversed behind the running row, which makes one bitonic
-// sequence, and a single bitonic merge network (log2(2P) stages) sorts it.
-// The first k entries are the top-k of the union, ordered. The "+1" in the
+// 64-bit composite key (ord_key(score) << 32 | ~(index + 1)) and merged by a
+// merge path: each thread binary-searches the split of its k/256 outputs and
+// merges them sequentially (O(k) work, two barriers, instead of a bitonic
+// network's log2(2k) stages). The first k entries are the top-k of the
+// union, ordered. The "+1" in the
 // composite makes the (-inf, -1) sentinel outrank a masked (-inf, j)
 // placeholder exactly as succ() does (test_topk.cpp:48).
 //
@@ -73,31 +74,57 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams 
         }
     }
 
-    int P = 1;
-    while (P < p.k) P <<= 1;
-    for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        a[i] = i < p.k ? pack(rv[i], ri[i]) : 0ull;
-        a[2 * P - 1 - i] = i < p.width ? pack(cv[i], ci[i]) : 0ull;
+    // Merge path: both lists (sorted best first) are staged as composites;
+    // thread t produces outputs [t*E, (t+1)*E) of the merged order after
+    // locating its start by a binary search over the split (co-rank), then
+    // merges E entries sequentially. Ties (identical sentinel composites)
+    // go to the running row first; either way the output bytes are the same.
+    const int nr = p.k, nc = p.width;
+    uint64_t* run = a;
+    uint64_t* cand = a + nr;
+    if ((nr & 3) == 0 && (nc & 3) == 0 && (p.cand_ld & 3) == 0) {  // 16-byte loads, 4 entries each
+        for (int i = 4 * threadIdx.x; i < nr + nc; i += 4 * blockDim.x) {
+            const bool r = i < nr;
+            const float4 v = *reinterpret_cast<const float4*>(r ? rv + i : cv + (i - nr));
+            const int4 x = *reinterpret_cast<const int4*>(r ? ri + i : ci + (i - nr));
+            a[i] = pack(v.x, x.x);
+            a[i + 1] = pack(v.y, x.y);
+            a[i + 2] = pack(v.z, x.z);
+            a[i + 3] = pack(v.w, x.w);
+        }
+    } else {
+        for (int i = threadIdx.x; i < nr; i += blockDim.x) run[i] = pack(rv[i], ri[i]);
+        for (int i = threadIdx.x; i < nc; i += blockDim.x) cand[i] = pack(cv[i], ci[i]);
     }
     __syncthreads();
-    for (int stride = P; stride > 0; stride >>= 1) {
-        for (int i = threadIdx.x; i < P; i += blockDim.x) {
-            const int lo = 2 * i - (i & (stride - 1));
-            const int hi = lo + stride;
-            const uint64_t x = a[lo], y = a[hi];
-            if (x < y) {
-                a[lo] = y;
-                a[hi] = x;
+    // (rv / ri were consumed into shared memory above: outputs go straight
+    // to global)
+    const int E = (nr + kMergeThreads - 1) / kMergeThreads;
+    const int d0 = threadIdx.x * E;
+    if (d0 < nr) {
+        int lo = d0 - nc > 0 ? d0 - nc : 0, hi = d0 < nr ? d0 : nr;
+        int i = lo;
+        while (lo <= hi) {
+            i = (lo + hi) >> 1;
+            const int j = d0 - i;
+            if (i > 0 && j < nc && run[i - 1] < cand[j]) {
+                hi = i - 1;
+            } else if (j > 0 && i < nr && cand[j - 1] <= run[i]) {
+                lo = i + 1;
+            } else {
+                break;
             }
         }
-        __syncthreads();
-    }
-    for (int e = threadIdx.x; e < p.k; e += blockDim.x) {
-        float v;
-        int32_t idx;
-        unpack(a[e], v, idx);
-        rv[e] = v;
-        ri[e] = idx;
+        int j = d0 - i;
+#pragma unroll 1
+        for (int e = 0; e < E && d0 + e < nr; ++e) {
+            const bool take_run = j >= nc || (i < nr && run[i] >= cand[j]);
+            float v;
+            int32_t idx;
+            unpack(take_run ? run[i++] : cand[j++], v, idx);
+            rv[d0 + e] = v;
+            ri[d0 + e] = idx;
+        }
     }
 }
 
@@ -169,9 +196,7 @@ namespace csaidx_kern {
 cudaError_t launch_merge(const MergeParams& p, cudaStream_t stream) {
     if (p.nrows <= 0) return cudaSuccess;
     if (p.k > kMaxK) return cudaErrorInvalidValue;
-    int P = 1;
-    while (P < p.k) P <<= 1;
-    const size_t smem = 2 * static_cast<size_t>(P) * sizeof(uint64_t);
+    const size_t smem = (static_cast<size_t>(p.k) + static_cast<size_t>(p.width)) * sizeof(uint64_t);
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
