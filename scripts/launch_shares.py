@@ -11,15 +11,17 @@ from collections import defaultdict
 rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
 hdr = rows[0]
 ki, vi, ii = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("ID")
+STEP = ("score_tc", "score_exact", "select", "merge", "finalize", "fill_sentinel", "bool_mask", "tau_kernel")
 launches = [(int(r[ii]), r[ki].split("(")[0].replace("<unnamed>::", ""), float(r[vi].replace(",", "")))
             for r in rows[1:] if r[hdr.index("Metric Name")] == "gpu__time_duration.sum"]
-half = launches[len(launches) // 2:]  # second half = the timed step of --steps 1 --warmup 1
+# the indexer step's kernels only (input generation / setup launches are not part of a step)
+launches = [x for x in launches if any(t in x[1] for t in STEP)]
 tot = defaultdict(float)
 cnt = defaultdict(int)
-for _, n, t in half:
+for _, n, t in launches:
     tot[n] += t
     cnt[n] += 1
 s = sum(tot.values())
-print(f"{len(launches)} launches; last {len(half)} (one step): {s/1e6:.2f} ms under ncu")
+print(f"{len(launches)} step launches (all steps of the run): {s/1e6:.2f} ms under ncu")
 for n in sorted(tot, key=lambda n: -tot[n]):
     print(f"  {n:40s} n={cnt[n]:4d}  {tot[n]/1e6:8.2f} ms  {100*tot[n]/s:5.1f}%")
