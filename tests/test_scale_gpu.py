@@ -135,3 +135,41 @@ def test_c2_chunked_equals_gpu_materialize_bitwise():
     assert np.array_equal(idx.cpu().numpy(), ref.indices)
     assert np.array_equal(val.cpu().numpy().view(np.uint32), ref.values.view(np.uint32))
     row_properties(ref.indices[0], ref.values[0], 0, m, k)
+
+
+def test_c4_rank_shard_properties_and_sampled_oracle_rows():
+    """C4 (S=1,048,576, T=262,144, k=1024) as rank 0 of an 8-GPU run: the
+    rank's LPT chunks with rank-local q / w (generated per chunk from the
+    same counter-based streams as a full draw). Every row: the structural
+    properties; sampled rows incl. the longest (t = S-1, 262,144 legal keys):
+    the north-star rule against the oracle on the consumed bf16 operands."""
+    from paper_2605_02568_b200.shard import plan_shards
+
+    B, S, H, D, m, k, cs = 1, 1048576, 64, 128, 4, 1024, 1024
+    T = S // m
+    shards, _ = plan_shards(S, m, cs, 8)
+    mine = shards[0]
+    e = Engine(0)
+    q = torch.cat([e.gen_normal_bf16(cs * H * D, D ** -0.5, 3, 1, s0 * H * D) for s0 in mine])
+    w = torch.cat([e.gen_normal_f32(cs * H, (D * H) ** -0.5, 3, 3, s0 * H) for s0 in mine])
+    kc = e.gen_normal_bf16(B * T * D, D ** -0.5, 3, 2)
+    dims = api.ProblemDims.create(B, S, m, H, D, k)
+    cfg = api.DriverConfig(tile=api.TileConfig(cs, T))
+    idx, val, st = api.run_chunked_device(q, kc, w, dims, cfg, mine, local_rows=True)
+    hi, hv = idx[0].cpu().numpy(), val[0].cpu().numpy()
+    for c, s0 in enumerate(mine):
+        row_properties(hi[c * cs:(c + 1) * cs], hv[c * cs:(c + 1) * cs], s0, m, k)
+    assert S - cs in mine  # LPT hands rank 0 the heaviest chunk
+    picks = [(mine.index(S - cs), cs - 1), (mine.index(S - cs), 17), (len(mine) // 2, 511), (len(mine) - 1, 0)]
+    rows_t = [mine[c] + r for c, r in picks]
+    local = [c * cs + r for c, r in picks]
+    orc = Oracle()
+    kcf = kc.float().view(-1, D).cpu().numpy()
+    scores = []
+    for t, lr in zip(rows_t, local):
+        L = (t + 1) // m
+        qrow = q[lr * H * D:(lr + 1) * H * D].float().view(H, D).cpu().numpy()
+        wrow = w[lr * H:(lr + 1) * H].cpu().numpy()
+        scores.append(orc.score_tile(qrow[None, None], kcf[None, :L], wrow[None, None], 0, 0, 1, L)[0, 0])
+    rep = check_rows(hi[local], hv[local], scores, [(t + 1) // m for t in rows_t], k)
+    assert rep["rows"] == len(rows_t)
