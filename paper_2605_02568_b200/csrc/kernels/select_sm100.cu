@@ -991,7 +991,7 @@ cudaError_t launch_select_variant(const SelectParams& p, cudaStream_t stream) {
 
 int select_variant() {
     static int v = [] {
-        const char* s = getenv("CSAIDX_SELECT_VARIANT");  // A/B knob (dev): 0 = 8 x float4 / 3 CTAs, 1 = 4 x float4 / 4 CTAs
+        const char* s = getenv("CSAIDX_SELECT_VARIANT");  // A/B knob (dev): 0 = by k, 1 = 4 x float4 / 4 CTAs, 2 = 8 x float4 / 4 CTAs
         return s != nullptr ? atoi(s) : 0;
     }();
     return v;
@@ -1009,6 +1009,10 @@ cudaError_t launch_select(const SelectParams& p, cudaStream_t stream) {
     // persistent warp-specialised form streaming rows through a TMA
     // bulk-copy ring (2 CTAs/SM; 3.7 vs 5.3 TB/s on long rows).
     if (select_variant() == 1) return launch_select_variant<4, 4>(p, stream);
+    // k <= 512 (<= 29 KB of shared memory per row): a 4th CTA per SM at 64
+    // registers pays off (0.080 vs 0.087 ms on 2048 rows of 32K at k = 512);
+    // at k = 1024 the register-starved stream loses (0.109 vs 0.102 ms)
+    if (p.k <= 512 || select_variant() == 2) return launch_select_variant<8, 4>(p, stream);
     return launch_select_variant<8, 3>(p, stream);
 }
 
