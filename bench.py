@@ -408,6 +408,9 @@ def main():
         e2e = {"value": (pairs_mine if args.simulate_rank else pairs_total) / (e2e_ms / 1000.0),
                "unit": "legal pairs/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "pcie_gbs": (h2d + d2h) / (e2e_ms / 1000.0) / 1e9,
+               "bound": "PCIe: the fp32 q rows (the reference API's input type) cross the bus once; H2D of "
+                        "chunk c+1 and D2H of chunk c-1 overlap chunk c's kernels",
                "path": "csaidx_host_run_chunked_local (libcsaidx.so C entry of csaidx::run_chunked over this "
                        "rank's rows), pinned fp32 host operands, H2D/D2H inside the timed region"}
         # cheap end-to-end correctness guard: the host API must agree with the resident run
