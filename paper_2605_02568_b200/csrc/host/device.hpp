@@ -105,6 +105,12 @@ struct ChunkPlan {
     int64_t ct = 0;  // clamped c_T
     std::vector<int64_t> starts;
     std::vector<int64_t> out_row0;
+    // Processing order (indices into starts): latest chunk first. Causal
+    // work grows with s0, so with host transfers the heavy chunks' kernels
+    // run while the light chunks' rows are still crossing PCIe, and the
+    // step ends on cheap chunks instead of a compute tail. Results and
+    // RunStats do not depend on the order.
+    std::vector<size_t> order;
 };
 
 ChunkPlan plan_chunks(const ProblemDims& dims, const TileConfig& tile, const std::vector<int64_t>* starts);
@@ -112,8 +118,8 @@ ChunkPlan plan_chunks(const ProblemDims& dims, const TileConfig& tile, const std
 // Per-chunk callbacks around run_plan's main-lane work (used to overlap host
 // transfers of neighbouring chunks on the engine's copy lanes).
 struct ChunkHooks {
-    std::function<void(size_t)> before;  // before chunk c's first kernel
-    std::function<void(size_t)> after;   // after chunk c's finalize
+    std::function<void(size_t)> before;  // before the o-th processed chunk's first kernel (plan.order[o])
+    std::function<void(size_t)> after;   // after its finalize
 };
 
 // process_query_tile (driver.cpp:36-106) for every chunk of the plan, on

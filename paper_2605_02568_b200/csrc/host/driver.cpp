@@ -50,6 +50,10 @@ ChunkPlan plan_chunks(const ProblemDims& dims, const TileConfig& tile, const std
         plan.out_row0.push_back(row);
         row += std::min(c.cs, dims.seq_len - s0);
     }
+    plan.order.resize(plan.starts.size());
+    for (size_t i = 0; i < plan.order.size(); ++i) plan.order[i] = i;
+    std::stable_sort(plan.order.begin(), plan.order.end(),
+                     [&](size_t a, size_t b) { return plan.starts[a] > plan.starts[b]; });
     return plan;
 }
 
@@ -92,12 +96,13 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
         pf_sample = DeviceBuffer(e, static_cast<size_t>(B * plan.cs * lds) * sizeof(float));
     }
 
-    for (size_t c = 0; c < plan.starts.size(); ++c) {
+    for (size_t o = 0; o < plan.order.size(); ++o) {
+        const size_t c = plan.order[o];
         const int64_t s0 = plan.starts[c];
         const int64_t rows = std::min(plan.cs, dims.seq_len - s0);
         const int64_t op_rows = ops.op_rows > 0 ? ops.op_rows : dims.seq_len;
         const int64_t op_row0 = ops.op_rows > 0 ? plan.out_row0[c] : s0;
-        if (hooks.before) hooks.before(c);
+        if (hooks.before) hooks.before(o);
         LedgerCharge buffer_charge(ledger, "topk_buffer", run_buffer_bytes(B, rows, k));
         // One key tile covering all T keys: its select is a copy into the
         // all-sentinel buffer followed by the sentinel pass, so it writes the
@@ -173,7 +178,7 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
                                        config.ablation == Ablation::none ? 1 : 0, out_idx, out_val, out_rows,
                                        plan.out_row0[c]));
         }
-        if (hooks.after) hooks.after(c);
+        if (hooks.after) hooks.after(o);
     }
     check(csaidx_engine_check(e));
 }
@@ -256,14 +261,15 @@ void run_chunked_rows_view(const HostView& in, const ProblemDims& dims, const Dr
     DeviceBuffer idx(e, n * sizeof(int64_t)), val(e, n * sizeof(float));
     const DeviceOps ops{q.as<void>(), kc.as<void>(), w.as<float>(), dtype, out_rows};
     constexpr int kMainLane = 0, kInLane = 1, kOutLane = 2;
-    auto upload_chunk = [&](size_t c) {
+    auto upload_chunk = [&](size_t o) {  // o-th chunk in processing order
+        const size_t c = plan.order[o];
         const int64_t s0 = plan.starts[c], rows = std::min(plan.cs, dims.seq_len - s0);
         for (int64_t b = 0; b < B; ++b) {
             const int64_t lrow = b * out_rows + plan.out_row0[c];  // operand row on device
             const int64_t hrow = in.local_rows ? lrow : b * dims.seq_len + s0;  // ... and on the host
             const int64_t qoff = hrow * qrow, woff = hrow * dims.heads;
             if (dtype == CSAIDX_DTYPE_BF16) {
-                DeviceBuffer& sb = slab[c % 2];
+                DeviceBuffer& sb = slab[o % 2];
                 check(csaidx_cuda_copy(e, sb.as<void>(), in.q + qoff, static_cast<size_t>(rows * qrow) * sizeof(float)));
                 check(csaidx_cuda_to_bf16(e, sb.as<float>(), q.as<uint16_t>() + lrow * qrow, rows * qrow, strict ? 1 : 0));
             } else {
@@ -273,12 +279,12 @@ void run_chunked_rows_view(const HostView& in, const ProblemDims& dims, const Dr
             check(csaidx_cuda_copy(e, w.as<float>() + lrow * dims.heads, in.w + woff,
                                    static_cast<size_t>(rows * dims.heads) * sizeof(float)));
         }
-        check(csaidx_engine_signal(e, static_cast<int>(c % 32)));
+        check(csaidx_engine_signal(e, static_cast<int>(o % 32)));
     };
     ChunkHooks hooks;
-    hooks.before = [&](size_t c) {
+    hooks.before = [&](size_t o) {
         check(csaidx_engine_use_lane(e, kInLane));
-        if (c == 0) {
+        if (o == 0) {
             if (dtype == CSAIDX_DTYPE_BF16) {
                 DeviceBuffer tmp(e, static_cast<size_t>(dims.kc_elems()) * sizeof(float));
                 tmp.upload(in.kc, static_cast<size_t>(dims.kc_elems()) * sizeof(float));
@@ -288,14 +294,15 @@ void run_chunked_rows_view(const HostView& in, const ProblemDims& dims, const Dr
             }
             upload_chunk(0);
         }
-        if (c + 1 < plan.starts.size()) upload_chunk(c + 1);
+        if (o + 1 < plan.order.size()) upload_chunk(o + 1);
         check(csaidx_engine_use_lane(e, kMainLane));
-        check(csaidx_engine_await(e, static_cast<int>(c % 32)));
+        check(csaidx_engine_await(e, static_cast<int>(o % 32)));
     };
-    hooks.after = [&](size_t c) {
-        check(csaidx_engine_signal(e, static_cast<int>(32 + c % 32)));
+    hooks.after = [&](size_t o) {
+        const size_t c = plan.order[o];
+        check(csaidx_engine_signal(e, static_cast<int>(32 + o % 32)));
         check(csaidx_engine_use_lane(e, kOutLane));
-        check(csaidx_engine_await(e, static_cast<int>(32 + c % 32)));
+        check(csaidx_engine_await(e, static_cast<int>(32 + o % 32)));
         const int64_t rows = std::min(plan.cs, dims.seq_len - plan.starts[c]);
         for (int64_t b = 0; b < B; ++b) {
             const int64_t off = (b * out_rows + plan.out_row0[c]) * k;
