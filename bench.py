@@ -11,14 +11,18 @@ query chunk -> gather of the [S, k] index output to rank 0 (N>1).
 * value  — legal (causal) query·key pairs per second, whole job, operands
            resident in HBM (bf16 q/kc generated on device), max over ranks.
 * e2e    — the same metric through the reference-facing host API
-           (csaidx_host_run_chunked_rows) from pinned fp32 host buffers, H2D
-           of q/kc/w and D2H of indices+values inside the timed region.
+           (csaidx_host_run_chunked_local: the rank's rows of q / w) from
+           pinned fp32 host buffers, H2D of q/kc/w and D2H of indices+values
+           inside the timed region.
 * roofline — score kernel (tcgen05): algorithmic FLOPs (16,384 per legal
            pair) / event-timed kernel ms, vs MEASURED_PEAKS.json.
 * cpu_baseline — the reference C++ library (oracle/_ref, compiled from the
            reference sources) on this host's cores, bounded sample.
 
 `--impl reference` times that reference CPU path alone (rank 0).
+`--simulate-rank R/N` measures rank R's exact shard of an N-GPU run on one
+GPU; `--backend gloo` runs the N>1 path with several ranks on one GPU (a
+logic check; collectives staged through host memory).
 """
 from __future__ import annotations
 
