@@ -140,6 +140,9 @@ __device__ __forceinline__ float head_reduce_tmem(uint32_t taddr, const float* _
     return ((a0.x + a0.y) + (a1.x + a1.y)) + ((a2.x + a2.y) + (a3.x + a3.y));
 }
 
+// kFilter: the fused select pre-filter variant (tau / candidate bitmap,
+// CSAIDX_SELECT_PREFILTER=1); the production kernel carries none of it.
+template <bool kFilter>
 __global__ void __launch_bounds__(kNumThreads, 1)
     score_tc_kernel(const __grid_constant__ CUtensorMap qmap,
                     const __grid_constant__ CUtensorMap kmap, const __grid_constant__ ScoreTcParams p) {
@@ -366,7 +369,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                     l = l < 0 ? 0 : (l > p.cols ? p.cols : l);
                 }
                 lim[g] = static_cast<int>(l);
-                tq[g] = (p.tau != nullptr && qi < it.nrows) ? p.tau[grow] : 0.f;
+                tq[g] = (kFilter && qi < it.nrows) ? p.tau[grow] : 0.f;
             }
             mbar_wait(&w_full[wb], (qiter / kWBufs) & 1);
             ++qiter;
@@ -390,7 +393,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                             if (legal && !isfinite(acc)) atomicOr(p.nonfinite, 1);
                             orow[g][jo] = legal ? acc : neg_inf;
                         }
-                        if (p.tau != nullptr) {
+                        if (kFilter) {
                             // fused select pre-filter: one candidate word per
                             // warp (32 consecutive key columns)
                             const uint32_t m = __ballot_sync(0xffffffffu, legal && acc >= tq[g]);
@@ -526,14 +529,18 @@ cudaError_t launch_score_tc(const CUtensorMap& qmap, const CUtensorMap& kmap, Sc
     if (p.nitems <= 0) return cudaSuccess;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(score_tc_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(kSmemBytes));
-        if (e != cudaSuccess) return e;
+        for (auto* fn : {score_tc_kernel<false>, score_tc_kernel<true>}) {
+            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(kSmemBytes));
+            if (e != cudaSuccess) return e;
+        }
         attr_set = true;
     }
     const int grid = p.nitems < num_sms ? p.nitems : num_sms;
-    score_tc_kernel<<<grid, kNumThreads, kSmemBytes, stream>>>(qmap, kmap, p);
+    if (p.tau != nullptr)
+        score_tc_kernel<true><<<grid, kNumThreads, kSmemBytes, stream>>>(qmap, kmap, p);
+    else
+        score_tc_kernel<false><<<grid, kNumThreads, kSmemBytes, stream>>>(qmap, kmap, p);
     return cudaGetLastError();
 }
 
