@@ -140,9 +140,12 @@ __device__ __forceinline__ float head_reduce_tmem(uint32_t taddr, const float* _
     return ((a0.x + a0.y) + (a1.x + a1.y)) + ((a2.x + a2.y) + (a3.x + a3.y));
 }
 
-// kFilter: the fused select pre-filter variant (tau / candidate bitmap,
-// CSAIDX_SELECT_PREFILTER=1); the production kernel carries none of it.
-template <bool kFilter>
+// Instances: kMode 0 = plain masked score tile (production), 1 = strided
+// key-tile sample (kt_stride > 1), 2 = plain + candidate bitmap against tau
+// (the fused select pre-filter, CSAIDX_SELECT_PREFILTER=1); kProbe adds the
+// per-role wait-cycle counters (dev). The production instance carries none
+// of the optional code.
+template <int kMode, bool kProbe>
 __global__ void __launch_bounds__(kNumThreads, 1)
     score_tc_kernel(const __grid_constant__ CUtensorMap qmap,
                     const __grid_constant__ CUtensorMap kmap, const __grid_constant__ ScoreTcParams p) {
@@ -167,7 +170,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     Item* items = reinterpret_cast<Item*>(bars + 14 + 2 * kItemSlots + kWBufs);  // [kItemSlots]
 
     const int warp = threadIdx.x / 32;
-    long long* const probe = p.probe;  // optional per-CTA wait-cycle counters (profiling)
+    constexpr bool kFilter = kMode == 2;
+    long long* const probe = kProbe ? p.probe : nullptr;  // per-CTA wait-cycle counters (profiling)
+    const int64_t kts = kMode == 1 ? p.kt_stride : 1;  // key-tile stride (sample mode)
 
     if (warp == 0 && elect_one()) {
         tma_prefetch(&qmap);
@@ -254,7 +259,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                     mbar_wait(&k_empty[s], ((kiter / kStages) & 1) ^ 1);
                     if (probe) pw_k += clock64() - c0;
                     mbar_expect_tx(&k_full[s], kKStageBytes);
-                    const int32_t krow = static_cast<int32_t>(krow0 + static_cast<int64_t>(kt) * p.kt_stride * kBlockKeys);
+                    const int32_t krow = static_cast<int32_t>(krow0 + static_cast<int64_t>(kt) * kts * kBlockKeys);
                     for (int hf = 0; hf < 2; ++hf) {
                         tma_load_2d_hint(k_smem + s * kKStageBytes + hf * kKHalfBytes, &kmap, &k_full[s], hf * 64,
                                          krow, keep);
@@ -374,10 +379,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             mbar_wait(&w_full[wb], (qiter / kWBufs) & 1);
             ++qiter;
             const int cols = static_cast<int>(p.cols);
-            const int out_cols = p.kt_stride == 1 ? cols : static_cast<int>(p.ld);
+            const int out_cols = kts == 1 ? cols : static_cast<int>(p.ld);
             for (int kt = it.kt_begin; kt < it.kt_end; ++kt) {
                 const int jo = kt * kBlockKeys + quarter * 32 + static_cast<int>(lane);  // output column
-                const int j = jo + kt * (p.kt_stride - 1) * kBlockKeys;                 // key column
+                const int j = jo + kt * (kts - 1) * kBlockKeys;                 // key column
 #pragma unroll
                 for (int g = 0; g < kGroups; ++g) {
                     const uint32_t a = aiter & 1;
@@ -529,7 +534,8 @@ cudaError_t launch_score_tc(const CUtensorMap& qmap, const CUtensorMap& kmap, Sc
     if (p.nitems <= 0) return cudaSuccess;
     static bool attr_set = false;
     if (!attr_set) {
-        for (auto* fn : {score_tc_kernel<false>, score_tc_kernel<true>}) {
+        for (auto* fn : {score_tc_kernel<0, false>, score_tc_kernel<0, true>, score_tc_kernel<1, false>,
+                         score_tc_kernel<2, false>}) {
             cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  static_cast<int>(kSmemBytes));
             if (e != cudaSuccess) return e;
@@ -538,9 +544,13 @@ cudaError_t launch_score_tc(const CUtensorMap& qmap, const CUtensorMap& kmap, Sc
     }
     const int grid = p.nitems < num_sms ? p.nitems : num_sms;
     if (p.tau != nullptr)
-        score_tc_kernel<true><<<grid, kNumThreads, kSmemBytes, stream>>>(qmap, kmap, p);
+        score_tc_kernel<2, false><<<grid, kNumThreads, kSmemBytes, stream>>>(qmap, kmap, p);
+    else if (p.kt_stride > 1)
+        score_tc_kernel<1, false><<<grid, kNumThreads, kSmemBytes, stream>>>(qmap, kmap, p);
+    else if (p.probe != nullptr)
+        score_tc_kernel<0, true><<<grid, kNumThreads, kSmemBytes, stream>>>(qmap, kmap, p);
     else
-        score_tc_kernel<false><<<grid, kNumThreads, kSmemBytes, stream>>>(qmap, kmap, p);
+        score_tc_kernel<0, false><<<grid, kNumThreads, kSmemBytes, stream>>>(qmap, kmap, p);
     return cudaGetLastError();
 }
 
