@@ -483,7 +483,8 @@ int launch_tc(csaidx_engine* e, const void* q, const void* kc, const float* w, c
         op_row0 = s0;
     }
     CUtensorMap qmap, kmap;
-    if (int rc = make_map(&qmap, q, static_cast<uint64_t>(d->batch * op_rows * d->heads), d->head_dim, 256))
+    if (int rc = make_map(&qmap, q, static_cast<uint64_t>(d->batch * op_rows * d->heads), d->head_dim,
+                          static_cast<uint32_t>(csaidx_kern::score_tc_q_box_rows())))
         return rc;
     if (int rc = make_map(&kmap, kc, static_cast<uint64_t>(d->batch * d->key_blocks), d->head_dim, 128)) return rc;
     ScoreTcParams p{};

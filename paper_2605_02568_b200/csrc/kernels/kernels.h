@@ -157,6 +157,7 @@ namespace csaidx_kern {
 
 bool score_tc_supported(int64_t heads, int64_t head_dim);
 size_t score_tc_smem_bytes();
+int score_tc_q_box_rows();  // rows of the q TMA box (one query group x 64 heads)
 cudaError_t launch_score_tc(const CUtensorMap& qmap, const CUtensorMap& kmap, ScoreTcParams p,
                             int num_sms, cudaStream_t stream);
 cudaError_t launch_score_exact(const ScoreExactParams& p, cudaStream_t stream);

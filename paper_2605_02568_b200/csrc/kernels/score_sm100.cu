@@ -38,18 +38,23 @@ namespace {
 constexpr int kHeads = 64;
 constexpr int kDim = 128;
 constexpr int kBlockKeys = 128;                 // UMMA M (TMEM lanes)
-constexpr int kQPerGroup = 4;                   // queries per UMMA N
-constexpr int kUmmaN = kQPerGroup * kHeads;     // 256
-constexpr int kGroups = 2;                      // query groups per work item
-constexpr int kQPerItem = kQPerGroup * kGroups; // 8
+#ifndef CSAIDX_QGROUP
+#define CSAIDX_QGROUP 4
+#endif
+constexpr int kQPerGroup = CSAIDX_QGROUP;       // queries per UMMA N (4: N = 256, 2: N = 128)
+constexpr int kUmmaN = kQPerGroup * kHeads;
+constexpr int kQPerItem = 8;
+constexpr int kGroups = kQPerItem / kQPerGroup; // query groups per work item
+constexpr int kAcc = 512 / kUmmaN;              // TMEM accumulator buffers (512 columns)
+static_assert(kQPerGroup == 4 || kQPerGroup == 2, "query group of 4 or 2");
 constexpr int kStages = 2;
 constexpr int kMinTilesPerPiece = 32;           // >= 4096 keys per work item
 constexpr int kKSteps = kDim / 16;              // UMMA_K = 16 for bf16
 constexpr int kItemSlots = 4;
 
 constexpr uint32_t kHalfRowBytes = 128;                          // 64 bf16
-constexpr uint32_t kQHalfBytes = kUmmaN * kHalfRowBytes;         // 32 KiB
-constexpr uint32_t kQGroupBytes = 2 * kQHalfBytes;               // 64 KiB
+constexpr uint32_t kQHalfBytes = kUmmaN * kHalfRowBytes;         // 32 / 16 KiB
+constexpr uint32_t kQGroupBytes = 2 * kQHalfBytes;               // 64 / 32 KiB
 constexpr uint32_t kKHalfBytes = kBlockKeys * kHalfRowBytes;     // 16 KiB
 constexpr uint32_t kKStageBytes = 2 * kKHalfBytes;               // 32 KiB
 constexpr uint32_t kQBytes = kGroups * kQGroupBytes;             // 128 KiB
@@ -61,7 +66,10 @@ constexpr uint32_t kBarOffset = kWOffset + kWBufs * kWBufBytes;  // + 6 KiB
 constexpr uint32_t kSmemBytes = kBarOffset + 512 + 1024;         // barriers, items, align slack
 
 constexpr int kNumThreads = 640;  // 4 control warps + 16 epilogue warps
-constexpr int kEpiWarps = 16;     // 4 per TMEM lane quarter, one query of each group each
+constexpr int kEpiWarps = 16;     // 4 per TMEM lane quarter, 2 queries of the item each
+// Epilogue warps draining each accumulator: every warp (groups of 4) or the
+// 4 warps, one per lane quarter, that own the group (groups of 2).
+constexpr int kAccDrainers = kQPerGroup == 4 ? kEpiWarps : 4;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kIdesc = idesc_bf16_f32(kBlockKeys, kUmmaN);
 
@@ -157,17 +165,17 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     uint8_t* k_smem = smem + kQBytes;
     float* w_smem = reinterpret_cast<float*>(smem + kWOffset);  // [kWBufs][8][64]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOffset);
-    uint64_t* k_full = bars + 0;      // [kStages]
-    uint64_t* k_empty = bars + 2;     // [kStages]
-    uint64_t* q_full = bars + 4;      // [kGroups] one per query-group buffer
-    uint64_t* q_empty = bars + 6;     // [kGroups]
-    uint64_t* acc_full = bars + 8;    // [2]
-    uint64_t* acc_empty = bars + 10;  // [2]
-    uint64_t* item_full = bars + 12;                // [kItemSlots]
-    uint64_t* item_empty = bars + 12 + kItemSlots;  // [kItemSlots]
-    uint64_t* w_full = bars + 12 + 2 * kItemSlots;  // [kWBufs]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12 + 2 * kItemSlots + kWBufs);
-    Item* items = reinterpret_cast<Item*>(bars + 14 + 2 * kItemSlots + kWBufs);  // [kItemSlots]
+    uint64_t* k_full = bars;                          // [kStages]
+    uint64_t* k_empty = k_full + kStages;             // [kStages]
+    uint64_t* q_full = k_empty + kStages;             // [kGroups] one per query-group buffer
+    uint64_t* q_empty = q_full + kGroups;             // [kGroups]
+    uint64_t* acc_full = q_empty + kGroups;           // [kAcc]
+    uint64_t* acc_empty = acc_full + kAcc;            // [kAcc]
+    uint64_t* item_full = acc_empty + kAcc;           // [kItemSlots]
+    uint64_t* item_empty = item_full + kItemSlots;    // [kItemSlots]
+    uint64_t* w_full = item_empty + kItemSlots;       // [kWBufs]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_full + kWBufs);
+    Item* items = reinterpret_cast<Item*>(w_full + kWBufs + 2);  // [kItemSlots]
 
     const int warp = threadIdx.x / 32;
     constexpr bool kFilter = kMode == 2;
@@ -185,9 +193,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             mbar_init(&q_full[g], 1);
             mbar_init(&q_empty[g], 1);
         }
-        for (int a = 0; a < 2; ++a) {
+        for (int a = 0; a < kAcc; ++a) {
             mbar_init(&acc_full[a], 1);
-            mbar_init(&acc_empty[a], kEpiWarps);
+            mbar_init(&acc_empty[a], kAccDrainers);
         }
         for (int s = 0; s < kItemSlots; ++s) {
             mbar_init(&item_full[s], 1);
@@ -265,7 +273,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                                          krow, keep);
                     }
                     ++kiter;
-                    if (kt == it.kt_begin) load_group(1);
+                    if (kt == it.kt_begin)
+                        for (int g = 1; g < kGroups; ++g) load_group(g);
                 }
                 ++qiter;
             }
@@ -307,9 +316,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                             if (probe) mw_q += clock64() - c0;
                             tc_fence_after();
                         }
-                        const uint32_t a = aiter & 1;
+                        const uint32_t a = aiter % kAcc;
                         if (probe) c0 = clock64();
-                        mbar_wait(&acc_empty[a], ((aiter >> 1) & 1) ^ 1);
+                        mbar_wait(&acc_empty[a], ((aiter / kAcc) & 1) ^ 1);
                         if (probe) mw_acc += clock64() - c0;
                         tc_fence_after();
                         const uint32_t d_tmem = tmem_base + a * kUmmaN;
@@ -337,7 +346,11 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         const int quarter = warp & 3;
         const int qsel = (warp - 4) >> 2;
         const uint32_t lane = lane_id();
-        const uint32_t row_taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + qsel * kHeads;
+        const uint32_t quarter_taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
+        // The warp's two queries of every item: query qsel of each 4-query
+        // group (groups of 4), or both queries of group qsel (groups of 2).
+        int wq[2];
+        for (int u = 0; u < 2; ++u) wq[u] = kQPerGroup == 4 ? u * kQPerGroup + qsel : qsel * kQPerGroup + u;
         uint32_t aiter = 0, qiter = 0;
         long long ew_acc = 0;
         const long long e_start = probe ? clock64() : 0;
@@ -357,24 +370,24 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             }
             const uint32_t wb = qiter % kWBufs;
             const float* w_item = w_smem + wb * (kQPerItem * kHeads);
-            // Per-item constants of this warp's 2 queries (one per group):
-            // output row and the causal limit (first illegal column, t0-relative).
-            float* orow[kGroups];
-            int lim[kGroups];
-            float tq[kGroups];  // candidate thresholds (filter mode)
+            // Per-item constants of this warp's 2 queries: output row and the
+            // causal limit (first illegal column, t0-relative).
+            float* orow[2];
+            int lim[2];
+            float tq[2];  // candidate thresholds (filter mode)
 #pragma unroll
-            for (int g = 0; g < kGroups; ++g) {
-                const int qi = g * kQPerGroup + qsel;
+            for (int u = 0; u < 2; ++u) {
+                const int qi = wq[u];
                 const int64_t r = it.r0 + qi;
                 const int64_t grow = static_cast<int64_t>(it.b) * p.rows + r;
-                orow[g] = p.out + grow * p.ld;
+                orow[u] = p.out + grow * p.ld;
                 int64_t l = p.cols;
                 if (p.apply_mask) {
                     l = t_legal_dev(p.s0 + r, p.ratio) - p.t0;
                     l = l < 0 ? 0 : (l > p.cols ? p.cols : l);
                 }
-                lim[g] = static_cast<int>(l);
-                tq[g] = (kFilter && qi < it.nrows) ? p.tau[grow] : 0.f;
+                lim[u] = static_cast<int>(l);
+                tq[u] = (kFilter && qi < it.nrows) ? p.tau[grow] : 0.f;
             }
             mbar_wait(&w_full[wb], (qiter / kWBufs) & 1);
             ++qiter;
@@ -382,29 +395,39 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             const int out_cols = kts == 1 ? cols : static_cast<int>(p.ld);
             for (int kt = it.kt_begin; kt < it.kt_end; ++kt) {
                 const int jo = kt * kBlockKeys + quarter * 32 + static_cast<int>(lane);  // output column
-                const int j = jo + kt * (kts - 1) * kBlockKeys;                 // key column
+                const int j = jo + kt * (kts - 1) * kBlockKeys;                            // key column
+                // groups of 4: one accumulator per query (both buffers per key
+                // tile); groups of 2: the warp's group's buffer holds both
+                constexpr int kUnits = kQPerGroup == 4 ? 2 : 1;
+                constexpr int kPerUnit = 2 / kUnits;
 #pragma unroll
-                for (int g = 0; g < kGroups; ++g) {
-                    const uint32_t a = aiter & 1;
+                for (int un = 0; un < kUnits; ++un) {
+                    const uint32_t a = kQPerGroup == 4 ? aiter % kAcc : static_cast<uint32_t>(qsel);
+                    const uint32_t par = kQPerGroup == 4 ? (aiter / kAcc) & 1 : aiter & 1;
                     const long long c0 = probe ? clock64() : 0;
-                    mbar_wait(&acc_full[a], (aiter >> 1) & 1);
+                    mbar_wait(&acc_full[a], par);
                     if (probe) ew_acc += clock64() - c0;
                     tc_fence_after();
-                    const int qi = g * kQPerGroup + qsel;  // query within item
-                    if (qi < it.nrows) {                   // warp-uniform
-                        const float acc = head_reduce_tmem(row_taddr + a * kUmmaN, w_item + qi * kHeads);
-                        const bool legal = j < lim[g];
-                        if (jo < out_cols) {
-                            if (legal && !isfinite(acc)) atomicOr(p.nonfinite, 1);
-                            orow[g][jo] = legal ? acc : neg_inf;
-                        }
-                        if (kFilter) {
-                            // fused select pre-filter: one candidate word per
-                            // warp (32 consecutive key columns)
-                            const uint32_t m = __ballot_sync(0xffffffffu, legal && acc >= tq[g]);
-                            if (lane == 0) {
-                                const int64_t grow = static_cast<int64_t>(it.b) * p.rows + it.r0 + qi;
-                                p.pass_bits[grow * p.bits_ld + (jo >> 5)] = m;
+#pragma unroll
+                    for (int pu = 0; pu < kPerUnit; ++pu) {
+                        const int u = un * kPerUnit + pu;
+                        const int qi = wq[u];
+                        if (qi < it.nrows) {  // warp-uniform
+                            const uint32_t col = a * kUmmaN + (qi % kQPerGroup) * kHeads;
+                            const float acc = head_reduce_tmem(quarter_taddr + col, w_item + qi * kHeads);
+                            const bool legal = j < lim[u];
+                            if (jo < out_cols) {
+                                if (legal && !isfinite(acc)) atomicOr(p.nonfinite, 1);
+                                orow[u][jo] = legal ? acc : neg_inf;
+                            }
+                            if (kFilter) {
+                                // fused select pre-filter: one candidate word per
+                                // warp (32 consecutive key columns)
+                                const uint32_t m = __ballot_sync(0xffffffffu, legal && acc >= tq[u]);
+                                if (lane == 0) {
+                                    const int64_t grow = static_cast<int64_t>(it.b) * p.rows + it.r0 + qi;
+                                    p.pass_bits[grow * p.bits_ld + (jo >> 5)] = m;
+                                }
                             }
                         }
                     }
@@ -496,6 +519,8 @@ bool score_tc_supported(int64_t heads, int64_t head_dim) {
 }
 
 size_t score_tc_smem_bytes() { return kSmemBytes; }
+
+int score_tc_q_box_rows() { return kUmmaN; }
 
 cudaError_t launch_score_tc(const CUtensorMap& qmap, const CUtensorMap& kmap, ScoreTcParams p,
                             int num_sms, cudaStream_t stream) {
