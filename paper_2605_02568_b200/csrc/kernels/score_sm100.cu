@@ -7,10 +7,13 @@
 //
 //  * score_tc_kernel — the production path for the V4 indexer shape
 //    (H_I = 64, d_h = 128). A warp-specialised, persistent tcgen05 GEMM with
-//    keys as M (128 TMEM lanes) and (query x head) as N (4 queries x 64 heads
-//    = 256 columns). q and kc tiles are staged by TMA with 128-byte swizzle,
-//    w rows by a bulk copy; the fp32 accumulator lives in TMEM (2 x 256
-//    columns, double buffered); the epilogue warps read one key row per
+//    keys as M (128 TMEM lanes) and (query x head) as N (2 queries x 64 heads
+//    = 128 columns; CSAIDX_QGROUP=4 builds the 256-column form). q and kc
+//    tiles are staged by TMA with 128-byte swizzle, w rows by a bulk copy;
+//    the fp32 accumulators live in TMEM (4 x 128 columns); each is drained
+//    by the 4 epilogue warps owning its query pair, which reduce both
+//    queries together (the epilogue is latency bound, so the pair's
+//    independent chains are what buys throughput); the epilogue warps read one key row per
 //    thread with tcgen05.ld and fold ReLU, the w-weighted head reduction and
 //    the causal mask before the only store, so the [B,S,H_I,T] per-head
 //    intermediate never exists. Work items (8 queries x <= tpp key tiles)
@@ -39,7 +42,7 @@ constexpr int kHeads = 64;
 constexpr int kDim = 128;
 constexpr int kBlockKeys = 128;                 // UMMA M (TMEM lanes)
 #ifndef CSAIDX_QGROUP
-#define CSAIDX_QGROUP 4
+#define CSAIDX_QGROUP 2
 #endif
 constexpr int kQPerGroup = CSAIDX_QGROUP;       // queries per UMMA N (4: N = 256, 2: N = 128)
 constexpr int kUmmaN = kQPerGroup * kHeads;
@@ -118,34 +121,58 @@ __device__ __forceinline__ void decode_item(const ScoreTcParams& p, int idx, Ite
 // the 96 registers a 640-thread CTA allows; chain assignment and order do
 // not depend on the slicing. ncu: the epilogue's top stall is the short
 // scoreboard (w from shared memory / TMEM loads), then issue contention.
-__device__ __forceinline__ void relu_fma8(const float (&v)[8], const float* __restrict__ w8, float2& a0, float2& a1,
-                                          float2& a2, float2& a3) {
-    const float4 wl = *reinterpret_cast<const float4*>(w8);
-    const float4 wh = *reinterpret_cast<const float4*>(w8 + 4);
-    a0 = __ffma2_rn(make_float2(fmaxf(v[0], 0.f), fmaxf(v[1], 0.f)), make_float2(wl.x, wl.y), a0);
-    a1 = __ffma2_rn(make_float2(fmaxf(v[2], 0.f), fmaxf(v[3], 0.f)), make_float2(wl.z, wl.w), a1);
-    a2 = __ffma2_rn(make_float2(fmaxf(v[4], 0.f), fmaxf(v[5], 0.f)), make_float2(wh.x, wh.y), a2);
-    a3 = __ffma2_rn(make_float2(fmaxf(v[6], 0.f), fmaxf(v[7], 0.f)), make_float2(wh.z, wh.w), a3);
-}
+// One query's 64 head partials in eight 8-column TMEM slices (the load of
+// slice s+1 in flight while slice s is reduced), two packed FFMA2 chains.
+// head_reduce_tmem2 below computes exactly this per query (same chains,
+// same order), so a score never depends on whether its query was reduced
+// alone or paired — the results stay tiling invariant bit for bit.
+__device__ __forceinline__ void relu_fma8x(const float (&v)[8], const float* __restrict__ w8, float2& a0,
+                                           float2& a1);
 
-// Eight 8-column TMEM slices, the load of slice s+1 in flight while slice s
-// is reduced (two 8-register buffers: the same 16 registers as one
-// 16-column slice; measured equal to unpipelined 16-column slices).
 __device__ __forceinline__ float head_reduce_tmem(uint32_t taddr, const float* __restrict__ wq) {
-    float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+    float2 a0 = make_float2(0.f, 0.f), a1 = a0;
     float va[8], vb[8];
     tmem_ld8(taddr, va);
     tmem_ld_wait();
 #pragma unroll
     for (int s = 0; s < 8; s += 2) {
         tmem_ld8(taddr + (s + 1) * 8, vb);
-        relu_fma8(va, wq + s * 8, a0, a1, a2, a3);
+        relu_fma8x(va, wq + s * 8, a0, a1);
         tmem_ld_wait();
         if (s + 2 < 8) tmem_ld8(taddr + (s + 2) * 8, va);
-        relu_fma8(vb, wq + (s + 1) * 8, a0, a1, a2, a3);
+        relu_fma8x(vb, wq + (s + 1) * 8, a0, a1);
         if (s + 2 < 8) tmem_ld_wait();
     }
-    return ((a0.x + a0.y) + (a1.x + a1.y)) + ((a2.x + a2.y) + (a3.x + a3.y));
+    return (a0.x + a0.y) + (a1.x + a1.y);
+}
+
+// Two queries of the same accumulator (query groups of 2) reduced together:
+// both 8-column slices are loaded before one wait, and the two independent
+// chains interleave, halving the waits per pair and doubling the epilogue's
+// instruction-level parallelism (it is latency bound: ~35% of issue slots).
+__device__ __forceinline__ void relu_fma8x(const float (&v)[8], const float* __restrict__ w8, float2& a0,
+                                           float2& a1) {
+    const float4 wl = *reinterpret_cast<const float4*>(w8);
+    const float4 wh = *reinterpret_cast<const float4*>(w8 + 4);
+    a0 = __ffma2_rn(make_float2(fmaxf(v[0], 0.f), fmaxf(v[1], 0.f)), make_float2(wl.x, wl.y), a0);
+    a1 = __ffma2_rn(make_float2(fmaxf(v[2], 0.f), fmaxf(v[3], 0.f)), make_float2(wl.z, wl.w), a1);
+    a0 = __ffma2_rn(make_float2(fmaxf(v[4], 0.f), fmaxf(v[5], 0.f)), make_float2(wh.x, wh.y), a0);
+    a1 = __ffma2_rn(make_float2(fmaxf(v[6], 0.f), fmaxf(v[7], 0.f)), make_float2(wh.z, wh.w), a1);
+}
+
+__device__ __forceinline__ float2 head_reduce_tmem2(uint32_t taddr0, uint32_t taddr1, const float* __restrict__ w0,
+                                                    const float* __restrict__ w1) {
+    float2 a0 = make_float2(0.f, 0.f), a1 = a0, b0 = a0, b1 = a0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        float va[8], vb[8];
+        tmem_ld8(taddr0 + s * 8, va);
+        tmem_ld8(taddr1 + s * 8, vb);
+        tmem_ld_wait();
+        relu_fma8x(va, w0 + s * 8, a0, a1);
+        relu_fma8x(vb, w1 + s * 8, b0, b1);
+    }
+    return make_float2((a0.x + a0.y) + (a1.x + a1.y), (b0.x + b0.y) + (b1.x + b1.y));
 }
 
 // Instances: kMode 0 = plain masked score tile (production), 1 = strided
@@ -408,13 +435,21 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                     mbar_wait(&acc_full[a], par);
                     if (probe) ew_acc += clock64() - c0;
                     tc_fence_after();
+                    float2 pair_acc = make_float2(0.f, 0.f);
+                    if (kPerUnit == 2 && wq[1] < it.nrows) {  // both queries of the accumulator at once
+                        const uint32_t col = a * kUmmaN;
+                        pair_acc = head_reduce_tmem2(quarter_taddr + col, quarter_taddr + col + kHeads,
+                                                     w_item + wq[0] * kHeads, w_item + wq[1] * kHeads);
+                    }
 #pragma unroll
                     for (int pu = 0; pu < kPerUnit; ++pu) {
                         const int u = un * kPerUnit + pu;
                         const int qi = wq[u];
                         if (qi < it.nrows) {  // warp-uniform
                             const uint32_t col = a * kUmmaN + (qi % kQPerGroup) * kHeads;
-                            const float acc = head_reduce_tmem(quarter_taddr + col, w_item + qi * kHeads);
+                            const float acc = (kPerUnit == 2 && wq[1] < it.nrows)
+                                                  ? (pu == 0 ? pair_acc.x : pair_acc.y)
+                                                  : head_reduce_tmem(quarter_taddr + col, w_item + qi * kHeads);
                             const bool legal = j < lim[u];
                             if (jo < out_cols) {
                                 if (legal && !isfinite(acc)) atomicOr(p.nonfinite, 1);
