@@ -44,6 +44,9 @@ constexpr int kBlockKeys = 128;                 // UMMA M (TMEM lanes)
 #ifndef CSAIDX_QGROUP
 #define CSAIDX_QGROUP 2
 #endif
+#ifndef CSAIDX_EPI_REGS
+#define CSAIDX_EPI_REGS 1  // next TMEM slice pair prefetched (needs the 576-thread register budget)
+#endif
 constexpr int kQPerGroup = CSAIDX_QGROUP;       // queries per UMMA N (4: N = 256, 2: N = 128)
 constexpr int kUmmaN = kQPerGroup * kHeads;
 constexpr int kQPerItem = 8;
@@ -68,7 +71,13 @@ constexpr int kWBufs = 3;                                        // see the prod
 constexpr uint32_t kBarOffset = kWOffset + kWBufs * kWBufBytes;  // + 6 KiB
 constexpr uint32_t kSmemBytes = kBarOffset + 512 + 1024;         // barriers, items, align slack
 
-constexpr int kNumThreads = 640;  // 4 control warps + 16 epilogue warps
+// Warp roles: 0 = scheduler + TMA producer, 1 = TMEM owner + MMA issuer,
+// 2..17 = epilogue. Two control warps (not four) leave 576 threads, so the
+// epilogue gets 112 registers (65536 / 576): room to keep the next TMEM
+// slice pair in flight. TMEM lane access goes by warp % 4, so any 4
+// consecutive epilogue warps cover the 4 lane quarters.
+constexpr int kFirstEpiWarp = 2;
+constexpr int kNumThreads = 576;
 constexpr int kEpiWarps = 16;     // 4 per TMEM lane quarter, 2 queries of the item each
 // Epilogue warps draining each accumulator: every warp (groups of 4) or the
 // 4 warps, one per lane quarter, that own the group (groups of 2).
@@ -163,6 +172,29 @@ __device__ __forceinline__ void relu_fma8x(const float (&v)[8], const float* __r
 __device__ __forceinline__ float2 head_reduce_tmem2(uint32_t taddr0, uint32_t taddr1, const float* __restrict__ w0,
                                                     const float* __restrict__ w1) {
     float2 a0 = make_float2(0.f, 0.f), a1 = a0, b0 = a0, b1 = a0;
+#if CSAIDX_EPI_REGS
+    // the next slice pair's loads are in flight while the current pair is
+    // reduced
+    float va[8], vb[8], vc[8], vd[8];
+    tmem_ld8(taddr0, va);
+    tmem_ld8(taddr1, vb);
+    tmem_ld_wait();
+#pragma unroll
+    for (int s = 0; s < 8; s += 2) {
+        tmem_ld8(taddr0 + (s + 1) * 8, vc);
+        tmem_ld8(taddr1 + (s + 1) * 8, vd);
+        relu_fma8x(va, w0 + s * 8, a0, a1);
+        relu_fma8x(vb, w1 + s * 8, b0, b1);
+        tmem_ld_wait();
+        if (s + 2 < 8) {
+            tmem_ld8(taddr0 + (s + 2) * 8, va);
+            tmem_ld8(taddr1 + (s + 2) * 8, vb);
+        }
+        relu_fma8x(vc, w0 + (s + 1) * 8, a0, a1);
+        relu_fma8x(vd, w1 + (s + 1) * 8, b0, b1);
+        if (s + 2 < 8) tmem_ld_wait();
+    }
+#else
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
         float va[8], vb[8];
@@ -172,6 +204,7 @@ __device__ __forceinline__ float2 head_reduce_tmem2(uint32_t taddr0, uint32_t ta
         relu_fma8x(va, w0 + s * 8, a0, a1);
         relu_fma8x(vb, w1 + s * 8, b0, b1);
     }
+#endif
     return make_float2((a0.x + a0.y) + (a1.x + a1.y), (b0.x + b0.y) + (b1.x + b1.y));
 }
 
@@ -231,7 +264,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         for (int wb = 0; wb < kWBufs; ++wb) mbar_init(&w_full[wb], 1);
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+    if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -365,13 +398,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                 }
             }
         }
-    } else if (warp >= 4) {
+    } else if (warp >= kFirstEpiWarp) {
         // ------------------------------------------------ epilogue
         // 16 warps: warp w reads TMEM lanes 32*(w % 4).. (its key quarter)
-        // and owns query qsel = (w - 4) / 4 of every 4-query group, so each
-        // accumulator is drained by 4 warps per SM sub-partition.
+        // and owns slot qsel = (w - 2) / 4: query qsel of every 4-query group
+        // (QG = 4) or the query pair of group qsel (QG = 2).
         const int quarter = warp & 3;
-        const int qsel = (warp - 4) >> 2;
+        const int qsel = (warp - kFirstEpiWarp) >> 2;
         const uint32_t lane = lane_id();
         const uint32_t quarter_taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16);
         // The warp's two queries of every item: query qsel of each 4-query
@@ -389,7 +422,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&item_empty[slot]);
             if (it.kt_begin < 0) {
-                if (probe && warp == 4 && lane == 0) {
+                if (probe && warp == kFirstEpiWarp && lane == 0) {
                     probe[blockIdx.x * 8 + 4] = ew_acc;
                     probe[blockIdx.x * 8 + 5] = clock64() - e_start;
                 }
@@ -477,7 +510,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 
     tc_fence_before();
     __syncthreads();
-    if (warp == 2) {
+    if (warp == 1) {
         tc_fence_after();
         tmem_dealloc<kTmemCols>(tmem_base);
     }
