@@ -70,9 +70,9 @@ int csaidx_engine_destroy(csaidx_engine* e);
 int csaidx_engine_set_stream(csaidx_engine* e, void* stream);
 int csaidx_engine_use_own_stream(csaidx_engine* e);
 int csaidx_engine_get_stream(csaidx_engine* e, void** stream);
-/* Copy lanes for overlapping host transfers with compute: subsequent calls
- * enqueue on lane 0 (the main stream set above), 1 (copy-in) or 2
- * (copy-out). signal records event `slot` (0..63) on the current lane;
+/* Lanes for overlapping host transfers and kernels: subsequent calls
+ * enqueue on lane 0 (the main stream set above), 1 (copy-in), 2 (copy-out)
+ * or 3 (a second compute stream). signal records event `slot` (0..127) on the current lane;
  * await makes the current lane wait for the slot's latest signal. */
 int csaidx_engine_use_lane(csaidx_engine* e, int lane);
 int csaidx_engine_signal(csaidx_engine* e, int slot);
@@ -81,6 +81,11 @@ int csaidx_engine_await(csaidx_engine* e, int slot);
  * staging buffer whose copy was enqueued before the signal). */
 int csaidx_engine_sync_slot(csaidx_engine* e, int slot);
 int csaidx_engine_num_sms(csaidx_engine* e, int* num_sms);
+/* SM partition for running a select beside the score kernel: score launches
+ * use at most score_sms CTAs (one per SM) and select launches run as
+ * select_sms persistent CTAs of several rows each (one per SM). 0, 0 = the
+ * whole GPU for every launch (the default). Results do not depend on it. */
+int csaidx_engine_set_partition(csaidx_engine* e, int score_sms, int select_sms);
 /* Synchronizes the stream, then reports (and clears) latched data errors. */
 int csaidx_engine_check(csaidx_engine* e);
 /* Device bytes currently held / high-water through csaidx_cuda_alloc. */
@@ -168,6 +173,9 @@ int csaidx_cuda_select(csaidx_engine* e, const float* scores, int64_t batch, int
                        int apply_mask, int64_t k, float* cand_val, int32_t* cand_idx,
                        int64_t cand_ld);
 int csaidx_cuda_select_capacity(void);
+/* 1 when the persistent multi-row select (csaidx_engine_set_partition) fits
+ * shared memory for this k (k <= 1365 with 3 rows per CTA). */
+int csaidx_cuda_select_overlap_capable(int64_t k);
 
 /* Fused select pre-filter (an implementation of the same tile_topk
  * contract; results are identical to csaidx_cuda_select on every input):

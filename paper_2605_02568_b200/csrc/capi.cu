@@ -83,10 +83,13 @@ struct csaidx_engine {
     std::vector<Pending> pending;
     std::vector<cudaEvent_t> event_pool;
     // copy lanes for overlapping host transfers with compute (created lazily)
-    cudaStream_t lanes[3] = {nullptr, nullptr, nullptr};  // [0] = main (== stream when lane 0 active)
+    cudaStream_t lanes[4] = {nullptr, nullptr, nullptr, nullptr};  // [0] = main (== stream when lane 0 active)
     cudaStream_t main_stream = nullptr;
     int lane = 0;
-    cudaEvent_t slots[64] = {};
+    cudaEvent_t slots[128] = {};
+    // SM partition while a select runs beside the score kernel (0 = whole GPU)
+    int score_sms = 0;
+    int select_sms = 0;
     long long* select_probe = nullptr;  // optional per-row phase clocks (profiling)
     long long* score_probe = nullptr;   // optional per-CTA wait counters (profiling)
 };
@@ -218,7 +221,7 @@ int csaidx_engine_destroy(csaidx_engine* e) {
     }
     for (cudaEvent_t ev : e->event_pool) cudaEventDestroy(ev);
     if (e->flags) cudaFree(e->flags);
-    for (int i = 1; i < 3; ++i)
+    for (int i = 1; i < 4; ++i)
         if (e->lanes[i]) cudaStreamDestroy(e->lanes[i]);
     for (cudaEvent_t ev : e->slots)
         if (ev) cudaEventDestroy(ev);
@@ -237,7 +240,8 @@ int csaidx_engine_set_stream(csaidx_engine* e, void* stream) {
 
 int csaidx_engine_use_lane(csaidx_engine* e, int lane) {
     if (int rc = set_device(e)) return rc;
-    if (lane < 0 || lane > 2) return fail(CSAIDX_INVALID_ARGUMENT, "lane must be 0 (main), 1 (copy-in) or 2 (copy-out)");
+    if (lane < 0 || lane > 3)
+        return fail(CSAIDX_INVALID_ARGUMENT, "lane must be 0 (main), 1 (copy-in), 2 (copy-out) or 3 (side compute)");
     if (e->lane == 0) e->main_stream = e->stream;
     if (lane > 0 && e->lanes[lane] == nullptr)
         CSAIDX_CUDA_TRY(cudaStreamCreateWithFlags(&e->lanes[lane], cudaStreamNonBlocking), "cudaStreamCreate(lane)");
@@ -248,7 +252,7 @@ int csaidx_engine_use_lane(csaidx_engine* e, int lane) {
 
 int csaidx_engine_signal(csaidx_engine* e, int slot) {
     if (int rc = set_device(e)) return rc;
-    if (slot < 0 || slot >= 64) return fail(CSAIDX_INVALID_ARGUMENT, "event slot out of range");
+    if (slot < 0 || slot >= 128) return fail(CSAIDX_INVALID_ARGUMENT, "event slot out of range");
     if (e->slots[slot] == nullptr)
         CSAIDX_CUDA_TRY(cudaEventCreateWithFlags(&e->slots[slot], cudaEventDisableTiming), "cudaEventCreate");
     CSAIDX_CUDA_TRY(cudaEventRecord(e->slots[slot], e->stream), "cudaEventRecord");
@@ -257,7 +261,7 @@ int csaidx_engine_signal(csaidx_engine* e, int slot) {
 
 int csaidx_engine_await(csaidx_engine* e, int slot) {
     if (int rc = set_device(e)) return rc;
-    if (slot < 0 || slot >= 64) return fail(CSAIDX_INVALID_ARGUMENT, "event slot out of range");
+    if (slot < 0 || slot >= 128) return fail(CSAIDX_INVALID_ARGUMENT, "event slot out of range");
     if (e->slots[slot] == nullptr) return CSAIDX_OK;  // never signalled: nothing to wait for
     CSAIDX_CUDA_TRY(cudaStreamWaitEvent(e->stream, e->slots[slot], 0), "cudaStreamWaitEvent");
     return CSAIDX_OK;
@@ -265,7 +269,7 @@ int csaidx_engine_await(csaidx_engine* e, int slot) {
 
 int csaidx_engine_sync_slot(csaidx_engine* e, int slot) {
     if (int rc = set_device(e)) return rc;
-    if (slot < 0 || slot >= 64) return fail(CSAIDX_INVALID_ARGUMENT, "event slot out of range");
+    if (slot < 0 || slot >= 128) return fail(CSAIDX_INVALID_ARGUMENT, "event slot out of range");
     if (e->slots[slot] == nullptr) return CSAIDX_OK;
     CSAIDX_CUDA_TRY(cudaEventSynchronize(e->slots[slot]), "cudaEventSynchronize");
     return CSAIDX_OK;
@@ -291,10 +295,19 @@ int csaidx_engine_num_sms(csaidx_engine* e, int* num_sms) {
     return CSAIDX_OK;
 }
 
+int csaidx_engine_set_partition(csaidx_engine* e, int score_sms, int select_sms) {
+    if (e == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null engine");
+    if (score_sms < 0 || select_sms < 0 || score_sms + select_sms > e->num_sms)
+        return fail(CSAIDX_INVALID_ARGUMENT, "partition exceeds the SM count");
+    e->score_sms = score_sms;
+    e->select_sms = select_sms;
+    return CSAIDX_OK;
+}
+
 int csaidx_engine_check(csaidx_engine* e) {
     if (int rc = set_device(e)) return rc;
     CSAIDX_CUDA_TRY(cudaStreamSynchronize(e->stream), "cudaStreamSynchronize");
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < 4; ++i) {
         cudaStream_t s = i == 0 ? e->main_stream : e->lanes[i];
         if (s != nullptr && s != e->stream) CSAIDX_CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize(lane)");
     }
@@ -510,7 +523,9 @@ int launch_tc(csaidx_engine* e, const void* q, const void* kc, const float* w, c
     p.bits_ld = bits_ld;
     p.probe = e->score_probe;
     LaunchScope ls(e, CSAIDX_KIND_SCORE);
-    CSAIDX_CUDA_TRY(csaidx_kern::launch_score_tc(qmap, kmap, p, e->num_sms, e->stream), "score_tc");
+    CSAIDX_CUDA_TRY(csaidx_kern::launch_score_tc(qmap, kmap, p, e->score_sms > 0 ? e->score_sms : e->num_sms,
+                                                 e->stream),
+                    "score_tc");
     return CSAIDX_OK;
 }
 
@@ -660,6 +675,10 @@ int csaidx_cuda_apply_bool_mask(csaidx_engine* e, float* scores, int64_t ld, con
 
 int csaidx_cuda_select_capacity(void) { return csaidx_kern::select_max_take(); }
 
+int csaidx_cuda_select_overlap_capable(int64_t k) {
+    return k >= 1 && k <= csaidx_kern::select_max_take() && csaidx_kern::select_fat_fits(static_cast<int>(k)) ? 1 : 0;
+}
+
 }  // extern "C"
 
 namespace {
@@ -701,6 +720,7 @@ int select_impl(csaidx_engine* e, const float* scores, int64_t batch, int64_t ro
     p.final_idx = final_idx;
     p.final_rows = final_rows;
     p.final_row0 = final_row0;
+    p.persistent_ctas = e->select_sms;
     LaunchScope ls(e, CSAIDX_KIND_SELECT);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_select(p, e->stream), "select");
     return CSAIDX_OK;

@@ -108,6 +108,15 @@ void DeviceBuffer::upload(const void* host, size_t bytes) { check(csaidx_cuda_co
 
 void DeviceBuffer::download(void* host, size_t bytes) const { check(csaidx_cuda_copy(e_, host, ptr_, bytes)); }
 
+int select_overlap_sms() {
+    // Off by default: measured slower at C3 (profiles/r01_ncu_history.md) —
+    // the score kernel loses more than the SMs it gives up once a select
+    // runs beside it (shared power cap and HBM), and the select on a few
+    // SMs does not get faster per SM.
+    const char* v = std::getenv("CSAIDX_SELECT_SMS");
+    return v != nullptr ? std::atoi(v) : 0;
+}
+
 bool prefilter_enabled() {
     const char* v = std::getenv("CSAIDX_SELECT_PREFILTER");
     return v != nullptr && std::string(v) == "1";

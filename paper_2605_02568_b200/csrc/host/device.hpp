@@ -56,6 +56,9 @@ private:
 // saves in the select (-2 ms), so it stays an A/B option. The
 // sample pass scores at most kPrefilterSampleTiles 128-key tiles per row.
 bool prefilter_enabled();
+// SMs given to the select while it runs beside the next chunk's score kernel
+// (CSAIDX_SELECT_SMS; default 0 = no overlap: each select uses the GPU).
+int select_overlap_sms();
 constexpr int64_t kPrefilterSampleTiles = 16;
 
 int kernel_code(ScoreKernel kernel);  // throws like resolve_score_kernel for unavailable kernels

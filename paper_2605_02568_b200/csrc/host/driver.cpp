@@ -96,8 +96,36 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
         pf_sample = DeviceBuffer(e, static_cast<size_t>(B * plan.cs * lds) * sizeof(float));
     }
 
+    // Select beside score: with one key tile per query chunk (c_T >= T) on
+    // the tensor-core path, chunk o's select runs on a few SMs (persistent,
+    // several rows per CTA) on a second compute lane while chunk o+1's score
+    // runs on the rest; the score tiles are double buffered. Results are
+    // identical (the same kernels per row); only the SM assignment changes.
+    const bool overlap = plan.ct >= T && !prefilter && !config.bool_mask_tile && plan.order.size() >= 2 &&
+                         csaidx_cuda_score_uses_tensor_cores(&cd, ops.dtype, mcode, kcode) != 0 &&
+                         csaidx_cuda_select_overlap_capable(k) != 0 && select_overlap_sms() > 0;
+    DeviceBuffer scores2;
+    struct PartitionGuard {
+        csaidx_engine* e = nullptr;
+        ~PartitionGuard() {
+            if (e != nullptr) csaidx_engine_set_partition(e, 0, 0);
+        }
+    } partition;
+    if (overlap) {
+        scores2 = DeviceBuffer(e, static_cast<size_t>(B * plan.cs * ld) * sizeof(float));
+        int nsm = 0;
+        check(csaidx_engine_num_sms(e, &nsm));
+        const int x = std::min(select_overlap_sms(), nsm / 3);
+        check(csaidx_engine_set_partition(e, nsm - x, x));
+        partition.e = e;
+    }
+    constexpr int kScoreDone = 64, kSelectDone = 96, kSideLane = 3;
+
     for (size_t o = 0; o < plan.order.size(); ++o) {
         const size_t c = plan.order[o];
+        float* const sbuf = overlap && (o & 1) ? scores2.as<float>() : scores.as<float>();
+        // (overlap) the buffer was last read by chunk o-2's select
+        if (overlap && o >= 2) check(csaidx_engine_await(e, kSelectDone + static_cast<int>((o - 2) % 32)));
         const int64_t s0 = plan.starts[c];
         const int64_t rows = std::min(plan.cs, dims.seq_len - s0);
         const int64_t op_rows = ops.op_rows > 0 ? ops.op_rows : dims.seq_len;
@@ -132,17 +160,17 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
                                                 pf_sample.as<float>(), lds));
                 check(csaidx_cuda_row_threshold(e, pf_sample.as<float>(), lds, B, rows, cols, s0, t0, dims.ratio,
                                                 stride, k, pf_tau.as<float>()));
-                check(csaidx_cuda_score_filtered(e, ops.q, ops.kc, ops.w, &cd, s0, rows, t0, cols, scores.as<float>(),
+                check(csaidx_cuda_score_filtered(e, ops.q, ops.kc, ops.w, &cd, s0, rows, t0, cols, sbuf,
                                                  ld, pf_tau.as<float>(), pf_bits.as<uint32_t>(), bits_ld));
             } else if (config.bool_mask_tile) {
                 check(csaidx_cuda_score_rows(e, ops.q, ops.kc, ops.dtype, ops.w, &cd, s0, rows, t0, cols, mcode, kcode,
-                                             0, scores.as<float>(), ld, op_rows, op_row0));
+                                             0, sbuf, ld, op_rows, op_row0));
                 LedgerCharge mask_charge(ledger, "mask_tile", static_cast<uint64_t>(rows) * static_cast<uint64_t>(cols));
                 check(csaidx_cuda_bool_mask(e, keep.as<uint8_t>(), s0, t0, rows, cols, dims.ratio));
-                check(csaidx_cuda_apply_bool_mask(e, scores.as<float>(), ld, keep.as<uint8_t>(), B, rows, cols));
+                check(csaidx_cuda_apply_bool_mask(e, sbuf, ld, keep.as<uint8_t>(), B, rows, cols));
             } else {
                 check(csaidx_cuda_score_rows(e, ops.q, ops.kc, ops.dtype, ops.w, &cd, s0, rows, t0, cols, mcode, kcode,
-                                             1, scores.as<float>(), ld, op_rows, op_row0));
+                                             1, sbuf, ld, op_rows, op_row0));
             }
             ++stats.dispatch_count;
             const int64_t width = std::min(k, cols);
@@ -150,17 +178,23 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
             const bool overwrite = config.ablation == Ablation::a1_no_merge;
             auto select = [&](float* v, int32_t* i, int64_t out_ld) {
                 if (filtered)
-                    check(csaidx_cuda_select_from_candidates(e, scores.as<float>(), B, rows, ld, cols, s0, t0,
+                    check(csaidx_cuda_select_from_candidates(e, sbuf, B, rows, ld, cols, s0, t0,
                                                              dims.ratio, k, pf_bits.as<uint32_t>(), bits_ld, v, i,
                                                              out_ld));
                 else
-                    check(csaidx_cuda_select(e, scores.as<float>(), B, rows, ld, cols, s0, t0, dims.ratio, 1, k, v, i,
+                    check(csaidx_cuda_select(e, sbuf, B, rows, ld, cols, s0, t0, dims.ratio, 1, k, v, i,
                                              out_ld));
             };
             if (one_tile) {
-                check(csaidx_cuda_select_final(e, scores.as<float>(), B, rows, ld, cols, s0, t0, dims.ratio, k,
+                if (overlap) {  // select on the side lane once this chunk's score is done
+                    check(csaidx_engine_signal(e, kScoreDone + static_cast<int>(o % 32)));
+                    check(csaidx_engine_use_lane(e, kSideLane));
+                    check(csaidx_engine_await(e, kScoreDone + static_cast<int>(o % 32)));
+                }
+                check(csaidx_cuda_select_final(e, sbuf, B, rows, ld, cols, s0, t0, dims.ratio, k,
                                                filtered ? pf_bits.as<uint32_t>() : nullptr, bits_ld, out_idx, out_val,
                                                out_rows, plan.out_row0[c]));
+                if (overlap) check(csaidx_engine_signal(e, kSelectDone + static_cast<int>(o % 32)));
                 finalized = true;
             } else if (first && width == k) {
                 // merge into all-sentinel rows (or A1 overwrite) == copy
@@ -178,7 +212,12 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
                                        config.ablation == Ablation::none ? 1 : 0, out_idx, out_val, out_rows,
                                        plan.out_row0[c]));
         }
-        if (hooks.after) hooks.after(o);
+        // (overlap) still on the side lane when this chunk's select was
+        // enqueued there: hooks.after signals from it and returns to lane 0
+        if (hooks.after)
+            hooks.after(o);
+        else
+            check(csaidx_engine_use_lane(e, 0));
     }
     check(csaidx_engine_check(e));
 }

@@ -94,6 +94,9 @@ struct SelectParams {
     // int64 indices; entries past min(k, n) are (-inf, -1).
     int64_t* final_idx;
     int64_t final_rows, final_row0;
+    // > 0: run as that many persistent CTAs, one per SM, each with several
+    // row groups (to share the GPU with a concurrently running score kernel)
+    int persistent_ctas;
 };
 
 // Per-row candidate threshold from a strided sample of the row's scores
@@ -164,6 +167,7 @@ cudaError_t launch_score_exact(const ScoreExactParams& p, cudaStream_t stream);
 
 int select_max_take();
 int select_cand_capacity(int k);  // candidate-list length the select kernel accepts for this k
+bool select_fat_fits(int k);      // the persistent multi-row form fits shared memory for this k
 cudaError_t launch_select(const SelectParams& p, cudaStream_t stream);
 cudaError_t launch_tau(const TauParams& p, cudaStream_t stream);
 cudaError_t launch_merge(const MergeParams& p, cudaStream_t stream);

@@ -39,10 +39,14 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
-// All selection code runs on one group of kThreads threads synchronised by
-// named barrier 1 (the whole CTA of select_kernel / tau_kernel), so the row
-// stages can also serve a CTA with extra, non-participating warps.
-__device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory"); }
+// A CTA may host several row groups of kThreads threads (the persistent
+// select_fat_kernel); every row-stage helper works on its group: gtid() is
+// the thread's index in the group and csync() the group's own barrier.
+__device__ __forceinline__ int gtid() { return static_cast<int>(threadIdx.x) & (kThreads - 1); }
+__device__ __forceinline__ int gidx() { return static_cast<int>(threadIdx.x) / kThreads; }
+__device__ __forceinline__ void csync() {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + gidx()), "n"(kThreads) : "memory");
+}
 constexpr int kBins = 2048;
 constexpr int kMaxTake = 4096;    // largest min(k, n) a row may select
 constexpr int kMaxCand = 8192;    // largest shared candidate list
@@ -90,7 +94,7 @@ __device__ __forceinline__ int64_t composite_col(uint64_t c) {
 __device__ void bitonic_sort_desc(uint64_t* a, int P) {
     for (int size = 2; size <= P; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int i = threadIdx.x; i < P / 2; i += kThreads) {
+            for (int i = gtid(); i < P / 2; i += kThreads) {
                 const int lo = 2 * i - (i & (stride - 1));
                 const int hi = lo + stride;
                 const bool desc = (lo & size) == 0;
@@ -115,7 +119,7 @@ __device__ void bitonic_sort_desc(uint64_t* a, int P) {
 template <int E>
 __device__ __forceinline__ void bitonic_sort_desc_regs(uint64_t* a) {
     constexpr int P = E * kThreads;
-    const int t = threadIdx.x;
+    const int t = gtid();
     uint64_t x[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) x[e] = a[t * E + e];
@@ -180,9 +184,9 @@ __device__ void sort_desc(uint64_t* a, int P) {
 // kk-th largest element: every thread sums a run of bins, a block scan
 // locates the run, its owner walks it. out3 = {bin, count above, bin count}.
 __device__ void find_bin(const uint32_t* hist, int nbins, uint32_t kk, uint32_t* out3, uint32_t* wsum) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = gtid() & 31, warp = gtid() >> 5;
     const int per = nbins >= kThreads ? nbins / kThreads : 1;
-    const int hi = nbins - static_cast<int>(threadIdx.x) * per;  // thread 0 owns the highest bins
+    const int hi = nbins - gtid() * per;  // thread 0 owns the highest bins
     uint32_t sum = 0;
     for (int b = hi - 1; b >= hi - per && b >= 0; --b) sum += hist[b];
     uint32_t incl = sum;
@@ -219,15 +223,15 @@ __device__ void find_bin(const uint32_t* hist, int nbins, uint32_t kk, uint32_t*
 __device__ void smem_take_top(const uint64_t* a, int n, uint32_t kk, uint64_t* dst, uint32_t* hist, uint32_t* res,
                               uint32_t* wsum, uint32_t* counter) {
     __shared__ unsigned long long s_mm[2];
-    const int lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
+    const int lane = gtid() & 31;
+    if (gtid() == 0) {
         s_mm[0] = ~0ull;
         s_mm[1] = 0ull;
         *counter = 0;
     }
     csync();
     unsigned long long mn = ~0ull, mx = 0ull;
-    for (int i = threadIdx.x; i < n; i += kThreads) {
+    for (int i = gtid(); i < n; i += kThreads) {
         mn = min(mn, static_cast<unsigned long long>(a[i]));
         mx = max(mx, static_cast<unsigned long long>(a[i]));
     }
@@ -247,9 +251,9 @@ __device__ void smem_take_top(const uint64_t* a, int n, uint32_t kk, uint64_t* d
     while (pbits < 64) {
         const int wbits = 64 - pbits < 11 ? 64 - pbits : 11;
         const int shift = 64 - pbits - wbits;
-        for (int i = threadIdx.x; i < kBins; i += kThreads) hist[i] = 0;
+        for (int i = gtid(); i < kBins; i += kThreads) hist[i] = 0;
         csync();
-        for (int i = threadIdx.x; i < n; i += kThreads) {
+        for (int i = gtid(); i < n; i += kThreads) {
             const uint64_t v = a[i];
             if (pbits == 0 || (v >> (64 - pbits)) == prefix)
                 atomicAdd(&hist[static_cast<uint32_t>(v >> shift) & ((1u << wbits) - 1u)], 1u);
@@ -265,7 +269,7 @@ __device__ void smem_take_top(const uint64_t* a, int n, uint32_t kk, uint64_t* d
     }
     // keep the values whose top pbits are >= prefix (exactly the requested count)
     const int nr = (n + 31) & ~31;
-    for (int i = threadIdx.x; i < nr; i += kThreads) {
+    for (int i = gtid(); i < nr; i += kThreads) {
         const uint64_t v = i < n ? a[i] : 0ull;
         const bool keep = i < n && (pbits >= 64 ? v >= prefix : (v >> (64 - pbits)) >= prefix);
         const uint32_t m = __ballot_sync(0xffffffffu, keep);
@@ -296,8 +300,8 @@ __device__ __forceinline__ int fin_bin(uint64_t c, float lo, float scale) {
 // (plo, pscale).
 __device__ bool bucket_finish(uint64_t* a, int n, int take, uint64_t* tmp, int tmp_cap, uint32_t* start,
                               uint32_t* cur, uint32_t* wsum, uint32_t* sc, bool prebuilt, float plo, float pscale) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) {
+    const int lane = gtid() & 31, warp = gtid() >> 5;
+    if (gtid() == 0) {
         sc[0] = 0xffffffffu;  // min key
         sc[1] = 0u;           // max key
         sc[2] = 0u;           // overflow flag
@@ -305,9 +309,9 @@ __device__ bool bucket_finish(uint64_t* a, int n, int take, uint64_t* tmp, int t
     }
     float lo = plo, scale = pscale;  // prebuilt: start[] already holds the histogram over (plo, pscale)
     if (!prebuilt) {
-        for (int i = threadIdx.x; i < kFinBins; i += kThreads) start[i] = 0;
+        for (int i = gtid(); i < kFinBins; i += kThreads) start[i] = 0;
         uint32_t kmin = 0xffffffffu, kmax = 0u;
-        for (int i = threadIdx.x; i < n; i += kThreads) {
+        for (int i = gtid(); i < n; i += kThreads) {
             const uint32_t key = static_cast<uint32_t>(a[i] >> 32);
             kmin = min(kmin, key);
             kmax = max(kmax, key);
@@ -324,7 +328,7 @@ __device__ bool bucket_finish(uint64_t* a, int n, int take, uint64_t* tmp, int t
         const float hi = ord_key_to_float(sc[1]);
         scale = static_cast<float>(kFinBins) / (hi - lo);
         if (!(hi > lo) || !isfinite(scale)) scale = 0.f;
-        for (int i = threadIdx.x; i < n; i += kThreads) atomicAdd(&start[fin_bin(a[i], lo, scale)], 1u);
+        for (int i = gtid(); i < n; i += kThreads) atomicAdd(&start[fin_bin(a[i], lo, scale)], 1u);
     }
     csync();
     // descending exclusive scan: thread t owns bins [NB-4t-4, NB-4t), highest first
@@ -332,8 +336,8 @@ __device__ bool bucket_finish(uint64_t* a, int n, int take, uint64_t* tmp, int t
     static_assert(kFinBins % 256 == 0, "bins per thread");
     uint32_t c[kPer];
     uint32_t sum = 0;
-    const int top = kFinBins - 1 - kPer * static_cast<int>(threadIdx.x);
-    if (threadIdx.x < 256) {
+    const int top = kFinBins - 1 - kPer * gtid();
+    if (gtid() < 256) {
 #pragma unroll
         for (int u = 0; u < kPer; ++u) {
             c[u] = start[top - u];
@@ -350,7 +354,7 @@ __device__ bool bucket_finish(uint64_t* a, int n, int take, uint64_t* tmp, int t
     csync();
     uint32_t before = 0;
     for (int w = 0; w < warp; ++w) before += wsum[w];
-    if (threadIdx.x < 256) {
+    if (gtid() < 256) {
         uint32_t run = before + incl - sum;
         const uint32_t tk = static_cast<uint32_t>(take);
 #pragma unroll
@@ -368,13 +372,13 @@ __device__ bool bucket_finish(uint64_t* a, int n, int take, uint64_t* tmp, int t
     csync();
     if (sc[2] != 0u) return false;
     const uint32_t extent = sc[3];
-    for (int i = threadIdx.x; i < n; i += kThreads) {
+    for (int i = gtid(); i < n; i += kThreads) {
         const uint64_t v = a[i];
         const int b = fin_bin(v, lo, scale);
         if (start[b] < static_cast<uint32_t>(take)) tmp[atomicAdd(&cur[b], 1u)] = v;
     }
     csync();
-    for (uint32_t s = threadIdx.x; s < extent; s += kThreads) {
+    for (uint32_t s = gtid(); s < extent; s += kThreads) {
         const uint64_t v = tmp[s];
         const int b = fin_bin(v, lo, scale);
         const uint32_t b0 = start[b], b1 = cur[b];
@@ -395,11 +399,11 @@ __device__ __forceinline__ bool prefix_match(uint32_t key, uint32_t prefix, int 
 }
 
 __device__ void histogram_pass(const float* row, int64_t n, uint32_t prefix, int pbits, int wbits, uint32_t* hist) {
-    for (int i = threadIdx.x; i < kBins; i += kThreads) hist[i] = 0;
+    for (int i = gtid(); i < kBins; i += kThreads) hist[i] = 0;
     csync();
     const int shift = 32 - pbits - wbits;
     const uint32_t mask = (1u << wbits) - 1u;
-    for (int64_t i = threadIdx.x; i < n; i += kThreads) {
+    for (int64_t i = gtid(); i < n; i += kThreads) {
         const uint32_t key = ord_key(__ldg(row + i));
         if (prefix_match(key, prefix, pbits)) atomicAdd(&hist[(key >> shift) & mask], 1u);
     }
@@ -410,12 +414,12 @@ __device__ void histogram_pass(const float* row, int64_t n, uint32_t prefix, int
 // above_dst, entries equal to it to eq_dst (first eq_limit in index order).
 __device__ void collect_pass(const float* row, int64_t n, uint32_t prefix, int pbits, uint64_t* above_dst,
                              uint64_t* eq_dst, uint32_t eq_limit, uint32_t* wtot) {
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
+    const int lane = gtid() & 31;
+    const int warp = gtid() >> 5;
     uint32_t run_above = 0, run_eq = 0;
     int parity = 0;
     for (int64_t base = 0; base < n; base += kThreads) {
-        const int64_t i = base + threadIdx.x;
+        const int64_t i = base + gtid();
         uint32_t key = 0;
         int cls = 0;
         if (i < n) {
@@ -478,10 +482,10 @@ __device__ void exact_global_select(const float* row, int64_t n, int k, uint64_t
     } else {
         collect_pass(row, n, prefix, pbits, buf, cand, static_cast<uint32_t>(cand_cap), wtot);
         const int P = pow2_at_least(static_cast<int>(bin_count));
-        for (int i = static_cast<int>(bin_count) + threadIdx.x; i < P; i += kThreads) cand[i] = 0;
+        for (int i = static_cast<int>(bin_count) + gtid(); i < P; i += kThreads) cand[i] = 0;
         csync();
         sort_desc(cand, P);
-        for (uint32_t i = threadIdx.x; i < kk; i += kThreads) buf[above + i] = cand[i];
+        for (uint32_t i = gtid(); i < kk; i += kThreads) buf[above + i] = cand[i];
     }
     csync();
 }
@@ -500,11 +504,11 @@ __device__ void gather_candidates(const float* row, const uint32_t* idx_list, in
         uint32_t cc[kGatherPer];
 #pragma unroll
         for (int g = 0; g < kGatherPer; ++g) {
-            const int i = threadIdx.x + g * kThreads;
+            const int i = gtid() + g * kThreads;
             cc[g] = i < count ? idx_list[i] : 0u;
         }
         csync();  // the list (it may alias hist) is consumed
-        for (int i = threadIdx.x; i < kFinBins; i += kThreads) hist[i] = 0;
+        for (int i = gtid(); i < kFinBins; i += kThreads) hist[i] = 0;
         pb_lo = lo_f;
         pb_scale = static_cast<float>(kFinBins) / (hi_f - lo_f);
         if (!(hi_f > lo_f) || !isfinite(pb_scale)) pb_scale = 0.f;
@@ -514,10 +518,10 @@ __device__ void gather_candidates(const float* row, const uint32_t* idx_list, in
             float vv[8];
 #pragma unroll
             for (int g = 0; g < 8; ++g)
-                vv[g] = threadIdx.x + (h + g) * kThreads < count ? __ldg(row + cc[h + g]) : 0.f;
+                vv[g] = gtid() + (h + g) * kThreads < count ? __ldg(row + cc[h + g]) : 0.f;
 #pragma unroll
             for (int g = 0; g < 8; ++g) {
-                const int i = threadIdx.x + (h + g) * kThreads;
+                const int i = gtid() + (h + g) * kThreads;
                 if (i < count) {
                     const uint64_t c = composite(ord_key(vv[g]), cc[h + g]);
                     cand[i] = c;
@@ -528,7 +532,7 @@ __device__ void gather_candidates(const float* row, const uint32_t* idx_list, in
         prebuilt = true;
     } else if (count >= 0) {
         constexpr int G = 8;
-        for (int base = threadIdx.x; base < count; base += G * kThreads) {
+        for (int base = gtid(); base < count; base += G * kThreads) {
             uint32_t cc[G];
             float vv[G];
 #pragma unroll
@@ -564,14 +568,14 @@ __device__ const uint64_t* finish_row(const float* row, int64_t n, int take, int
         if (count > take) {
             smem_take_top(cand, count, static_cast<uint32_t>(take), buf, hist, res, wsum, counter);
         } else {
-            for (int i = threadIdx.x; i < count; i += kThreads) buf[i] = cand[i];
+            for (int i = gtid(); i < count; i += kThreads) buf[i] = cand[i];
         }
     } else {
-        if (threadIdx.x == 0 && fallbacks != nullptr) atomicAdd(fallbacks, 1);
+        if (gtid() == 0 && fallbacks != nullptr) atomicAdd(fallbacks, 1);
         exact_global_select(row, n, take, buf, cand, L.cand_cap, hist, wtot, res, wsum);
     }
     const int P = pow2_at_least(take);
-    for (int i = take + threadIdx.x; i < P; i += kThreads) buf[i] = 0;
+    for (int i = take + gtid(); i < P; i += kThreads) buf[i] = 0;
     csync();
     sort_desc(buf, P);
     return buf;
@@ -588,7 +592,7 @@ __device__ void write_row(const SelectParams& p, int b, int64_t row_id, int take
     const float neg_inf = -__int_as_float(0x7f800000);
     if (final_out) {
         int64_t* oi = p.final_idx + orow * p.out_ld;
-        for (int e = threadIdx.x; e < p.width; e += kThreads) {
+        for (int e = gtid(); e < p.width; e += kThreads) {
             if (e < take) {
                 const uint64_t c = result[e];
                 const float v = ord_key_to_float(static_cast<uint32_t>(c >> 32));
@@ -602,7 +606,7 @@ __device__ void write_row(const SelectParams& p, int b, int64_t row_id, int take
         return;
     }
     int32_t* oi = p.out_idx + orow * p.out_ld;
-    for (int e = threadIdx.x; e < p.width; e += kThreads) {
+    for (int e = gtid(); e < p.width; e += kThreads) {
         if (e < take) {
             const uint64_t c = result[e];
             ov[e] = ord_key_to_float(static_cast<uint32_t>(c >> 32));
@@ -617,9 +621,9 @@ __device__ void write_row(const SelectParams& p, int b, int64_t row_id, int take
 // ------------------------------------------------------------------ kernel
 
 
-template <int kUnroll, int kMinBlocks>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const SelectParams p) {
-    extern __shared__ __align__(16) uint8_t smem_raw[];
+// One row (b, row_id) on one row group, with that group's shared memory.
+template <int kUnroll>
+__device__ __forceinline__ void select_row(const SelectParams& p, int b, int64_t row_id, uint8_t* smem_raw) {
     const int k = p.k;
     const Layout L = layout_for(k);
     uint64_t* cand = reinterpret_cast<uint64_t*>(smem_raw);  // [cand_cap]
@@ -630,8 +634,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const Sele
     uint32_t* res = wsum + kWarps;                           // [8]
     uint32_t* counter = res + 4;
 
-    const int64_t row_id = blockIdx.x;
-    const int b = blockIdx.y;
     int64_t n = p.cols;
     if (p.apply_mask) {
         n = (p.s0 + row_id + 1) / p.ratio - p.t0;
@@ -639,10 +641,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const Sele
     }
     const float* row = p.scores + (static_cast<int64_t>(b) * p.rows + row_id) * p.ld;
     const int take = static_cast<int>(n < k ? n : k);
-    const int lane = threadIdx.x & 31;
+    const int lane = gtid() & 31;
 
     const uint64_t* result = buf;  // sorted selection, best first (buf or cand)
-    long long* clk = p.phase_clk != nullptr && threadIdx.x == 0 && b == 0 ? p.phase_clk + row_id * 8 : nullptr;
+    long long* clk = p.phase_clk != nullptr && gtid() == 0 && b == 0 ? p.phase_clk + row_id * 8 : nullptr;
     if (clk) clk[0] = clock64();
     if (take > 0) {
         int count = -1;  // candidates in cand[], or -1 -> fallback
@@ -655,19 +657,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const Sele
             // contain the exact top-take and fit the list.
             const uint32_t* bits = p.pass_bits + (static_cast<int64_t>(b) * p.rows + row_id) * p.bits_ld;
             const int nw = static_cast<int>((n + 31) >> 5);
-            if (threadIdx.x == 0) *counter = 0;
+            if (gtid() == 0) *counter = 0;
             csync();
             uint32_t loc = 0;
-            for (int i = threadIdx.x; i < nw; i += kThreads) loc += __popc(__ldg(bits + i));
+            for (int i = gtid(); i < nw; i += kThreads) loc += __popc(__ldg(bits + i));
             loc = __reduce_add_sync(0xffffffffu, loc);
             if (lane == 0 && loc != 0) atomicAdd(counter, loc);
             csync();
             const uint32_t tot = *counter;
             csync();
             if (tot >= static_cast<uint32_t>(take) && tot <= static_cast<uint32_t>(L.cand_cap)) {
-                if (threadIdx.x == 0) *counter = 0;
+                if (gtid() == 0) *counter = 0;
                 csync();
-                for (int i = threadIdx.x; i < nw; i += kThreads) {
+                for (int i = gtid(); i < nw; i += kThreads) {
                     uint32_t m = __ldg(bits + i);
                     if (m == 0) continue;
                     uint32_t pos = atomicAdd(counter, static_cast<uint32_t>(__popc(m)));
@@ -678,14 +680,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const Sele
                     }
                 }
                 pre = static_cast<int>(tot);
-                if (threadIdx.x == 0 && p.cand_hits != nullptr) atomicAdd(p.cand_hits, 1);
+                if (gtid() == 0 && p.cand_hits != nullptr) atomicAdd(p.cand_hits, 1);
                 csync();
             }
         }
         if (pre >= 0) {
             count = pre;
         } else if (n <= L.cand_cap) {
-            for (int64_t i = threadIdx.x; i < n; i += kThreads) cand[i] = composite(ord_key(__ldg(row + i)), i);
+            for (int64_t i = gtid(); i < n; i += kThreads) cand[i] = composite(ord_key(__ldg(row + i)), i);
             count = static_cast<int>(n);
             csync();
         } else {
@@ -697,7 +699,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const Sele
             if (nseg < 1) nseg = 1;
             const int64_t seg_stride = (n / nseg) & ~int64_t{3};
             constexpr int kSegsPerWarp = kSampleSegs / kWarps;  // 8
-            const int w = threadIdx.x >> 5;
+            const int w = gtid() >> 5;
             float4 sv[kSegsPerWarp];
 #pragma unroll
             for (int u = 0; u < kSegsPerWarp; ++u) {
@@ -715,13 +717,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const Sele
                     kmax = max(kmax, max(max(k0, k1), max(k2, k3)));
                 }
             }
-            if (threadIdx.x == 0) {
+            if (gtid() == 0) {
                 *counter = 0;
                 res[0] = res[1] = res[2] = 0u;  // find_bin leaves them when the rank is out of range
                 res[6] = 0xffffffffu;
                 res[7] = 0u;
             }
-            for (int i = threadIdx.x; i < kBins; i += kThreads) hist[i] = 0;
+            for (int i = gtid(); i < kBins; i += kThreads) hist[i] = 0;
             csync();
             kmin = __reduce_min_sync(0xffffffffu, kmin);
             kmax = __reduce_max_sync(0xffffffffu, kmax);
@@ -750,8 +752,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const Sele
                 float scale = static_cast<float>(kBins) / (hi - lo);
                 if (!(hi > lo) || !isfinite(scale)) break;  // degenerate: keep tau = lo
                 if (pass > 0) {
-                    for (int i = threadIdx.x; i < kBins; i += kThreads) hist[i] = 0;
-                    if (threadIdx.x == 0) res[0] = res[1] = res[2] = 0u;
+                    for (int i = gtid(); i < kBins; i += kThreads) hist[i] = 0;
+                    if (gtid() == 0) res[0] = res[1] = res[2] = 0u;
                     csync();
                 }
 #pragma unroll
@@ -795,7 +797,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const Sele
             const int64_t n4r = (n4 + step - 1) / step * step;
             const uint32_t cap = static_cast<uint32_t>(
                 min(L.cand_cap, 2 * L.buf_cap + kBins));  // idx list capacity
-            for (int64_t it = threadIdx.x; it < n4r; it += step) {
+            for (int64_t it = gtid(); it < n4r; it += step) {
                 float4 v[kUnroll];
 #pragma unroll
                 for (int u = 0; u < kUnroll; ++u) {
@@ -834,7 +836,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const Sele
                     ++pos;
                 }
             }
-            if (threadIdx.x < 32) {  // the < 4 entries past the last float4
+            if (gtid() < 32) {  // the < 4 entries past the last float4
                 const int64_t i = 4 * n4 + lane;
                 const bool inb = i < n;
                 const uint32_t key = inb ? ord_key(__ldg(row + i)) : 0u;
@@ -870,6 +872,29 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const Sele
     write_row(p, b, row_id, take, result);
 }
 
+template <int kUnroll, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const SelectParams p) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    select_row<kUnroll>(p, static_cast<int>(blockIdx.y), blockIdx.x, smem_raw);
+}
+
+// Persistent form for running beside the score kernel on a few SMs: one
+// fat CTA per SM holding kFatGroups independent row groups (each its own
+// shared memory slice and barrier) that walk the rows with a grid stride.
+constexpr int kFatGroups = 3;
+
+__global__ void __launch_bounds__(kThreads * kFatGroups, 1) select_fat_kernel(const SelectParams p) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    uint8_t* mine = smem_raw + static_cast<size_t>(gidx()) * smem_bytes_for(p.k);
+    const int64_t nrows = p.rows * p.batch;
+    for (int64_t rr = static_cast<int64_t>(blockIdx.x) * kFatGroups + gidx(); rr < nrows;
+         rr += static_cast<int64_t>(gridDim.x) * kFatGroups) {
+        const int b = static_cast<int>(rr / p.rows);
+        select_row<8>(p, b, rr - static_cast<int64_t>(b) * p.rows, mine);
+        csync();  // the group's shared memory is reused by its next row
+    }
+}
+
 // ------------------------------------------------------------------ tau
 constexpr int kTauMaxSamples = 8192;
 
@@ -880,29 +905,29 @@ __global__ void __launch_bounds__(kThreads) tau_kernel(const TauParams p) {
     __shared__ uint32_t res[8];
     const int64_t row_id = blockIdx.x;
     const int b = blockIdx.y;
-    const int lane = threadIdx.x & 31;
+    const int lane = gtid() & 31;
     int64_t n = (p.s0 + row_id + 1) / p.ratio - p.t0;
     n = n < 0 ? 0 : (n > p.cols ? p.cols : n);
     float* out = p.tau + static_cast<int64_t>(b) * p.rows + row_id;
     const float neg_inf = -__int_as_float(0x7f800000);
     if (n <= p.cand_cap) {  // the whole legal row fits the candidate list
-        if (threadIdx.x == 0) *out = neg_inf;
+        if (gtid() == 0) *out = neg_inf;
         return;
     }
     const int64_t vt = ((n + 127) / 128 + p.kt_stride - 1) / p.kt_stride;
     int64_t nv = vt * 128;
     if (nv > p.lds) nv = p.lds;
     const float* srow = p.sample + (static_cast<int64_t>(b) * p.rows + row_id) * p.lds;
-    if (threadIdx.x == 0) {
+    if (gtid() == 0) {
         res[4] = 0;
         res[6] = 0xffffffffu;
         res[7] = 0u;
     }
-    for (int i = threadIdx.x; i < kBins; i += kThreads) hist[i] = 0;
+    for (int i = gtid(); i < kBins; i += kThreads) hist[i] = 0;
     csync();
     uint32_t kmin = 0xffffffffu, kmax = 0u;
     const int64_t nvr = (nv + 31) & ~int64_t{31};
-    for (int64_t i = threadIdx.x; i < nvr; i += kThreads) {
+    for (int64_t i = gtid(); i < nvr; i += kThreads) {
         const float v = i < nv ? __ldg(srow + i) : neg_inf;
         const bool keep = v != neg_inf;  // legal sampled entries (scores are finite)
         const uint32_t m = __ballot_sync(0xffffffffu, keep);
@@ -929,7 +954,7 @@ __global__ void __launch_bounds__(kThreads) tau_kernel(const TauParams p) {
     int r = static_cast<int>((static_cast<int64_t>(target) * ns) / n);
     if (r < 1) r = 1;
     if (ns == 0 || r > ns) {  // sample too thin to cut: keep everything (the select falls back)
-        if (threadIdx.x == 0) *out = neg_inf;
+        if (gtid() == 0) *out = neg_inf;
         return;
     }
     const uint32_t lo = res[6], hi_k = res[7];
@@ -942,10 +967,10 @@ __global__ void __launch_bounds__(kThreads) tau_kernel(const TauParams p) {
         const int wbits = 32 - pbits < 11 ? 32 - pbits : 11;
         const int shift = 32 - pbits - wbits;
         if (pass > 0) {
-            for (int i = threadIdx.x; i < kBins; i += kThreads) hist[i] = 0;
+            for (int i = gtid(); i < kBins; i += kThreads) hist[i] = 0;
             csync();
         }
-        for (int i = threadIdx.x; i < ns; i += kThreads) {
+        for (int i = gtid(); i < ns; i += kThreads) {
             const uint32_t v = s_keys[i];
             if (pbits == 0 || (v >> (32 - pbits)) == prefix) atomicAdd(&hist[(v >> shift) & ((1u << wbits) - 1u)], 1u);
         }
@@ -956,7 +981,7 @@ __global__ void __launch_bounds__(kThreads) tau_kernel(const TauParams p) {
         pbits += wbits;
         csync();
     }
-    if (threadIdx.x == 0) *out = ord_key_to_float(pbits >= 32 ? prefix : (prefix << (32 - pbits)));
+    if (gtid() == 0) *out = ord_key_to_float(pbits >= 32 ? prefix : (prefix << (32 - pbits)));
 }
 
 }  // namespace
@@ -998,8 +1023,24 @@ int select_variant() {
 }
 }  // namespace
 
+// 227 KiB of opt-in shared memory per block, less 1 KiB for static shared
+// variables of the row stages
+constexpr size_t kFatSmemMax = 226 * 1024;
+bool select_fat_fits(int k) { return kFatGroups * smem_bytes_for(k) <= kFatSmemMax; }
+
 cudaError_t launch_select(const SelectParams& p, cudaStream_t stream) {
     if (p.rows <= 0 || p.batch <= 0) return cudaSuccess;
+    if (p.persistent_ctas > 0 && p.phase_clk == nullptr && select_fat_fits(p.k)) {
+        static bool fat_attr = false;
+        if (!fat_attr) {
+            cudaError_t e = cudaFuncSetAttribute(select_fat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(kFatSmemMax));
+            if (e != cudaSuccess) return e;
+            fat_attr = true;
+        }
+        select_fat_kernel<<<p.persistent_ctas, kThreads * kFatGroups, kFatGroups * smem_bytes_for(p.k), stream>>>(p);
+        return cudaGetLastError();
+    }
     // 8 float4 in flight per thread, 3 CTAs per SM (measured faster than
     // 4 x float4 at 4 CTAs per SM: scripts/probe_select.py)
     // 8 float4 in flight per thread at 3 CTAs per SM measured faster than

@@ -163,6 +163,11 @@ class Engine:
                                                 bits.shape[-1] if bits is not None else 0, _p(out_idx), _p(out_val),
                                                 out_idx.shape[1], out_row0))
 
+    def set_partition(self, score_sms: int, select_sms: int):
+        """csaidx_engine_set_partition: score launches on score_sms SMs, selects as
+        select_sms persistent multi-row CTAs (0, 0 = the whole GPU)."""
+        check(self.lib.csaidx_engine_set_partition(self.handle, score_sms, select_sms))
+
     def candidate_hits(self, reset: bool = True) -> int:
         n = c_int64(0)
         check(self.lib.csaidx_engine_candidate_hits(self.handle, byref(n), int(reset)))

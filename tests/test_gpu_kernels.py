@@ -261,6 +261,31 @@ def test_select_final_equals_select_then_finalize(engine, S, cols, k, m):
     assert np.array_equal(got, ri.astype(np.int64))
 
 
+@pytest.mark.parametrize("cols,k", [(40000, 1024), (3000, 512), (9000, 100)])
+def test_persistent_multirow_select_equals_per_row_select(engine, cols, k):
+    """The persistent 3-rows-per-CTA select (used beside the score kernel)
+    gives the per-row kernel's bytes, incl. heavy ties and short rows."""
+    rng = np.random.default_rng(cols)
+    B, rows = 2, 37
+    x = rng.normal(0, 1, (B, rows, cols)).astype(np.float32)
+    x[1] = np.round(x[1] * 8) / 8
+    ld = (cols + 3) // 4 * 4
+    pad = np.zeros((B, rows, ld), np.float32)
+    pad[:, :, :cols] = x
+    dev = to_dev(pad)
+    v0, i0 = engine.select(dev, B, rows, cols, cols + 5000, 0, 1, k)
+    engine.check()
+    engine.set_partition(100, 7)
+    try:
+        v1, i1 = engine.select(dev, B, rows, cols, cols + 5000, 0, 1, k)
+        engine.check()
+    finally:
+        engine.set_partition(0, 0)
+    assert torch.equal(i0, i1) and torch.equal(v0.view(torch.int32), v1.view(torch.int32))
+    wv, wi = ref_select(x, cols + 5000, 0, 1, k)
+    assert np.array_equal(i1.cpu().numpy(), wi)
+
+
 def test_select_all_equal_scores_take_smallest_indices(engine):
     B, rows, cols, k = 1, 3, 10000, 100
     scores = np.zeros((B, rows, cols), np.float32)

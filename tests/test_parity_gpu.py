@@ -208,6 +208,27 @@ def test_csat_dump_loads_into_hbm_rank_local(orc, tmp_path):
         api.load_inputs_device(tmp_path / "bad.csat", dims64, cfg, strict=True, dtype=0)
 
 
+@pytest.mark.parametrize("sms", ["0", "12", "40"])
+def test_select_beside_score_overlap_is_byte_identical(orc, monkeypatch, sms):
+    """One key tile per chunk on the tensor-core path: selects running beside
+    the next chunk's score kernel (CSAIDX_SELECT_SMS SMs, double-buffered
+    tiles, a second compute lane) give the same bytes as the serial path,
+    through the device entry and the host entry (copy lanes on top)."""
+    import torch
+
+    q, kc, w = orc.generate_inputs(1, 4096, 4, 64, 128, 31, bf16=True)
+    dims = api.ProblemDims.create(1, 4096, 4, 64, 128, 256)
+    cfg = api.DriverConfig(tile=api.TileConfig(512, 10 ** 6))
+    monkeypatch.setenv("CSAIDX_SELECT_SMS", "0")
+    ref, _ = api.run_chunked(api.IndexerInputs.validated(q, kc, w, dims), dims, cfg)
+    monkeypatch.setenv("CSAIDX_SELECT_SMS", sms)
+    got, _ = api.run_chunked(api.IndexerInputs.validated(q, kc, w, dims), dims, cfg)
+    assert np.array_equal(got.indices, ref.indices) and np.array_equal(bits(got.values), bits(ref.values))
+    qd, kd, wd = (torch.from_numpy(a).cuda() for a in (q, kc, w))
+    di, dv, _ = api.run_chunked_device(qd.to(torch.bfloat16), kd.to(torch.bfloat16), wd, dims, cfg)
+    assert np.array_equal(di.cpu().numpy(), ref.indices)
+
+
 def test_ablations_follow_reference_semantics(orc):
     # acceptance.cpp:339-380 directions at a small V4-like shape
     inputs, dims, (q, kc, w) = inputs_for(orc, 1, 2048, 4, 8, 64, 64, 1)
