@@ -126,10 +126,11 @@ __device__ __forceinline__ void decode_item(const ScoreTcParams& p, int idx, Ite
 // FFMA2 does not double the FMA pipe's rate, so the ALU pipe taking every
 // ReLU is the balanced split.
 //
-// The 64 columns are read from TMEM in slices so the whole epilogue fits
-// the 96 registers a 640-thread CTA allows; chain assignment and order do
+// The 64 columns are read from TMEM in 8-column slices so the epilogue fits
+// the 112 registers a 576-thread CTA allows; chain assignment and order do
 // not depend on the slicing. ncu: the epilogue's top stall is the short
-// scoreboard (w from shared memory / TMEM loads), then issue contention.
+// scoreboard (w from shared memory / TMEM loads), then issue contention; it
+// is latency bound, hence the paired form below.
 // One query's 64 head partials in eight 8-column TMEM slices (the load of
 // slice s+1 in flight while slice s is reduced), two packed FFMA2 chains.
 // head_reduce_tmem2 below computes exactly this per query (same chains,
