@@ -72,7 +72,7 @@ int csaidx_engine_use_own_stream(csaidx_engine* e);
 int csaidx_engine_get_stream(csaidx_engine* e, void** stream);
 /* Lanes for overlapping host transfers and kernels: subsequent calls
  * enqueue on lane 0 (the main stream set above), 1 (copy-in), 2 (copy-out)
- * or 3 (a second compute stream). signal records event `slot` (0..127) on the current lane;
+ * or 3 (a second compute stream). signal records event `slot` (0..191) on the current lane;
  * await makes the current lane wait for the slot's latest signal. */
 int csaidx_engine_use_lane(csaidx_engine* e, int lane);
 int csaidx_engine_signal(csaidx_engine* e, int slot);

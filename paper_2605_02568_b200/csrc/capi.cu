@@ -86,7 +86,7 @@ struct csaidx_engine {
     cudaStream_t lanes[4] = {nullptr, nullptr, nullptr, nullptr};  // [0] = main (== stream when lane 0 active)
     cudaStream_t main_stream = nullptr;
     int lane = 0;
-    cudaEvent_t slots[128] = {};
+    cudaEvent_t slots[192] = {};
     // SM partition while a select runs beside the score kernel (0 = whole GPU)
     int score_sms = 0;
     int select_sms = 0;
@@ -252,7 +252,7 @@ int csaidx_engine_use_lane(csaidx_engine* e, int lane) {
 
 int csaidx_engine_signal(csaidx_engine* e, int slot) {
     if (int rc = set_device(e)) return rc;
-    if (slot < 0 || slot >= 128) return fail(CSAIDX_INVALID_ARGUMENT, "event slot out of range");
+    if (slot < 0 || slot >= 192) return fail(CSAIDX_INVALID_ARGUMENT, "event slot out of range");
     if (e->slots[slot] == nullptr)
         CSAIDX_CUDA_TRY(cudaEventCreateWithFlags(&e->slots[slot], cudaEventDisableTiming), "cudaEventCreate");
     CSAIDX_CUDA_TRY(cudaEventRecord(e->slots[slot], e->stream), "cudaEventRecord");
@@ -261,7 +261,7 @@ int csaidx_engine_signal(csaidx_engine* e, int slot) {
 
 int csaidx_engine_await(csaidx_engine* e, int slot) {
     if (int rc = set_device(e)) return rc;
-    if (slot < 0 || slot >= 128) return fail(CSAIDX_INVALID_ARGUMENT, "event slot out of range");
+    if (slot < 0 || slot >= 192) return fail(CSAIDX_INVALID_ARGUMENT, "event slot out of range");
     if (e->slots[slot] == nullptr) return CSAIDX_OK;  // never signalled: nothing to wait for
     CSAIDX_CUDA_TRY(cudaStreamWaitEvent(e->stream, e->slots[slot], 0), "cudaStreamWaitEvent");
     return CSAIDX_OK;
@@ -269,7 +269,7 @@ int csaidx_engine_await(csaidx_engine* e, int slot) {
 
 int csaidx_engine_sync_slot(csaidx_engine* e, int slot) {
     if (int rc = set_device(e)) return rc;
-    if (slot < 0 || slot >= 128) return fail(CSAIDX_INVALID_ARGUMENT, "event slot out of range");
+    if (slot < 0 || slot >= 192) return fail(CSAIDX_INVALID_ARGUMENT, "event slot out of range");
     if (e->slots[slot] == nullptr) return CSAIDX_OK;
     CSAIDX_CUDA_TRY(cudaEventSynchronize(e->slots[slot]), "cudaEventSynchronize");
     return CSAIDX_OK;

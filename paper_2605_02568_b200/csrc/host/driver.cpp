@@ -292,33 +292,48 @@ void run_chunked_rows_view(const HostView& in, const ProblemDims& dims, const Dr
     // order, the same row layout as the outputs)
     DeviceBuffer q(e, static_cast<size_t>(B * out_rows * qrow) * esz), kc(e, static_cast<size_t>(dims.kc_elems()) * esz),
         w(e, static_cast<size_t>(B * out_rows * dims.heads) * sizeof(float));
-    DeviceBuffer slab[2];
+    constexpr int kSlabs = 8, kConvDone = 128;  // fp32 staging slabs; event slots of their conversion
+    DeviceBuffer slab[kSlabs];
     if (dtype == CSAIDX_DTYPE_BF16) {
-        for (auto& sb : slab) sb = DeviceBuffer(e, static_cast<size_t>(plan.cs * qrow) * sizeof(float));
+        for (auto& sb : slab) sb = DeviceBuffer(e, static_cast<size_t>(B * plan.cs * qrow) * sizeof(float));
     }
     const size_t n = static_cast<size_t>(B * out_rows * k);
     DeviceBuffer idx(e, n * sizeof(int64_t)), val(e, n * sizeof(float));
     const DeviceOps ops{q.as<void>(), kc.as<void>(), w.as<float>(), dtype, out_rows};
     constexpr int kMainLane = 0, kInLane = 1, kOutLane = 2;
-    auto upload_chunk = [&](size_t o) {  // o-th chunk in processing order
+    // Copy-in lane: raw fp32 rows only, so the DMA engine never waits for
+    // SMs (a conversion kernel queued on the copy lane would sit behind the
+    // persistent score kernel and stall the next copy). The bf16 rounding of
+    // chunk o runs on the main lane right before chunk o's score; kSlabs
+    // staging slabs let the copies run up to kSlabs chunks ahead.
+    auto upload_raw = [&](size_t o) {  // o-th chunk in processing order, on the copy-in lane
         const size_t c = plan.order[o];
         const int64_t s0 = plan.starts[c], rows = std::min(plan.cs, dims.seq_len - s0);
+        if (dtype == CSAIDX_DTYPE_BF16 && o >= kSlabs)  // slab o % kSlabs: chunk o - kSlabs converted
+            check(csaidx_engine_await(e, kConvDone + static_cast<int>((o - kSlabs) % 32)));
         for (int64_t b = 0; b < B; ++b) {
             const int64_t lrow = b * out_rows + plan.out_row0[c];  // operand row on device
             const int64_t hrow = in.local_rows ? lrow : b * dims.seq_len + s0;  // ... and on the host
             const int64_t qoff = hrow * qrow, woff = hrow * dims.heads;
-            if (dtype == CSAIDX_DTYPE_BF16) {
-                DeviceBuffer& sb = slab[o % 2];
-                check(csaidx_cuda_copy(e, sb.as<void>(), in.q + qoff, static_cast<size_t>(rows * qrow) * sizeof(float)));
-                check(csaidx_cuda_to_bf16(e, sb.as<float>(), q.as<uint16_t>() + lrow * qrow, rows * qrow, strict ? 1 : 0));
-            } else {
-                check(csaidx_cuda_copy(e, q.as<float>() + lrow * qrow, in.q + qoff,
-                                       static_cast<size_t>(rows * qrow) * sizeof(float)));
-            }
+            void* qdst = dtype == CSAIDX_DTYPE_BF16
+                             ? static_cast<void*>(slab[o % kSlabs].as<float>() + b * rows * qrow)
+                             : static_cast<void*>(q.as<float>() + lrow * qrow);
+            check(csaidx_cuda_copy(e, qdst, in.q + qoff, static_cast<size_t>(rows * qrow) * sizeof(float)));
             check(csaidx_cuda_copy(e, w.as<float>() + lrow * dims.heads, in.w + woff,
                                    static_cast<size_t>(rows * dims.heads) * sizeof(float)));
         }
         check(csaidx_engine_signal(e, static_cast<int>(o % 32)));
+    };
+    auto convert = [&](size_t o) {  // on the main lane, after chunk o's copy
+        if (dtype != CSAIDX_DTYPE_BF16) return;
+        const size_t c = plan.order[o];
+        const int64_t rows = std::min(plan.cs, dims.seq_len - plan.starts[c]);
+        for (int64_t b = 0; b < B; ++b) {
+            const int64_t lrow = b * out_rows + plan.out_row0[c];
+            check(csaidx_cuda_to_bf16(e, slab[o % kSlabs].as<float>() + b * rows * qrow,
+                                      q.as<uint16_t>() + lrow * qrow, rows * qrow, strict ? 1 : 0));
+        }
+        check(csaidx_engine_signal(e, kConvDone + static_cast<int>(o % 32)));
     };
     ChunkHooks hooks;
     hooks.before = [&](size_t o) {
@@ -331,11 +346,12 @@ void run_chunked_rows_view(const HostView& in, const ProblemDims& dims, const Dr
             } else {
                 kc.upload(in.kc, static_cast<size_t>(dims.kc_elems()) * sizeof(float));
             }
-            upload_chunk(0);
+            upload_raw(0);
         }
-        if (o + 1 < plan.order.size()) upload_chunk(o + 1);
+        if (o + 1 < plan.order.size()) upload_raw(o + 1);
         check(csaidx_engine_use_lane(e, kMainLane));
         check(csaidx_engine_await(e, static_cast<int>(o % 32)));
+        convert(o);
     };
     hooks.after = [&](size_t o) {
         const size_t c = plan.order[o];
