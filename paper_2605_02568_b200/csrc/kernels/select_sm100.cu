@@ -53,7 +53,12 @@ constexpr int kMaxCand = 8192;    // largest shared candidate list
 constexpr int kGatherPer = 16;     // survivors per thread the fused gather handles (4096)
 constexpr int kSampleSegs = 64;    // 512-byte segments: <= 8192 sampled keys per row
 
-constexpr int kFinBins = 1024;   // value-linear buckets of the bucket finish
+#ifndef CSAIDX_FIN_BINS
+#define CSAIDX_FIN_BINS 1024
+#endif
+constexpr int kFinBins = CSAIDX_FIN_BINS;  // value-linear buckets of the bucket finish
+// histogram region: the threshold's kBins bins, or the finish's start + cur
+constexpr int kHistWords = 2 * kFinBins > kBins ? 2 * kFinBins : kBins;
 constexpr int kMaxBucket = 128;  // largest bucket the finish ranks pairwise
 
 struct Layout {
@@ -78,7 +83,7 @@ __host__ __device__ inline Layout layout_for(int k) {
 
 __host__ __device__ inline size_t smem_bytes_for(int k) {
     const Layout l = layout_for(k);
-    return static_cast<size_t>(l.cand_cap + l.buf_cap) * sizeof(uint64_t) + kBins * sizeof(uint32_t) +
+    return static_cast<size_t>(l.cand_cap + l.buf_cap) * sizeof(uint64_t) + kHistWords * sizeof(uint32_t) +
            (4 * kWarps + 16) * sizeof(uint32_t);
 }
 
@@ -629,7 +634,7 @@ __device__ __forceinline__ void select_row(const SelectParams& p, int b, int64_t
     uint64_t* cand = reinterpret_cast<uint64_t*>(smem_raw);  // [cand_cap]
     uint64_t* buf = cand + L.cand_cap;                       // [buf_cap]
     uint32_t* hist = reinterpret_cast<uint32_t*>(buf + L.buf_cap);
-    uint32_t* wtot = hist + kBins;                           // [2][2*kWarps]
+    uint32_t* wtot = hist + kHistWords;                           // [2][2*kWarps]
     uint32_t* wsum = wtot + 4 * kWarps;                      // [kWarps] (find_bin)
     uint32_t* res = wsum + kWarps;                           // [8]
     uint32_t* counter = res + 4;
@@ -796,7 +801,7 @@ __device__ __forceinline__ void select_row(const SelectParams& p, int b, int64_t
             const int64_t step = kUnroll * static_cast<int64_t>(kThreads);
             const int64_t n4r = (n4 + step - 1) / step * step;
             const uint32_t cap = static_cast<uint32_t>(
-                min(L.cand_cap, 2 * L.buf_cap + kBins));  // idx list capacity
+                min(L.cand_cap, 2 * L.buf_cap + kHistWords));  // idx list capacity
             for (int64_t it = gtid(); it < n4r; it += step) {
                 float4 v[kUnroll];
 #pragma unroll
