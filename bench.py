@@ -282,12 +282,15 @@ def main():
             n = min(slice_rows, max_rows - r0)
             part = send[:, r0:r0 + n].contiguous()
             if backend == "nccl":
-                dst = [gathered[r, :, r0:r0 + n] for r in range(world)] if rank == 0 else None
                 if rank == 0:
-                    bufs = [torch.empty_like(part) for _ in range(world)]
-                    dist.gather(part, bufs, dst=0)
-                    for r in range(world):
-                        dst[r].copy_(bufs[r])
+                    dst = [gathered[r, :, r0:r0 + n] for r in range(world)]
+                    if all(t.is_contiguous() for t in dst):  # B = 1: receive in place
+                        dist.gather(part, dst, dst=0)
+                    else:
+                        bufs = [torch.empty_like(part) for _ in range(world)]
+                        dist.gather(part, bufs, dst=0)
+                        for r in range(world):
+                            dst[r].copy_(bufs[r])
                 else:
                     dist.gather(part, None, dst=0)
             else:
