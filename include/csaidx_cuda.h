@@ -80,6 +80,12 @@ int csaidx_engine_await(csaidx_engine* e, int slot);
 /* Host-side wait for the slot's latest signal (e.g. before reusing a pinned
  * staging buffer whose copy was enqueued before the signal). */
 int csaidx_engine_sync_slot(csaidx_engine* e, int slot);
+/* The current lane waits (on the device) for all work enqueued so far on
+ * `stream` (a cudaStream_t; NULL = the legacy default stream, which itself
+ * orders after every blocking stream). The device-pointer driver entries
+ * call it with NULL on entry, so operands produced on the default stream
+ * need no host synchronisation before the call. */
+int csaidx_engine_await_stream(csaidx_engine* e, void* stream);
 int csaidx_engine_num_sms(csaidx_engine* e, int* num_sms);
 /* SM partition for running a select beside the score kernel: score launches
  * use at most score_sms CTAs (one per SM) and select launches run as
@@ -155,6 +161,15 @@ int csaidx_cuda_score_rows(csaidx_engine* e, const void* q, const void* kc, int 
                            const csaidx_dims* dims, int64_t s0, int64_t rows, int64_t t0, int64_t cols,
                            int mode, int kernel, int apply_mask, float* out, int64_t ld,
                            int64_t op_rows, int64_t op_row0);
+/* csaidx_cuda_score_rows on the tcgen05 path that also writes, per row, the
+ * maximum legal score of every 32-key group: gmax[(b * rows + i) * gmax_ld +
+ * j / 32] (-inf when the group has no legal key; gmax_ld >= ceil(cols/32)).
+ * A select given these maxima (csaidx_cuda_select_final's gmax) reads only
+ * the groups that can hold a top-k score on long rows: two-level select. */
+int csaidx_cuda_score_gmax(csaidx_engine* e, const void* q_bf16, const void* kc_bf16, const float* w,
+                           const csaidx_dims* dims, int64_t s0, int64_t rows, int64_t t0, int64_t cols,
+                           float* out, int64_t ld, int64_t op_rows, int64_t op_row0,
+                           float* gmax, int64_t gmax_ld);
 /* 1 when csaidx_cuda_score would take the tcgen05 path for these arguments. */
 int csaidx_cuda_score_uses_tensor_cores(const csaidx_dims* dims, int dtype, int mode, int kernel);
 
@@ -217,11 +232,13 @@ int csaidx_cuda_select_from_candidates(csaidx_engine* e, const float* scores, in
  * all-sentinel TopKBuffer is a copy, so each row's exact top-min(k, n) goes
  * straight to out_idx/out_val[b, out_row0 + i, 0..k) (int64, fp32), sorted
  * under succ, the rest (-inf, -1). pass_bits: optional candidate bitmap of
- * csaidx_cuda_score_filtered (NULL = stream the scores). Replaces
+ * csaidx_cuda_score_filtered (NULL = stream the scores); gmax: optional group
+ * maxima of csaidx_cuda_score_gmax (NULL = one-level select). Replaces
  * select + finalize (two launches and the int32 run buffer round trip). */
 int csaidx_cuda_select_final(csaidx_engine* e, const float* scores, int64_t batch, int64_t rows,
                              int64_t ld, int64_t cols, int64_t s0, int64_t t0, int64_t ratio,
                              int64_t k, const uint32_t* pass_bits, int64_t bits_ld,
+                             const float* gmax, int64_t gmax_ld,
                              int64_t* out_idx, float* out_val, int64_t out_rows, int64_t out_row0);
 
 /* merge_topk / overwrite_topk (topk.hpp:73-82, topk.cpp:134-191) over nrows

@@ -93,6 +93,7 @@ CUDA_SYMBOLS = {
     "csaidx_engine_signal": (c_int, [c_void_p, c_int]),
     "csaidx_engine_await": (c_int, [c_void_p, c_int]),
     "csaidx_engine_sync_slot": (c_int, [c_void_p, c_int]),
+    "csaidx_engine_await_stream": (c_int, [c_void_p, c_void_p]),
     "csaidx_engine_set_partition": (c_int, [c_void_p, c_int, c_int]),
     "csaidx_cuda_select_overlap_capable": (c_int, [c_int64]),
     "csaidx_cuda_alloc": (c_int, [c_void_p, c_size_t, POINTER(c_void_p)]),
@@ -146,7 +147,12 @@ CUDA_SYMBOLS = {
     "csaidx_cuda_select_final": (
         c_int,
         [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64,
-         c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int64],
+         c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int64],
+    ),
+    "csaidx_cuda_score_gmax": (
+        c_int,
+        [c_void_p, c_void_p, c_void_p, c_void_p, POINTER(Dims), c_int64, c_int64, c_int64, c_int64,
+         c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64],
     ),
     "csaidx_cuda_merge": (
         c_int,

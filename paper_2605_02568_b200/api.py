@@ -387,6 +387,11 @@ def run_chunked_device(q, kc, w, dims: ProblemDims, config: DriverConfig, chunk_
     import torch
 
     dtype = _capi.DTYPE_BF16 if q.dtype == torch.bfloat16 else _capi.DTYPE_F32
+    # the entry orders itself after the legacy default stream; work on a
+    # torch side stream has to be complete first
+    cur = torch.cuda.current_stream(q.device)
+    if cur.cuda_stream != 0:
+        cur.synchronize()
     starts = None
     n_chunks = 0
     rows = dims.seq_len

@@ -87,6 +87,7 @@ struct csaidx_engine {
     cudaStream_t main_stream = nullptr;
     int lane = 0;
     cudaEvent_t slots[192] = {};
+    cudaEvent_t entry_event = nullptr;  // csaidx_engine_await_stream
     // SM partition while a select runs beside the score kernel (0 = whole GPU)
     int score_sms = 0;
     int select_sms = 0;
@@ -225,6 +226,7 @@ int csaidx_engine_destroy(csaidx_engine* e) {
         if (e->lanes[i]) cudaStreamDestroy(e->lanes[i]);
     for (cudaEvent_t ev : e->slots)
         if (ev) cudaEventDestroy(ev);
+    if (e->entry_event) cudaEventDestroy(e->entry_event);
     if (e->own_stream) cudaStreamDestroy(e->own_stream);
     delete e;
     return CSAIDX_OK;
@@ -272,6 +274,17 @@ int csaidx_engine_sync_slot(csaidx_engine* e, int slot) {
     if (slot < 0 || slot >= 192) return fail(CSAIDX_INVALID_ARGUMENT, "event slot out of range");
     if (e->slots[slot] == nullptr) return CSAIDX_OK;
     CSAIDX_CUDA_TRY(cudaEventSynchronize(e->slots[slot]), "cudaEventSynchronize");
+    return CSAIDX_OK;
+}
+
+int csaidx_engine_await_stream(csaidx_engine* e, void* stream) {
+    if (int rc = set_device(e)) return rc;
+    cudaStream_t src = stream == nullptr ? cudaStreamLegacy : static_cast<cudaStream_t>(stream);
+    if (src == e->stream) return CSAIDX_OK;
+    if (e->entry_event == nullptr)
+        CSAIDX_CUDA_TRY(cudaEventCreateWithFlags(&e->entry_event, cudaEventDisableTiming), "cudaEventCreate");
+    CSAIDX_CUDA_TRY(cudaEventRecord(e->entry_event, src), "cudaEventRecord(await_stream)");
+    CSAIDX_CUDA_TRY(cudaStreamWaitEvent(e->stream, e->entry_event, 0), "cudaStreamWaitEvent(await_stream)");
     return CSAIDX_OK;
 }
 
@@ -490,7 +503,8 @@ namespace {
 // score_tc launch shared by the plain, sampled and filtered entry points.
 int launch_tc(csaidx_engine* e, const void* q, const void* kc, const float* w, const csaidx_dims* d, int64_t s0,
               int64_t rows, int64_t t0, int64_t cols, int apply_mask, float* out, int64_t ld, int kt_stride,
-              const float* tau, uint32_t* pass_bits, int64_t bits_ld, int64_t op_rows = -1, int64_t op_row0 = -1) {
+              const float* tau, uint32_t* pass_bits, int64_t bits_ld, int64_t op_rows = -1, int64_t op_row0 = -1,
+              float* gmax = nullptr, int64_t gmax_ld = 0) {
     if (op_rows < 0) {
         op_rows = d->seq_len;
         op_row0 = s0;
@@ -521,6 +535,8 @@ int launch_tc(csaidx_engine* e, const void* q, const void* kc, const float* w, c
     p.tau = tau;
     p.pass_bits = pass_bits;
     p.bits_ld = bits_ld;
+    p.gmax = gmax;
+    p.gmax_ld = gmax_ld;
     p.probe = e->score_probe;
     LaunchScope ls(e, CSAIDX_KIND_SCORE);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_score_tc(qmap, kmap, p, e->score_sms > 0 ? e->score_sms : e->num_sms,
@@ -654,6 +670,22 @@ int csaidx_cuda_score_rows(csaidx_engine* e, const void* q, const void* kc, int 
     return CSAIDX_OK;
 }
 
+int csaidx_cuda_score_gmax(csaidx_engine* e, const void* q_bf16, const void* kc_bf16, const float* w,
+                           const csaidx_dims* d, int64_t s0, int64_t rows, int64_t t0, int64_t cols, float* out,
+                           int64_t ld, int64_t op_rows, int64_t op_row0, float* gmax, int64_t gmax_ld) {
+    if (int rc = set_device(e)) return rc;
+    if (int rc = check_tile(d, s0, rows, t0, cols)) return rc;
+    if (!csaidx_cuda_score_uses_tensor_cores(d, CSAIDX_DTYPE_BF16, CSAIDX_MODE_FP32, CSAIDX_KERNEL_AUTO))
+        return fail(CSAIDX_INVALID_ARGUMENT, "score_gmax: tensor-core shape only");
+    if (ld < cols || (ld % 4) != 0) return fail(CSAIDX_INVALID_ARGUMENT, "score: ld must be >= cols and a multiple of 4");
+    if (op_rows < 1 || op_row0 < 0 || op_row0 + rows > op_rows)
+        return fail(CSAIDX_INVALID_ARGUMENT, "score: operand rows [op_row0, op_row0 + rows) outside op_rows");
+    if (gmax == nullptr || gmax_ld < (cols + 31) / 32)
+        return fail(CSAIDX_INVALID_ARGUMENT, "score_gmax: gmax_ld < ceil(cols / 32)");
+    return launch_tc(e, q_bf16, kc_bf16, w, d, s0, rows, t0, cols, 1, out, ld, 1, nullptr, nullptr, 0, op_rows, op_row0,
+                     gmax, gmax_ld);
+}
+
 int csaidx_cuda_bool_mask(csaidx_engine* e, uint8_t* keep, int64_t s0, int64_t t0, int64_t rows, int64_t cols,
                           int64_t ratio) {
     if (int rc = set_device(e)) return rc;
@@ -686,7 +718,7 @@ namespace {
 int select_impl(csaidx_engine* e, const float* scores, int64_t batch, int64_t rows, int64_t ld, int64_t cols,
                 int64_t s0, int64_t t0, int64_t ratio, int apply_mask, int64_t k, float* cand_val, int32_t* cand_idx,
                 int64_t cand_ld, const uint32_t* pass_bits, int64_t bits_ld, int64_t* final_idx = nullptr,
-                int64_t final_rows = 0, int64_t final_row0 = 0) {
+                int64_t final_rows = 0, int64_t final_row0 = 0, const float* gmax = nullptr, int64_t gmax_ld = 0) {
     if (int rc = set_device(e)) return rc;
     if (k < 1) return fail(CSAIDX_INVALID_ARGUMENT, "tile_topk: top_k must be >= 1");
     if (rows < 1 || cols < 1 || batch < 1 || ratio < 1) return fail(CSAIDX_INVALID_ARGUMENT, "select: bad extents");
@@ -721,6 +753,8 @@ int select_impl(csaidx_engine* e, const float* scores, int64_t batch, int64_t ro
     p.final_rows = final_rows;
     p.final_row0 = final_row0;
     p.persistent_ctas = e->select_sms;
+    p.gmax = gmax;
+    p.gmax_ld = gmax_ld;
     LaunchScope ls(e, CSAIDX_KIND_SELECT);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_select(p, e->stream), "select");
     return CSAIDX_OK;
@@ -750,14 +784,17 @@ int csaidx_cuda_select_from_candidates(csaidx_engine* e, const float* scores, in
 
 int csaidx_cuda_select_final(csaidx_engine* e, const float* scores, int64_t batch, int64_t rows, int64_t ld,
                              int64_t cols, int64_t s0, int64_t t0, int64_t ratio, int64_t k, const uint32_t* pass_bits,
-                             int64_t bits_ld, int64_t* out_idx, float* out_val, int64_t out_rows, int64_t out_row0) {
+                             int64_t bits_ld, const float* gmax, int64_t gmax_ld, int64_t* out_idx, float* out_val,
+                             int64_t out_rows, int64_t out_row0) {
     if (out_idx == nullptr || out_val == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "select_final: null output");
     if (out_row0 < 0 || out_row0 + rows > out_rows)
         return fail(CSAIDX_INVALID_ARGUMENT, "select_final: rows out of range");
     if (pass_bits != nullptr && bits_ld < csaidx_cuda_candidate_words(cols))
         return fail(CSAIDX_INVALID_ARGUMENT, "select_final: bits_ld < csaidx_cuda_candidate_words(cols)");
+    if (gmax != nullptr && gmax_ld < (cols + 31) / 32)
+        return fail(CSAIDX_INVALID_ARGUMENT, "select_final: gmax_ld < ceil(cols / 32)");
     return select_impl(e, scores, batch, rows, ld, cols, s0, t0, ratio, 1, k, out_val, nullptr, k, pass_bits, bits_ld,
-                       out_idx, out_rows, out_row0);
+                       out_idx, out_rows, out_row0, gmax, gmax_ld);
 }
 
 int csaidx_cuda_merge(csaidx_engine* e, float* run_val, int32_t* run_idx, int64_t nrows, int64_t k,

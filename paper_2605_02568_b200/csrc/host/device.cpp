@@ -108,6 +108,14 @@ void DeviceBuffer::upload(const void* host, size_t bytes) { check(csaidx_cuda_co
 
 void DeviceBuffer::download(void* host, size_t bytes) const { check(csaidx_cuda_copy(e_, host, ptr_, bytes)); }
 
+bool two_level_enabled() {
+    // Off by default (CSAIDX_TWO_LEVEL=1 enables): at C4 the select drops
+    // 22.4 -> 15.0 ms but the group-max epilogue costs the score kernel
+    // 210 -> 227 ms (profiles/r01_ncu_history.md).
+    const char* v = std::getenv("CSAIDX_TWO_LEVEL");
+    return v != nullptr && std::string(v) == "1";
+}
+
 int select_overlap_sms() {
     // Off by default: measured slower at C3 (profiles/r01_ncu_history.md) —
     // the score kernel loses more than the SMs it gives up once a select

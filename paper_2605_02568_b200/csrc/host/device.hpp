@@ -59,6 +59,8 @@ bool prefilter_enabled();
 // SMs given to the select while it runs beside the next chunk's score kernel
 // (CSAIDX_SELECT_SMS; default 0 = no overlap: each select uses the GPU).
 int select_overlap_sms();
+// Two-level select for long rows (CSAIDX_TWO_LEVEL, default on).
+bool two_level_enabled();
 constexpr int64_t kPrefilterSampleTiles = 16;
 
 int kernel_code(ScoreKernel kernel);  // throws like resolve_score_kernel for unavailable kernels

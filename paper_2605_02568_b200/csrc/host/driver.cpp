@@ -104,6 +104,18 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
     const bool overlap = plan.ct >= T && !prefilter && !config.bool_mask_tile && plan.order.size() >= 2 &&
                          csaidx_cuda_score_uses_tensor_cores(&cd, ops.dtype, mcode, kcode) != 0 &&
                          csaidx_cuda_select_overlap_capable(k) != 0 && select_overlap_sms() > 0;
+    // Two-level select (csaidx_cuda_score_gmax): when rows can span >= 4k
+    // 32-key groups the score epilogue also writes each group's maximum, and
+    // the select reads only the ~k groups that can hold a top-k score
+    // (CSAIDX_TWO_LEVEL=0 disables).
+    const bool two_level = plan.ct >= T && !prefilter && !config.bool_mask_tile && two_level_enabled() &&
+                           csaidx_cuda_score_uses_tensor_cores(&cd, ops.dtype, mcode, kcode) != 0 &&
+                           ceil_div(plan.ct, 32) >= 4 * k;
+    const int64_t gmax_ld = ceil_div(plan.ct, 32);
+    DeviceBuffer gmax_buf[2];  // double buffered like the score tiles when the select runs beside the score
+    if (two_level)
+        for (int i = 0; i < (overlap ? 2 : 1); ++i)
+            gmax_buf[i] = DeviceBuffer(e, static_cast<size_t>(B * plan.cs * gmax_ld) * sizeof(float));
     DeviceBuffer scores2;
     struct PartitionGuard {
         csaidx_engine* e = nullptr;
@@ -124,6 +136,7 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
     for (size_t o = 0; o < plan.order.size(); ++o) {
         const size_t c = plan.order[o];
         float* const sbuf = overlap && (o & 1) ? scores2.as<float>() : scores.as<float>();
+        float* const gbuf = two_level ? gmax_buf[overlap ? (o & 1) : 0].as<float>() : nullptr;
         // (overlap) the buffer was last read by chunk o-2's select
         if (overlap && o >= 2) check(csaidx_engine_await(e, kSelectDone + static_cast<int>((o - 2) % 32)));
         const int64_t s0 = plan.starts[c];
@@ -168,6 +181,9 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
                 LedgerCharge mask_charge(ledger, "mask_tile", static_cast<uint64_t>(rows) * static_cast<uint64_t>(cols));
                 check(csaidx_cuda_bool_mask(e, keep.as<uint8_t>(), s0, t0, rows, cols, dims.ratio));
                 check(csaidx_cuda_apply_bool_mask(e, sbuf, ld, keep.as<uint8_t>(), B, rows, cols));
+            } else if (two_level) {
+                check(csaidx_cuda_score_gmax(e, ops.q, ops.kc, ops.w, &cd, s0, rows, t0, cols, sbuf, ld, op_rows, op_row0,
+                                             gbuf, gmax_ld));
             } else {
                 check(csaidx_cuda_score_rows(e, ops.q, ops.kc, ops.dtype, ops.w, &cd, s0, rows, t0, cols, mcode, kcode,
                                              1, sbuf, ld, op_rows, op_row0));
@@ -192,8 +208,9 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
                     check(csaidx_engine_await(e, kScoreDone + static_cast<int>(o % 32)));
                 }
                 check(csaidx_cuda_select_final(e, sbuf, B, rows, ld, cols, s0, t0, dims.ratio, k,
-                                               filtered ? pf_bits.as<uint32_t>() : nullptr, bits_ld, out_idx, out_val,
-                                               out_rows, plan.out_row0[c]));
+                                               filtered ? pf_bits.as<uint32_t>() : nullptr, bits_ld,
+                                               gbuf, two_level ? gmax_ld : 0,
+                                               out_idx, out_val, out_rows, plan.out_row0[c]));
                 if (overlap) check(csaidx_engine_signal(e, kSelectDone + static_cast<int>(o % 32)));
                 finalized = true;
             } else if (first && width == k) {
@@ -453,6 +470,8 @@ void run_chunked_device(const DeviceOperands& ops, const ProblemDims& dims, cons
         throw std::invalid_argument("run_chunked_device: operand dtype does not match the selected score kernel");
     std::lock_guard<std::mutex> lock(detail::engine_mutex());
     csaidx_engine* e = detail::engine();
+    // the operands were produced by the caller's (default-stream) work
+    detail::check(csaidx_engine_await_stream(e, nullptr));
     RunStats stats;
     detail::run_plan(e, detail::DeviceOps{ops.q, ops.kc, ops.w, ops.dtype, ops.local_rows ? out_rows : 0}, dims,
                      config, plan, out_indices, out_values, out_rows, ledger, stats);

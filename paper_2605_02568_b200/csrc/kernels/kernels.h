@@ -36,6 +36,11 @@ struct ScoreTcParams {
     const float* tau;
     uint32_t* pass_bits;
     int64_t bits_ld;
+    // Optional group maxima (two-level select): gmax[(b*rows + r) * gmax_ld +
+    // j / 32] = max of the legal scores of key columns [32 (j/32), +32) of
+    // row r (-inf when none is legal).
+    float* gmax;
+    int64_t gmax_ld;
     // Optional profiling counters, [grid][8] clock64 cycles: MMA waits on
     // k_full / acc_empty / q_full, MMA span, epilogue (warp 4) wait on
     // acc_full, epilogue span, producer waits on k_empty / q_empty.
@@ -94,6 +99,11 @@ struct SelectParams {
     // int64 indices; entries past min(k, n) are (-inf, -1).
     int64_t* final_idx;
     int64_t final_rows, final_row0;
+    // Optional group maxima of the rows (ScoreTcParams::gmax): rows whose
+    // legal length spans many more groups than k take the two-level path
+    // (read the maxima, then only the groups that can hold a top-k score).
+    const float* gmax;
+    int64_t gmax_ld;
     // > 0: run as that many persistent CTAs, one per SM, each with several
     // row groups (to share the GPU with a concurrently running score kernel)
     int persistent_ctas;

@@ -211,7 +211,8 @@ __device__ __forceinline__ float2 head_reduce_tmem2(uint32_t taddr0, uint32_t ta
 
 // Instances: kMode 0 = plain masked score tile (production), 1 = strided
 // key-tile sample (kt_stride > 1), 2 = plain + candidate bitmap against tau
-// (the fused select pre-filter, CSAIDX_SELECT_PREFILTER=1); kProbe adds the
+// (the fused select pre-filter, CSAIDX_SELECT_PREFILTER=1), 3 = plain +
+// per-32-key group maxima (two-level select for long rows); kProbe adds the
 // per-role wait-cycle counters (dev). The production instance carries none
 // of the optional code.
 template <int kMode, bool kProbe>
@@ -240,6 +241,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 
     const int warp = threadIdx.x / 32;
     constexpr bool kFilter = kMode == 2;
+    constexpr bool kGmax = kMode == 3;
     long long* const probe = kProbe ? p.probe : nullptr;  // per-CTA wait-cycle counters (profiling)
     const int64_t kts = kMode == 1 ? p.kt_stride : 1;  // key-tile stride (sample mode)
 
@@ -469,25 +471,49 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                     mbar_wait(&acc_full[a], par);
                     if (probe) ew_acc += clock64() - c0;
                     tc_fence_after();
-                    float2 pair_acc = make_float2(0.f, 0.f);
+                    // Drain the accumulator into registers, release it to the MMA
+                    // warp, then do the stores (and mode epilogues) off its
+                    // critical path.
+                    float accv[kPerUnit];
                     if (kPerUnit == 2 && wq[1] < it.nrows) {  // both queries of the accumulator at once
                         const uint32_t col = a * kUmmaN;
-                        pair_acc = head_reduce_tmem2(quarter_taddr + col, quarter_taddr + col + kHeads,
-                                                     w_item + wq[0] * kHeads, w_item + wq[1] * kHeads);
+                        const float2 pr = head_reduce_tmem2(quarter_taddr + col, quarter_taddr + col + kHeads,
+                                                            w_item + wq[0] * kHeads, w_item + wq[1] * kHeads);
+                        accv[0] = pr.x;
+                        accv[kPerUnit - 1] = pr.y;
+                    } else {
+#pragma unroll
+                        for (int pu = 0; pu < kPerUnit; ++pu) {
+                            const int qi = wq[un * kPerUnit + pu];
+                            accv[pu] = qi < it.nrows  // warp-uniform
+                                           ? head_reduce_tmem(quarter_taddr + a * kUmmaN + (qi % kQPerGroup) * kHeads,
+                                                              w_item + qi * kHeads)
+                                           : 0.f;
+                        }
                     }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&acc_empty[a]);
 #pragma unroll
                     for (int pu = 0; pu < kPerUnit; ++pu) {
                         const int u = un * kPerUnit + pu;
                         const int qi = wq[u];
                         if (qi < it.nrows) {  // warp-uniform
-                            const uint32_t col = a * kUmmaN + (qi % kQPerGroup) * kHeads;
-                            const float acc = (kPerUnit == 2 && wq[1] < it.nrows)
-                                                  ? (pu == 0 ? pair_acc.x : pair_acc.y)
-                                                  : head_reduce_tmem(quarter_taddr + col, w_item + qi * kHeads);
+                            const float acc = accv[pu];
                             const bool legal = j < lim[u];
                             if (jo < out_cols) {
                                 if (legal && !isfinite(acc)) atomicOr(p.nonfinite, 1);
                                 orow[u][jo] = legal ? acc : neg_inf;
+                            }
+                            if (kGmax) {
+                                // max over the warp's 32 key columns: one redux.sync on
+                                // the order-preserving integer key
+                                const uint32_t gk = __reduce_max_sync(
+                                    0xffffffffu, ord_key((legal && jo < out_cols) ? acc : neg_inf));
+                                if (lane == 0 && jo < out_cols) {
+                                    const int64_t grow = static_cast<int64_t>(it.b) * p.rows + it.r0 + qi;
+                                    p.gmax[grow * p.gmax_ld + (jo >> 5)] = ord_key_to_float(gk);
+                                }
                             }
                             if (kFilter) {
                                 // fused select pre-filter: one candidate word per
@@ -500,9 +526,6 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                             }
                         }
                     }
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&acc_empty[a]);
                     ++aiter;
                 }
             }
@@ -629,7 +652,7 @@ cudaError_t launch_score_tc(const CUtensorMap& qmap, const CUtensorMap& kmap, Sc
     static bool attr_set = false;
     if (!attr_set) {
         for (auto* fn : {score_tc_kernel<0, false>, score_tc_kernel<0, true>, score_tc_kernel<1, false>,
-                         score_tc_kernel<2, false>}) {
+                         score_tc_kernel<2, false>, score_tc_kernel<3, false>}) {
             cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  static_cast<int>(kSmemBytes));
             if (e != cudaSuccess) return e;
@@ -639,6 +662,8 @@ cudaError_t launch_score_tc(const CUtensorMap& qmap, const CUtensorMap& kmap, Sc
     const int grid = p.nitems < num_sms ? p.nitems : num_sms;
     if (p.tau != nullptr)
         score_tc_kernel<2, false><<<grid, kNumThreads, kSmemBytes, stream>>>(qmap, kmap, p);
+    else if (p.gmax != nullptr)
+        score_tc_kernel<3, false><<<grid, kNumThreads, kSmemBytes, stream>>>(qmap, kmap, p);
     else if (p.kt_stride > 1)
         score_tc_kernel<1, false><<<grid, kNumThreads, kSmemBytes, stream>>>(qmap, kmap, p);
     else if (p.probe != nullptr)

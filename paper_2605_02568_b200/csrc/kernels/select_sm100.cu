@@ -48,9 +48,13 @@ __device__ __forceinline__ void csync() {
     asm volatile("bar.sync %0, %1;" ::"r"(1 + gidx()), "n"(kThreads) : "memory");
 }
 constexpr int kBins = 2048;
+constexpr int kMaxRowGroups = 4;  // row groups per CTA (select_fat_kernel uses kFatGroups)
 constexpr int kMaxTake = 4096;    // largest min(k, n) a row may select
 constexpr int kMaxCand = 8192;    // largest shared candidate list
 constexpr int kGatherPer = 16;     // survivors per thread the fused gather handles (4096)
+// two-level select only pays when a row spans many more 32-key groups than
+// k (it reads ~k groups instead of the whole row)
+constexpr int kTwoLevelMinGroupsPerK = 2;
 constexpr int kSampleSegs = 64;    // 512-byte segments: <= 8192 sampled keys per row
 
 #ifndef CSAIDX_FIN_BINS
@@ -227,7 +231,10 @@ __device__ void find_bin(const uint32_t* hist, int nbins, uint32_t kk, uint32_t*
 // of a row and share their leading bits); usually two 11-bit passes.
 __device__ void smem_take_top(const uint64_t* a, int n, uint32_t kk, uint64_t* dst, uint32_t* hist, uint32_t* res,
                               uint32_t* wsum, uint32_t* counter) {
-    __shared__ unsigned long long s_mm[2];
+    // one min/max pair per row group (the persistent kernel's groups share
+    // the CTA's static shared memory)
+    __shared__ unsigned long long s_mm_all[kMaxRowGroups][2];
+    unsigned long long* s_mm = s_mm_all[gidx()];
     const int lane = gtid() & 31;
     if (gtid() == 0) {
         s_mm[0] = ~0ull;
@@ -689,13 +696,140 @@ __device__ __forceinline__ void select_row(const SelectParams& p, int b, int64_t
                 csync();
             }
         }
+        bool have = false;  // candidates ready in cand[0, count)
         if (pre >= 0) {
             count = pre;
+            have = true;
         } else if (n <= L.cand_cap) {
             for (int64_t i = gtid(); i < n; i += kThreads) cand[i] = composite(ord_key(__ldg(row + i)), i);
             count = static_cast<int>(n);
             csync();
-        } else {
+            have = true;
+        }
+        const int ngroups = static_cast<int>((n + 31) >> 5);
+        if (!have && p.gmax != nullptr && ngroups >= kTwoLevelMinGroupsPerK * k && ngroups <= 2 * L.cand_cap) {
+            // Two-level select: with g_k the k-th largest 32-key group
+            // maximum, at least k scores are >= g_k and every score >= g_k
+            // lies in a group whose maximum is >= g_k. So only those groups
+            // (about k of them) are read, and their entries >= g_k (about
+            // 1.1-1.3 k) are the candidates. A threshold that admits fewer
+            // than `take` or more than the list holds falls through to the
+            // sampled path below (exact either way).
+            const float* gmr = p.gmax + (static_cast<int64_t>(b) * p.rows + row_id) * p.gmax_ld;
+            float* gsm = reinterpret_cast<float*>(cand);  // the row's group maxima
+            if (gtid() == 0) {
+                *counter = 0;
+                res[0] = res[1] = res[2] = 0u;
+                res[6] = 0xffffffffu;
+                res[7] = 0u;
+            }
+            for (int i = gtid(); i < kBins; i += kThreads) hist[i] = 0;
+            uint32_t kmin = 0xffffffffu, kmax = 0u;
+            for (int g = gtid(); g < ngroups; g += kThreads) {
+                const float v = __ldg(gmr + g);
+                gsm[g] = v;
+                const uint32_t key = ord_key(v);
+                kmin = min(kmin, key);
+                kmax = max(kmax, key);
+            }
+            kmin = __reduce_min_sync(0xffffffffu, kmin);
+            kmax = __reduce_max_sync(0xffffffffu, kmax);
+            csync();
+            if (lane == 0) {
+                atomicMin(&res[6], kmin);
+                atomicMax(&res[7], kmax);
+            }
+            csync();
+            const float gmin = ord_key_to_float(res[6]), gmaxv = ord_key_to_float(res[7]);
+            float lo = gmin, hi = gmaxv, tau_g = gmin;
+            uint32_t rr = static_cast<uint32_t>(take);
+#pragma unroll 1
+            for (int pass = 0; pass < 2; ++pass) {
+                const float scale = static_cast<float>(kBins) / (hi - lo);
+                if (!(hi > lo) || !isfinite(scale)) break;
+                if (pass > 0) {
+                    for (int i = gtid(); i < kBins; i += kThreads) hist[i] = 0;
+                    if (gtid() == 0) res[0] = res[1] = res[2] = 0u;
+                    csync();
+                }
+                for (int g = gtid(); g < ngroups; g += kThreads) {
+                    const float v = gsm[g];
+                    if (v >= lo && v <= hi)
+                        atomicAdd(&hist[static_cast<int>(fminf((v - lo) * scale, static_cast<float>(kBins - 1)))], 1u);
+                }
+                csync();
+                find_bin(hist, kBins, rr, res, wsum);
+                const uint32_t bin = res[0], above = res[1], cnt = res[2];
+                csync();
+                const float width = (hi - lo) / static_cast<float>(kBins);
+                const float blo = lo + static_cast<float>(bin) * width;
+                tau_g = blo > lo ? blo : lo;
+                if (cnt * 8u <= rr || cnt <= 4u) break;
+                rr -= above;
+                hi = fminf(hi, blo + width);
+                lo = tau_g;
+            }
+            if (tau_g == 0.f) tau_g = 0.f;  // -0.0 -> +0.0
+            // groups that can hold a score >= tau_g, listed in buf
+            uint32_t* glist = reinterpret_cast<uint32_t*>(buf);
+            const uint32_t gcap = static_cast<uint32_t>(2 * L.buf_cap);
+            for (int g0 = 0; g0 < ngroups; g0 += kThreads) {
+                const int g = g0 + gtid();
+                const bool keep = g < ngroups && gsm[g] >= tau_g;
+                const uint32_t m = __ballot_sync(0xffffffffu, keep);
+                uint32_t base = 0;
+                if (lane == 0 && m != 0) base = atomicAdd(counter, __popc(m));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
+                if (keep && pos < gcap) glist[pos] = static_cast<uint32_t>(g);
+            }
+            csync();
+            const uint32_t ng = *counter;
+            csync();
+            if (ng <= gcap) {
+                // one group (128 B, 8 x float4) per thread in flight; the
+                // survivors' columns go to the list in the histogram region
+                if (gtid() == 0) *counter = 0;
+                csync();
+                uint32_t* idx2 = hist;
+                const uint32_t cap2 = static_cast<uint32_t>(kHistWords);
+                for (uint32_t t = gtid(); t < ng; t += kThreads) {
+                    const uint32_t g = glist[t];
+                    const float4* src = reinterpret_cast<const float4*>(row + static_cast<int64_t>(g) * 32);
+                    float4 v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = __ldg(src + u);
+                    const int64_t lim = n - static_cast<int64_t>(g) * 32;  // valid columns in the group
+                    uint32_t m = 0;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        m |= (v[u].x >= tau_g && 4 * u + 0 < lim ? 1u : 0u) << (4 * u + 0);
+                        m |= (v[u].y >= tau_g && 4 * u + 1 < lim ? 1u : 0u) << (4 * u + 1);
+                        m |= (v[u].z >= tau_g && 4 * u + 2 < lim ? 1u : 0u) << (4 * u + 2);
+                        m |= (v[u].w >= tau_g && 4 * u + 3 < lim ? 1u : 0u) << (4 * u + 3);
+                    }
+                    if (m != 0) {
+                        uint32_t pos = atomicAdd(counter, static_cast<uint32_t>(__popc(m)));
+                        while (m != 0) {
+                            const int bit = __ffs(m) - 1;
+                            m &= m - 1;
+                            if (pos < cap2) idx2[pos] = g * 32 + static_cast<uint32_t>(bit);
+                            ++pos;
+                        }
+                    }
+                }
+                csync();
+                const uint32_t total = *counter;
+                csync();
+                if (total >= static_cast<uint32_t>(take) && total <= cap2) {
+                    count = static_cast<int>(total);
+                    gather_candidates(row, idx2, count, cand, hist, tau_g, gmaxv, prebuilt, pb_lo, pb_scale);
+                    have = true;
+                    if (gtid() == 0 && p.cand_hits != nullptr) atomicAdd(p.cand_hits, 1);
+                }
+            }
+        }
+        if (!have) {
             // 1. sample evenly spaced 512-byte segments (one float4 per lane,
             //    ~1/16 of the row, <= 8192 values), held in registers; each
             //    warp issues all of its loads before consuming them
@@ -887,6 +1021,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) select_kernel(const Sele
 // fat CTA per SM holding kFatGroups independent row groups (each its own
 // shared memory slice and barrier) that walk the rows with a grid stride.
 constexpr int kFatGroups = 3;
+static_assert(kFatGroups <= kMaxRowGroups, "per-group static shared slots");
 
 __global__ void __launch_bounds__(kThreads * kFatGroups, 1) select_fat_kernel(const SelectParams p) {
     extern __shared__ __align__(16) uint8_t smem_raw[];

@@ -88,11 +88,13 @@ class Engine:
     def gen_normal_bf16(self, n: int, stddev: float, seed: int, stream_id: int, offset: int = 0) -> torch.Tensor:
         out = torch.empty(n, dtype=torch.bfloat16, device=f"cuda:{self.device}")
         check(self.lib.csaidx_cuda_gen_normal_bf16(self.handle, _p(out), n, stddev, seed, stream_id, offset))
+        self.check()  # the tensor may be handed to torch or another engine next
         return out
 
     def gen_normal_f32(self, n: int, stddev: float, seed: int, stream_id: int, offset: int = 0) -> torch.Tensor:
         out = torch.empty(n, dtype=torch.float32, device=f"cuda:{self.device}")
         check(self.lib.csaidx_cuda_gen_normal_f32(self.handle, _p(out), n, stddev, seed, stream_id, offset))
+        self.check()
         return out
 
     # ------------------------------------------------------------ hot path
@@ -155,13 +157,28 @@ class Engine:
                                                           _p(idx), width))
         return val, idx
 
-    def select_final(self, scores, batch, rows, cols, s0, t0, ratio, k, out_idx, out_val, out_row0, bits=None):
-        """tile_topk + sentinel pass straight into int64/fp32 output rows [b, out_row0 + i, :k]."""
+    def select_final(self, scores, batch, rows, cols, s0, t0, ratio, k, out_idx, out_val, out_row0, bits=None,
+                     gmax=None):
+        """tile_topk + sentinel pass straight into int64/fp32 output rows [b, out_row0 + i, :k]
+        (gmax: group maxima of score_gmax -> two-level select on long rows)."""
         ld = scores.shape[-1]
         check(self.lib.csaidx_cuda_select_final(self.handle, _p(scores), batch, rows, ld, cols, s0, t0, ratio, k,
-                                                _p(bits) if bits is not None else None,
-                                                bits.shape[-1] if bits is not None else 0, _p(out_idx), _p(out_val),
-                                                out_idx.shape[1], out_row0))
+                                                _p(bits), bits.shape[-1] if bits is not None else 0,
+                                                _p(gmax), gmax.shape[-1] if gmax is not None else 0,
+                                                _p(out_idx), _p(out_val), out_idx.shape[1], out_row0))
+
+    def score_gmax(self, q, kc, w, dims: Dims, s0, rows, t0, cols, fill=None):
+        """Masked tcgen05 score tile + per-32-key group maxima of every row
+        (fill: initial value of both outputs, to expose unwritten entries)."""
+        ld = (cols + 3) // 4 * 4
+        out = torch.empty((dims.batch, rows, ld), dtype=torch.float32, device=q.device)
+        gmax = torch.empty((dims.batch, rows, (cols + 31) // 32), dtype=torch.float32, device=q.device)
+        if fill is not None:
+            out.fill_(fill)
+            gmax.fill_(fill)
+        check(self.lib.csaidx_cuda_score_gmax(self.handle, _p(q), _p(kc), _p(w), byref(dims), s0, rows, t0, cols,
+                                              _p(out), ld, dims.seq_len, s0, _p(gmax), gmax.shape[-1]))
+        return out, gmax
 
     def set_partition(self, score_sms: int, select_sms: int):
         """csaidx_engine_set_partition: score launches on score_sms SMs, selects as

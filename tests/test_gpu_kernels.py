@@ -286,6 +286,67 @@ def test_persistent_multirow_select_equals_per_row_select(engine, cols, k):
     assert np.array_equal(i1.cpu().numpy(), wi)
 
 
+def _v4_dims(S, k, m=4):
+    from paper_2605_02568_b200.engine import dims_struct
+
+    return dims_struct(1, S, 64, 128, m, k)
+
+
+def test_score_gmax_is_the_group_max_of_the_tile(engine):
+    """score_gmax: the tile is the plain score tile bit for bit and gmax[r, g]
+    the max of row r's legal scores in key columns [32 g, 32 g + 32), for every
+    group that overlaps the row's legal prefix (key tiles wholly past the causal
+    limit are skipped and their groups left unwritten; select never reads them)."""
+    S, m = 8192, 4
+    T = S // m
+    q = engine.gen_normal_bf16(S * 64 * 128, 128 ** -0.5, 5, 1)
+    kc = engine.gen_normal_bf16(T * 128, 128 ** -0.5, 5, 2)
+    w = engine.gen_normal_f32(S * 64, (64 * 128) ** -0.5, 5, 3)
+    d = _v4_dims(S, 64)
+    s0, rows, cols = 6000, 100, T
+    plain = engine.score(q, kc, w, d, s0, rows, 0, cols, apply_mask=True)
+    tile, gmax = engine.score_gmax(q, kc, w, d, s0, rows, 0, cols)
+    engine.check()
+    legal = (s0 + np.arange(rows) + 1) // m
+    # key tiles wholly past a row's causal limit may be left unwritten
+    ti, pi = tile[0].view(torch.int32).cpu().numpy(), plain[0].view(torch.int32).cpu().numpy()
+    for r in range(rows):
+        written = min(cols, (int(legal[r]) + 127) // 128 * 128)
+        assert np.array_equal(ti[r, :written], pi[r, :written]), r
+    t = tile[0, :, :cols].cpu().numpy()
+    g = gmax[0].cpu().numpy()
+    for r in range(rows):
+        x = np.where(np.arange(cols) < legal[r], t[r], -np.inf)
+        ref = np.pad(x, (0, g.shape[1] * 32 - cols), constant_values=-np.inf).reshape(-1, 32).max(axis=1)
+        ng = (min(int(legal[r]), cols) + 31) // 32
+        assert np.array_equal(g[r, :ng], ref[:ng].astype(np.float32)), r
+
+
+@pytest.mark.parametrize("k", [64, 100])
+def test_two_level_select_equals_one_level(engine, k):
+    """select_final with group maxima (reads only the groups that can hold a
+    top-k score) gives the one-level select's bytes on real score rows."""
+    S, m = 32768, 4
+    T = S // m
+    q = engine.gen_normal_bf16(S * 64 * 128, 128 ** -0.5, 7, 1)
+    kc = engine.gen_normal_bf16(T * 128, 128 ** -0.5, 7, 2)
+    w = engine.gen_normal_f32(S * 64, (64 * 128) ** -0.5, 7, 3)
+    d = _v4_dims(S, k)
+    s0, rows = S - 300, 300
+    tile, gmax = engine.score_gmax(q, kc, w, d, s0, rows, 0, T)
+    oi1 = torch.full((1, rows, k), 7, dtype=torch.int64, device="cuda")
+    ov1 = torch.zeros((1, rows, k), dtype=torch.float32, device="cuda")
+    oi2, ov2 = oi1.clone(), ov1.clone()
+    drv_hits = engine.candidate_hits(reset=True)
+    engine.select_final(tile, 1, rows, T, s0, 0, m, k, oi1, ov1, 0)
+    engine.check()
+    assert engine.candidate_hits(reset=True) == 0
+    engine.select_final(tile, 1, rows, T, s0, 0, m, k, oi2, ov2, 0, gmax=gmax)
+    engine.check()
+    assert engine.candidate_hits(reset=True) == rows  # every row took the two-level path
+    assert torch.equal(oi1, oi2) and torch.equal(ov1.view(torch.int32), ov2.view(torch.int32))
+
+
 def test_select_all_equal_scores_take_smallest_indices(engine):
     B, rows, cols, k = 1, 3, 10000, 100
     scores = np.zeros((B, rows, cols), np.float32)

@@ -229,6 +229,60 @@ def test_select_beside_score_overlap_is_byte_identical(orc, monkeypatch, sms):
     assert np.array_equal(di.cpu().numpy(), ref.indices)
 
 
+def test_two_level_select_in_the_driver_is_byte_identical(monkeypatch):
+    """Rows spanning >= 4k key groups make the driver score with group maxima
+    and select two-level; CSAIDX_TWO_LEVEL=0 gives the same bytes."""
+    import torch
+
+    from paper_2605_02568_b200.engine import Engine
+
+    e = Engine(0)
+    S, m, k = 65536, 4, 64
+    T = S // m
+    q = e.gen_normal_bf16(S * 64 * 128, 128 ** -0.5, 9, 1)
+    kc = e.gen_normal_bf16(T * 128, 128 ** -0.5, 9, 2)
+    w = e.gen_normal_f32(S * 64, (64 * 128) ** -0.5, 9, 3)
+    dims = api.ProblemDims.create(1, S, m, 64, 128, k)
+    cfg = api.DriverConfig(tile=api.TileConfig(2048, T))
+    starts = [S - 2048, 40960, 8192]
+    monkeypatch.setenv("CSAIDX_TWO_LEVEL", "0")
+    i0, v0, _ = api.run_chunked_device(q, kc, w, dims, cfg, starts)
+    monkeypatch.setenv("CSAIDX_TWO_LEVEL", "1")
+    drv = api.KernelStats(api.driver_engine(0))
+    drv.candidate_hits(reset=True)
+    i1, v1, _ = api.run_chunked_device(q, kc, w, dims, cfg, starts)
+    a, b = i0.cpu().numpy().reshape(-1, k), i1.cpu().numpy().reshape(-1, k)
+    bad = np.argwhere((a != b).any(axis=1)).ravel()
+    detail = [(int(r), a[r][a[r] != b[r]][:4].tolist(), b[r][a[r] != b[r]][:4].tolist()) for r in bad[:3]]
+    assert len(bad) == 0, (len(bad), detail)
+    assert torch.equal(v0.view(torch.int32), v1.view(torch.int32))
+    assert drv.candidate_hits(reset=True) > 2048  # the long rows went two-level
+
+
+def test_device_entry_orders_after_default_stream_work():
+    """csaidx_device_run_chunked waits on the device for the operands' producer
+    on the default stream: a copy queued behind a long sleep is seen."""
+    import torch
+
+    from paper_2605_02568_b200.engine import Engine
+
+    e = Engine(0)
+    S, m, k = 8192, 4, 64
+    T = S // m
+    q_src = e.gen_normal_bf16(S * 64 * 128, 128 ** -0.5, 4, 1)
+    kc = e.gen_normal_bf16(T * 128, 128 ** -0.5, 4, 2)
+    w = e.gen_normal_f32(S * 64, (64 * 128) ** -0.5, 4, 3)
+    dims = api.ProblemDims.create(1, S, m, 64, 128, k)
+    cfg = api.DriverConfig(tile=api.TileConfig(2048, T))
+    want_i, want_v, _ = api.run_chunked_device(q_src, kc, w, dims, cfg)
+    q = torch.zeros_like(q_src)
+    torch.cuda.synchronize()
+    torch.cuda._sleep(200_000_000)  # ~0.1 s on the default stream
+    q.copy_(q_src)                  # the operand is produced after the sleep
+    got_i, got_v, _ = api.run_chunked_device(q, kc, w, dims, cfg)
+    assert torch.equal(want_i, got_i) and torch.equal(want_v.view(torch.int32), got_v.view(torch.int32))
+
+
 def test_ablations_follow_reference_semantics(orc):
     # acceptance.cpp:339-380 directions at a small V4-like shape
     inputs, dims, (q, kc, w) = inputs_for(orc, 1, 2048, 4, 8, 64, 64, 1)
