@@ -410,16 +410,24 @@ def main():
             else:
                 dist.all_reduce(h, op=dist.ReduceOp.MAX)
             e2e_ms = float(h.item())
-        h2d = B * rows * H * D * 4 + B * T * D * 4 + B * rows * H * 4
+        # q crosses PCIe as bf16 when the entry rounds it on the host cores
+        # (CSAIDX_HOST_ROUND, default on), else as the caller's fp32
+        host_round = os.environ.get("CSAIDX_HOST_ROUND", "1") != "0"
+        host_threads = max(1, int(os.environ.get("CSAIDX_HOST_THREADS", (os.cpu_count() or 2) - 1)))
+        h2d = B * rows * H * D * (2 if host_round else 4) + B * T * D * 4 + B * rows * H * 4
         d2h = B * rows * k * 12
         e2e = {"value": (pairs_mine if args.simulate_rank else pairs_total) / (e2e_ms / 1000.0),
                "unit": "legal pairs/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "pcie_gbs": (h2d + d2h) / (e2e_ms / 1000.0) / 1e9,
-               "bound": "PCIe: the fp32 q rows (the reference API's input type) cross the bus once; H2D of "
-                        "chunk c+1 and D2H of chunk c-1 overlap chunk c's kernels",
+               "bound": ("q rows are rounded fp32 -> bf16 on the host cores into pinned slabs (a producer "
+                         "thread runs up to 8 chunks ahead) and cross PCIe once at 2 B/entry; H2D of chunk c+1 "
+                         "and D2H of chunk c-1 overlap chunk c's kernels" if host_round else
+                         "PCIe: the fp32 q rows (the reference API's input type) cross the bus once; H2D of "
+                         "chunk c+1 and D2H of chunk c-1 overlap chunk c's kernels"),
+               "host_rounding": {"on": host_round, "threads": host_threads if host_round else 0},
                "path": "csaidx_host_run_chunked_local (libcsaidx.so C entry of csaidx::run_chunked over this "
-                       "rank's rows), pinned fp32 host operands, H2D/D2H inside the timed region"}
+                       "rank's rows), pinned fp32 host operands, host rounding + H2D/D2H inside the timed region"}
         # cheap end-to-end correctness guard: the host API must agree with the resident run
         assert torch.equal(oi, out_idx.cpu()), "host-API result differs from the device-resident run"
 
@@ -454,7 +462,7 @@ def main():
                        "dense_pairs_per_s": B * S * T / (ms / 1000.0)},
             "hbm_peak_gb": hbm_peak / 1e9,
             "ledger_peak_bytes": st.ledger_peak_bytes,
-            "roofline": {"bound": "tensor", "kernel": "score_tc_kernel (tcgen05 kind::f16, M=128 keys x N=256 q-heads)",
+            "roofline": {"bound": "tensor", "kernel": "score_tc_kernel (tcgen05 kind::f16, M=128 keys x N=128 = 2 queries x 64 heads)",
                          "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
                          "frac": (achieved_tflops / peak_tflops) if achieved_tflops else None,
                          "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",

@@ -138,6 +138,13 @@ int csaidx_host_choose_path(const csaidx_dims* dims, uint64_t threshold, int* pa
                             uint64_t* predicted);
 int64_t csaidx_host_t_legal(int64_t t, int64_t ratio);
 int64_t csaidx_host_k_eff(int64_t t, int64_t ratio, int64_t top_k);
+/* The host rounding of the pipelined entry (csaidx_host_run_chunked*):
+ * fp32 -> bf16, round to nearest even (bit-identical to the device's
+ * csaidx_cuda_to_bf16 for finite inputs), on the host worker pool
+ * (CSAIDX_HOST_THREADS). Flags: any non-finite entry / any entry that is not
+ * bf16-representable (the checks of IndexerInputs::validated,
+ * types.cpp:73-92, and of strict mode). */
+int csaidx_host_round_bf16(const float* src, uint16_t* dst, uint64_t n, int* nonfinite, int* inexact);
 
 #ifdef __cplusplus
 }

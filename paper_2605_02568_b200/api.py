@@ -114,6 +114,7 @@ HOST_SYMBOLS = {
     "csaidx_host_choose_path": (c_int, [POINTER(Dims), c_uint64, POINTER(c_int), POINTER(c_uint64)]),
     "csaidx_host_t_legal": (c_int64, [c_int64, c_int64]),
     "csaidx_host_k_eff": (c_int64, [c_int64, c_int64, c_int64]),
+    "csaidx_host_round_bf16": (c_int, [c_void_p, c_void_p, c_uint64, POINTER(c_int), POINTER(c_int)]),
 }
 
 _host = None
@@ -473,6 +474,17 @@ def k_eff(t: int, ratio: int, top_k: int) -> int:
     if top_k < 0:
         raise _capi.InvalidArgument("k_eff: top_k must be >= 0")
     return int(host_lib().csaidx_host_k_eff(t, ratio, top_k))
+
+
+def round_bf16(src: np.ndarray):
+    """Host rounding of the pipelined entry (csaidx_host_round_bf16): fp32 ->
+    bf16 bit patterns (uint16), plus the non-finite / inexact flags."""
+    src = np.ascontiguousarray(src, dtype=np.float32)
+    dst = np.empty(src.shape, dtype=np.uint16)
+    nf, ix = ctypes.c_int(0), ctypes.c_int(0)
+    _check(host_lib().csaidx_host_round_bf16(src.ctypes.data_as(c_void_p), dst.ctypes.data_as(c_void_p), src.size,
+                                             ctypes.byref(nf), ctypes.byref(ix)))
+    return dst, bool(nf.value), bool(ix.value)
 
 
 def dispatch_count_model(dims: ProblemDims, tile: TileConfig) -> int:

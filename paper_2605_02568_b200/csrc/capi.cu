@@ -245,8 +245,14 @@ int csaidx_engine_use_lane(csaidx_engine* e, int lane) {
     if (lane < 0 || lane > 3)
         return fail(CSAIDX_INVALID_ARGUMENT, "lane must be 0 (main), 1 (copy-in), 2 (copy-out) or 3 (side compute)");
     if (e->lane == 0) e->main_stream = e->stream;
-    if (lane > 0 && e->lanes[lane] == nullptr)
-        CSAIDX_CUDA_TRY(cudaStreamCreateWithFlags(&e->lanes[lane], cudaStreamNonBlocking), "cudaStreamCreate(lane)");
+    if (lane > 0 && e->lanes[lane] == nullptr) {
+        // the side compute lane gets the highest stream priority: its CTAs
+        // are dispatched first when SMs free up (a select beside a score)
+        int least = 0, greatest = 0;
+        CSAIDX_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest), "cudaDeviceGetStreamPriorityRange");
+        CSAIDX_CUDA_TRY(cudaStreamCreateWithPriority(&e->lanes[lane], cudaStreamNonBlocking, lane == 3 ? greatest : least),
+                        "cudaStreamCreate(lane)");
+    }
     e->stream = lane == 0 ? e->main_stream : e->lanes[lane];
     e->lane = lane;
     return CSAIDX_OK;

@@ -12,6 +12,7 @@
 #include "csaidx/tensor_io.hpp"
 #include "csaidx_host.h"
 #include "device.hpp"
+#include "host_convert.hpp"
 
 namespace {
 
@@ -335,6 +336,15 @@ int64_t csaidx_host_k_eff(int64_t t, int64_t ratio, int64_t top_k) {
     int64_t r = -1;
     guarded([&] { r = csaidx::k_eff(t, ratio, top_k); });
     return r;
+}
+
+int csaidx_host_round_bf16(const float* src, uint16_t* dst, uint64_t n, int* nonfinite, int* inexact) {
+    return guarded([&] {
+        if ((src == nullptr || dst == nullptr) && n > 0) throw std::invalid_argument("round_bf16: null buffer");
+        const csaidx::detail::Bf16Flags f = csaidx::detail::host_to_bf16(src, dst, static_cast<size_t>(n));
+        if (nonfinite != nullptr) *nonfinite = f.nonfinite ? 1 : 0;
+        if (inexact != nullptr) *inexact = f.inexact ? 1 : 0;
+    });
 }
 
 }  // extern "C"

@@ -7,10 +7,17 @@
 #include "csaidx/driver.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
+#include <string>
+#include <thread>
 
 #include "csaidx/causal.hpp"
 #include "device.hpp"
+#include "host_convert.hpp"
 
 namespace csaidx {
 
@@ -281,6 +288,70 @@ void download_result(csaidx_engine* e, const DeviceBuffer& idx, const DeviceBuff
 
 }  // namespace
 
+namespace {
+
+// Pinned bf16 staging slabs of the host-rounding pipeline, kept across calls
+// (pinning hundreds of MiB per call would cost more than the transfer).
+// Guarded by engine_mutex().
+struct PinnedSlabs {
+    std::vector<void*> ptr;
+    size_t bytes = 0;
+    uint16_t* get(csaidx_engine* e, int i, int count, size_t need) {
+        if (need > bytes || static_cast<int>(ptr.size()) < count) {
+            for (void* p : ptr) csaidx_cuda_host_free(e, p);
+            ptr.assign(static_cast<size_t>(count), nullptr);
+            bytes = std::max(need, bytes);
+            for (auto& p : ptr) check(csaidx_cuda_host_alloc(e, bytes, &p));
+        }
+        return static_cast<uint16_t*>(ptr[static_cast<size_t>(i)]);
+    }
+};
+
+PinnedSlabs& pinned_slabs() {
+    static PinnedSlabs s;
+    return s;
+}
+
+// State shared by the host-rounding producer thread and the thread that
+// drives the lanes: the producer rounds chunk o's q rows into slab
+// o % slabs once the copy of chunk o - slabs out of it has completed.
+struct HostRounder {
+    std::mutex mu;
+    std::condition_variable cv;
+    size_t converted = 0;  // chunks [0, converted) are in their slabs
+    size_t enqueued = 0;   // ... and their copies are queued
+    bool stop = false;
+    std::string error;
+    std::thread th;
+
+    ~HostRounder() {
+        {
+            std::lock_guard<std::mutex> g(mu);
+            stop = true;
+        }
+        cv.notify_all();
+        if (th.joinable()) th.join();
+    }
+    void fail(const std::string& what) {
+        {
+            std::lock_guard<std::mutex> g(mu);
+            error = what;
+        }
+        cv.notify_all();
+    }
+};
+
+// CSAIDX_HOST_TRACE=1: per-chunk host timestamps of the pipelined entry
+bool host_trace() {
+    static const bool v = std::getenv("CSAIDX_HOST_TRACE") != nullptr;
+    return v;
+}
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
 void run_chunked_rows_view(const HostView& in, const ProblemDims& dims, const DriverConfig& config,
                            const std::vector<int64_t>* starts, int64_t* host_idx, float* host_val, int64_t out_rows,
                            MemoryLedger& ledger, RunStats* stats_out) {
@@ -309,10 +380,66 @@ void run_chunked_rows_view(const HostView& in, const ProblemDims& dims, const Dr
     // order, the same row layout as the outputs)
     DeviceBuffer q(e, static_cast<size_t>(B * out_rows * qrow) * esz), kc(e, static_cast<size_t>(dims.kc_elems()) * esz),
         w(e, static_cast<size_t>(B * out_rows * dims.heads) * sizeof(float));
-    constexpr int kSlabs = 8, kConvDone = 128;  // fp32 staging slabs; event slots of their conversion
+    constexpr int kSlabs = 8, kConvDone = 128;  // staging slabs; event slots of their conversion
+    // host_round: q rows are rounded to bf16 on the host cores into pinned
+    // slabs by a producer thread running ahead of the copies, and cross PCIe
+    // at 2 bytes per entry (PCIe bounds the end-to-end call); otherwise fp32
+    // rows are copied into device slabs and rounded there.
+    // (Measured: rounding only part of the chunks on the host, to balance
+    // PCIe against host DRAM bandwidth, was slower than rounding all.)
+    const bool host_round = dtype == CSAIDX_DTYPE_BF16 && host_round_enabled();
+    const size_t slab_elems = static_cast<size_t>(B * plan.cs * qrow);
     DeviceBuffer slab[kSlabs];
-    if (dtype == CSAIDX_DTYPE_BF16) {
-        for (auto& sb : slab) sb = DeviceBuffer(e, static_cast<size_t>(B * plan.cs * qrow) * sizeof(float));
+    if (dtype == CSAIDX_DTYPE_BF16 && !host_round) {
+        for (auto& sb : slab) sb = DeviceBuffer(e, slab_elems * sizeof(float));
+    }
+    const int hslabs = host_slab_count();  // <= 32: the copy-done slots
+    std::vector<uint16_t*> hslab(static_cast<size_t>(hslabs), nullptr);
+    if (host_round)
+        for (int i = 0; i < hslabs; ++i)
+            hslab[static_cast<size_t>(i)] = pinned_slabs().get(e, i, hslabs, slab_elems * sizeof(uint16_t));
+    const double t_start = now_ms();
+    HostRounder rounder;
+    if (host_round) {
+        rounder.th = std::thread([&] {
+            try {
+                for (size_t o = 0; o < plan.order.size(); ++o) {
+                    const double t0 = now_ms();
+                    if (o >= static_cast<size_t>(hslabs)) {
+                        {
+                            std::unique_lock<std::mutex> g(rounder.mu);
+                            rounder.cv.wait(g, [&] { return rounder.stop || rounder.enqueued > o - hslabs; });
+                            if (rounder.stop) return;
+                        }
+                        // the copy out of this slab (chunk o - hslabs) has finished
+                        check(csaidx_engine_sync_slot(e, static_cast<int>((o - hslabs) % 32)));
+                    }
+                    const double t1 = now_ms();
+                    const size_t c = plan.order[o];
+                    const int64_t s0 = plan.starts[c], rows = std::min(plan.cs, dims.seq_len - s0);
+                    Bf16Flags f;
+                    for (int64_t b = 0; b < B; ++b) {
+                        const int64_t hrow = in.local_rows ? b * out_rows + plan.out_row0[c] : b * dims.seq_len + s0;
+                        const Bf16Flags fb = host_to_bf16(in.q + hrow * qrow, hslab[o % hslabs] + b * rows * qrow,
+                                                          static_cast<size_t>(rows * qrow));
+                        f.nonfinite = f.nonfinite || fb.nonfinite;
+                        f.inexact = f.inexact || fb.inexact;
+                    }
+                    if (host_trace())
+                        std::fprintf(stderr, "round %zu wait %.3f convert %.3f at %.3f\n", o, t1 - t0, now_ms() - t1,
+                                     now_ms() - t_start);
+                    if (f.nonfinite) return rounder.fail("IndexerInputs: non-finite entry in q/kc");
+                    if (strict && f.inexact) return rounder.fail("operand is not bf16-representable (strict mode)");
+                    {
+                        std::lock_guard<std::mutex> g(rounder.mu);
+                        rounder.converted = o + 1;
+                    }
+                    rounder.cv.notify_all();
+                }
+            } catch (const std::exception& ex) {
+                rounder.fail(ex.what());
+            }
+        });
     }
     const size_t n = static_cast<size_t>(B * out_rows * k);
     DeviceBuffer idx(e, n * sizeof(int64_t)), val(e, n * sizeof(float));
@@ -323,7 +450,33 @@ void run_chunked_rows_view(const HostView& in, const ProblemDims& dims, const Dr
     // persistent score kernel and stall the next copy). The bf16 rounding of
     // chunk o runs on the main lane right before chunk o's score; kSlabs
     // staging slabs let the copies run up to kSlabs chunks ahead.
+    auto upload_rounded = [&](size_t o) {  // host_round: chunk o's bf16 slab and w rows, on the copy-in lane
+        const size_t c = plan.order[o];
+        const int64_t s0 = plan.starts[c], rows = std::min(plan.cs, dims.seq_len - s0);
+        const double t0 = now_ms();
+        {
+            std::unique_lock<std::mutex> g(rounder.mu);
+            rounder.cv.wait(g, [&] { return rounder.converted > o || !rounder.error.empty(); });
+            if (rounder.converted <= o) throw std::invalid_argument(rounder.error);
+        }
+        if (host_trace()) std::fprintf(stderr, "upload %zu waited %.3f at %.3f\n", o, now_ms() - t0, now_ms() - t_start);
+        for (int64_t b = 0; b < B; ++b) {
+            const int64_t lrow = b * out_rows + plan.out_row0[c];
+            const int64_t hrow = in.local_rows ? lrow : b * dims.seq_len + s0;
+            check(csaidx_cuda_copy(e, q.as<uint16_t>() + lrow * qrow, hslab[o % hslabs] + b * rows * qrow,
+                                   static_cast<size_t>(rows * qrow) * sizeof(uint16_t)));
+            check(csaidx_cuda_copy(e, w.as<float>() + lrow * dims.heads, in.w + hrow * dims.heads,
+                                   static_cast<size_t>(rows * dims.heads) * sizeof(float)));
+        }
+        check(csaidx_engine_signal(e, static_cast<int>(o % 32)));
+        {
+            std::lock_guard<std::mutex> g(rounder.mu);
+            rounder.enqueued = o + 1;
+        }
+        rounder.cv.notify_all();
+    };
     auto upload_raw = [&](size_t o) {  // o-th chunk in processing order, on the copy-in lane
+        if (host_round) return upload_rounded(o);
         const size_t c = plan.order[o];
         const int64_t s0 = plan.starts[c], rows = std::min(plan.cs, dims.seq_len - s0);
         if (dtype == CSAIDX_DTYPE_BF16 && o >= kSlabs)  // slab o % kSlabs: chunk o - kSlabs converted
@@ -342,7 +495,7 @@ void run_chunked_rows_view(const HostView& in, const ProblemDims& dims, const Dr
         check(csaidx_engine_signal(e, static_cast<int>(o % 32)));
     };
     auto convert = [&](size_t o) {  // on the main lane, after chunk o's copy
-        if (dtype != CSAIDX_DTYPE_BF16) return;
+        if (dtype != CSAIDX_DTYPE_BF16 || host_round) return;
         const size_t c = plan.order[o];
         const int64_t rows = std::min(plan.cs, dims.seq_len - plan.starts[c]);
         for (int64_t b = 0; b < B; ++b) {

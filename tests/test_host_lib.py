@@ -8,6 +8,8 @@ import ctypes
 import os
 import re
 
+import numpy as np
+
 import pytest
 
 from paper_2605_02568_b200 import _capi, api
@@ -92,3 +94,37 @@ def test_no_gpu_means_loud_failure_not_fallback():
     inputs = api.IndexerInputs.validated([1.0] * 8, [1.0, 2.0], [1.0] * 8, d)
     with pytest.raises(_capi.CsaidxError):
         api.run_chunked(inputs, d)
+
+
+@pytest.mark.parametrize("n", [37, 1_000_003])
+def test_host_round_bf16_is_round_to_nearest_even(n):
+    """csaidx_host_round_bf16 (the pipelined entry's host rounding) gives the
+    bf16 bit patterns of torch's RNE conversion (== __float2bfloat16_rn on
+    device) incl. ties, subnormals, signed zeros and overflow to inf."""
+    import torch
+
+    rng = np.random.default_rng(n)
+    x = (rng.normal(0, 1, n) * np.exp2(rng.integers(-140, 120, n))).astype(np.float32)
+    u = x.view(np.uint32)
+    u[::7] = (u[::7] & 0xffff0000) | 0x8000          # exact ties, both lsb parities
+    x[1::11] = np.float32(1.5e-41)                     # subnormal
+    x[2::13] = np.float32(-0.0)
+    x[3::17] = np.finfo(np.float32).max                # rounds up to inf
+    got, nonfinite, inexact = api.round_bf16(x)
+    want = torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(got, want)
+    assert not nonfinite and inexact
+
+
+def test_host_round_bf16_flags():
+    exact = np.array([1.0, -2.5, 0.0, 3.0e38], np.float32)
+    exact = (exact.view(np.uint32) & 0xffff0000).view(np.float32)
+    _, nf, ix = api.round_bf16(exact)
+    assert not nf and not ix
+    bad = np.ones(100_000, np.float32)
+    bad[77_777] = np.inf
+    _, nf, _ = api.round_bf16(bad)
+    assert nf
+    bad[77_777] = np.nan
+    _, nf, _ = api.round_bf16(bad)
+    assert nf

@@ -334,3 +334,47 @@ def test_sentinel_contract_exhaustive(orc):
                 res, _ = api.run_chunked(inputs, dims, api.DriverConfig(tile=api.TileConfig(cs, ct)))
                 rc, idx, val, _ = orc.run_chunked(q, kc, w, m, k, cs, ct)
                 assert np.array_equal(res.indices, idx) and np.array_equal(bits(res.values), bits(val))
+
+
+def test_host_rounding_matches_device_rounding(orc, monkeypatch):
+    """The pipelined host entry rounds q on the host cores (CSAIDX_HOST_ROUND,
+    default) or on the device: same bytes, incl. B=2, rank-local rows and more
+    chunks than staging slabs; non-finite and (strict) inexact q rows raise
+    invalid_argument either way."""
+    B, S, m, H, D, k = 2, 8192, 4, 64, 128, 64
+    q, kc, w = orc.generate_inputs(B, S, m, H, D, 3)
+    dims = api.ProblemDims.create(B, S, m, H, D, k)
+    cfg = api.DriverConfig(tile=api.TileConfig(256, S // m))
+    starts = list(range(0, S, 256))[::-1][:20]  # 20 chunks > 8 slabs
+    rows = len(starts) * 256
+    q4 = np.asarray(q, np.float32).reshape(B, S, H, D)
+    w3 = np.asarray(w, np.float32).reshape(B, S, H)
+    ql = np.ascontiguousarray(np.concatenate([q4[:, s:s + 256] for s in starts], axis=1))
+    wl = np.ascontiguousarray(np.concatenate([w3[:, s:s + 256] for s in starts], axis=1))
+    kcf = np.asarray(kc, np.float32)
+    outs = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("CSAIDX_HOST_ROUND", mode)
+        oi = np.empty((B, rows, k), np.int64)
+        ov = np.empty((B, rows, k), np.float32)
+        api.run_chunked_rows(q4, kcf, w3, dims, cfg, starts, oi, ov)
+        li = np.empty_like(oi)
+        lv = np.empty_like(ov)
+        api.run_chunked_rows(ql, kcf, wl, dims, cfg, starts, li, lv, local_rows=True)
+        assert np.array_equal(oi, li) and np.array_equal(bits(ov), bits(lv))
+        outs[mode] = (oi, ov)
+    assert np.array_equal(outs["0"][0], outs["1"][0]) and np.array_equal(bits(outs["0"][1]), bits(outs["1"][1]))
+    for mode in ("0", "1"):
+        monkeypatch.setenv("CSAIDX_HOST_ROUND", mode)
+        bad = q4.copy()
+        bad[1, starts[13] + 5, 7, 3] = np.nan
+        oi = np.empty((B, rows, k), np.int64)
+        ov = np.empty((B, rows, k), np.float32)
+        with pytest.raises(InvalidArgument):
+            api.run_chunked_rows(bad, kcf, w3, dims, cfg, starts, oi, ov)
+        inexact = q4.copy()
+        inexact[0, starts[17] + 1, 0, 0] = np.float32(1.0000001)
+        strict = api.DriverConfig(tile=api.TileConfig(256, S // m), strict_bf16=True)
+        with pytest.raises(InvalidArgument):
+            api.run_chunked_rows(inexact, kcf, w3, dims, strict, starts, oi, ov)
+        api.run_chunked_rows(inexact, kcf, w3, dims, cfg, starts, oi, ov)  # rounds when not strict
