@@ -412,8 +412,10 @@ def main():
             e2e_ms = float(h.item())
         # q crosses PCIe as bf16 when the entry rounds it on the host cores
         # (CSAIDX_HOST_ROUND, default on), else as the caller's fp32
-        host_round = os.environ.get("CSAIDX_HOST_ROUND", "1") != "0"
-        host_threads = max(1, int(os.environ.get("CSAIDX_HOST_THREADS", (os.cpu_count() or 2) - 1)))
+        host_round = (os.environ.get("CSAIDX_HOST_ROUND", "0") != "0" if "CSAIDX_HOST_ROUND" in os.environ
+                      else int(os.environ.get("LOCAL_WORLD_SIZE", "1")) <= 1)
+        host_threads = int(os.environ.get("CSAIDX_HOST_THREADS", 0)) or max(
+            1, len(os.sched_getaffinity(0)) // int(os.environ.get("LOCAL_WORLD_SIZE", "1")) - 1)
         h2d = B * rows * H * D * (2 if host_round else 4) + B * T * D * 4 + B * rows * H * 4
         d2h = B * rows * k * 12
         e2e = {"value": (pairs_mine if args.simulate_rank else pairs_total) / (e2e_ms / 1000.0),

@@ -26,14 +26,14 @@ Bf16Flags host_to_bf16(const float* src, uint16_t* dst, size_t n);
 uint16_t host_bf16_rne(float x);
 
 // Threads of a parallel region incl. the caller (CSAIDX_HOST_THREADS,
-// default: host cores - 1).
+// default: usable cores / LOCAL_WORLD_SIZE - 1).
 int host_threads();
 
 // Runs fn(0) .. fn(parts - 1) on the pool and the calling thread; blocks.
 void host_parallel_for(int parts, const std::function<void(int)>& fn);
 
-// Whether the pipelined host entry rounds q on the host (CSAIDX_HOST_ROUND,
-// default on; 0 = copy fp32 rows and round on the device).
+// Whether the pipelined host entry rounds q on the host (CSAIDX_HOST_ROUND=1 /
+// 0; default: on unless several ranks share the node, LOCAL_WORLD_SIZE > 1).
 bool host_round_enabled();
 
 // Pinned bf16 staging slabs of that pipeline (CSAIDX_HOST_SLABS, 2..32)
