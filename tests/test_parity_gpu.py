@@ -208,12 +208,13 @@ def test_csat_dump_loads_into_hbm_rank_local(orc, tmp_path):
         api.load_inputs_device(tmp_path / "bad.csat", dims64, cfg, strict=True, dtype=0)
 
 
-@pytest.mark.parametrize("sms", ["0", "12", "40"])
+@pytest.mark.parametrize("sms", ["0", "12", "40", "-1"])
 def test_select_beside_score_overlap_is_byte_identical(orc, monkeypatch, sms):
     """One key tile per chunk on the tensor-core path: selects running beside
-    the next chunk's score kernel (CSAIDX_SELECT_SMS SMs, double-buffered
-    tiles, a second compute lane) give the same bytes as the serial path,
-    through the device entry and the host entry (copy lanes on top)."""
+    the next chunk's score kernel (CSAIDX_SELECT_SMS SMs, or -1: no partition,
+    a high-priority select lane; double-buffered tiles, a second compute lane)
+    give the same bytes as the serial path, through the device entry and the
+    host entry (copy lanes on top)."""
     import torch
 
     q, kc, w = orc.generate_inputs(1, 4096, 4, 64, 128, 31, bf16=True)
