@@ -57,9 +57,10 @@ private:
 // sample pass scores at most kPrefilterSampleTiles 128-key tiles per row.
 bool prefilter_enabled();
 // SMs given to the select while it runs beside the next chunk's score kernel
-// (CSAIDX_SELECT_SMS; default 0 = no overlap: each select uses the GPU).
+// (CSAIDX_SELECT_SMS; default 0 = no overlap: each select uses the GPU;
+// -1 = overlap without a partition, the select lane at top priority).
 int select_overlap_sms();
-// Two-level select for long rows (CSAIDX_TWO_LEVEL, default on).
+// Two-level select for long rows (CSAIDX_TWO_LEVEL=1; default off).
 bool two_level_enabled();
 constexpr int64_t kPrefilterSampleTiles = 16;
 

@@ -108,13 +108,17 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
     // several rows per CTA) on a second compute lane while chunk o+1's score
     // runs on the rest; the score tiles are double buffered. Results are
     // identical (the same kernels per row); only the SM assignment changes.
+    // select_overlap_sms() < 0: no partition — both kernels take whole SMs
+    // as they free up, the select lane first (stream priority), so each
+    // kernel's tail is filled by the other's start.
+    const int overlap_sms = select_overlap_sms();
     const bool overlap = plan.ct >= T && !prefilter && !config.bool_mask_tile && plan.order.size() >= 2 &&
                          csaidx_cuda_score_uses_tensor_cores(&cd, ops.dtype, mcode, kcode) != 0 &&
-                         csaidx_cuda_select_overlap_capable(k) != 0 && select_overlap_sms() > 0;
+                         (overlap_sms < 0 || (overlap_sms > 0 && csaidx_cuda_select_overlap_capable(k) != 0));
     // Two-level select (csaidx_cuda_score_gmax): when rows can span >= 4k
     // 32-key groups the score epilogue also writes each group's maximum, and
     // the select reads only the ~k groups that can hold a top-k score
-    // (CSAIDX_TWO_LEVEL=0 disables).
+    // (opt-in, CSAIDX_TWO_LEVEL=1: measured slower overall at C4).
     const bool two_level = plan.ct >= T && !prefilter && !config.bool_mask_tile && two_level_enabled() &&
                            csaidx_cuda_score_uses_tensor_cores(&cd, ops.dtype, mcode, kcode) != 0 &&
                            ceil_div(plan.ct, 32) >= 4 * k;
@@ -132,11 +136,13 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
     } partition;
     if (overlap) {
         scores2 = DeviceBuffer(e, static_cast<size_t>(B * plan.cs * ld) * sizeof(float));
-        int nsm = 0;
-        check(csaidx_engine_num_sms(e, &nsm));
-        const int x = std::min(select_overlap_sms(), nsm / 3);
-        check(csaidx_engine_set_partition(e, nsm - x, x));
-        partition.e = e;
+        if (overlap_sms > 0) {
+            int nsm = 0;
+            check(csaidx_engine_num_sms(e, &nsm));
+            const int x = std::min(overlap_sms, nsm / 3);
+            check(csaidx_engine_set_partition(e, nsm - x, x));
+            partition.e = e;
+        }
     }
     constexpr int kScoreDone = 64, kSelectDone = 96, kSideLane = 3;
 
