@@ -110,8 +110,8 @@ void DeviceBuffer::download(void* host, size_t bytes) const { check(csaidx_cuda_
 
 bool two_level_enabled() {
     // Off by default (CSAIDX_TWO_LEVEL=1 enables): at C4 the select drops
-    // 22.4 -> 15.0 ms but the group-max epilogue costs the score kernel
-    // 210 -> 227 ms (profiles/r01_ncu_history.md).
+    // 22.0 -> 14.9 ms but the group-max epilogue costs the score kernel
+    // 206 -> 216.5 ms (profiles/r01_ncu_history.md).
     const char* v = std::getenv("CSAIDX_TWO_LEVEL");
     return v != nullptr && std::string(v) == "1";
 }

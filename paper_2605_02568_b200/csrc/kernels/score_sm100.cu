@@ -506,13 +506,15 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                                 orow[u][jo] = legal ? acc : neg_inf;
                             }
                             if (kGmax) {
-                                // max over the warp's 32 key columns: one redux.sync on
-                                // the order-preserving integer key
-                                const uint32_t gk = __reduce_max_sync(
-                                    0xffffffffu, ord_key((legal && jo < out_cols) ? acc : neg_inf));
+                                // max over the warp's 32 key columns: one float redux.sync
+                                // (sm_100a)
+                                float gm;
+                                asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;"
+                                             : "=f"(gm)
+                                             : "f"((legal && jo < out_cols) ? acc : neg_inf));
                                 if (lane == 0 && jo < out_cols) {
                                     const int64_t grow = static_cast<int64_t>(it.b) * p.rows + it.r0 + qi;
-                                    p.gmax[grow * p.gmax_ld + (jo >> 5)] = ord_key_to_float(gk);
+                                    p.gmax[grow * p.gmax_ld + (jo >> 5)] = gm;
                                 }
                             }
                             if (kFilter) {
