@@ -185,6 +185,8 @@ def main():
     ap.add_argument("--ct", type=int, default=None)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gather-groups", type=int, default=4,
+                    help="N>1: run each rank's chunks in this many groups, gathering group j during group j+1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no e2e/baseline)")
     ap.add_argument("--simulate-rank", default=None, metavar="R/N",
@@ -257,15 +259,36 @@ def main():
         kc = torch.empty(B * T * D, dtype=torch.bfloat16, device="cuda")
     out_idx = torch.empty((B, rows, k), dtype=torch.int64, device="cuda")
     out_val = torch.empty((B, rows, k), dtype=torch.float32, device="cuda")
-    # Gather of the int32 index rows to rank 0, in slices of <= 256 MB per
-    # rank so the staging stays bounded; rank 0 holds the [world, B, rows, k]
-    # int32 result (allocated in --simulate-rank 0/N too, for peak HBM).
+    # Gather of the int32 index rows to rank 0, overlapped with the compute:
+    # each rank runs its chunks in G groups (G = --gather-groups, 1 for B > 1
+    # where a group's rows are not contiguous) and gathers group j's rows
+    # (async on NCCL's stream) while group j+1 computes. Every rank splits
+    # every shard the same way, so group j's padded size is known to all.
+    G = max(1, args.gather_groups) if (world > 1 or plan_world > 1) and B == 1 else 1
+
+    def split(lst):
+        n = len(lst)
+        return [lst[n * j // G: n * (j + 1) // G] for j in range(G)]
+
+    def group_rows(shard):  # [(r0, r1)] of each group in the rank's local stack
+        out, r0 = [], 0
+        for grp in split(shard):
+            r1 = r0 + (api.chunk_rows(dims, cfg, grp) if grp else 0)
+            out.append((r0, r1))
+            r0 = r1
+        return out
+
+    my_groups = split(mine)
+    granges = [group_rows(sh) for sh in shards]          # [rank][group] -> (r0, r1)
+    gmax = [max(gr[j][1] - gr[j][0] for gr in granges) for j in range(G)]
     max_rows = max(api.chunk_rows(dims, cfg, sh) for sh in shards)
-    slice_rows = max(1, min(max_rows, (256 << 20) // (B * k * 4)))
+    pad = max(gmax)
     gathered = None
-    if plan_rank == 0 and plan_world > 1:
-        gathered = torch.empty((plan_world, B, max_rows, k), dtype=torch.int32, device="cuda")
-    send = torch.zeros((B, max_rows, k), dtype=torch.int32, device="cuda") if world > 1 else None
+    if plan_rank == 0 and plan_world > 1:  # also in --simulate-rank 0/N, for peak HBM
+        gathered = torch.empty((plan_world, B, max_rows + pad, k), dtype=torch.int32, device="cuda")
+    send = torch.zeros((B, max_rows + pad, k), dtype=torch.int32, device="cuda") if world > 1 else None
+    q_rows = q.view(B, rows, H * D)
+    w_rows = w.view(B, rows, H)
     torch.cuda.synchronize()
 
     def bcast(t):
@@ -276,40 +299,51 @@ def main():
             dist.broadcast(h, src=0)
             t.copy_(h)
 
-    def gather_rows():
-        send[:, :rows].copy_(out_idx)  # int64 -> int32 (indices < T)
-        for r0 in range(0, max_rows, slice_rows):
-            n = min(slice_rows, max_rows - r0)
-            part = send[:, r0:r0 + n].contiguous()
-            if backend == "nccl":
-                if rank == 0:
-                    dst = [gathered[r, :, r0:r0 + n] for r in range(world)]
-                    if all(t.is_contiguous() for t in dst):  # B = 1: receive in place
-                        dist.gather(part, dst, dst=0)
-                    else:
-                        bufs = [torch.empty_like(part) for _ in range(world)]
-                        dist.gather(part, bufs, dst=0)
-                        for r in range(world):
-                            dst[r].copy_(bufs[r])
-                else:
-                    dist.gather(part, None, dst=0)
-            else:
-                h = part.cpu()
-                bufs = [torch.empty_like(h) for _ in range(world)] if rank == 0 else None
-                dist.gather(h, bufs, dst=0)
-                if rank == 0:
-                    for r in range(world):
-                        gathered[r, :, r0:r0 + n].copy_(bufs[r])
+    def gather_group(j):
+        r0, r1 = granges[rank][j]
+        send[:, r0:r1].copy_(out_idx[:, r0:r1])  # int64 -> int32 (indices < T)
+        part = send[:, r0:r0 + gmax[j]]
+        if backend == "nccl":
+            dst = [gathered[r, :, granges[r][j][0]:granges[r][j][0] + gmax[j]] for r in range(world)] \
+                if rank == 0 else None
+            return dist.gather(part, dst, dst=0, async_op=True)
+        h = part.cpu()
+        bufs = [torch.empty_like(h) for _ in range(world)] if rank == 0 else None
+        dist.gather(h, bufs, dst=0)
+        if rank == 0:
+            for r in range(world):
+                gathered[r, :, granges[r][j][0]:granges[r][j][0] + gmax[j]].copy_(bufs[r])
+        return None
+
+    def run_groups(after_group=None):
+        st = None
+        works = []
+        for j, grp in enumerate(my_groups):
+            r0, r1 = granges[plan_rank][j]
+            if grp:
+                st = api.run_chunked_device(q_rows[:, r0:r1], kc, w_rows[:, r0:r1], dims, cfg, grp,
+                                            out_idx[:, r0:r1], out_val[:, r0:r1], local_rows=True)[2]
+            if after_group is not None:
+                works.append(after_group(j))
+        for wk in works:
+            if wk is not None:
+                wk.wait()
+        return st
 
     stats_box = {}
 
     def step():
         if world > 1:
             bcast(kc)  # keys once over NVLink
-        st = api.run_chunked_device(q, kc, w, dims, cfg, mine, out_idx, out_val, local_rows=True)[2]
+        if G == 1:
+            st = api.run_chunked_device(q, kc, w, dims, cfg, mine, out_idx, out_val, local_rows=True)[2]
+            if world > 1:
+                w0 = gather_group(0)  # only the [S, k] indices travel
+                if w0 is not None:
+                    w0.wait()
+        else:
+            st = run_groups(gather_group if world > 1 else None)
         stats_box["st"] = st
-        if world > 1:
-            gather_rows()  # only the [S, k] indices travel
 
     drv = api.KernelStats(api.driver_engine(local))
     for _ in range(args.warmup):
@@ -351,7 +385,10 @@ def main():
 
         parts = [gathered[r][:, : api.chunk_rows(dims, cfg, shards[r])].cpu().numpy() for r in range(world)]
         full = assemble(parts, shards, S, cs)
-        gather_ok = bool(np.array_equal(full[:, mine[0]:mine[0] + 1], out_idx[:, :1].cpu().numpy()))
+        # rank 0's own rows came back intact, and every gathered entry is a
+        # key index or the -1 sentinel (no stale / padding rows leaked in)
+        gather_ok = bool(np.array_equal(parts[0], out_idx.cpu().numpy().astype(np.int32)) and
+                         full.min() >= -1 and full.max() < T)
     kinds = {"score": _capi.KIND_SCORE, "select": _capi.KIND_SELECT, "merge": _capi.KIND_MERGE,
              "finalize": _capi.KIND_FINALIZE, "prep": _capi.KIND_PREP}
     kstats = {name: drv.get(kd) for name, kd in kinds.items()}
@@ -486,7 +523,8 @@ def main():
             "run_stats": {"dispatch_count": st.dispatch_count, "tiles_skipped_masked": st.tiles_skipped_masked},
             "multi_gpu": {"rank_work_pairs": loads, "gather_reassembly_ok": gather_ok,
                           "collectives": (f"broadcast kc (bf16) from rank 0 + gather of int32 [rows,k] index rows to "
-                                          f"rank 0 in {slice_rows}-row slices ({backend})") if world > 1 else "none",
+                                          f"rank 0 in {G} row groups, group j's gather overlapping group j+1's "
+                                          f"compute ({backend})") if world > 1 else "none",
                           "rank_rows": rows, "rank_pairs": pairs_mine},
         }
         print(json.dumps(line), flush=True)
