@@ -304,12 +304,23 @@ struct PinnedSlabs {
     size_t bytes = 0;
     uint16_t* get(csaidx_engine* e, int i, int count, size_t need) {
         if (need > bytes || static_cast<int>(ptr.size()) < count) {
-            for (void* p : ptr) csaidx_cuda_host_free(e, p);
+            release(e);
             ptr.assign(static_cast<size_t>(count), nullptr);
-            bytes = std::max(need, bytes);
-            for (auto& p : ptr) check(csaidx_cuda_host_alloc(e, bytes, &p));
+            bytes = need;
+            try {
+                for (auto& p : ptr) check(csaidx_cuda_host_alloc(e, bytes, &p));
+            } catch (...) {
+                release(e);  // all or nothing
+                throw;
+            }
         }
         return static_cast<uint16_t*>(ptr[static_cast<size_t>(i)]);
+    }
+    void release(csaidx_engine* e) {
+        for (void* p : ptr)
+            if (p != nullptr) csaidx_cuda_host_free(e, p);
+        ptr.clear();
+        bytes = 0;
     }
 };
 
@@ -393,17 +404,22 @@ void run_chunked_rows_view(const HostView& in, const ProblemDims& dims, const Dr
     // rows are copied into device slabs and rounded there.
     // (Measured: rounding only part of the chunks on the host, to balance
     // PCIe against host DRAM bandwidth, was slower than rounding all.)
-    const bool host_round = dtype == CSAIDX_DTYPE_BF16 && host_round_enabled();
     const size_t slab_elems = static_cast<size_t>(B * plan.cs * qrow);
+    const int hslabs = host_slab_count();  // <= 32: the copy-done slots
+    std::vector<uint16_t*> hslab(static_cast<size_t>(hslabs), nullptr);
+    bool host_round = dtype == CSAIDX_DTYPE_BF16 && host_round_enabled();
+    if (host_round) {
+        try {
+            for (int i = 0; i < hslabs; ++i)
+                hslab[static_cast<size_t>(i)] = pinned_slabs().get(e, i, hslabs, slab_elems * sizeof(uint16_t));
+        } catch (const std::exception&) {
+            host_round = false;  // no pinned staging available: round on the device
+        }
+    }
     DeviceBuffer slab[kSlabs];
     if (dtype == CSAIDX_DTYPE_BF16 && !host_round) {
         for (auto& sb : slab) sb = DeviceBuffer(e, slab_elems * sizeof(float));
     }
-    const int hslabs = host_slab_count();  // <= 32: the copy-done slots
-    std::vector<uint16_t*> hslab(static_cast<size_t>(hslabs), nullptr);
-    if (host_round)
-        for (int i = 0; i < hslabs; ++i)
-            hslab[static_cast<size_t>(i)] = pinned_slabs().get(e, i, hslabs, slab_elems * sizeof(uint16_t));
     const double t_start = now_ms();
     HostRounder rounder;
     if (host_round) {
