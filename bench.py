@@ -185,6 +185,8 @@ def main():
     ap.add_argument("--ct", type=int, default=None)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1: how rank 0 collects the index rows (peer stores from the select, or NCCL gather)")
     ap.add_argument("--gather-groups", type=int, default=4,
                     help="N>1: run each rank's chunks in this many groups, gathering group j during group j+1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -264,7 +266,11 @@ def main():
     # where a group's rows are not contiguous) and gathers group j's rows
     # (async on NCCL's stream) while group j+1 computes. Every rank splits
     # every shard the same way, so group j's padded size is known to all.
-    G = max(1, args.gather_groups) if (world > 1 or plan_world > 1) and B == 1 else 1
+    # --gather p2p (default): no gather collective — the final select kernels
+    # store every rank's int32 index rows straight into rank 0's [B, S, k]
+    # buffer through a CUDA IPC peer mapping (NVLink), fused with the select.
+    p2p = args.gather == "p2p" and world > 1
+    G = max(1, args.gather_groups) if (world > 1 or plan_world > 1) and B == 1 and args.gather == "nccl" else 1
 
     def split(lst):
         n = len(lst)
@@ -284,9 +290,9 @@ def main():
     max_rows = max(api.chunk_rows(dims, cfg, sh) for sh in shards)
     pad = max(gmax)
     gathered = None
-    if plan_rank == 0 and plan_world > 1:  # also in --simulate-rank 0/N, for peak HBM
+    if plan_rank == 0 and plan_world > 1 and not p2p:  # also in --simulate-rank 0/N, for peak HBM
         gathered = torch.empty((plan_world, B, max_rows + pad, k), dtype=torch.int32, device="cuda")
-    send = torch.zeros((B, max_rows + pad, k), dtype=torch.int32, device="cuda") if world > 1 else None
+    send = torch.zeros((B, max_rows + pad, k), dtype=torch.int32, device="cuda") if world > 1 and not p2p else None
     q_rows = q.view(B, rows, H * D)
     w_rows = w.view(B, rows, H)
     torch.cuda.synchronize()
@@ -332,12 +338,30 @@ def main():
 
     stats_box = {}
 
+    drv_h = api.driver_engine(local)
+    sink = sink_ptr = None
+    if p2p:
+        if rank == 0:
+            sink = torch.full((B, S, k), -2, dtype=torch.int32, device="cuda")
+            handle = [api.ipc_handle(drv_h, sink.data_ptr())]
+        else:
+            handle = [None]
+        dist.broadcast_object_list(handle, src=0)
+        sink_ptr = sink.data_ptr() if rank == 0 else api.ipc_open(drv_h, handle[0])
+        api.set_index_sink(drv_h, sink_ptr, S)
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda") if p2p else None
+
     def step():
         if world > 1:
             bcast(kc)  # keys once over NVLink
         if G == 1:
             st = api.run_chunked_device(q, kc, w, dims, cfg, mine, out_idx, out_val, local_rows=True)[2]
-            if world > 1:
+            if p2p:  # every rank's rows are in rank 0's buffer once all ranks pass this point
+                if backend == "nccl":
+                    dist.all_reduce(flag)
+                else:
+                    dist.barrier()
+            elif world > 1:
                 w0 = gather_group(0)  # only the [S, k] indices travel
                 if w0 is not None:
                     w0.wait()
@@ -345,7 +369,7 @@ def main():
             st = run_groups(gather_group if world > 1 else None)
         stats_box["st"] = st
 
-    drv = api.KernelStats(api.driver_engine(local))
+    drv = api.KernelStats(drv_h)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -379,7 +403,28 @@ def main():
             t = h
         ms = float(t.item())
     gather_ok = None
-    if world > 1 and rank == 0:
+    if p2p:
+        # untimed check: rank 0's buffer holds every rank's rows (per-rank
+        # checksums over each shard's rows), its own rows bit for bit, and no
+        # row was left unwritten
+        api.set_index_sink(drv_h, None)
+        torch.cuda.synchronize()
+        mine_sum = int(out_idx.sum().item())
+        sums = [None] * world
+        dist.all_gather_object(sums, mine_sum)
+        if rank == 0:
+            full = sink.cpu().numpy()
+            ok = full.min() >= -1 and full.max() < T
+            for r in range(world):
+                rows_r = np.concatenate([np.arange(s0, min(s0 + cs, S)) for s0 in shards[r]])
+                ok = ok and int(full[:, rows_r].astype(np.int64).sum()) == sums[r]
+            own = np.concatenate([np.arange(s0, min(s0 + cs, S)) for s0 in mine])
+            ok = ok and np.array_equal(full[:, own], out_idx.cpu().numpy().astype(np.int32))
+            gather_ok = bool(ok)
+        dist.barrier()
+        if rank != 0:
+            api.ipc_close(drv_h, sink_ptr)
+    elif world > 1 and rank == 0:
         # the gathered rows reassemble into sequence order (checked once, untimed)
         from paper_2605_02568_b200.shard import assemble
 
@@ -522,9 +567,13 @@ def main():
             "e2e": e2e,
             "run_stats": {"dispatch_count": st.dispatch_count, "tiles_skipped_masked": st.tiles_skipped_masked},
             "multi_gpu": {"rank_work_pairs": loads, "gather_reassembly_ok": gather_ok,
-                          "collectives": (f"broadcast kc (bf16) from rank 0 + gather of int32 [rows,k] index rows to "
-                                          f"rank 0 in {G} row groups, group j's gather overlapping group j+1's "
-                                          f"compute ({backend})") if world > 1 else "none",
+                          "collectives": ("none on the data path: broadcast kc (bf16) from rank 0; the final select "
+                                          "kernels store each rank's int32 [rows,k] index rows straight into rank 0's "
+                                          f"[B,S,k] buffer over a CUDA IPC peer mapping (fused gather); a 1-element "
+                                          f"{backend} barrier ends the step") if p2p else
+                                         ((f"broadcast kc (bf16) from rank 0 + gather of int32 [rows,k] index rows to "
+                                           f"rank 0 in {G} row groups, group j's gather overlapping group j+1's "
+                                           f"compute ({backend})") if world > 1 else "none"),
                           "rank_rows": rows, "rank_pairs": pairs_mine},
         }
         print(json.dumps(line), flush=True)

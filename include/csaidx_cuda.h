@@ -86,6 +86,20 @@ int csaidx_engine_sync_slot(csaidx_engine* e, int slot);
  * call it with NULL on entry, so operands produced on the default stream
  * need no host synchronisation before the call. */
 int csaidx_engine_await_stream(csaidx_engine* e, void* stream);
+/* Index sink: from now on every final output row written by
+ * csaidx_cuda_select_final / csaidx_cuda_finalize for query position s of
+ * batch b is also stored as int32 indices at dst[(b * seq_len + s) * k ..]
+ * (a [B, seq_len, k] buffer). dst may be another GPU's memory mapped with
+ * csaidx_cuda_ipc_open: then the final kernels of a query-sharded run write
+ * their rows straight into the collecting rank over NVLink, fusing the
+ * gather of the driver's result (reference run_chunked, driver.cpp:115-165,
+ * assembles TopKResult rows; SURVEY §8e's gather) into the select.
+ * NULL disables. */
+int csaidx_engine_set_index_sink(csaidx_engine* e, int32_t* dst, int64_t seq_len);
+/* CUDA IPC of a device allocation (64-byte handle) for the index sink. */
+int csaidx_cuda_ipc_handle(csaidx_engine* e, void* dev_ptr, void* handle);
+int csaidx_cuda_ipc_open(csaidx_engine* e, const void* handle, void** dev_ptr);
+int csaidx_cuda_ipc_close(csaidx_engine* e, void* dev_ptr);
 int csaidx_engine_num_sms(csaidx_engine* e, int* num_sms);
 /* SM partition for running a select beside the score kernel: score launches
  * use at most score_sms CTAs (one per SM) and select launches run as

@@ -426,6 +426,32 @@ def driver_engine(device: int = 0):
     return h
 
 
+def set_index_sink(engine, dst_ptr: int | None, seq_len: int = 0):
+    """csaidx_engine_set_index_sink: final rows are also stored as int32 into
+    the [B, seq_len, k] buffer at dst_ptr (possibly a peer GPU's, see ipc_open);
+    None disables."""
+    _check_cuda(_capi.cuda_lib().csaidx_engine_set_index_sink(engine, c_void_p(dst_ptr or 0), seq_len))
+
+
+def ipc_handle(engine, dev_ptr: int) -> bytes:
+    """64-byte CUDA IPC handle of a device allocation."""
+    buf = ctypes.create_string_buffer(64)
+    _check_cuda(_capi.cuda_lib().csaidx_cuda_ipc_handle(engine, c_void_p(dev_ptr), buf))
+    return buf.raw
+
+
+def ipc_open(engine, handle: bytes) -> int:
+    """Maps another process's allocation (peer access enabled lazily)."""
+    ptr = c_void_p()
+    _check_cuda(_capi.cuda_lib().csaidx_cuda_ipc_open(engine, ctypes.create_string_buffer(handle, 64),
+                                                      ctypes.byref(ptr)))
+    return ptr.value
+
+
+def ipc_close(engine, dev_ptr: int):
+    _check_cuda(_capi.cuda_lib().csaidx_cuda_ipc_close(engine, c_void_p(dev_ptr)))
+
+
 class KernelStats:
     """Launch counts / event-timed device ms per kernel class of an engine."""
 

@@ -88,6 +88,8 @@ struct csaidx_engine {
     int lane = 0;
     cudaEvent_t slots[192] = {};
     cudaEvent_t entry_event = nullptr;  // csaidx_engine_await_stream
+    int32_t* sink = nullptr;            // csaidx_engine_set_index_sink
+    int64_t sink_seq = 0;
     // SM partition while a select runs beside the score kernel (0 = whole GPU)
     int score_sms = 0;
     int select_sms = 0;
@@ -464,6 +466,38 @@ int csaidx_cuda_copy(csaidx_engine* e, void* dst, const void* src, size_t bytes)
     return CSAIDX_OK;
 }
 
+int csaidx_engine_set_index_sink(csaidx_engine* e, int32_t* dst, int64_t seq_len) {
+    if (e == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null engine");
+    if (dst != nullptr && seq_len < 1) return fail(CSAIDX_INVALID_ARGUMENT, "index sink: seq_len must be >= 1");
+    e->sink = dst;
+    e->sink_seq = dst != nullptr ? seq_len : 0;
+    return CSAIDX_OK;
+}
+
+int csaidx_cuda_ipc_handle(csaidx_engine* e, void* dev_ptr, void* handle) {
+    if (int rc = set_device(e)) return rc;
+    if (dev_ptr == nullptr || handle == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "ipc_handle: null argument");
+    cudaIpcMemHandle_t h;
+    CSAIDX_CUDA_TRY(cudaIpcGetMemHandle(&h, dev_ptr), "cudaIpcGetMemHandle");
+    std::memcpy(handle, &h, sizeof(h));
+    return CSAIDX_OK;
+}
+
+int csaidx_cuda_ipc_open(csaidx_engine* e, const void* handle, void** dev_ptr) {
+    if (int rc = set_device(e)) return rc;
+    if (dev_ptr == nullptr || handle == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "ipc_open: null argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    CSAIDX_CUDA_TRY(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    return CSAIDX_OK;
+}
+
+int csaidx_cuda_ipc_close(csaidx_engine* e, void* dev_ptr) {
+    if (int rc = set_device(e)) return rc;
+    CSAIDX_CUDA_TRY(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
+    return CSAIDX_OK;
+}
+
 int csaidx_cuda_host_alloc(csaidx_engine* e, size_t bytes, void** ptr) {
     if (int rc = set_device(e)) return rc;
     if (ptr == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "host_alloc: null out pointer");
@@ -758,6 +792,10 @@ int select_impl(csaidx_engine* e, const float* scores, int64_t batch, int64_t ro
     p.final_idx = final_idx;
     p.final_rows = final_rows;
     p.final_row0 = final_row0;
+    if (final_idx != nullptr) {
+        p.sink = e->sink;
+        p.sink_seq = e->sink_seq;
+    }
     p.persistent_ctas = e->select_sms;
     p.gmax = gmax;
     p.gmax_ld = gmax_ld;
@@ -854,6 +892,8 @@ int csaidx_cuda_finalize(csaidx_engine* e, const float* run_val, const int32_t* 
     p.out_row0 = out_row0;
     p.trail_flag = e->flags + kTrail;
     p.keff_flag = e->flags + kKeff;
+    p.sink = e->sink;
+    p.sink_seq = e->sink_seq;
     LaunchScope ls(e, CSAIDX_KIND_FINALIZE);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_finalize(p, e->stream), "finalize");
     return CSAIDX_OK;

@@ -107,6 +107,11 @@ struct SelectParams {
     // > 0: run as that many persistent CTAs, one per SM, each with several
     // row groups (to share the GPU with a concurrently running score kernel)
     int persistent_ctas;
+    // Optional index sink (with final_idx): row r of batch b is also stored
+    // as int32 indices at sink + (b * sink_seq + s0 + r) * out_ld — a [B, S, k]
+    // buffer that may live in another GPU's memory (CUDA IPC peer mapping)
+    int32_t* sink;
+    int64_t sink_seq;
 };
 
 // Per-row candidate threshold from a strided sample of the row's scores
@@ -155,6 +160,8 @@ struct FinalizeParams {
     int64_t out_rows, out_row0;
     int* trail_flag;        // sentinel entries do not trail
     int* keff_flag;         // valid != k_eff
+    int32_t* sink;          // optional [B, sink_seq, k] int32 copy (SelectParams::sink)
+    int64_t sink_seq;
 };
 
 // ------------------------------------------------------------------ prep

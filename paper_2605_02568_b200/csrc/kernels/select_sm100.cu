@@ -604,16 +604,20 @@ __device__ void write_row(const SelectParams& p, int b, int64_t row_id, int take
     const float neg_inf = -__int_as_float(0x7f800000);
     if (final_out) {
         int64_t* oi = p.final_idx + orow * p.out_ld;
+        int32_t* si = p.sink != nullptr ? p.sink + (static_cast<int64_t>(b) * p.sink_seq + p.s0 + row_id) * p.out_ld
+                                        : nullptr;
         for (int e = gtid(); e < p.width; e += kThreads) {
+            int64_t idx = -1;
             if (e < take) {
                 const uint64_t c = result[e];
                 const float v = ord_key_to_float(static_cast<uint32_t>(c >> 32));
                 ov[e] = v;
-                oi[e] = v == neg_inf ? -1 : composite_col(c) + p.t0;
+                idx = v == neg_inf ? -1 : composite_col(c) + p.t0;
             } else {
                 ov[e] = neg_inf;
-                oi[e] = -1;
             }
+            oi[e] = idx;
+            if (si != nullptr) si[e] = static_cast<int32_t>(idx);  // peer store when the sink is remote
         }
         return;
     }

@@ -379,3 +379,75 @@ def test_host_rounding_matches_device_rounding(orc, monkeypatch):
         with pytest.raises(InvalidArgument):
             api.run_chunked_rows(inexact, kcf, w3, dims, strict, starts, oi, ov)
         api.run_chunked_rows(inexact, kcf, w3, dims, cfg, starts, oi, ov)  # rounds when not strict
+
+
+@pytest.mark.parametrize("key_tile", [10 ** 6, 512])
+def test_index_sink_receives_the_final_rows(orc, key_tile):
+    """csaidx_engine_set_index_sink: the final kernels (select_final with one
+    key tile, finalize after merges) also store each row's indices as int32
+    at its sequence position in a [B, S, k] buffer."""
+    import torch
+
+    q, kc, w = orc.generate_inputs(2, 4096, 4, 64, 128, 17, bf16=True)
+    dims = api.ProblemDims.create(2, 4096, 4, 64, 128, 128)
+    cfg = api.DriverConfig(tile=api.TileConfig(512, key_tile))
+    qd, kd, wd = (torch.from_numpy(a).cuda() for a in (q, kc, w))
+    qd, kd = qd.to(torch.bfloat16), kd.to(torch.bfloat16)
+    starts = [3584, 512, 2048]
+    h = api.driver_engine(0)
+    sink = torch.full((2, 4096, 128), -7, dtype=torch.int32, device="cuda")
+    api.set_index_sink(h, sink.data_ptr(), 4096)
+    try:
+        oi, _, _ = api.run_chunked_device(qd, kd, wd, dims, cfg, starts)
+    finally:
+        api.set_index_sink(h, None)
+    torch.cuda.synchronize()
+    for n, s0 in enumerate(starts):
+        assert torch.equal(sink[:, s0:s0 + 512], oi[:, n * 512:(n + 1) * 512].to(torch.int32))
+    untouched = torch.ones(4096, dtype=torch.bool)
+    for s0 in starts:
+        untouched[s0:s0 + 512] = False
+    assert bool((sink[:, untouched] == -7).all())
+
+
+def _sink_child(handle, q, kc, w, starts, done):
+    import torch
+
+    from paper_2605_02568_b200 import api as capi
+
+    h = capi.driver_engine(0)
+    ptr = capi.ipc_open(h, handle)
+    capi.set_index_sink(h, ptr, 4096)
+    dims = capi.ProblemDims.create(1, 4096, 4, 64, 128, 64)
+    cfg = capi.DriverConfig(tile=capi.TileConfig(512, 10 ** 6))
+    qd, kd, wd = (torch.from_numpy(a).cuda() for a in (q, kc, w))
+    oi, _, _ = capi.run_chunked_device(qd.to(torch.bfloat16), kd.to(torch.bfloat16), wd, dims, cfg, starts)
+    capi.set_index_sink(h, None)
+    torch.cuda.synchronize()
+    capi.ipc_close(h, ptr)
+    done.put(int(oi.sum().item()))
+
+
+def test_index_sink_through_cuda_ipc_from_another_process(orc):
+    """The fused gather of a query-sharded run: another process (a rank)
+    writes its final rows into this process's buffer through a CUDA IPC
+    mapping (same GPU here; peer GPUs over NVLink in a multi-GPU run)."""
+    import torch
+    import torch.multiprocessing as mp
+
+    q, kc, w = orc.generate_inputs(1, 4096, 4, 64, 128, 23, bf16=True)
+    sink = torch.full((1, 4096, 64), -7, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    handle = api.ipc_handle(api.driver_engine(0), sink.data_ptr())
+    starts = [1024, 3072]
+    ctx = mp.get_context("spawn")
+    done = ctx.Queue()
+    p = ctx.Process(target=_sink_child, args=(handle, q, kc, w, starts, done))
+    p.start()
+    total = done.get(timeout=300)
+    p.join(timeout=60)
+    assert p.exitcode == 0
+    got = sink.cpu().numpy()
+    rows = np.r_[1024:1536, 3072:3584]
+    assert int(got[:, rows].astype(np.int64).sum()) == total
+    assert got[:, rows].min() >= -1 and (np.delete(got, rows, axis=1) == -7).all()
