@@ -180,6 +180,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
             if (si != nullptr) si[e] = inf ? -1 : ri[e];
         }
     }
+    if (si != nullptr) __threadfence_system();  // peer stores performed before the kernel retires
     if (first_inf < p.k) atomicMin(&s_first, first_inf);
     if (real != 0) atomicAdd(&s_real, real);
     __syncthreads();

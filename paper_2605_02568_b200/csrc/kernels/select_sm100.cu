@@ -619,6 +619,7 @@ __device__ void write_row(const SelectParams& p, int b, int64_t row_id, int take
             oi[e] = idx;
             if (si != nullptr) si[e] = static_cast<int32_t>(idx);  // peer store when the sink is remote
         }
+        if (si != nullptr) __threadfence_system();  // the peer stores are performed before the kernel retires
         return;
     }
     int32_t* oi = p.out_idx + orow * p.out_ld;
