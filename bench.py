@@ -288,7 +288,7 @@ def main():
     granges = [group_rows(sh) for sh in shards]          # [rank][group] -> (r0, r1)
     gmax = [max(gr[j][1] - gr[j][0] for gr in granges) for j in range(G)]
     max_rows = max(api.chunk_rows(dims, cfg, sh) for sh in shards)
-    pad = max(gmax)
+    pad = max(gmax) if G > 1 else 0  # grouped gather: group j may be sent padded to the longest shard
     gathered = None
     if plan_rank == 0 and plan_world > 1 and not p2p:  # also in --simulate-rank 0/N, for peak HBM
         gathered = torch.empty((plan_world, B, max_rows + pad, k), dtype=torch.int32, device="cuda")
