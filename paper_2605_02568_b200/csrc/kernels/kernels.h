@@ -175,6 +175,16 @@ struct ConvertParams {
 
 namespace csaidx_kern {
 
+// Function attributes (cudaFuncSetAttribute) belong to a device context:
+// launchers keep one "already set" flag per device.
+constexpr int kMaxDevices = 64;
+inline int attr_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d < 0 ? 0 : (d >= kMaxDevices ? kMaxDevices - 1 : d);
+}
+
+
 bool score_tc_supported(int64_t heads, int64_t head_dim);
 size_t score_tc_smem_bytes();
 int score_tc_q_box_rows();  // rows of the q TMA box (one query group x 64 heads)

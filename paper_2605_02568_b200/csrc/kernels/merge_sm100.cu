@@ -203,12 +203,13 @@ cudaError_t launch_merge(const MergeParams& p, cudaStream_t stream) {
     if (p.nrows <= 0) return cudaSuccess;
     if (p.k > kMaxK) return cudaErrorInvalidValue;
     const size_t smem = (static_cast<size_t>(p.k) + static_cast<size_t>(p.width)) * sizeof(uint64_t);
-    static bool attr_set = false;
-    if (!attr_set) {
+    static bool attr_set[kMaxDevices] = {};
+    const int attr_set_dev = attr_device();
+    if (!attr_set[attr_set_dev]) {
         cudaError_t e = cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(2 * kMaxK * sizeof(uint64_t)));
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_set[attr_set_dev] = true;
     }
     merge_kernel<<<static_cast<unsigned>(p.nrows), kMergeThreads, smem, stream>>>(p);
     return cudaGetLastError();

@@ -651,15 +651,16 @@ cudaError_t launch_score_tc(const CUtensorMap& qmap, const CUtensorMap& kmap, Sc
     for (int pc = 0; pc < p.npieces; ++pc) p.piece_start[pc + 1] = p.piece_start[pc] + count[pc] * p.batch;
     p.nitems = p.piece_start[p.npieces];
     if (p.nitems <= 0) return cudaSuccess;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static bool attr_set[kMaxDevices] = {};
+    const int attr_set_dev = attr_device();
+    if (!attr_set[attr_set_dev]) {
         for (auto* fn : {score_tc_kernel<0, false>, score_tc_kernel<0, true>, score_tc_kernel<1, false>,
                          score_tc_kernel<2, false>, score_tc_kernel<3, false>}) {
             cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  static_cast<int>(kSmemBytes));
             if (e != cudaSuccess) return e;
         }
-        attr_set = true;
+        attr_set[attr_set_dev] = true;
     }
     const int grid = p.nitems < num_sms ? p.nitems : num_sms;
     if (p.tau != nullptr)

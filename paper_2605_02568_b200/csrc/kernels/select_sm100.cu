@@ -1147,12 +1147,13 @@ cudaError_t launch_tau(const TauParams& p, cudaStream_t stream) {
 namespace {
 template <int U, int MB>
 cudaError_t launch_select_variant(const SelectParams& p, cudaStream_t stream) {
-    static bool attr_set = false;
-    if (!attr_set) {
+    static bool attr_set[kMaxDevices] = {};
+    const int attr_set_dev = attr_device();
+    if (!attr_set[attr_set_dev]) {
         cudaError_t e = cudaFuncSetAttribute(select_kernel<U, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem_bytes_for(kMaxTake)));
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_set[attr_set_dev] = true;
     }
     const dim3 grid(static_cast<unsigned>(p.rows), static_cast<unsigned>(p.batch));
     select_kernel<U, MB><<<grid, kThreads, smem_bytes_for(p.k), stream>>>(p);
@@ -1176,12 +1177,13 @@ bool select_fat_fits(int k) { return kFatGroups * smem_bytes_for(k) <= kFatSmemM
 cudaError_t launch_select(const SelectParams& p, cudaStream_t stream) {
     if (p.rows <= 0 || p.batch <= 0) return cudaSuccess;
     if (p.persistent_ctas > 0 && p.phase_clk == nullptr && select_fat_fits(p.k)) {
-        static bool fat_attr = false;
-        if (!fat_attr) {
+        static bool fat_attr[kMaxDevices] = {};
+        const int fat_attr_dev = attr_device();
+        if (!fat_attr[fat_attr_dev]) {
             cudaError_t e = cudaFuncSetAttribute(select_fat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  static_cast<int>(kFatSmemMax));
             if (e != cudaSuccess) return e;
-            fat_attr = true;
+            fat_attr[fat_attr_dev] = true;
         }
         select_fat_kernel<<<p.persistent_ctas, kThreads * kFatGroups, kFatGroups * smem_bytes_for(p.k), stream>>>(p);
         return cudaGetLastError();
