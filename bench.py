@@ -423,7 +423,7 @@ def main():
             gather_ok = bool(ok)
         dist.barrier()
         if rank != 0:
-            api.ipc_close(drv_h, sink_ptr)
+            api.ipc_close(drv_h, sink_ptr, handle[0])
     elif world > 1 and rank == 0:
         # the gathered rows reassemble into sequence order (checked once, untimed)
         from paper_2605_02568_b200.shard import assemble

@@ -96,10 +96,14 @@ int csaidx_engine_await_stream(csaidx_engine* e, void* stream);
  * assembles TopKResult rows; SURVEY §8e's gather) into the select.
  * NULL disables. */
 int csaidx_engine_set_index_sink(csaidx_engine* e, int32_t* dst, int64_t seq_len);
-/* CUDA IPC of a device allocation (64-byte handle) for the index sink. */
-int csaidx_cuda_ipc_handle(csaidx_engine* e, void* dev_ptr, void* handle);
-int csaidx_cuda_ipc_open(csaidx_engine* e, const void* handle, void** dev_ptr);
-int csaidx_cuda_ipc_close(csaidx_engine* e, void* dev_ptr);
+/* CUDA IPC of a device pointer for the index sink: a 64-byte handle of the
+ * allocation that holds dev_ptr plus dev_ptr's offset inside it (caching
+ * allocators hand out blocks inside larger allocations). open maps the
+ * allocation in this process and returns the same byte; close takes the
+ * pointer open returned and the same offset. */
+int csaidx_cuda_ipc_handle(csaidx_engine* e, void* dev_ptr, void* handle, uint64_t* offset);
+int csaidx_cuda_ipc_open(csaidx_engine* e, const void* handle, uint64_t offset, void** dev_ptr);
+int csaidx_cuda_ipc_close(csaidx_engine* e, void* dev_ptr, uint64_t offset);
 int csaidx_engine_num_sms(csaidx_engine* e, int* num_sms);
 /* SM partition for running a select beside the score kernel: score launches
  * use at most score_sms CTAs (one per SM) and select launches run as

@@ -433,23 +433,26 @@ def set_index_sink(engine, dst_ptr: int | None, seq_len: int = 0):
     _check_cuda(_capi.cuda_lib().csaidx_engine_set_index_sink(engine, c_void_p(dst_ptr or 0), seq_len))
 
 
-def ipc_handle(engine, dev_ptr: int) -> bytes:
-    """64-byte CUDA IPC handle of a device allocation."""
+def ipc_handle(engine, dev_ptr: int) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of the allocation holding dev_ptr, offset)."""
     buf = ctypes.create_string_buffer(64)
-    _check_cuda(_capi.cuda_lib().csaidx_cuda_ipc_handle(engine, c_void_p(dev_ptr), buf))
-    return buf.raw
+    off = c_uint64()
+    _check_cuda(_capi.cuda_lib().csaidx_cuda_ipc_handle(engine, c_void_p(dev_ptr), buf, ctypes.byref(off)))
+    return buf.raw, off.value
 
 
-def ipc_open(engine, handle: bytes) -> int:
-    """Maps another process's allocation (peer access enabled lazily)."""
+def ipc_open(engine, handle: tuple[bytes, int]) -> int:
+    """Maps another process's allocation (peer access enabled lazily); the
+    returned pointer addresses the same byte as the exporter's dev_ptr."""
+    raw, off = handle
     ptr = c_void_p()
-    _check_cuda(_capi.cuda_lib().csaidx_cuda_ipc_open(engine, ctypes.create_string_buffer(handle, 64),
+    _check_cuda(_capi.cuda_lib().csaidx_cuda_ipc_open(engine, ctypes.create_string_buffer(raw, 64), off,
                                                       ctypes.byref(ptr)))
     return ptr.value
 
 
-def ipc_close(engine, dev_ptr: int):
-    _check_cuda(_capi.cuda_lib().csaidx_cuda_ipc_close(engine, c_void_p(dev_ptr)))
+def ipc_close(engine, dev_ptr: int, handle: tuple[bytes, int]):
+    _check_cuda(_capi.cuda_lib().csaidx_cuda_ipc_close(engine, c_void_p(dev_ptr), handle[1]))
 
 
 class KernelStats:

@@ -60,6 +60,25 @@ EncodeTiledFn get_encode_fn() {
     return fn;
 }
 
+using AddressRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+// cuMemGetAddressRange: the base of the allocation holding a pointer (CUDA
+// IPC maps whole allocations; a caching allocator's block may sit at an
+// offset inside one).
+AddressRangeFn get_range_fn() {
+    static AddressRangeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess) {
+            fn = reinterpret_cast<AddressRangeFn>(ptr);
+        }
+    });
+    return fn;
+}
+
 }  // namespace
 
 struct csaidx_engine {
@@ -474,27 +493,37 @@ int csaidx_engine_set_index_sink(csaidx_engine* e, int32_t* dst, int64_t seq_len
     return CSAIDX_OK;
 }
 
-int csaidx_cuda_ipc_handle(csaidx_engine* e, void* dev_ptr, void* handle) {
+int csaidx_cuda_ipc_handle(csaidx_engine* e, void* dev_ptr, void* handle, uint64_t* offset) {
     if (int rc = set_device(e)) return rc;
-    if (dev_ptr == nullptr || handle == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "ipc_handle: null argument");
+    if (dev_ptr == nullptr || handle == nullptr || offset == nullptr)
+        return fail(CSAIDX_INVALID_ARGUMENT, "ipc_handle: null argument");
+    AddressRangeFn range = get_range_fn();
+    if (range == nullptr) return fail(CSAIDX_CUDA_ERROR, "cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+        return fail(CSAIDX_INVALID_ARGUMENT, "ipc_handle: not a device allocation");
     cudaIpcMemHandle_t h;
-    CSAIDX_CUDA_TRY(cudaIpcGetMemHandle(&h, dev_ptr), "cudaIpcGetMemHandle");
+    CSAIDX_CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)), "cudaIpcGetMemHandle");
     std::memcpy(handle, &h, sizeof(h));
+    *offset = reinterpret_cast<CUdeviceptr>(dev_ptr) - base;
     return CSAIDX_OK;
 }
 
-int csaidx_cuda_ipc_open(csaidx_engine* e, const void* handle, void** dev_ptr) {
+int csaidx_cuda_ipc_open(csaidx_engine* e, const void* handle, uint64_t offset, void** dev_ptr) {
     if (int rc = set_device(e)) return rc;
     if (dev_ptr == nullptr || handle == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "ipc_open: null argument");
     cudaIpcMemHandle_t h;
     std::memcpy(&h, handle, sizeof(h));
-    CSAIDX_CUDA_TRY(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    void* base = nullptr;
+    CSAIDX_CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    *dev_ptr = static_cast<char*>(base) + offset;
     return CSAIDX_OK;
 }
 
-int csaidx_cuda_ipc_close(csaidx_engine* e, void* dev_ptr) {
+int csaidx_cuda_ipc_close(csaidx_engine* e, void* dev_ptr, uint64_t offset) {
     if (int rc = set_device(e)) return rc;
-    CSAIDX_CUDA_TRY(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
+    CSAIDX_CUDA_TRY(cudaIpcCloseMemHandle(static_cast<char*>(dev_ptr) - offset), "cudaIpcCloseMemHandle");
     return CSAIDX_OK;
 }
 

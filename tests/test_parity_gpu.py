@@ -424,7 +424,7 @@ def _sink_child(handle, q, kc, w, starts, done):
     oi, _, _ = capi.run_chunked_device(qd.to(torch.bfloat16), kd.to(torch.bfloat16), wd, dims, cfg, starts)
     capi.set_index_sink(h, None)
     torch.cuda.synchronize()
-    capi.ipc_close(h, ptr)
+    capi.ipc_close(h, ptr, handle)
     done.put(int(oi.sum().item()))
 
 
@@ -436,7 +436,8 @@ def test_index_sink_through_cuda_ipc_from_another_process(orc):
     import torch.multiprocessing as mp
 
     q, kc, w = orc.generate_inputs(1, 4096, 4, 64, 128, 23, bf16=True)
-    sink = torch.full((1, 4096, 64), -7, dtype=torch.int32, device="cuda")
+    backing = torch.full((4096 * 64 + 4096,), -7, dtype=torch.int32, device="cuda")
+    sink = backing[4096:].view(1, 4096, 64)  # at an offset inside the allocation
     torch.cuda.synchronize()
     handle = api.ipc_handle(api.driver_engine(0), sink.data_ptr())
     starts = [1024, 3072]
