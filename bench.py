@@ -270,7 +270,30 @@ def main():
     # store every rank's int32 index rows straight into rank 0's [B, S, k]
     # buffer through a CUDA IPC peer mapping (NVLink), fused with the select.
     p2p = args.gather == "p2p" and world > 1
-    G = max(1, args.gather_groups) if (world > 1 or plan_world > 1) and B == 1 and args.gather == "nccl" else 1
+    drv_h = api.driver_engine(local)
+    sink = sink_ptr = None
+    handle = [None]
+    if p2p:
+        try:
+            if rank == 0:
+                sink = torch.full((B, S, k), -2, dtype=torch.int32, device="cuda")
+                handle = [api.ipc_handle(drv_h, sink.data_ptr())]
+            dist.broadcast_object_list(handle, src=0)
+            sink_ptr = sink.data_ptr() if rank == 0 else api.ipc_open(drv_h, handle[0])
+            ok = True
+        except Exception as ex:  # no CUDA IPC / peer access here: fall back to the NCCL gather
+            print(f"rank {rank}: peer index sink unavailable ({ex}); using the NCCL gather", file=sys.stderr)
+            ok = False
+        oks = [None] * world
+        dist.all_gather_object(oks, ok)
+        if all(oks):
+            api.set_index_sink(drv_h, sink_ptr, S)
+        else:
+            if ok and rank != 0:
+                api.ipc_close(drv_h, sink_ptr, handle[0])
+            p2p, sink, sink_ptr = False, None, None
+    G = max(1, args.gather_groups) if (world > 1 or plan_world > 1) and B == 1 and not p2p and \
+        not (world == 1 and args.gather == "p2p") else 1
 
     def split(lst):
         n = len(lst)
@@ -338,17 +361,6 @@ def main():
 
     stats_box = {}
 
-    drv_h = api.driver_engine(local)
-    sink = sink_ptr = None
-    if p2p:
-        if rank == 0:
-            sink = torch.full((B, S, k), -2, dtype=torch.int32, device="cuda")
-            handle = [api.ipc_handle(drv_h, sink.data_ptr())]
-        else:
-            handle = [None]
-        dist.broadcast_object_list(handle, src=0)
-        sink_ptr = sink.data_ptr() if rank == 0 else api.ipc_open(drv_h, handle[0])
-        api.set_index_sink(drv_h, sink_ptr, S)
     flag = torch.zeros(1, dtype=torch.int32, device="cuda") if p2p else None
 
     def step():
