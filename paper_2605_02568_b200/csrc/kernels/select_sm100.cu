@@ -28,6 +28,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "kernels.h"
 #include "sm100_ptx.cuh"
@@ -948,16 +949,18 @@ __device__ __forceinline__ void select_row(const SelectParams& p, int b, int64_t
                     const int64_t i4 = it + u * kThreads;
                     v[u] = i4 < n4 ? __ldg(row4 + i4) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
                 }
-                uint32_t m = 0;
+                // one bit per entry: 4 * kUnroll bits (64-bit mask above 8 float4)
+                using Mask = typename std::conditional<(kUnroll > 8), unsigned long long, uint32_t>::type;
+                Mask m = 0;
 #pragma unroll
                 for (int u = 0; u < kUnroll; ++u) {
-                    m |= (v[u].x >= tau_f ? 1u : 0u) << (4 * u + 0);
-                    m |= (v[u].y >= tau_f ? 1u : 0u) << (4 * u + 1);
-                    m |= (v[u].z >= tau_f ? 1u : 0u) << (4 * u + 2);
-                    m |= (v[u].w >= tau_f ? 1u : 0u) << (4 * u + 3);
+                    m |= static_cast<Mask>(v[u].x >= tau_f ? 1u : 0u) << (4 * u + 0);
+                    m |= static_cast<Mask>(v[u].y >= tau_f ? 1u : 0u) << (4 * u + 1);
+                    m |= static_cast<Mask>(v[u].z >= tau_f ? 1u : 0u) << (4 * u + 2);
+                    m |= static_cast<Mask>(v[u].w >= tau_f ? 1u : 0u) << (4 * u + 3);
                 }
                 if (!__any_sync(0xffffffffu, m != 0)) continue;
-                const uint32_t c = __popc(m);
+                const uint32_t c = kUnroll > 8 ? __popcll(m) : __popc(static_cast<uint32_t>(m));
                 uint32_t incl = c;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -973,7 +976,8 @@ __device__ __forceinline__ void select_row(const SelectParams& p, int b, int64_t
                 // column only: the divergent body stays a handful of
                 // instructions.
                 while (m != 0) {
-                    const int bit = __ffs(m) - 1;
+                    const int bit = kUnroll > 8 ? __ffsll(static_cast<long long>(m)) - 1
+                                                : __ffs(static_cast<int>(m)) - 1;
                     m &= m - 1;
                     if (pos < cap)
                         idx_list[pos] = static_cast<uint32_t>(4 * (it + (bit >> 2) * kThreads) + (bit & 3));
@@ -1162,7 +1166,7 @@ cudaError_t launch_select_variant(const SelectParams& p, cudaStream_t stream) {
 
 int select_variant() {
     static int v = [] {
-        const char* s = getenv("CSAIDX_SELECT_VARIANT");  // A/B knob (dev): 0 = by k, 1 = 4 x float4 / 4 CTAs, 2 = 8 x float4 / 4 CTAs
+        const char* s = getenv("CSAIDX_SELECT_VARIANT");  // A/B knob (dev): 0 = by k, 1 = 4 x float4 / 4 CTAs, 2 = 8 x float4 / 4 CTAs, 3 = 8 x float4 / 3 CTAs
         return s != nullptr ? atoi(s) : 0;
     }();
     return v;
@@ -1197,11 +1201,15 @@ cudaError_t launch_select(const SelectParams& p, cudaStream_t stream) {
     // persistent warp-specialised form streaming rows through a TMA
     // bulk-copy ring (2 CTAs/SM; 3.7 vs 5.3 TB/s on long rows).
     if (select_variant() == 1) return launch_select_variant<4, 4>(p, stream);
+    if (select_variant() == 3) return launch_select_variant<8, 3>(p, stream);
     // k <= 512 (<= 29 KB of shared memory per row): a 4th CTA per SM at 64
     // registers pays off (0.080 vs 0.087 ms on 2048 rows of 32K at k = 512);
     // at k = 1024 the register-starved stream loses (0.109 vs 0.102 ms)
     if (p.k <= 512 || select_variant() == 2) return launch_select_variant<8, 4>(p, stream);
-    return launch_select_variant<8, 3>(p, stream);
+    // 16 float4 (256 B) per thread per iteration at 3 CTAs per SM (80
+    // registers, no spills): 2-3% faster than 8 (0.101 vs 0.104 ms at
+    // n = 32K, 0.407 vs 0.418 ms at n = 256K; variant 3 = the 8-float4 form)
+    return launch_select_variant<16, 3>(p, stream);
 }
 
 }  // namespace csaidx_kern
