@@ -149,7 +149,8 @@ def test_score_exact_is_bit_exact(engine, H, D, fp16):
         assert np.all(np.isfinite(got))
 
 
-@pytest.mark.parametrize("cols,k,quant", [(300, 16, False), (5000, 512, False), (20000, 1024, True), (9000, 2048, True), (7, 10, False)])
+@pytest.mark.parametrize("cols,k,quant", [(300, 16, False), (5000, 512, False), (20000, 1024, True), (9000, 2048, True),
+                                          (7, 10, False), (40000, 4096, False), (12000, 4096, True), (4096, 4096, False)])
 def test_select_matches_sorted_reference(engine, cols, k, quant):
     rng = np.random.default_rng(cols + k)
     B, rows, m = 2, 9, 1
@@ -499,3 +500,13 @@ def test_prefilter_falls_back_when_the_bitmap_is_unusable(engine, how):
         assert hits == int(np.sum(n_rows <= cap))
     if how == "all_ties":
         assert np.array_equal(fi[0, -1].cpu().numpy(), np.arange(k, dtype=np.int32))
+
+
+def test_select_rejects_k_above_capacity(engine):
+    """k beyond the GPU selection capacity (4096) fails loudly with
+    invalid_argument instead of falling back to a CPU path."""
+    from paper_2605_02568_b200._capi import InvalidArgument
+
+    x = torch.zeros((1, 2, 8192), dtype=torch.float32, device="cuda")
+    with pytest.raises(InvalidArgument):
+        engine.select(x, 1, 2, 8192, 10 ** 6, 0, 1, 4097)
