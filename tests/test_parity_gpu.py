@@ -452,3 +452,17 @@ def test_index_sink_through_cuda_ipc_from_another_process(orc):
     rows = np.r_[1024:1536, 3072:3584]
     assert int(got[:, rows].astype(np.int64).sum()) == total
     assert got[:, rows].min() >= -1 and (np.delete(got, rows, axis=1) == -7).all()
+
+
+def test_tensor_core_path_at_max_k_matches_reference_rule(orc):
+    """k = 4096 (the GPU selection capacity) through the pipelined host
+    entry on V4-shaped inputs: sampled rows (some with fewer than k legal
+    keys, some with 2k) obey the north-star rule against the oracle."""
+    S, m, k = 32768, 4, 4096
+    inputs, dims, (q, kc, w) = inputs_for(orc, 1, S, m, 64, 128, k, 5, bf16=True)
+    res, _ = api.run_chunked(inputs, dims, api.DriverConfig(tile=api.TileConfig(2048, S // m)))
+    rows = [100, 16383, 16387, 20000, 32767]
+    full = [orc.score_tile(q, kc, w, s, 0, 1, S // m)[0][0] for s in rows]
+    legal = [(s + 1) // m for s in rows]
+    rep = check_rows(res.indices[0][rows], res.values[0][rows], full, legal, k)
+    assert rep["rows"] == len(rows)
