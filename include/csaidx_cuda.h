@@ -112,6 +112,12 @@ int csaidx_engine_num_sms(csaidx_engine* e, int* num_sms);
 int csaidx_engine_set_partition(csaidx_engine* e, int score_sms, int select_sms);
 /* Synchronizes the stream, then reports (and clears) latched data errors. */
 int csaidx_engine_check(csaidx_engine* e);
+/* Synchronizes, then reports in *seen (and clears) whether a non-strict
+ * csaidx_cuda_to_bf16 since the last call met a value bf16 cannot represent.
+ * The host driver then re-runs on fp32 operands with the exact-order kernel,
+ * so ScoreKernel::auto_detect gives the reference's scores on any fp32 input
+ * (score.cpp:18-43 resolves auto to a kernel bit-identical to the scalar one). */
+int csaidx_engine_take_inexact(csaidx_engine* e, int* seen);
 /* Device bytes currently held / high-water through csaidx_cuda_alloc. */
 int csaidx_engine_mem_stats(csaidx_engine* e, uint64_t* live, uint64_t* peak);
 int csaidx_engine_reset_peak(csaidx_engine* e);
@@ -155,7 +161,8 @@ int csaidx_cuda_host_free(csaidx_engine* e, void* ptr);
 
 /* fp32 -> bf16 (RNE) staging of q / kc (IndexerInputs::validated,
  * types.cpp:73-92: rejects non-finite; strict also rejects values that are
- * not bf16-representable). src/dst are device pointers. */
+ * not bf16-representable, otherwise they are only noted for
+ * csaidx_engine_take_inexact). src/dst are device pointers. */
 int csaidx_cuda_to_bf16(csaidx_engine* e, const float* src, uint16_t* dst, int64_t n, int strict);
 
 /* Operand element type of q / kc on device. */

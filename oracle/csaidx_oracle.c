@@ -9,6 +9,7 @@
 #include "csaidx_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -219,6 +220,66 @@ void orc_score_tile(const float* q, const float* kc, const float* w, int64_t bat
                        out + (b * rows + i) * cols);
         }
     }
+}
+
+/* Threaded driver of score_span over independent rows (test infrastructure:
+ * the reference scores one row per call; the per-score op order is the
+ * same, so the split only changes which thread computes a score). */
+#define ORC_PIECE 4096
+typedef struct {
+    const float *q, *w, *kc;
+    const int64_t *kc_row0, *legal, *piece0, *offset;
+    int64_t nrows, npieces, heads, head_dim;
+    float* out;
+    int64_t next;
+    pthread_mutex_t mu;
+} rows_job;
+
+static void* rows_worker(void* arg) {
+    rows_job* j = (rows_job*)arg;
+    for (;;) {
+        pthread_mutex_lock(&j->mu);
+        const int64_t p = j->next++;
+        pthread_mutex_unlock(&j->mu);
+        if (p >= j->npieces) break;
+        int64_t r = 0; /* row owning piece p: piece0 is ascending */
+        int64_t lo = 0, hi = j->nrows - 1;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) / 2;
+            if (j->piece0[mid] <= p) lo = mid; else hi = mid - 1;
+        }
+        r = lo;
+        const int64_t c0 = (p - j->piece0[r]) * ORC_PIECE;
+        const int64_t n = j->legal[r] - c0 < ORC_PIECE ? j->legal[r] - c0 : ORC_PIECE;
+        score_span(j->q + r * j->heads * j->head_dim, j->w + r * j->heads,
+                   j->kc + (j->kc_row0[r] + c0) * j->head_dim, n, j->heads, j->head_dim, 0,
+                   j->out + j->offset[r] + c0);
+    }
+    return NULL;
+}
+
+void orc_score_rows(const float* q_rows, const float* w_rows, const float* kc, const int64_t* kc_row0,
+                    const int64_t* legal, int64_t nrows, int64_t heads, int64_t head_dim, int nthreads,
+                    float* out) {
+    if (nrows <= 0) return;
+    int64_t* piece0 = (int64_t*)malloc((size_t)nrows * sizeof(int64_t));
+    int64_t* offset = (int64_t*)malloc((size_t)nrows * sizeof(int64_t));
+    int64_t np = 0, off = 0;
+    for (int64_t r = 0; r < nrows; ++r) {
+        piece0[r] = np;
+        offset[r] = off;
+        np += (legal[r] + ORC_PIECE - 1) / ORC_PIECE;
+        off += legal[r];
+    }
+    rows_job j = {q_rows, w_rows, kc, kc_row0, legal, piece0, offset, nrows, np, heads, head_dim, out, 0,
+                  PTHREAD_MUTEX_INITIALIZER};
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t th[256];
+    for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, rows_worker, &j);
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+    free(piece0);
+    free(offset);
 }
 
 /* ------------------------------------------------------------ topk.cpp */

@@ -76,6 +76,17 @@ int64_t orc_row_topk(const float* q_row, const float* w_row, const float* kc, in
                      int64_t heads, int64_t head_dim, int64_t legal, int64_t k, float* out_v,
                      int64_t* out_i);
 
+/* Many full causal rows at once (the sampled-row oracle at scale): row r is
+ * query q_rows[r] ([heads, head_dim]) with weights w_rows[r] ([heads])
+ * against keys kc + kc_row0[r] * head_dim, over its first legal[r] keys;
+ * scores land at out + offset[r] (offset[r] = sum of legal[<r]). Each score
+ * follows score_scalar.cpp:20-34 exactly (score_span); the work is split in
+ * 4096-key pieces over nthreads POSIX threads, so results do not depend on
+ * the thread count. */
+void orc_score_rows(const float* q_rows, const float* w_rows, const float* kc, const int64_t* kc_row0,
+                    const int64_t* legal, int64_t nrows, int64_t heads, int64_t head_dim, int nthreads,
+                    float* out);
+
 /* recall.cpp:9-64 — returns rows evaluated; fills mean/min/pct_perfect. */
 int64_t orc_recall(const int64_t* ref_idx, const int64_t* test_idx, int64_t nrows, int64_t top_k,
                    double* mean, double* min_r, double* pct_perfect, double* pct_below99);

@@ -55,6 +55,7 @@ class Oracle:
                                                                        c_void_p]
         L.orc_row_topk.restype = c_int64
         L.orc_row_topk.argtypes = [c_void_p] * 3 + [c_int64] * 5 + [c_void_p, c_void_p]
+        L.orc_score_rows.argtypes = [c_void_p] * 5 + [c_int64] * 3 + [c_int, c_void_p]
         L.orc_recall.restype = c_int64
         L.orc_recall.argtypes = [c_void_p, c_void_p, c_int64, c_int64] + [POINTER(c_double)] * 4
 
@@ -100,6 +101,25 @@ class Oracle:
         out = np.empty((B, rows, cols), np.float32)
         self.L.orc_score_tile(_p(q), _p(kc), _p(w), B, S, T, H, D, s0, t0, rows, cols, int(fp16), _p(out))
         return out
+
+    def score_rows(self, q_rows, w_rows, kc, kc_row0, legal, threads=None):
+        """Full causal rows in the reference op order (orc_score_rows):
+        q_rows [n, H, D], w_rows [n, H], kc [rows, D] (row r uses keys
+        kc[kc_row0[r] : kc_row0[r] + legal[r]]). Returns a list of 1-D score
+        arrays (views into one buffer)."""
+        q_rows = np.ascontiguousarray(q_rows, np.float32)
+        w_rows = np.ascontiguousarray(w_rows, np.float32)
+        kc = np.ascontiguousarray(kc, np.float32)
+        n, H, D = q_rows.shape
+        r0 = np.ascontiguousarray(kc_row0, np.int64)
+        lg = np.ascontiguousarray(legal, np.int64)
+        assert r0.shape == (n,) and lg.shape == (n,) and w_rows.shape == (n, H)
+        assert np.all(r0 + lg <= kc.shape[0])
+        out = np.empty(max(int(lg.sum()), 1), np.float32)
+        self.L.orc_score_rows(_p(q_rows), _p(w_rows), _p(kc), _p(r0), _p(lg), n, H, D,
+                              int(threads or os.cpu_count() or 1), _p(out))
+        off = np.concatenate([[0], np.cumsum(lg)])
+        return [out[off[i]:off[i + 1]] for i in range(n)]
 
     def oracle_topk(self, row: np.ndarray, k: int, legal: int):
         row = np.ascontiguousarray(row, np.float32)

@@ -40,7 +40,19 @@ int cuda_fail(cudaError_t err, const char* where) {
         if (_e != cudaSuccess) return cuda_fail(_e, where); \
     } while (0)
 
-enum Flag { kNonfiniteScore = 0, kInexact = 1, kNonfiniteInput = 2, kTrail = 3, kKeff = 4, kOverlap = 5, kNumFlags = 8 };
+// kInexactSeen: a non-strict bf16 staging met a value bf16 cannot hold (not
+// an error: the host driver then re-runs on fp32 operands with the exact
+// kernel, csaidx_engine_take_inexact)
+enum Flag {
+    kNonfiniteScore = 0,
+    kInexact = 1,
+    kNonfiniteInput = 2,
+    kTrail = 3,
+    kKeff = 4,
+    kOverlap = 5,
+    kInexactSeen = 6,
+    kNumFlags = 8
+};
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -354,9 +366,12 @@ int csaidx_engine_check(csaidx_engine* e) {
     int h[kNumFlags];
     CSAIDX_CUDA_TRY(cudaMemcpy(h, e->flags, sizeof(h), cudaMemcpyDeviceToHost), "flags D2H");
     bool any = false;
-    for (int f : h) any = any || f != 0;
+    for (int i = 0; i < kNumFlags; ++i) any = any || (i != kInexactSeen && h[i] != 0);
     if (!any) return CSAIDX_OK;
-    CSAIDX_CUDA_TRY(cudaMemset(e->flags, 0, sizeof(h)), "flags reset");
+    // reset the error flags; kInexactSeen is consumed by csaidx_engine_take_inexact
+    CSAIDX_CUDA_TRY(cudaMemset(e->flags, 0, kInexactSeen * sizeof(int)), "flags reset");
+    CSAIDX_CUDA_TRY(cudaMemset(e->flags + kInexactSeen + 1, 0, (kNumFlags - kInexactSeen - 1) * sizeof(int)),
+                    "flags reset");
     if (h[kNonfiniteInput]) return fail(CSAIDX_INVALID_ARGUMENT, "IndexerInputs: non-finite entry in q/kc");
     if (h[kInexact]) return fail(CSAIDX_INVALID_ARGUMENT, "operand is not bf16-representable (strict mode)");
     if (h[kOverlap]) return fail(CSAIDX_INVALID_ARGUMENT, "merge_topk: overlapping indices between buffer and tile");
@@ -364,6 +379,21 @@ int csaidx_engine_check(csaidx_engine* e) {
     if (h[kTrail]) return fail(CSAIDX_LOGIC_ERROR, "run_chunked: sentinel entries do not trail");
     if (h[kKeff]) return fail(CSAIDX_LOGIC_ERROR, "run_chunked: row valid count != k_eff");
     return fail(CSAIDX_LOGIC_ERROR, "unknown device flag");
+}
+
+int csaidx_engine_take_inexact(csaidx_engine* e, int* seen) {
+    if (int rc = set_device(e)) return rc;
+    if (seen == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "take_inexact: null out pointer");
+    CSAIDX_CUDA_TRY(cudaStreamSynchronize(e->stream), "cudaStreamSynchronize");
+    for (int i = 0; i < 4; ++i) {
+        cudaStream_t s = i == 0 ? e->main_stream : e->lanes[i];
+        if (s != nullptr && s != e->stream) CSAIDX_CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize(lane)");
+    }
+    int h = 0;
+    CSAIDX_CUDA_TRY(cudaMemcpy(&h, e->flags + kInexactSeen, sizeof(int), cudaMemcpyDeviceToHost), "flag D2H");
+    if (h != 0) CSAIDX_CUDA_TRY(cudaMemset(e->flags + kInexactSeen, 0, sizeof(int)), "flag reset");
+    *seen = h != 0;
+    return CSAIDX_OK;
 }
 
 int csaidx_engine_mem_stats(csaidx_engine* e, uint64_t* live, uint64_t* peak) {
@@ -552,7 +582,7 @@ int csaidx_cuda_memset(csaidx_engine* e, void* dst, int value, size_t bytes) {
 int csaidx_cuda_to_bf16(csaidx_engine* e, const float* src, uint16_t* dst, int64_t n, int strict) {
     if (int rc = set_device(e)) return rc;
     if (n < 0) return fail(CSAIDX_INVALID_ARGUMENT, "to_bf16: negative length");
-    ConvertParams p{src, reinterpret_cast<__nv_bfloat16*>(dst), n, strict ? e->flags + kInexact : nullptr,
+    ConvertParams p{src, reinterpret_cast<__nv_bfloat16*>(dst), n, e->flags + (strict ? kInexact : kInexactSeen),
                     e->flags + kNonfiniteInput};
     LaunchScope ls(e, CSAIDX_KIND_PREP);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_convert_bf16(p, e->stream), "convert_bf16");

@@ -179,6 +179,22 @@ void stage_bf16(csaidx_engine* e, DeviceBuffer& dst, int64_t dst_off, const floa
 StagedOperands::StagedOperands(csaidx_engine* e, const HostView& host, const ProblemDims& dims, int dtype,
                                bool strict, const std::vector<std::pair<int64_t, int64_t>>* row_ranges)
     : dtype_(dtype) {
+    stage(e, host, dims, strict, row_ranges);
+    if (dtype_ == CSAIDX_DTYPE_BF16 && !strict) {
+        // auto_detect on operands bf16 cannot hold: the exact-order kernel on
+        // fp32 operands (the reference's auto scores any fp32 input exactly)
+        int seen = 0;
+        check(csaidx_engine_take_inexact(e, &seen));
+        if (seen) {
+            dtype_ = CSAIDX_DTYPE_F32;
+            stage(e, host, dims, strict, row_ranges);
+        }
+    }
+}
+
+void StagedOperands::stage(csaidx_engine* e, const HostView& host, const ProblemDims& dims, bool strict,
+                           const std::vector<std::pair<int64_t, int64_t>>* row_ranges) {
+    const int dtype = dtype_;
     const int64_t nq = dims.q_elems(), nk = dims.kc_elems(), nw = dims.w_elems();
     const size_t esz = dtype == CSAIDX_DTYPE_BF16 ? 2 : 4;
     q_ = DeviceBuffer(e, static_cast<size_t>(nq) * esz);

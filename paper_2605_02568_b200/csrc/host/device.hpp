@@ -89,7 +89,9 @@ struct DeviceOps {
 };
 
 // Device copies of q / kc / w. dtype bf16 stages through a bounded fp32
-// slab and rounds on device; fp32 copies straight.
+// slab and rounds on device; fp32 copies straight. A non-strict bf16 request
+// on operands bf16 cannot hold falls back to fp32 operands (ops().dtype
+// tells which), so auto_detect scores them with the exact-order kernel.
 class StagedOperands {
 public:
     // row_ranges (s0, rows): only these query rows of q / w are staged (all
@@ -99,6 +101,8 @@ public:
     [[nodiscard]] DeviceOps ops() const { return {q_.as<void>(), kc_.as<void>(), w_.as<float>(), dtype_}; }
 
 private:
+    void stage(csaidx_engine* e, const HostView& host, const ProblemDims& dims, bool strict,
+               const std::vector<std::pair<int64_t, int64_t>>* row_ranges);
     DeviceBuffer q_, kc_, w_;
     int dtype_;
 };

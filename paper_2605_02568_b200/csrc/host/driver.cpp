@@ -338,6 +338,7 @@ struct HostRounder {
     size_t converted = 0;  // chunks [0, converted) are in their slabs
     size_t enqueued = 0;   // ... and their copies are queued
     bool stop = false;
+    bool inexact = false;  // a q row is not bf16-representable (non-strict): re-run on fp32
     std::string error;
     std::thread th;
 
@@ -369,9 +370,38 @@ double now_ms() {
 
 }  // namespace
 
+namespace {
+
+// The operands are not bf16-representable: ScoreKernel::auto_detect then
+// re-runs on fp32 operands with the exact-order kernel (the reference's auto
+// kernel is bit-identical to its scalar one on any fp32 input).
+struct OperandsNotBf16 : std::exception {
+    const char* what() const noexcept override { return "operands are not bf16-representable"; }
+};
+
+void run_chunked_rows_impl(const HostView& in, const ProblemDims& dims, const DriverConfig& config,
+                           const std::vector<int64_t>* starts, int64_t* host_idx, float* host_val, int64_t out_rows,
+                           MemoryLedger& ledger, RunStats* stats_out, int dtype);
+
+}  // namespace
+
 void run_chunked_rows_view(const HostView& in, const ProblemDims& dims, const DriverConfig& config,
                            const std::vector<int64_t>* starts, int64_t* host_idx, float* host_val, int64_t out_rows,
                            MemoryLedger& ledger, RunStats* stats_out) {
+    const int dtype = operand_dtype(dims, mode_code(config.mode), kernel_code(config.kernel));
+    try {
+        run_chunked_rows_impl(in, dims, config, starts, host_idx, host_val, out_rows, ledger, stats_out, dtype);
+    } catch (const OperandsNotBf16&) {
+        run_chunked_rows_impl(in, dims, config, starts, host_idx, host_val, out_rows, ledger, stats_out,
+                              CSAIDX_DTYPE_F32);
+    }
+}
+
+namespace {
+
+void run_chunked_rows_impl(const HostView& in, const ProblemDims& dims, const DriverConfig& config,
+                           const std::vector<int64_t>* starts, int64_t* host_idx, float* host_val, int64_t out_rows,
+                           MemoryLedger& ledger, RunStats* stats_out, int dtype) {
     const ChunkPlan plan = plan_chunks(dims, config.tile, starts);
     int64_t need = 0;
     std::vector<std::pair<int64_t, int64_t>> ranges;
@@ -381,8 +411,6 @@ void run_chunked_rows_view(const HostView& in, const ProblemDims& dims, const Dr
         need = plan.out_row0[c] + rows;
     }
     if (out_rows < need) throw std::invalid_argument("run_chunked: out_rows too small for the chunk list");
-    const int kcode = kernel_code(config.kernel);
-    const int dtype = operand_dtype(dims, mode_code(config.mode), kcode);
     const bool strict = gpu::options().strict_bf16;
     std::lock_guard<std::mutex> lock(engine_mutex());
     csaidx_engine* e = engine();
@@ -452,6 +480,10 @@ void run_chunked_rows_view(const HostView& in, const ProblemDims& dims, const Dr
                                      now_ms() - t_start);
                     if (f.nonfinite) return rounder.fail("IndexerInputs: non-finite entry in q/kc");
                     if (strict && f.inexact) return rounder.fail("operand is not bf16-representable (strict mode)");
+                    if (f.inexact) {
+                        rounder.inexact = true;
+                        return rounder.fail("operands are not bf16-representable");
+                    }
                     {
                         std::lock_guard<std::mutex> g(rounder.mu);
                         rounder.converted = o + 1;
@@ -479,7 +511,10 @@ void run_chunked_rows_view(const HostView& in, const ProblemDims& dims, const Dr
         {
             std::unique_lock<std::mutex> g(rounder.mu);
             rounder.cv.wait(g, [&] { return rounder.converted > o || !rounder.error.empty(); });
-            if (rounder.converted <= o) throw std::invalid_argument(rounder.error);
+            if (rounder.converted <= o) {
+                if (rounder.inexact) throw OperandsNotBf16();
+                throw std::invalid_argument(rounder.error);
+            }
         }
         if (host_trace()) std::fprintf(stderr, "upload %zu waited %.3f at %.3f\n", o, now_ms() - t0, now_ms() - t_start);
         for (int64_t b = 0; b < B; ++b) {
@@ -532,9 +567,14 @@ void run_chunked_rows_view(const HostView& in, const ProblemDims& dims, const Dr
         check(csaidx_engine_use_lane(e, kInLane));
         if (o == 0) {
             if (dtype == CSAIDX_DTYPE_BF16) {
-                DeviceBuffer tmp(e, static_cast<size_t>(dims.kc_elems()) * sizeof(float));
-                tmp.upload(in.kc, static_cast<size_t>(dims.kc_elems()) * sizeof(float));
-                check(csaidx_cuda_to_bf16(e, tmp.as<float>(), kc.as<uint16_t>(), dims.kc_elems(), strict ? 1 : 0));
+                // kc is small: rounded on the host (bit-identical to the
+                // device rounding), which also tells representability up front
+                std::vector<uint16_t> kc16(static_cast<size_t>(dims.kc_elems()));
+                const Bf16Flags f = host_to_bf16(in.kc, kc16.data(), kc16.size());
+                if (f.nonfinite) throw std::invalid_argument("IndexerInputs: non-finite entry in q/kc");
+                if (f.inexact && strict) throw std::invalid_argument("operand is not bf16-representable (strict mode)");
+                if (f.inexact) throw OperandsNotBf16();
+                kc.upload(kc16.data(), kc16.size() * sizeof(uint16_t));
             } else {
                 kc.upload(in.kc, static_cast<size_t>(dims.kc_elems()) * sizeof(float));
             }
@@ -564,10 +604,20 @@ void run_chunked_rows_view(const HostView& in, const ProblemDims& dims, const Dr
     } catch (...) {
         csaidx_engine_use_lane(e, kMainLane);
         csaidx_engine_check(e);  // drain every lane before the buffers go away
+        int seen = 0;
+        csaidx_engine_take_inexact(e, &seen);
         throw;
+    }
+    if (dtype == CSAIDX_DTYPE_BF16 && !host_round && !strict) {
+        // the device rounding noted a q value bf16 cannot hold
+        int seen = 0;
+        check(csaidx_engine_take_inexact(e, &seen));
+        if (seen) throw OperandsNotBf16();
     }
     if (stats_out != nullptr) *stats_out = stats;
 }
+
+}  // namespace
 
 TopKResult run_chunked_view(const HostView& in, const ProblemDims& dims, const DriverConfig& config,
                             MemoryLedger& ledger, RunStats* stats_out) {

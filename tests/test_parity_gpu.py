@@ -343,7 +343,7 @@ def test_host_rounding_matches_device_rounding(orc, monkeypatch):
     chunks than staging slabs; non-finite and (strict) inexact q rows raise
     invalid_argument either way."""
     B, S, m, H, D, k = 2, 8192, 4, 64, 128, 64
-    q, kc, w = orc.generate_inputs(B, S, m, H, D, 3)
+    q, kc, w = orc.generate_inputs(B, S, m, H, D, 3, bf16=True)
     dims = api.ProblemDims.create(B, S, m, H, D, k)
     cfg = api.DriverConfig(tile=api.TileConfig(256, S // m))
     starts = list(range(0, S, 256))[::-1][:20]  # 20 chunks > 8 slabs
@@ -378,7 +378,39 @@ def test_host_rounding_matches_device_rounding(orc, monkeypatch):
         strict = api.DriverConfig(tile=api.TileConfig(256, S // m), strict_bf16=True)
         with pytest.raises(InvalidArgument):
             api.run_chunked_rows(inexact, kcf, w3, dims, strict, starts, oi, ov)
-        api.run_chunked_rows(inexact, kcf, w3, dims, cfg, starts, oi, ov)  # rounds when not strict
+        # not strict: auto_detect re-runs on the fp32 operands with the
+        # exact-order kernel, i.e. ScoreKernel.scalar's bytes
+        api.run_chunked_rows(inexact, kcf, w3, dims, cfg, starts, oi, ov)
+        scal = api.DriverConfig(tile=api.TileConfig(256, S // m), kernel=api.ScoreKernel.scalar)
+        si = np.empty_like(oi)
+        sv = np.empty_like(ov)
+        api.run_chunked_rows(inexact, kcf, w3, dims, scal, starts, si, sv)
+        assert np.array_equal(oi, si) and np.array_equal(bits(ov), bits(sv))
+
+
+def test_auto_detect_on_fp32_inputs_is_bit_exact_like_the_reference(orc):
+    """the reference's auto_detect scores arbitrary fp32 operands
+    with a kernel bit-identical to its scalar one (score.cpp:18-43). At the
+    V4 shape the B200 build takes tcgen05 only for bf16-representable
+    operands; otherwise (q, kc, or just one late q row inexact) it runs the
+    exact-order kernel on fp32 operands: bit-exact indices and values."""
+    B, S, m, H, D, k = 1, 1024, 4, 64, 128, 64
+    q, kc, w = orc.generate_inputs(B, S, m, H, D, 5)  # raw fp32 draws
+    qb, kcb = orc.bf16_round(q), orc.bf16_round(kc)
+    cases = {"q+kc": (q, kc), "kc": (qb, kc)}
+    late = qb.copy()
+    late[0, S - 3, 5, 7] = np.float32(late[0, S - 3, 5, 7] * np.float32(1.0000001))
+    cases["one late q row"] = (late, kcb)
+    dims = api.ProblemDims.create(B, S, m, H, D, k)
+    for name, (qq, kk) in cases.items():
+        inputs = api.IndexerInputs.validated(qq, kk, w, dims)
+        rc, oi, ov, _ = orc.run_chunked(qq, kk, w, m, k, 256, S // m)
+        assert rc == 0
+        for cs, ct in ((256, S // m), (128, 64)):
+            res, _ = api.run_chunked(inputs, dims, api.DriverConfig(tile=api.TileConfig(cs, ct)))
+            assert np.array_equal(res.indices, oi) and np.array_equal(bits(res.values), bits(ov)), (name, cs, ct)
+        mres, _ = api.run_materialize(inputs, dims)
+        assert np.array_equal(mres.indices, oi) and np.array_equal(bits(mres.values), bits(ov)), name
 
 
 @pytest.mark.parametrize("key_tile", [10 ** 6, 512])
