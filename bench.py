@@ -287,7 +287,7 @@ def main():
         oks = [None] * world
         dist.all_gather_object(oks, ok)
         if all(oks):
-            api.set_index_sink(drv_h, sink_ptr, S)
+            api.set_index_sink(drv_h, sink_ptr, B, S, k)
         else:
             if ok and rank != 0:
                 api.ipc_close(drv_h, sink_ptr, handle[0])

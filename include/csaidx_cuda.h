@@ -89,13 +89,14 @@ int csaidx_engine_await_stream(csaidx_engine* e, void* stream);
 /* Index sink: from now on every final output row written by
  * csaidx_cuda_select_final / csaidx_cuda_finalize for query position s of
  * batch b is also stored as int32 indices at dst[(b * seq_len + s) * k ..]
- * (a [B, seq_len, k] buffer). dst may be another GPU's memory mapped with
+ * (a [batch, seq_len, k] buffer; a final launch whose batch count, k or
+ * rows do not fit it fails with CSAIDX_INVALID_ARGUMENT). dst may be another GPU's memory mapped with
  * csaidx_cuda_ipc_open: then the final kernels of a query-sharded run write
  * their rows straight into the collecting rank over NVLink, fusing the
  * gather of the driver's result (reference run_chunked, driver.cpp:115-165,
  * assembles TopKResult rows; SURVEY §8e's gather) into the select.
  * NULL disables. */
-int csaidx_engine_set_index_sink(csaidx_engine* e, int32_t* dst, int64_t seq_len);
+int csaidx_engine_set_index_sink(csaidx_engine* e, int32_t* dst, int64_t batch, int64_t seq_len, int64_t k);
 /* CUDA IPC of a device pointer for the index sink: a 64-byte handle of the
  * allocation that holds dev_ptr plus dev_ptr's offset inside it (caching
  * allocators hand out blocks inside larger allocations). open maps the

@@ -95,7 +95,7 @@ CUDA_SYMBOLS = {
     "csaidx_engine_await": (c_int, [c_void_p, c_int]),
     "csaidx_engine_sync_slot": (c_int, [c_void_p, c_int]),
     "csaidx_engine_await_stream": (c_int, [c_void_p, c_void_p]),
-    "csaidx_engine_set_index_sink": (c_int, [c_void_p, c_void_p, c_int64]),
+    "csaidx_engine_set_index_sink": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64]),
     "csaidx_cuda_ipc_handle": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(c_uint64)]),
     "csaidx_cuda_ipc_open": (c_int, [c_void_p, c_void_p, c_uint64, POINTER(c_void_p)]),
     "csaidx_cuda_ipc_close": (c_int, [c_void_p, c_void_p, c_uint64]),

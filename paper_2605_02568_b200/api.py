@@ -426,11 +426,11 @@ def driver_engine(device: int = 0):
     return h
 
 
-def set_index_sink(engine, dst_ptr: int | None, seq_len: int = 0):
+def set_index_sink(engine, dst_ptr: int | None, batch: int = 0, seq_len: int = 0, k: int = 0):
     """csaidx_engine_set_index_sink: final rows are also stored as int32 into
-    the [B, seq_len, k] buffer at dst_ptr (possibly a peer GPU's, see ipc_open);
-    None disables."""
-    _check_cuda(_capi.cuda_lib().csaidx_engine_set_index_sink(engine, c_void_p(dst_ptr or 0), seq_len))
+    the [batch, seq_len, k] buffer at dst_ptr (possibly a peer GPU's, see
+    ipc_open); None disables."""
+    _check_cuda(_capi.cuda_lib().csaidx_engine_set_index_sink(engine, c_void_p(dst_ptr or 0), batch, seq_len, k))
 
 
 def ipc_handle(engine, dev_ptr: int) -> tuple[bytes, int]:

@@ -120,7 +120,7 @@ struct csaidx_engine {
     cudaEvent_t slots[192] = {};
     cudaEvent_t entry_event = nullptr;  // csaidx_engine_await_stream
     int32_t* sink = nullptr;            // csaidx_engine_set_index_sink
-    int64_t sink_seq = 0;
+    int64_t sink_batch = 0, sink_seq = 0, sink_k = 0;
     // SM partition while a select runs beside the score kernel (0 = whole GPU)
     int score_sms = 0;
     int select_sms = 0;
@@ -515,11 +515,14 @@ int csaidx_cuda_copy(csaidx_engine* e, void* dst, const void* src, size_t bytes)
     return CSAIDX_OK;
 }
 
-int csaidx_engine_set_index_sink(csaidx_engine* e, int32_t* dst, int64_t seq_len) {
+int csaidx_engine_set_index_sink(csaidx_engine* e, int32_t* dst, int64_t batch, int64_t seq_len, int64_t k) {
     if (e == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "null engine");
-    if (dst != nullptr && seq_len < 1) return fail(CSAIDX_INVALID_ARGUMENT, "index sink: seq_len must be >= 1");
+    if (dst != nullptr && (batch < 1 || seq_len < 1 || k < 1))
+        return fail(CSAIDX_INVALID_ARGUMENT, "index sink: batch, seq_len and k must be >= 1");
     e->sink = dst;
+    e->sink_batch = dst != nullptr ? batch : 0;
     e->sink_seq = dst != nullptr ? seq_len : 0;
+    e->sink_k = dst != nullptr ? k : 0;
     return CSAIDX_OK;
 }
 
@@ -814,6 +817,19 @@ int csaidx_cuda_select_overlap_capable(int64_t k) {
 
 namespace {
 
+// The index sink holds [sink_batch, sink_seq, sink_k] int32: a final write
+// of rows [s0, s0 + rows) of `batch` batches at row stride k must fit it.
+int check_sink(const csaidx_engine* e, int64_t batch, int64_t s0, int64_t rows, int64_t k) {
+    if (e->sink == nullptr) return CSAIDX_OK;
+    if (batch != e->sink_batch || k != e->sink_k || s0 < 0 || s0 + rows > e->sink_seq)
+        return fail(CSAIDX_INVALID_ARGUMENT,
+                    "index sink [%lld, %lld, %lld] does not cover rows [%lld, %lld) of %lld batches at k = %lld",
+                    static_cast<long long>(e->sink_batch), static_cast<long long>(e->sink_seq),
+                    static_cast<long long>(e->sink_k), static_cast<long long>(s0), static_cast<long long>(s0 + rows),
+                    static_cast<long long>(batch), static_cast<long long>(k));
+    return CSAIDX_OK;
+}
+
 int select_impl(csaidx_engine* e, const float* scores, int64_t batch, int64_t rows, int64_t ld, int64_t cols,
                 int64_t s0, int64_t t0, int64_t ratio, int apply_mask, int64_t k, float* cand_val, int32_t* cand_idx,
                 int64_t cand_ld, const uint32_t* pass_bits, int64_t bits_ld, int64_t* final_idx = nullptr,
@@ -852,6 +868,7 @@ int select_impl(csaidx_engine* e, const float* scores, int64_t batch, int64_t ro
     p.final_rows = final_rows;
     p.final_row0 = final_row0;
     if (final_idx != nullptr) {
+        if (int rc = check_sink(e, batch, s0, rows, cand_ld)) return rc;
         p.sink = e->sink;
         p.sink_seq = e->sink_seq;
     }
@@ -951,6 +968,7 @@ int csaidx_cuda_finalize(csaidx_engine* e, const float* run_val, const int32_t* 
     p.out_row0 = out_row0;
     p.trail_flag = e->flags + kTrail;
     p.keff_flag = e->flags + kKeff;
+    if (int rc = check_sink(e, batch, s0, rows, k)) return rc;
     p.sink = e->sink;
     p.sink_seq = e->sink_seq;
     LaunchScope ls(e, CSAIDX_KIND_FINALIZE);

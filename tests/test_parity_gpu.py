@@ -428,7 +428,7 @@ def test_index_sink_receives_the_final_rows(orc, key_tile):
     starts = [3584, 512, 2048]
     h = api.driver_engine(0)
     sink = torch.full((2, 4096, 128), -7, dtype=torch.int32, device="cuda")
-    api.set_index_sink(h, sink.data_ptr(), 4096)
+    api.set_index_sink(h, sink.data_ptr(), 2, 4096, 128)
     try:
         oi, _, _ = api.run_chunked_device(qd, kd, wd, dims, cfg, starts)
     finally:
@@ -440,6 +440,21 @@ def test_index_sink_receives_the_final_rows(orc, key_tile):
     for s0 in starts:
         untouched[s0:s0 + 512] = False
     assert bool((sink[:, untouched] == -7).all())
+    # a final launch that does not fit the registered sink (other
+    # k, batch count or sequence length) fails instead of writing past it
+    api.set_index_sink(h, sink.data_ptr(), 2, 4096, 64)
+    try:
+        with pytest.raises(InvalidArgument):
+            api.run_chunked_device(qd, kd, wd, dims, cfg, starts)
+    finally:
+        api.set_index_sink(h, None)
+    api.set_index_sink(h, sink.data_ptr(), 2, 2048, 128)
+    try:
+        with pytest.raises(InvalidArgument):
+            api.run_chunked_device(qd, kd, wd, dims, cfg, [2048])
+        api.run_chunked_device(qd, kd, wd, dims, cfg, [1536])  # rows [1536, 2048) fit
+    finally:
+        api.set_index_sink(h, None)
 
 
 def _sink_child(handle, q, kc, w, starts, done):
@@ -449,7 +464,7 @@ def _sink_child(handle, q, kc, w, starts, done):
 
     h = capi.driver_engine(0)
     ptr = capi.ipc_open(h, handle)
-    capi.set_index_sink(h, ptr, 4096)
+    capi.set_index_sink(h, ptr, 1, 4096, 64)
     dims = capi.ProblemDims.create(1, 4096, 4, 64, 128, 64)
     cfg = capi.DriverConfig(tile=capi.TileConfig(512, 10 ** 6))
     qd, kd, wd = (torch.from_numpy(a).cuda() for a in (q, kc, w))
