@@ -10,6 +10,7 @@
 #include "csaidx/driver.hpp"
 #include "csaidx/memory_ledger.hpp"
 #include "csaidx/types.hpp"
+#include "csaidx_cuda.h"
 
 namespace csaidx::gpu {
 
@@ -63,5 +64,61 @@ void run_chunked_device(const DeviceOperands& ops, const ProblemDims& dims,
 void load_inputs_device(const std::string& path, const ProblemDims& dims, const TileConfig& tile,
                         const std::vector<int64_t>* chunk_starts, int dtype, bool strict, void* q, void* kc,
                         float* w);
+
+// ------------------------------------------------------------ multi-GPU
+// Query-sharded driver, one process (rank) per GPU. The reference runs the
+// same query-tile loop on `DriverConfig::threads` host workers over
+// contiguous blocks of tiles (driver.cpp:115-165); here the workers are GPUs,
+// the chunks are dealt by causal work (LPT), and the only exchanges are the
+// ones north_star names: the keys are broadcast once from rank 0 and only
+// the [B, S, k] int32 index rows travel back to rank 0.
+
+// LPT assignment of the c_S query chunks by causal work (cost of a chunk =
+// its legal (query, key) pairs, B-independent): chunks in decreasing cost
+// (ties: later chunk first), each to the least-loaded rank (ties: lowest
+// rank). Returns per-rank ascending chunk starts; loads = per-rank cost.
+std::vector<std::vector<int64_t>> plan_shards(const ProblemDims& dims, int64_t query_tile, int world,
+                                              std::vector<uint64_t>* loads = nullptr);
+
+enum class GatherMode {
+    peer = 0,        // final select/finalize kernels store rows into rank 0's buffer (CUDA IPC over NVLink)
+    collective = 1,  // rows gathered after the compute through the transport's gatherv
+};
+
+// One rank of a query-sharded run: the plan, the peer mapping of rank 0's
+// result buffer (set up once), and the per-step exchange. The transport
+// (include/csaidx_cuda.h csaidx_collectives: NCCL, or a caller's own) must
+// outlive the object.
+class MultiRank {
+public:
+    // root_out: rank 0's device [B, S, k] int32 result (ignored elsewhere).
+    MultiRank(const csaidx_collectives& comm, const ProblemDims& dims, const DriverConfig& config, GatherMode mode,
+              int32_t* root_out);
+    ~MultiRank();
+    MultiRank(const MultiRank&) = delete;
+    MultiRank& operator=(const MultiRank&) = delete;
+
+    const std::vector<int64_t>& chunks() const { return plan_[static_cast<size_t>(rank_)]; }
+    int64_t rows() const { return rows_[static_cast<size_t>(rank_)]; }  // this rank's rows per batch
+
+    // One step. q / w: this rank's rows (DeviceOperands::local_rows layout,
+    // chunks() order); kc: [B, T, d_h] on every rank, read on rank 0 and
+    // overwritten by the broadcast elsewhere. local_idx / local_val: this
+    // rank's [B, rows(), k] outputs (null: kept inside). On return the step
+    // is complete on every rank and rank 0's root_out holds all rows.
+    void run(const void* q, void* kc, int dtype, const float* w, int64_t* local_idx, float* local_val,
+             MemoryLedger& ledger, RunStats* stats = nullptr);
+
+private:
+    struct Impl;
+    Impl* impl_;
+    csaidx_collectives comm_;
+    ProblemDims dims_;
+    DriverConfig config_;
+    GatherMode mode_;
+    int rank_, world_;
+    std::vector<std::vector<int64_t>> plan_;
+    std::vector<int64_t> rows_;
+};
 
 }  // namespace csaidx::gpu

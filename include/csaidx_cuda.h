@@ -300,6 +300,52 @@ int csaidx_cuda_gen_normal_bf16(csaidx_engine* e, uint16_t* dst, int64_t n, doub
 int csaidx_cuda_gen_normal_f32(csaidx_engine* e, float* dst, int64_t n, double stddev,
                                uint64_t seed, uint64_t stream_id, int64_t offset);
 
+/* ------------------------------------------------------------ multi-GPU
+ * Transport of the query-sharded driver (csaidx_multi_*, csaidx_host.h): one
+ * process per GPU; the driver broadcasts the keys, exchanges small host blobs
+ * (the peer-sink IPC handle), synchronizes, and optionally gathers the int32
+ * index rows. The reference parallelizes the same query-tile loop over host
+ * threads (driver.cpp:131-161, DriverConfig::threads); its ranks are GPUs here.
+ * All callbacks return CSAIDX_OK or an error code. */
+typedef struct csaidx_collectives {
+    void* ctx;
+    int rank;
+    int world;
+    /* 1: bcast / gatherv take device pointers and are ordered on `stream`
+     * (NCCL); 0: they take host pointers and complete before returning (the
+     * driver stages device data through host memory around them). */
+    int device_buffers;
+    /* bytes at buf on rank `root` -> buf on every rank (in place) */
+    int (*bcast)(void* ctx, void* buf, size_t bytes, int root, void* stream);
+    /* every rank's `bytes` at in -> out[world * bytes] on every rank (host pointers) */
+    int (*allgather_host)(void* ctx, const void* in, void* out, size_t bytes);
+    /* returns on every rank once all ranks called it and the work queued on
+     * `stream` (this rank's kernels, incl. their peer stores) has completed */
+    int (*barrier)(void* ctx, void* stream);
+    /* rank r's send_bytes at send -> root's recv + recv_off[r] (recv_bytes[r]
+     * bytes; recv / recv_* only significant on root) */
+    int (*gatherv)(void* ctx, const void* send, size_t send_bytes, void* recv, const size_t* recv_bytes,
+                   const size_t* recv_off, int root, void* stream);
+} csaidx_collectives;
+
+/* NCCL transport (libnccl.so.2 resolved at run time with dlopen: the copy the
+ * process already loaded, e.g. PyTorch's, or the system library). The
+ * 128-byte unique id is created on one rank and handed to all others by the
+ * caller (any out-of-band channel). ncclBroadcast / ncclAllGather /
+ * ncclAllReduce / grouped ncclSend+ncclRecv on the caller's stream. */
+int csaidx_nccl_unique_id(uint8_t id[128]);
+int csaidx_nccl_collectives_create(int rank, int world, const uint8_t id[128], int device,
+                                   csaidx_collectives** out);
+int csaidx_nccl_collectives_destroy(csaidx_collectives* c);
+
+/* int64 -> int32 index rows (indices < 2^31) and a row scatter: row r of
+ * src (row_elems int32) -> dst + dst_row[r] * row_elems (dst_row on device). */
+int csaidx_cuda_narrow_indices(csaidx_engine* e, const int64_t* src, int32_t* dst, int64_t n);
+int csaidx_cuda_scatter_rows(csaidx_engine* e, const int32_t* src, int32_t* dst, const int64_t* dst_row,
+                             int64_t nrows, int64_t row_elems);
+/* Synchronizes the engine's current stream (no flag check). */
+int csaidx_engine_sync(csaidx_engine* e);
+
 #ifdef __cplusplus
 }
 #endif

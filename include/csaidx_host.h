@@ -146,6 +146,35 @@ int64_t csaidx_host_k_eff(int64_t t, int64_t ratio, int64_t top_k);
  * types.cpp:73-92, and of strict mode). */
 int csaidx_host_round_bf16(const float* src, uint16_t* dst, uint64_t n, int* nonfinite, int* inexact);
 
+/* ------------------------------------------------------------ multi-GPU
+ * The query-sharded driver (csaidx::gpu::MultiRank, include/csaidx/gpu.hpp):
+ * one process per GPU over a csaidx_collectives transport (NCCL:
+ * csaidx_nccl_collectives_create, or the caller's own). Replaces the
+ * reference's threaded run_chunked (driver.cpp:115-165, DriverConfig::threads)
+ * for ranks = GPUs. */
+#define CSAIDX_GATHER_PEER 0       /* final kernels store rows into rank 0's buffer over a CUDA IPC mapping */
+#define CSAIDX_GATHER_COLLECTIVE 1 /* rows gathered after the compute (transport gatherv) */
+
+/* LPT plan: rank's ascending chunk starts (up to cap) and their count; loads
+ * (optional, [world]) = per-rank causal pairs per batch. */
+int csaidx_host_plan_shards(const csaidx_dims* dims, int64_t query_tile, int world, int rank, int64_t* starts,
+                            int64_t cap, int64_t* n_chunks, uint64_t* loads);
+
+typedef struct csaidx_multi csaidx_multi;
+/* root_out: rank 0's device [B, S, k] int32 result (NULL elsewhere). Sets up
+ * the plan and, for the peer gather, maps rank 0's buffer on every rank. */
+int csaidx_multi_create(const csaidx_collectives* comm, const csaidx_dims* dims, const csaidx_run_config* cfg,
+                        int gather_mode, int32_t* root_out, csaidx_multi** out);
+/* This rank's chunk starts (valid until destroy) and rows per batch. */
+int csaidx_multi_chunks(const csaidx_multi* m, const int64_t** starts, int64_t* n_chunks, int64_t* rows);
+/* One step: q / w this rank's rows (chunks order, [B, rows, ...]); kc
+ * [B, T, d_h] read on rank 0 and broadcast into kc elsewhere; local_idx /
+ * local_val this rank's [B, rows, k] outputs or NULL. Returns when rank 0's
+ * root_out holds every rank's rows. */
+int csaidx_multi_run(csaidx_multi* m, const void* q, void* kc, int dtype, const float* w, int64_t* local_idx,
+                     float* local_val, csaidx_run_stats* stats);
+int csaidx_multi_destroy(csaidx_multi* m);
+
 #ifdef __cplusplus
 }
 #endif

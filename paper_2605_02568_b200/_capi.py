@@ -81,6 +81,9 @@ CUDA_SYMBOLS = {
     "csaidx_engine_num_sms": (c_int, [c_void_p, POINTER(c_int)]),
     "csaidx_engine_check": (c_int, [c_void_p]),
     "csaidx_engine_take_inexact": (c_int, [c_void_p, POINTER(c_int)]),
+    "csaidx_engine_sync": (c_int, [c_void_p]),
+    "csaidx_cuda_narrow_indices": (c_int, [c_void_p, c_void_p, c_void_p, c_int64]),
+    "csaidx_cuda_scatter_rows": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64]),
     "csaidx_engine_mem_stats": (c_int, [c_void_p, POINTER(c_uint64), POINTER(c_uint64)]),
     "csaidx_engine_reset_peak": (c_int, [c_void_p]),
     "csaidx_engine_set_profiling": (c_int, [c_void_p, c_int]),

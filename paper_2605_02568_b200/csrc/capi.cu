@@ -948,6 +948,29 @@ int csaidx_cuda_fill_sentinel(csaidx_engine* e, float* val, int32_t* idx, int64_
     return CSAIDX_OK;
 }
 
+int csaidx_cuda_narrow_indices(csaidx_engine* e, const int64_t* src, int32_t* dst, int64_t n) {
+    if (int rc = set_device(e)) return rc;
+    if (n < 0) return fail(CSAIDX_INVALID_ARGUMENT, "narrow_indices: negative length");
+    LaunchScope ls(e, CSAIDX_KIND_PREP);
+    CSAIDX_CUDA_TRY(csaidx_kern::launch_narrow(src, dst, n, e->stream), "narrow_indices");
+    return CSAIDX_OK;
+}
+
+int csaidx_cuda_scatter_rows(csaidx_engine* e, const int32_t* src, int32_t* dst, const int64_t* dst_row,
+                             int64_t nrows, int64_t row_elems) {
+    if (int rc = set_device(e)) return rc;
+    if (nrows < 0 || row_elems < 1) return fail(CSAIDX_INVALID_ARGUMENT, "scatter_rows: bad extents");
+    LaunchScope ls(e, CSAIDX_KIND_PREP);
+    CSAIDX_CUDA_TRY(csaidx_kern::launch_scatter_rows(src, dst, dst_row, nrows, row_elems, e->stream), "scatter_rows");
+    return CSAIDX_OK;
+}
+
+int csaidx_engine_sync(csaidx_engine* e) {
+    if (int rc = set_device(e)) return rc;
+    CSAIDX_CUDA_TRY(cudaStreamSynchronize(e->stream), "cudaStreamSynchronize");
+    return CSAIDX_OK;
+}
+
 int csaidx_cuda_finalize(csaidx_engine* e, const float* run_val, const int32_t* run_idx, int64_t batch, int64_t rows,
                          int64_t s0, int64_t ratio, int64_t k, int check_keff, int64_t* out_idx, float* out_val,
                          int64_t out_rows, int64_t out_row0) {
@@ -1010,6 +1033,203 @@ int csaidx_cuda_gen_normal_f32(csaidx_engine* e, float* dst, int64_t n, double s
     if (int rc = set_device(e)) return rc;
     LaunchScope ls(e, CSAIDX_KIND_PREP);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_gen_normal_f32(dst, n, stddev, seed, stream_id, offset, e->stream), "gen_f32");
+    return CSAIDX_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ NCCL transport
+// libnccl.so.2 is resolved with dlopen at first use (the copy the process
+// already loaded, e.g. PyTorch's, or the system library), so the C-ABI
+// library has no link-time NCCL dependency.
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace {
+
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*group_start)() = nullptr;
+    ncclResult_t (*group_end)() = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (h == nullptr) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (h == nullptr) {
+            a.why = std::string("dlopen(libnccl.so.2) failed: ") + dlerror();
+            return a;
+        }
+        auto sym = [&](auto& fn, const char* name) {
+            fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+            if (fn == nullptr && a.why.empty()) a.why = std::string("libnccl lacks ") + name;
+        };
+        sym(a.get_unique_id, "ncclGetUniqueId");
+        sym(a.comm_init_rank, "ncclCommInitRank");
+        sym(a.comm_destroy, "ncclCommDestroy");
+        sym(a.broadcast, "ncclBroadcast");
+        sym(a.all_gather, "ncclAllGather");
+        sym(a.all_reduce, "ncclAllReduce");
+        sym(a.send, "ncclSend");
+        sym(a.recv, "ncclRecv");
+        sym(a.group_start, "ncclGroupStart");
+        sym(a.group_end, "ncclGroupEnd");
+        sym(a.error_string, "ncclGetErrorString");
+        a.ok = a.why.empty();
+        return a;
+    }();
+    return api;
+}
+
+#define CSAIDX_NCCL_TRY(expr, where)                                                                  \
+    do {                                                                                              \
+        ncclResult_t _r = (expr);                                                                     \
+        if (_r != ncclSuccess) return fail(CSAIDX_RUNTIME_ERROR, "%s: NCCL error %s", where,          \
+                                           nccl().error_string != nullptr ? nccl().error_string(_r) : "?"); \
+    } while (0)
+
+struct NcclCtx {
+    csaidx_collectives pub{};
+    ncclComm_t comm = nullptr;
+    int device = 0;
+    void* scratch = nullptr;  // device bytes for blobs / the barrier word
+    size_t scratch_bytes = 0;
+    cudaStream_t own = nullptr;
+};
+
+int nccl_bcast(void* ctx, void* buf, size_t bytes, int root, void* stream) {
+    auto* c = static_cast<NcclCtx*>(ctx);
+    CSAIDX_CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
+    CSAIDX_NCCL_TRY(nccl().broadcast(buf, buf, bytes, ncclUint8, root, c->comm, static_cast<cudaStream_t>(stream)),
+                    "ncclBroadcast");
+    return CSAIDX_OK;
+}
+
+int nccl_scratch(NcclCtx* c, size_t bytes) {
+    if (c->scratch_bytes >= bytes) return CSAIDX_OK;
+    if (c->scratch != nullptr) cudaFree(c->scratch);
+    c->scratch = nullptr;
+    c->scratch_bytes = 0;
+    CSAIDX_CUDA_TRY(cudaMalloc(&c->scratch, bytes), "cudaMalloc(nccl scratch)");
+    c->scratch_bytes = bytes;
+    return CSAIDX_OK;
+}
+
+int nccl_allgather_host(void* ctx, const void* in, void* out, size_t bytes) {
+    auto* c = static_cast<NcclCtx*>(ctx);
+    CSAIDX_CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
+    const size_t all = bytes * static_cast<size_t>(c->pub.world);
+    if (int rc = nccl_scratch(c, bytes + all)) return rc;
+    char* d = static_cast<char*>(c->scratch);
+    CSAIDX_CUDA_TRY(cudaMemcpyAsync(d, in, bytes, cudaMemcpyHostToDevice, c->own), "allgather H2D");
+    CSAIDX_NCCL_TRY(nccl().all_gather(d, d + bytes, bytes, ncclUint8, c->comm, c->own), "ncclAllGather");
+    CSAIDX_CUDA_TRY(cudaMemcpyAsync(out, d + bytes, all, cudaMemcpyDeviceToHost, c->own), "allgather D2H");
+    CSAIDX_CUDA_TRY(cudaStreamSynchronize(c->own), "cudaStreamSynchronize");
+    return CSAIDX_OK;
+}
+
+int nccl_barrier(void* ctx, void* stream) {
+    auto* c = static_cast<NcclCtx*>(ctx);
+    CSAIDX_CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
+    if (int rc = nccl_scratch(c, 64)) return rc;
+    auto s = static_cast<cudaStream_t>(stream);
+    CSAIDX_NCCL_TRY(nccl().all_reduce(c->scratch, c->scratch, 1, ncclInt32, ncclSum, c->comm, s), "ncclAllReduce");
+    CSAIDX_CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    return CSAIDX_OK;
+}
+
+int nccl_gatherv(void* ctx, const void* send, size_t send_bytes, void* recv, const size_t* recv_bytes,
+                 const size_t* recv_off, int root, void* stream) {
+    auto* c = static_cast<NcclCtx*>(ctx);
+    CSAIDX_CUDA_TRY(cudaSetDevice(c->device), "cudaSetDevice");
+    auto s = static_cast<cudaStream_t>(stream);
+    CSAIDX_NCCL_TRY(nccl().group_start(), "ncclGroupStart");
+    if (c->pub.rank == root) {
+        for (int r = 0; r < c->pub.world; ++r) {
+            char* dst = static_cast<char*>(recv) + recv_off[r];
+            if (r == root) {
+                if (recv_bytes[r] > 0)
+                    CSAIDX_CUDA_TRY(cudaMemcpyAsync(dst, send, recv_bytes[r], cudaMemcpyDeviceToDevice, s),
+                                    "gatherv self copy");
+            } else if (recv_bytes[r] > 0) {
+                CSAIDX_NCCL_TRY(nccl().recv(dst, recv_bytes[r], ncclUint8, r, c->comm, s), "ncclRecv");
+            }
+        }
+    } else if (send_bytes > 0) {
+        CSAIDX_NCCL_TRY(nccl().send(send, send_bytes, ncclUint8, root, c->comm, s), "ncclSend");
+    }
+    CSAIDX_NCCL_TRY(nccl().group_end(), "ncclGroupEnd");
+    return CSAIDX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int csaidx_nccl_unique_id(uint8_t id[128]) {
+    if (id == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "nccl_unique_id: null out");
+    if (!nccl().ok) return fail(CSAIDX_RUNTIME_ERROR, "NCCL unavailable: %s", nccl().why.c_str());
+    ncclUniqueId u;
+    CSAIDX_NCCL_TRY(nccl().get_unique_id(&u), "ncclGetUniqueId");
+    static_assert(sizeof(u) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(id, &u, 128);
+    return CSAIDX_OK;
+}
+
+int csaidx_nccl_collectives_create(int rank, int world, const uint8_t id[128], int device,
+                                   csaidx_collectives** out) {
+    if (out == nullptr || id == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "nccl_collectives: null argument");
+    if (world < 1 || rank < 0 || rank >= world) return fail(CSAIDX_INVALID_ARGUMENT, "nccl_collectives: bad rank");
+    if (!nccl().ok) return fail(CSAIDX_RUNTIME_ERROR, "NCCL unavailable: %s", nccl().why.c_str());
+    CSAIDX_CUDA_TRY(cudaSetDevice(device), "cudaSetDevice");
+    auto* c = new NcclCtx();
+    c->device = device;
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    ncclResult_t r = nccl().comm_init_rank(&c->comm, world, u, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        return fail(CSAIDX_RUNTIME_ERROR, "ncclCommInitRank: %s", nccl().error_string(r));
+    }
+    if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess) {
+        nccl().comm_destroy(c->comm);
+        delete c;
+        return fail(CSAIDX_CUDA_ERROR, "cudaStreamCreate failed");
+    }
+    c->pub.ctx = c;
+    c->pub.rank = rank;
+    c->pub.world = world;
+    c->pub.device_buffers = 1;
+    c->pub.bcast = nccl_bcast;
+    c->pub.allgather_host = nccl_allgather_host;
+    c->pub.barrier = nccl_barrier;
+    c->pub.gatherv = nccl_gatherv;
+    *out = &c->pub;
+    return CSAIDX_OK;
+}
+
+int csaidx_nccl_collectives_destroy(csaidx_collectives* pub) {
+    if (pub == nullptr) return CSAIDX_OK;
+    auto* c = static_cast<NcclCtx*>(pub->ctx);
+    cudaSetDevice(c->device);
+    if (c->own) cudaStreamSynchronize(c->own);
+    if (c->comm) nccl().comm_destroy(c->comm);
+    if (c->scratch) cudaFree(c->scratch);
+    if (c->own) cudaStreamDestroy(c->own);
+    delete c;
     return CSAIDX_OK;
 }
 

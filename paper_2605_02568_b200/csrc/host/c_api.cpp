@@ -347,4 +347,80 @@ int csaidx_host_round_bf16(const float* src, uint16_t* dst, uint64_t n, int* non
     });
 }
 
+int csaidx_host_plan_shards(const csaidx_dims* dims, int64_t query_tile, int world, int rank, int64_t* starts,
+                            int64_t cap, int64_t* n_chunks, uint64_t* loads) {
+    return guarded([&] {
+        const csaidx::ProblemDims d = from_c(dims);
+        if (n_chunks == nullptr) throw std::invalid_argument("plan_shards: null n_chunks");
+        if (rank < 0 || rank >= world) throw std::invalid_argument("plan_shards: rank outside [0, world)");
+        std::vector<uint64_t> ld;
+        const auto plan = csaidx::gpu::plan_shards(d, query_tile, world, &ld);
+        const auto& mine = plan[static_cast<size_t>(rank)];
+        *n_chunks = static_cast<int64_t>(mine.size());
+        if (starts != nullptr)
+            for (size_t i = 0; i < mine.size() && static_cast<int64_t>(i) < cap; ++i) starts[i] = mine[i];
+        if (loads != nullptr) std::memcpy(loads, ld.data(), ld.size() * sizeof(uint64_t));
+    });
+}
+
+}  // extern "C"
+
+struct csaidx_multi {
+    csaidx_run_config cfg;
+    csaidx::gpu::MultiRank* rank;
+};
+
+extern "C" {
+
+int csaidx_multi_create(const csaidx_collectives* comm, const csaidx_dims* dims, const csaidx_run_config* cfg,
+                        int gather_mode, int32_t* root_out, csaidx_multi** out) {
+    return guarded([&] {
+        if (comm == nullptr || out == nullptr) throw std::invalid_argument("multi_create: null argument");
+        if (gather_mode != CSAIDX_GATHER_PEER && gather_mode != CSAIDX_GATHER_COLLECTIVE)
+            throw std::invalid_argument("multi_create: unknown gather mode");
+        const csaidx::ProblemDims d = from_c(dims);
+        const csaidx::DriverConfig c = from_c(cfg);
+        auto* m = new csaidx_multi{*cfg, nullptr};
+        try {
+            m->rank = new csaidx::gpu::MultiRank(*comm, d, c,
+                                                 gather_mode == CSAIDX_GATHER_PEER ? csaidx::gpu::GatherMode::peer
+                                                                                   : csaidx::gpu::GatherMode::collective,
+                                                 root_out);
+        } catch (...) {
+            delete m;
+            throw;
+        }
+        *out = m;
+    });
+}
+
+int csaidx_multi_chunks(const csaidx_multi* m, const int64_t** starts, int64_t* n_chunks, int64_t* rows) {
+    return guarded([&] {
+        if (m == nullptr) throw std::invalid_argument("multi_chunks: null handle");
+        if (starts != nullptr) *starts = m->rank->chunks().data();
+        if (n_chunks != nullptr) *n_chunks = static_cast<int64_t>(m->rank->chunks().size());
+        if (rows != nullptr) *rows = m->rank->rows();
+    });
+}
+
+int csaidx_multi_run(csaidx_multi* m, const void* q, void* kc, int dtype, const float* w, int64_t* local_idx,
+                     float* local_val, csaidx_run_stats* stats) {
+    return guarded([&] {
+        if (m == nullptr) throw std::invalid_argument("multi_run: null handle");
+        (void)from_c(&m->cfg);  // this rank's device / stream options
+        csaidx::MemoryLedger ledger;
+        csaidx::RunStats rs;
+        m->rank->run(q, kc, dtype, w, local_idx, local_val, ledger, &rs);
+        fill_stats(stats, rs, ledger, 1);
+    });
+}
+
+int csaidx_multi_destroy(csaidx_multi* m) {
+    return guarded([&] {
+        if (m == nullptr) return;
+        delete m->rank;
+        delete m;
+    });
+}
+
 }  // extern "C"

@@ -206,6 +206,9 @@ cudaError_t launch_bool_mask(uint8_t* keep, int64_t rows, int64_t cols, int64_t 
                              int64_t ratio, cudaStream_t stream);
 cudaError_t launch_apply_bool_mask(float* scores, int64_t ld, const uint8_t* keep, int64_t batch,
                                    int64_t rows, int64_t cols, cudaStream_t stream);
+cudaError_t launch_narrow(const int64_t* src, int32_t* dst, int64_t n, cudaStream_t stream);
+cudaError_t launch_scatter_rows(const int32_t* src, int32_t* dst, const int64_t* dst_row, int64_t nrows,
+                                int64_t row_elems, cudaStream_t stream);
 // Counter-based synthetic normal generator (splitmix64 hash of the element
 // index + Box-Muller), rounded to bf16 or kept fp32.
 cudaError_t launch_gen_normal_bf16(__nv_bfloat16* dst, int64_t n, double stddev, uint64_t seed,

@@ -103,9 +103,47 @@ unsigned grid_for(int64_t n, int threads) {
     return static_cast<unsigned>(g);
 }
 
+__global__ void narrow_kernel(const int64_t* __restrict__ src, int32_t* __restrict__ dst, int64_t n) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        dst[i] = static_cast<int32_t>(src[i]);
+}
+
+// one warp per row; rows are k int32 (k % 4 == 0: 16-byte copies)
+__global__ void scatter_rows_kernel(const int32_t* __restrict__ src, int32_t* __restrict__ dst,
+                                    const int64_t* __restrict__ dst_row, int64_t nrows, int64_t row_elems) {
+    const int lane = threadIdx.x & 31;
+    const bool vec = (row_elems & 3) == 0;
+    for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; r < nrows;
+         r += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+        const int32_t* s = src + r * row_elems;
+        int32_t* d = dst + __ldg(dst_row + r) * row_elems;
+        if (vec) {
+            for (int64_t i = lane; i < row_elems / 4; i += 32)
+                reinterpret_cast<int4*>(d)[i] = __ldg(reinterpret_cast<const int4*>(s) + i);
+        } else {
+            for (int64_t i = lane; i < row_elems; i += 32) d[i] = __ldg(s + i);
+        }
+    }
+}
+
 }  // namespace
 
 namespace csaidx_kern {
+
+cudaError_t launch_narrow(const int64_t* src, int32_t* dst, int64_t n, cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    narrow_kernel<<<grid_for(n, 256), 256, 0, stream>>>(src, dst, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_rows(const int32_t* src, int32_t* dst, const int64_t* dst_row, int64_t nrows,
+                                int64_t row_elems, cudaStream_t stream) {
+    if (nrows <= 0) return cudaSuccess;
+    scatter_rows_kernel<<<grid_for(nrows * 32, 256), 256, 0, stream>>>(src, dst, dst_row, nrows, row_elems);
+    return cudaGetLastError();
+}
+
 
 cudaError_t launch_convert_bf16(const ConvertParams& p, cudaStream_t stream) {
     if (p.n <= 0) return cudaSuccess;

@@ -1,11 +1,11 @@
-"""Query-axis sharding for multi-GPU runs (one process per GPU).
+"""Query-axis sharding helpers for multi-GPU runs (one process per GPU).
 
-Query rows are independent (reference driver.cpp:132-133), so the c_S query
-chunks are split across ranks; only two exchanges exist: the keys are
-broadcast once from rank 0, and the [S, k] index rows are gathered back.
-Chunk cost is proportional to its causal work (sum of t_legal over its
-rows), so contiguous blocks would hand the last rank ~(2P-1)/P^2 of the work;
-chunks are assigned by LPT (longest first, to the least-loaded rank) instead.
+The plan itself is the library's (csaidx::gpu::plan_shards, C++; LPT over
+the c_S chunks by causal work — see paper_2605_02568_b200/multi.py). Query
+rows are independent (reference driver.cpp:132-133), so only two exchanges
+exist: the keys are broadcast once from rank 0 and the [S, k] index rows are
+collected on rank 0. These helpers keep the old (S, m, c_S, world) call form
+for bench.py and the tests.
 """
 from __future__ import annotations
 
@@ -25,16 +25,11 @@ def chunk_work(seq_len: int, ratio: int, query_tile: int, s0: int) -> int:
 
 
 def plan_shards(seq_len: int, ratio: int, query_tile: int, world: int):
-    """-> (per-rank sorted chunk-start lists, per-rank work)."""
-    starts = chunk_starts(seq_len, query_tile)
-    cost = sorted(((chunk_work(seq_len, ratio, query_tile, s), s) for s in starts), reverse=True)
-    loads = [0] * world
-    owned: list[list[int]] = [[] for _ in range(world)]
-    for c, s in cost:
-        r = min(range(world), key=lambda i: (loads[i], i))
-        loads[r] += c
-        owned[r].append(s)
-    return [sorted(o) for o in owned], loads
+    """-> (per-rank sorted chunk-start lists, per-rank work): the library's LPT plan."""
+    from . import api, multi
+
+    dims = api.ProblemDims.create(1, seq_len, ratio, 1, 1, 1)
+    return multi.plan_shards(dims, query_tile, world)
 
 
 def rows_of(seq_len: int, query_tile: int, starts) -> int:

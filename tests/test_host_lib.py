@@ -33,8 +33,11 @@ def test_library_exports_every_declared_symbol(header, lib):
 
 
 def test_python_binding_covers_the_headers():
-    assert set(declared("csaidx_cuda.h")) == set(_capi.CUDA_SYMBOLS)
-    assert set(declared("csaidx_host.h")) == set(api.HOST_SYMBOLS)
+    from paper_2605_02568_b200 import multi
+
+    assert set(declared("csaidx_cuda.h")) == set(_capi.CUDA_SYMBOLS) | set(multi._SYMBOLS)
+    assert set(declared("csaidx_host.h")) == set(api.HOST_SYMBOLS) | set(multi._HOST_SYMBOLS)
+    multi._libs()  # every binding resolves
 
 
 def test_problem_dims_create_and_rejections():
