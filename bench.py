@@ -186,9 +186,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
-                    help="N>1: how rank 0 collects the index rows (peer stores from the select, or NCCL gather)")
-    ap.add_argument("--gather-groups", type=int, default=4,
-                    help="N>1: run each rank's chunks in this many groups, gathering group j during group j+1")
+                    help="N>1: how rank 0 collects the index rows (peer stores from the select, or a collective "
+                         "gather after the compute)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no e2e/baseline)")
     ap.add_argument("--simulate-rank", default=None, metavar="R/N",
@@ -261,63 +260,42 @@ def main():
         kc = torch.empty(B * T * D, dtype=torch.bfloat16, device="cuda")
     out_idx = torch.empty((B, rows, k), dtype=torch.int64, device="cuda")
     out_val = torch.empty((B, rows, k), dtype=torch.float32, device="cuda")
-    # Gather of the int32 index rows to rank 0, overlapped with the compute:
-    # each rank runs its chunks in G groups (G = --gather-groups, 1 for B > 1
-    # where a group's rows are not contiguous) and gathers group j's rows
-    # (async on NCCL's stream) while group j+1 computes. Every rank splits
-    # every shard the same way, so group j's padded size is known to all.
-    # --gather p2p (default): no gather collective — the final select kernels
-    # store every rank's int32 index rows straight into rank 0's [B, S, k]
-    # buffer through a CUDA IPC peer mapping (NVLink), fused with the select.
-    p2p = args.gather == "p2p" and world > 1
+    # N > 1: the library's query-sharded driver (csaidx_multi_*, C++
+    # csaidx::gpu::MultiRank) runs the step: kc broadcast from rank 0 over
+    # the transport (NCCL, or gloo for the one-GPU logic check), this rank's
+    # chunks, and the int32 [B, S, k] index rows into rank 0's buffer — stored
+    # there by the final select kernels over a CUDA IPC peer mapping
+    # (--gather p2p, default) or gathered after the compute (--gather nccl).
     drv_h = api.driver_engine(local)
-    sink = sink_ptr = None
-    handle = [None]
-    if p2p:
+    mr = sink = comm = None
+    p2p = False
+    if world > 1:
+        from paper_2605_02568_b200 import multi
+
+        if backend == "nccl":
+            uid = [multi.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            comm = multi.NcclCollectives(rank, world, uid[0], local)
+        else:
+            comm = multi.TorchCollectives()
+        if rank == 0:
+            sink = torch.full((B, S, k), -2, dtype=torch.int32, device="cuda")
+        mode = multi.GATHER_PEER if args.gather == "p2p" else multi.GATHER_COLLECTIVE
         try:
-            if rank == 0:
-                sink = torch.full((B, S, k), -2, dtype=torch.int32, device="cuda")
-                handle = [api.ipc_handle(drv_h, sink.data_ptr())]
-            dist.broadcast_object_list(handle, src=0)
-            sink_ptr = sink.data_ptr() if rank == 0 else api.ipc_open(drv_h, handle[0])
+            mr = multi.MultiRank(comm, dims, cfg, mode, sink)
             ok = True
-        except Exception as ex:  # no CUDA IPC / peer access here: fall back to the NCCL gather
-            print(f"rank {rank}: peer index sink unavailable ({ex}); using the NCCL gather", file=sys.stderr)
+        except Exception as ex:  # no CUDA IPC / peer access: the collective gather
+            print(f"rank {rank}: peer index sink unavailable ({ex}); using the collective gather", file=sys.stderr)
             ok = False
         oks = [None] * world
         dist.all_gather_object(oks, ok)
-        if all(oks):
-            api.set_index_sink(drv_h, sink_ptr, B, S, k)
-        else:
-            if ok and rank != 0:
-                api.ipc_close(drv_h, sink_ptr, handle[0])
-            p2p, sink, sink_ptr = False, None, None
-    G = max(1, args.gather_groups) if (world > 1 or plan_world > 1) and B == 1 and not p2p and \
-        not (world == 1 and args.gather == "p2p") else 1
-
-    def split(lst):
-        n = len(lst)
-        return [lst[n * j // G: n * (j + 1) // G] for j in range(G)]
-
-    def group_rows(shard):  # [(r0, r1)] of each group in the rank's local stack
-        out, r0 = [], 0
-        for grp in split(shard):
-            r1 = r0 + (api.chunk_rows(dims, cfg, grp) if grp else 0)
-            out.append((r0, r1))
-            r0 = r1
-        return out
-
-    my_groups = split(mine)
-    granges = [group_rows(sh) for sh in shards]          # [rank][group] -> (r0, r1)
-    gmax = [max(gr[j][1] - gr[j][0] for gr in granges) for j in range(G)]
-    max_rows = max(api.chunk_rows(dims, cfg, sh) for sh in shards)
-    pad = max(gmax) if G > 1 else 0  # grouped gather: group j may be sent padded to the longest shard
-    gathered = None
-    if plan_rank == 0 and plan_world > 1 and not p2p:  # also in --simulate-rank 0/N, for peak HBM
-        gathered = torch.empty((plan_world, B, max_rows + pad, k), dtype=torch.int32, device="cuda")
-    send = torch.zeros((B, max_rows + pad, k), dtype=torch.int32, device="cuda") if world > 1 and not p2p else None
-    q_rows = q.view(B, rows, H * D)
-    w_rows = w.view(B, rows, H)
+        if not all(oks):
+            if mr is not None:
+                mr.close()
+            mode = multi.GATHER_COLLECTIVE
+            mr = multi.MultiRank(comm, dims, cfg, mode, sink)
+        p2p = mode == multi.GATHER_PEER
+        assert mr.chunks == mine and mr.rows == rows
     torch.cuda.synchronize()
 
     def bcast(t):
@@ -328,57 +306,13 @@ def main():
             dist.broadcast(h, src=0)
             t.copy_(h)
 
-    def gather_group(j):
-        r0, r1 = granges[rank][j]
-        send[:, r0:r1].copy_(out_idx[:, r0:r1])  # int64 -> int32 (indices < T)
-        part = send[:, r0:r0 + gmax[j]]
-        if backend == "nccl":
-            dst = [gathered[r, :, granges[r][j][0]:granges[r][j][0] + gmax[j]] for r in range(world)] \
-                if rank == 0 else None
-            return dist.gather(part, dst, dst=0, async_op=True)
-        h = part.cpu()
-        bufs = [torch.empty_like(h) for _ in range(world)] if rank == 0 else None
-        dist.gather(h, bufs, dst=0)
-        if rank == 0:
-            for r in range(world):
-                gathered[r, :, granges[r][j][0]:granges[r][j][0] + gmax[j]].copy_(bufs[r])
-        return None
-
-    def run_groups(after_group=None):
-        st = None
-        works = []
-        for j, grp in enumerate(my_groups):
-            r0, r1 = granges[plan_rank][j]
-            if grp:
-                st = api.run_chunked_device(q_rows[:, r0:r1], kc, w_rows[:, r0:r1], dims, cfg, grp,
-                                            out_idx[:, r0:r1], out_val[:, r0:r1], local_rows=True)[2]
-            if after_group is not None:
-                works.append(after_group(j))
-        for wk in works:
-            if wk is not None:
-                wk.wait()
-        return st
-
     stats_box = {}
 
-    flag = torch.zeros(1, dtype=torch.int32, device="cuda") if p2p else None
-
     def step():
-        if world > 1:
-            bcast(kc)  # keys once over NVLink
-        if G == 1:
-            st = api.run_chunked_device(q, kc, w, dims, cfg, mine, out_idx, out_val, local_rows=True)[2]
-            if p2p:  # every rank's rows are in rank 0's buffer once all ranks pass this point
-                if backend == "nccl":
-                    dist.all_reduce(flag)
-                else:
-                    dist.barrier()
-            elif world > 1:
-                w0 = gather_group(0)  # only the [S, k] indices travel
-                if w0 is not None:
-                    w0.wait()
+        if mr is not None:
+            st = mr.run(q, kc, w, out_idx, out_val)
         else:
-            st = run_groups(gather_group if world > 1 else None)
+            st = api.run_chunked_device(q, kc, w, dims, cfg, mine, out_idx, out_val, local_rows=True)[2]
         stats_box["st"] = st
 
     drv = api.KernelStats(drv_h)
@@ -415,11 +349,10 @@ def main():
             t = h
         ms = float(t.item())
     gather_ok = None
-    if p2p:
+    if world > 1:
         # untimed check: rank 0's buffer holds every rank's rows (per-rank
         # checksums over each shard's rows), its own rows bit for bit, and no
         # row was left unwritten
-        api.set_index_sink(drv_h, None)
         torch.cuda.synchronize()
         mine_sum = int(out_idx.sum().item())
         sums = [None] * world
@@ -434,18 +367,6 @@ def main():
             ok = ok and np.array_equal(full[:, own], out_idx.cpu().numpy().astype(np.int32))
             gather_ok = bool(ok)
         dist.barrier()
-        if rank != 0:
-            api.ipc_close(drv_h, sink_ptr, handle[0])
-    elif world > 1 and rank == 0:
-        # the gathered rows reassemble into sequence order (checked once, untimed)
-        from paper_2605_02568_b200.shard import assemble
-
-        parts = [gathered[r][:, : api.chunk_rows(dims, cfg, shards[r])].cpu().numpy() for r in range(world)]
-        full = assemble(parts, shards, S, cs)
-        # rank 0's own rows came back intact, and every gathered entry is a
-        # key index or the -1 sentinel (no stale / padding rows leaked in)
-        gather_ok = bool(np.array_equal(parts[0], out_idx.cpu().numpy().astype(np.int32)) and
-                         full.min() >= -1 and full.max() < T)
     kinds = {"score": _capi.KIND_SCORE, "select": _capi.KIND_SELECT, "merge": _capi.KIND_MERGE,
              "finalize": _capi.KIND_FINALIZE, "prep": _capi.KIND_PREP}
     kstats = {name: drv.get(kd) for name, kd in kinds.items()}
@@ -579,18 +500,23 @@ def main():
             "e2e": e2e,
             "run_stats": {"dispatch_count": st.dispatch_count, "tiles_skipped_masked": st.tiles_skipped_masked},
             "multi_gpu": {"rank_work_pairs": loads, "gather_reassembly_ok": gather_ok,
-                          "collectives": ("none on the data path: broadcast kc (bf16) from rank 0; the final select "
-                                          "kernels store each rank's int32 [rows,k] index rows straight into rank 0's "
-                                          f"[B,S,k] buffer over a CUDA IPC peer mapping (fused gather); a 1-element "
-                                          f"{backend} barrier ends the step") if p2p else
-                                         ((f"broadcast kc (bf16) from rank 0 + gather of int32 [rows,k] index rows to "
-                                           f"rank 0 in {G} row groups, group j's gather overlapping group j+1's "
-                                           f"compute ({backend})") if world > 1 else "none"),
+                          "driver": ("libcsaidx.so csaidx_multi_run (csaidx::gpu::MultiRank), "
+                                     f"{'NCCL' if backend == 'nccl' else 'gloo host-staged'} transport")
+                          if world > 1 else "single GPU",
+                          "collectives": ("broadcast kc (bf16) from rank 0; the final select kernels store each "
+                                          "rank's int32 [rows,k] index rows straight into rank 0's [B,S,k] buffer "
+                                          "over a CUDA IPC peer mapping (fused gather); a 1-element barrier ends "
+                                          "the step") if p2p else
+                                         ("broadcast kc (bf16) from rank 0 + gather of the int32 [rows,k] index "
+                                          "rows to rank 0 after the compute (grouped send/recv), scattered into "
+                                          "sequence order on rank 0" if world > 1 else "none"),
                           "rank_rows": rows, "rank_pairs": pairs_mine},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
+        mr.close()
+        comm.close()
         dist.destroy_process_group()
 
 
