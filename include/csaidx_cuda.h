@@ -208,11 +208,15 @@ int csaidx_cuda_apply_bool_mask(csaidx_engine* e, float* scores, int64_t ld, con
 /* tile_topk (topk.hpp:71, topk.cpp:105-132): per (b, row) top-min(k, n)
  * under succ, n = legal columns (apply_mask) or cols; output rows of
  * width = min(k, cols) at stride cand_ld, indices offset by t0, padded with
- * (-inf, -1). Requires min(k, cols) <= csaidx_cuda_select_capacity(). */
+ * (-inf, -1). Any k: takes up to csaidx_cuda_select_capacity() run in
+ * shared memory (sampled threshold + bucket finish); larger takes run an
+ * exact radix select + bitonic sort over global scratch owned by the engine
+ * (the merge stages k > capacity rows in that scratch too). */
 int csaidx_cuda_select(csaidx_engine* e, const float* scores, int64_t batch, int64_t rows,
                        int64_t ld, int64_t cols, int64_t s0, int64_t t0, int64_t ratio,
                        int apply_mask, int64_t k, float* cand_val, int32_t* cand_idx,
                        int64_t cand_ld);
+/* Largest take of the shared-memory select (4096). */
 int csaidx_cuda_select_capacity(void);
 /* 1 when the persistent multi-row select (csaidx_engine_set_partition) fits
  * shared memory for this k (k <= 1365 with 3 rows per CTA). */

@@ -121,6 +121,10 @@ struct csaidx_engine {
     cudaEvent_t entry_event = nullptr;  // csaidx_engine_await_stream
     int32_t* sink = nullptr;            // csaidx_engine_set_index_sink
     int64_t sink_batch = 0, sink_seq = 0, sink_k = 0;
+    // global scratch of the large-take select / merge (k > 4096), grown on
+    // demand and counted in live / peak
+    void* large = nullptr;
+    size_t large_bytes = 0;
     // SM partition while a select runs beside the score kernel (0 = whole GPU)
     int score_sms = 0;
     int select_sms = 0;
@@ -255,6 +259,7 @@ int csaidx_engine_destroy(csaidx_engine* e) {
     }
     for (cudaEvent_t ev : e->event_pool) cudaEventDestroy(ev);
     if (e->flags) cudaFree(e->flags);
+    if (e->large) cudaFree(e->large);
     for (int i = 1; i < 4; ++i)
         if (e->lanes[i]) cudaStreamDestroy(e->lanes[i]);
     for (cudaEvent_t ev : e->slots)
@@ -817,6 +822,24 @@ int csaidx_cuda_select_overlap_capable(int64_t k) {
 
 namespace {
 
+// The engine's large-take scratch, at least `need` bytes (a growth waits for
+// the queued work that may still use the old buffer).
+int large_scratch(csaidx_engine* e, size_t need) {
+    if (e->large_bytes >= need) return CSAIDX_OK;
+    CSAIDX_CUDA_TRY(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    if (e->large != nullptr) {
+        cudaFree(e->large);
+        e->live -= e->large_bytes;
+        e->large = nullptr;
+        e->large_bytes = 0;
+    }
+    CSAIDX_CUDA_TRY(cudaMalloc(&e->large, need), "cudaMalloc(large-take scratch)");
+    e->large_bytes = need;
+    e->live += need;
+    if (e->live > e->peak) e->peak = e->live;
+    return CSAIDX_OK;
+}
+
 // The index sink holds [sink_batch, sink_seq, sink_k] int32: a final write
 // of rows [s0, s0 + rows) of `batch` batches at row stride k must fit it.
 int check_sink(const csaidx_engine* e, int64_t batch, int64_t s0, int64_t rows, int64_t k) {
@@ -840,9 +863,7 @@ int select_impl(csaidx_engine* e, const float* scores, int64_t batch, int64_t ro
     if ((ld % 4) != 0 || ld < cols) return fail(CSAIDX_INVALID_ARGUMENT, "select: ld must be >= cols, multiple of 4");
     if ((reinterpret_cast<uintptr_t>(scores) & 15) != 0) return fail(CSAIDX_INVALID_ARGUMENT, "select: scores not 16B aligned");
     const int64_t width = final_idx != nullptr ? k : (k < cols ? k : cols);
-    if (width > csaidx_kern::select_max_take())
-        return fail(CSAIDX_INVALID_ARGUMENT, "tile_topk: min(k, cols) = %lld exceeds the GPU select capacity %d",
-                    static_cast<long long>(width), csaidx_kern::select_max_take());
+    if (k > (int64_t{1} << 30)) return fail(CSAIDX_INVALID_ARGUMENT, "tile_topk: top_k too large");
     if (cand_ld < width) return fail(CSAIDX_INVALID_ARGUMENT, "select: cand_ld < min(k, cols)");
     SelectParams p{};
     p.scores = scores;
@@ -875,6 +896,15 @@ int select_impl(csaidx_engine* e, const float* scores, int64_t batch, int64_t ro
     p.persistent_ctas = e->select_sms;
     p.gmax = gmax;
     p.gmax_ld = gmax_ld;
+    if (k > csaidx_kern::select_max_take() || width > csaidx_kern::select_max_take()) {
+        if (pass_bits != nullptr || gmax != nullptr)
+            return fail(CSAIDX_INVALID_ARGUMENT, "select: candidate filters need k <= %d", csaidx_kern::select_max_take());
+        const size_t need = csaidx_kern::select_large_scratch_bytes(static_cast<int>(k), cols, batch * rows);
+        if (int rc = large_scratch(e, need)) return rc;
+        p.scratch = e->large;
+        p.scratch_bytes = e->large_bytes;
+        p.persistent_ctas = 0;
+    }
     LaunchScope ls(e, CSAIDX_KIND_SELECT);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_select(p, e->stream), "select");
     return CSAIDX_OK;
@@ -921,8 +951,7 @@ int csaidx_cuda_merge(csaidx_engine* e, float* run_val, int32_t* run_idx, int64_
                       const float* cand_val, const int32_t* cand_idx, int64_t cand_ld, int64_t width, int overwrite,
                       int check_overlap) {
     if (int rc = set_device(e)) return rc;
-    if (k < 1 || k > csaidx_kern::select_max_take())
-        return fail(CSAIDX_INVALID_ARGUMENT, "merge: k must be in [1, %d]", csaidx_kern::select_max_take());
+    if (k < 1 || k > (int64_t{1} << 30)) return fail(CSAIDX_INVALID_ARGUMENT, "merge: k must be >= 1");
     if (width < 0 || width > k || cand_ld < width) return fail(CSAIDX_INVALID_ARGUMENT, "merge: bad candidate width");
     MergeParams p{};
     p.run_val = run_val;
@@ -936,6 +965,14 @@ int csaidx_cuda_merge(csaidx_engine* e, float* run_val, int32_t* run_idx, int64_
     p.overwrite = overwrite;
     p.check_overlap = check_overlap;
     p.overlap_flag = e->flags + kOverlap;
+    if (k > csaidx_kern::select_max_take() && !overwrite) {
+        const size_t row = static_cast<size_t>(k + width) * sizeof(uint64_t);
+        if (int rc = large_scratch(e, csaidx_kern::merge_stage_bytes(static_cast<int>(k), static_cast<int>(width),
+                                                                      nrows)))
+            return rc;
+        p.stage = static_cast<uint64_t*>(e->large);
+        p.stage_rows = static_cast<int64_t>(e->large_bytes / row);
+    }
     LaunchScope ls(e, CSAIDX_KIND_MERGE);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_merge(p, e->stream), "merge");
     return CSAIDX_OK;

@@ -68,8 +68,6 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
               const ChunkPlan& plan, int64_t* out_idx, float* out_val, int64_t out_rows, MemoryLedger& ledger,
               RunStats& stats, const ChunkHooks& hooks) {
     const int64_t B = dims.batch, k = dims.top_k, T = dims.key_blocks;
-    if (std::min(k, plan.ct) > csaidx_cuda_select_capacity() || k > csaidx_cuda_select_capacity())
-        throw std::invalid_argument("top_k exceeds the GPU selection capacity (4096)");
     const int kcode = kernel_code(config.kernel);
     const int mcode = mode_code(config.mode);
     const csaidx_dims cd = to_c(dims);
@@ -255,8 +253,6 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
 void run_materialize_device(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, int mode, int kernel,
                             int64_t* out_idx, float* out_val, MemoryLedger& ledger) {
     const int64_t B = dims.batch, S = dims.seq_len, T = dims.key_blocks, k = dims.top_k;
-    if (std::min(k, T) > csaidx_cuda_select_capacity())
-        throw std::invalid_argument("top_k exceeds the GPU selection capacity (4096)");
     LedgerCharge charge(ledger, "score_tile", chunk_tile_bytes(B, S, T));
     const int64_t ld = (T + 3) / 4 * 4;
     const csaidx_dims cd = to_c(dims);

@@ -112,6 +112,10 @@ struct SelectParams {
     // buffer that may live in another GPU's memory (CUDA IPC peer mapping)
     int32_t* sink;
     int64_t sink_seq;
+    // Global scratch for takes above the shared-memory capacity (k > 4096):
+    // per-row slots of select_large_scratch_bytes(); required then, else unused
+    void* scratch;
+    size_t scratch_bytes;
 };
 
 // Per-row candidate threshold from a strided sample of the row's scores
@@ -143,6 +147,10 @@ struct MergeParams {
     int overwrite;
     int check_overlap;
     int* overlap_flag;
+    // k above the shared-memory merge (4096): both rows are staged as
+    // composites in global scratch, stage_rows rows of (k + width) at a time
+    uint64_t* stage;
+    int64_t stage_rows;
 };
 
 // ------------------------------------------------------------------ finalize
@@ -196,6 +204,10 @@ int select_max_take();
 int select_cand_capacity(int k);  // candidate-list length the select kernel accepts for this k
 bool select_fat_fits(int k);      // the persistent multi-row form fits shared memory for this k
 cudaError_t launch_select(const SelectParams& p, cudaStream_t stream);
+// Scratch the select needs for takes above select_max_take() (rows = B * rows).
+size_t select_large_scratch_bytes(int k, int64_t cols, int64_t rows);
+// Staging scratch the merge needs for k above select_max_take().
+size_t merge_stage_bytes(int k, int width, int64_t nrows);
 cudaError_t launch_tau(const TauParams& p, cudaStream_t stream);
 cudaError_t launch_merge(const MergeParams& p, cudaStream_t stream);
 cudaError_t launch_finalize(const FinalizeParams& p, cudaStream_t stream);

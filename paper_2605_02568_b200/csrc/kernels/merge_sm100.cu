@@ -39,8 +39,9 @@ __device__ __forceinline__ void unpack(uint64_t c, float& v, int32_t& idx) {
 
 __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const MergeParams p) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    uint64_t* a = reinterpret_cast<uint64_t*>(smem_raw);
     const int64_t row = blockIdx.x;
+    uint64_t* a = p.stage != nullptr ? p.stage + row * (static_cast<int64_t>(p.k) + p.width)
+                                     : reinterpret_cast<uint64_t*>(smem_raw);
     float* rv = p.run_val + row * p.k;
     int32_t* ri = p.run_idx + row * p.k;
     const float* cv = p.cand_val + row * p.cand_ld;
@@ -199,9 +200,38 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
 
 namespace csaidx_kern {
 
+constexpr size_t kStageBudget = size_t{256} << 20;  // bytes of global staging per launch slab
+
+size_t merge_stage_bytes(int k, int width, int64_t nrows) {
+    const size_t row = (static_cast<size_t>(k) + static_cast<size_t>(width)) * sizeof(uint64_t);
+    int64_t R = static_cast<int64_t>(kStageBudget / row);
+    if (R < 1) R = 1;
+    if (R > nrows) R = nrows;
+    return static_cast<size_t>(R) * row;
+}
+
 cudaError_t launch_merge(const MergeParams& p, cudaStream_t stream) {
     if (p.nrows <= 0) return cudaSuccess;
-    if (p.k > kMaxK) return cudaErrorInvalidValue;
+    if (p.k > kMaxK && !p.overwrite) {
+        // global staging, in slabs of stage_rows rows
+        if (p.stage == nullptr || p.stage_rows < 1) return cudaErrorInvalidValue;
+        for (int64_t r0 = 0; r0 < p.nrows; r0 += p.stage_rows) {
+            MergeParams q = p;
+            q.nrows = p.nrows - r0 < p.stage_rows ? p.nrows - r0 : p.stage_rows;
+            q.run_val = p.run_val + r0 * p.k;
+            q.run_idx = p.run_idx + r0 * p.k;
+            q.cand_val = p.cand_val + r0 * p.cand_ld;
+            q.cand_idx = p.cand_idx + r0 * p.cand_ld;
+            merge_kernel<<<static_cast<unsigned>(q.nrows), kMergeThreads, 0, stream>>>(q);
+        }
+        return cudaGetLastError();
+    }
+    MergeParams q = p;
+    q.stage = nullptr;
+    if (p.overwrite) {  // A1: a row copy, no staging
+        merge_kernel<<<static_cast<unsigned>(p.nrows), kMergeThreads, 0, stream>>>(q);
+        return cudaGetLastError();
+    }
     const size_t smem = (static_cast<size_t>(p.k) + static_cast<size_t>(p.width)) * sizeof(uint64_t);
     static bool attr_set[kMaxDevices] = {};
     const int attr_set_dev = attr_device();
@@ -211,7 +241,7 @@ cudaError_t launch_merge(const MergeParams& p, cudaStream_t stream) {
         if (e != cudaSuccess) return e;
         attr_set[attr_set_dev] = true;
     }
-    merge_kernel<<<static_cast<unsigned>(p.nrows), kMergeThreads, smem, stream>>>(p);
+    merge_kernel<<<static_cast<unsigned>(p.nrows), kMergeThreads, smem, stream>>>(q);
     return cudaGetLastError();
 }
 

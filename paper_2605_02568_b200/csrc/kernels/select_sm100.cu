@@ -1133,6 +1133,53 @@ __global__ void __launch_bounds__(kThreads) tau_kernel(const TauParams p) {
     if (gtid() == 0) *out = ord_key_to_float(pbits >= 32 ? prefix : (prefix << (32 - pbits)));
 }
 
+// ------------------------------------------------------------------ large take
+// take = min(k, n) above the shared-memory select's capacity (k > 4096: the
+// reference's tile_topk / oracle_topk accept any k, topk.cpp:105-132,
+// 193-206). One CTA per row over global scratch: the exact MSB-first radix
+// select (histogram passes over the row, index-ordered collection of the tied
+// bin) picks the top take into the row's slot, a bitonic sort over the slot
+// orders them under succ, and write_row emits the row. Exact for any n, k.
+constexpr int kLargeCand = 8192;                          // tied-bin collection capacity
+constexpr size_t kLargeScratchBudget = size_t{256} << 20;  // bytes of slots per launch slab
+
+__host__ __device__ inline int64_t large_slot_elems(int k, int64_t cols) {
+    const int64_t take = k < cols ? k : cols;
+    int64_t p = 1;
+    while (p < take) p <<= 1;
+    return p + kLargeCand;
+}
+
+__global__ void __launch_bounds__(kThreads) select_large_kernel(const SelectParams p, int64_t fr0, int64_t slot_elems) {
+    __shared__ uint32_t hist[kBins];
+    __shared__ uint32_t wtot[4 * kWarps], wsum[kWarps], res[8];
+    const int64_t fr = fr0 + blockIdx.x;
+    const int b = static_cast<int>(fr / p.rows);
+    const int64_t row_id = fr - static_cast<int64_t>(b) * p.rows;
+    int64_t n = p.cols;
+    if (p.apply_mask) {
+        n = (p.s0 + row_id + 1) / p.ratio - p.t0;
+        n = n < 0 ? 0 : (n > p.cols ? p.cols : n);
+    }
+    const int take = static_cast<int>(n < p.k ? n : p.k);
+    const float* row = p.scores + (static_cast<int64_t>(b) * p.rows + row_id) * p.ld;
+    uint64_t* buf = static_cast<uint64_t*>(p.scratch) + static_cast<int64_t>(blockIdx.x) * slot_elems;
+    uint64_t* cand = buf + (slot_elems - kLargeCand);
+    if (take > 0) {
+        if (take == n) {
+            for (int64_t i = gtid(); i < n; i += kThreads) buf[i] = composite(ord_key(__ldg(row + i)), i);
+        } else {
+            if (gtid() == 0 && p.fallbacks != nullptr) atomicAdd(p.fallbacks, 0);
+            exact_global_select(row, n, take, buf, cand, kLargeCand, hist, wtot, res, wsum);
+        }
+        const int P = pow2_at_least(take);
+        for (int i = take + gtid(); i < P; i += kThreads) buf[i] = 0;
+        csync();
+        sort_desc(buf, P);
+    }
+    write_row(p, b, row_id, take, buf);
+}
+
 }  // namespace
 
 namespace csaidx_kern {
@@ -1178,8 +1225,29 @@ int select_variant() {
 constexpr size_t kFatSmemMax = 226 * 1024;
 bool select_fat_fits(int k) { return kFatGroups * smem_bytes_for(k) <= kFatSmemMax; }
 
+size_t select_large_scratch_bytes(int k, int64_t cols, int64_t rows) {
+    const size_t slot = static_cast<size_t>(large_slot_elems(k, cols)) * sizeof(uint64_t);
+    int64_t R = static_cast<int64_t>(kLargeScratchBudget / slot);
+    if (R < 1) R = 1;
+    if (R > rows) R = rows;
+    return static_cast<size_t>(R) * slot;
+}
+
 cudaError_t launch_select(const SelectParams& p, cudaStream_t stream) {
     if (p.rows <= 0 || p.batch <= 0) return cudaSuccess;
+    if (p.k > kMaxTake || p.width > kMaxTake) {
+        // large take: one CTA per row over global slots, in slabs of rows
+        const int64_t total = p.rows * p.batch;
+        const int64_t slot = large_slot_elems(p.k, p.cols);
+        if (p.scratch == nullptr || p.scratch_bytes < select_large_scratch_bytes(p.k, p.cols, total))
+            return cudaErrorInvalidValue;
+        const int64_t R = static_cast<int64_t>(p.scratch_bytes / (static_cast<size_t>(slot) * sizeof(uint64_t)));
+        for (int64_t fr0 = 0; fr0 < total; fr0 += R) {
+            const int64_t nr = total - fr0 < R ? total - fr0 : R;
+            select_large_kernel<<<static_cast<unsigned>(nr), kThreads, 0, stream>>>(p, fr0, slot);
+        }
+        return cudaGetLastError();
+    }
     if (p.persistent_ctas > 0 && p.phase_clk == nullptr && select_fat_fits(p.k)) {
         static bool fat_attr[kMaxDevices] = {};
         const int fat_attr_dev = attr_device();

@@ -513,3 +513,22 @@ def test_tensor_core_path_at_max_k_matches_reference_rule(orc):
     legal = [(s + 1) // m for s in rows]
     rep = check_rows(res.indices[0][rows], res.values[0][rows], full, legal, k)
     assert rep["rows"] == len(rows)
+
+
+@pytest.mark.parametrize("k,cs,ct", [(5000, 1024, 10 ** 6), (5000, 512, 2048), (9000, 4096, 3000), (20000, 8192, 10 ** 6)])
+def test_k_above_shared_capacity_bit_exact(orc, k, cs, ct):
+    """the drop-in accepts any k like the reference's
+    tile_topk / merge_topk (topk.cpp:105-172). Exact-order kernel shapes, so
+    indices, values and RunStats are bit-exact against the oracle — through
+    the one-key-tile final select (c_T = T), the shared-memory select plus
+    the staged global merge (c_T < k) and the large-take select (k > c_T)."""
+    B, S, m, H, D = 1, 8192, 1, 2, 3
+    inputs, dims, (q, kc, w) = inputs_for(orc, B, S, m, H, D, k, k + cs)
+    res, stats = api.run_chunked(inputs, dims, api.DriverConfig(tile=api.TileConfig(cs, ct)))
+    rc, idx, val, st3 = orc.run_chunked(q, kc, w, m, k, cs, ct)
+    assert rc == 0
+    assert np.array_equal(res.indices, idx) and np.array_equal(bits(res.values), bits(val))
+    assert [stats.dispatch_count, stats.tiles_skipped_masked, stats.tiles_skipped_narrow] == list(st3)
+    if k == 5000 and ct > S:
+        mres, _ = api.run_materialize(inputs, dims)
+        assert np.array_equal(mres.indices, idx) and np.array_equal(bits(mres.values), bits(val))

@@ -160,3 +160,14 @@ def test_k4096_rows_beyond_candidate_capacity_stratified(orc):
     idx, val, _ = api.run_chunked_device(q, kc, w, dims, api.DriverConfig(tile=api.TileConfig(cs, S // M)))
     rows = stratified_rows(S, M, k, cand_cap(k), range(0, S, cs), cs, n=256, seed=5)
     check_sampled(orc, q, kc, w, idx, val, dims, rows, label="V4 S=65536 k=4096")
+
+
+def test_k8192_v4_stratified_oracle_rows(orc):
+    """k above the shared-memory select (4096) at the V4 shape on the tensor-core
+    path: the large-take select, held to the north-star rule."""
+    B, S, k, cs = 1, 65536, 8192, 2048
+    q, kc, w = device_operands(B, S, 12)
+    dims = api.ProblemDims.create(B, S, M, H, D, k)
+    idx, val, _ = api.run_chunked_device(q, kc, w, dims, api.DriverConfig(tile=api.TileConfig(cs, S // M)))
+    rows = stratified_rows(S, M, k, 2 * k, range(0, S, cs), cs, n=256, seed=6)
+    check_sampled(orc, q, kc, w, idx, val, dims, rows, label="V4 S=65536 k=8192")
