@@ -802,10 +802,13 @@ __device__ __forceinline__ void select_row(const SelectParams& p, int b, int64_t
                 for (uint32_t t = gtid(); t < ng; t += kThreads) {
                     const uint32_t g = glist[t];
                     const float4* src = reinterpret_cast<const float4*>(row + static_cast<int64_t>(g) * 32);
+                    const int64_t lim = n - static_cast<int64_t>(g) * 32;  // valid columns in the group
+                    // a partial last group loads only the float4s holding legal
+                    // columns (the rest may lie past the row's allocation)
                     float4 v[8];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) v[u] = __ldg(src + u);
-                    const int64_t lim = n - static_cast<int64_t>(g) * 32;  // valid columns in the group
+                    for (int u = 0; u < 8; ++u)
+                        v[u] = 4 * u < lim ? __ldg(src + u) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
                     uint32_t m = 0;
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
