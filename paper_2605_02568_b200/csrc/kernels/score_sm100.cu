@@ -570,10 +570,11 @@ __device__ __forceinline__ void score_exact_one(const ScoreExactParams& p, int b
     const int64_t t = p.t0 + j;
     const float neg_inf = -__int_as_float(0x7f800000);
     float* dst = p.out + (static_cast<int64_t>(b) * p.rows + i) * p.ld + j;
-    if (p.apply_mask && t >= t_legal_dev(s, p.ratio)) {
-        *dst = neg_inf;
-        return;
-    }
+    // Causally illegal entries are scored too: the reference checks the
+    // whole tile for non-finite fp32 scores before mask_tile
+    // (score.cpp:90-97, then causal.cpp:30-41), so an overflow at a future
+    // position raises runtime_error here as well.
+    const bool masked = p.apply_mask && t >= t_legal_dev(s, p.ratio);
     const bool f32 = p.operand_f32 != 0;
     const int64_t orow = static_cast<int64_t>(b) * p.op_rows + s + p.op_shift;
     const int64_t qbase = (orow * p.heads) * p.head_dim;
@@ -592,7 +593,7 @@ __device__ __forceinline__ void score_exact_one(const ScoreExactParams& p, int b
         if (p.fp16) acc = half_round_sat(acc);
     }
     if (!p.fp16 && !isfinite(acc)) atomicOr(p.nonfinite, 1);
-    *dst = acc;
+    *dst = masked ? neg_inf : acc;
 }
 
 __global__ void score_exact_kernel(const ScoreExactParams p) {

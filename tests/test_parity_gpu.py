@@ -532,3 +532,25 @@ def test_k_above_shared_capacity_bit_exact(orc, k, cs, ct):
     if k == 5000 and ct > S:
         mres, _ = api.run_materialize(inputs, dims)
         assert np.array_equal(mres.indices, idx) and np.array_equal(bits(mres.values), bits(val))
+
+
+def test_overflow_at_a_causally_illegal_position_raises_like_the_reference(orc):
+    """the reference scores the whole tile and rejects any
+    non-finite fp32 score before masking (score.cpp:90-97 then
+    causal.cpp:30-41), so an overflow that only occurs at a future (masked)
+    position still raises runtime_error. Row 0 has no legal key at m = 4;
+    q[0] * kc[0] overflows, every legal product stays finite."""
+    B, S, m, H, D, k = 1, 64, 4, 2, 5, 4
+    q, kc, w = orc.generate_inputs(B, S, m, H, D, 3)
+    q[0, 0] = 1e30
+    kc[0, 0] = 1e30
+    dims = api.ProblemDims.create(B, S, m, H, D, k)
+    inputs = api.IndexerInputs.validated(q, kc, w, dims)
+    for cfg in (api.DriverConfig(tile=api.TileConfig(16, 8)), api.DriverConfig(tile=api.TileConfig(S, S // m))):
+        with pytest.raises(ScoreRuntimeError):
+            api.run_chunked(inputs, dims, cfg)
+    with pytest.raises(ScoreRuntimeError):
+        api.run_materialize(inputs, dims)
+    # the same rows without the future overflow run through
+    q[0, 0] = 0.5
+    api.run_chunked(api.IndexerInputs.validated(q, kc, w, dims), dims, api.DriverConfig(tile=api.TileConfig(16, 8)))
