@@ -258,8 +258,16 @@ def main():
         kc = eng.gen_normal_bf16(B * T * D, D ** -0.5, 1, 2)
     else:
         kc = torch.empty(B * T * D, dtype=torch.bfloat16, device="cuda")
-    out_idx = torch.empty((B, rows, k), dtype=torch.int64, device="cuda")
-    out_val = torch.empty((B, rows, k), dtype=torch.float32, device="cuda")
+    # Output rows. A query-sharded rank (N > 1, or --simulate-rank 0/N)
+    # keeps no int64 / fp32 rows of its own: the final kernels store the
+    # int32 index rows into rank 0's [B, S, k] buffer and nothing else
+    # (north_star: only the [S, k] index output is collected); the local rows
+    # are produced once after the timed region for the correctness checks.
+    sink_only = world > 1 or (args.simulate_rank is not None and plan_rank == 0 and plan_world > 1)
+    out_idx = out_val = None
+    if not sink_only:
+        out_idx = torch.empty((B, rows, k), dtype=torch.int64, device="cuda")
+        out_val = torch.empty((B, rows, k), dtype=torch.float32, device="cuda")
     # N > 1: the library's query-sharded driver (csaidx_multi_*, C++
     # csaidx::gpu::MultiRank) runs the step: kc broadcast from rank 0 over
     # the transport (NCCL, or gloo for the one-GPU logic check), this rank's
@@ -269,6 +277,8 @@ def main():
     drv_h = api.driver_engine(local)
     mr = sink = comm = None
     p2p = False
+    if world == 1 and sink_only:  # --simulate-rank 0/N: rank 0's [B, S, k] int32 result buffer
+        sink = torch.full((B, S, k), -2, dtype=torch.int32, device="cuda")
     if world > 1:
         from paper_2605_02568_b200 import multi
 
@@ -311,6 +321,12 @@ def main():
     def step():
         if mr is not None:
             st = mr.run(q, kc, w, out_idx, out_val)
+        elif sink is not None:
+            api.set_index_sink(drv_h, sink.data_ptr(), B, S, k)
+            try:
+                st = api.run_chunked_device(q, kc, w, dims, cfg, mine, local_rows=True, outputs=False)[2]
+            finally:
+                api.set_index_sink(drv_h, None)
         else:
             st = api.run_chunked_device(q, kc, w, dims, cfg, mine, out_idx, out_val, local_rows=True)[2]
         stats_box["st"] = st
@@ -337,6 +353,14 @@ def main():
     torch.cuda.synchronize()
     clk = clocks.stop()
     drv.profiling(False)
+    # everything the line reports about the timed steps, before any untimed check runs
+    kinds = {"score": _capi.KIND_SCORE, "select": _capi.KIND_SELECT, "merge": _capi.KIND_MERGE,
+             "finalize": _capi.KIND_FINALIZE, "prep": _capi.KIND_PREP}
+    kstats = {name: drv.get(kd) for name, kd in kinds.items()}
+    _, drv_peak = drv.mem()
+    fallbacks = drv.select_fallbacks()
+    cand_hits = drv.candidate_hits()
+    hbm_peak = torch.cuda.max_memory_allocated() + drv_peak
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
         dist.barrier()
@@ -349,6 +373,13 @@ def main():
             t = h
         ms = float(t.item())
     gather_ok = None
+    if sink_only:  # this rank's own rows, once, for the checks below (untimed)
+        out_idx = torch.empty((B, rows, k), dtype=torch.int64, device="cuda")
+        out_val = torch.empty((B, rows, k), dtype=torch.float32, device="cuda")
+        api.run_chunked_device(q, kc, w, dims, cfg, mine, out_idx, out_val, local_rows=True)
+        if world == 1:
+            own = np.concatenate([np.arange(s0, min(s0 + cs, S)) for s0 in mine])
+            gather_ok = bool(np.array_equal(sink[:, own].cpu().numpy(), out_idx.cpu().numpy().astype(np.int32)))
     if world > 1:
         # untimed check: rank 0's buffer holds every rank's rows (per-rank
         # checksums over each shard's rows), its own rows bit for bit, and no
@@ -367,9 +398,6 @@ def main():
             ok = ok and np.array_equal(full[:, own], out_idx.cpu().numpy().astype(np.int32))
             gather_ok = bool(ok)
         dist.barrier()
-    kinds = {"score": _capi.KIND_SCORE, "select": _capi.KIND_SELECT, "merge": _capi.KIND_MERGE,
-             "finalize": _capi.KIND_FINALIZE, "prep": _capi.KIND_PREP}
-    kstats = {name: drv.get(kd) for name, kd in kinds.items()}
     launches = sum(n for n, _ in kstats.values())
     score_n, score_ms = kstats["score"]
     peaks, peak_src = load_peaks()
@@ -385,10 +413,6 @@ def main():
             sel_traffic = tj.get("select_dram_bytes_per_launch")
     sel_n, sel_ms = kstats["select"]
     select_gbs = (pairs_mine * 4 * args.steps) / (sel_ms / 1000.0) / 1e9 if sel_ms > 0 else None
-    _, drv_peak = drv.mem()
-    fallbacks = drv.select_fallbacks()
-    cand_hits = drv.candidate_hits()
-    hbm_peak = torch.cuda.max_memory_allocated() + drv_peak
     st = stats_box["st"]
 
     # ---------------------------------------------------------- e2e (host API)

@@ -47,7 +47,9 @@ struct DeviceOperands {
 // Device-resident Algorithm 2 over a subset of query chunks (all chunks when
 // chunk_starts is null). Chunk starts must be multiples of the clamped c_S;
 // chunk c of the list writes its rows to out rows [row0_c, row0_c + rows_c)
-// where row0 accumulates over the list. Outputs are device [B, out_rows, k].
+// where row0 accumulates over the list. Outputs are device [B, out_rows, k];
+// both may be null while an index sink is set on the driver's engine
+// (csaidx_engine_set_index_sink): the sink then receives the only copy.
 void run_chunked_device(const DeviceOperands& ops, const ProblemDims& dims,
                         const DriverConfig& config, const std::vector<int64_t>* chunk_starts,
                         int64_t* out_indices, float* out_values, int64_t out_rows,
@@ -104,8 +106,10 @@ public:
     // One step. q / w: this rank's rows (DeviceOperands::local_rows layout,
     // chunks() order); kc: [B, T, d_h] on every rank, read on rank 0 and
     // overwritten by the broadcast elsewhere. local_idx / local_val: this
-    // rank's [B, rows(), k] outputs (null: kept inside). On return the step
-    // is complete on every rank and rank 0's root_out holds all rows.
+    // rank's [B, rows(), k] outputs; both null with the peer gather: rank
+    // 0's int32 rows are the only output (the final kernels write nothing
+    // else), with the collective gather: kept inside. On return the step is
+    // complete on every rank and rank 0's root_out holds all rows.
     void run(const void* q, void* kc, int dtype, const float* w, int64_t* local_idx, float* local_val,
              MemoryLedger& ledger, RunStats* stats = nullptr);
 

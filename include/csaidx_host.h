@@ -169,7 +169,8 @@ int csaidx_multi_create(const csaidx_collectives* comm, const csaidx_dims* dims,
 int csaidx_multi_chunks(const csaidx_multi* m, const int64_t** starts, int64_t* n_chunks, int64_t* rows);
 /* One step: q / w this rank's rows (chunks order, [B, rows, ...]); kc
  * [B, T, d_h] read on rank 0 and broadcast into kc elsewhere; local_idx /
- * local_val this rank's [B, rows, k] outputs or NULL. Returns when rank 0's
+ * local_val this rank's [B, rows, k] outputs, or both NULL (peer gather:
+ * rank 0's int32 rows are then the only output). Returns when rank 0's
  * root_out holds every rank's rows. */
 int csaidx_multi_run(csaidx_multi* m, const void* q, void* kc, int dtype, const float* w, int64_t* local_idx,
                      float* local_val, csaidx_run_stats* stats);

@@ -380,11 +380,13 @@ def load_inputs_device(path, dims: ProblemDims, config: DriverConfig, chunk_star
 
 
 def run_chunked_device(q, kc, w, dims: ProblemDims, config: DriverConfig, chunk_starts=None, out_idx=None,
-                       out_val=None, local_rows=False):
+                       out_val=None, local_rows=False, outputs=True):
     """Device-resident Algorithm 2 (csaidx_device_run_chunked): torch CUDA tensors in, torch tensors out.
 
     local_rows: q / w hold only the listed chunks' rows, stacked in list order
-    (csaidx_device_run_chunked_local), as a query-sharded rank keeps them."""
+    (csaidx_device_run_chunked_local), as a query-sharded rank keeps them.
+    outputs=False: no int64 / fp32 output rows (needs an index sink on the
+    driver engine, set_index_sink, which then holds the only copy)."""
     import torch
 
     dtype = _capi.DTYPE_BF16 if q.dtype == torch.bfloat16 else _capi.DTYPE_F32
@@ -401,7 +403,7 @@ def run_chunked_device(q, kc, w, dims: ProblemDims, config: DriverConfig, chunk_
         n_chunks = starts.size
         cs = min(config.tile.query_tile, dims.seq_len)
         rows = int(sum(min(cs, dims.seq_len - int(s)) for s in starts))
-    if out_idx is None:
+    if out_idx is None and outputs:
         out_idx = torch.empty((dims.batch, rows, dims.top_k), dtype=torch.int64, device=q.device)
         out_val = torch.empty((dims.batch, rows, dims.top_k), dtype=torch.float32, device=q.device)
     st = RunStatsC()
@@ -412,8 +414,10 @@ def run_chunked_device(q, kc, w, dims: ProblemDims, config: DriverConfig, chunk_
         raise ValueError("local_rows: q / w must hold exactly the listed chunks' rows")
     _check(entry(
         c_void_p(q.data_ptr()), c_void_p(kc.data_ptr()), dtype, c_void_p(w.data_ptr()), ctypes.byref(cd),
-        ctypes.byref(cc), None if starts is None else _ptr(starts), n_chunks, c_void_p(out_idx.data_ptr()),
-        c_void_p(out_val.data_ptr()), out_idx.shape[1], ctypes.byref(st)))
+        ctypes.byref(cc), None if starts is None else _ptr(starts), n_chunks,
+        c_void_p(out_idx.data_ptr()) if out_idx is not None else None,
+        c_void_p(out_val.data_ptr()) if out_val is not None else None,
+        out_idx.shape[1] if out_idx is not None else rows, ctypes.byref(st)))
     stats = RunStats(st.dispatch_count, st.tiles_skipped_masked, st.tiles_skipped_narrow, st.ledger_peak_bytes,
                      st.device_peak_bytes, ExecutionPath.chunked)
     return out_idx, out_val, stats

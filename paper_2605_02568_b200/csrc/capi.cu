@@ -862,7 +862,7 @@ int select_impl(csaidx_engine* e, const float* scores, int64_t batch, int64_t ro
     if (rows < 1 || cols < 1 || batch < 1 || ratio < 1) return fail(CSAIDX_INVALID_ARGUMENT, "select: bad extents");
     if ((ld % 4) != 0 || ld < cols) return fail(CSAIDX_INVALID_ARGUMENT, "select: ld must be >= cols, multiple of 4");
     if ((reinterpret_cast<uintptr_t>(scores) & 15) != 0) return fail(CSAIDX_INVALID_ARGUMENT, "select: scores not 16B aligned");
-    const int64_t width = final_idx != nullptr ? k : (k < cols ? k : cols);
+    const int64_t width = final_rows > 0 ? k : (k < cols ? k : cols);
     if (k > (int64_t{1} << 30)) return fail(CSAIDX_INVALID_ARGUMENT, "tile_topk: top_k too large");
     if (cand_ld < width) return fail(CSAIDX_INVALID_ARGUMENT, "select: cand_ld < min(k, cols)");
     SelectParams p{};
@@ -888,10 +888,11 @@ int select_impl(csaidx_engine* e, const float* scores, int64_t batch, int64_t ro
     p.final_idx = final_idx;
     p.final_rows = final_rows;
     p.final_row0 = final_row0;
-    if (final_idx != nullptr) {
+    if (final_rows > 0) {  // select_final
         if (int rc = check_sink(e, batch, s0, rows, cand_ld)) return rc;
         p.sink = e->sink;
         p.sink_seq = e->sink_seq;
+        p.sink_only = final_idx == nullptr ? 1 : 0;
     }
     p.persistent_ctas = e->select_sms;
     p.gmax = gmax;
@@ -936,7 +937,8 @@ int csaidx_cuda_select_final(csaidx_engine* e, const float* scores, int64_t batc
                              int64_t cols, int64_t s0, int64_t t0, int64_t ratio, int64_t k, const uint32_t* pass_bits,
                              int64_t bits_ld, const float* gmax, int64_t gmax_ld, int64_t* out_idx, float* out_val,
                              int64_t out_rows, int64_t out_row0) {
-    if (out_idx == nullptr || out_val == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "select_final: null output");
+    if ((out_idx == nullptr) != (out_val == nullptr) || (out_idx == nullptr && e != nullptr && e->sink == nullptr))
+        return fail(CSAIDX_INVALID_ARGUMENT, "select_final: null output (allowed for both only with an index sink)");
     if (out_row0 < 0 || out_row0 + rows > out_rows)
         return fail(CSAIDX_INVALID_ARGUMENT, "select_final: rows out of range");
     if (pass_bits != nullptr && bits_ld < csaidx_cuda_candidate_words(cols))
@@ -1013,6 +1015,8 @@ int csaidx_cuda_finalize(csaidx_engine* e, const float* run_val, const int32_t* 
                          int64_t out_rows, int64_t out_row0) {
     if (int rc = set_device(e)) return rc;
     if (out_row0 < 0 || out_row0 + rows > out_rows) return fail(CSAIDX_INVALID_ARGUMENT, "finalize: rows out of range");
+    if ((out_idx == nullptr) != (out_val == nullptr) || (out_idx == nullptr && e->sink == nullptr))
+        return fail(CSAIDX_INVALID_ARGUMENT, "finalize: null output (allowed for both only with an index sink)");
     FinalizeParams p{};
     p.run_val = run_val;
     p.run_idx = run_idx;

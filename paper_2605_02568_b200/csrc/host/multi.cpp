@@ -157,7 +157,10 @@ void MultiRank::run(const void* q, void* kc, int dtype, const float* w, int64_t*
                     MemoryLedger& ledger, RunStats* stats) {
     Impl& m = *impl_;
     const int64_t B = dims_.batch, k = dims_.top_k, n_out = B * rows() * k;
-    if (local_idx == nullptr || local_val == nullptr) {
+    if (mode_ == GatherMode::peer && local_idx == nullptr && local_val == nullptr) {
+        // the rows' only copy is the int32 one in rank 0's buffer: the final
+        // kernels skip the local int64 / fp32 rows (less HBM, fewer writes)
+    } else if (local_idx == nullptr || local_val == nullptr) {
         std::lock_guard<std::mutex> lock(detail::engine_mutex());
         if (m.own_idx.bytes() < static_cast<size_t>(n_out) * 8) {
             m.own_idx = detail::DeviceBuffer(m.e, static_cast<size_t>(n_out) * 8);

@@ -112,6 +112,7 @@ struct SelectParams {
     // buffer that may live in another GPU's memory (CUDA IPC peer mapping)
     int32_t* sink;
     int64_t sink_seq;
+    int sink_only;  // final rows go to the sink only (final_idx / out_val unused)
     // Global scratch for takes above the shared-memory capacity (k > 4096):
     // per-row slots of select_large_scratch_bytes(); required then, else unused
     void* scratch;
@@ -169,7 +170,7 @@ struct FinalizeParams {
     int* trail_flag;        // sentinel entries do not trail
     int* keff_flag;         // valid != k_eff
     int32_t* sink;          // optional [B, sink_seq, k] int32 copy (SelectParams::sink)
-    int64_t sink_seq;
+    int64_t sink_seq;       // (out_idx / out_val null: the sink is the only output)
 };
 
 // ------------------------------------------------------------------ prep

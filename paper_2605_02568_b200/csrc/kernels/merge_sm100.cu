@@ -139,8 +139,9 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
     const float* rv = p.run_val + row * p.k;
     const int32_t* ri = p.run_idx + row * p.k;
     const float neg_inf = -__int_as_float(0x7f800000);
-    int64_t* oi = p.out_idx + (static_cast<int64_t>(b) * p.out_rows + p.out_row0 + i) * p.k;
-    float* ov = p.out_val + (static_cast<int64_t>(b) * p.out_rows + p.out_row0 + i) * p.k;
+    const bool outs = p.out_idx != nullptr;  // else the sink is the only output
+    int64_t* oi = outs ? p.out_idx + (static_cast<int64_t>(b) * p.out_rows + p.out_row0 + i) * p.k : nullptr;
+    float* ov = outs ? p.out_val + (static_cast<int64_t>(b) * p.out_rows + p.out_row0 + i) * p.k : nullptr;
     int32_t* si = p.sink != nullptr ? p.sink + (static_cast<int64_t>(b) * p.sink_seq + p.s0 + i) * p.k : nullptr;
     if (threadIdx.x == 0) {
         s_first = p.k;
@@ -163,9 +164,11 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
                 real += inf ? 0 : 1;
                 o[u] = inf ? -1ll : static_cast<long long>(xx[u]);
             }
-            *reinterpret_cast<float4*>(ov + e) = v;
-            *reinterpret_cast<longlong2*>(oi + e) = make_longlong2(o[0], o[1]);
-            *reinterpret_cast<longlong2*>(oi + e + 2) = make_longlong2(o[2], o[3]);
+            if (outs) {
+                *reinterpret_cast<float4*>(ov + e) = v;
+                *reinterpret_cast<longlong2*>(oi + e) = make_longlong2(o[0], o[1]);
+                *reinterpret_cast<longlong2*>(oi + e + 2) = make_longlong2(o[2], o[3]);
+            }
             if (si != nullptr)
                 *reinterpret_cast<int4*>(si + e) = make_int4(static_cast<int>(o[0]), static_cast<int>(o[1]),
                                                              static_cast<int>(o[2]), static_cast<int>(o[3]));
@@ -176,8 +179,10 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeParams p) {
             const bool inf = v == neg_inf;
             if (inf && e < first_inf) first_inf = e;
             real += inf ? 0 : 1;
-            ov[e] = v;
-            oi[e] = inf ? -1 : static_cast<int64_t>(ri[e]);
+            if (outs) {
+                ov[e] = v;
+                oi[e] = inf ? -1 : static_cast<int64_t>(ri[e]);
+            }
             if (si != nullptr) si[e] = inf ? -1 : ri[e];
         }
     }

@@ -598,31 +598,33 @@ __device__ const uint64_t* finish_row(const float* row, int64_t n, int take, int
 // (-inf, -1); int32 candidate rows, or with final_idx the int64 output rows
 // of the fused sentinel pass (finalize_kernel semantics).
 __device__ void write_row(const SelectParams& p, int b, int64_t row_id, int take, const uint64_t* result) {
-    const bool final_out = p.final_idx != nullptr;
+    const bool final_out = p.final_idx != nullptr || p.sink_only;
     const int64_t orow = final_out ? static_cast<int64_t>(b) * p.final_rows + p.final_row0 + row_id
                                    : static_cast<int64_t>(b) * p.rows + row_id;
-    float* ov = p.out_val + orow * p.out_ld;
     const float neg_inf = -__int_as_float(0x7f800000);
     if (final_out) {
-        int64_t* oi = p.final_idx + orow * p.out_ld;
+        // sink_only: the int32 sink row is the only output (a query-sharded
+        // rank whose rows are collected in rank 0's buffer)
+        float* ov = p.sink_only ? nullptr : p.out_val + orow * p.out_ld;
+        int64_t* oi = p.sink_only ? nullptr : p.final_idx + orow * p.out_ld;
         int32_t* si = p.sink != nullptr ? p.sink + (static_cast<int64_t>(b) * p.sink_seq + p.s0 + row_id) * p.out_ld
                                         : nullptr;
         for (int e = gtid(); e < p.width; e += kThreads) {
             int64_t idx = -1;
+            float v = neg_inf;
             if (e < take) {
                 const uint64_t c = result[e];
-                const float v = ord_key_to_float(static_cast<uint32_t>(c >> 32));
-                ov[e] = v;
+                v = ord_key_to_float(static_cast<uint32_t>(c >> 32));
                 idx = v == neg_inf ? -1 : composite_col(c) + p.t0;
-            } else {
-                ov[e] = neg_inf;
             }
-            oi[e] = idx;
+            if (ov != nullptr) ov[e] = v;
+            if (oi != nullptr) oi[e] = idx;
             if (si != nullptr) si[e] = static_cast<int32_t>(idx);  // peer store when the sink is remote
         }
         if (si != nullptr) __threadfence_system();  // the peer stores are performed before the kernel retires
         return;
     }
+    float* ov = p.out_val + orow * p.out_ld;
     int32_t* oi = p.out_idx + orow * p.out_ld;
     for (int e = gtid(); e < p.width; e += kThreads) {
         if (e < take) {

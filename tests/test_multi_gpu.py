@@ -86,6 +86,14 @@ def _worker(rank, world, port, gather, q_out):
             r += n
         if rank == 0:  # the assembled result: every rank's rows at their positions
             ok &= bool(torch.equal(root, fi.to(torch.int32)))
+        if gather == 0:  # peer gather without local outputs: rank 0's rows are the only copy
+            if rank == 0:
+                root.fill_(-7)
+            dist.barrier()
+            mr.run(q, kc, w)
+            torch.cuda.synchronize()
+            if rank == 0:
+                ok &= bool(torch.equal(root, fi.to(torch.int32)))
         mr.close()
     except Exception as ex:  # noqa: BLE001
         print(f"rank {rank}: {type(ex).__name__}: {ex}", flush=True)

@@ -455,6 +455,19 @@ def test_index_sink_receives_the_final_rows(orc, key_tile):
         api.run_chunked_device(qd, kd, wd, dims, cfg, [1536])  # rows [1536, 2048) fit
     finally:
         api.set_index_sink(h, None)
+    # sink only: no int64 / fp32 rows, the sink holds the same indices
+    sink2 = torch.full((2, 4096, 128), -7, dtype=torch.int32, device="cuda")
+    api.set_index_sink(h, sink2.data_ptr(), 2, 4096, 128)
+    try:
+        none_i, none_v, _ = api.run_chunked_device(qd, kd, wd, dims, cfg, starts, outputs=False)
+    finally:
+        api.set_index_sink(h, None)
+    assert none_i is None and none_v is None
+    torch.cuda.synchronize()
+    for n, s0 in enumerate(starts):
+        assert torch.equal(sink2[:, s0:s0 + 512], oi[:, n * 512:(n + 1) * 512].to(torch.int32))
+    with pytest.raises(InvalidArgument):  # no sink: outputs are required
+        api.run_chunked_device(qd, kd, wd, dims, cfg, starts, outputs=False)
 
 
 def _sink_child(handle, q, kc, w, starts, done):
