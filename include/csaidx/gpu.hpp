@@ -20,6 +20,9 @@ struct Options {
     void* stream = nullptr;    // cudaStream_t to enqueue on; nullptr = engine's own stream
 };
 
+// Options of the calling thread (and the default of threads that never set
+// their own). Each thread drives its own engine per device, so calls from
+// several threads run concurrently on their own streams.
 void set_options(const Options& options);
 Options options();
 

@@ -11,16 +11,27 @@ namespace csaidx {
 namespace gpu {
 
 namespace {
+// The process default (the last set_options of any thread) and the calling
+// thread's own setting: C-ABI entry points set the options of the thread
+// that calls them, so threads driving different devices / streams do not
+// see each other's.
 std::mutex g_opt_mu;
 Options g_options;
+thread_local bool t_opt_set = false;
+thread_local Options t_options;
 }  // namespace
 
 void set_options(const Options& o) {
-    std::lock_guard<std::mutex> lock(g_opt_mu);
-    g_options = o;
+    {
+        std::lock_guard<std::mutex> lock(g_opt_mu);
+        g_options = o;
+    }
+    t_options = o;
+    t_opt_set = true;
 }
 
 Options options() {
+    if (t_opt_set) return t_options;
     std::lock_guard<std::mutex> lock(g_opt_mu);
     return g_options;
 }
@@ -52,16 +63,19 @@ void check(int rc) {
     if (rc != CSAIDX_OK) throw_status(rc, csaidx_cuda_last_error());
 }
 
+// One engine per (thread, device): its own stream, lanes, latched flags and
+// scratch, so API calls from different threads run concurrently (each on its
+// thread's stream) instead of serialising on one process-wide engine. The
+// mutex guards a thread's engine against the helper threads of its own call.
 std::mutex& engine_mutex() {
-    static std::mutex mu;
+    thread_local std::mutex mu;
     return mu;
 }
 
 csaidx_engine* engine() {
-    static std::mutex mu;
-    static std::map<int, csaidx_engine*> engines;  // intentionally never destroyed (CUDA teardown order)
+    // intentionally never destroyed (CUDA teardown order at process exit)
+    thread_local std::map<int, csaidx_engine*> engines;
     const gpu::Options o = gpu::options();
-    std::lock_guard<std::mutex> lock(mu);
     auto it = engines.find(o.device);
     if (it == engines.end()) {
         csaidx_engine* e = nullptr;

@@ -21,7 +21,9 @@ namespace csaidx::detail {
 void check(int rc);
 [[noreturn]] void throw_status(int rc, const char* what);
 
-// Engine of gpu::options().device with the configured stream applied.
+// The calling thread's engine for gpu::options().device, with the configured
+// stream applied (one engine per thread and device: calls from different
+// threads overlap); engine_mutex() guards it within the thread's own call.
 csaidx_engine* engine();
 std::mutex& engine_mutex();
 

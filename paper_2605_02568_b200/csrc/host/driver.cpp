@@ -294,7 +294,7 @@ namespace {
 
 // Pinned bf16 staging slabs of the host-rounding pipeline, kept across calls
 // (pinning hundreds of MiB per call would cost more than the transfer).
-// Guarded by engine_mutex().
+// One set per calling thread (see engine()).
 struct PinnedSlabs {
     std::vector<void*> ptr;
     size_t bytes = 0;
@@ -321,7 +321,7 @@ struct PinnedSlabs {
 };
 
 PinnedSlabs& pinned_slabs() {
-    static PinnedSlabs s;
+    thread_local PinnedSlabs s;  // per calling thread, like its engine
     return s;
 }
 
