@@ -455,8 +455,8 @@ def main():
                       else int(os.environ.get("LOCAL_WORLD_SIZE", "1")) <= 1)
         host_threads = int(os.environ.get("CSAIDX_HOST_THREADS", 0)) or max(
             1, len(os.sched_getaffinity(0)) // int(os.environ.get("LOCAL_WORLD_SIZE", "1")) - 1)
-        h2d = B * rows * H * D * (2 if host_round else 4) + B * T * D * 4 + B * rows * H * 4
-        d2h = B * rows * k * 12
+        # bytes the last call moved (counted by the library)
+        h2d, d2h, fp32_chunks, n_chunks = api.last_transfer()
         e2e = {"value": (pairs_mine if args.simulate_rank else pairs_total) / (e2e_ms / 1000.0),
                "unit": "legal pairs/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -466,7 +466,8 @@ def main():
                          "and D2H of chunk c-1 overlap chunk c's kernels" if host_round else
                          "PCIe: the fp32 q rows (the reference API's input type) cross the bus once; H2D of "
                          "chunk c+1 and D2H of chunk c-1 overlap chunk c's kernels"),
-               "host_rounding": {"on": host_round, "threads": host_threads if host_round else 0},
+               "host_rounding": {"on": host_round, "threads": host_threads if host_round else 0,
+                                 "chunks_sent_fp32": fp32_chunks, "chunks": n_chunks},
                "path": "csaidx_host_run_chunked_local (libcsaidx.so C entry of csaidx::run_chunked over this "
                        "rank's rows), pinned fp32 host operands, host rounding + H2D/D2H inside the timed region"}
         # cheap end-to-end correctness guard: the host API must agree with the resident run

@@ -146,6 +146,11 @@ int64_t csaidx_host_k_eff(int64_t t, int64_t ratio, int64_t top_k);
  * types.cpp:73-92, and of strict mode). */
 int csaidx_host_round_bf16(const float* src, uint16_t* dst, uint64_t n, int* nonfinite, int* inexact);
 
+/* Host <-> device bytes the calling thread's last host-buffer chunked call
+ * moved (inputs in, index / value rows out) and how many of its query chunks
+ * crossed PCIe as fp32 rather than host-rounded bf16. */
+int csaidx_host_last_transfer(uint64_t* h2d_bytes, uint64_t* d2h_bytes, int64_t* fp32_chunks, int64_t* chunks);
+
 /* ------------------------------------------------------------ multi-GPU
  * The query-sharded driver (csaidx::gpu::MultiRank, include/csaidx/gpu.hpp):
  * one process per GPU over a csaidx_collectives transport (NCCL:

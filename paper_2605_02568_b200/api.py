@@ -115,6 +115,7 @@ HOST_SYMBOLS = {
     "csaidx_host_t_legal": (c_int64, [c_int64, c_int64]),
     "csaidx_host_k_eff": (c_int64, [c_int64, c_int64, c_int64]),
     "csaidx_host_round_bf16": (c_int, [c_void_p, c_void_p, c_uint64, POINTER(c_int), POINTER(c_int)]),
+    "csaidx_host_last_transfer": (c_int, [POINTER(c_uint64), POINTER(c_uint64), POINTER(c_int64), POINTER(c_int64)]),
 }
 
 _host = None
@@ -548,3 +549,11 @@ def choose_path(dims: ProblemDims, threshold_bytes: int):
     _check(host_lib().csaidx_host_choose_path(ctypes.byref(cd), threshold_bytes, ctypes.byref(path),
                                               ctypes.byref(pred)))
     return ExecutionPath(path.value), pred.value
+
+
+def last_transfer():
+    """(h2d bytes, d2h bytes, chunks sent as fp32, chunks) of this thread's
+    last host-buffer chunked call (csaidx_host_last_transfer)."""
+    h, d, r, n = c_uint64(), c_uint64(), c_int64(), c_int64()
+    _check(host_lib().csaidx_host_last_transfer(ctypes.byref(h), ctypes.byref(d), ctypes.byref(r), ctypes.byref(n)))
+    return h.value, d.value, r.value, n.value

@@ -347,6 +347,16 @@ int csaidx_host_round_bf16(const float* src, uint16_t* dst, uint64_t n, int* non
     });
 }
 
+int csaidx_host_last_transfer(uint64_t* h2d_bytes, uint64_t* d2h_bytes, int64_t* fp32_chunks, int64_t* chunks) {
+    return guarded([&] {
+        const csaidx::detail::Transfer& t = csaidx::detail::last_transfer();
+        if (h2d_bytes != nullptr) *h2d_bytes = t.h2d;
+        if (d2h_bytes != nullptr) *d2h_bytes = t.d2h;
+        if (fp32_chunks != nullptr) *fp32_chunks = t.fp32_chunks;
+        if (chunks != nullptr) *chunks = t.chunks;
+    });
+}
+
 int csaidx_host_plan_shards(const csaidx_dims* dims, int64_t query_tile, int world, int rank, int64_t* starts,
                             int64_t cap, int64_t* n_chunks, uint64_t* loads) {
     return guarded([&] {

@@ -156,4 +156,13 @@ TopKResult run_materialize_view(const HostView& in, const ProblemDims& dims, Acc
 
 void validate_dims(const ProblemDims& d);
 
+// Host <-> device bytes of the calling thread's last host-buffer chunked
+// call, and how many of its chunks crossed PCIe as fp32 (all of them unless
+// q was rounded to bf16 on the host).
+struct Transfer {
+    uint64_t h2d = 0, d2h = 0;
+    int64_t fp32_chunks = 0, chunks = 0;
+};
+Transfer& last_transfer();
+
 }  // namespace csaidx::detail

@@ -366,6 +366,11 @@ double now_ms() {
 
 }  // namespace
 
+Transfer& last_transfer() {
+    thread_local Transfer t;
+    return t;
+}
+
 namespace {
 
 // The operands are not bf16-representable: ScoreKernel::auto_detect then
@@ -609,6 +614,15 @@ void run_chunked_rows_impl(const HostView& in, const ProblemDims& dims, const Dr
         int seen = 0;
         check(csaidx_engine_take_inexact(e, &seen));
         if (seen) throw OperandsNotBf16();
+    }
+    // bytes this call moved over PCIe (csaidx_host_last_transfer)
+    {
+        const uint64_t qe = static_cast<uint64_t>(B * need) * static_cast<uint64_t>(qrow);
+        const uint64_t q_bytes = qe * (dtype == CSAIDX_DTYPE_BF16 && host_round ? 2 : 4);
+        last_transfer() = Transfer{q_bytes + static_cast<uint64_t>(dims.kc_elems()) * esz +
+                                       static_cast<uint64_t>(B * need * dims.heads) * 4,
+                                   static_cast<uint64_t>(B * need * k) * 12, host_round ? 0 : static_cast<int64_t>(plan.order.size()),
+                                   static_cast<int64_t>(plan.order.size())};
     }
     if (stats_out != nullptr) *stats_out = stats;
 }
