@@ -72,9 +72,13 @@ struct Layout {
 };
 
 __host__ __device__ inline int pow2_at_least(int x) {
+#ifdef __CUDA_ARCH__
+    return x <= 1 ? 1 : 1 << (32 - __clz(x - 1));  // one instruction instead of a loop per call
+#else
     int p = 1;
     while (p < x) p <<= 1;
     return p;
+#endif
 }
 
 __host__ __device__ inline Layout layout_for(int k) {
@@ -511,35 +515,43 @@ __device__ void exact_global_select(const float* row, int64_t n, int k, uint64_t
 // finish buckets over [lo_f, hi_f] (threshold, sample max) are counted into
 // hist[0, kFinBins) on the way (prebuilt). count < 0: nothing to do.
 __device__ void gather_candidates(const float* row, const uint32_t* idx_list, int count, uint64_t* cand,
-                                  uint32_t* hist, float lo_f, float hi_f, bool& prebuilt, float& pb_lo,
+                                  uint32_t* hist, float lo_f, uint32_t* max_slot, bool& prebuilt, float& pb_lo,
                                   float& pb_scale, bool build_hist = true) {
     if (build_hist && count >= 0 && count <= kGatherPer * kThreads) {
+        // every survivor's score in registers first: the finish buckets span
+        // [threshold, the survivors' true maximum] (the sample maximum would
+        // leave the scores above it in one clamped top bucket, whose pairwise
+        // ranking is quadratic and which can overflow into the slow path)
         uint32_t cc[kGatherPer];
+        float vv[kGatherPer];
 #pragma unroll
         for (int g = 0; g < kGatherPer; ++g) {
             const int i = gtid() + g * kThreads;
             cc[g] = i < count ? idx_list[i] : 0u;
         }
-        csync();  // the list (it may alias hist) is consumed
+#pragma unroll
+        for (int g = 0; g < kGatherPer; ++g)
+            vv[g] = gtid() + g * kThreads < count ? __ldg(row + cc[g]) : -INFINITY;
+        float vmax = -INFINITY;
+#pragma unroll
+        for (int g = 0; g < kGatherPer; ++g) vmax = fmaxf(vmax, vv[g]);
+        const uint32_t kmax = __reduce_max_sync(0xffffffffu, vmax > -INFINITY ? ord_key(vmax) : 0u);
+        if (gtid() == 0) *max_slot = 0u;
+        csync();  // the list (it may alias hist) is consumed; max_slot reset
         for (int i = gtid(); i < kFinBins; i += kThreads) hist[i] = 0;
+        if ((gtid() & 31) == 0) atomicMax(max_slot, kmax);
+        csync();
+        const float hi_f = ord_key_to_float(*max_slot);
         pb_lo = lo_f;
         pb_scale = static_cast<float>(kFinBins) / (hi_f - lo_f);
         if (!(hi_f > lo_f) || !isfinite(pb_scale)) pb_scale = 0.f;
-        csync();
 #pragma unroll
-        for (int h = 0; h < kGatherPer; h += 8) {
-            float vv[8];
-#pragma unroll
-            for (int g = 0; g < 8; ++g)
-                vv[g] = gtid() + (h + g) * kThreads < count ? __ldg(row + cc[h + g]) : 0.f;
-#pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                const int i = gtid() + (h + g) * kThreads;
-                if (i < count) {
-                    const uint64_t c = composite(ord_key(vv[g]), cc[h + g]);
-                    cand[i] = c;
-                    atomicAdd(&hist[fin_bin(c, pb_lo, pb_scale)], 1u);
-                }
+        for (int g = 0; g < kGatherPer; ++g) {
+            const int i = gtid() + g * kThreads;
+            if (i < count) {
+                const uint64_t c = composite(ord_key(vv[g]), cc[g]);
+                cand[i] = c;
+                atomicAdd(&hist[fin_bin(c, pb_lo, pb_scale)], 1u);
             }
         }
         prebuilt = true;
@@ -834,7 +846,7 @@ __device__ __forceinline__ void select_row(const SelectParams& p, int b, int64_t
                 csync();
                 if (total >= static_cast<uint32_t>(take) && total <= cap2) {
                     count = static_cast<int>(total);
-                    gather_candidates(row, idx2, count, cand, hist, tau_g, gmaxv, prebuilt, pb_lo, pb_scale);
+                    gather_candidates(row, idx2, count, cand, hist, tau_g, res + 5, prebuilt, pb_lo, pb_scale);
                     have = true;
                     if (gtid() == 0 && p.cand_hits != nullptr) atomicAdd(p.cand_hits, 1);
                 }
@@ -1006,7 +1018,7 @@ __device__ __forceinline__ void select_row(const SelectParams& p, int b, int64_t
             csync();
             const uint32_t total = *counter;
             count = (total >= static_cast<uint32_t>(k) && total <= cap) ? static_cast<int>(total) : -1;
-            gather_candidates(row, idx_list, count, cand, hist, tau_f, smax, prebuilt, pb_lo, pb_scale);
+            gather_candidates(row, idx_list, count, cand, hist, tau_f, res + 5, prebuilt, pb_lo, pb_scale);
         }
 
         if (clk) clk[2] = clock64();
