@@ -1186,7 +1186,6 @@ __global__ void __launch_bounds__(kThreads) select_large_kernel(const SelectPara
         if (take == n) {
             for (int64_t i = gtid(); i < n; i += kThreads) buf[i] = composite(ord_key(__ldg(row + i)), i);
         } else {
-            if (gtid() == 0 && p.fallbacks != nullptr) atomicAdd(p.fallbacks, 0);
             exact_global_select(row, n, take, buf, cand, kLargeCand, hist, wtot, res, wsum);
         }
         const int P = pow2_at_least(take);
