@@ -859,7 +859,9 @@ __device__ __forceinline__ void select_row(const SelectParams& p, int b, int64_t
             int nseg = static_cast<int>(n / 2048);
             if (nseg > kSampleSegs) nseg = kSampleSegs;
             if (nseg < 1) nseg = 1;
-            const int64_t seg_stride = (n / nseg) & ~int64_t{3};
+            // 32-bit arithmetic: a row's legal length is < 2^31 (n <= T)
+            const int n32 = static_cast<int>(n);
+            const int64_t seg_stride = (n32 / nseg) & ~3;
             constexpr int kSegsPerWarp = kSampleSegs / kWarps;  // 8
             const int w = gtid() >> 5;
             float4 sv[kSegsPerWarp];
@@ -899,7 +901,7 @@ __device__ __forceinline__ void select_row(const SelectParams& p, int b, int64_t
             // ~2k survivors: a comfortable margin over k (misses -> the slow
             // exact fallback) while the shared list stays at <= 4k entries
             const int target = (2 * k < (L.cand_cap * 3) / 4) ? 2 * k : (L.cand_cap * 3) / 4;
-            int r = static_cast<int>((static_cast<int64_t>(target) * ns) / n);
+            int r = (target * ns) / n32;  // <= 6144 * 8192: no overflow
             if (r < 1) r = 1;
             // The sample's rank-r value by value-linear histograms over
             // [sample min, sample max]: one pass, plus a refinement pass
