@@ -131,7 +131,8 @@ int csaidx_engine_reset_peak(csaidx_engine* e);
 #define CSAIDX_KIND_MERGE 2
 #define CSAIDX_KIND_FINALIZE 3
 #define CSAIDX_KIND_PREP 4
-#define CSAIDX_NUM_KINDS 5
+#define CSAIDX_KIND_ATTENTION 5
+#define CSAIDX_NUM_KINDS 6
 int csaidx_engine_set_profiling(csaidx_engine* e, int enabled);
 int csaidx_engine_kernel_stats(csaidx_engine* e, int kind, int64_t* launches, double* total_ms);
 int csaidx_engine_reset_stats(csaidx_engine* e);
@@ -216,6 +217,24 @@ int csaidx_cuda_select(csaidx_engine* e, const float* scores, int64_t batch, int
                        int64_t ld, int64_t cols, int64_t s0, int64_t t0, int64_t ratio,
                        int apply_mask, int64_t k, float* cand_val, int32_t* cand_idx,
                        int64_t cand_ld);
+/* Sparse attention over the indexer's top-k (the CSA step
+ * that consumes TopK(t), outside the reference's scope,
+ * SPEC.md:8). For every (b, t) and head h:
+ *   out[b,t,h,:dv] = sum_j softmax_j(sm_scale * q[b,t,h,:] . kv[b,i_j,:]) kv[b,i_j,:dv]
+ *   lse[b,t,h]     = log sum_j exp(sm_scale * q[b,t,h,:] . kv[b,i_j,:])
+ * over the entries i_j of indices[b,t,0:k] with 0 <= i_j < kv_len (others,
+ * e.g. the -1 padding, are skipped; a row with none gets out = 0 and
+ * lse = -inf). One shared latent KV head (MQA, the sparse-MLA layout):
+ * q bf16 [B, S, heads, dqk], kv bf16 [B, kv_len, dqk], indices int32
+ * [B, S, idx_ld], out bf16 [B, S, heads, dv] (rows of out_ld >= dv), lse
+ * fp32 [B, S, heads] or NULL. Compiled shape: heads = 128, dqk = 576,
+ * dv = 512 (else CSAIDX_INVALID_ARGUMENT). tcgen05 kernel, two CTAs per
+ * query (one per half of dv). */
+int csaidx_cuda_sparse_attention(csaidx_engine* e, const void* q_bf16, const void* kv_bf16,
+                                 const int32_t* indices, int64_t batch, int64_t seq_len,
+                                 int64_t kv_len, int64_t heads, int64_t dqk, int64_t dv, int64_t k,
+                                 int64_t idx_ld, float sm_scale, void* out_bf16, int64_t out_ld,
+                                 float* lse);
 /* Largest take of the shared-memory select (4096). */
 int csaidx_cuda_select_capacity(void);
 /* 1 when the persistent multi-row select (csaidx_engine_set_partition) fits

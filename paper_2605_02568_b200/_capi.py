@@ -8,7 +8,7 @@ from __future__ import annotations
 
 import ctypes
 import os
-from ctypes import POINTER, c_char_p, c_double, c_int, c_int64, c_size_t, c_uint64, c_void_p
+from ctypes import POINTER, c_char_p, c_double, c_float, c_int, c_int64, c_size_t, c_uint64, c_void_p
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
 CUDA_LIB = os.path.join(LIB_DIR, "libcsaidx_cuda.so")
@@ -18,7 +18,7 @@ OK, INVALID_ARGUMENT, RUNTIME_ERROR, OVERFLOW_ERROR, LOGIC_ERROR, CUDA_ERROR = r
 KERNEL_AUTO, KERNEL_EXACT = 0, 1
 DTYPE_BF16, DTYPE_F32 = 0, 1
 MODE_FP32, MODE_FP16_EMULATED = 0, 1
-KIND_SCORE, KIND_SELECT, KIND_MERGE, KIND_FINALIZE, KIND_PREP = range(5)
+KIND_SCORE, KIND_SELECT, KIND_MERGE, KIND_FINALIZE, KIND_PREP, KIND_ATTENTION = range(6)
 
 
 class CsaidxError(RuntimeError):
@@ -167,6 +167,11 @@ CUDA_SYMBOLS = {
         [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_int64, c_int64, c_int, c_int],
     ),
     "csaidx_cuda_fill_sentinel": (c_int, [c_void_p, c_void_p, c_void_p, c_int64]),
+    "csaidx_cuda_sparse_attention": (
+        c_int,
+        [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64,
+         c_int64, c_float, c_void_p, c_int64, c_void_p],
+    ),
     "csaidx_cuda_finalize": (
         c_int,
         [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_int, c_void_p, c_void_p,

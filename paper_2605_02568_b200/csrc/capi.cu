@@ -980,6 +980,47 @@ int csaidx_cuda_merge(csaidx_engine* e, float* run_val, int32_t* run_idx, int64_
     return CSAIDX_OK;
 }
 
+int csaidx_cuda_sparse_attention(csaidx_engine* e, const void* q_bf16, const void* kv_bf16, const int32_t* indices,
+                                 int64_t batch, int64_t seq_len, int64_t kv_len, int64_t heads, int64_t dqk,
+                                 int64_t dv, int64_t k, int64_t idx_ld, float sm_scale, void* out_bf16,
+                                 int64_t out_ld, float* lse) {
+    if (int rc = set_device(e)) return rc;
+    if (heads != 128 || dqk != 576 || dv != 512)
+        return fail(CSAIDX_INVALID_ARGUMENT, "sparse_attention: compiled for heads = 128, dqk = 576, dv = 512");
+    if (batch < 1 || seq_len < 0 || kv_len < 1 || k < 1 || k > 4096 || idx_ld < k || out_ld < dv || (out_ld % 8) != 0)
+        return fail(CSAIDX_INVALID_ARGUMENT,
+                    "sparse_attention: bad extents (1 <= k <= 4096, idx_ld >= k, out_ld >= dv, out_ld %% 8 == 0)");
+    if (q_bf16 == nullptr || kv_bf16 == nullptr || indices == nullptr || out_bf16 == nullptr)
+        return fail(CSAIDX_INVALID_ARGUMENT, "sparse_attention: null operand");
+    if (batch * kv_len > (int64_t{1} << 31) - 1 || batch * seq_len * heads > (int64_t{1} << 31) - 1 ||
+        2 * seq_len > (int64_t{1} << 31) - 1 || batch > 65535)
+        return fail(CSAIDX_INVALID_ARGUMENT, "sparse_attention: extents exceed the 32-bit TMA coordinates");
+    if ((reinterpret_cast<uintptr_t>(q_bf16) & 15) != 0 || (reinterpret_cast<uintptr_t>(kv_bf16) & 15) != 0 ||
+        (reinterpret_cast<uintptr_t>(out_bf16) & 15) != 0)
+        return fail(CSAIDX_INVALID_ARGUMENT, "sparse_attention: operands must be 16-byte aligned");
+    if (seq_len == 0) return CSAIDX_OK;
+    CUtensorMap qmap;
+    // q as [B*S*heads, dqk] rows (box 64 x 128: one panel of a query's heads)
+    if (int rc = make_map(&qmap, q_bf16, static_cast<uint64_t>(batch * seq_len * heads), static_cast<uint64_t>(dqk), 128))
+        return rc;
+    SparseMlaParams p{};
+    p.q = static_cast<const __nv_bfloat16*>(q_bf16);
+    p.kv = static_cast<const __nv_bfloat16*>(kv_bf16);
+    p.indices = indices;
+    p.idx_ld = idx_ld;
+    p.out = static_cast<__nv_bfloat16*>(out_bf16);
+    p.out_ld = out_ld;
+    p.lse = lse;
+    p.seq_len = seq_len;
+    p.kv_len = kv_len;
+    p.batch = static_cast<int>(batch);
+    p.k = static_cast<int>(k);
+    p.sm_scale = sm_scale;
+    LaunchScope ls(e, CSAIDX_KIND_ATTENTION);
+    CSAIDX_CUDA_TRY(csaidx_kern::launch_sparse_mla(qmap, p, e->stream), "sparse_attention");
+    return CSAIDX_OK;
+}
+
 int csaidx_cuda_fill_sentinel(csaidx_engine* e, float* val, int32_t* idx, int64_t n) {
     if (int rc = set_device(e)) return rc;
     LaunchScope ls(e, CSAIDX_KIND_PREP);

@@ -1,0 +1,420 @@
+// Sparse attention over the indexer's top-k (the CSA step
+// after the indexer: "a sparse attention kernel reads only
+// TopK(t) ... for each query"; PAPER.md:360-375 composes the chunked indexer
+// with TileLang's sparse MLA kernel). The reference stops at the index list
+// (SPEC.md:8 puts the attention step out of its scope), so the operator here
+// follows the sparse-MLA definition that kernel family implements:
+//
+//   out[b,t,h,:] = sum_j softmax_j(sm_scale * q[b,t,h,:] . kv[b,i_j,:]) * kv[b,i_j,:Dv]
+//   lse[b,t,h]   = log sum_j exp(sm_scale * q[b,t,h,:] . kv[b,i_j,:])
+//
+// over the valid entries i_j of indices[b,t,:] (0 <= i_j < T; -1 = padding),
+// with one shared latent KV head (MQA): kv rows of Dqk = 576 (the first
+// Dv = 512 are also the values), H = 128 query heads, bf16 in / fp32
+// accumulate / bf16 out.
+//
+// B200 design (one CTA per (query, half of Dv), 1 CTA per SM by shared memory):
+//  * heads are the UMMA M dimension (128 TMEM lanes), so every softmax
+//    statistic of a head lives in one thread;
+//  * the QK^T product has few keys per block (N = 32), so with both operands
+//    in shared memory every MMA would re-read the 4 KiB Q slice for 1 KiB of
+//    keys (shared-memory bound at ~40% of the MMA rate; the first version,
+//    N = 16 from shared memory, ran at 0.22 of peak). Q therefore lives in
+//    TMEM as the A operand (tcgen05.mma ... [a_tmem]) for its first 384 dims
+//    (192 columns of packed bf16 pairs); the last 192 dims stay in shared
+//    memory (3 SW128 panels, TMA) because TMEM also holds O and S;
+//  * the selected KV rows are gathered 32 per block by 128 producer threads
+//    with cp.async (16-byte pieces written straight into the SW128 K-major
+//    layout; completion tracked by the stage's mbarrier), 4 stages deep
+//    (TMA tile::gather4 — 4 rows x 128 B per instruction — was measured
+//    first: the 72 instructions per stage made the TMA unit the bottleneck);
+//  * S = Q K^T (M=128, N=32, K=576) into TMEM; the softmax warps read S
+//    (tcgen05.ld), keep the running max / sum in registers (exp2 domain,
+//    lazy rescale: O is only rescaled when the max grows by more than 2^8),
+//    and write P as packed bf16 over the S columns they just read
+//    (tcgen05.st) — P is the A operand of O += P V (A from TMEM, M=128,
+//    N=256, K=32), whose B operand is the same gathered KV tile read MN-major
+//    (no transpose copy);
+//  * O [128 x 256] fp32 stays in TMEM for the whole query; the two CTAs of a
+//    query each own half of Dv and both compute S (the QK product is
+//    duplicated: 65% of the issued MMA work is useful at Dqk = 576, Dv = 512).
+//    TMEM: Q 192 + O 256 + S/P 2 x 32 = 512 columns.
+// Warp roles: 0-3 softmax + epilogue (TMEM lane quarters; they also stage Q
+// into TMEM), 4-7 producers (Q tail by TMA, KV rows by cp.async), 8 TMEM
+// owner + MMA issuer.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.h"
+#include "sm100_ptx.cuh"
+
+using namespace csaidx_dev;
+
+namespace {
+
+constexpr int kH = 128;                    // query heads = UMMA M
+constexpr int kDqk = 576;
+constexpr int kDvHalf = 256;               // Dv columns per CTA = UMMA N of PV
+constexpr int kPanels = kDqk / 64;         // 9 SW128 panels of 64 bf16
+constexpr int kQTmemSteps = 24;            // K steps of 16 whose Q slice is in TMEM (dims 0..383)
+constexpr int kQSmemPanels = kPanels - kQTmemSteps / 4;  // 3 panels in shared memory (dims 384..575)
+constexpr int kBlk = 32;                   // keys per block = UMMA N of QK, K of PV
+constexpr int kStages = 4;
+constexpr int kQPanelBytes = kH * 128;                 // 16 KiB
+constexpr int kQBytes = kQSmemPanels * kQPanelBytes;   // 48 KiB
+constexpr int kKvPanelBytes = kBlk * 128;              // 4 KiB
+constexpr int kKvStageBytes = kPanels * kKvPanelBytes; // 36 KiB
+constexpr int kKvOffset = kQBytes;
+constexpr int kMaxK = 4096;                            // indices staged in shared memory
+constexpr int kIdxOffset = kKvOffset + kStages * kKvStageBytes;
+constexpr int kBarOffset = kIdxOffset + kMaxK * 4;
+constexpr int kSmemBytes = kBarOffset + 256 + 1024;    // barriers + align slack
+constexpr int kThreads = 288;              // 4 softmax + 4 producer + 1 MMA warps
+constexpr int kProducers = 128;
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kColQ = 0, kColO = 192, kColS = 448;  // S (and P over it): 2 x 32 columns
+constexpr float kRescaleLog2 = 8.0f;       // lazy rescale threshold (factor 256)
+
+// D[tmem] (+)= A[tmem] * B[smem desc] (A = P, packed bf16 pairs per column).
+__device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+    const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+        "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+        "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// MN-major SW128 descriptor (B of O += P V): the gathered tile read with Dv
+// as N: 64-element rows of 128 B, 8-row (key) atoms of 1 KiB (SBO), the
+// next 64 Dv columns one panel further (LBO).
+__device__ __forceinline__ uint64_t sw128_mnmajor_desc(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+    d |= static_cast<uint64_t>(1u) << 46;
+    d |= static_cast<uint64_t>(2u) << 61;
+    return d;
+}
+
+constexpr uint32_t kIdescQK = idesc_bf16_f32(kH, kBlk);
+constexpr uint32_t kIdescPV = idesc_bf16_f32(kH, kDvHalf) | (1u << 16);  // B MN-major
+
+__global__ void __launch_bounds__(kThreads, 1)
+    sparse_mla_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ SparseMlaParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* q_smem = smem;
+    uint8_t* kv_smem = smem + kKvOffset;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOffset);
+    uint64_t* q_full = bars;                    // [1]
+    uint64_t* kv_full = q_full + 1;             // [kStages]
+    uint64_t* kv_empty = kv_full + kStages;     // [kStages]
+    uint64_t* s_full = kv_empty + kStages;      // [2]
+    uint64_t* p_full = s_full + 2;              // [2]
+    uint64_t* q_tmem = p_full + 2;              // [1] Q slice staged into TMEM
+    uint32_t* valid_w = reinterpret_cast<uint32_t*>(q_tmem + 1);  // [kStages]
+    uint32_t* tmem_slot = valid_w + kStages;
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    const int half = blockIdx.x & 1;
+    const int64_t tq = blockIdx.x >> 1;  // query within the batch
+    const int b = blockIdx.y;
+    const int nb = (p.k + kBlk - 1) / kBlk;
+
+    if (threadIdx.x == 0) {
+        mbar_init(q_full, 1);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&kv_full[s], kProducers);  // one cp.async arrive per producer thread
+            mbar_init(&kv_empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&s_full[s], 1);
+            mbar_init(&p_full[s], 4);  // one arrive per softmax warp
+        }
+        mbar_init(q_tmem, 4);  // one arrive per softmax warp
+        fence_barrier_init();
+    }
+    if (warp == 8) tmem_alloc<kTmemCols>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp >= 4 && warp < 8) {
+        // ---------------------------------------------------------- producers
+        const int pt = threadIdx.x - 128;  // 0..127
+        const int32_t* idx_row = p.indices + (static_cast<int64_t>(b) * p.seq_len + tq) * p.idx_ld;
+        if (pt == 0) {
+            tma_prefetch(&qmap);
+            mbar_expect_tx(q_full, kQBytes);
+            const int32_t qrow = static_cast<int32_t>((static_cast<int64_t>(b) * p.seq_len + tq) * kH);
+            for (int pn = 0; pn < kQSmemPanels; ++pn)
+                tma_load_2d(q_smem + pn * kQPanelBytes, &qmap, q_full, (kQTmemSteps / 4 + pn) * 64, qrow);
+        }
+        // the query's k indices -> shared memory once (row of the gather; -1 for padding)
+        int32_t* idx_s = reinterpret_cast<int32_t*>(smem + kIdxOffset);
+        for (int i = pt; i < nb * kBlk; i += kProducers) {
+            const int32_t idx = i < p.k ? __ldg(idx_row + i) : -1;
+            idx_s[i] = (idx >= 0 && idx < p.kv_len) ? idx : -1;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kProducers) : "memory");
+        // this thread's 18 pieces of every block: row r, 16-byte column cc of 72
+        // (the same for every block: only the gathered row changes)
+        constexpr int kPieces = (kBlk * kPanels * 8) / kProducers;
+        uint32_t soff[kPieces];
+        int srow[kPieces];
+#pragma unroll
+        for (int u = 0; u < kPieces; ++u) {
+            const int c = pt + u * kProducers;
+            const int r = c / (kPanels * 8);
+            const int cc = c - r * (kPanels * 8);
+            srow[u] = r | (cc << 8);
+            soff[u] = (cc >> 3) * kKvPanelBytes + r * 128 + (((cc & 7) ^ (r & 7)) << 4);
+        }
+        const char* kv_b = reinterpret_cast<const char*>(p.kv) + static_cast<int64_t>(b) * p.kv_len * (kDqk * 2);
+        for (int j = 0; j < nb; ++j) {
+            const int s = j % kStages;
+            const int32_t idx = idx_s[j * kBlk + lane];  // one index per lane
+            const uint32_t vmask = __ballot_sync(0xffffffffu, idx >= 0);
+            const int32_t krow = idx >= 0 ? idx : 0;  // padding reads row 0 (finite), masked in the softmax
+            mbar_wait(&kv_empty[s], ((j / kStages) & 1) ^ 1);
+            if (pt == 0) valid_w[s] = vmask;
+            const uint32_t st = smem_u32(kv_smem + s * kKvStageBytes);
+#pragma unroll
+            for (int u = 0; u < kPieces; ++u) {
+                const int32_t row = __shfl_sync(0xffffffffu, krow, srow[u] & 255);
+                const char* src = kv_b + static_cast<int64_t>(row) * (kDqk * 2) + (srow[u] >> 8) * 16;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st + soff[u]), "l"(src) : "memory");
+            }
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&kv_full[s])) : "memory");
+        }
+    } else if (warp == 8) {
+        // ---------------------------------------------------------- MMA issuer
+        if (elect_one()) {
+            const uint32_t q_base = smem_u32(q_smem);
+            const uint32_t kv_base = smem_u32(kv_smem);
+            mbar_wait(q_full, 0);
+            mbar_wait(q_tmem, 0);
+            tc_fence_after();
+            auto issue_pv = [&](int j) {
+                const int s = j % kStages;
+                mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+                tc_fence_after();
+                const uint32_t vb = kv_base + s * kKvStageBytes + (half * 4) * kKvPanelBytes;
+#pragma unroll
+                for (int kk = 0; kk < kBlk / 16; ++kk)  // 16 keys per K step: 8 columns of P, 2 KiB of rows
+                    umma_bf16_ts(tmem + kColO, tmem + kColS + (j & 1) * kBlk + kk * 8,
+                                 sw128_mnmajor_desc(vb + kk * 2048, kKvPanelBytes, 1024), kIdescPV,
+                                 (j > 0 || kk > 0) ? 1u : 0u);
+                umma_commit(&kv_empty[s]);  // stage free and O holds PV of block j
+            };
+            for (int j = 0; j < nb; ++j) {
+                const int s = j % kStages;
+                mbar_wait(&kv_full[s], (j / kStages) & 1);
+                fence_proxy_async();  // cp.async (generic proxy) writes -> the tensor core's reads
+                tc_fence_after();
+                const uint32_t st = kv_base + s * kKvStageBytes;
+                const uint32_t d = tmem + kColS + (j & 1) * kBlk;
+#pragma unroll
+                for (int kk = 0; kk < kQTmemSteps; ++kk)  // Q slice from TMEM: 8 columns per 16 dims
+                    umma_bf16_ts(d, tmem + kColQ + kk * 8,
+                                 sw128_kmajor_desc(st + (kk >> 2) * kKvPanelBytes + (kk & 3) * 32), kIdescQK,
+                                 kk > 0 ? 1u : 0u);
+#pragma unroll
+                for (int kk = kQTmemSteps; kk < kDqk / 16; ++kk) {  // Q tail from shared memory
+                    const uint32_t qa = q_base + ((kk - kQTmemSteps) >> 2) * kQPanelBytes + (kk & 3) * 32;
+                    const uint32_t kb = st + (kk >> 2) * kKvPanelBytes + (kk & 3) * 32;
+                    umma_bf16(d, sw128_kmajor_desc(qa), sw128_kmajor_desc(kb), kIdescQK, 1u);
+                }
+                umma_commit(&s_full[j & 1]);
+                if (j > 0) issue_pv(j - 1);
+            }
+            if (nb > 0) issue_pv(nb - 1);
+        }
+    } else {
+        // ---------------------------------------------------------- softmax + epilogue
+        const int row = warp * 32 + lane;  // head
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+        const float scale_log2 = p.sm_scale * 1.4426950408889634f;
+        const float ninf = -INFINITY;
+        {
+            // this head's Q[0:384] -> TMEM lane `row`, columns 0..191 (bf16
+            // pairs); 16 loads of 16 B in flight per batch
+            const uint4* qsrc = reinterpret_cast<const uint4*>(
+                p.q + ((static_cast<int64_t>(b) * p.seq_len + tq) * kH + row) * kDqk);
+#pragma unroll 1
+            for (int c0 = 0; c0 < kQTmemSteps * 8; c0 += 64) {
+                uint32_t w[64];
+                uint4* w4 = reinterpret_cast<uint4*>(w);
+#pragma unroll
+                for (int v = 0; v < 16; ++v) w4[v] = __ldg(qsrc + c0 / 4 + v);
+                tmem_st16(lane_base + kColQ + c0, *reinterpret_cast<uint32_t(*)[16]>(w));
+                tmem_st16(lane_base + kColQ + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(w + 16));
+                tmem_st16(lane_base + kColQ + c0 + 32, *reinterpret_cast<uint32_t(*)[16]>(w + 32));
+                tmem_st16(lane_base + kColQ + c0 + 48, *reinterpret_cast<uint32_t(*)[16]>(w + 48));
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(q_tmem);
+        }
+        float m = ninf, l = 0.f;
+        for (int j = 0; j < nb; ++j) {
+            const int s = j % kStages;
+            mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+            mbar_wait(&kv_full[s], (j / kStages) & 1);  // completed: orders the valid word
+            tc_fence_after();
+            float x[kBlk];
+            tmem_ld32(lane_base + kColS + (j & 1) * kBlk, x);
+            const uint32_t vm = valid_w[s];
+            tmem_ld_wait();
+            float mx = ninf;
+#pragma unroll
+            for (int c = 0; c < kBlk; ++c) {
+                x[c] = ((vm >> c) & 1u) ? x[c] * scale_log2 : ninf;
+                mx = fmaxf(mx, x[c]);
+            }
+            float alpha = 1.f;
+            bool rescale = false;
+            if (mx > m) {
+                if (m == ninf) {
+                    m = mx;  // O is unwritten (j == 0) or all zero: nothing to rescale
+                } else if (mx > m + kRescaleLog2) {
+                    alpha = ex2(m - mx);
+                    l *= alpha;
+                    m = mx;
+                    rescale = true;
+                }
+            }
+                        if (__any_sync(0xffffffffu, rescale)) {
+                // PV of block j-1 has landed in O. Its commit is kv_empty of
+                // block j-1's stage; that barrier's previous phase (PV of block
+                // j-5) completed before block j-1 was loaded and its next one
+                // (PV of block j+3) needs this warp's P of block j+3, so a
+                // parity wait here is exact even though this warp skips the
+                // blocks without a rescale. (tcgen05.commit completions are
+                // not ordered across barriers: a single o_done barrier waited
+                // only on rescaling blocks returned early and corrupted O.)
+                mbar_wait(&kv_empty[(j - 1) % kStages], ((j - 1) / kStages) & 1);
+                tc_fence_after();
+#pragma unroll 1
+                for (int c0 = 0; c0 < kDvHalf; c0 += 32) {
+                    float o[32];
+                    tmem_ld32(lane_base + kColO + c0, o);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) o[c] *= alpha;
+                    tmem_st32(lane_base + kColO + c0, o);
+                }
+                tmem_st_wait();
+            }
+            uint32_t pk[kBlk / 2];
+            float sum = 0.f;
+#pragma unroll
+            for (int c = 0; c < kBlk; c += 2) {
+                const float p0 = m == ninf ? 0.f : ex2(x[c] - m);
+                const float p1 = m == ninf ? 0.f : ex2(x[c + 1] - m);
+                sum += p0 + p1;
+                const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                pk[c / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+            }
+            l += sum;
+            tmem_st16(lane_base + kColS + (j & 1) * kBlk, pk);  // P over the S columns just read
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[j & 1]);
+        }
+        // epilogue: O / l -> bf16 rows of this head, lse (half 0)
+        if (nb > 0) mbar_wait(&kv_empty[(nb - 1) % kStages], ((nb - 1) / kStages) & 1);  // last PV landed
+        tc_fence_after();
+        const float inv_l = l > 0.f ? 1.f / l : 0.f;
+        __nv_bfloat16* orow =
+            p.out + ((static_cast<int64_t>(b) * p.seq_len + tq) * kH + row) * p.out_ld + half * kDvHalf;
+#pragma unroll 1
+        for (int c0 = 0; c0 < kDvHalf; c0 += 32) {
+            float o[32];
+            tmem_ld32(lane_base + kColO + c0, o);
+            tmem_ld_wait();
+            uint4 pk[4];
+            uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+            for (int c = 0; c < 32; c += 2) {
+                const __nv_bfloat162 h2 = __floats2bfloat162_rn(o[c] * inv_l, o[c + 1] * inv_l);
+                pw[c / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+            }
+            uint4* dst = reinterpret_cast<uint4*>(orow + c0);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) dst[v] = pk[v];
+        }
+        if (half == 0 && p.lse != nullptr)
+            p.lse[(static_cast<int64_t>(b) * p.seq_len + tq) * kH + row] =
+                l > 0.f ? (m + log2f(l)) * 0.6931471805599453f : ninf;
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 8) {
+        tc_fence_after();
+        tmem_dealloc<kTmemCols>(tmem);
+    }
+}
+
+}  // namespace
+
+namespace csaidx_kern {
+
+int sparse_mla_smem_bytes() { return kSmemBytes; }
+
+cudaError_t launch_sparse_mla(const CUtensorMap& qmap, const SparseMlaParams& p,
+                              cudaStream_t stream) {
+    if (p.seq_len <= 0 || p.batch <= 0) return cudaSuccess;
+    static bool attr_set[kMaxDevices] = {};
+    const int dev = attr_device();
+    if (!attr_set[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(sparse_mla_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        if (e != cudaSuccess) return e;
+        attr_set[dev] = true;
+    }
+    const dim3 grid(static_cast<unsigned>(2 * p.seq_len), static_cast<unsigned>(p.batch));
+    sparse_mla_kernel<<<grid, kThreads, kSmemBytes, stream>>>(qmap, p);
+    return cudaGetLastError();
+}
+
+}  // namespace csaidx_kern

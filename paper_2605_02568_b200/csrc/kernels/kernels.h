@@ -173,6 +173,25 @@ struct FinalizeParams {
     int64_t sink_seq;       // (out_idx / out_val null: the sink is the only output)
 };
 
+// ------------------------------------------------------------------ sparse attention (f4)
+// out[b,t,h,:Dv] = softmax over the valid indices[b,t,:] of
+// sm_scale * q[b,t,h,:] . kv[b,i,:], applied to kv[b,i,:Dv]; H = 128,
+// Dqk = 576, Dv = 512 (one shared latent KV head). q is read through a TMA
+// map built by the C-ABI entry, the gathered kv rows by cp.async.
+struct SparseMlaParams {
+    const __nv_bfloat16* q;  // [B, S, 128, 576]
+    const __nv_bfloat16* kv; // [B, kv_len, 576]
+    const int32_t* indices;  // [B, S, idx_ld], -1 = padding
+    int64_t idx_ld;
+    __nv_bfloat16* out;      // [B, S, 128, out_ld]
+    int64_t out_ld;
+    float* lse;              // optional [B, S, 128]
+    int64_t seq_len, kv_len;
+    int batch;
+    int k;
+    float sm_scale;
+};
+
 // ------------------------------------------------------------------ prep
 struct ConvertParams {
     const float* src;
@@ -205,6 +224,8 @@ int select_max_take();
 int select_cand_capacity(int k);  // candidate-list length the select kernel accepts for this k
 bool select_fat_fits(int k);      // the persistent multi-row form fits shared memory for this k
 cudaError_t launch_select(const SelectParams& p, cudaStream_t stream);
+int sparse_mla_smem_bytes();
+cudaError_t launch_sparse_mla(const CUtensorMap& qmap, const SparseMlaParams& p, cudaStream_t stream);
 // Scratch the select needs for takes above select_max_take() (rows = B * rows).
 size_t select_large_scratch_bytes(int k, int64_t cols, int64_t rows);
 // Staging scratch the merge needs for k above select_max_take().

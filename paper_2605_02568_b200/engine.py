@@ -180,6 +180,23 @@ class Engine:
                                               _p(out), ld, dims.seq_len, s0, _p(gmax), gmax.shape[-1]))
         return out, gmax
 
+    # ------------------------------------------------ sparse attention (f4)
+    def sparse_attention(self, q, kv, indices, sm_scale, out=None, lse=True):
+        """Sparse MLA-style attention over indices [B, S, k] (int32, -1 = padding):
+        q bf16 [B, S, 128, 576], kv bf16 [B, T, 576] -> out bf16 [B, S, 128, 512]
+        (+ lse fp32 [B, S, 128]); csaidx_cuda_sparse_attention."""
+        B, S, H, Dqk = q.shape
+        T = kv.shape[1]
+        k = indices.shape[-1]
+        dv = 512
+        if out is None:
+            out = torch.empty((B, S, H, dv), dtype=torch.bfloat16, device=q.device)
+        lse_t = torch.empty((B, S, H), dtype=torch.float32, device=q.device) if lse else None
+        check(self.lib.csaidx_cuda_sparse_attention(self.handle, _p(q), _p(kv), _p(indices), B, S, T, H, Dqk, dv, k,
+                                                    indices.stride(1), float(sm_scale), _p(out), out.stride(2),
+                                                    _p(lse_t) if lse_t is not None else None))
+        return out, lse_t
+
     def set_partition(self, score_sms: int, select_sms: int):
         """csaidx_engine_set_partition: score launches on score_sms SMs, selects as
         select_sms persistent multi-row CTAs (0, 0 = the whole GPU)."""
