@@ -39,9 +39,13 @@
 //    query each own half of Dv and both compute S (the QK product is
 //    duplicated: 65% of the issued MMA work is useful at Dqk = 576, Dv = 512).
 //    TMEM: Q 192 + O 256 + S/P 2 x 32 = 512 columns.
-// Warp roles: 0-3 softmax + epilogue (TMEM lane quarters; they also stage Q
-// into TMEM), 4-7 producers (Q tail by TMA, KV rows by cp.async), 8 TMEM
-// owner + MMA issuer.
+// Persistent: one CTA per SM walks (b, query, half) items round-robin and
+// every barrier phase runs on across items, so the next item's Q staging,
+// gathers and first S MMAs overlap the current item's last softmax blocks and
+// epilogue (a CTA per item spent ~15K cycles per item in prologue / epilogue).
+// Warp roles: 0-3 softmax + epilogue (TMEM lane quarters), 4-7 KV producers
+// (cp.async gather), 8 TMEM owner + MMA issuer, 9-12 Q stagers (Q head into
+// TMEM, Q tail by TMA, once the previous item's S MMAs are done).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -71,7 +75,7 @@ constexpr int kMaxK = 4096;                            // indices staged in shar
 constexpr int kIdxOffset = kKvOffset + kStages * kKvStageBytes;
 constexpr int kBarOffset = kIdxOffset + kMaxK * 4;
 constexpr int kSmemBytes = kBarOffset + 256 + 1024;    // barriers + align slack
-constexpr int kThreads = 288;              // 4 softmax + 4 producer + 1 MMA warps
+constexpr int kThreads = 416;              // 4 softmax + 4 KV producer + 1 MMA + 4 Q-staging warps
 constexpr int kProducers = 128;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColQ = 0, kColO = 192, kColS = 448;  // S (and P over it): 2 x 32 columns
@@ -140,22 +144,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* q_smem = smem;
     uint8_t* kv_smem = smem + kKvOffset;
+    int32_t* idx_s = reinterpret_cast<int32_t*>(smem + kIdxOffset);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOffset);
-    uint64_t* q_full = bars;                    // [1]
+    uint64_t* q_full = bars;                    // [1] Q tail in shared memory (TMA), per item
     uint64_t* kv_full = q_full + 1;             // [kStages]
-    uint64_t* kv_empty = kv_full + kStages;     // [kStages]
+    uint64_t* kv_empty = kv_full + kStages;     // [kStages] committed after the block's PV
     uint64_t* s_full = kv_empty + kStages;      // [2]
     uint64_t* p_full = s_full + 2;              // [2]
-    uint64_t* q_tmem = p_full + 2;              // [1] Q slice staged into TMEM
-    uint32_t* valid_w = reinterpret_cast<uint32_t*>(q_tmem + 1);  // [kStages]
+    uint64_t* q_tmem = p_full + 2;              // [1] Q head staged into TMEM, per item
+    uint64_t* q_free = q_tmem + 1;              // [1] every S MMA of the item done (Q reusable)
+    uint64_t* o_free = q_free + 1;              // [1] the epilogue has read O
+    uint32_t* valid_w = reinterpret_cast<uint32_t*>(o_free + 1);  // [kStages]
     uint32_t* tmem_slot = valid_w + kStages;
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
-    const int half = blockIdx.x & 1;
-    const int64_t tq = blockIdx.x >> 1;  // query within the batch
-    const int b = blockIdx.y;
-    const int nb = (p.k + kBlk - 1) / kBlk;
+    const int nb = (p.k + kBlk - 1) / kBlk;  // blocks per item
+    const int64_t nitems = 2 * p.seq_len * p.batch;  // (b, query, half of Dv)
 
     if (threadIdx.x == 0) {
         mbar_init(q_full, 1);
@@ -167,7 +172,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&s_full[s], 1);
             mbar_init(&p_full[s], 4);  // one arrive per softmax warp
         }
-        mbar_init(q_tmem, 4);  // one arrive per softmax warp
+        mbar_init(q_tmem, 4);    // one arrive per Q-staging warp
+        mbar_init(q_free, 1);
+        mbar_init(o_free, 4);    // one arrive per softmax warp
         fence_barrier_init();
     }
     if (warp == 8) tmem_alloc<kTmemCols>(tmem_slot);
@@ -176,108 +183,91 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    // Items are handed out round-robin: item = blockIdx.x + i * gridDim.x,
+    // (b, query, half) = decoded below. Every role walks the same sequence;
+    // barrier phases run on across items (block counter g = i * nb + j).
+    auto decode = [&](int64_t item, int& b, int64_t& tq, int& half) {
+        half = static_cast<int>(item & 1);
+        const int64_t qi = item >> 1;
+        b = static_cast<int>(qi / p.seq_len);
+        tq = qi - static_cast<int64_t>(b) * p.seq_len;
+    };
+
     if (warp >= 4 && warp < 8) {
-        // ---------------------------------------------------------- producers
+        // ---------------------------------------------------------- KV producers
         const int pt = threadIdx.x - 128;  // 0..127
-        const int32_t* idx_row = p.indices + (static_cast<int64_t>(b) * p.seq_len + tq) * p.idx_ld;
-        if (pt == 0) {
-            tma_prefetch(&qmap);
-            mbar_expect_tx(q_full, kQBytes);
-            const int32_t qrow = static_cast<int32_t>((static_cast<int64_t>(b) * p.seq_len + tq) * kH);
-            for (int pn = 0; pn < kQSmemPanels; ++pn)
-                tma_load_2d(q_smem + pn * kQPanelBytes, &qmap, q_full, (kQTmemSteps / 4 + pn) * 64, qrow);
-        }
-        // the query's k indices -> shared memory once (row of the gather; -1 for padding)
-        int32_t* idx_s = reinterpret_cast<int32_t*>(smem + kIdxOffset);
-        for (int i = pt; i < nb * kBlk; i += kProducers) {
-            const int32_t idx = i < p.k ? __ldg(idx_row + i) : -1;
-            idx_s[i] = (idx >= 0 && idx < p.kv_len) ? idx : -1;
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(kProducers) : "memory");
-        // this thread's 18 pieces of every block: row r, 16-byte column cc of 72
-        // (the same for every block: only the gathered row changes)
-        constexpr int kPieces = (kBlk * kPanels * 8) / kProducers;
+        // thread pt copies row r = pt / 4 of every block, 16-byte pieces
+        // cc = pt % 4 + 4u (u < 18): one 64-bit row address per block, the
+        // pieces at immediate offsets; smem offsets are the same every block
+        constexpr int kPieces = (kBlk * kPanels * 8) / kProducers;  // 18
+        static_assert(kProducers == 4 * kBlk, "4 producer threads per gathered row");
+        const int r = pt >> 2;
         uint32_t soff[kPieces];
-        int srow[kPieces];
 #pragma unroll
         for (int u = 0; u < kPieces; ++u) {
-            const int c = pt + u * kProducers;
-            const int r = c / (kPanels * 8);
-            const int cc = c - r * (kPanels * 8);
-            srow[u] = r | (cc << 8);
+            const int cc = (pt & 3) + 4 * u;
             soff[u] = (cc >> 3) * kKvPanelBytes + r * 128 + (((cc & 7) ^ (r & 7)) << 4);
         }
-        const char* kv_b = reinterpret_cast<const char*>(p.kv) + static_cast<int64_t>(b) * p.kv_len * (kDqk * 2);
-        for (int j = 0; j < nb; ++j) {
-            const int s = j % kStages;
-            const int32_t idx = idx_s[j * kBlk + lane];  // one index per lane
-            const uint32_t vmask = __ballot_sync(0xffffffffu, idx >= 0);
-            const int32_t krow = idx >= 0 ? idx : 0;  // padding reads row 0 (finite), masked in the softmax
-            mbar_wait(&kv_empty[s], ((j / kStages) & 1) ^ 1);
-            if (pt == 0) valid_w[s] = vmask;
-            const uint32_t st = smem_u32(kv_smem + s * kKvStageBytes);
-#pragma unroll
-            for (int u = 0; u < kPieces; ++u) {
-                const int32_t row = __shfl_sync(0xffffffffu, krow, srow[u] & 255);
-                const char* src = kv_b + static_cast<int64_t>(row) * (kDqk * 2) + (srow[u] >> 8) * 16;
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st + soff[u]), "l"(src) : "memory");
+        uint32_t g = 0, it = 0;
+        for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x, ++it) {
+            int b, half;
+            int64_t tq;
+            decode(item, b, tq, half);
+            // the item's k indices -> shared memory (row of the gather; -1 for
+            // padding); idx_s is reused once the softmax has read every valid word
+            const int32_t* idx_row = p.indices + (static_cast<int64_t>(b) * p.seq_len + tq) * p.idx_ld;
+            asm volatile("bar.sync 1, %0;" ::"n"(kProducers) : "memory");  // previous item's reads of idx_s done
+            for (int i = pt; i < nb * kBlk; i += kProducers) {
+                const int32_t idx = i < p.k ? __ldg(idx_row + i) : -1;
+                idx_s[i] = (idx >= 0 && idx < p.kv_len) ? idx : -1;
             }
-            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&kv_full[s])) : "memory");
-        }
-    } else if (warp == 8) {
-        // ---------------------------------------------------------- MMA issuer
-        if (elect_one()) {
-            const uint32_t q_base = smem_u32(q_smem);
-            const uint32_t kv_base = smem_u32(kv_smem);
-            mbar_wait(q_full, 0);
-            mbar_wait(q_tmem, 0);
-            tc_fence_after();
-            auto issue_pv = [&](int j) {
-                const int s = j % kStages;
-                mbar_wait(&p_full[j & 1], (j >> 1) & 1);
-                tc_fence_after();
-                const uint32_t vb = kv_base + s * kKvStageBytes + (half * 4) * kKvPanelBytes;
+            asm volatile("bar.sync 1, %0;" ::"n"(kProducers) : "memory");
+            const char* kv_b = reinterpret_cast<const char*>(p.kv) + static_cast<int64_t>(b) * p.kv_len * (kDqk * 2) +
+                               (pt & 3) * 16;
+            for (int j = 0; j < nb; ++j, ++g) {
+                const int s = g % kStages;
+                const int32_t myidx = idx_s[j * kBlk + r];
+                const char* src = kv_b + static_cast<int64_t>(myidx >= 0 ? myidx : 0) * (kDqk * 2);  // padding: row 0
+                uint32_t vmask = 0;
+                if (warp == 4) vmask = __ballot_sync(0xffffffffu, idx_s[j * kBlk + lane] >= 0);
+                mbar_wait(&kv_empty[s], ((g / kStages) & 1) ^ 1);
+                if (pt == 0) valid_w[s] = vmask;
+                const uint32_t st = smem_u32(kv_smem + s * kKvStageBytes);
 #pragma unroll
-                for (int kk = 0; kk < kBlk / 16; ++kk)  // 16 keys per K step: 8 columns of P, 2 KiB of rows
-                    umma_bf16_ts(tmem + kColO, tmem + kColS + (j & 1) * kBlk + kk * 8,
-                                 sw128_mnmajor_desc(vb + kk * 2048, kKvPanelBytes, 1024), kIdescPV,
-                                 (j > 0 || kk > 0) ? 1u : 0u);
-                umma_commit(&kv_empty[s]);  // stage free and O holds PV of block j
-            };
-            for (int j = 0; j < nb; ++j) {
-                const int s = j % kStages;
-                mbar_wait(&kv_full[s], (j / kStages) & 1);
-                fence_proxy_async();  // cp.async (generic proxy) writes -> the tensor core's reads
-                tc_fence_after();
-                const uint32_t st = kv_base + s * kKvStageBytes;
-                const uint32_t d = tmem + kColS + (j & 1) * kBlk;
-#pragma unroll
-                for (int kk = 0; kk < kQTmemSteps; ++kk)  // Q slice from TMEM: 8 columns per 16 dims
-                    umma_bf16_ts(d, tmem + kColQ + kk * 8,
-                                 sw128_kmajor_desc(st + (kk >> 2) * kKvPanelBytes + (kk & 3) * 32), kIdescQK,
-                                 kk > 0 ? 1u : 0u);
-#pragma unroll
-                for (int kk = kQTmemSteps; kk < kDqk / 16; ++kk) {  // Q tail from shared memory
-                    const uint32_t qa = q_base + ((kk - kQTmemSteps) >> 2) * kQPanelBytes + (kk & 3) * 32;
-                    const uint32_t kb = st + (kk >> 2) * kKvPanelBytes + (kk & 3) * 32;
-                    umma_bf16(d, sw128_kmajor_desc(qa), sw128_kmajor_desc(kb), kIdescQK, 1u);
-                }
-                umma_commit(&s_full[j & 1]);
-                if (j > 0) issue_pv(j - 1);
+                for (int u = 0; u < kPieces; ++u)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st + soff[u]), "l"(src + 64 * u)
+                                 : "memory");
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&kv_full[s]))
+                             : "memory");
             }
-            if (nb > 0) issue_pv(nb - 1);
         }
-    } else {
-        // ---------------------------------------------------------- softmax + epilogue
-        const int row = warp * 32 + lane;  // head
-        const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-        const float scale_log2 = p.sm_scale * 1.4426950408889634f;
-        const float ninf = -INFINITY;
-        {
-            // this head's Q[0:384] -> TMEM lane `row`, columns 0..191 (bf16
-            // pairs); 16 loads of 16 B in flight per batch
-            const uint4* qsrc = reinterpret_cast<const uint4*>(
-                p.q + ((static_cast<int64_t>(b) * p.seq_len + tq) * kH + row) * kDqk);
+    } else if (warp >= 9) {
+        // ---------------------------------------------------------- Q stagers
+        // warps 9..12 cover TMEM lane quarters 1,2,3,0; thread = head
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+        uint32_t it = 0;
+        for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x, ++it) {
+            int b, half;
+            int64_t tq;
+            decode(item, b, tq, half);
+            const int64_t qrow = (static_cast<int64_t>(b) * p.seq_len + tq) * kH;
+            const uint4* qsrc = reinterpret_cast<const uint4*>(p.q + (qrow + row) * kDqk);
+            // warm L2 with this head's row while the previous item still owns Q
+#pragma unroll
+            for (int c = 0; c < kDqk * 2; c += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(qsrc) + c));
+            if (it > 0) {
+                mbar_wait(q_free, (it - 1) & 1);  // every S MMA of the previous item has completed
+                tc_fence_after();
+            }
+            if (warp == 9 && lane == 0) {  // Q tail (dims 384..575) by TMA
+                mbar_expect_tx(q_full, kQBytes);
+                for (int pn = 0; pn < kQSmemPanels; ++pn)
+                    tma_load_2d(q_smem + pn * kQPanelBytes, &qmap, q_full, (kQTmemSteps / 4 + pn) * 64,
+                                static_cast<int32_t>(qrow));
+            }
+            // Q head (dims 0..383) -> TMEM lane `row`, columns 0..191 (bf16 pairs)
 #pragma unroll 1
             for (int c0 = 0; c0 < kQTmemSteps * 8; c0 += 64) {
                 uint32_t w[64];
@@ -294,98 +284,165 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(q_tmem);
         }
-        float m = ninf, l = 0.f;
-        for (int j = 0; j < nb; ++j) {
-            const int s = j % kStages;
-            mbar_wait(&s_full[j & 1], (j >> 1) & 1);
-            mbar_wait(&kv_full[s], (j / kStages) & 1);  // completed: orders the valid word
-            tc_fence_after();
-            float x[kBlk];
-            tmem_ld32(lane_base + kColS + (j & 1) * kBlk, x);
-            const uint32_t vm = valid_w[s];
-            tmem_ld_wait();
-            float mx = ninf;
-#pragma unroll
-            for (int c = 0; c < kBlk; ++c) {
-                x[c] = ((vm >> c) & 1u) ? x[c] * scale_log2 : ninf;
-                mx = fmaxf(mx, x[c]);
-            }
-            float alpha = 1.f;
-            bool rescale = false;
-            if (mx > m) {
-                if (m == ninf) {
-                    m = mx;  // O is unwritten (j == 0) or all zero: nothing to rescale
-                } else if (mx > m + kRescaleLog2) {
-                    alpha = ex2(m - mx);
-                    l *= alpha;
-                    m = mx;
-                    rescale = true;
-                }
-            }
-                        if (__any_sync(0xffffffffu, rescale)) {
-                // PV of block j-1 has landed in O. Its commit is kv_empty of
-                // block j-1's stage; that barrier's previous phase (PV of block
-                // j-5) completed before block j-1 was loaded and its next one
-                // (PV of block j+3) needs this warp's P of block j+3, so a
-                // parity wait here is exact even though this warp skips the
-                // blocks without a rescale. (tcgen05.commit completions are
-                // not ordered across barriers: a single o_done barrier waited
-                // only on rescaling blocks returned early and corrupted O.)
-                mbar_wait(&kv_empty[(j - 1) % kStages], ((j - 1) / kStages) & 1);
+    } else if (warp == 8) {
+        // ---------------------------------------------------------- MMA issuer
+        if (elect_one()) {
+            const uint32_t q_base = smem_u32(q_smem);
+            const uint32_t kv_base = smem_u32(kv_smem);
+            uint32_t g = 0, it = 0;
+            for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x, ++it) {
+                const int half = static_cast<int>(item & 1);
+                mbar_wait(q_full, it & 1);
+                mbar_wait(q_tmem, it & 1);
                 tc_fence_after();
-#pragma unroll 1
-                for (int c0 = 0; c0 < kDvHalf; c0 += 32) {
-                    float o[32];
-                    tmem_ld32(lane_base + kColO + c0, o);
-                    tmem_ld_wait();
+                auto issue_pv = [&](int j, uint32_t gj) {
+                    const int s = gj % kStages;
+                    if (j == 0 && it > 0) mbar_wait(o_free, (it - 1) & 1);  // the last epilogue has read O
+                    mbar_wait(&p_full[gj & 1], (gj >> 1) & 1);
+                    tc_fence_after();
+                    const uint32_t vb = kv_base + s * kKvStageBytes + (half * 4) * kKvPanelBytes;
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) o[c] *= alpha;
-                    tmem_st32(lane_base + kColO + c0, o);
+                    for (int kk = 0; kk < kBlk / 16; ++kk)  // 16 keys per K step: 8 columns of P, 2 KiB of rows
+                        umma_bf16_ts(tmem + kColO, tmem + kColS + (gj & 1) * kBlk + kk * 8,
+                                     sw128_mnmajor_desc(vb + kk * 2048, kKvPanelBytes, 1024), kIdescPV,
+                                     (j > 0 || kk > 0) ? 1u : 0u);
+                    umma_commit(&kv_empty[s]);  // stage free and O holds PV of block j
+                };
+                for (int j = 0; j < nb; ++j) {
+                    const uint32_t gj = g + j;
+                    const int s = gj % kStages;
+                    mbar_wait(&kv_full[s], (gj / kStages) & 1);
+                    fence_proxy_async();  // cp.async (generic proxy) writes -> the tensor core's reads
+                    tc_fence_after();
+                    const uint32_t st = kv_base + s * kKvStageBytes;
+                    const uint32_t d = tmem + kColS + (gj & 1) * kBlk;
+#pragma unroll
+                    for (int kk = 0; kk < kQTmemSteps; ++kk)  // Q head from TMEM: 8 columns per 16 dims
+                        umma_bf16_ts(d, tmem + kColQ + kk * 8,
+                                     sw128_kmajor_desc(st + (kk >> 2) * kKvPanelBytes + (kk & 3) * 32), kIdescQK,
+                                     kk > 0 ? 1u : 0u);
+#pragma unroll
+                    for (int kk = kQTmemSteps; kk < kDqk / 16; ++kk) {  // Q tail from shared memory
+                        const uint32_t qa = q_base + ((kk - kQTmemSteps) >> 2) * kQPanelBytes + (kk & 3) * 32;
+                        const uint32_t kb = st + (kk >> 2) * kKvPanelBytes + (kk & 3) * 32;
+                        umma_bf16(d, sw128_kmajor_desc(qa), sw128_kmajor_desc(kb), kIdescQK, 1u);
+                    }
+                    umma_commit(&s_full[gj & 1]);
+                    if (j == nb - 1) umma_commit(q_free);  // Q (TMEM head, smem tail) reusable
+                    if (j > 0) issue_pv(j - 1, gj - 1);
                 }
-                tmem_st_wait();
+                issue_pv(nb - 1, g + nb - 1);
+                g += nb;
             }
-            uint32_t pk[kBlk / 2];
-            float sum = 0.f;
+        }
+    } else {
+        // ---------------------------------------------------------- softmax + epilogue
+        const int row = warp * 32 + lane;  // head
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+        const float scale_log2 = p.sm_scale * 1.4426950408889634f;
+        const float ninf = -INFINITY;
+        uint32_t g = 0, it = 0;
+        for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x, ++it) {
+            int b, half;
+            int64_t tq;
+            decode(item, b, tq, half);
+            float m = ninf, l = 0.f;
+            for (int j = 0; j < nb; ++j, ++g) {
+                const int s = g % kStages;
+                mbar_wait(&s_full[g & 1], (g >> 1) & 1);
+                mbar_wait(&kv_full[s], (g / kStages) & 1);  // completed: orders the valid word
+                tc_fence_after();
+                float x[kBlk];
+                tmem_ld32(lane_base + kColS + (g & 1) * kBlk, x);
+                const uint32_t vm = valid_w[s];
+                tmem_ld_wait();
+                float mx = ninf;
 #pragma unroll
-            for (int c = 0; c < kBlk; c += 2) {
-                const float p0 = m == ninf ? 0.f : ex2(x[c] - m);
-                const float p1 = m == ninf ? 0.f : ex2(x[c + 1] - m);
-                sum += p0 + p1;
-                const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-                pk[c / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+                for (int c = 0; c < kBlk; ++c) {
+                    x[c] = ((vm >> c) & 1u) ? x[c] * scale_log2 : ninf;
+                    mx = fmaxf(mx, x[c]);
+                }
+                float alpha = 1.f;
+                bool rescale = false;
+                if (mx > m) {
+                    if (m == ninf) {
+                        m = mx;  // O is unwritten (j == 0) or all zero: nothing to rescale
+                    } else if (mx > m + kRescaleLog2) {
+                        alpha = ex2(m - mx);
+                        l *= alpha;
+                        m = mx;
+                        rescale = true;
+                    }
+                }
+                if (__any_sync(0xffffffffu, rescale)) {
+                    // PV of block j-1 has landed in O. Its commit is kv_empty of
+                    // that block's stage; the barrier's previous phase (PV of
+                    // block g-5) completed before block g-1 was loaded and its
+                    // next one (PV of block g+3) needs this warp's P of block
+                    // g+3, so a parity wait here is exact even though this warp
+                    // skips the blocks without a rescale. (tcgen05.commit
+                    // completions are not ordered across barriers: a single
+                    // o_done barrier waited only on rescaling blocks returned
+                    // early and corrupted O.)
+                    mbar_wait(&kv_empty[(g - 1) % kStages], ((g - 1) / kStages) & 1);
+                    tc_fence_after();
+#pragma unroll 1
+                    for (int c0 = 0; c0 < kDvHalf; c0 += 32) {
+                        float o[32];
+                        tmem_ld32(lane_base + kColO + c0, o);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) o[c] *= alpha;
+                        tmem_st32(lane_base + kColO + c0, o);
+                    }
+                    tmem_st_wait();
+                }
+                uint32_t pk[kBlk / 2];
+                float sum = 0.f;
+#pragma unroll
+                for (int c = 0; c < kBlk; c += 2) {
+                    const float p0 = m == ninf ? 0.f : ex2(x[c] - m);
+                    const float p1 = m == ninf ? 0.f : ex2(x[c + 1] - m);
+                    sum += p0 + p1;
+                    const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                    pk[c / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+                }
+                l += sum;
+                tmem_st16(lane_base + kColS + (g & 1) * kBlk, pk);  // P over the S columns just read
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&p_full[g & 1]);
             }
-            l += sum;
-            tmem_st16(lane_base + kColS + (j & 1) * kBlk, pk);  // P over the S columns just read
-            tmem_st_wait();
+            // epilogue: O / l -> bf16 rows of this head, lse (half 0)
+            mbar_wait(&kv_empty[(g - 1) % kStages], ((g - 1) / kStages) & 1);  // the item's last PV landed
+            tc_fence_after();
+            const float inv_l = l > 0.f ? 1.f / l : 0.f;
+            __nv_bfloat16* orow =
+                p.out + ((static_cast<int64_t>(b) * p.seq_len + tq) * kH + row) * p.out_ld + half * kDvHalf;
+#pragma unroll 1
+            for (int c0 = 0; c0 < kDvHalf; c0 += 32) {
+                float o[32];
+                tmem_ld32(lane_base + kColO + c0, o);
+                tmem_ld_wait();
+                uint4 pk[4];
+                uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+                for (int c = 0; c < 32; c += 2) {
+                    const __nv_bfloat162 h2 = __floats2bfloat162_rn(o[c] * inv_l, o[c + 1] * inv_l);
+                    pw[c / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+                }
+                uint4* dst = reinterpret_cast<uint4*>(orow + c0);
+#pragma unroll
+                for (int v = 0; v < 4; ++v) dst[v] = pk[v];
+            }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&p_full[j & 1]);
+            if (lane == 0) mbar_arrive(o_free);  // the next item's first PV may overwrite O
+            if (half == 0 && p.lse != nullptr)
+                p.lse[(static_cast<int64_t>(b) * p.seq_len + tq) * kH + row] =
+                    l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : ninf;
         }
-        // epilogue: O / l -> bf16 rows of this head, lse (half 0)
-        if (nb > 0) mbar_wait(&kv_empty[(nb - 1) % kStages], ((nb - 1) / kStages) & 1);  // last PV landed
-        tc_fence_after();
-        const float inv_l = l > 0.f ? 1.f / l : 0.f;
-        __nv_bfloat16* orow =
-            p.out + ((static_cast<int64_t>(b) * p.seq_len + tq) * kH + row) * p.out_ld + half * kDvHalf;
-#pragma unroll 1
-        for (int c0 = 0; c0 < kDvHalf; c0 += 32) {
-            float o[32];
-            tmem_ld32(lane_base + kColO + c0, o);
-            tmem_ld_wait();
-            uint4 pk[4];
-            uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
-#pragma unroll
-            for (int c = 0; c < 32; c += 2) {
-                const __nv_bfloat162 h2 = __floats2bfloat162_rn(o[c] * inv_l, o[c + 1] * inv_l);
-                pw[c / 2] = *reinterpret_cast<const uint32_t*>(&h2);
-            }
-            uint4* dst = reinterpret_cast<uint4*>(orow + c0);
-#pragma unroll
-            for (int v = 0; v < 4; ++v) dst[v] = pk[v];
-        }
-        if (half == 0 && p.lse != nullptr)
-            p.lse[(static_cast<int64_t>(b) * p.seq_len + tq) * kH + row] =
-                l > 0.f ? (m + log2f(l)) * 0.6931471805599453f : ninf;
     }
 
     tc_fence_before();
@@ -412,7 +469,12 @@ cudaError_t launch_sparse_mla(const CUtensorMap& qmap, const SparseMlaParams& p,
         if (e != cudaSuccess) return e;
         attr_set[dev] = true;
     }
-    const dim3 grid(static_cast<unsigned>(2 * p.seq_len), static_cast<unsigned>(p.batch));
+    // persistent: one CTA per SM walks the (b, query, half) items round-robin
+    int sms = 0, cur = 0;
+    cudaGetDevice(&cur);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cur);
+    const int64_t items = 2 * p.seq_len * p.batch;
+    const unsigned grid = static_cast<unsigned>(items < sms ? items : sms);
     sparse_mla_kernel<<<grid, kThreads, kSmemBytes, stream>>>(qmap, p);
     return cudaGetLastError();
 }
