@@ -120,6 +120,32 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+// 2^y for a pair on the FMA / ALU pipes (y <= ~8 here): round-to-nearest
+// split y = n + f (f in [-1/2, 1/2]) by the 1.5 * 2^23 trick, a quartic for
+// 2^f (max relative error 5.3e-6: far below P's bf16 rounding, and l = sum p
+// stays within the lse tolerance; a cubic's 1.7e-4 did not), 2^n added
+// to the exponent field. Half of each block's exponentials take this path so
+// the MUFU pipe is not the softmax's bound (the FA4 split).
+__device__ __forceinline__ float2 exp2_poly2(float2 y) {
+    const float2 magic = make_float2(12582912.f, 12582912.f);
+    y.x = fmaxf(y.x, -127.f);
+    y.y = fmaxf(y.y, -127.f);
+    const float2 t = __fadd2_rn(y, magic);
+    const float2 f = __fadd2_rn(y, __fadd2_rn(magic, make_float2(-t.x, -t.y)));  // y - (t - magic)
+    float2 p = __ffma2_rn(make_float2(0.009591416f, 0.009591416f), f, make_float2(0.05587532f, 0.05587532f));
+    p = __ffma2_rn(p, f, make_float2(0.24023689f, 0.24023689f));
+    p = __ffma2_rn(p, f, make_float2(0.69312757f, 0.69312757f));
+    p = __ffma2_rn(p, f, make_float2(1.f, 1.f));
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // MN-major SW128 descriptor (B of O += P V): the gathered tile read with Dv
@@ -356,12 +382,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_ld32(lane_base + kColS + (g & 1) * kBlk, x);
                 const uint32_t vm = valid_w[s];
                 tmem_ld_wait();
-                float mx = ninf;
+                if (vm != 0xffffffffu) {  // block-uniform: padding / out-of-range keys -> -inf
 #pragma unroll
-                for (int c = 0; c < kBlk; ++c) {
-                    x[c] = ((vm >> c) & 1u) ? x[c] * scale_log2 : ninf;
-                    mx = fmaxf(mx, x[c]);
+                    for (int c = 0; c < kBlk; ++c) x[c] = ((vm >> c) & 1u) ? x[c] : ninf;
                 }
+                // raw block max (3-input FMNMX tree), then the exp2 domain
+                float t3[11];
+#pragma unroll
+                for (int c = 0; c < 10; ++c) t3[c] = max3f(x[3 * c], x[3 * c + 1], x[3 * c + 2]);
+                t3[10] = fmaxf(x[30], x[31]);
+                const float mx = max3f(max3f(max3f(t3[0], t3[1], t3[2]), max3f(t3[3], t3[4], t3[5]),
+                                             max3f(t3[6], t3[7], t3[8])),
+                                       t3[9], t3[10]) * scale_log2;
                 float alpha = 1.f;
                 bool rescale = false;
                 if (mx > m) {
@@ -397,15 +429,32 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     tmem_st_wait();
                 }
+                // p = 2^(s * scale_log2 - m): one FFMA2 per pair for the argument,
+                // MUFU.EX2 for the first half of the block, the FMA-pipe quartic for
+                // the second; pairwise sums; packed to bf16 pairs for the PV MMA
                 uint32_t pk[kBlk / 2];
                 float sum = 0.f;
+                if (m != ninf) {
+                    const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m, -m);
+                    float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-                for (int c = 0; c < kBlk; c += 2) {
-                    const float p0 = m == ninf ? 0.f : ex2(x[c] - m);
-                    const float p1 = m == ninf ? 0.f : ex2(x[c + 1] - m);
-                    sum += p0 + p1;
-                    const __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-                    pk[c / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+                    for (int c = 0; c < kBlk; c += 2) {
+                        const float2 a = __ffma2_rn(make_float2(x[c], x[c + 1]), sc2, nm2);
+                        float2 pr;
+                        if (c < kBlk / 2) {
+                            pr.x = ex2(a.x);
+                            pr.y = ex2(a.y);
+                        } else {
+                            pr = exp2_poly2(a);
+                        }
+                        acc = __fadd2_rn(acc, pr);
+                        const __nv_bfloat162 h2 = __floats2bfloat162_rn(pr.x, pr.y);
+                        pk[c / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+                    }
+                    sum = acc.x + acc.y;
+                } else {
+#pragma unroll
+                    for (int c = 0; c < kBlk / 2; ++c) pk[c] = 0u;
                 }
                 l += sum;
                 tmem_st16(lane_base + kColS + (g & 1) * kBlk, pk);  // P over the S columns just read
