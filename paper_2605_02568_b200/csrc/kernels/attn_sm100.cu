@@ -180,7 +180,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* q_tmem = p_full + 2;              // [1] Q head staged into TMEM, per item
     uint64_t* q_free = q_tmem + 1;              // [1] every S MMA of the item done (Q reusable)
     uint64_t* o_free = q_free + 1;              // [1] the epilogue has read O
-    uint32_t* valid_w = reinterpret_cast<uint32_t*>(o_free + 1);  // [kStages]
+    uint64_t* vw_free = o_free + 1;             // [kStages] the softmax warps have read the valid word
+    uint32_t* valid_w = reinterpret_cast<uint32_t*>(vw_free + kStages);  // [kStages]
     uint32_t* tmem_slot = valid_w + kStages;
 
     const int warp = threadIdx.x / 32;
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         mbar_init(q_full, 1);
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(&kv_full[s], kProducers);  // one cp.async arrive per producer thread
+            mbar_init(&kv_full[s], kProducers + 1);  // one cp.async arrive per producer thread + the valid word
             mbar_init(&kv_empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
@@ -201,6 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(q_tmem, 4);    // one arrive per Q-staging warp
         mbar_init(q_free, 1);
         mbar_init(o_free, 4);    // one arrive per softmax warp
+        for (int s = 0; s < kStages; ++s) mbar_init(&vw_free[s], 4);
         fence_barrier_init();
     }
     if (warp == 8) tmem_alloc<kTmemCols>(tmem_slot);
@@ -257,12 +259,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t vmask = 0;
                 if (warp == 4) vmask = __ballot_sync(0xffffffffu, idx_s[j * kBlk + lane] >= 0);
                 mbar_wait(&kv_empty[s], ((g / kStages) & 1) ^ 1);
-                if (pt == 0) valid_w[s] = vmask;
+                // this thread's copies into the stage for block g - 4 have landed
+                // (the MMA consumed them, so this never waits); the group wait
+                // makes that ordering visible to tools that track cp.async
+                // (racecheck does not model the mbarrier completion)
+                asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 1) : "memory");
+                if (pt == 0) {
+                    // the valid word of block g - 4 has been read (a thread-to-thread
+                    // barrier, so the reuse is ordered without going through the
+                    // tensor core's commits; it has always completed by now)
+                    mbar_wait(&vw_free[s], ((g / kStages) & 1) ^ 1);
+                    valid_w[s] = vmask;
+                    mbar_arrive(&kv_full[s]);  // release: the softmax reads the word after kv_full
+                }
                 const uint32_t st = smem_u32(kv_smem + s * kKvStageBytes);
 #pragma unroll
                 for (int u = 0; u < kPieces; ++u)
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st + soff[u]), "l"(src + 64 * u)
                                  : "memory");
+                asm volatile("cp.async.commit_group;" ::: "memory");
                 asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&kv_full[s]))
                              : "memory");
             }
@@ -380,7 +395,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 float x[kBlk];
                 tmem_ld32(lane_base + kColS + (g & 1) * kBlk, x);
-                const uint32_t vm = valid_w[s];
+                // lane 0 reads the valid word and releases it (its own arrive orders
+                // its own read), the warp gets it by shuffle
+                uint32_t vm = 0;
+                if (lane == 0) {
+                    vm = valid_w[s];
+                    mbar_arrive(&vw_free[s]);
+                }
+                vm = __shfl_sync(0xffffffffu, vm, 0);
                 tmem_ld_wait();
                 if (vm != 0xffffffffu) {  // block-uniform: padding / out-of-range keys -> -inf
 #pragma unroll

@@ -10,6 +10,9 @@ a size the sanitizer finishes in seconds to a minute.
   persistent the persistent multi-row select (SM partition)
   two_level  the group-maxima score epilogue + two-level select, incl. a
              row whose last 32-key group is partial at the end of the buffer
+  attention  the sparse attention over top-k indices (persistent tcgen05
+             kernel: cp.async gathers, TMEM Q / S / P / O, lazy rescale),
+             with padding, an empty row, out-of-range indices, large logits
 """
 import os
 import sys
@@ -91,6 +94,19 @@ def case_two_level(e):
     oi2 = torch.zeros((1, 64, k2), dtype=torch.int64, device="cuda")
     ov2 = torch.zeros((1, 64, k2), dtype=torch.float32, device="cuda")
     e.select_final(tile2, 1, 64, T2, S2 - 64, 0, m, k2, oi2, ov2, 0, gmax=gmax2)
+
+
+def case_attention(e):
+    H, D = 128, 576
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for (B, S, T, k, scale) in [(1, 6, 300, 100, 1.0), (2, 3, 2048, 512, 4.0)]:
+        q = (torch.randn(B, S, H, D, device="cuda", generator=g) * scale).to(torch.bfloat16)
+        kv = torch.randn(B, T, D, device="cuda", generator=g).to(torch.bfloat16)
+        idx = torch.argsort(torch.rand(B * S, T, device="cuda", generator=g), dim=1)[:, :k].reshape(B, S, k).int()
+        idx[:, 0, k // 2:] = -1
+        idx[:, 1, :] = -1
+        idx[:, 2, 0] = T + 3
+        e.sparse_attention(q, kv, idx.contiguous(), D ** -0.5)
 
 
 if __name__ == "__main__":

@@ -4,7 +4,8 @@ hazards) and synccheck (barrier misuse) on small workloads that drive every
 kernel family through the C-ABI (scripts/sanitize_case.py): the V4 step
 (tcgen05 score + fused select), an exact-kernel key tiling (select + merge +
 finalize), the select's sampled / heavy-tie / exact-fallback / large-take
-paths, the persistent multi-row select and the two-level select. Each run
+paths, the persistent multi-row select, the two-level select and the sparse
+attention kernel. Each run
 must report zero errors / hazards."""
 import os
 import shutil
@@ -29,7 +30,7 @@ def need_gpu():
 
 
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
-@pytest.mark.parametrize("case", ["smoke", "select", "persistent", "two_level"])
+@pytest.mark.parametrize("case", ["smoke", "select", "persistent", "two_level", "attention"])
 def test_sanitizer_reports_no_hazards(tool, case):
     cmd = [SANITIZER, "--tool", tool, "--error-exitcode", "7", "--print-limit", "20", sys.executable,
            os.path.join(ROOT, "scripts", "sanitize_case.py"), case]
