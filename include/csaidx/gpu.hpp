@@ -18,6 +18,11 @@ struct Options {
     int device = 0;            // CUDA ordinal used by the host-API entry points
     bool strict_bf16 = false;  // reject q / kc values that are not bf16-representable
     void* stream = nullptr;    // cudaStream_t to enqueue on; nullptr = engine's own stream
+    // AccumulationMode::fp16_emulated with ScoreKernel::auto_detect on the V4
+    // shape runs on the tensor cores (the reference's binary16 rounding points
+    // applied to the MMA's dot products: agreement to binary16 rounding, not
+    // bit for bit; the default keeps the bit-exact CUDA-core kernel)
+    bool fp16_tensor_cores = false;
 };
 
 // Options of the calling thread (and the default of threads that never set

@@ -39,6 +39,9 @@ extern "C" {
 /* Score kernel request, mirrors ScoreKernel (score.hpp:19-27). */
 #define CSAIDX_KERNEL_AUTO 0   /* tcgen05 when the shape allows, else exact */
 #define CSAIDX_KERNEL_EXACT 1  /* CUDA-core kernel in the reference op order */
+#define CSAIDX_KERNEL_TENSOR 2 /* tcgen05 also for fp16_emulated: the reference's binary16 rounding points
+                                  (score_scalar.cpp:29-32, half.cpp:84-91) applied to the MMA's dot
+                                  products, so agreement is to binary16 rounding, not bit for bit */
 
 /* AccumulationMode (score.hpp:11-17). */
 #define CSAIDX_MODE_FP32 0

@@ -42,6 +42,7 @@ typedef struct csaidx_run_config {
     int device;
     int strict_bf16;
     void* stream;                  /* cudaStream_t or NULL (engine stream) */
+    int fp16_tensor_cores;         /* gpu::Options::fp16_tensor_cores */
 } csaidx_run_config;
 
 /* RunStats (driver.hpp:55-59) + the path taken and both peaks. */

@@ -62,6 +62,7 @@ class RunConfig(Structure):
         ("device", c_int),
         ("strict_bf16", c_int),
         ("stream", c_void_p),
+        ("fp16_tensor_cores", c_int),
     ]
 
 
@@ -197,11 +198,13 @@ class DriverConfig:
     device: int = 0
     strict_bf16: bool = False
     stream: int = 0
+    fp16_tensor_cores: bool = False
 
     def c(self) -> RunConfig:
         return RunConfig(self.tile.query_tile, self.tile.key_tile, int(self.mode), int(self.ablation),
                          int(self.kernel), int(self.causal_early_exit), int(self.bool_mask_tile), self.threads,
-                         self.auto_threshold_bytes, self.device, int(self.strict_bf16), c_void_p(self.stream))
+                         self.auto_threshold_bytes, self.device, int(self.strict_bf16), c_void_p(self.stream),
+                         int(self.fp16_tensor_cores))
 
 
 @dataclass

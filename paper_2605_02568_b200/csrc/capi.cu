@@ -599,8 +599,10 @@ int csaidx_cuda_to_bf16(csaidx_engine* e, const float* src, uint16_t* dst, int64
 
 int csaidx_cuda_score_uses_tensor_cores(const csaidx_dims* d, int dtype, int mode, int kernel) {
     if (d == nullptr) return 0;
-    return kernel == CSAIDX_KERNEL_AUTO && mode == CSAIDX_MODE_FP32 && dtype == CSAIDX_DTYPE_BF16 &&
-           csaidx_kern::score_tc_supported(d->heads, d->head_dim);
+    const bool mode_ok = (kernel == CSAIDX_KERNEL_AUTO && mode == CSAIDX_MODE_FP32) ||
+                         (kernel == CSAIDX_KERNEL_TENSOR &&
+                          (mode == CSAIDX_MODE_FP32 || mode == CSAIDX_MODE_FP16_EMULATED));
+    return mode_ok && dtype == CSAIDX_DTYPE_BF16 && csaidx_kern::score_tc_supported(d->heads, d->head_dim);
 }
 
 }  // extern "C"
@@ -611,7 +613,7 @@ namespace {
 int launch_tc(csaidx_engine* e, const void* q, const void* kc, const float* w, const csaidx_dims* d, int64_t s0,
               int64_t rows, int64_t t0, int64_t cols, int apply_mask, float* out, int64_t ld, int kt_stride,
               const float* tau, uint32_t* pass_bits, int64_t bits_ld, int64_t op_rows = -1, int64_t op_row0 = -1,
-              float* gmax = nullptr, int64_t gmax_ld = 0) {
+              float* gmax = nullptr, int64_t gmax_ld = 0, bool fp16 = false) {
     if (op_rows < 0) {
         op_rows = d->seq_len;
         op_row0 = s0;
@@ -644,6 +646,7 @@ int launch_tc(csaidx_engine* e, const void* q, const void* kc, const float* w, c
     p.bits_ld = bits_ld;
     p.gmax = gmax;
     p.gmax_ld = gmax_ld;
+    p.fp16 = fp16 ? 1 : 0;
     p.probe = e->score_probe;
     LaunchScope ls(e, CSAIDX_KIND_SCORE);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_score_tc(qmap, kmap, p, e->score_sms > 0 ? e->score_sms : e->num_sms,
@@ -743,11 +746,11 @@ int csaidx_cuda_score_rows(csaidx_engine* e, const void* q, const void* kc, int 
         return fail(CSAIDX_INVALID_ARGUMENT, "score: unknown accumulation mode");
     if (dtype != CSAIDX_DTYPE_BF16 && dtype != CSAIDX_DTYPE_F32)
         return fail(CSAIDX_INVALID_ARGUMENT, "score: unknown operand dtype");
-    if (kernel != CSAIDX_KERNEL_AUTO && kernel != CSAIDX_KERNEL_EXACT)
+    if (kernel != CSAIDX_KERNEL_AUTO && kernel != CSAIDX_KERNEL_EXACT && kernel != CSAIDX_KERNEL_TENSOR)
         return fail(CSAIDX_INVALID_ARGUMENT, "score: unknown kernel request");
     if (csaidx_cuda_score_uses_tensor_cores(d, dtype, mode, kernel)) {
         return launch_tc(e, q, kc, w, d, s0, rows, t0, cols, apply_mask, out, ld, 1, nullptr, nullptr, 0, op_rows,
-                         op_row0);
+                         op_row0, nullptr, 0, mode == CSAIDX_MODE_FP16_EMULATED);
     } else {
         ScoreExactParams p{};
         p.q = q;

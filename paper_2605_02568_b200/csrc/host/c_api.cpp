@@ -74,6 +74,7 @@ csaidx::DriverConfig from_c(const csaidx_run_config* c) {
     o.device = c->device;
     o.strict_bf16 = c->strict_bf16 != 0;
     o.stream = c->stream;
+    o.fp16_tensor_cores = c->fp16_tensor_cores != 0;
     csaidx::gpu::set_options(o);
     return cfg;
 }
@@ -103,7 +104,7 @@ void csaidx_host_default_config(csaidx_run_config* cfg) {
     if (cfg == nullptr) return;
     const csaidx::DriverConfig d;
     *cfg = csaidx_run_config{d.tile.query_tile, d.tile.key_tile, CSAIDX_MODE_FP32, CSAIDX_ABLATION_NONE,
-                             CSAIDX_SCORE_AUTO, 1, 0, 1, d.auto_threshold_bytes, 0, 0, nullptr};
+                             CSAIDX_SCORE_AUTO, 1, 0, 1, d.auto_threshold_bytes, 0, 0, nullptr, 0};
 }
 
 int csaidx_host_engine(int device, csaidx_engine** out) {

@@ -144,9 +144,13 @@ bool prefilter_enabled() {
     return v != nullptr && std::string(v) == "1";
 }
 
-int kernel_code(ScoreKernel kernel) {
+int kernel_code(ScoreKernel kernel, AccumulationMode mode) {
     switch (kernel) {
-        case ScoreKernel::auto_detect: return CSAIDX_KERNEL_AUTO;
+        case ScoreKernel::auto_detect:
+            // fp16_emulated stays on the bit-exact kernel unless the caller
+            // opts into the tensor-core form (gpu::Options::fp16_tensor_cores)
+            return mode == AccumulationMode::fp16_emulated && gpu::options().fp16_tensor_cores ? CSAIDX_KERNEL_TENSOR
+                                                                                                : CSAIDX_KERNEL_AUTO;
         case ScoreKernel::scalar: return CSAIDX_KERNEL_EXACT;
         case ScoreKernel::avx2:
             throw std::invalid_argument("avx2 kernel requested but this build has no AVX2 kernel (B200 path)");

@@ -66,7 +66,7 @@ int select_overlap_sms();
 bool two_level_enabled();
 constexpr int64_t kPrefilterSampleTiles = 16;
 
-int kernel_code(ScoreKernel kernel);  // throws like resolve_score_kernel for unavailable kernels
+int kernel_code(ScoreKernel kernel, AccumulationMode mode);  // throws like resolve_score_kernel for unavailable kernels
 int mode_code(AccumulationMode mode);
 csaidx_dims to_c(const ProblemDims& d);
 

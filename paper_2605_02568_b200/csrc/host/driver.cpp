@@ -68,7 +68,7 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
               const ChunkPlan& plan, int64_t* out_idx, float* out_val, int64_t out_rows, MemoryLedger& ledger,
               RunStats& stats, const ChunkHooks& hooks) {
     const int64_t B = dims.batch, k = dims.top_k, T = dims.key_blocks;
-    const int kcode = kernel_code(config.kernel);
+    const int kcode = kernel_code(config.kernel, config.mode);
     const int mcode = mode_code(config.mode);
     const csaidx_dims cd = to_c(dims);
     const int64_t ld = (plan.ct + 3) / 4 * 4;
@@ -389,7 +389,7 @@ void run_chunked_rows_impl(const HostView& in, const ProblemDims& dims, const Dr
 void run_chunked_rows_view(const HostView& in, const ProblemDims& dims, const DriverConfig& config,
                            const std::vector<int64_t>* starts, int64_t* host_idx, float* host_val, int64_t out_rows,
                            MemoryLedger& ledger, RunStats* stats_out) {
-    const int dtype = operand_dtype(dims, mode_code(config.mode), kernel_code(config.kernel));
+    const int dtype = operand_dtype(dims, mode_code(config.mode), kernel_code(config.kernel, config.mode));
     try {
         run_chunked_rows_impl(in, dims, config, starts, host_idx, host_val, out_rows, ledger, stats_out, dtype);
     } catch (const OperandsNotBf16&) {
@@ -641,7 +641,7 @@ TopKResult run_materialize_view(const HostView& in, const ProblemDims& dims, Acc
                                 MemoryLedger& ledger, ScoreKernel kernel) {
     validate_dims(dims);
     TopKResult out = TopKResult::sized(dims);
-    const int kcode = kernel_code(kernel);
+    const int kcode = kernel_code(kernel, mode);
     const int mcode = mode_code(mode);
     std::lock_guard<std::mutex> lock(engine_mutex());
     csaidx_engine* e = engine();
@@ -700,7 +700,7 @@ void run_chunked_device(const DeviceOperands& ops, const ProblemDims& dims, cons
     int64_t need = 0;
     for (size_t c = 0; c < plan.starts.size(); ++c) need = plan.out_row0[c] + std::min(plan.cs, dims.seq_len - plan.starts[c]);
     if (out_rows < need) throw std::invalid_argument("run_chunked_device: out_rows too small for the chunk list");
-    const int kcode = detail::kernel_code(config.kernel);
+    const int kcode = detail::kernel_code(config.kernel, config.mode);
     if (ops.dtype != detail::operand_dtype(dims, detail::mode_code(config.mode), kcode))
         throw std::invalid_argument("run_chunked_device: operand dtype does not match the selected score kernel");
     std::lock_guard<std::mutex> lock(detail::engine_mutex());

@@ -34,7 +34,7 @@ ScoreTile score_tile(const IndexerInputs& inputs, const ProblemDims& dims, int64
                      int64_t cols, AccumulationMode mode, MemoryLedger& ledger, ScoreKernel kernel) {
     if (rows < 1 || cols < 1 || s0 < 0 || t0 < 0 || s0 + rows > dims.seq_len || t0 + cols > dims.key_blocks)
         throw std::invalid_argument("score_tile: tile out of range");
-    const int kcode = detail::kernel_code(kernel);
+    const int kcode = detail::kernel_code(kernel, mode);
     const int mcode = detail::mode_code(mode);
 
     ScoreTile tile;

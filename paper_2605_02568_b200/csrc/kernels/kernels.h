@@ -26,6 +26,7 @@ struct ScoreTcParams {
     int64_t op_rows, op_shift;
     int batch;
     int apply_mask;
+    int fp16;  // AccumulationMode::fp16_emulated epilogue (binary16 rounding points)
     // Sample mode: tile kt of the launch covers physical key tile
     // kt * kt_stride; outputs use the compacted (virtual) column kt*128+lane.
     int kt_stride;

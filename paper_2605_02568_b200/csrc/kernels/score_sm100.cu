@@ -209,10 +209,63 @@ __device__ __forceinline__ float2 head_reduce_tmem2(uint32_t taddr0, uint32_t ta
     return make_float2((a0.x + a0.y) + (a1.x + a1.y), (b0.x + b0.y) + (b1.x + b1.y));
 }
 
+// fp16_emulated on the tensor cores (AccumulationMode::fp16_emulated,
+// score_scalar.cpp:29-32 / half.cpp:84-91): each head's dot product (the
+// MMA's fp32 value) is rounded to binary16 with saturation, ReLU'd as
+// x < 0 ? 0 : x, and acc = half(acc + w * r) is accumulated in ascending h
+// with the multiply and the add rounded separately — the reference's
+// rounding points; only the dot product's own summation order differs from
+// the scalar kernel (the MMA's), so results agree to binary16 rounding, not
+// bit for bit (score_exact_kernel stays the bit-exact path). Both queries of
+// an accumulator pair run in one packed chain: cvt.rn.satfinite.f16x2 +
+// FMUL2 / FADD2.
+__device__ __forceinline__ float2 half2_round_sat(float a, float b) {
+    uint32_t h;
+    asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(b), "f"(a));  // b -> upper, a -> lower
+    const __half2 v = *reinterpret_cast<const __half2*>(&h);
+    return make_float2(__low2float(v), __high2float(v));
+}
+
+__device__ __forceinline__ float2 head_reduce_fp16_2(uint32_t taddr0, uint32_t taddr1, const float* __restrict__ w0,
+                                                     const float* __restrict__ w1) {
+    float2 acc = make_float2(0.f, 0.f);
+    float va[8], vb[8], vc[8], vd[8];
+    tmem_ld8(taddr0, va);
+    tmem_ld8(taddr1, vb);
+    tmem_ld_wait();
+#pragma unroll
+    for (int s = 0; s < 8; s += 2) {
+        tmem_ld8(taddr0 + (s + 1) * 8, vc);
+        tmem_ld8(taddr1 + (s + 1) * 8, vd);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const float2 d = half2_round_sat(va[c], vb[c]);
+            const float2 r = make_float2(d.x < 0.f ? 0.f : d.x, d.y < 0.f ? 0.f : d.y);
+            acc = __fadd2_rn(acc, __fmul2_rn(make_float2(w0[s * 8 + c], w1[s * 8 + c]), r));
+            acc = half2_round_sat(acc.x, acc.y);
+        }
+        tmem_ld_wait();
+        if (s + 2 < 8) {
+            tmem_ld8(taddr0 + (s + 2) * 8, va);
+            tmem_ld8(taddr1 + (s + 2) * 8, vb);
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const float2 d = half2_round_sat(vc[c], vd[c]);
+            const float2 r = make_float2(d.x < 0.f ? 0.f : d.x, d.y < 0.f ? 0.f : d.y);
+            acc = __fadd2_rn(acc, __fmul2_rn(make_float2(w0[(s + 1) * 8 + c], w1[(s + 1) * 8 + c]), r));
+            acc = half2_round_sat(acc.x, acc.y);
+        }
+        if (s + 2 < 8) tmem_ld_wait();
+    }
+    return acc;
+}
+
 // Instances: kMode 0 = plain masked score tile (production), 1 = strided
 // key-tile sample (kt_stride > 1), 2 = plain + candidate bitmap against tau
 // (the fused select pre-filter, CSAIDX_SELECT_PREFILTER=1), 3 = plain +
-// per-32-key group maxima (two-level select for long rows); kProbe adds the
+// per-32-key group maxima (two-level select for long rows), 4 = plain with
+// the fp16_emulated epilogue (head_reduce_fp16_2); kProbe adds the
 // per-role wait-cycle counters (dev). The production instance carries none
 // of the optional code.
 template <int kMode, bool kProbe>
@@ -242,6 +295,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     const int warp = threadIdx.x / 32;
     constexpr bool kFilter = kMode == 2;
     constexpr bool kGmax = kMode == 3;
+    constexpr bool kFp16 = kMode == 4;
     long long* const probe = kProbe ? p.probe : nullptr;  // per-CTA wait-cycle counters (profiling)
     const int64_t kts = kMode == 1 ? p.kt_stride : 1;  // key-tile stride (sample mode)
 
@@ -475,7 +529,18 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                     // warp, then do the stores (and mode epilogues) off its
                     // critical path.
                     float accv[kPerUnit];
-                    if (kPerUnit == 2 && wq[1] < it.nrows) {  // both queries of the accumulator at once
+                    if (kFp16) {  // the unit's queries in one packed chain (a missing second one repeats the first)
+                        const int q0 = wq[un * kPerUnit];
+                        const int q1 = (kPerUnit == 2 && wq[un * kPerUnit + kPerUnit - 1] < it.nrows)
+                                           ? wq[un * kPerUnit + kPerUnit - 1]
+                                           : q0;
+                        const float2 pr = head_reduce_fp16_2(
+                            quarter_taddr + a * kUmmaN + (q0 % kQPerGroup) * kHeads,
+                            quarter_taddr + a * kUmmaN + (q1 % kQPerGroup) * kHeads, w_item + q0 * kHeads,
+                            w_item + q1 * kHeads);
+                        accv[0] = pr.x;
+                        accv[kPerUnit - 1] = pr.y;
+                    } else if (kPerUnit == 2 && wq[1] < it.nrows) {  // both queries of the accumulator at once
                         const uint32_t col = a * kUmmaN;
                         const float2 pr = head_reduce_tmem2(quarter_taddr + col, quarter_taddr + col + kHeads,
                                                             w_item + wq[0] * kHeads, w_item + wq[1] * kHeads);
@@ -502,7 +567,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                             const float acc = accv[pu];
                             const bool legal = j < lim[u];
                             if (jo < out_cols) {
-                                if (legal && !isfinite(acc)) atomicOr(p.nonfinite, 1);
+                                if (!kFp16 && legal && !isfinite(acc)) atomicOr(p.nonfinite, 1);
                                 orow[u][jo] = legal ? acc : neg_inf;
                             }
                             if (kGmax) {
@@ -656,7 +721,7 @@ cudaError_t launch_score_tc(const CUtensorMap& qmap, const CUtensorMap& kmap, Sc
     const int attr_set_dev = attr_device();
     if (!attr_set[attr_set_dev]) {
         for (auto* fn : {score_tc_kernel<0, false>, score_tc_kernel<0, true>, score_tc_kernel<1, false>,
-                         score_tc_kernel<2, false>, score_tc_kernel<3, false>}) {
+                         score_tc_kernel<2, false>, score_tc_kernel<3, false>, score_tc_kernel<4, false>}) {
             cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  static_cast<int>(kSmemBytes));
             if (e != cudaSuccess) return e;
@@ -664,7 +729,9 @@ cudaError_t launch_score_tc(const CUtensorMap& qmap, const CUtensorMap& kmap, Sc
         attr_set[attr_set_dev] = true;
     }
     const int grid = p.nitems < num_sms ? p.nitems : num_sms;
-    if (p.tau != nullptr)
+    if (p.fp16)
+        score_tc_kernel<4, false><<<grid, kNumThreads, kSmemBytes, stream>>>(qmap, kmap, p);
+    else if (p.tau != nullptr)
         score_tc_kernel<2, false><<<grid, kNumThreads, kSmemBytes, stream>>>(qmap, kmap, p);
     else if (p.gmax != nullptr)
         score_tc_kernel<3, false><<<grid, kNumThreads, kSmemBytes, stream>>>(qmap, kmap, p);
