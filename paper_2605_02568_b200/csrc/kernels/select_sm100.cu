@@ -650,6 +650,200 @@ __device__ void write_row(const SelectParams& p, int b, int64_t row_id, int take
     }
 }
 
+// Sampled threshold of a long row (n > cand_cap): ~n/16 scores as evenly
+// spaced 512-byte segments (one float4 per lane, <= 8192 values) held in
+// registers, value-linear histograms over the sample's range (plus one
+// refinement pass inside a coarse rank bin) -> a threshold expected to keep
+// ~2k of the row's entries. Uses hist (kBins words), res, wsum, counter.
+__device__ __forceinline__ float sample_threshold(const float* row, int64_t n, int k, const Layout& L, uint32_t* hist,
+                                               uint32_t* res, uint32_t* wsum, uint32_t* counter) {
+    const int lane = gtid() & 31;
+    // sample evenly spaced 512-byte segments (one float4 per lane,
+    //    ~1/16 of the row, <= 8192 values), held in registers; each
+    //    warp issues all of its loads before consuming them
+    int nseg = static_cast<int>(n / 2048);
+    if (nseg > kSampleSegs) nseg = kSampleSegs;
+    if (nseg < 1) nseg = 1;
+    // 32-bit arithmetic: a row's legal length is < 2^31 (n <= T)
+    const int n32 = static_cast<int>(n);
+    const int64_t seg_stride = (n32 / nseg) & ~3;
+    constexpr int kSegsPerWarp = kSampleSegs / kWarps;  // 8
+    const int w = gtid() >> 5;
+    float4 sv[kSegsPerWarp];
+#pragma unroll
+    for (int u = 0; u < kSegsPerWarp; ++u) {
+        const int sg = w + u * kWarps;
+        sv[u] = sg < nseg ? __ldg(reinterpret_cast<const float4*>(row + sg * seg_stride) + lane)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    uint32_t kmin = 0xffffffffu, kmax = 0u;
+#pragma unroll
+    for (int u = 0; u < kSegsPerWarp; ++u) {
+        if (w + u * kWarps < nseg) {
+            const uint32_t k0 = ord_key(sv[u].x), k1 = ord_key(sv[u].y);
+            const uint32_t k2 = ord_key(sv[u].z), k3 = ord_key(sv[u].w);
+            kmin = min(kmin, min(min(k0, k1), min(k2, k3)));
+            kmax = max(kmax, max(max(k0, k1), max(k2, k3)));
+        }
+    }
+    if (gtid() == 0) {
+        *counter = 0;
+        res[0] = res[1] = res[2] = 0u;  // find_bin leaves them when the rank is out of range
+        res[6] = 0xffffffffu;
+        res[7] = 0u;
+    }
+    for (int i = gtid(); i < kBins; i += kThreads) hist[i] = 0;
+    csync();
+    kmin = __reduce_min_sync(0xffffffffu, kmin);
+    kmax = __reduce_max_sync(0xffffffffu, kmax);
+    if (lane == 0) {
+        atomicMin(&res[6], kmin);
+        atomicMax(&res[7], kmax);
+    }
+    csync();
+    const int ns = 128 * nseg;
+    // ~2k survivors: a comfortable margin over k (misses -> the slow
+    // exact fallback) while the shared list stays at <= 4k entries
+    const int target = (2 * k < (L.cand_cap * 3) / 4) ? 2 * k : (L.cand_cap * 3) / 4;
+    int r = (target * ns) / n32;  // <= 6144 * 8192: no overflow
+    if (r < 1) r = 1;
+    // The sample's rank-r value by value-linear histograms over
+    // [sample min, sample max]: one pass, plus a refinement pass
+    // inside the rank-r bin when that bin is coarse (outliers,
+    // heavy tails). tau = the lower edge of the final bin.
+    const float smin = ord_key_to_float(res[6]), smax = ord_key_to_float(res[7]);
+    float lo = smin, hi = smax;
+    uint32_t rr = static_cast<uint32_t>(r);
+    float tau_f = smin;
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+        float scale = static_cast<float>(kBins) / (hi - lo);
+        if (!(hi > lo) || !isfinite(scale)) break;  // degenerate: keep tau = lo
+        if (pass > 0) {
+            for (int i = gtid(); i < kBins; i += kThreads) hist[i] = 0;
+            if (gtid() == 0) res[0] = res[1] = res[2] = 0u;
+            csync();
+        }
+#pragma unroll
+        for (int u = 0; u < kSegsPerWarp; ++u) {
+            if (w + u * kWarps < nseg) {
+                const float vs[4] = {sv[u].x, sv[u].y, sv[u].z, sv[u].w};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const float v = vs[c];
+                    if (v >= lo && v <= hi)
+                        atomicAdd(&hist[static_cast<int>(fminf((v - lo) * scale, static_cast<float>(kBins - 1)))],
+                                  1u);
+                }
+            }
+        }
+        csync();
+        find_bin(hist, kBins, rr, res, wsum);
+        const uint32_t bin = res[0], above = res[1], cnt = res[2];
+        csync();
+        const float width = (hi - lo) / static_cast<float>(kBins);
+        const float blo = lo + static_cast<float>(bin) * width;
+        tau_f = blo > lo ? blo : lo;
+        if (cnt * 8u <= rr || cnt <= 4u) break;  // fine enough
+        rr -= above;
+        hi = fminf(hi, blo + width);
+        lo = tau_f;
+    }
+    // scores are compared as floats: ord_key is monotone and folds
+    // -0.0 onto +0.0 exactly like the float order
+    if (tau_f == 0.f) tau_f = 0.f;  // -0.0 -> +0.0
+
+    return tau_f;
+}
+
+// One streaming pass over a long row keeping the entries >= tau_f: survivor
+// columns listed in the buf + hist region (warp scan + one shared atomic per
+// warp), then gathered back (L2 hits) into the composites cand[0, count) with
+// the finish histogram prebuilt. Returns count (-1: the threshold kept fewer
+// than k or more than the list holds -> exact fallback).
+template <int kUnroll>
+__device__ __forceinline__ int stream_collect(const float* row, int64_t n, int k, float tau_f, const Layout& L,
+                                              uint64_t* cand, uint64_t* buf, uint32_t* hist, uint32_t* res,
+                                              uint32_t* counter, bool& prebuilt, float& pb_lo, float& pb_scale) {
+    const int lane = gtid() & 31;
+    const uint32_t tau = ord_key(tau_f);
+    if (gtid() == 0) *counter = 0;
+    csync();
+    int count = -1;
+    // survivors are recorded as column indices only (the composites
+    // are gathered after the pass); the list aliases buf + hist
+    uint32_t* idx_list = reinterpret_cast<uint32_t*>(buf);
+
+    // 2. stream the row once; keep entries >= tau
+    const float4* row4 = reinterpret_cast<const float4*>(row);
+    const int64_t n4 = n >> 2;
+    const int64_t step = kUnroll * static_cast<int64_t>(kThreads);
+    const int64_t n4r = (n4 + step - 1) / step * step;
+    const uint32_t cap = static_cast<uint32_t>(
+        min(L.cand_cap, 2 * L.buf_cap + kHistWords));  // idx list capacity
+    for (int64_t it = gtid(); it < n4r; it += step) {
+        float4 v[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const int64_t i4 = it + u * kThreads;
+            v[u] = i4 < n4 ? __ldg(row4 + i4) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        }
+        // one bit per entry: 4 * kUnroll bits (64-bit mask above 8 float4)
+        using Mask = typename std::conditional<(kUnroll > 8), unsigned long long, uint32_t>::type;
+        Mask m = 0;
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            m |= static_cast<Mask>(v[u].x >= tau_f ? 1u : 0u) << (4 * u + 0);
+            m |= static_cast<Mask>(v[u].y >= tau_f ? 1u : 0u) << (4 * u + 1);
+            m |= static_cast<Mask>(v[u].z >= tau_f ? 1u : 0u) << (4 * u + 2);
+            m |= static_cast<Mask>(v[u].w >= tau_f ? 1u : 0u) << (4 * u + 3);
+        }
+        if (!__any_sync(0xffffffffu, m != 0)) continue;
+        const uint32_t c = kUnroll > 8 ? __popcll(m) : __popc(static_cast<uint32_t>(m));
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        uint32_t base = 0;
+        if (lane == 31) base = atomicAdd(counter, incl);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        uint32_t pos = base + incl - c;
+        // Survivors are ~6% of entries: walk only the set bits (the
+        // warp iterates max-popc times, usually 2-4) and record the
+        // column only: the divergent body stays a handful of
+        // instructions.
+        while (m != 0) {
+            const int bit = kUnroll > 8 ? __ffsll(static_cast<long long>(m)) - 1
+                                        : __ffs(static_cast<int>(m)) - 1;
+            m &= m - 1;
+            if (pos < cap)
+                idx_list[pos] = static_cast<uint32_t>(4 * (it + (bit >> 2) * kThreads) + (bit & 3));
+            ++pos;
+        }
+    }
+    if (gtid() < 32) {  // the < 4 entries past the last float4
+        const int64_t i = 4 * n4 + lane;
+        const bool inb = i < n;
+        const uint32_t key = inb ? ord_key(__ldg(row + i)) : 0u;
+        const bool pass = inb && key >= tau;
+        const uint32_t mm = __ballot_sync(0xffffffffu, pass);
+        if (mm != 0) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(counter, __popc(mm));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            const uint32_t pos = base + __popc(mm & ((1u << lane) - 1u));
+            if (pass && pos < cap) idx_list[pos] = static_cast<uint32_t>(i);
+        }
+    }
+    csync();
+    const uint32_t total = *counter;
+    count = (total >= static_cast<uint32_t>(k) && total <= cap) ? static_cast<int>(total) : -1;
+    gather_candidates(row, idx_list, count, cand, hist, tau_f, res + 5, prebuilt, pb_lo, pb_scale);
+    return count;
+}
+
 // ------------------------------------------------------------------ kernel
 
 
@@ -853,174 +1047,9 @@ __device__ __forceinline__ void select_row(const SelectParams& p, int b, int64_t
             }
         }
         if (!have) {
-            // 1. sample evenly spaced 512-byte segments (one float4 per lane,
-            //    ~1/16 of the row, <= 8192 values), held in registers; each
-            //    warp issues all of its loads before consuming them
-            int nseg = static_cast<int>(n / 2048);
-            if (nseg > kSampleSegs) nseg = kSampleSegs;
-            if (nseg < 1) nseg = 1;
-            // 32-bit arithmetic: a row's legal length is < 2^31 (n <= T)
-            const int n32 = static_cast<int>(n);
-            const int64_t seg_stride = (n32 / nseg) & ~3;
-            constexpr int kSegsPerWarp = kSampleSegs / kWarps;  // 8
-            const int w = gtid() >> 5;
-            float4 sv[kSegsPerWarp];
-#pragma unroll
-            for (int u = 0; u < kSegsPerWarp; ++u) {
-                const int sg = w + u * kWarps;
-                sv[u] = sg < nseg ? __ldg(reinterpret_cast<const float4*>(row + sg * seg_stride) + lane)
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            uint32_t kmin = 0xffffffffu, kmax = 0u;
-#pragma unroll
-            for (int u = 0; u < kSegsPerWarp; ++u) {
-                if (w + u * kWarps < nseg) {
-                    const uint32_t k0 = ord_key(sv[u].x), k1 = ord_key(sv[u].y);
-                    const uint32_t k2 = ord_key(sv[u].z), k3 = ord_key(sv[u].w);
-                    kmin = min(kmin, min(min(k0, k1), min(k2, k3)));
-                    kmax = max(kmax, max(max(k0, k1), max(k2, k3)));
-                }
-            }
-            if (gtid() == 0) {
-                *counter = 0;
-                res[0] = res[1] = res[2] = 0u;  // find_bin leaves them when the rank is out of range
-                res[6] = 0xffffffffu;
-                res[7] = 0u;
-            }
-            for (int i = gtid(); i < kBins; i += kThreads) hist[i] = 0;
-            csync();
-            kmin = __reduce_min_sync(0xffffffffu, kmin);
-            kmax = __reduce_max_sync(0xffffffffu, kmax);
-            if (lane == 0) {
-                atomicMin(&res[6], kmin);
-                atomicMax(&res[7], kmax);
-            }
-            csync();
-            if (clk) clk[5] = clock64();
-            const int ns = 128 * nseg;
-            // ~2k survivors: a comfortable margin over k (misses -> the slow
-            // exact fallback) while the shared list stays at <= 4k entries
-            const int target = (2 * k < (L.cand_cap * 3) / 4) ? 2 * k : (L.cand_cap * 3) / 4;
-            int r = (target * ns) / n32;  // <= 6144 * 8192: no overflow
-            if (r < 1) r = 1;
-            // The sample's rank-r value by value-linear histograms over
-            // [sample min, sample max]: one pass, plus a refinement pass
-            // inside the rank-r bin when that bin is coarse (outliers,
-            // heavy tails). tau = the lower edge of the final bin.
-            const float smin = ord_key_to_float(res[6]), smax = ord_key_to_float(res[7]);
-            float lo = smin, hi = smax;
-            uint32_t rr = static_cast<uint32_t>(r);
-            float tau_f = smin;
-#pragma unroll 1
-            for (int pass = 0; pass < 2; ++pass) {
-                float scale = static_cast<float>(kBins) / (hi - lo);
-                if (!(hi > lo) || !isfinite(scale)) break;  // degenerate: keep tau = lo
-                if (pass > 0) {
-                    for (int i = gtid(); i < kBins; i += kThreads) hist[i] = 0;
-                    if (gtid() == 0) res[0] = res[1] = res[2] = 0u;
-                    csync();
-                }
-#pragma unroll
-                for (int u = 0; u < kSegsPerWarp; ++u) {
-                    if (w + u * kWarps < nseg) {
-                        const float vs[4] = {sv[u].x, sv[u].y, sv[u].z, sv[u].w};
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            const float v = vs[c];
-                            if (v >= lo && v <= hi)
-                                atomicAdd(&hist[static_cast<int>(fminf((v - lo) * scale, static_cast<float>(kBins - 1)))],
-                                          1u);
-                        }
-                    }
-                }
-                csync();
-                find_bin(hist, kBins, rr, res, wsum);
-                const uint32_t bin = res[0], above = res[1], cnt = res[2];
-                csync();
-                const float width = (hi - lo) / static_cast<float>(kBins);
-                const float blo = lo + static_cast<float>(bin) * width;
-                tau_f = blo > lo ? blo : lo;
-                if (cnt * 8u <= rr || cnt <= 4u) break;  // fine enough
-                rr -= above;
-                hi = fminf(hi, blo + width);
-                lo = tau_f;
-            }
-            // scores are compared as floats: ord_key is monotone and folds
-            // -0.0 onto +0.0 exactly like the float order
-            if (tau_f == 0.f) tau_f = 0.f;  // -0.0 -> +0.0
-            const uint32_t tau = ord_key(tau_f);
-            // survivors are recorded as column indices only (the composites
-            // are gathered after the pass); the list aliases buf + hist
-            uint32_t* idx_list = reinterpret_cast<uint32_t*>(buf);
-
-            if (clk) clk[1] = clock64();
-            // 2. stream the row once; keep entries >= tau
-            const float4* row4 = reinterpret_cast<const float4*>(row);
-            const int64_t n4 = n >> 2;
-            const int64_t step = kUnroll * static_cast<int64_t>(kThreads);
-            const int64_t n4r = (n4 + step - 1) / step * step;
-            const uint32_t cap = static_cast<uint32_t>(
-                min(L.cand_cap, 2 * L.buf_cap + kHistWords));  // idx list capacity
-            for (int64_t it = gtid(); it < n4r; it += step) {
-                float4 v[kUnroll];
-#pragma unroll
-                for (int u = 0; u < kUnroll; ++u) {
-                    const int64_t i4 = it + u * kThreads;
-                    v[u] = i4 < n4 ? __ldg(row4 + i4) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-                }
-                // one bit per entry: 4 * kUnroll bits (64-bit mask above 8 float4)
-                using Mask = typename std::conditional<(kUnroll > 8), unsigned long long, uint32_t>::type;
-                Mask m = 0;
-#pragma unroll
-                for (int u = 0; u < kUnroll; ++u) {
-                    m |= static_cast<Mask>(v[u].x >= tau_f ? 1u : 0u) << (4 * u + 0);
-                    m |= static_cast<Mask>(v[u].y >= tau_f ? 1u : 0u) << (4 * u + 1);
-                    m |= static_cast<Mask>(v[u].z >= tau_f ? 1u : 0u) << (4 * u + 2);
-                    m |= static_cast<Mask>(v[u].w >= tau_f ? 1u : 0u) << (4 * u + 3);
-                }
-                if (!__any_sync(0xffffffffu, m != 0)) continue;
-                const uint32_t c = kUnroll > 8 ? __popcll(m) : __popc(static_cast<uint32_t>(m));
-                uint32_t incl = c;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += t;
-                }
-                uint32_t base = 0;
-                if (lane == 31) base = atomicAdd(counter, incl);
-                base = __shfl_sync(0xffffffffu, base, 31);
-                uint32_t pos = base + incl - c;
-                // Survivors are ~6% of entries: walk only the set bits (the
-                // warp iterates max-popc times, usually 2-4) and record the
-                // column only: the divergent body stays a handful of
-                // instructions.
-                while (m != 0) {
-                    const int bit = kUnroll > 8 ? __ffsll(static_cast<long long>(m)) - 1
-                                                : __ffs(static_cast<int>(m)) - 1;
-                    m &= m - 1;
-                    if (pos < cap)
-                        idx_list[pos] = static_cast<uint32_t>(4 * (it + (bit >> 2) * kThreads) + (bit & 3));
-                    ++pos;
-                }
-            }
-            if (gtid() < 32) {  // the < 4 entries past the last float4
-                const int64_t i = 4 * n4 + lane;
-                const bool inb = i < n;
-                const uint32_t key = inb ? ord_key(__ldg(row + i)) : 0u;
-                const bool pass = inb && key >= tau;
-                const uint32_t mm = __ballot_sync(0xffffffffu, pass);
-                if (mm != 0) {
-                    uint32_t base = 0;
-                    if (lane == 0) base = atomicAdd(counter, __popc(mm));
-                    base = __shfl_sync(0xffffffffu, base, 0);
-                    const uint32_t pos = base + __popc(mm & ((1u << lane) - 1u));
-                    if (pass && pos < cap) idx_list[pos] = static_cast<uint32_t>(i);
-                }
-            }
-            csync();
-            const uint32_t total = *counter;
-            count = (total >= static_cast<uint32_t>(k) && total <= cap) ? static_cast<int>(total) : -1;
-            gather_candidates(row, idx_list, count, cand, hist, tau_f, res + 5, prebuilt, pb_lo, pb_scale);
+            const float tau_f = sample_threshold(row, n, k, L, hist, res, wsum, counter);
+            count = stream_collect<kUnroll>(row, n, k, tau_f, L, cand, buf, hist, res, counter, prebuilt, pb_lo,
+                                            pb_scale);
         }
 
         if (clk) clk[2] = clock64();
