@@ -50,10 +50,12 @@ def _inputs(B, S, T, k, seed, scale=1.0):
 
 
 @pytest.mark.parametrize("B,S,T,k", [(1, 4, 64, 16), (1, 8, 256, 64), (2, 5, 300, 100), (1, 12, 4096, 1024),
-                                     (1, 3, 8192, 2048), (2, 3, 5000, 4096)])
+                                     (1, 3, 8192, 2048), (2, 3, 5000, 4096), (1, 1, 10, 1), (3, 2, 40, 33),
+                                     (1, 400, 2048, 96)])
 def test_sparse_attention_matches_oracle(eng, B, S, T, k):
     q, kv, idx = _inputs(B, S, T, k, seed=B * 1000 + S * 10 + k)
-    idx[:, 0, k // 2:] = -1          # padding tail
+    if k > 1:
+        idx[:, 0, k // 2:] = -1      # padding tail
     if S > 2:
         idx[:, 1, :] = -1            # a query with no valid index
         idx[:, 2, 0] = T + 7         # out of range: skipped
