@@ -78,14 +78,15 @@ void load_inputs_device(const std::string& path, const ProblemDims& dims, const 
 // ------------------------------------------------------------ downstream
 // The consumer of the index list (the attention step the
 // reference leaves out): sparse MLA-style attention
-// of 128 query heads over the rows indices[b, t, 0:k] of one shared latent
-// KV head (576 dims, values = the first 512), on the calling thread's
-// engine and stream. Device pointers: q bf16 [B, S, 128, 576], kv bf16
-// [B, kv_len, 576], indices int32 [B, S, idx_ld] (-1 / out of range =
-// skipped), out bf16 [B, S, 128, 512], lse fp32 [B, S, 128] or null.
-// Throws invalid_argument for other shapes (csaidx_cuda_sparse_attention).
+// of `heads` (a multiple of 128) query heads over the rows indices[b, t, 0:k]
+// of one shared latent KV head (576 dims, values = the first 512), on the
+// calling thread's engine and stream. Device pointers: q bf16 [B, S, heads,
+// 576], kv bf16 [B, kv_len, 576], indices int32 [B, S, idx_ld] (-1 / out of
+// range = skipped), out bf16 [B, S, heads, 512], lse fp32 [B, S, heads] or
+// null. Throws invalid_argument for other shapes (csaidx_cuda_sparse_attention).
 void sparse_attention(const void* q, const void* kv, const int32_t* indices, int64_t batch, int64_t seq_len,
-                      int64_t kv_len, int64_t k, int64_t idx_ld, float sm_scale, void* out, float* lse);
+                      int64_t kv_len, int64_t heads, int64_t k, int64_t idx_ld, float sm_scale, void* out,
+                      float* lse);
 
 // ------------------------------------------------------------ multi-GPU
 // Query-sharded driver, one process (rank) per GPU. The reference runs the

@@ -230,9 +230,9 @@ int csaidx_cuda_select(csaidx_engine* e, const float* scores, int64_t batch, int
  * lse = -inf). One shared latent KV head (MQA, the sparse-MLA layout):
  * q bf16 [B, S, heads, dqk], kv bf16 [B, kv_len, dqk], indices int32
  * [B, S, idx_ld], out bf16 [B, S, heads, dv] (rows of out_ld >= dv), lse
- * fp32 [B, S, heads] or NULL. Compiled shape: heads = 128, dqk = 576,
- * dv = 512 (else CSAIDX_INVALID_ARGUMENT). tcgen05 kernel, two CTAs per
- * query (one per half of dv). */
+ * fp32 [B, S, heads] or NULL. Compiled shape: heads = a multiple of 128,
+ * dqk = 576, dv = 512 (else CSAIDX_INVALID_ARGUMENT). tcgen05 kernel, one
+ * work item per (query, group of 128 heads, half of dv). */
 int csaidx_cuda_sparse_attention(csaidx_engine* e, const void* q_bf16, const void* kv_bf16,
                                  const int32_t* indices, int64_t batch, int64_t seq_len,
                                  int64_t kv_len, int64_t heads, int64_t dqk, int64_t dv, int64_t k,

@@ -988,8 +988,9 @@ int csaidx_cuda_sparse_attention(csaidx_engine* e, const void* q_bf16, const voi
                                  int64_t dv, int64_t k, int64_t idx_ld, float sm_scale, void* out_bf16,
                                  int64_t out_ld, float* lse) {
     if (int rc = set_device(e)) return rc;
-    if (heads != 128 || dqk != 576 || dv != 512)
-        return fail(CSAIDX_INVALID_ARGUMENT, "sparse_attention: compiled for heads = 128, dqk = 576, dv = 512");
+    if (heads < 128 || heads % 128 != 0 || dqk != 576 || dv != 512)
+        return fail(CSAIDX_INVALID_ARGUMENT,
+                    "sparse_attention: compiled for heads = a multiple of 128, dqk = 576, dv = 512");
     if (batch < 1 || seq_len < 0 || kv_len < 1 || k < 1 || k > 4096 || idx_ld < k || out_ld < dv || (out_ld % 8) != 0)
         return fail(CSAIDX_INVALID_ARGUMENT,
                     "sparse_attention: bad extents (1 <= k <= 4096, idx_ld >= k, out_ld >= dv, out_ld %% 8 == 0)");
@@ -1018,6 +1019,7 @@ int csaidx_cuda_sparse_attention(csaidx_engine* e, const void* q_bf16, const voi
     p.kv_len = kv_len;
     p.batch = static_cast<int>(batch);
     p.k = static_cast<int>(k);
+    p.head_groups = static_cast<int>(heads / 128);
     p.sm_scale = sm_scale;
     LaunchScope ls(e, CSAIDX_KIND_ATTENTION);
     CSAIDX_CUDA_TRY(csaidx_kern::launch_sparse_mla(qmap, p, e->stream), "sparse_attention");

@@ -45,9 +45,10 @@ DeviceMemory device_memory() {
 void reset_device_peak() { detail::check(csaidx_engine_reset_peak(detail::engine())); }
 
 void sparse_attention(const void* q, const void* kv, const int32_t* indices, int64_t batch, int64_t seq_len,
-                      int64_t kv_len, int64_t k, int64_t idx_ld, float sm_scale, void* out, float* lse) {
-    detail::check(csaidx_cuda_sparse_attention(detail::engine(), q, kv, indices, batch, seq_len, kv_len, 128, 576, 512,
-                                               k, idx_ld, sm_scale, out, 512, lse));
+                      int64_t kv_len, int64_t heads, int64_t k, int64_t idx_ld, float sm_scale, void* out,
+                      float* lse) {
+    detail::check(csaidx_cuda_sparse_attention(detail::engine(), q, kv, indices, batch, seq_len, kv_len, heads, 576,
+                                               512, k, idx_ld, sm_scale, out, 512, lse));
 }
 
 }  // namespace gpu

@@ -187,7 +187,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     const int nb = (p.k + kBlk - 1) / kBlk;  // blocks per item
-    const int64_t nitems = 2 * p.seq_len * p.batch;  // (b, query, half of Dv)
+    const int G = p.head_groups;  // groups of 128 query heads
+    const int64_t nitems = 2 * p.seq_len * p.batch * G;  // (b, query, head group, half of Dv)
 
     if (threadIdx.x == 0) {
         mbar_init(q_full, 1);
@@ -212,13 +213,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = *tmem_slot;
 
     // Items are handed out round-robin: item = blockIdx.x + i * gridDim.x,
-    // (b, query, half) = decoded below. Every role walks the same sequence;
-    // barrier phases run on across items (block counter g = i * nb + j).
-    auto decode = [&](int64_t item, int& b, int64_t& tq, int& half) {
+    // (b, query, head group, half) = decoded below. Every role walks the same
+    // sequence; barrier phases run on across items (block counter g = i * nb
+    // + j). hrow = the item's first head row in the [B * S * H] q / out rows.
+    auto decode = [&](int64_t item, int& b, int64_t& tq, int& half, int64_t& hrow) {
         half = static_cast<int>(item & 1);
-        const int64_t qi = item >> 1;
+        const int64_t qg = item >> 1;
+        const int64_t qi = qg / G;
         b = static_cast<int>(qi / p.seq_len);
         tq = qi - static_cast<int64_t>(b) * p.seq_len;
+        hrow = qg * kH;  // ((b * S + tq) * G + hg) * 128
     };
 
     if (warp >= 4 && warp < 8) {
@@ -239,8 +243,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t g = 0, it = 0;
         for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x, ++it) {
             int b, half;
-            int64_t tq;
-            decode(item, b, tq, half);
+            int64_t tq, hrow;
+            decode(item, b, tq, half, hrow);
             // the item's k indices -> shared memory (row of the gather; -1 for
             // padding); idx_s is reused once the softmax has read every valid word
             const int32_t* idx_row = p.indices + (static_cast<int64_t>(b) * p.seq_len + tq) * p.idx_ld;
@@ -291,9 +295,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t it = 0;
         for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x, ++it) {
             int b, half;
-            int64_t tq;
-            decode(item, b, tq, half);
-            const int64_t qrow = (static_cast<int64_t>(b) * p.seq_len + tq) * kH;
+            int64_t tq, hrow;
+            decode(item, b, tq, half, hrow);
+            const int64_t qrow = hrow;
             const uint4* qsrc = reinterpret_cast<const uint4*>(p.q + (qrow + row) * kDqk);
             // warm L2 with this head's row while the previous item still owns Q
 #pragma unroll
@@ -385,8 +389,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t g = 0, it = 0;
         for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x, ++it) {
             int b, half;
-            int64_t tq;
-            decode(item, b, tq, half);
+            int64_t tq, hrow;
+            decode(item, b, tq, half, hrow);
             float m = ninf, l = 0.f;
             for (int j = 0; j < nb; ++j, ++g) {
                 const int s = g % kStages;
@@ -490,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const float inv_l = l > 0.f ? 1.f / l : 0.f;
             __nv_bfloat16* orow =
-                p.out + ((static_cast<int64_t>(b) * p.seq_len + tq) * kH + row) * p.out_ld + half * kDvHalf;
+                p.out + (hrow + row) * p.out_ld + half * kDvHalf;
 #pragma unroll 1
             for (int c0 = 0; c0 < kDvHalf; c0 += 32) {
                 float o[32];
@@ -511,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(o_free);  // the next item's first PV may overwrite O
             if (half == 0 && p.lse != nullptr)
-                p.lse[(static_cast<int64_t>(b) * p.seq_len + tq) * kH + row] =
+                p.lse[hrow + row] =
                     l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : ninf;
         }
     }

@@ -176,20 +176,21 @@ struct FinalizeParams {
 
 // ------------------------------------------------------------------ sparse attention (f4)
 // out[b,t,h,:Dv] = softmax over the valid indices[b,t,:] of
-// sm_scale * q[b,t,h,:] . kv[b,i,:], applied to kv[b,i,:Dv]; H = 128,
+// sm_scale * q[b,t,h,:] . kv[b,i,:], applied to kv[b,i,:Dv]; H = 128 g,
 // Dqk = 576, Dv = 512 (one shared latent KV head). q is read through a TMA
 // map built by the C-ABI entry, the gathered kv rows by cp.async.
 struct SparseMlaParams {
-    const __nv_bfloat16* q;  // [B, S, 128, 576]
+    const __nv_bfloat16* q;  // [B, S, H, 576]
     const __nv_bfloat16* kv; // [B, kv_len, 576]
     const int32_t* indices;  // [B, S, idx_ld], -1 = padding
     int64_t idx_ld;
-    __nv_bfloat16* out;      // [B, S, 128, out_ld]
+    __nv_bfloat16* out;      // [B, S, H, out_ld]
     int64_t out_ld;
-    float* lse;              // optional [B, S, 128]
+    float* lse;              // optional [B, S, H]
     int64_t seq_len, kv_len;
     int batch;
     int k;
+    int head_groups;         // H / 128
     float sm_scale;
 };
 

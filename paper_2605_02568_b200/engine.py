@@ -183,8 +183,8 @@ class Engine:
     # ------------------------------------------------ sparse attention (f4)
     def sparse_attention(self, q, kv, indices, sm_scale, out=None, lse=True):
         """Sparse MLA-style attention over indices [B, S, k] (int32, -1 = padding):
-        q bf16 [B, S, 128, 576], kv bf16 [B, T, 576] -> out bf16 [B, S, 128, 512]
-        (+ lse fp32 [B, S, 128]); csaidx_cuda_sparse_attention."""
+        q bf16 [B, S, H, 576] (H a multiple of 128), kv bf16 [B, T, 576] ->
+        out bf16 [B, S, H, 512] (+ lse fp32 [B, S, H]); csaidx_cuda_sparse_attention."""
         B, S, H, Dqk = q.shape
         T = kv.shape[1]
         k = indices.shape[-1]

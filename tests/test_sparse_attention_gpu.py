@@ -41,9 +41,9 @@ def _check(out, lse, q, kv, idx, sc):
     return float((err[live] / (rowmax[live] + 1e-30)).max())
 
 
-def _inputs(B, S, T, k, seed, scale=1.0):
+def _inputs(B, S, T, k, seed, scale=1.0, heads=H):
     g = torch.Generator(device="cuda").manual_seed(seed)
-    q = (torch.randn(B, S, H, DQK, device="cuda", generator=g) * scale).to(torch.bfloat16)
+    q = (torch.randn(B, S, heads, DQK, device="cuda", generator=g) * scale).to(torch.bfloat16)
     kv = torch.randn(B, T, DQK, device="cuda", generator=g).to(torch.bfloat16)
     idx = torch.argsort(torch.rand(B * S, T, device="cuda", generator=g), dim=1)[:, :k]
     return q, kv, idx.reshape(B, S, k).int().contiguous()
@@ -59,6 +59,18 @@ def test_sparse_attention_matches_oracle(eng, B, S, T, k):
     if S > 2:
         idx[:, 1, :] = -1            # a query with no valid index
         idx[:, 2, 0] = T + 7         # out of range: skipped
+    sc = DQK ** -0.5
+    out, lse = eng.sparse_attention(q, kv, idx, sc)
+    _check(out, lse, q, kv, idx, sc)
+
+
+@pytest.mark.parametrize("heads", [256, 384])
+def test_sparse_attention_head_groups(eng, heads):
+    """H a multiple of 128: one work item per group of 128 heads."""
+    B, S, T, k = 2, 5, 1000, 200
+    q, kv, idx = _inputs(B, S, T, k, seed=heads, heads=heads)
+    idx[:, 1, :] = -1
+    idx[:, 0, 150:] = -1
     sc = DQK ** -0.5
     out, lse = eng.sparse_attention(q, kv, idx, sc)
     _check(out, lse, q, kv, idx, sc)
