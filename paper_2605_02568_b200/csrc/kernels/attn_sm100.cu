@@ -10,36 +10,36 @@
 //
 // over the valid entries i_j of indices[b,t,:] (0 <= i_j < T; -1 = padding),
 // with one shared latent KV head (MQA): kv rows of Dqk = 576 (the first
-// Dv = 512 are also the values), H = 128 query heads, bf16 in / fp32
+// Dv = 512 are also the values), H = 128 g query heads, bf16 in / fp32
 // accumulate / bf16 out.
 //
-// B200 design (one CTA per (query, half of Dv), 1 CTA per SM by shared memory):
+// B200 design (work item = (query, group of 128 heads, half of Dv); one
+// persistent CTA per SM, shared memory and TMEM both full):
 //  * heads are the UMMA M dimension (128 TMEM lanes), so every softmax
 //    statistic of a head lives in one thread;
-//  * the QK^T product has few keys per block (N = 32), so with both operands
-//    in shared memory every MMA would re-read the 4 KiB Q slice for 1 KiB of
-//    keys (shared-memory bound at ~40% of the MMA rate; the first version,
-//    N = 16 from shared memory, ran at 0.22 of peak). Q therefore lives in
-//    TMEM as the A operand (tcgen05.mma ... [a_tmem]) for its first 384 dims
-//    (192 columns of packed bf16 pairs); the last 192 dims stay in shared
-//    memory (3 SW128 panels, TMA) because TMEM also holds O and S;
+//  * S = Q K^T per block of 32 keys (M = 128, N = 32, K = 576). Q's first 384
+//    dims are the TMEM A operand (tcgen05.mma ... [a_tmem], 192 columns of
+//    packed bf16 pairs), the last 192 stay in shared memory (3 SW128 panels,
+//    TMA). An M = 128 MMA costs >= ~46 cycles for any N < 128 (measured,
+//    profiles/r02_mma_floor.md), so the 36 QK instructions per block bound
+//    the kernel; wider blocks (N = 48 / 64) lost because shared memory then
+//    holds fewer gather stages (profiles/r02_attention.md);
 //  * the selected KV rows are gathered 32 per block by 128 producer threads
 //    with cp.async (16-byte pieces written straight into the SW128 K-major
 //    layout; completion tracked by the stage's mbarrier), 4 stages deep
-//    (TMA tile::gather4 — 4 rows x 128 B per instruction — was measured
-//    first: the 72 instructions per stage made the TMA unit the bottleneck);
-//  * S = Q K^T (M=128, N=32, K=576) into TMEM; the softmax warps read S
-//    (tcgen05.ld), keep the running max / sum in registers (exp2 domain,
-//    lazy rescale: O is only rescaled when the max grows by more than 2^8),
-//    and write P as packed bf16 over the S columns they just read
-//    (tcgen05.st) — P is the A operand of O += P V (A from TMEM, M=128,
-//    N=256, K=32), whose B operand is the same gathered KV tile read MN-major
-//    (no transpose copy);
-//  * O [128 x 256] fp32 stays in TMEM for the whole query; the two CTAs of a
-//    query each own half of Dv and both compute S (the QK product is
-//    duplicated: 65% of the issued MMA work is useful at Dqk = 576, Dv = 512).
+//    (TMA tile::gather4 — 4 rows x 128 B per instruction — is bound by the
+//    TMA unit's instruction rate);
+//  * the softmax warps read S (tcgen05.ld), keep the running max / sum in
+//    registers (exp2 domain, lazy rescale: O is only rescaled when the max
+//    grows by more than 2^8), and write P as packed bf16 over the S columns
+//    they just read (tcgen05.st) — P is the A operand of O += P V (A from
+//    TMEM, M = 128, N = 256, K = 32), whose B operand is the same gathered KV
+//    tile read MN-major (no transpose copy);
+//  * O [128 x 256] fp32 stays in TMEM for the whole item; the two items of a
+//    (query, head group) each own half of Dv and both compute S (65% of the
+//    issued MMA work is useful at Dqk = 576, Dv = 512).
 //    TMEM: Q 192 + O 256 + S/P 2 x 32 = 512 columns.
-// Persistent: one CTA per SM walks (b, query, half) items round-robin and
+// Persistent: one CTA per SM walks the items round-robin and
 // every barrier phase runs on across items, so the next item's Q staging,
 // gathers and first S MMAs overlap the current item's last softmax blocks and
 // epilogue (a CTA per item spent ~15K cycles per item in prologue / epilogue).
