@@ -43,11 +43,11 @@ def test_fp16_tile_matches_reference_rounding(orc):
     qt = torch.from_numpy(q).cuda().to(torch.bfloat16)
     kt = torch.from_numpy(kc).cuda().to(torch.bfloat16)
     wt = torch.from_numpy(w).cuda()
-    for s0, rows in [(0, 256), (512, 512)]:
-        out = e.score(qt, kt, wt, dims, s0, rows, 0, T, mode=MODE_FP16, kernel=KERNEL_TENSOR)
+    for s0, rows, t0, cols in [(0, 256, 0, T), (512, 512, 0, T), (101, 37, 16, 131)]:  # + a partial item
+        out = e.score(qt, kt, wt, dims, s0, rows, t0, cols, mode=MODE_FP16, kernel=KERNEL_TENSOR)
         e.check()
-        got = out[:, :, :T].cpu().numpy()
-        ref = orc.score_tile(q, kc, w, s0, 0, rows, T, fp16=True)
+        got = out[:, :, :cols].cpu().numpy()
+        ref = orc.score_tile(q, kc, w, s0, t0, rows, cols, fp16=True)
         same = got.view(np.uint32) == ref.view(np.uint32)
         assert same.mean() >= 0.99, same.mean()
         scale = _ulp16(np.abs(ref).max(axis=-1, keepdims=True))
