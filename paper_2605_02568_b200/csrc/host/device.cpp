@@ -146,6 +146,11 @@ int select_overlap_sms() {
     return v != nullptr ? std::atoi(v) : 0;
 }
 
+uint64_t key_tile_budget() {
+    const char* v = std::getenv("CSAIDX_KEY_TILE_BYTES");
+    return v != nullptr ? std::strtoull(v, nullptr, 10) : (uint64_t{2} << 30);
+}
+
 bool prefilter_enabled() {
     const char* v = std::getenv("CSAIDX_SELECT_PREFILTER");
     return v != nullptr && std::string(v) == "1";

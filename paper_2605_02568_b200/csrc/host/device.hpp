@@ -64,6 +64,9 @@ bool prefilter_enabled();
 int select_overlap_sms();
 // Two-level select for long rows (CSAIDX_TWO_LEVEL=1; default off).
 bool two_level_enabled();
+// Device score-tile budget for widening the key tile (CSAIDX_KEY_TILE_BYTES,
+// default 2 GiB; 0 keeps the requested c_T).
+uint64_t key_tile_budget();
 constexpr int64_t kPrefilterSampleTiles = 16;
 
 int kernel_code(ScoreKernel kernel, AccumulationMode mode);  // throws like resolve_score_kernel for unavailable kernels
@@ -126,6 +129,12 @@ struct ChunkPlan {
 };
 
 ChunkPlan plan_chunks(const ProblemDims& dims, const TileConfig& tile, const std::vector<int64_t>* starts);
+
+// Key tile the device runs for a plan (driver.cpp): the requested c_T, or a
+// multiple of it (up to T) that fits key_tile_budget() bytes of fp32 scores
+// when the results cannot depend on it. RunStats and ledger charges always
+// follow the requested tiles.
+int64_t physical_key_tile(const ProblemDims& dims, const DriverConfig& config, const ChunkPlan& plan);
 
 // Per-chunk callbacks around run_plan's main-lane work (used to overlap host
 // transfers of neighbouring chunks on the engine's copy lanes).

@@ -38,6 +38,22 @@ Clamped clamp(const ProblemDims& dims, const TileConfig& tile) {
 
 }  // namespace
 
+int64_t physical_key_tile(const ProblemDims& dims, const DriverConfig& config, const ChunkPlan& plan) {
+    // Under production semantics the final rows are the top-k_eff of every
+    // legal entry under one total order however the key range is split (the
+    // reference's chunked == materialize contract, test_driver.cpp), so the
+    // device widens the key tile up to the score-buffer budget: one score
+    // launch and one select per chunk instead of a select + merge per
+    // requested tile. Ablations and the boolean-mask tile keep the requested
+    // tiles (their results or charges depend on them).
+    const int64_t T = dims.key_blocks;
+    if (plan.ct >= T || config.ablation != Ablation::none || config.bool_mask_tile) return plan.ct;
+    const uint64_t per_tile = static_cast<uint64_t>(dims.batch * plan.cs * ((plan.ct + 3) / 4 * 4)) * sizeof(float);
+    const int64_t tiles = ceil_div(T, plan.ct);
+    const int64_t f = std::min<int64_t>(tiles, std::max<int64_t>(1, static_cast<int64_t>(key_tile_budget() / per_tile)));
+    return f >= tiles ? T : plan.ct * f;
+}
+
 ChunkPlan plan_chunks(const ProblemDims& dims, const TileConfig& tile, const std::vector<int64_t>* starts) {
     const Clamped c = clamp(dims, tile);
     ChunkPlan plan;
@@ -71,8 +87,9 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
     const int kcode = kernel_code(config.kernel, config.mode);
     const int mcode = mode_code(config.mode);
     const csaidx_dims cd = to_c(dims);
-    const int64_t ld = (plan.ct + 3) / 4 * 4;
-    const int64_t width_max = std::min(k, plan.ct);
+    const int64_t ct = physical_key_tile(dims, config, plan);
+    const int64_t ld = (ct + 3) / 4 * 4;
+    const int64_t width_max = std::min(k, ct);
 
     // Device working set, sized once for the largest tile and reused.
     DeviceBuffer scores(e, static_cast<size_t>(B * plan.cs * ld) * sizeof(float));
@@ -81,7 +98,7 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
     DeviceBuffer run_v(e, static_cast<size_t>(B * plan.cs * k) * 4);
     DeviceBuffer run_i(e, static_cast<size_t>(B * plan.cs * k) * 4);
     DeviceBuffer keep;
-    if (config.bool_mask_tile) keep = DeviceBuffer(e, static_cast<size_t>(plan.cs * plan.ct));
+    if (config.bool_mask_tile) keep = DeviceBuffer(e, static_cast<size_t>(plan.cs * ct));
 
     // Fused select pre-filter (csaidx_cuda.h): tensor-core tiles whose longest
     // legal row exceeds the candidate list. Same results as the plain select;
@@ -89,11 +106,11 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
     const int cap = csaidx_cuda_candidate_capacity(k);
     const bool prefilter = prefilter_enabled() && !config.bool_mask_tile && cap > 0 && ops.op_rows == 0 &&
                            csaidx_cuda_score_uses_tensor_cores(&cd, ops.dtype, mcode, kcode) != 0;
-    const int64_t tiles_max = ceil_div(plan.ct, 128);
+    const int64_t tiles_max = ceil_div(ct, 128);
     // per tile: stride = ceil(tiles / kPrefilterSampleTiles) -> at most
     // min(tiles, kPrefilterSampleTiles) sampled tiles
     const int64_t lds = std::min<int64_t>(tiles_max, kPrefilterSampleTiles) * 128;
-    const int64_t bits_ld = csaidx_cuda_candidate_words(plan.ct);
+    const int64_t bits_ld = csaidx_cuda_candidate_words(ct);
     DeviceBuffer pf_bits, pf_tau, pf_sample;
     if (prefilter) {
         pf_bits = DeviceBuffer(e, static_cast<size_t>(B * plan.cs * bits_ld) * sizeof(uint32_t));
@@ -110,17 +127,17 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
     // as they free up, the select lane first (stream priority), so each
     // kernel's tail is filled by the other's start.
     const int overlap_sms = select_overlap_sms();
-    const bool overlap = plan.ct >= T && !prefilter && !config.bool_mask_tile && plan.order.size() >= 2 &&
+    const bool overlap = ct >= T && !prefilter && !config.bool_mask_tile && plan.order.size() >= 2 &&
                          csaidx_cuda_score_uses_tensor_cores(&cd, ops.dtype, mcode, kcode) != 0 &&
                          (overlap_sms < 0 || (overlap_sms > 0 && csaidx_cuda_select_overlap_capable(k) != 0));
     // Two-level select (csaidx_cuda_score_gmax): when rows can span >= 4k
     // 32-key groups the score epilogue also writes each group's maximum, and
     // the select reads only the ~k groups that can hold a top-k score
     // (opt-in, CSAIDX_TWO_LEVEL=1: measured slower overall at C4).
-    const bool two_level = plan.ct >= T && !prefilter && !config.bool_mask_tile && two_level_enabled() &&
+    const bool two_level = ct >= T && !prefilter && !config.bool_mask_tile && two_level_enabled() &&
                            csaidx_cuda_score_uses_tensor_cores(&cd, ops.dtype, mcode, kcode) != 0 &&
-                           ceil_div(plan.ct, 32) >= 4 * k;
-    const int64_t gmax_ld = ceil_div(plan.ct, 32);
+                           ceil_div(ct, 32) >= 4 * k;
+    const int64_t gmax_ld = ceil_div(ct, 32);
     DeviceBuffer gmax_buf[2];  // double buffered like the score tiles when the select runs beside the score
     if (two_level)
         for (int i = 0; i < (overlap ? 2 : 1); ++i)
@@ -160,21 +177,40 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
         // all-sentinel buffer followed by the sentinel pass, so it writes the
         // output rows directly (csaidx_cuda_select_final) and the buffer is
         // only initialised if the tile ends up skipped.
-        const bool one_tile = plan.ct >= T;
+        const bool one_tile = ct >= T;
         bool finalized = false;
         if (!one_tile) check(csaidx_cuda_fill_sentinel(e, run_v.as<float>(), run_i.as<int32_t>(), B * rows * k));
         bool first = true;
-        for (int64_t t0 = 0; t0 < T; t0 += plan.ct) {
-            const int64_t cols = std::min(plan.ct, T - t0);
-            if (config.ablation == Ablation::a2_skip_narrow && cols < k) {
-                ++stats.tiles_skipped_narrow;
+        for (int64_t t0 = 0; t0 < T; t0 += ct) {
+            // The requested (logical) key tiles inside this physical one, with
+            // the reference's per-tile decisions and ledger charges in its
+            // order (driver.cpp:44-69); `end` closes the dispatched ones.
+            int64_t end = t0;
+            bool exited = false;
+            for (int64_t l0 = t0; l0 < std::min(T, t0 + ct); l0 += plan.ct) {
+                const int64_t lcols = std::min(plan.ct, T - l0);
+                if (config.ablation == Ablation::a2_skip_narrow && lcols < k) {
+                    ++stats.tiles_skipped_narrow;
+                    continue;
+                }
+                if (config.causal_early_exit && tile_fully_masked(s0, rows, l0, dims.ratio)) {
+                    stats.tiles_skipped_masked += ceil_div(T - l0, plan.ct);
+                    exited = true;
+                    break;
+                }
+                LedgerCharge tile_charge(ledger, "score_tile", chunk_tile_bytes(B, rows, lcols));
+                if (config.bool_mask_tile) {
+                    LedgerCharge mask_charge(ledger, "mask_tile", static_cast<uint64_t>(rows) * static_cast<uint64_t>(lcols));
+                }
+                LedgerCharge scratch_charge(ledger, "tile_topk_scratch", tile_scratch_bytes(B, rows, lcols, k));
+                ++stats.dispatch_count;
+                end = l0 + lcols;
+            }
+            if (end == t0) {
+                if (exited) break;
                 continue;
             }
-            if (config.causal_early_exit && tile_fully_masked(s0, rows, t0, dims.ratio)) {
-                stats.tiles_skipped_masked += ceil_div(T - t0, plan.ct);
-                break;
-            }
-            LedgerCharge tile_charge(ledger, "score_tile", chunk_tile_bytes(B, rows, cols));
+            const int64_t cols = end - t0;
             const int64_t legal_max = std::min(cols, (s0 + rows) / dims.ratio - t0);
             const bool filtered = prefilter && legal_max > cap;
             if (filtered) {
@@ -189,7 +225,6 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
             } else if (config.bool_mask_tile) {
                 check(csaidx_cuda_score_rows(e, ops.q, ops.kc, ops.dtype, ops.w, &cd, s0, rows, t0, cols, mcode, kcode,
                                              0, sbuf, ld, op_rows, op_row0));
-                LedgerCharge mask_charge(ledger, "mask_tile", static_cast<uint64_t>(rows) * static_cast<uint64_t>(cols));
                 check(csaidx_cuda_bool_mask(e, keep.as<uint8_t>(), s0, t0, rows, cols, dims.ratio));
                 check(csaidx_cuda_apply_bool_mask(e, sbuf, ld, keep.as<uint8_t>(), B, rows, cols));
             } else if (two_level) {
@@ -199,9 +234,7 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
                 check(csaidx_cuda_score_rows(e, ops.q, ops.kc, ops.dtype, ops.w, &cd, s0, rows, t0, cols, mcode, kcode,
                                              1, sbuf, ld, op_rows, op_row0));
             }
-            ++stats.dispatch_count;
             const int64_t width = std::min(k, cols);
-            LedgerCharge scratch_charge(ledger, "tile_topk_scratch", tile_scratch_bytes(B, rows, cols, k));
             const bool overwrite = config.ablation == Ablation::a1_no_merge;
             auto select = [&](float* v, int32_t* i, int64_t out_ld) {
                 if (filtered)
@@ -233,6 +266,7 @@ void run_plan(csaidx_engine* e, const DeviceOps& ops, const ProblemDims& dims, c
                                         cand_i.as<int32_t>(), width, width, overwrite ? 1 : 0, 0));
             }
             first = false;
+            if (exited) break;
         }
         if (!finalized) {
             if (one_tile) check(csaidx_cuda_fill_sentinel(e, run_v.as<float>(), run_i.as<int32_t>(), B * rows * k));

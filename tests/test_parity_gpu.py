@@ -42,6 +42,15 @@ def gold():
     return np.load(GOLDEN)
 
 
+@pytest.fixture(params=["fused", "requested"])
+def key_tiles(request, monkeypatch):
+    """Run a test with the device's widened key tile (default) and with the
+    requested c_T kept (CSAIDX_KEY_TILE_BYTES=0: select + merge per tile)."""
+    if request.param == "requested":
+        monkeypatch.setenv("CSAIDX_KEY_TILE_BYTES", "0")
+    return request.param
+
+
 def bits(a):
     return np.ascontiguousarray(a, np.float32).view(np.uint32)
 
@@ -52,7 +61,7 @@ def inputs_for(orc, B, S, m, H, D, k, seed, bf16=False):
     return api.IndexerInputs.validated(q, kc, w, dims), dims, (q, kc, w)
 
 
-def test_golden_driver_cases_bit_exact(orc, gold):
+def test_golden_driver_cases_bit_exact(orc, gold, key_tiles):
     for n, (B, S, m, H, D, k, seed, cs, ct, fp16, abl, ee, bm) in enumerate(gold["drv_cases"]):
         inputs, dims, _ = inputs_for(orc, int(B), int(S), int(m), int(H), int(D), int(k), int(seed))
         cfg = api.DriverConfig(tile=api.TileConfig(int(cs), int(ct)), mode=api.AccumulationMode(int(fp16)),
@@ -94,7 +103,7 @@ def c1(orc):
 
 
 @pytest.mark.parametrize("cs,ct", [(256, 256), (2048, 8192), (4096, 1024), (100, 300)])
-def test_c1_parity_against_oracle(c1, cs, ct):
+def test_c1_parity_against_oracle(c1, cs, ct, key_tiles):
     inputs, dims, full = c1
     res, st = api.run_chunked(inputs, dims, api.DriverConfig(tile=api.TileConfig(cs, ct)))
     legal = (np.arange(4096) + 1) // 4
@@ -105,7 +114,7 @@ def test_c1_parity_against_oracle(c1, cs, ct):
         if t0 < (min(s0 + cs, 4096)) // 4)
 
 
-def test_c1_chunked_equals_materialize_bitwise(c1):
+def test_c1_chunked_equals_materialize_bitwise(c1, key_tiles):
     inputs, dims, _ = c1
     ref, st = api.run_materialize(inputs, dims)
     for cs, ct in [(256, 256), (4096, 1024), (333, 77)]:
@@ -115,6 +124,32 @@ def test_c1_chunked_equals_materialize_bitwise(c1):
     via, stats = api.dispatch(inputs, dims)
     assert stats.path == api.ExecutionPath.materialize  # 4096*64*1024*4 = 2^30 <= threshold
     assert np.array_equal(via.indices, ref.indices)
+
+
+@pytest.mark.parametrize("budget", ["0", str(1 << 20), str(3 << 19), str(2 << 20), str(64 << 20)])
+@pytest.mark.parametrize("early_exit", [True, False])
+def test_widened_key_tiles_keep_results_stats_and_ledger(orc, monkeypatch, budget, early_exit):
+    """physical_key_tile (driver.cpp): the device key tile widened to 2x /
+    3x / 4x of the requested one (budgets over 512 KiB score tiles, the last
+    physical tile ragged) or to all of T gives the same rows, RunStats and
+    ledger peak as the requested tiling, on both kernel families at B = 2;
+    the exact-order shape also bit-exact against the oracle."""
+    for (B, S, m, H, D, k, bf16) in [(2, 3000, 4, 64, 128, 96, True), (2, 2500, 1, 2, 3, 200, False)]:
+        inputs, dims, (q, kc, w) = inputs_for(orc, B, S, m, H, D, k, 7, bf16=bf16)
+        cfg = api.DriverConfig(tile=api.TileConfig(512, 128), causal_early_exit=early_exit)
+        monkeypatch.setenv("CSAIDX_KEY_TILE_BYTES", "0")
+        ref, rst = api.run_chunked(inputs, dims, cfg)
+        monkeypatch.setenv("CSAIDX_KEY_TILE_BYTES", budget)
+        got, gst = api.run_chunked(inputs, dims, cfg)
+        assert np.array_equal(got.indices, ref.indices)
+        assert np.array_equal(bits(got.values), bits(ref.values))
+        assert (gst.dispatch_count, gst.tiles_skipped_masked, gst.tiles_skipped_narrow, gst.ledger_peak_bytes) == \
+            (rst.dispatch_count, rst.tiles_skipped_masked, rst.tiles_skipped_narrow, rst.ledger_peak_bytes)
+        if not bf16:
+            rc, idx, val, st3 = orc.run_chunked(q, kc, w, m, k, 512, 128, early_exit=early_exit)
+            assert rc == 0
+            assert np.array_equal(got.indices, idx) and np.array_equal(bits(got.values), bits(val))
+            assert [gst.dispatch_count, gst.tiles_skipped_masked, gst.tiles_skipped_narrow] == list(st3)
 
 
 def test_chunk_subset_entry_matches_full_run(c1):
@@ -529,7 +564,7 @@ def test_tensor_core_path_at_max_k_matches_reference_rule(orc):
 
 
 @pytest.mark.parametrize("k,cs,ct", [(5000, 1024, 10 ** 6), (5000, 512, 2048), (9000, 4096, 3000), (20000, 8192, 10 ** 6)])
-def test_k_above_shared_capacity_bit_exact(orc, k, cs, ct):
+def test_k_above_shared_capacity_bit_exact(orc, k, cs, ct, key_tiles):
     """the drop-in accepts any k like the reference's
     tile_topk / merge_topk (topk.cpp:105-172). Exact-order kernel shapes, so
     indices, values and RunStats are bit-exact against the oracle — through
