@@ -3,6 +3,9 @@ c_S in {512..8192}, c_T in {4096..T}, k in {256, 512, 1024, 2048}.
 
 For every point: device-timed step (CUDA events, warm-up first), legal
 pairs/s, the reference ledger's transient peak and the device high-water.
+Points with c_T < T are also timed with the device key tile held at c_T
+(CSAIDX_KEY_TILE_BYTES=0): `ms` is the default (widened key tile),
+`ms_key_tile_as_requested` the select + merge per requested tile.
 Recall: every point's output must equal, byte for byte, the (c_S=2048,
 c_T=T) run of the same k (score values do not depend on the tiling and the
 merge is exact), and that run is held to the north-star rule
@@ -45,6 +48,7 @@ dims_k = {}
 for k in (256, 512, 1024, 2048):
     dims = api.ProblemDims.create(B, S, m, H, D, k)
     ref = None
+    ref_bytes = 0
     for cs in (2048, 512, 1024, 4096, 8192):
         for ct in (T, 4096, 8192, 16384):
             cfg = api.DriverConfig(tile=api.TileConfig(cs, ct))
@@ -59,9 +63,12 @@ for k in (256, 512, 1024, 2048):
             ms = ev0.elapsed_time(ev1)
             line = {"k": k, "c_S": cs, "c_T": ct, "ms": round(ms, 3), "legal_pairs_per_s": pairs / (ms / 1e3),
                     "dispatch_count": st.dispatch_count, "ledger_peak_bytes": st.ledger_peak_bytes,
-                    "device_peak_gb": round((torch.cuda.max_memory_allocated() + st.device_peak_bytes) / 1e9, 3)}
+                    # the held reference rows (ref) are not part of this run's working set
+                    "device_peak_gb": round((torch.cuda.max_memory_allocated() - ref_bytes + st.device_peak_bytes) / 1e9,
+                                            3)}
             if ref is None:
                 ref = (idx.clone(), val.clone())
+                ref_bytes = idx.numel() * idx.element_size() + val.numel() * val.element_size()
                 hi, hv = idx.cpu().numpy(), val.cpu().numpy()
                 recall = []
                 for b in range(B):
@@ -75,5 +82,22 @@ for k in (256, 512, 1024, 2048):
             else:
                 line["equal_to_reference_tiling"] = bool(torch.equal(idx, ref[0]) and
                                                          torch.equal(val.view(torch.int32), ref[1].view(torch.int32)))
+            if ct < T:
+                # the same point with the device key tile held at c_T (select +
+                # merge per requested tile, driver.cpp physical_key_tile)
+                os.environ["CSAIDX_KEY_TILE_BYTES"] = "0"
+                api.run_chunked_device(q, kc, w, dims, cfg)
+                torch.cuda.synchronize()
+                ev0.record()
+                idx2, val2, st2 = api.run_chunked_device(q, kc, w, dims, cfg)
+                ev1.record()
+                torch.cuda.synchronize()
+                del os.environ["CSAIDX_KEY_TILE_BYTES"]
+                line["ms_key_tile_as_requested"] = round(ev0.elapsed_time(ev1), 3)
+                line["as_requested_equal"] = bool(torch.equal(idx2, idx) and
+                                                  torch.equal(val2.view(torch.int32), val.view(torch.int32)) and
+                                                  st2.dispatch_count == st.dispatch_count and
+                                                  st2.ledger_peak_bytes == st.ledger_peak_bytes)
+                del idx2, val2
             print(json.dumps(line), flush=True)
             del idx, val
