@@ -1022,7 +1022,14 @@ int csaidx_cuda_sparse_attention(csaidx_engine* e, const void* q_bf16, const voi
     p.head_groups = static_cast<int>(heads / 128);
     p.sm_scale = sm_scale;
     LaunchScope ls(e, CSAIDX_KIND_ATTENTION);
-    CSAIDX_CUDA_TRY(csaidx_kern::launch_sparse_mla(qmap, p, e->stream), "sparse_attention");
+    // CTA-pair kernel by default (Dqk split across the pair); CSAIDX_ATTN_PAIR=0
+    // runs the single-CTA kernel (both halves of Dv compute all of S)
+    const char* pv = getenv("CSAIDX_ATTN_PAIR");
+    const bool pair = pv == nullptr || pv[0] != '0';
+    if (pair)
+        CSAIDX_CUDA_TRY(csaidx_kern::launch_sparse_mla_pair(p, e->stream), "sparse_attention");
+    else
+        CSAIDX_CUDA_TRY(csaidx_kern::launch_sparse_mla(qmap, p, e->stream), "sparse_attention");
     return CSAIDX_OK;
 }
 

@@ -19,6 +19,14 @@ pytestmark = pytest.mark.gpu
 H, DQK, DV = 128, 576, 512
 
 
+@pytest.fixture(autouse=True, params=["pair", "single"])
+def kernel_form(request, monkeypatch):
+    """Every case on both kernels: the CTA-pair form (default; Dqk split
+    across a cluster of 2) and the single-CTA form (CSAIDX_ATTN_PAIR=0)."""
+    monkeypatch.setenv("CSAIDX_ATTN_PAIR", "1" if request.param == "pair" else "0")
+    return request.param
+
+
 @pytest.fixture(scope="module")
 def eng():
     from paper_2605_02568_b200.engine import Engine
