@@ -48,9 +48,12 @@ constexpr int kMaxK = 4096;
 constexpr int kIdxOffset = kStages * kKvStageBytes;
 constexpr int kXchgSlotBytes = kH * kBlk * 4;               // 16 KiB
 constexpr int kXchgOffset = kIdxOffset + kMaxK * 4;
-constexpr int kBarOffset = kXchgOffset + 2 * kXchgSlotBytes;
-constexpr int kSmemBytes = kBarOffset + 512 + 1024;
-constexpr int kThreads = 416;
+constexpr int kRedOffset = kXchgOffset + 2 * kXchgSlotBytes;  // row maxima [2][2][128] + row sums [2][128]
+constexpr int kBarOffset = kRedOffset + 3072;
+constexpr int kSmemBytes = kBarOffset + 1024 + 1024;
+constexpr int kSmWarps = 8;                // softmax warps: 2 per TMEM lane quarter, 16 keys of a block each
+constexpr int kCols = kBlk / 2;
+constexpr int kThreads = 544;              // 8 softmax + 4 KV producer + 1 MMA + 4 Q-staging warps
 constexpr int kProducers = 128;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColQ = 0, kColO = 192;
@@ -62,6 +65,17 @@ __device__ __forceinline__ uint32_t s_col(uint32_t g) {
     return i == 0 ? 448u : (i == 1 ? 480u : 144u);  // 144..175 lie past Q's 144 columns
 }
 constexpr float kRescaleLog2 = 8.0f;
+#ifndef CSAIDX_ATTN_PROBE
+#define CSAIDX_ATTN_PROBE 0  // (dev) clock64 stamps of CTA 0's softmax warp 0 and MMA issuer per block
+#endif
+#if CSAIDX_ATTN_PROBE
+constexpr int kProbeBlocks = 2048;
+__device__ long long g_attn_probe[kProbeBlocks * 8];
+#define PROBE(slot) \
+    if (blockIdx.x == 0 && g < kProbeBlocks) g_attn_probe[g * 8 + (slot)] = clock64();
+#else
+#define PROBE(slot)
+#endif
 #ifndef CSAIDX_PAIR_DBG
 #define CSAIDX_PAIR_DBG 0  // (dev timing only) 1: no exchange at all, 2: send but never wait for the peer
 #endif
@@ -94,6 +108,12 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
         "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
         "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
         : "memory");
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
 }
 
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -204,9 +224,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* q_free = q_tmem + 1;               // [1]
     uint64_t* o_free = q_free + 1;               // [1]
     uint64_t* vw_free = o_free + 1;              // [kStages]
-    uint64_t* x_full = vw_free + kStages;        // [2][4] the peer's partial landed (tx bytes)
-    uint64_t* x_free = x_full + 8;               // [2][4] the peer has read my partial
-    uint32_t* valid_w = reinterpret_cast<uint32_t*>(x_free + 8);  // [kStages]
+    uint64_t* x_full = vw_free + kStages;        // [2][kSmWarps] the peer's partial landed (tx bytes)
+    uint64_t* x_free = x_full + 2 * kSmWarps;    // [2][kSmWarps] the peer has read my partial
+    uint32_t* valid_w = reinterpret_cast<uint32_t*>(x_free + 2 * kSmWarps);  // [kStages]
+    float* mx_s = reinterpret_cast<float*>(smem + kRedOffset);  // [2 blocks][2 halves][128 heads]
+    float* l_s = mx_s + 4 * kH;                                  // [2 halves][128 heads]
     uint32_t* tmem_slot = valid_w + kStages;
 
     const int warp = threadIdx.x / 32;
@@ -222,22 +244,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&kv_full[s], kProducers + 1);
             mbar_init(&kv_empty[s], 1);
-            mbar_init(&vw_free[s], 4);
+            mbar_init(&vw_free[s], kSmWarps);
         }
         for (int s = 0; s < kSSlots; ++s) {
             mbar_init(&s_full[s], 1);
-            mbar_init(&p_full[s], 4);
+            mbar_init(&p_full[s], kSmWarps);
         }
         mbar_init(q_tmem, 4);
         mbar_init(q_free, 1);
-        mbar_init(o_free, 4);
-        for (int i = 0; i < 8; ++i) {
+        mbar_init(o_free, kSmWarps);
+        for (int i = 0; i < 2 * kSmWarps; ++i) {
             mbar_init(&x_full[i], 1);
             mbar_init(&x_free[i], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 8) tmem_alloc<kTmemCols>(tmem_slot);
+    if (warp == 12) tmem_alloc<kTmemCols>(tmem_slot);
     tc_fence_before();
     cluster_sync_all();  // barriers of both CTAs initialised before any remote traffic
     tc_fence_after();
@@ -250,9 +272,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         hrow = item * kH;  // ((b * S + tq) * G + hg) * 128
     };
 
-    if (warp >= 4 && warp < 8) {
+    if (warp >= 8 && warp < 12) {
         // ---------------------------------------------------------- KV producers
-        const int pt = threadIdx.x - 128;
+        const int pt = threadIdx.x - 256;
         constexpr int kPieces = (kBlk * kCtaPanels * 8) / kProducers;  // 10
         static_assert(kProducers == 4 * kBlk, "4 producer threads per gathered row");
         const int r = pt >> 2;
@@ -282,7 +304,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int32_t myidx = idx_s[j * kBlk + r];
                 const char* src = kv_b + static_cast<int64_t>(myidx >= 0 ? myidx : 0) * (kDqk * 2);
                 uint32_t vmask = 0;
-                if (warp == 4) vmask = __ballot_sync(0xffffffffu, idx_s[j * kBlk + lane] >= 0);
+                if (warp == 8) vmask = __ballot_sync(0xffffffffu, idx_s[j * kBlk + lane] >= 0);
                 mbar_wait(&kv_empty[s], ((g / kStages) & 1) ^ 1);
                 asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 1) : "memory");
                 if (pt == 0) {
@@ -300,7 +322,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                              : "memory");
             }
         }
-    } else if (warp >= 9) {
+    } else if (warp >= 13) {
         // ---------------------------------------------------------- Q stagers
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
@@ -342,7 +364,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(q_tmem);
         }
-    } else if (warp == 8) {
+    } else if (warp == 12) {
         // ---------------------------------------------------------- MMA issuer
         if (elect_one()) {
             const uint32_t kv_base = smem_u32(kv_smem);
@@ -362,11 +384,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const int s = gj % kStages;
                     if (j == 0 && it > 0) mbar_wait(o_free, (it - 1) & 1);
                     mbar_wait(&p_full[gj % kSSlots], (gj / kSSlots) & 1);
+                    {
+                        const uint32_t g = gj;
+                        PROBE(5)
+                    }
                     tc_fence_after();
                     const uint32_t vb = kv_base + s * kKvStageBytes;  // V = local panels 0..3
 #pragma unroll
                     for (int kk = 0; kk < kBlk / 16; ++kk)
-                        umma_bf16_ts(tmem + kColO, tmem + s_col(gj) + kk * 8,
+                        umma_bf16_ts(tmem + kColO, tmem + s_col(gj) + kk * 16,
                                      sw128_mnmajor_desc(vb + kk * 2048, kKvPanelBytes, 1024), kIdescPV,
                                      (j > 0 || kk > 0) ? 1u : 0u);
                     umma_commit(&kv_empty[s]);
@@ -374,6 +400,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 auto issue_qk = [&](int j, uint32_t gj) {
                     const int s = gj % kStages;
                     mbar_wait(&kv_full[s], (gj / kStages) & 1);
+                    {
+                        const uint32_t g = gj;
+                        PROBE(4)
+                    }
                     fence_proxy_async();
                     tc_fence_after();
                     const uint32_t st = kv_base + s * kKvStageBytes;
@@ -399,34 +429,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
     } else {
         // ---------------------------------------------------------- softmax + epilogue
-        const int row = warp * 32 + lane;
-        const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+        // warp = (half of the block's keys hf, TMEM lane quarter): the pair of
+        // warps of a quarter share the row max through shared memory each
+        // block and the row sum at the end
+        const int quarter = warp & 3, hf = warp >> 2;
+        const int row = quarter * 32 + lane;
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
         const float scale_log2 = p.sm_scale * 1.4426950408889634f;
         const float ninf = -INFINITY;
-        // exchange addresses: my partial goes to the peer's slot, chunk-major
-        // [chunk][head] x 16 B (conflict-free both ways)
+        auto pair_sync = [&] {  // the two warps of this quarter
+            tc_fence_before();
+            asm volatile("bar.sync %0, 64;" ::"r"(2 + quarter) : "memory");
+            tc_fence_after();
+        };
+        // exchange: my 16 columns of the partial go to the peer's slot,
+        // chunk-major [chunk][head] x 16 B (conflict free both ways)
         const uint32_t x_local = smem_u32(xchg);
         const uint32_t x_peer = peer_addr(x_local, peer);
-        // peer's x_full (I complete its tx) / x_free (I release its slot), per slot
         const uint32_t xf_peer0 = peer_addr(smem_u32(&x_full[warp]), peer);
-        const uint32_t xf_peer1 = peer_addr(smem_u32(&x_full[4 + warp]), peer);
+        const uint32_t xf_peer1 = peer_addr(smem_u32(&x_full[kSmWarps + warp]), peer);
         const uint32_t xr_peer0 = peer_addr(smem_u32(&x_free[warp]), peer);
-        const uint32_t xr_peer1 = peer_addr(smem_u32(&x_free[4 + warp]), peer);
-        // own partial of block gs: wait for it, read it and st.async it to the
-        // peer's exchange slot (after the peer released that slot), and post
-        // the receive of the peer's partial of the same block
-        auto send = [&](uint32_t gs, float (&y)[kBlk]) {
+        const uint32_t xr_peer1 = peer_addr(smem_u32(&x_free[kSmWarps + warp]), peer);
+        const uint32_t xoff = ((4 * hf) * kH + row) * 16;  // first chunk of this warp's columns
+        // own partial of block gs: read it, st.async it to the peer (after the
+        // peer released the slot), post the receive of the peer's partial
+        auto send = [&](uint32_t gs, float (&y)[kCols]) {
             const int sl = static_cast<int>(gs & 1);
             mbar_wait(&s_full[gs % kSSlots], (gs / kSSlots) & 1);
             tc_fence_after();
-            tmem_ld32(lane_base + s_col(gs), y);
-            if (lane == 0) mbar_expect_tx(&x_full[sl * 4 + warp], 32 * kBlk * 4);
+            tmem_ld16(lane_base + s_col(gs) + hf * kCols, y);
+            if (lane == 0) mbar_expect_tx(&x_full[sl * kSmWarps + warp], 32 * kCols * 4);
             tmem_ld_wait();
             if (CSAIDX_PAIR_DBG == 1) return;
-            if (CSAIDX_PAIR_DBG == 0) mbar_wait_cluster(&x_free[sl * 4 + warp], ((gs >> 1) & 1) ^ 1);
+            if (CSAIDX_PAIR_DBG == 0) mbar_wait_cluster(&x_free[sl * kSmWarps + warp], ((gs >> 1) & 1) ^ 1);
 #pragma unroll
-            for (int q = 0; q < kBlk / 4; ++q)
-                st_async_v4(x_peer + sl * kXchgSlotBytes + (q * kH + row) * 16, y[4 * q], y[4 * q + 1], y[4 * q + 2],
+            for (int q = 0; q < kCols / 4; ++q)
+                st_async_v4(x_peer + sl * kXchgSlotBytes + xoff + q * kH * 16, y[4 * q], y[4 * q + 1], y[4 * q + 2],
                             y[4 * q + 3], sl ? xf_peer1 : xf_peer0);
         };
         uint32_t g = 0;
@@ -434,28 +472,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int b;
             int64_t tq, hrow;
             decode(item, b, tq, hrow);
-            float m = ninf, l = 0.f;
-            float nxt[kBlk];
+            float m = ninf, l = 0.f;  // l: this warp's keys only (same m in both warps)
+            float nxt[kCols];
             send(g, nxt);
             for (int j = 0; j < nb; ++j, ++g) {
                 const int s = g % kStages;
                 const int sl = static_cast<int>(g & 1);
-                float x[kBlk];
+                float x[kCols];
+                if (warp == 0 && lane == 0) { PROBE(0) }
 #pragma unroll
-                for (int c = 0; c < kBlk; ++c) x[c] = nxt[c];
+                for (int c = 0; c < kCols; ++c) x[c] = nxt[c];
                 if (j + 1 < nb) send(g + 1, nxt);  // overlaps the exchange with this block's softmax
+                if (warp == 0 && lane == 0) { PROBE(1) }
                 mbar_wait(&kv_full[s], (g / kStages) & 1);  // completed: orders the valid word
                 uint32_t vm = 0;
                 if (lane == 0) {
                     vm = valid_w[s];
                     mbar_arrive(&vw_free[s]);
                 }
-                vm = __shfl_sync(0xffffffffu, vm, 0);
+                vm = (__shfl_sync(0xffffffffu, vm, 0) >> (kCols * hf)) & 0xffffu;
                 // the peer's partial -> S = S_0 + S_1 (same bits in both CTAs)
-                if (CSAIDX_PAIR_DBG == 0) mbar_wait_cluster(&x_full[sl * 4 + warp], (g >> 1) & 1);
+                if (CSAIDX_PAIR_DBG == 0) mbar_wait_cluster(&x_full[sl * kSmWarps + warp], (g >> 1) & 1);
+                if (warp == 0 && lane == 0) { PROBE(2) }
 #pragma unroll
-                for (int q = 0; q < kBlk / 4 && CSAIDX_PAIR_DBG != 1; ++q) {
-                    const float4 v = *reinterpret_cast<const float4*>(xchg + sl * kXchgSlotBytes + (q * kH + row) * 16);
+                for (int q = 0; q < kCols / 4 && CSAIDX_PAIR_DBG != 1; ++q) {
+                    const float4 v = *reinterpret_cast<const float4*>(xchg + sl * kXchgSlotBytes + xoff + q * kH * 16);
                     x[4 * q] += v.x;
                     x[4 * q + 1] += v.y;
                     x[4 * q + 2] += v.z;
@@ -463,17 +504,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
                 __syncwarp();
                 if (lane == 0 && CSAIDX_PAIR_DBG == 0) remote_arrive(sl ? xr_peer1 : xr_peer0);  // the peer may refill my slot
-                if (vm != 0xffffffffu) {
+                if (vm != 0xffffu) {
 #pragma unroll
-                    for (int c = 0; c < kBlk; ++c) x[c] = ((vm >> c) & 1u) ? x[c] : ninf;
+                    for (int c = 0; c < kCols; ++c) x[c] = ((vm >> c) & 1u) ? x[c] : ninf;
                 }
-                float t3[11];
-#pragma unroll
-                for (int c = 0; c < 10; ++c) t3[c] = max3f(x[3 * c], x[3 * c + 1], x[3 * c + 2]);
-                t3[10] = fmaxf(x[30], x[31]);
-                const float mx = max3f(max3f(max3f(t3[0], t3[1], t3[2]), max3f(t3[3], t3[4], t3[5]),
-                                             max3f(t3[6], t3[7], t3[8])),
-                                       t3[9], t3[10]) * scale_log2;
+                const float mh = max3f(max3f(max3f(x[0], x[1], x[2]), max3f(x[3], x[4], x[5]), max3f(x[6], x[7], x[8])),
+                                       max3f(max3f(x[9], x[10], x[11]), max3f(x[12], x[13], x[14]), x[15]), ninf);
+                mx_s[(sl * 2 + hf) * kH + row] = mh;
+                pair_sync();
+                const float mx = fmaxf(mh, mx_s[(sl * 2 + (hf ^ 1)) * kH + row]) * scale_log2;
                 float alpha = 1.f;
                 bool rescale = false;
                 if (mx > m) {
@@ -487,11 +526,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                 }
                 if (__any_sync(0xffffffffu, rescale)) {
-                    // PV of block g-1 landed (exact parity wait: attn_sm100.cu)
+                    // PV of block g-1 landed (exact parity wait: attn_sm100.cu);
+                    // each warp of the quarter rescales its half of O's columns
                     mbar_wait(&kv_empty[(g - 1) % kStages], ((g - 1) / kStages) & 1);
                     tc_fence_after();
 #pragma unroll 1
-                    for (int c0 = 0; c0 < kDvHalf; c0 += 32) {
+                    for (int c0 = hf * (kDvHalf / 2); c0 < (hf + 1) * (kDvHalf / 2); c0 += 32) {
                         float o[32];
                         tmem_ld32(lane_base + kColO + c0, o);
                         tmem_ld_wait();
@@ -501,16 +541,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                     tmem_st_wait();
                 }
-                uint32_t pk[kBlk / 2];
-                float sum = 0.f;
+                uint32_t pk[kCols / 2];
                 if (m != ninf) {
                     const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m, -m);
                     float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-                    for (int c = 0; c < kBlk; c += 2) {
+                    for (int c = 0; c < kCols; c += 2) {
                         const float2 a = __ffma2_rn(make_float2(x[c], x[c + 1]), sc2, nm2);
                         float2 pr;
-                        if (c < kBlk / 2) {
+                        if (c < kCols / 2) {
                             pr.x = ex2(a.x);
                             pr.y = ex2(a.y);
                         } else {
@@ -520,24 +559,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         const __nv_bfloat162 h2 = __floats2bfloat162_rn(pr.x, pr.y);
                         pk[c / 2] = *reinterpret_cast<const uint32_t*>(&h2);
                     }
-                    sum = acc.x + acc.y;
+                    l += acc.x + acc.y;
                 } else {
 #pragma unroll
-                    for (int c = 0; c < kBlk / 2; ++c) pk[c] = 0u;
+                    for (int c = 0; c < kCols / 2; ++c) pk[c] = 0u;
                 }
-                l += sum;
-                tmem_st16(lane_base + s_col(g), pk);
+                // P of these 16 keys over the first 8 of the warp's own S columns
+                tmem_st8(lane_base + s_col(g) + hf * kCols, pk);
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&p_full[g % kSSlots]);
+                if (warp == 0 && lane == 0) { PROBE(3) }
             }
-            mbar_wait(&kv_empty[(g - 1) % kStages], ((g - 1) / kStages) & 1);
-            tc_fence_after();
-            const float inv_l = l > 0.f ? 1.f / l : 0.f;
+            // the row sum over both warps' keys (same order in both: l_0 + l_1)
+            l_s[hf * kH + row] = l;
+            mbar_wait(&kv_empty[(g - 1) % kStages], ((g - 1) / kStages) & 1);  // the item's last PV landed
+            pair_sync();
+            const float lt = l_s[row] + l_s[kH + row];
+            const float inv_l = lt > 0.f ? 1.f / lt : 0.f;
             __nv_bfloat16* orow = p.out + (hrow + row) * p.out_ld + rank * kDvHalf;
 #pragma unroll 1
-            for (int c0 = 0; c0 < kDvHalf; c0 += 32) {
+            for (int c0 = hf * (kDvHalf / 2); c0 < (hf + 1) * (kDvHalf / 2); c0 += 32) {
                 float o[32];
                 tmem_ld32(lane_base + kColO + c0, o);
                 tmem_ld_wait();
@@ -555,20 +598,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(o_free);
-            if (rank == 0 && p.lse != nullptr)
-                p.lse[hrow + row] = l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : ninf;
+            if (rank == 0 && hf == 0 && p.lse != nullptr)
+                p.lse[hrow + row] = lt > 0.f ? (m + __log2f(lt)) * 0.6931471805599453f : ninf;
+            // l_s is rewritten only after the next item's blocks, which pass pair_sync
         }
     }
 
     tc_fence_before();
     cluster_sync_all();  // no remote arrive / st.async may target an exited CTA
-    if (warp == 8) {
+    if (warp == 12) {
         tc_fence_after();
         tmem_dealloc<kTmemCols>(tmem);
     }
 }
 
 }  // namespace
+
+#if CSAIDX_ATTN_PROBE
+extern "C" int csaidx_dev_attn_probe(long long* out, int n) {
+    return static_cast<int>(cudaMemcpyFromSymbol(out, g_attn_probe, sizeof(long long) * n));
+}
+#endif
 
 namespace csaidx_kern {
 
