@@ -1027,7 +1027,7 @@ int csaidx_cuda_sparse_attention(csaidx_engine* e, const void* q_bf16, const voi
     const char* pv = getenv("CSAIDX_ATTN_PAIR");
     const bool pair = pv == nullptr || pv[0] != '0';
     if (pair)
-        CSAIDX_CUDA_TRY(csaidx_kern::launch_sparse_mla_pair(p, e->stream), "sparse_attention");
+        CSAIDX_CUDA_TRY(csaidx_kern::launch_sparse_mla_pair(qmap, p, e->stream), "sparse_attention");
     else
         CSAIDX_CUDA_TRY(csaidx_kern::launch_sparse_mla(qmap, p, e->stream), "sparse_attention");
     return CSAIDX_OK;

@@ -41,20 +41,21 @@ constexpr int kDqkHalf = 288;              // contraction dims per CTA
 constexpr int kQkSteps = kDqkHalf / 16;    // 18 MMAs per block per CTA
 constexpr int kCtaPanels = 5;              // SW128 panels gathered per CTA
 constexpr int kBlk = 32;
-constexpr int kStages = 6;
+constexpr int kStages = 5;
 constexpr int kKvPanelBytes = kBlk * 128;                   // 4 KiB
 constexpr int kKvStageBytes = kCtaPanels * kKvPanelBytes;   // 20 KiB
-constexpr int kMaxK = 4096;
-constexpr int kIdxOffset = kStages * kKvStageBytes;
+constexpr int kQPanelBytes = 128 * 128;                     // 128 heads x 64 dims
+constexpr int kQBytes = kCtaPanels * kQPanelBytes;          // this CTA's 288 dims (+32 zero-filled / unused) = 80 KiB
+constexpr int kKvOffset = kQBytes;
 constexpr int kXchgSlotBytes = kH * kBlk * 4;               // 16 KiB
-constexpr int kXchgOffset = kIdxOffset + kMaxK * 4;
+constexpr int kXchgOffset = kKvOffset + kStages * kKvStageBytes;
 constexpr int kRedOffset = kXchgOffset + 2 * kXchgSlotBytes;  // row maxima [2][2][128] + row sums [2][128]
 constexpr int kBarOffset = kRedOffset + 3072;
 constexpr int kSmemBytes = kBarOffset + 1024 + 1024;
-constexpr int kSmWarps = 8;                // softmax warps: 2 per TMEM lane quarter, 16 keys of a block each
-constexpr int kCols = kBlk / 2;
-constexpr int kThreads = 544;              // 8 softmax + 4 KV producer + 1 MMA + 4 Q-staging warps
+constexpr int kSmWarps = 8;                // softmax warps: two teams of 4 (one per TMEM lane quarter), alternating blocks
+constexpr int kThreads = 544;              // 8 softmax + 4 KV producer + 1 MMA + 4 epilogue / Q-TMA warps
 constexpr int kProducers = 128;
+constexpr int kWarpMma = 12, kWarpEpi = 13;  // epilogue warps 13..16 cover TMEM lane quarters 1, 2, 3, 0
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColQ = 0, kColO = 192;
 // three S/P slots: the softmax sends block j+1's partial before it works on
@@ -75,6 +76,9 @@ __device__ long long g_attn_probe[kProbeBlocks * 8];
     if (blockIdx.x == 0 && g < kProbeBlocks) g_attn_probe[g * 8 + (slot)] = clock64();
 #else
 #define PROBE(slot)
+#endif
+#ifndef CSAIDX_PAIR_L1PF
+#define CSAIDX_PAIR_L1PF 0  // (measured slower) L1 prefetch of a block's rows before its stage frees (cp.async.ca then hits L1)
 #endif
 #ifndef CSAIDX_PAIR_DBG
 #define CSAIDX_PAIR_DBG 0  // (dev timing only) 1: no exchange at all, 2: send but never wait for the peer
@@ -207,28 +211,30 @@ constexpr uint32_t kIdescQK = idesc_bf16_f32(kH, kBlk);
 constexpr uint32_t kIdescPV = idesc_bf16_f32(kH, kDvHalf) | (1u << 16);  // B MN-major
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    sparse_mla_pair_kernel(const __grid_constant__ SparseMlaParams p) {
+    sparse_mla_pair_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ SparseMlaParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // the same offset in both CTAs (the dynamic window starts at the same
     // address), so mapa of a local address names the peer's twin
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint8_t* kv_smem = smem;
-    int32_t* idx_s = reinterpret_cast<int32_t*>(smem + kIdxOffset);
+    uint8_t* q_smem = smem;  // the next item's Q (TMA), copied into TMEM by tcgen05.cp
+    uint8_t* kv_smem = smem + kKvOffset;
     uint8_t* xchg = smem + kXchgOffset;  // [2 slots][8 chunks][128 heads] x 16 B, written by the peer
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOffset);
     uint64_t* kv_full = bars;                    // [kStages]
     uint64_t* kv_empty = kv_full + kStages;      // [kStages]
     uint64_t* s_full = kv_empty + kStages;       // [kSSlots]
     uint64_t* p_full = s_full + kSSlots;         // [kSSlots]
-    uint64_t* q_tmem = p_full + kSSlots;         // [1]
-    uint64_t* q_free = q_tmem + 1;               // [1]
-    uint64_t* o_free = q_free + 1;               // [1]
+    uint64_t* q_sfull = p_full + kSSlots;        // [1] an item's Q landed in shared memory (TMA)
+    uint64_t* q_sfree = q_sfull + 1;             // [1] its copy into TMEM completed (shared Q reusable)
+    uint64_t* o_free = q_sfree + 1;              // [1]
     uint64_t* vw_free = o_free + 1;              // [kStages]
     uint64_t* x_full = vw_free + kStages;        // [2][kSmWarps] the peer's partial landed (tx bytes)
     uint64_t* x_free = x_full + 2 * kSmWarps;    // [2][kSmWarps] the peer has read my partial
     uint32_t* valid_w = reinterpret_cast<uint32_t*>(x_free + 2 * kSmWarps);  // [kStages]
-    float* mx_s = reinterpret_cast<float*>(smem + kRedOffset);  // [2 blocks][2 halves][128 heads]
-    float* l_s = mx_s + 4 * kH;                                  // [2 halves][128 heads]
+    float* m_s = reinterpret_cast<float*>(smem + kRedOffset);  // [team][128 heads] running max after its last block
+    float* ml_s = m_s + 2 * kH;                                 // [team][2][128 heads] (m, l) at the item's end
+    uint64_t* m_ready = reinterpret_cast<uint64_t*>(smem + kBarOffset + 512);  // [team][quarter] m_s published
+    uint64_t* ml_ready = m_ready + kSmWarps;  // [quarter] both teams' (m, l) of an item written
     uint32_t* tmem_slot = valid_w + kStages;
 
     const int warp = threadIdx.x / 32;
@@ -244,22 +250,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&kv_full[s], kProducers + 1);
             mbar_init(&kv_empty[s], 1);
-            mbar_init(&vw_free[s], kSmWarps);
+            mbar_init(&vw_free[s], 4);
         }
         for (int s = 0; s < kSSlots; ++s) {
             mbar_init(&s_full[s], 1);
-            mbar_init(&p_full[s], kSmWarps);
+            mbar_init(&p_full[s], 4);
         }
-        mbar_init(q_tmem, 4);
-        mbar_init(q_free, 1);
-        mbar_init(o_free, kSmWarps);
+        mbar_init(q_sfull, 1);
+        mbar_init(q_sfree, 1);
+        mbar_init(o_free, 4);  // one arrive per stager warp (the epilogue)
         for (int i = 0; i < 2 * kSmWarps; ++i) {
             mbar_init(&x_full[i], 1);
             mbar_init(&x_free[i], 1);
         }
+        for (int i = 0; i < kSmWarps; ++i) mbar_init(&m_ready[i], 1);
+        for (int i = 0; i < 4; ++i) mbar_init(&ml_ready[i], 2);  // one arrive per team
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 12) tmem_alloc<kTmemCols>(tmem_slot);
+    if (warp == kWarpMma) tmem_alloc<kTmemCols>(tmem_slot);
     tc_fence_before();
     cluster_sync_all();  // barriers of both CTAs initialised before any remote traffic
     tc_fence_after();
@@ -272,10 +280,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         hrow = item * kH;  // ((b * S + tq) * G + hg) * 128
     };
 
-    if (warp >= 8 && warp < 12) {
+    if (warp >= 8 && warp < kWarpMma) {
         // ---------------------------------------------------------- KV producers
-        const int pt = threadIdx.x - 256;
-        constexpr int kPieces = (kBlk * kCtaPanels * 8) / kProducers;  // 10
+        const int pt = threadIdx.x - 256;  // 0..127: four threads per gathered row
+        constexpr int kPieces = (kBlk * kCtaPanels * 8) / kProducers;  // 10 pieces of 16 B
         static_assert(kProducers == 4 * kBlk, "4 producer threads per gathered row");
         const int r = pt >> 2;
         uint32_t soff[kPieces];
@@ -290,22 +298,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int64_t tq, hrow;
             decode(item, b, tq, hrow);
             const int32_t* idx_row = p.indices + (static_cast<int64_t>(b) * p.seq_len + tq) * p.idx_ld;
-            asm volatile("bar.sync 1, %0;" ::"n"(kProducers) : "memory");
-            for (int i = pt; i < nb * kBlk; i += kProducers) {
+            auto load_idx = [&](int i) {  // -1: padding, past k or out of range
                 const int32_t idx = i < p.k ? __ldg(idx_row + i) : -1;
-                idx_s[i] = (idx >= 0 && idx < p.kv_len) ? idx : -1;
-            }
-            asm volatile("bar.sync 1, %0;" ::"n"(kProducers) : "memory");
+                return (idx >= 0 && idx < p.kv_len) ? idx : -1;
+            };
             // this CTA's panels start at dim 256 * rank
             const char* kv_b = reinterpret_cast<const char*>(p.kv) + static_cast<int64_t>(b) * p.kv_len * (kDqk * 2) +
                                rank * 512 + (pt & 3) * 16;
+            int32_t nidx = load_idx(r), nval = warp == 8 ? load_idx(lane) : 0;  // block 0's, then one ahead
             for (int j = 0; j < nb; ++j, ++g) {
                 const int s = g % kStages;
-                const int32_t myidx = idx_s[j * kBlk + r];
+                const int32_t myidx = nidx;
+                const uint32_t vmask = warp == 8 ? __ballot_sync(0xffffffffu, nval >= 0) : 0u;
+                if (j + 1 < nb) {
+                    nidx = load_idx((j + 1) * kBlk + r);
+                    if (warp == 8) nval = load_idx((j + 1) * kBlk + lane);
+                }
                 const char* src = kv_b + static_cast<int64_t>(myidx >= 0 ? myidx : 0) * (kDqk * 2);
-                uint32_t vmask = 0;
-                if (warp == 8) vmask = __ballot_sync(0xffffffffu, idx_s[j * kBlk + lane] >= 0);
+#if CSAIDX_PAIR_L1PF
+                {
+                    // pull this block's rows toward the SM while the stage is
+                    // still in use: the copies below then hit L1 instead of
+                    // paying the L2 latency after the stage frees up
+                    const char* line = src - (pt & 3) * 16;  // the row's 640 bytes: 5 lines of 128 B
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(line + (pt & 3) * 128));
+                    if ((pt & 3) == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(line + 512));
+                }
+#endif
                 mbar_wait(&kv_empty[s], ((g / kStages) & 1) ^ 1);
+                if (pt == 0) { PROBE(6) }
                 asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 1) : "memory");
                 if (pt == 0) {
                     mbar_wait(&vw_free[s], ((g / kStages) & 1) ^ 1);
@@ -315,272 +336,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const uint32_t st = smem_u32(kv_smem + s * kKvStageBytes);
 #pragma unroll
                 for (int u = 0; u < kPieces; ++u)
+#if CSAIDX_PAIR_L1PF
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(st + soff[u]), "l"(src + 64 * u)
+                                 : "memory");
+#else
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st + soff[u]), "l"(src + 64 * u)
                                  : "memory");
+#endif
                 asm volatile("cp.async.commit_group;" ::: "memory");
                 asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&kv_full[s]))
                              : "memory");
+                if (pt == 0) { PROBE(7) }
             }
         }
-    } else if (warp >= 13) {
-        // ---------------------------------------------------------- Q stagers
+    } else if (warp >= kWarpEpi) {
+        // ---------------------------------------------------------- Q stagers + epilogue
+        // Stage item it's Q once item it-1's S MMAs retired, then write item
+        // it-1's output (O / l from TMEM) while the softmax teams already
+        // work on item it; the next item's first PV waits for o_free.
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-        uint32_t it = 0;
-        for (int64_t item = cid; item < nitems; item += ncl, ++it) {
-            int b;
-            int64_t tq, hrow;
-            decode(item, b, tq, hrow);
-            // this CTA's 288 dims of the head row
-            const uint4* qsrc = reinterpret_cast<const uint4*>(p.q + (hrow + row) * kDqk + rank * kDqkHalf);
-#pragma unroll
-            for (int c = 0; c < kDqkHalf * 2; c += 128)
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(qsrc) + c));
-            if (it > 0) {
-                mbar_wait(q_free, (it - 1) & 1);
-                tc_fence_after();
-            }
-#pragma unroll 1
-            for (int c0 = 0; c0 < 128; c0 += 64) {  // columns 0..127 (dims 0..255 of the half)
-                uint32_t w[64];
-                uint4* w4 = reinterpret_cast<uint4*>(w);
-#pragma unroll
-                for (int v = 0; v < 16; ++v) w4[v] = __ldg(qsrc + c0 / 4 + v);
-                tmem_st16(lane_base + kColQ + c0, *reinterpret_cast<uint32_t(*)[16]>(w));
-                tmem_st16(lane_base + kColQ + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(w + 16));
-                tmem_st16(lane_base + kColQ + c0 + 32, *reinterpret_cast<uint32_t(*)[16]>(w + 32));
-                tmem_st16(lane_base + kColQ + c0 + 48, *reinterpret_cast<uint32_t(*)[16]>(w + 48));
-            }
-            {  // columns 128..143 (dims 256..287 of the half)
-                uint32_t w[16];
-                uint4* w4 = reinterpret_cast<uint4*>(w);
-#pragma unroll
-                for (int v = 0; v < 4; ++v) w4[v] = __ldg(qsrc + 32 + v);
-                tmem_st16(lane_base + kColQ + 128, w);
-            }
-            tmem_st_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(q_tmem);
-        }
-    } else if (warp == 12) {
-        // ---------------------------------------------------------- MMA issuer
-        if (elect_one()) {
-            const uint32_t kv_base = smem_u32(kv_smem);
-            // K step kk of this CTA = global step 18 rank + kk: local panel
-            // (global >> 2) - 4 rank, 32-byte step (global & 3) inside it
-            uint32_t boff[kQkSteps];
-#pragma unroll
-            for (int kk = 0; kk < kQkSteps; ++kk) {
-                const int gk = kQkSteps * static_cast<int>(rank) + kk;
-                boff[kk] = ((gk >> 2) - 4 * static_cast<int>(rank)) * kKvPanelBytes + (gk & 3) * 32;
-            }
-            uint32_t g = 0, it = 0;
-            for (int64_t item = cid; item < nitems; item += ncl, ++it) {
-                mbar_wait(q_tmem, it & 1);
-                tc_fence_after();
-                auto issue_pv = [&](int j, uint32_t gj) {
-                    const int s = gj % kStages;
-                    if (j == 0 && it > 0) mbar_wait(o_free, (it - 1) & 1);
-                    mbar_wait(&p_full[gj % kSSlots], (gj / kSSlots) & 1);
-                    {
-                        const uint32_t g = gj;
-                        PROBE(5)
-                    }
-                    tc_fence_after();
-                    const uint32_t vb = kv_base + s * kKvStageBytes;  // V = local panels 0..3
-#pragma unroll
-                    for (int kk = 0; kk < kBlk / 16; ++kk)
-                        umma_bf16_ts(tmem + kColO, tmem + s_col(gj) + kk * 16,
-                                     sw128_mnmajor_desc(vb + kk * 2048, kKvPanelBytes, 1024), kIdescPV,
-                                     (j > 0 || kk > 0) ? 1u : 0u);
-                    umma_commit(&kv_empty[s]);
-                };
-                auto issue_qk = [&](int j, uint32_t gj) {
-                    const int s = gj % kStages;
-                    mbar_wait(&kv_full[s], (gj / kStages) & 1);
-                    {
-                        const uint32_t g = gj;
-                        PROBE(4)
-                    }
-                    fence_proxy_async();
-                    tc_fence_after();
-                    const uint32_t st = kv_base + s * kKvStageBytes;
-                    const uint32_t d = tmem + s_col(gj);
-#pragma unroll
-                    for (int kk = 0; kk < kQkSteps; ++kk)
-                        umma_bf16_ts(d, tmem + kColQ + kk * 8, sw128_kmajor_desc(st + boff[kk]), kIdescQK,
-                                     kk > 0 ? 1u : 0u);
-                    umma_commit(&s_full[gj % kSSlots]);
-                    if (j == nb - 1) umma_commit(q_free);
-                };
-                // QK two blocks ahead of PV: the softmax of block j starts by
-                // sending S(j+1), and QK(j+2) (the slot of P(j-1), whose PV
-                // was issued one iteration earlier) runs while it waits for P(j)
-                issue_qk(0, g);
-                if (nb > 1) issue_qk(1, g + 1);
-                for (int j = 0; j < nb; ++j) {
-                    if (j + 2 < nb) issue_qk(j + 2, g + j + 2);
-                    issue_pv(j, g + j);
-                }
-                g += nb;
-            }
-        }
-    } else {
-        // ---------------------------------------------------------- softmax + epilogue
-        // warp = (half of the block's keys hf, TMEM lane quarter): the pair of
-        // warps of a quarter share the row max through shared memory each
-        // block and the row sum at the end
-        const int quarter = warp & 3, hf = warp >> 2;
-        const int row = quarter * 32 + lane;
-        const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-        const float scale_log2 = p.sm_scale * 1.4426950408889634f;
         const float ninf = -INFINITY;
-        auto pair_sync = [&] {  // the two warps of this quarter
-            tc_fence_before();
-            asm volatile("bar.sync %0, 64;" ::"r"(2 + quarter) : "memory");
+        auto epilogue = [&](uint32_t ie, int64_t hrow_e) {
+            mbar_wait(&ml_ready[quarter], ie & 1);  // both teams' (m, l) of item ie
+            const float m0 = ml_s[row], l0 = ml_s[kH + row], m1 = ml_s[2 * kH + row], l1 = ml_s[3 * kH + row];
+            const float M = fmaxf(m0, m1);
+            const float L = (l0 > 0.f ? l0 * ex2(m0 - M) : 0.f) + (l1 > 0.f ? l1 * ex2(m1 - M) : 0.f);
+            const float inv_l = L > 0.f ? 1.f / L : 0.f;
+            const uint32_t gl = (ie + 1) * static_cast<uint32_t>(nb) - 1;  // the item's last block
+            mbar_wait(&kv_empty[gl % kStages], (gl / kStages) & 1);       // its PV landed (exact: next phase needs o_free)
             tc_fence_after();
-        };
-        // exchange: my 16 columns of the partial go to the peer's slot,
-        // chunk-major [chunk][head] x 16 B (conflict free both ways)
-        const uint32_t x_local = smem_u32(xchg);
-        const uint32_t x_peer = peer_addr(x_local, peer);
-        const uint32_t xf_peer0 = peer_addr(smem_u32(&x_full[warp]), peer);
-        const uint32_t xf_peer1 = peer_addr(smem_u32(&x_full[kSmWarps + warp]), peer);
-        const uint32_t xr_peer0 = peer_addr(smem_u32(&x_free[warp]), peer);
-        const uint32_t xr_peer1 = peer_addr(smem_u32(&x_free[kSmWarps + warp]), peer);
-        const uint32_t xoff = ((4 * hf) * kH + row) * 16;  // first chunk of this warp's columns
-        // own partial of block gs: read it, st.async it to the peer (after the
-        // peer released the slot), post the receive of the peer's partial
-        auto send = [&](uint32_t gs, float (&y)[kCols]) {
-            const int sl = static_cast<int>(gs & 1);
-            mbar_wait(&s_full[gs % kSSlots], (gs / kSSlots) & 1);
-            tc_fence_after();
-            tmem_ld16(lane_base + s_col(gs) + hf * kCols, y);
-            if (lane == 0) mbar_expect_tx(&x_full[sl * kSmWarps + warp], 32 * kCols * 4);
-            tmem_ld_wait();
-            if (CSAIDX_PAIR_DBG == 1) return;
-            if (CSAIDX_PAIR_DBG == 0) mbar_wait_cluster(&x_free[sl * kSmWarps + warp], ((gs >> 1) & 1) ^ 1);
-#pragma unroll
-            for (int q = 0; q < kCols / 4; ++q)
-                st_async_v4(x_peer + sl * kXchgSlotBytes + xoff + q * kH * 16, y[4 * q], y[4 * q + 1], y[4 * q + 2],
-                            y[4 * q + 3], sl ? xf_peer1 : xf_peer0);
-        };
-        uint32_t g = 0;
-        for (int64_t item = cid; item < nitems; item += ncl) {
-            int b;
-            int64_t tq, hrow;
-            decode(item, b, tq, hrow);
-            float m = ninf, l = 0.f;  // l: this warp's keys only (same m in both warps)
-            float nxt[kCols];
-            send(g, nxt);
-            for (int j = 0; j < nb; ++j, ++g) {
-                const int s = g % kStages;
-                const int sl = static_cast<int>(g & 1);
-                float x[kCols];
-                if (warp == 0 && lane == 0) { PROBE(0) }
-#pragma unroll
-                for (int c = 0; c < kCols; ++c) x[c] = nxt[c];
-                if (j + 1 < nb) send(g + 1, nxt);  // overlaps the exchange with this block's softmax
-                if (warp == 0 && lane == 0) { PROBE(1) }
-                mbar_wait(&kv_full[s], (g / kStages) & 1);  // completed: orders the valid word
-                uint32_t vm = 0;
-                if (lane == 0) {
-                    vm = valid_w[s];
-                    mbar_arrive(&vw_free[s]);
-                }
-                vm = (__shfl_sync(0xffffffffu, vm, 0) >> (kCols * hf)) & 0xffffu;
-                // the peer's partial -> S = S_0 + S_1 (same bits in both CTAs)
-                if (CSAIDX_PAIR_DBG == 0) mbar_wait_cluster(&x_full[sl * kSmWarps + warp], (g >> 1) & 1);
-                if (warp == 0 && lane == 0) { PROBE(2) }
-#pragma unroll
-                for (int q = 0; q < kCols / 4 && CSAIDX_PAIR_DBG != 1; ++q) {
-                    const float4 v = *reinterpret_cast<const float4*>(xchg + sl * kXchgSlotBytes + xoff + q * kH * 16);
-                    x[4 * q] += v.x;
-                    x[4 * q + 1] += v.y;
-                    x[4 * q + 2] += v.z;
-                    x[4 * q + 3] += v.w;
-                }
-                __syncwarp();
-                if (lane == 0 && CSAIDX_PAIR_DBG == 0) remote_arrive(sl ? xr_peer1 : xr_peer0);  // the peer may refill my slot
-                if (vm != 0xffffu) {
-#pragma unroll
-                    for (int c = 0; c < kCols; ++c) x[c] = ((vm >> c) & 1u) ? x[c] : ninf;
-                }
-                const float mh = max3f(max3f(max3f(x[0], x[1], x[2]), max3f(x[3], x[4], x[5]), max3f(x[6], x[7], x[8])),
-                                       max3f(max3f(x[9], x[10], x[11]), max3f(x[12], x[13], x[14]), x[15]), ninf);
-                mx_s[(sl * 2 + hf) * kH + row] = mh;
-                pair_sync();
-                const float mx = fmaxf(mh, mx_s[(sl * 2 + (hf ^ 1)) * kH + row]) * scale_log2;
-                float alpha = 1.f;
-                bool rescale = false;
-                if (mx > m) {
-                    if (m == ninf) {
-                        m = mx;
-                    } else if (mx > m + kRescaleLog2) {
-                        alpha = ex2(m - mx);
-                        l *= alpha;
-                        m = mx;
-                        rescale = true;
-                    }
-                }
-                if (__any_sync(0xffffffffu, rescale)) {
-                    // PV of block g-1 landed (exact parity wait: attn_sm100.cu);
-                    // each warp of the quarter rescales its half of O's columns
-                    mbar_wait(&kv_empty[(g - 1) % kStages], ((g - 1) / kStages) & 1);
-                    tc_fence_after();
+            __nv_bfloat16* orow = p.out + (hrow_e + row) * p.out_ld + rank * kDvHalf;
 #pragma unroll 1
-                    for (int c0 = hf * (kDvHalf / 2); c0 < (hf + 1) * (kDvHalf / 2); c0 += 32) {
-                        float o[32];
-                        tmem_ld32(lane_base + kColO + c0, o);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int c = 0; c < 32; ++c) o[c] *= alpha;
-                        tmem_st32(lane_base + kColO + c0, o);
-                    }
-                    tmem_st_wait();
-                }
-                uint32_t pk[kCols / 2];
-                if (m != ninf) {
-                    const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m, -m);
-                    float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-                    for (int c = 0; c < kCols; c += 2) {
-                        const float2 a = __ffma2_rn(make_float2(x[c], x[c + 1]), sc2, nm2);
-                        float2 pr;
-                        if (c < kCols / 2) {
-                            pr.x = ex2(a.x);
-                            pr.y = ex2(a.y);
-                        } else {
-                            pr = exp2_poly2(a);
-                        }
-                        acc = __fadd2_rn(acc, pr);
-                        const __nv_bfloat162 h2 = __floats2bfloat162_rn(pr.x, pr.y);
-                        pk[c / 2] = *reinterpret_cast<const uint32_t*>(&h2);
-                    }
-                    l += acc.x + acc.y;
-                } else {
-#pragma unroll
-                    for (int c = 0; c < kCols / 2; ++c) pk[c] = 0u;
-                }
-                // P of these 16 keys over the first 8 of the warp's own S columns
-                tmem_st8(lane_base + s_col(g) + hf * kCols, pk);
-                tmem_st_wait();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&p_full[g % kSSlots]);
-                if (warp == 0 && lane == 0) { PROBE(3) }
-            }
-            // the row sum over both warps' keys (same order in both: l_0 + l_1)
-            l_s[hf * kH + row] = l;
-            mbar_wait(&kv_empty[(g - 1) % kStages], ((g - 1) / kStages) & 1);  // the item's last PV landed
-            pair_sync();
-            const float lt = l_s[row] + l_s[kH + row];
-            const float inv_l = lt > 0.f ? 1.f / lt : 0.f;
-            __nv_bfloat16* orow = p.out + (hrow + row) * p.out_ld + rank * kDvHalf;
-#pragma unroll 1
-            for (int c0 = hf * (kDvHalf / 2); c0 < (hf + 1) * (kDvHalf / 2); c0 += 32) {
+            for (int c0 = 0; c0 < kDvHalf; c0 += 32) {
                 float o[32];
                 tmem_ld32(lane_base + kColO + c0, o);
                 tmem_ld_wait();
@@ -598,15 +387,299 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(o_free);
-            if (rank == 0 && hf == 0 && p.lse != nullptr)
-                p.lse[hrow + row] = lt > 0.f ? (m + __log2f(lt)) * 0.6931471805599453f : ninf;
-            // l_s is rewritten only after the next item's blocks, which pass pair_sync
+            if (rank == 0 && p.lse != nullptr)
+                p.lse[hrow_e + row] = L > 0.f ? (M + __log2f(L)) * 0.6931471805599453f : ninf;
+        };
+        uint32_t it = 0;
+        int64_t prev_hrow = 0;
+        for (int64_t item = cid; item < nitems; item += ncl, ++it) {
+            int b;
+            int64_t tq, hrow;
+            decode(item, b, tq, hrow);
+            if (warp == kWarpEpi && lane == 0) {
+                // this CTA's 288 dims of the item's 128 head rows -> shared
+                // memory, once the previous item's Q has been copied to TMEM
+                if (it > 0) mbar_wait(q_sfree, (it - 1) & 1);
+                mbar_expect_tx(q_sfull, kQBytes);
+                for (int pn = 0; pn < kCtaPanels; ++pn)
+                    tma_load_2d(q_smem + pn * kQPanelBytes, &qmap, q_sfull,
+                                static_cast<int32_t>(rank * kDqkHalf + pn * 64), static_cast<int32_t>(hrow));
+            }
+            __syncwarp();
+            if (it > 0) epilogue(it - 1, prev_hrow);
+            prev_hrow = hrow;
+        }
+        if (it > 0) epilogue(it - 1, prev_hrow);
+    } else if (warp == kWarpMma) {
+        // ---------------------------------------------------------- MMA issuer
+        if (elect_one()) {
+            const uint32_t kv_base = smem_u32(kv_smem);
+            // K step kk of this CTA = global step 18 rank + kk: local panel
+            // (global >> 2) - 4 rank, 32-byte step (global & 3) inside it
+            auto boff = [&](int kk) {
+                const int gk = kQkSteps * static_cast<int>(rank) + kk;
+                return static_cast<uint32_t>(((gk >> 2) - 4 * static_cast<int>(rank)) * kKvPanelBytes + (gk & 3) * 32);
+            };
+            // One global block sequence over this cluster's items (block G =
+            // item G / nb, key block G % nb): QK runs two blocks ahead of PV
+            // across item boundaries too, so the next item's first scores are
+            // computed while the current item's last softmax blocks finish.
+            const uint32_t my_items = cid < nitems ? static_cast<uint32_t>((nitems - 1 - cid) / ncl + 1) : 0u;
+            const uint32_t total = my_items * static_cast<uint32_t>(nb);
+            auto issue_pv = [&](uint32_t gj) {
+                const uint32_t it = gj / nb;
+                const int j = static_cast<int>(gj - it * nb);
+                const int s = gj % kStages;
+                if (j == 0 && it > 0) mbar_wait(o_free, (it - 1) & 1);  // the last epilogue has read O
+                mbar_wait(&p_full[gj % kSSlots], (gj / kSSlots) & 1);
+                {
+                    const uint32_t g = gj;
+                    PROBE(5)
+                }
+                tc_fence_after();
+                const uint32_t vb = kv_base + s * kKvStageBytes;  // V = local panels 0..3
+#pragma unroll
+                for (int kk = 0; kk < kBlk / 16; ++kk)
+                    umma_bf16_ts(tmem + kColO, tmem + s_col(gj) + kk * 8,
+                                 sw128_mnmajor_desc(vb + kk * 2048, kKvPanelBytes, 1024), kIdescPV,
+                                 (j > 0 || kk > 0) ? 1u : 0u);
+                umma_commit(&kv_empty[s]);
+            };
+            auto issue_qk = [&](uint32_t gj) {
+                const uint32_t it = gj / nb;
+                const int j = static_cast<int>(gj - it * nb);
+                const int s = gj % kStages;
+                if (j == 0) {
+                    // the item's Q: shared memory -> TMEM columns 0..143, one
+                    // 128 x 256-bit copy per K step (in issue order with the
+                    // MMAs: the previous item's QK have read the old Q)
+                    mbar_wait(q_sfull, it & 1);
+                    tc_fence_after();
+                    const uint32_t qb = smem_u32(q_smem);
+#pragma unroll
+                    for (int kk = 0; kk < kQkSteps; ++kk)
+                        asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(tmem + kColQ + kk * 8),
+                                     "l"(sw128_kmajor_desc(qb + (kk >> 2) * kQPanelBytes + (kk & 3) * 32))
+                                     : "memory");
+                    umma_commit(q_sfree);
+                }
+                mbar_wait(&kv_full[s], (gj / kStages) & 1);
+                {
+                    const uint32_t g = gj;
+                    PROBE(4)
+                }
+                fence_proxy_async();
+                tc_fence_after();
+                const uint32_t st = kv_base + s * kKvStageBytes;
+                const uint32_t d = tmem + s_col(gj);
+#pragma unroll
+                for (int kk = 0; kk < kQkSteps; ++kk)
+                    umma_bf16_ts(d, tmem + kColQ + kk * 8, sw128_kmajor_desc(st + boff(kk)), kIdescQK,
+                                 kk > 0 ? 1u : 0u);
+                umma_commit(&s_full[gj % kSSlots]);
+            };
+            // Polling issue: QK(nq) and PV(np) each in order, QK at most two
+            // blocks ahead of PV (QK(G) reuses the S slot of P(G-3)), and
+            // whichever has its inputs goes first, so a late gather does not
+            // hold back a ready PV and a slow softmax does not hold back the
+            // next scores.
+            auto ready = [&](uint64_t* bar, uint32_t parity) {
+                uint32_t ok;
+                asm volatile(
+                    "{\n\t.reg .pred P;\n\t"
+                    "mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+                    "selp.u32 %0, 1, 0, P;\n\t}"
+                    : "=r"(ok)
+                    : "r"(smem_u32(bar)), "r"(parity)
+                    : "memory");
+                return ok != 0;
+            };
+            auto qk_ready = [&](uint32_t gj) {
+                const uint32_t it = gj / nb;
+                if (gj == it * nb && !ready(q_sfull, it & 1)) return false;
+                return ready(&kv_full[gj % kStages], (gj / kStages) & 1);
+            };
+            auto pv_ready = [&](uint32_t gj) {
+                const uint32_t it = gj / nb;
+                if (gj == it * nb && it > 0 && !ready(o_free, (it - 1) & 1)) return false;
+                return ready(&p_full[gj % kSSlots], (gj / kSSlots) & 1);
+            };
+            uint32_t nq = 0, np = 0;
+            while (np < total) {
+                if (nq < total && nq <= np + 2 && qk_ready(nq)) {
+                    issue_qk(nq);
+                    ++nq;
+                }
+                if (np < nq && pv_ready(np)) {
+                    issue_pv(np);
+                    ++np;
+                }
+            }
+        }
+    } else {
+        // ---------------------------------------------------------- softmax + epilogue
+        // Two teams of four warps (one per TMEM lane quarter) take alternate
+        // blocks of an item (team = j & 1), so two blocks' latency chains
+        // (S load, exchange with the peer, max, exponentials, P store) run at
+        // once. The running max passes from team to team through shared
+        // memory (m_ready); each team keeps its own row sum relative to the
+        // max it last used, and the two sums are combined at the item's end.
+        const int quarter = warp & 3, team = warp >> 2;
+        const int row = quarter * 32 + lane;
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+        const float scale_log2 = p.sm_scale * 1.4426950408889634f;
+        const float ninf = -INFINITY;
+        const int cnt0 = (nb + 1) / 2, cnt1 = nb / 2;  // blocks per item of team 0 / team 1
+        const int mycnt = team ? cnt1 : cnt0;
+        // exchange slot = team; chunk-major [chunk][head] x 16 B
+        const uint32_t x_peer = peer_addr(smem_u32(xchg), peer) + team * kXchgSlotBytes;
+        const uint8_t* x_mine = xchg + team * kXchgSlotBytes;
+        const int xb = team * 4 + quarter;  // this warp's x_full / x_free
+        const uint32_t xf_peer = peer_addr(smem_u32(&x_full[xb]), peer);
+        const uint32_t xr_peer = peer_addr(smem_u32(&x_free[xb]), peer);
+        uint32_t g = 0, it = 0;
+        for (int64_t item = cid; item < nitems; item += ncl, ++it) {
+            int b;
+            int64_t tq, hrow;
+            decode(item, b, tq, hrow);
+            float m = ninf, l = 0.f;  // this team's max in use and its row sum relative to it
+            for (int j = team; j < nb; j += 2) {
+                const uint32_t gb = g + j;  // global block
+                const uint32_t n = it * mycnt + (j >> 1);  // this team's block count: barrier phases
+                const int s = gb % kStages;
+                float x[kBlk];
+                if ((warp & 3) == 0 && lane == 0) { const uint32_t g = gb; PROBE(0) }
+                mbar_wait(&s_full[gb % kSSlots], (gb / kSSlots) & 1);
+                tc_fence_after();
+                tmem_ld32(lane_base + s_col(gb), x);
+                if (lane == 0) mbar_expect_tx(&x_full[xb], 32 * kBlk * 4);
+                tmem_ld_wait();
+                if (CSAIDX_PAIR_DBG == 0) mbar_wait_cluster(&x_free[xb], (n & 1) ^ 1);
+#pragma unroll
+                for (int q = 0; q < kBlk / 4; ++q)
+                    st_async_v4(x_peer + (q * kH + row) * 16, x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3],
+                                xf_peer);
+                if ((warp & 3) == 0 && lane == 0) { const uint32_t g = gb; PROBE(1) }
+                mbar_wait(&kv_full[s], (gb / kStages) & 1);  // completed: orders the valid word
+                uint32_t vm = 0;
+                if (lane == 0) {
+                    vm = valid_w[s];
+                    mbar_arrive(&vw_free[s]);
+                }
+                vm = __shfl_sync(0xffffffffu, vm, 0);
+                // the peer's partial -> S = S_0 + S_1 (same bits in both CTAs)
+                if (CSAIDX_PAIR_DBG == 0) mbar_wait_cluster(&x_full[xb], n & 1);
+                if ((warp & 3) == 0 && lane == 0) { const uint32_t g = gb; PROBE(2) }
+#pragma unroll
+                for (int q = 0; q < kBlk / 4; ++q) {
+                    const float4 v = *reinterpret_cast<const float4*>(x_mine + (q * kH + row) * 16);
+                    x[4 * q] += v.x;
+                    x[4 * q + 1] += v.y;
+                    x[4 * q + 2] += v.z;
+                    x[4 * q + 3] += v.w;
+                }
+                __syncwarp();
+                if (lane == 0 && CSAIDX_PAIR_DBG == 0) remote_arrive(xr_peer);  // the peer may refill my slot
+                if (vm != 0xffffffffu) {
+#pragma unroll
+                    for (int c = 0; c < kBlk; ++c) x[c] = ((vm >> c) & 1u) ? x[c] : ninf;
+                }
+                float t3[11];
+#pragma unroll
+                for (int c = 0; c < 10; ++c) t3[c] = max3f(x[3 * c], x[3 * c + 1], x[3 * c + 2]);
+                t3[10] = fmaxf(x[30], x[31]);
+                const float mx = max3f(max3f(max3f(t3[0], t3[1], t3[2]), max3f(t3[3], t3[4], t3[5]),
+                                             max3f(t3[6], t3[7], t3[8])),
+                                       t3[9], t3[10]) * scale_log2;
+                // the max in use after block j-1 (the other team's), then the
+                // lazy rule: move it only when this block exceeds it by 2^8
+                float mprev = ninf;
+                if (j > 0) {
+                    const int ot = team ^ 1;
+                    const uint32_t on = it * (ot ? cnt1 : cnt0) + ((j - 1) >> 1);
+                    mbar_wait(&m_ready[ot * 4 + quarter], on & 1);
+                    mprev = m_s[ot * kH + row];
+                }
+                float mnew = mprev;
+                bool rescale = false;
+                float alpha = 1.f;
+                if (mx > mprev) {
+                    if (mprev == ninf) {
+                        mnew = mx;
+                    } else if (mx > mprev + kRescaleLog2) {
+                        alpha = ex2(mprev - mx);
+                        mnew = mx;
+                        rescale = true;
+                    }
+                }
+                m_s[team * kH + row] = mnew;  // the other team's next block reads it
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&m_ready[team * 4 + quarter]);
+                if (mnew != m) {  // this team's sum follows the max in use
+                    if (m != ninf) l *= ex2(m - mnew);
+                    m = mnew;
+                }
+                if (__any_sync(0xffffffffu, rescale)) {
+                    // PV of block gb-1 landed (exact parity wait: attn_sm100.cu)
+                    mbar_wait(&kv_empty[(gb - 1) % kStages], ((gb - 1) / kStages) & 1);
+                    tc_fence_after();
+#pragma unroll 1
+                    for (int c0 = 0; c0 < kDvHalf; c0 += 32) {
+                        float o[32];
+                        tmem_ld32(lane_base + kColO + c0, o);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) o[c] *= alpha;
+                        tmem_st32(lane_base + kColO + c0, o);
+                    }
+                    tmem_st_wait();
+                }
+                uint32_t pk[kBlk / 2];
+                if (m != ninf) {
+                    const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m, -m);
+                    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int c = 0; c < kBlk; c += 2) {
+                        const float2 a = __ffma2_rn(make_float2(x[c], x[c + 1]), sc2, nm2);
+                        float2 pr;
+                        if (c < kBlk / 2) {
+                            pr.x = ex2(a.x);
+                            pr.y = ex2(a.y);
+                        } else {
+                            pr = exp2_poly2(a);
+                        }
+                        acc = __fadd2_rn(acc, pr);
+                        const __nv_bfloat162 h2 = __floats2bfloat162_rn(pr.x, pr.y);
+                        pk[c / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+                    }
+                    l += acc.x + acc.y;
+                } else {
+#pragma unroll
+                    for (int c = 0; c < kBlk / 2; ++c) pk[c] = 0u;
+                }
+                tmem_st16(lane_base + s_col(gb), pk);  // P over the S columns just read
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&p_full[gb % kSSlots]);
+                if ((warp & 3) == 0 && lane == 0) { const uint32_t g = gb; PROBE(3) }
+            }
+            g += nb;
+            // (m, l) of this team -> the stagers' epilogue, once the previous
+            // item's epilogue has read ml_s (o_free; with nb >= 4 the blocks
+            // above already waited for it through PV(0), with fewer blocks
+            // this keeps ml_s and ml_ready one item deep)
+            if (it > 0) mbar_wait(o_free, (it - 1) & 1);
+            ml_s[(team * 2 + 0) * kH + row] = m;
+            ml_s[(team * 2 + 1) * kH + row] = l;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ml_ready[quarter]);
         }
     }
 
     tc_fence_before();
     cluster_sync_all();  // no remote arrive / st.async may target an exited CTA
-    if (warp == 12) {
+    if (warp == kWarpMma) {
         tc_fence_after();
         tmem_dealloc<kTmemCols>(tmem);
     }
@@ -624,7 +697,7 @@ namespace csaidx_kern {
 
 int sparse_mla_pair_smem_bytes() { return kSmemBytes; }
 
-cudaError_t launch_sparse_mla_pair(const SparseMlaParams& p, cudaStream_t stream) {
+cudaError_t launch_sparse_mla_pair(const CUtensorMap& qmap, const SparseMlaParams& p, cudaStream_t stream) {
     if (p.seq_len <= 0 || p.batch <= 0) return cudaSuccess;
     static bool attr_set[kMaxDevices] = {};
     const int dev = attr_device();
@@ -640,7 +713,7 @@ cudaError_t launch_sparse_mla_pair(const SparseMlaParams& p, cudaStream_t stream
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cur);
     const int64_t items = p.seq_len * p.batch * p.head_groups;
     const int64_t pairs = items < sms / 2 ? items : sms / 2;
-    sparse_mla_pair_kernel<<<static_cast<unsigned>(2 * pairs), kThreads, kSmemBytes, stream>>>(p);
+    sparse_mla_pair_kernel<<<static_cast<unsigned>(2 * pairs), kThreads, kSmemBytes, stream>>>(qmap, p);
     return cudaGetLastError();
 }
 

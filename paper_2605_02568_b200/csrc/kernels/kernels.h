@@ -230,7 +230,7 @@ int sparse_mla_smem_bytes();
 cudaError_t launch_sparse_mla(const CUtensorMap& qmap, const SparseMlaParams& p, cudaStream_t stream);
 int sparse_mla_pair_smem_bytes();
 // CTA-pair form (attn_pair_sm100.cu): same operator, Dqk split across a cluster of 2
-cudaError_t launch_sparse_mla_pair(const SparseMlaParams& p, cudaStream_t stream);
+cudaError_t launch_sparse_mla_pair(const CUtensorMap& qmap, const SparseMlaParams& p, cudaStream_t stream);
 // Scratch the select needs for takes above select_max_take() (rows = B * rows).
 size_t select_large_scratch_bytes(int k, int64_t cols, int64_t rows);
 // Staging scratch the merge needs for k above select_max_take().

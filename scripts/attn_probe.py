@@ -1,5 +1,8 @@
 """(dev, GPU box) per-block clock64 stamps of the CTA-pair attention kernel
-built with -DCSAIDX_ATTN_PROBE=1 (CTA 0: softmax warp 0 and the MMA issuer).
+built with -DCSAIDX_ATTN_PROBE=1 (CTA 0). Slots per block g: 0 softmax start,
+1 own partial sent, 2 peer partial landed, 3 P stored (the team handling g);
+4 MMA saw kv_full(g), 5 MMA saw p_full(g); 6 producer saw the stage free,
+7 producer issued the copies.
 usage: python scripts/attn_probe.py [S] [k]"""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -24,13 +27,13 @@ buf = (ctypes.c_longlong * n)()
 assert lib.csaidx_dev_attn_probe(buf, n) == 0
 a = np.frombuffer(buf, dtype=np.int64).reshape(2048, 8).astype(np.float64)
 nb = (k + 31) // 32
-blocks = a[64:1024]  # steady state
-d = lambda i, j: np.median(blocks[:, j] - blocks[:, i])
-per_block = np.median(np.diff(blocks[:, 0]))
-print(f"per block (softmax iteration start to start): {per_block:.0f} cycles")
-print(f"  send(g+1) [wait S(g+1), ld, st.async]: {d(0, 1):.0f}")
-print(f"  kv_full + valid word + wait peer partial: {d(1, 2):.0f}")
-print(f"  add + max + exp + P store + arrive: {d(2, 3):.0f}")
-print(f"  MMA: kv_full(g) seen -> p_full(g) seen: {d(4, 5):.0f}; QK(g) issue vs softmax start of g: {np.median(blocks[:, 4] - blocks[:, 0]):.0f}")
-print(f"  p_full(g) seen at MMA - P arrive by warp 0: {np.median(blocks[:, 5] - blocks[:, 3]):.0f}")
-print(f"  MMA kv_full waits start to start: {np.median(np.diff(blocks[:, 4])):.0f}")
+rows = [g for g in range(64, 1000) if 2 <= g % nb <= nb - 3]  # steady state, away from item boundaries
+B = a[rows]
+med = lambda v: float(np.median(v))
+print(f"steady block period (MMA kv_full seen): {med(np.diff(a[64:1000, 4])[[r - 64 for r in rows[:-1]]]):.0f} cycles")
+print(f"softmax (team of block g): start->sent {med(B[:,1]-B[:,0]):.0f}, sent->peer landed {med(B[:,2]-B[:,1]):.0f}, ->P stored {med(B[:,3]-B[:,2]):.0f}, total {med(B[:,3]-B[:,0]):.0f}")
+print(f"softmax start(g) - QK(g) kv_full seen: {med(B[:,0]-B[:,4]):.0f}; P stored(g) -> MMA sees p_full(g): {med(B[:,5]-B[:,3]):.0f}")
+print(f"producer: stage free(g) -> copies issued {med(B[:,7]-B[:,6]):.0f}; copies issued(g) -> MMA sees kv_full(g) {med(B[:,4]-B[:,7]):.0f}")
+print(f"stage free(g) - PV issue(g-5) [p_full seen]: {med(a[rows,6]-a[[r-5 for r in rows],5]):.0f}")
+bidx = [gg for gg in range(64, 999) if (gg + 1) % nb == 0]
+print(f"item boundary: MMA kv_full gap {med([a[gg+1,4]-a[gg,4] for gg in bidx]):.0f}, p_full gap {med([a[gg+1,5]-a[gg,5] for gg in bidx]):.0f}")
