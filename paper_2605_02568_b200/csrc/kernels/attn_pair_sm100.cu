@@ -41,21 +41,21 @@ constexpr int kDqkHalf = 288;              // contraction dims per CTA
 constexpr int kQkSteps = kDqkHalf / 16;    // 18 MMAs per block per CTA
 constexpr int kCtaPanels = 5;              // SW128 panels gathered per CTA
 constexpr int kBlk = 32;
-constexpr int kStages = 5;
+constexpr int kStages = 7;
 constexpr int kKvPanelBytes = kBlk * 128;                   // 4 KiB
 constexpr int kKvStageBytes = kCtaPanels * kKvPanelBytes;   // 20 KiB
 constexpr int kQPanelBytes = 128 * 128;                     // 128 heads x 64 dims
-constexpr int kQBytes = kCtaPanels * kQPanelBytes;          // this CTA's 288 dims (+32 zero-filled / unused) = 80 KiB
-constexpr int kKvOffset = kQBytes;
+constexpr int kQSlots = 2;                                  // Q panels in flight (TMA -> tcgen05.cp ring)
+constexpr int kKvOffset = kQSlots * kQPanelBytes;
 constexpr int kXchgSlotBytes = kH * kBlk * 4;               // 16 KiB
 constexpr int kXchgOffset = kKvOffset + kStages * kKvStageBytes;
 constexpr int kRedOffset = kXchgOffset + 2 * kXchgSlotBytes;  // row maxima [2][2][128] + row sums [2][128]
 constexpr int kBarOffset = kRedOffset + 3072;
 constexpr int kSmemBytes = kBarOffset + 1024 + 1024;
 constexpr int kSmWarps = 8;                // softmax warps: two teams of 4 (one per TMEM lane quarter), alternating blocks
-constexpr int kThreads = 544;              // 8 softmax + 4 KV producer + 1 MMA + 4 epilogue / Q-TMA warps
+constexpr int kThreads = 576;              // 8 softmax + 4 KV producer + 1 MMA + 4 epilogue + 1 Q-TMA warps
 constexpr int kProducers = 128;
-constexpr int kWarpMma = 12, kWarpEpi = 13;  // epilogue warps 13..16 cover TMEM lane quarters 1, 2, 3, 0
+constexpr int kWarpMma = 12, kWarpEpi = 13, kWarpQ = 17;  // epilogue warps 13..16 cover TMEM lane quarters 1, 2, 3, 0
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColQ = 0, kColO = 192;
 // three S/P slots: the softmax sends block j+1's partial before it works on
@@ -71,9 +71,9 @@ constexpr float kRescaleLog2 = 8.0f;
 #endif
 #if CSAIDX_ATTN_PROBE
 constexpr int kProbeBlocks = 2048;
-__device__ long long g_attn_probe[kProbeBlocks * 8];
+__device__ long long g_attn_probe[kProbeBlocks * 16];
 #define PROBE(slot) \
-    if (blockIdx.x == 0 && g < kProbeBlocks) g_attn_probe[g * 8 + (slot)] = clock64();
+    if (blockIdx.x == 0 && g < kProbeBlocks) g_attn_probe[g * 16 + (slot)] = clock64();
 #else
 #define PROBE(slot)
 #endif
@@ -216,7 +216,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // the same offset in both CTAs (the dynamic window starts at the same
     // address), so mapa of a local address names the peer's twin
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint8_t* q_smem = smem;  // the next item's Q (TMA), copied into TMEM by tcgen05.cp
+    uint8_t* q_smem = smem;  // ring of Q panels (TMA), copied into TMEM by tcgen05.cp
     uint8_t* kv_smem = smem + kKvOffset;
     uint8_t* xchg = smem + kXchgOffset;  // [2 slots][8 chunks][128 heads] x 16 B, written by the peer
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOffset);
@@ -224,18 +224,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* kv_empty = kv_full + kStages;      // [kStages]
     uint64_t* s_full = kv_empty + kStages;       // [kSSlots]
     uint64_t* p_full = s_full + kSSlots;         // [kSSlots]
-    uint64_t* q_sfull = p_full + kSSlots;        // [1] an item's Q landed in shared memory (TMA)
-    uint64_t* q_sfree = q_sfull + 1;             // [1] its copy into TMEM completed (shared Q reusable)
-    uint64_t* o_free = q_sfree + 1;              // [1]
+    uint64_t* q_sfull = p_full + kSSlots;        // [kQSlots] a Q panel landed in shared memory (TMA)
+    uint64_t* q_sfree = q_sfull + kQSlots;       // [kQSlots] its copy into TMEM completed (slot reusable)
+    uint64_t* o_free = q_sfree + kQSlots;        // [1]
     uint64_t* vw_free = o_free + 1;              // [kStages]
     uint64_t* x_full = vw_free + kStages;        // [2][kSmWarps] the peer's partial landed (tx bytes)
     uint64_t* x_free = x_full + 2 * kSmWarps;    // [2][kSmWarps] the peer has read my partial
     uint32_t* valid_w = reinterpret_cast<uint32_t*>(x_free + 2 * kSmWarps);  // [kStages]
     float* m_s = reinterpret_cast<float*>(smem + kRedOffset);  // [team][128 heads] running max after its last block
     float* ml_s = m_s + 2 * kH;                                 // [team][2][128 heads] (m, l) at the item's end
-    uint64_t* m_ready = reinterpret_cast<uint64_t*>(smem + kBarOffset + 512);  // [team][quarter] m_s published
+    uint64_t* m_ready = reinterpret_cast<uint64_t*>(smem + kBarOffset + 768);  // [team][quarter] m_s published
     uint64_t* ml_ready = m_ready + kSmWarps;  // [quarter] both teams' (m, l) of an item written
     uint32_t* tmem_slot = valid_w + kStages;
+    static_assert((3 * kStages + 2 * kSSlots + 2 * kQSlots + 1 + 4 * kSmWarps) * 8 + (kStages + 1) * 4 <= 768,
+                  "barrier block overlaps m_ready");
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -256,8 +258,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mbar_init(&s_full[s], 1);
             mbar_init(&p_full[s], 4);
         }
-        mbar_init(q_sfull, 1);
-        mbar_init(q_sfree, 1);
+        for (int i = 0; i < kQSlots; ++i) {
+            mbar_init(&q_sfull[i], 1);
+            mbar_init(&q_sfree[i], 1);
+        }
         mbar_init(o_free, 4);  // one arrive per stager warp (the epilogue)
         for (int i = 0; i < 2 * kSmWarps; ++i) {
             mbar_init(&x_full[i], 1);
@@ -349,6 +353,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (pt == 0) { PROBE(7) }
             }
         }
+    } else if (warp == kWarpQ) {
+        // ---------------------------------------------------------- Q panels by TMA
+        // panel P = it * 5 + pn (64 of this CTA's 288 dims of the item's 128
+        // head rows; the last one half used) into slot P % kQSlots once the
+        // panel kQSlots back has been copied into TMEM
+        if (lane == 0) {
+            uint32_t P = 0;
+            for (int64_t item = cid; item < nitems; item += ncl) {
+                int b;
+                int64_t tq, hrow;
+                decode(item, b, tq, hrow);
+                for (int pn = 0; pn < kCtaPanels; ++pn, ++P) {
+                    const int sl = P % kQSlots;
+                    mbar_wait(&q_sfree[sl], ((P / kQSlots) & 1) ^ 1);
+                    mbar_expect_tx(&q_sfull[sl], kQPanelBytes);
+                    tma_load_2d(q_smem + sl * kQPanelBytes, &qmap, &q_sfull[sl],
+                                static_cast<int32_t>(rank * kDqkHalf + pn * 64), static_cast<int32_t>(hrow));
+                }
+            }
+        }
     } else if (warp >= kWarpEpi) {
         // ---------------------------------------------------------- Q stagers + epilogue
         // Stage item it's Q once item it-1's S MMAs retired, then write item
@@ -396,16 +420,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int b;
             int64_t tq, hrow;
             decode(item, b, tq, hrow);
-            if (warp == kWarpEpi && lane == 0) {
-                // this CTA's 288 dims of the item's 128 head rows -> shared
-                // memory, once the previous item's Q has been copied to TMEM
-                if (it > 0) mbar_wait(q_sfree, (it - 1) & 1);
-                mbar_expect_tx(q_sfull, kQBytes);
-                for (int pn = 0; pn < kCtaPanels; ++pn)
-                    tma_load_2d(q_smem + pn * kQPanelBytes, &qmap, q_sfull,
-                                static_cast<int32_t>(rank * kDqkHalf + pn * 64), static_cast<int32_t>(hrow));
-            }
-            __syncwarp();
             if (it > 0) epilogue(it - 1, prev_hrow);
             prev_hrow = hrow;
         }
@@ -449,20 +463,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const uint32_t it = gj / nb;
                 const int j = static_cast<int>(gj - it * nb);
                 const int s = gj % kStages;
-                if (j == 0) {
-                    // the item's Q: shared memory -> TMEM columns 0..143, one
-                    // 128 x 256-bit copy per K step (in issue order with the
-                    // MMAs: the previous item's QK have read the old Q)
-                    mbar_wait(q_sfull, it & 1);
-                    tc_fence_after();
-                    const uint32_t qb = smem_u32(q_smem);
-#pragma unroll
-                    for (int kk = 0; kk < kQkSteps; ++kk)
-                        asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(tmem + kColQ + kk * 8),
-                                     "l"(sw128_kmajor_desc(qb + (kk >> 2) * kQPanelBytes + (kk & 3) * 32))
-                                     : "memory");
-                    umma_commit(q_sfree);
-                }
+                (void)j;
                 mbar_wait(&kv_full[s], (gj / kStages) & 1);
                 {
                     const uint32_t g = gj;
@@ -494,9 +495,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     : "memory");
                 return ok != 0;
             };
+            // Q panel P: shared memory -> TMEM columns 8 * (4 pn + t), one
+            // 128 x 256-bit copy per K step, in issue order with the MMAs (so
+            // after the previous item's QK, which read the old Q)
+            const uint32_t qb = smem_u32(q_smem);
+            auto issue_qcopy = [&](uint32_t P) {
+                const int sl = P % kQSlots;
+                const int pn = static_cast<int>(P % kCtaPanels);
+                mbar_wait(&q_sfull[sl], (P / kQSlots) & 1);
+                tc_fence_after();
+                const int steps = pn < 4 ? 4 : kQkSteps - 16;
+                for (int t = 0; t < steps; ++t)
+                    asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(tmem + kColQ + (4 * pn + t) * 8),
+                                 "l"(sw128_kmajor_desc(qb + sl * kQPanelBytes + t * 32))
+                                 : "memory");
+                umma_commit(&q_sfree[sl]);
+            };
+            const uint32_t total_q = my_items * kCtaPanels;
+            uint32_t nc = 0;  // Q panels copied
             auto qk_ready = [&](uint32_t gj) {
                 const uint32_t it = gj / nb;
-                if (gj == it * nb && !ready(q_sfull, it & 1)) return false;
+                if (gj == it * nb && nc < (it + 1) * kCtaPanels) return false;  // the item's Q not all in TMEM yet
                 return ready(&kv_full[gj % kStages], (gj / kStages) & 1);
             };
             auto pv_ready = [&](uint32_t gj) {
@@ -506,6 +525,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             };
             uint32_t nq = 0, np = 0;
             while (np < total) {
+                // the next item's Q panels once every QK of the current item is issued
+                if (nc < total_q && nq >= (nc / kCtaPanels) * nb &&
+                    ready(&q_sfull[nc % kQSlots], (nc / kQSlots) & 1)) {
+                    issue_qcopy(nc);
+                    ++nc;
+                }
                 if (nq < total && nq <= np + 2 && qk_ready(nq)) {
                     issue_qk(nq);
                     ++nq;
@@ -600,6 +625,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     mbar_wait(&m_ready[ot * 4 + quarter], on & 1);
                     mprev = m_s[ot * kH + row];
                 }
+                if ((warp & 3) == 0 && lane == 0) { const uint32_t g = gb; PROBE(8) }
                 float mnew = mprev;
                 bool rescale = false;
                 float alpha = 1.f;
@@ -657,6 +683,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int c = 0; c < kBlk / 2; ++c) pk[c] = 0u;
                 }
+                if ((warp & 3) == 0 && lane == 0) { const uint32_t g = gb; PROBE(9) }
                 tmem_st16(lane_base + s_col(gb), pk);  // P over the S columns just read
                 tmem_st_wait();
                 tc_fence_before();
