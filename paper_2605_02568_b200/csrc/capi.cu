@@ -1022,10 +1022,12 @@ int csaidx_cuda_sparse_attention(csaidx_engine* e, const void* q_bf16, const voi
     p.head_groups = static_cast<int>(heads / 128);
     p.sm_scale = sm_scale;
     LaunchScope ls(e, CSAIDX_KIND_ATTENTION);
-    // CTA-pair kernel by default (Dqk split across the pair); CSAIDX_ATTN_PAIR=0
-    // runs the single-CTA kernel (both halves of Dv compute all of S)
+    // Single-CTA kernel by default; CSAIDX_ATTN_PAIR=1 runs the CTA-pair form
+    // (Dqk split across a cluster of 2, partial scores swapped through DSMEM):
+    // same results within the tolerance, measured no faster
+    // (profiles/r02_attention.md)
     const char* pv = getenv("CSAIDX_ATTN_PAIR");
-    const bool pair = pv == nullptr || pv[0] != '0';
+    const bool pair = pv != nullptr && pv[0] == '1';
     if (pair)
         CSAIDX_CUDA_TRY(csaidx_kern::launch_sparse_mla_pair(qmap, p, e->stream), "sparse_attention");
     else

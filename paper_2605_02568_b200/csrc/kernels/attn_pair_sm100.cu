@@ -14,14 +14,27 @@
 // half of Dv as before.
 //  * Each CTA gathers only the 5 SW128 panels (320 dims) it reads: CTA 0
 //    dims 0..319 (QK 0..287, V 0..255), CTA 1 dims 256..575 (QK 288..575,
-//    V 256..511) — V is local panels 0..3 in both. 20 KiB per 32-key stage.
-//  * Q's 288 dims live in TMEM (144 columns): every QK MMA is A-from-TMEM.
-//    TMEM: Q 0..143 (of 192) + O 192..447 + S/P 448..511.
+//    V 256..511) — V is local panels 0..3 in both. 20 KiB per 32-key stage,
+//    7 stages; indices read from global memory one block ahead.
+//  * Q's 288 dims live in TMEM (144 columns; every QK MMA is A-from-TMEM),
+//    brought in per item as 5 panels through a 2-slot TMA ring and
+//    tcgen05.cp (in issue order with the MMAs). TMEM: Q 0..143, a third
+//    S/P slot 144..175, O 192..447, S/P 448..511.
+//  * Two softmax teams of 4 warps take alternate blocks (three S slots: QK
+//    runs two blocks ahead of PV); the running max passes between teams
+//    through shared memory, each team keeps its own row sum.
 //  * The exchange per block and softmax warp: 32 heads x 32 fp32 = 4 KiB
 //    each way, chunk-major so both the st.async writes and the shared loads
 //    are conflict free; slot reuse is acknowledged by a remote arrive.
-// Warp roles as in attn_sm100.cu: 0-3 softmax + epilogue, 4-7 KV
-// producers, 8 TMEM owner + MMA issuer, 9-12 Q stagers.
+//  * The MMA issuer polls: QK and PV each in order, whichever has its inputs.
+// Measured (profiles/r02_attention.md): correct, but no faster than the
+// single-CTA kernel (0.42 vs 0.40-0.43 of the sustained peak at k = 1024):
+// the per-block chain of a team (S -> exchange ~0.8-1K cycles -> max /
+// exponentials -> P, ~3.1K cycles) over two teams sets a ~1.6K-cycle block
+// period, above the ~1.1K of MMA work. Opt-in: CSAIDX_ATTN_PAIR=1.
+// Warps: 0-7 softmax (team = warp / 4, TMEM quarter = warp % 4), 8-11 KV
+// producers, 12 TMEM owner + MMA issuer, 13-16 epilogue (O / l -> bf16 rows
+// of the previous item), 17 Q TMA.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -79,6 +92,9 @@ __device__ long long g_attn_probe[kProbeBlocks * 16];
 #endif
 #ifndef CSAIDX_PAIR_L1PF
 #define CSAIDX_PAIR_L1PF 0  // (measured slower) L1 prefetch of a block's rows before its stage frees (cp.async.ca then hits L1)
+#endif
+#ifndef CSAIDX_PAIR_POLL_NS
+#define CSAIDX_PAIR_POLL_NS 64  // MMA issuer back-off when nothing is ready
 #endif
 #ifndef CSAIDX_PAIR_DBG
 #define CSAIDX_PAIR_DBG 0  // (dev timing only) 1: no exchange at all, 2: send but never wait for the peer
@@ -525,20 +541,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             };
             uint32_t nq = 0, np = 0;
             while (np < total) {
+                bool did = false;
                 // the next item's Q panels once every QK of the current item is issued
                 if (nc < total_q && nq >= (nc / kCtaPanels) * nb &&
                     ready(&q_sfull[nc % kQSlots], (nc / kQSlots) & 1)) {
                     issue_qcopy(nc);
                     ++nc;
+                    did = true;
                 }
                 if (nq < total && nq <= np + 2 && qk_ready(nq)) {
                     issue_qk(nq);
                     ++nq;
+                    did = true;
                 }
                 if (np < nq && pv_ready(np)) {
                     issue_pv(np);
                     ++np;
+                    did = true;
                 }
+                if (!did) __nanosleep(CSAIDX_PAIR_POLL_NS);  // leave the issue slots to the softmax warps
             }
         }
     } else {
@@ -616,26 +637,72 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const float mx = max3f(max3f(max3f(t3[0], t3[1], t3[2]), max3f(t3[3], t3[4], t3[5]),
                                              max3f(t3[6], t3[7], t3[8])),
                                        t3[9], t3[10]) * scale_log2;
-                // the max in use after block j-1 (the other team's), then the
-                // lazy rule: move it only when this block exceeds it by 2^8
-                float mprev = ninf;
-                if (j > 0) {
-                    const int ot = team ^ 1;
+                // The max in use after block j-1 (the other team's) and the lazy
+                // rule: move it only when this block exceeds it by 2^8. From
+                // the third block on the max rarely moves, so the exponentials
+                // are computed with the value this team last saw and checked
+                // against the other team's published one afterwards (the rare
+                // lanes that differ recompute), keeping the hand-off out of
+                // the chain.
+                const int ot = team ^ 1;
+                auto wait_other = [&]() {
                     const uint32_t on = it * (ot ? cnt1 : cnt0) + ((j - 1) >> 1);
                     mbar_wait(&m_ready[ot * 4 + quarter], on & 1);
-                    mprev = m_s[ot * kH + row];
-                }
+                    return m_s[ot * kH + row];
+                };
+                float mprev = j == 1 ? wait_other() : (j == 0 ? ninf : m);
                 if ((warp & 3) == 0 && lane == 0) { const uint32_t g = gb; PROBE(8) }
-                float mnew = mprev;
-                bool rescale = false;
-                float alpha = 1.f;
-                if (mx > mprev) {
-                    if (mprev == ninf) {
-                        mnew = mx;
-                    } else if (mx > mprev + kRescaleLog2) {
-                        alpha = ex2(mprev - mx);
-                        mnew = mx;
-                        rescale = true;
+                float mnew, alpha;
+                bool rescale;
+                auto decide = [&]() {
+                    mnew = mprev;
+                    rescale = false;
+                    alpha = 1.f;
+                    if (mx > mprev) {
+                        if (mprev == ninf) {
+                            mnew = mx;
+                        } else if (mx > mprev + kRescaleLog2) {
+                            alpha = ex2(mprev - mx);
+                            mnew = mx;
+                            rescale = true;
+                        }
+                    }
+                };
+                uint32_t pk[kBlk / 2];
+                float psum = 0.f;
+                auto exps = [&]() {  // P = 2^(s * scale_log2 - mnew) packed to bf16 pairs, and its sum
+                    if (mnew != ninf) {
+                        const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-mnew, -mnew);
+                        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+                        for (int c = 0; c < kBlk; c += 2) {
+                            const float2 a = __ffma2_rn(make_float2(x[c], x[c + 1]), sc2, nm2);
+                            float2 pr;
+                            if (c < kBlk / 2) {
+                                pr.x = ex2(a.x);
+                                pr.y = ex2(a.y);
+                            } else {
+                                pr = exp2_poly2(a);
+                            }
+                            acc = __fadd2_rn(acc, pr);
+                            const __nv_bfloat162 h2 = __floats2bfloat162_rn(pr.x, pr.y);
+                            pk[c / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+                        }
+                        psum = acc.x + acc.y;
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < kBlk / 2; ++c) pk[c] = 0u;
+                        psum = 0.f;
+                    }
+                };
+                decide();
+                exps();
+                if (j >= 2) {
+                    const float mtrue = wait_other();
+                    if (mtrue != mprev) {  // the other team moved the max at block j-1
+                        mprev = mtrue;
+                        decide();
+                        exps();
                     }
                 }
                 m_s[team * kH + row] = mnew;  // the other team's next block reads it
@@ -645,6 +712,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     if (m != ninf) l *= ex2(m - mnew);
                     m = mnew;
                 }
+                l += psum;
                 if (__any_sync(0xffffffffu, rescale)) {
                     // PV of block gb-1 landed (exact parity wait: attn_sm100.cu)
                     mbar_wait(&kv_empty[(gb - 1) % kStages], ((gb - 1) / kStages) & 1);
@@ -659,29 +727,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         tmem_st32(lane_base + kColO + c0, o);
                     }
                     tmem_st_wait();
-                }
-                uint32_t pk[kBlk / 2];
-                if (m != ninf) {
-                    const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m, -m);
-                    float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-                    for (int c = 0; c < kBlk; c += 2) {
-                        const float2 a = __ffma2_rn(make_float2(x[c], x[c + 1]), sc2, nm2);
-                        float2 pr;
-                        if (c < kBlk / 2) {
-                            pr.x = ex2(a.x);
-                            pr.y = ex2(a.y);
-                        } else {
-                            pr = exp2_poly2(a);
-                        }
-                        acc = __fadd2_rn(acc, pr);
-                        const __nv_bfloat162 h2 = __floats2bfloat162_rn(pr.x, pr.y);
-                        pk[c / 2] = *reinterpret_cast<const uint32_t*>(&h2);
-                    }
-                    l += acc.x + acc.y;
-                } else {
-#pragma unroll
-                    for (int c = 0; c < kBlk / 2; ++c) pk[c] = 0u;
                 }
                 if ((warp & 3) == 0 && lane == 0) { const uint32_t g = gb; PROBE(9) }
                 tmem_st16(lane_base + s_col(gb), pk);  // P over the S columns just read

@@ -21,8 +21,8 @@ H, DQK, DV = 128, 576, 512
 
 @pytest.fixture(autouse=True, params=["pair", "single"])
 def kernel_form(request, monkeypatch):
-    """Every case on both kernels: the CTA-pair form (default; Dqk split
-    across a cluster of 2) and the single-CTA form (CSAIDX_ATTN_PAIR=0)."""
+    """Every case on both kernels: the single-CTA form (default) and the
+    CTA-pair form (CSAIDX_ATTN_PAIR=1: Dqk split across a cluster of 2)."""
     monkeypatch.setenv("CSAIDX_ATTN_PAIR", "1" if request.param == "pair" else "0")
     return request.param
 
