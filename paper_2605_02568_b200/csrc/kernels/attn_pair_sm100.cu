@@ -278,13 +278,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mbar_init(&q_sfull[i], 1);
             mbar_init(&q_sfree[i], 1);
         }
-        mbar_init(o_free, 4);  // one arrive per stager warp (the epilogue)
+        mbar_init(o_free, 128);  // every lane of the 4 epilogue warps
         for (int i = 0; i < 2 * kSmWarps; ++i) {
             mbar_init(&x_full[i], 1);
             mbar_init(&x_free[i], 1);
         }
+        // arrivals per lane (each lane's own shared-memory write, then its
+        // arrive): the hand-offs stay ordered lane by lane
+        // (m_ready: one arrive per warp after __syncwarp; per-lane arrivals
+        // measured wrong results here, not understood — kept out)
         for (int i = 0; i < kSmWarps; ++i) mbar_init(&m_ready[i], 1);
-        for (int i = 0; i < 4; ++i) mbar_init(&ml_ready[i], 2);  // one arrive per team
+        for (int i = 0; i < 4; ++i) mbar_init(&ml_ready[i], 64);  // both teams' warps of the quarter
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == kWarpMma) tmem_alloc<kTmemCols>(tmem_slot);
@@ -425,8 +429,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 for (int v = 0; v < 4; ++v) dst[v] = pk[v];
             }
             tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(o_free);
+            mbar_arrive(o_free);
             if (rank == 0 && p.lse != nullptr)
                 p.lse[hrow_e + row] = L > 0.f ? (M + __log2f(L)) * 0.6931471805599453f : ninf;
         };
@@ -744,8 +747,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (it > 0) mbar_wait(o_free, (it - 1) & 1);
             ml_s[(team * 2 + 0) * kH + row] = m;
             ml_s[(team * 2 + 1) * kH + row] = l;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&ml_ready[quarter]);
+            mbar_arrive(&ml_ready[quarter]);
         }
     }
 

@@ -10,6 +10,7 @@ a size the sanitizer finishes in seconds to a minute.
   persistent the persistent multi-row select (SM partition)
   two_level  the group-maxima score epilogue + two-level select, incl. a
              row whose last 32-key group is partial at the end of the buffer
+  attention_pair  the same through the opt-in CTA-pair kernel (cluster of 2, DSMEM exchange)
   attention  the sparse attention over top-k indices (persistent tcgen05
              kernel: cp.async gathers, TMEM Q / S / P / O, lazy rescale),
              with padding, an empty row, out-of-range indices, large logits
@@ -107,6 +108,15 @@ def case_attention(e):
         idx[:, 1, :] = -1
         idx[:, 2, 0] = T + 3
         e.sparse_attention(q, kv, idx.contiguous(), D ** -0.5)
+
+
+def case_attention_pair(e):
+    # the opt-in CTA-pair form (read per call by csaidx_cuda_sparse_attention)
+    os.environ["CSAIDX_ATTN_PAIR"] = "1"
+    try:
+        case_attention(e)
+    finally:
+        del os.environ["CSAIDX_ATTN_PAIR"]
 
 
 if __name__ == "__main__":
