@@ -74,7 +74,8 @@ constexpr int kKvOffset = kQBytes;
 constexpr int kMaxK = 4096;                            // indices staged in shared memory
 constexpr int kIdxOffset = kKvOffset + kStages * kKvStageBytes;
 constexpr int kBarOffset = kIdxOffset + kMaxK * 4;
-constexpr int kSmemBytes = kBarOffset + 256 + 1024;    // barriers + align slack
+constexpr int kMlOffset = kBarOffset + 256;             // (m, l) per head row at an item's end
+constexpr int kSmemBytes = kMlOffset + 2 * kH * 4 + 1024;  // + align slack
 constexpr int kThreads = 416;              // 4 softmax + 4 KV producer + 1 MMA + 4 Q-staging warps
 constexpr int kProducers = 128;
 constexpr uint32_t kTmemCols = 512;
@@ -181,7 +182,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* q_free = q_tmem + 1;              // [1] every S MMA of the item done (Q reusable)
     uint64_t* o_free = q_free + 1;              // [1] the epilogue has read O
     uint64_t* vw_free = o_free + 1;             // [kStages] the softmax warps have read the valid word
-    uint32_t* valid_w = reinterpret_cast<uint32_t*>(vw_free + kStages);  // [kStages]
+    uint64_t* ml_ready = vw_free + kStages;     // [1] the softmax warps' (m, l) of an item written
+    uint32_t* valid_w = reinterpret_cast<uint32_t*>(ml_ready + 1);  // [kStages]
+    float* ml_s = reinterpret_cast<float*>(smem + kMlOffset);          // [m | l][128 heads]
     uint32_t* tmem_slot = valid_w + kStages;
 
     const int warp = threadIdx.x / 32;
@@ -202,7 +205,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar_init(q_tmem, 4);    // one arrive per Q-staging warp
         mbar_init(q_free, 1);
-        mbar_init(o_free, 4);    // one arrive per softmax warp
+        mbar_init(o_free, 256);  // every lane of the softmax and Q-staging warps (each writes half of O's columns)
+        mbar_init(ml_ready, 128);
         for (int s = 0; s < kStages; ++s) mbar_init(&vw_free[s], 4);
         fence_barrier_init();
     }
@@ -292,6 +296,38 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+        const float ninf = -INFINITY;
+        // O columns 128..255 of item ie (the softmax warps write 0..127)
+        auto epilogue_half = [&](uint32_t ie, int64_t hrow_e, int half_e) {
+            mbar_wait(ml_ready, ie & 1);
+            const float l = ml_s[kH + row];
+            const float inv_l = l > 0.f ? 1.f / l : 0.f;
+            const uint32_t gl = (ie + 1) * static_cast<uint32_t>(nb) - 1;  // the item's last block
+            mbar_wait(&kv_empty[gl % kStages], (gl / kStages) & 1);       // its PV landed (next phase needs o_free)
+            tc_fence_after();
+            __nv_bfloat16* orow = p.out + (hrow_e + row) * p.out_ld + half_e * kDvHalf;
+#pragma unroll 1
+            for (int c0 = kDvHalf / 2; c0 < kDvHalf; c0 += 32) {
+                float o[32];
+                tmem_ld32(lane_base + kColO + c0, o);
+                tmem_ld_wait();
+                uint4 pk[4];
+                uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+                for (int c = 0; c < 32; c += 2) {
+                    const __nv_bfloat162 h2 = __floats2bfloat162_rn(o[c] * inv_l, o[c + 1] * inv_l);
+                    pw[c / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+                }
+                uint4* dst = reinterpret_cast<uint4*>(orow + c0);
+#pragma unroll
+                for (int v = 0; v < 4; ++v) dst[v] = pk[v];
+            }
+            tc_fence_before();
+            mbar_arrive(o_free);
+            (void)ninf;
+        };
+        int64_t prev_hrow = 0;
+        int prev_half = 0;
         uint32_t it = 0;
         for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x, ++it) {
             int b, half;
@@ -328,7 +364,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(q_tmem);
+            if (it > 0) epilogue_half(it - 1, prev_hrow, prev_half);
+            prev_hrow = hrow;
+            prev_half = half;
         }
+        if (it > 0) epilogue_half(it - 1, prev_hrow, prev_half);
     } else if (warp == 8) {
         // ---------------------------------------------------------- MMA issuer
         if (elect_one()) {
@@ -489,14 +529,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&p_full[g & 1]);
             }
-            // epilogue: O / l -> bf16 rows of this head, lse (half 0)
+            // epilogue: O / l -> bf16 rows of this head (columns 0..127 here,
+            // 128..255 by the Q-staging warps, which read (m, l) from ml_s once
+            // the previous item's epilogue has released it), lse (half 0)
+            if (it > 0) mbar_wait(o_free, (it - 1) & 1);
+            ml_s[row] = m;
+            ml_s[kH + row] = l;
+            mbar_arrive(ml_ready);
             mbar_wait(&kv_empty[(g - 1) % kStages], ((g - 1) / kStages) & 1);  // the item's last PV landed
             tc_fence_after();
             const float inv_l = l > 0.f ? 1.f / l : 0.f;
             __nv_bfloat16* orow =
                 p.out + (hrow + row) * p.out_ld + half * kDvHalf;
 #pragma unroll 1
-            for (int c0 = 0; c0 < kDvHalf; c0 += 32) {
+            for (int c0 = 0; c0 < kDvHalf / 2; c0 += 32) {
                 float o[32];
                 tmem_ld32(lane_base + kColO + c0, o);
                 tmem_ld_wait();
@@ -512,8 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int v = 0; v < 4; ++v) dst[v] = pk[v];
             }
             tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(o_free);  // the next item's first PV may overwrite O
+            mbar_arrive(o_free);  // (with the Q-staging warps' arrivals) the next item's first PV may overwrite O
             if (half == 0 && p.lse != nullptr)
                 p.lse[hrow + row] =
                     l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : ninf;
