@@ -9,7 +9,7 @@
 // order (topk.hpp:23-26).
 //
 // Fast path (one streaming pass over the row):
-//   1. sample: evenly spaced 512-byte segments (~1/16 of the row), held in
+//   1. sample: evenly spaced 512-byte segments (~64 above the threshold), held in
 //      registers; a value-linear histogram over the sample's range (plus a
 //      refinement pass inside a coarse rank bin) picks a threshold expected
 //      to keep ~2k entries of the row;
@@ -57,6 +57,23 @@ constexpr int kGatherPer = 16;     // survivors per thread the fused gather hand
 // k (it reads ~k groups instead of the whole row)
 constexpr int kTwoLevelMinGroupsPerK = 2;
 constexpr int kSampleSegs = 64;    // 512-byte segments: <= 8192 sampled keys per row
+// Sample size: by default enough 128-key segments that the threshold sits
+// near rank CSAIDX_SAMPLE_RANK of the sample (n / (2 target) keys per
+// segment: 1/16 of the row at k = 512, 1/32 at k = 1024, 1/8 at k = 256);
+// CSAIDX_SAMPLE_DIV > 0 fixes one segment per that many keys instead (round
+// 1: 2048). Measured (profiles/r02_experiments.md): k = 256 rows 0.149 ->
+// 0.071 ms (sampled-threshold misses 12 -> 0 per 2048 rows), C3 select -2-3%,
+// C2 unchanged.
+#ifndef CSAIDX_SAMPLE_DIV
+#define CSAIDX_SAMPLE_DIV 0
+#endif
+#ifndef CSAIDX_SAMPLE_RANK
+#define CSAIDX_SAMPLE_RANK 64        // (CSAIDX_SAMPLE_DIV == 0) expected sample rank of the threshold
+#endif
+#ifndef CSAIDX_TAU_BINS
+#define CSAIDX_TAU_BINS 1024         // value-linear bins of the sampled threshold
+#endif
+constexpr int kTauBins = CSAIDX_TAU_BINS;
 
 #ifndef CSAIDX_FIN_BINS
 #define CSAIDX_FIN_BINS 1024
@@ -650,22 +667,32 @@ __device__ void write_row(const SelectParams& p, int b, int64_t row_id, int take
     }
 }
 
-// Sampled threshold of a long row (n > cand_cap): ~n/16 scores as evenly
-// spaced 512-byte segments (one float4 per lane, <= 8192 values) held in
-// registers, value-linear histograms over the sample's range (plus one
-// refinement pass inside a coarse rank bin) -> a threshold expected to keep
-// ~2k of the row's entries. Uses hist (kBins words), res, wsum, counter.
+// Sampled threshold of a long row (n > cand_cap): evenly spaced 512-byte
+// segments (one float4 per lane, <= 8192 values; about 64 sampled scores lie
+// above the threshold) held in registers, value-linear histograms over the
+// sample's range (plus one refinement pass inside a coarse rank bin) -> a
+// threshold expected to keep ~2k of the row's entries. Uses hist (kTauBins
+// words), res, wsum, counter.
 __device__ __forceinline__ float sample_threshold(const float* row, int64_t n, int k, const Layout& L, uint32_t* hist,
                                                uint32_t* res, uint32_t* wsum, uint32_t* counter) {
     const int lane = gtid() & 31;
     // sample evenly spaced 512-byte segments (one float4 per lane,
     //    ~1/16 of the row, <= 8192 values), held in registers; each
     //    warp issues all of its loads before consuming them
-    int nseg = static_cast<int>(n / 2048);
-    if (nseg > kSampleSegs) nseg = kSampleSegs;
-    if (nseg < 1) nseg = 1;
     // 32-bit arithmetic: a row's legal length is < 2^31 (n <= T)
     const int n32 = static_cast<int>(n);
+    // ~2k survivors: a comfortable margin over k (misses -> the slow
+    // exact fallback) while the shared list stays at <= 4k entries
+    const int target = (2 * k < (L.cand_cap * 3) / 4) ? 2 * k : (L.cand_cap * 3) / 4;
+#if CSAIDX_SAMPLE_DIV > 0
+    int nseg = static_cast<int>(n / CSAIDX_SAMPLE_DIV);
+#else
+    // sample size for a rank of ~CSAIDX_SAMPLE_RANK inside the sample,
+    // whatever k: segments of 128 keys, ns / n = rank / target
+    int nseg = static_cast<int>((static_cast<int64_t>(n32) * CSAIDX_SAMPLE_RANK) / (128 * static_cast<int64_t>(target)));
+#endif
+    if (nseg > kSampleSegs) nseg = kSampleSegs;
+    if (nseg < 1) nseg = 1;
     const int64_t seg_stride = (n32 / nseg) & ~3;
     constexpr int kSegsPerWarp = kSampleSegs / kWarps;  // 8
     const int w = gtid() >> 5;
@@ -692,7 +719,7 @@ __device__ __forceinline__ float sample_threshold(const float* row, int64_t n, i
         res[6] = 0xffffffffu;
         res[7] = 0u;
     }
-    for (int i = gtid(); i < kBins; i += kThreads) hist[i] = 0;
+    for (int i = gtid(); i < kTauBins; i += kThreads) hist[i] = 0;
     csync();
     kmin = __reduce_min_sync(0xffffffffu, kmin);
     kmax = __reduce_max_sync(0xffffffffu, kmax);
@@ -702,9 +729,6 @@ __device__ __forceinline__ float sample_threshold(const float* row, int64_t n, i
     }
     csync();
     const int ns = 128 * nseg;
-    // ~2k survivors: a comfortable margin over k (misses -> the slow
-    // exact fallback) while the shared list stays at <= 4k entries
-    const int target = (2 * k < (L.cand_cap * 3) / 4) ? 2 * k : (L.cand_cap * 3) / 4;
     int r = (target * ns) / n32;  // <= 6144 * 8192: no overflow
     if (r < 1) r = 1;
     // The sample's rank-r value by value-linear histograms over
@@ -717,10 +741,10 @@ __device__ __forceinline__ float sample_threshold(const float* row, int64_t n, i
     float tau_f = smin;
 #pragma unroll 1
     for (int pass = 0; pass < 2; ++pass) {
-        float scale = static_cast<float>(kBins) / (hi - lo);
+        float scale = static_cast<float>(kTauBins) / (hi - lo);
         if (!(hi > lo) || !isfinite(scale)) break;  // degenerate: keep tau = lo
         if (pass > 0) {
-            for (int i = gtid(); i < kBins; i += kThreads) hist[i] = 0;
+            for (int i = gtid(); i < kTauBins; i += kThreads) hist[i] = 0;
             if (gtid() == 0) res[0] = res[1] = res[2] = 0u;
             csync();
         }
@@ -732,16 +756,16 @@ __device__ __forceinline__ float sample_threshold(const float* row, int64_t n, i
                 for (int c = 0; c < 4; ++c) {
                     const float v = vs[c];
                     if (v >= lo && v <= hi)
-                        atomicAdd(&hist[static_cast<int>(fminf((v - lo) * scale, static_cast<float>(kBins - 1)))],
+                        atomicAdd(&hist[static_cast<int>(fminf((v - lo) * scale, static_cast<float>(kTauBins - 1)))],
                                   1u);
                 }
             }
         }
         csync();
-        find_bin(hist, kBins, rr, res, wsum);
+        find_bin(hist, kTauBins, rr, res, wsum);
         const uint32_t bin = res[0], above = res[1], cnt = res[2];
         csync();
-        const float width = (hi - lo) / static_cast<float>(kBins);
+        const float width = (hi - lo) / static_cast<float>(kTauBins);
         const float blo = lo + static_cast<float>(bin) * width;
         tau_f = blo > lo ? blo : lo;
         if (cnt * 8u <= rr || cnt <= 4u) break;  // fine enough

@@ -17,8 +17,10 @@ for round in 1 2; do
 for a in "$@"; do
   name=${a%%:*}; var=0; [[ $a == *:* ]] && var=${a##*:}
   build $name
-  CSAIDX_SELECT_VARIANT=$var timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | \
-    python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$a', round(d['ms_per_step'],2), round(d['kernels_ms_per_step']['select'],2), d['clocks']['sm_mhz'])"
+  for wl in ${AB_WORKLOADS:-c3}; do
+  CSAIDX_SELECT_VARIANT=$var timeout 300 python bench.py --workload $wl --steps 5 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | \
+    python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$a $wl', round(d['ms_per_step'],2), round(d['kernels_ms_per_step']['select'],2), d['clocks']['sm_mhz'])"
+  done
 done
 done
 cp /tmp/_select_orig.cu paper_2605_02568_b200/csrc/kernels/select_sm100.cu
