@@ -70,6 +70,9 @@ constexpr int kSampleSegs = 64;    // 512-byte segments: <= 8192 sampled keys pe
 #ifndef CSAIDX_SAMPLE_RANK
 #define CSAIDX_SAMPLE_RANK 64        // (CSAIDX_SAMPLE_DIV == 0) expected sample rank of the threshold
 #endif
+#ifndef CSAIDX_TARGET_X4
+#define CSAIDX_TARGET_X4 8           // expected survivors of the threshold = k * this / 4
+#endif
 #ifndef CSAIDX_TAU_BINS
 #define CSAIDX_TAU_BINS 1024         // value-linear bins of the sampled threshold
 #endif
@@ -683,7 +686,8 @@ __device__ __forceinline__ float sample_threshold(const float* row, int64_t n, i
     const int n32 = static_cast<int>(n);
     // ~2k survivors: a comfortable margin over k (misses -> the slow
     // exact fallback) while the shared list stays at <= 4k entries
-    const int target = (2 * k < (L.cand_cap * 3) / 4) ? 2 * k : (L.cand_cap * 3) / 4;
+    const int want = (k * CSAIDX_TARGET_X4) / 4;
+    const int target = (want < (L.cand_cap * 3) / 4) ? want : (L.cand_cap * 3) / 4;
 #if CSAIDX_SAMPLE_DIV > 0
     int nseg = static_cast<int>(n / CSAIDX_SAMPLE_DIV);
 #else
