@@ -510,8 +510,9 @@ def main():
                "unit": "legal pairs/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "pcie_gbs": (h2d + d2h) / (e2e_ms / 1000.0) / 1e9,
-               "bound": ("q rows are rounded fp32 -> bf16 on the host cores into pinned slabs (a producer "
-                         "thread runs up to 8 chunks ahead) and cross PCIe once at 2 B/entry; H2D of chunk c+1 "
+               "bound": ("q rows are rounded fp32 -> bf16 on the host cores, 8 MiB pieces through a 4-piece pinned "
+                         "ring copied as soon as each is written (the DMA reads them from the host LLC), and cross "
+                         "PCIe once at 2 B/entry; H2D of chunk c+1 "
                          "and D2H of chunk c-1 overlap chunk c's kernels" if host_round else
                          "PCIe: the fp32 q rows (the reference API's input type) cross the bus once; H2D of "
                          "chunk c+1 and D2H of chunk c-1 overlap chunk c's kernels"),

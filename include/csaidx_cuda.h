@@ -83,6 +83,12 @@ int csaidx_engine_await(csaidx_engine* e, int slot);
 /* Host-side wait for the slot's latest signal (e.g. before reusing a pinned
  * staging buffer whose copy was enqueued before the signal). */
 int csaidx_engine_sync_slot(csaidx_engine* e, int slot);
+/* A copy enqueued on an existing lane (1..3) without switching the current
+ * lane, then (slot >= 0) the slot's event recorded after it on that lane.
+ * For a second host thread feeding a lane while the calling thread drives
+ * the engine (the host-rounding ring of csaidx_host_run_chunked_*); the two
+ * threads must use disjoint slots. */
+int csaidx_engine_copy_on_lane(csaidx_engine* e, int lane, int slot, void* dst, const void* src, size_t bytes);
 /* The current lane waits (on the device) for all work enqueued so far on
  * `stream` (a cudaStream_t; NULL = the legacy default stream, which itself
  * orders after every blocking stream). The device-pointer driver entries

@@ -97,6 +97,7 @@ CUDA_SYMBOLS = {
     "csaidx_engine_signal": (c_int, [c_void_p, c_int]),
     "csaidx_engine_await": (c_int, [c_void_p, c_int]),
     "csaidx_engine_sync_slot": (c_int, [c_void_p, c_int]),
+    "csaidx_engine_copy_on_lane": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_size_t]),
     "csaidx_engine_await_stream": (c_int, [c_void_p, c_void_p]),
     "csaidx_engine_set_index_sink": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64]),
     "csaidx_cuda_ipc_handle": (c_int, [c_void_p, c_void_p, c_void_p, POINTER(c_uint64)]),

@@ -321,6 +321,20 @@ int csaidx_engine_sync_slot(csaidx_engine* e, int slot) {
     return CSAIDX_OK;
 }
 
+int csaidx_engine_copy_on_lane(csaidx_engine* e, int lane, int slot, void* dst, const void* src, size_t bytes) {
+    if (int rc = set_device(e)) return rc;
+    if (lane < 1 || lane > 3 || e->lanes[lane] == nullptr)
+        return fail(CSAIDX_INVALID_ARGUMENT, "copy_on_lane: lane must be 1..3 and already in use");
+    if (slot >= 192) return fail(CSAIDX_INVALID_ARGUMENT, "event slot out of range");
+    if (bytes != 0) CSAIDX_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, e->lanes[lane]), "cudaMemcpyAsync");
+    if (slot >= 0) {
+        if (e->slots[slot] == nullptr)
+            CSAIDX_CUDA_TRY(cudaEventCreateWithFlags(&e->slots[slot], cudaEventDisableTiming), "cudaEventCreate");
+        CSAIDX_CUDA_TRY(cudaEventRecord(e->slots[slot], e->lanes[lane]), "cudaEventRecord");
+    }
+    return CSAIDX_OK;
+}
+
 int csaidx_engine_await_stream(csaidx_engine* e, void* stream) {
     if (int rc = set_device(e)) return rc;
     cudaStream_t src = stream == nullptr ? cudaStreamLegacy : static_cast<cudaStream_t>(stream);

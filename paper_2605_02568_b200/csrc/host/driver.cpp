@@ -359,6 +359,11 @@ PinnedSlabs& pinned_slabs() {
     return s;
 }
 
+PinnedSlabs& pinned_ring() {
+    thread_local PinnedSlabs s;  // the ring pieces of CSAIDX_HOST_RING=1
+    return s;
+}
+
 // State shared by the host-rounding producer thread and the thread that
 // drives the lanes: the producer rounds chunk o's q rows into slab
 // o % slabs once the copy of chunk o - slabs out of it has completed.
@@ -471,10 +476,24 @@ void run_chunked_rows_impl(const HostView& in, const ProblemDims& dims, const Dr
     const int hslabs = host_slab_count();  // <= 32: the copy-done slots
     std::vector<uint16_t*> hslab(static_cast<size_t>(hslabs), nullptr);
     bool host_round = dtype == CSAIDX_DTYPE_BF16 && host_round_enabled();
+    // ring mode: pieces of piece_elems bf16 through ring_n pinned buffers
+    const bool ring = host_round && host_ring_enabled();
+    const int ring_n = host_ring_pieces();
+    const size_t piece_elems = static_cast<size_t>(host_piece_bytes()) / sizeof(uint16_t);
+    constexpr int kRingSlot0 = 160;  // event slots 160.. belong to the rounding thread
+    std::vector<uint16_t*> rslab(static_cast<size_t>(ring_n), nullptr);
     if (host_round) {
         try {
-            for (int i = 0; i < hslabs; ++i)
-                hslab[static_cast<size_t>(i)] = pinned_slabs().get(e, i, hslabs, slab_elems * sizeof(uint16_t));
+            if (ring) {
+                for (int i = 0; i < ring_n; ++i)
+                    rslab[static_cast<size_t>(i)] = pinned_ring().get(e, i, ring_n, piece_elems * sizeof(uint16_t));
+                // the copy-in lane exists before the rounding thread enqueues on it
+                check(csaidx_engine_use_lane(e, 1));
+                check(csaidx_engine_use_lane(e, 0));
+            } else {
+                for (int i = 0; i < hslabs; ++i)
+                    hslab[static_cast<size_t>(i)] = pinned_slabs().get(e, i, hslabs, slab_elems * sizeof(uint16_t));
+            }
         } catch (const std::exception&) {
             host_round = false;  // no pinned staging available: round on the device
         }
@@ -488,9 +507,10 @@ void run_chunked_rows_impl(const HostView& in, const ProblemDims& dims, const Dr
     if (host_round) {
         rounder.th = std::thread([&] {
             try {
+                size_t rc = 0;  // ring pieces issued
                 for (size_t o = 0; o < plan.order.size(); ++o) {
                     const double t0 = now_ms();
-                    if (o >= static_cast<size_t>(hslabs)) {
+                    if (!ring && o >= static_cast<size_t>(hslabs)) {
                         {
                             std::unique_lock<std::mutex> g(rounder.mu);
                             rounder.cv.wait(g, [&] { return rounder.stop || rounder.enqueued > o - hslabs; });
@@ -505,6 +525,25 @@ void run_chunked_rows_impl(const HostView& in, const ProblemDims& dims, const Dr
                     Bf16Flags f;
                     for (int64_t b = 0; b < B; ++b) {
                         const int64_t hrow = in.local_rows ? b * out_rows + plan.out_row0[c] : b * dims.seq_len + s0;
+                        if (ring) {
+                            // piece by piece: round into the ring slot (regular
+                            // stores, the lines stay cached) and copy it at once
+                            const size_t n = static_cast<size_t>(rows * qrow);
+                            const int64_t lrow = b * out_rows + plan.out_row0[c];
+                            for (size_t off = 0; off < n; off += piece_elems, ++rc) {
+                                const int slot = static_cast<int>(rc % static_cast<size_t>(ring_n));
+                                if (rc >= static_cast<size_t>(ring_n)) check(csaidx_engine_sync_slot(e, kRingSlot0 + slot));
+                                const size_t len = std::min(piece_elems, n - off);
+                                const Bf16Flags fb = host_to_bf16(in.q + hrow * qrow + off, rslab[static_cast<size_t>(slot)],
+                                                                  len, 0);
+                                f.nonfinite = f.nonfinite || fb.nonfinite;
+                                f.inexact = f.inexact || fb.inexact;
+                                if (f.nonfinite || f.inexact) break;  // reported below; nothing more to send
+                                check(csaidx_engine_copy_on_lane(e, 1, kRingSlot0 + slot, q.as<uint16_t>() + lrow * qrow + off,
+                                                                 rslab[static_cast<size_t>(slot)], len * sizeof(uint16_t)));
+                            }
+                            continue;
+                        }
                         const Bf16Flags fb = host_to_bf16(in.q + hrow * qrow, hslab[o % hslabs] + b * rows * qrow,
                                                           static_cast<size_t>(rows * qrow));
                         f.nonfinite = f.nonfinite || fb.nonfinite;
@@ -555,8 +594,9 @@ void run_chunked_rows_impl(const HostView& in, const ProblemDims& dims, const Dr
         for (int64_t b = 0; b < B; ++b) {
             const int64_t lrow = b * out_rows + plan.out_row0[c];
             const int64_t hrow = in.local_rows ? lrow : b * dims.seq_len + s0;
-            check(csaidx_cuda_copy(e, q.as<uint16_t>() + lrow * qrow, hslab[o % hslabs] + b * rows * qrow,
-                                   static_cast<size_t>(rows * qrow) * sizeof(uint16_t)));
+            if (!ring)  // (ring: the rounding thread has enqueued the pieces on this lane)
+                check(csaidx_cuda_copy(e, q.as<uint16_t>() + lrow * qrow, hslab[o % hslabs] + b * rows * qrow,
+                                       static_cast<size_t>(rows * qrow) * sizeof(uint16_t)));
             check(csaidx_cuda_copy(e, w.as<float>() + lrow * dims.heads, in.w + hrow * dims.heads,
                                    static_cast<size_t>(rows * dims.heads) * sizeof(float)));
         }

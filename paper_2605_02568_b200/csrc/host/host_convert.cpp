@@ -42,8 +42,7 @@ bool nt_stores() {
 }
 
 __attribute__((target("avx512f,avx512bw"))) void avx512_range(const float* src, uint16_t* dst, size_t n,
-                                                               uint32_t& bad_exp, uint32_t& low_bits) {
-    const bool nt = nt_stores();
+                                                               uint32_t& bad_exp, uint32_t& low_bits, bool nt) {
     const __m512i bias = _mm512_set1_epi32(0x7fff), one = _mm512_set1_epi32(1);
     const __m512i expm = _mm512_set1_epi32(0x7f800000), lowm = _mm512_set1_epi32(0xffff);
     __mmask16 nonfin = 0, inexact = 0;
@@ -184,7 +183,21 @@ int host_slab_count() {
 
 int64_t host_piece_bytes() {
     const char* v = std::getenv("CSAIDX_HOST_PIECE_KB");
-    return int64_t{1024} * std::clamp<int64_t>(v != nullptr ? std::atoll(v) : 4096, 64, 1 << 20);
+    return int64_t{1024} * std::clamp<int64_t>(v != nullptr ? std::atoll(v) : 8192, 64, 1 << 20);
+}
+
+bool host_ring_enabled() {
+    // Default on (CSAIDX_HOST_RING=0: whole-chunk slabs with non-temporal
+    // stores). C3 end to end on three boxes: 130.2-131.9 ms vs 132.3-138.5 ms
+    // with 8 MiB pieces through a 4-piece ring; 2 MiB pieces lose to the
+    // per-piece overhead (162-165 ms).
+    const char* v = std::getenv("CSAIDX_HOST_RING");
+    return v == nullptr || std::string(v) != "0";
+}
+
+int host_ring_pieces() {
+    const char* v = std::getenv("CSAIDX_HOST_RING_PIECES");
+    return std::clamp(v != nullptr ? std::atoi(v) : 4, 2, 32);
 }
 
 uint16_t host_bf16_rne(float x) {
@@ -201,7 +214,8 @@ void host_parallel_for(int parts, const std::function<void(int)>& fn) {
     pool().run(parts, fn);
 }
 
-Bf16Flags host_to_bf16(const float* src, uint16_t* dst, size_t n) {
+Bf16Flags host_to_bf16(const float* src, uint16_t* dst, size_t n, int nt_mode) {
+    const bool nt = nt_mode < 0 ? nt_stores() : nt_mode != 0;
     // parts of >= 256 KiB of source, 16-element aligned, a few per thread
     constexpr size_t kMinPart = size_t{1} << 16;
     const size_t want = static_cast<size_t>(host_threads()) * 4;
@@ -213,7 +227,7 @@ Bf16Flags host_to_bf16(const float* src, uint16_t* dst, size_t n) {
         const size_t a = std::min(n, per * static_cast<size_t>(p));
         const size_t b = p + 1 == static_cast<int>(parts) ? n : std::min(n, a + per);
         if (vec)
-            avx512_range(src + a, dst + a, b - a, bad[p], low[p]);
+            avx512_range(src + a, dst + a, b - a, bad[p], low[p], nt);
         else
             scalar_range(src + a, dst + a, b - a, bad[p], low[p]);
     });

@@ -20,7 +20,9 @@ struct Bf16Flags {
 
 // Rounds src[0, n) into dst[0, n) on the host worker pool (AVX-512 when the
 // CPU has it, else scalar; bit-identical either way).
-Bf16Flags host_to_bf16(const float* src, uint16_t* dst, size_t n);
+// nt: 1 = non-temporal stores (the destination is read back from DRAM later),
+// 0 = regular stores (it is read again while still cached), -1 = CSAIDX_HOST_NT.
+Bf16Flags host_to_bf16(const float* src, uint16_t* dst, size_t n, int nt = -1);
 
 // Scalar reference of one element (tests, tails).
 uint16_t host_bf16_rne(float x);
@@ -40,5 +42,12 @@ bool host_round_enabled();
 // and the bf16 bytes rounded and copied per piece (CSAIDX_HOST_PIECE_KB).
 int host_slab_count();
 int64_t host_piece_bytes();
+// Ring mode of the pipeline (default; CSAIDX_HOST_RING=0 turns it off): q
+// rounded piece by piece (CSAIDX_HOST_PIECE_KB of bf16, default 8 MiB) into
+// a small pinned ring (CSAIDX_HOST_RING_PIECES, default 4; regular stores)
+// whose pieces are copied right away, so the DMA reads them while they are
+// still in the host's last-level cache.
+bool host_ring_enabled();
+int host_ring_pieces();
 
 }  // namespace csaidx::detail
