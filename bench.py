@@ -484,11 +484,22 @@ def main():
         api.run_chunked_rows(qh, kch, wh, dims, ecfg, mine, oi, ov, local_rows=True)  # warm-up
         if world > 1:
             dist.barrier()
+        e2e_probe = os.environ.get("CSAIDX_BENCH_E2E_PROBE") == "1"  # (dev) kernel times + clocks inside e2e
+        if e2e_probe:
+            drv.reset()
+            drv.profiling(True)
+            eclk = ClockSampler(local)
+            eclk.start()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             api.run_chunked_rows(qh, kch, wh, dims, ecfg, mine, oi, ov, local_rows=True)
         torch.cuda.synchronize()
         e2e_ms = (time.perf_counter() - t0) * 1000 / args.e2e_steps
+        if e2e_probe:
+            ek = {name: drv.get(kd) for name, kd in kinds.items()}
+            print(json.dumps({"e2e_kernels_ms_per_step": {n: v[1] / args.e2e_steps for n, v in ek.items()},
+                              "e2e_clocks": eclk.stop()}), file=sys.stderr)
+            drv.profiling(False)
         if world > 1:
             h = torch.tensor([e2e_ms], dtype=torch.float64)
             if backend == "nccl":

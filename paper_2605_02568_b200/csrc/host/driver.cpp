@@ -359,6 +359,11 @@ PinnedSlabs& pinned_slabs() {
     return s;
 }
 
+PinnedSlabs& pinned_kc() {
+    thread_local PinnedSlabs s;  // bf16 kc staging (the copy then runs async at full PCIe speed)
+    return s;
+}
+
 PinnedSlabs& pinned_ring() {
     thread_local PinnedSlabs s;  // the ring pieces of CSAIDX_HOST_RING=1
     return s;
@@ -644,12 +649,20 @@ void run_chunked_rows_impl(const HostView& in, const ProblemDims& dims, const Dr
             if (dtype == CSAIDX_DTYPE_BF16) {
                 // kc is small: rounded on the host (bit-identical to the
                 // device rounding), which also tells representability up front
-                std::vector<uint16_t> kc16(static_cast<size_t>(dims.kc_elems()));
-                const Bf16Flags f = host_to_bf16(in.kc, kc16.data(), kc16.size());
+                const size_t kn = static_cast<size_t>(dims.kc_elems());
+                uint16_t* kc16 = nullptr;
+                std::vector<uint16_t> kc16v;  // pageable fallback when pinned staging is unavailable
+                try {
+                    kc16 = pinned_kc().get(e, 0, 1, kn * sizeof(uint16_t));
+                } catch (const std::exception&) {
+                    kc16v.resize(kn);
+                    kc16 = kc16v.data();
+                }
+                const Bf16Flags f = host_to_bf16(in.kc, kc16, kn);
                 if (f.nonfinite) throw std::invalid_argument("IndexerInputs: non-finite entry in q/kc");
                 if (f.inexact && strict) throw std::invalid_argument("operand is not bf16-representable (strict mode)");
                 if (f.inexact) throw OperandsNotBf16();
-                kc.upload(kc16.data(), kc16.size() * sizeof(uint16_t));
+                kc.upload(kc16, kn * sizeof(uint16_t));
             } else {
                 kc.upload(in.kc, static_cast<size_t>(dims.kc_elems()) * sizeof(float));
             }
