@@ -374,9 +374,10 @@ def test_sentinel_contract_exhaustive(orc):
 
 def test_host_rounding_matches_device_rounding(orc, monkeypatch):
     """The pipelined host entry rounds q on the host cores (CSAIDX_HOST_ROUND,
-    default) or on the device: same bytes, incl. B=2, rank-local rows and more
-    chunks than staging slabs; non-finite and (strict) inexact q rows raise
-    invalid_argument either way."""
+    default; through the pinned piece ring or whole-chunk slabs) or on the
+    device: same bytes, incl. B=2, rank-local rows, more chunks than staging
+    slabs and many (partial) ring pieces per chunk; non-finite and (strict)
+    inexact q rows raise invalid_argument every way."""
     B, S, m, H, D, k = 2, 8192, 4, 64, 128, 64
     q, kc, w = orc.generate_inputs(B, S, m, H, D, 3, bf16=True)
     dims = api.ProblemDims.create(B, S, m, H, D, k)
@@ -389,8 +390,17 @@ def test_host_rounding_matches_device_rounding(orc, monkeypatch):
     wl = np.ascontiguousarray(np.concatenate([w3[:, s:s + 256] for s in starts], axis=1))
     kcf = np.asarray(kc, np.float32)
     outs = {}
-    for mode in ("0", "1"):
-        monkeypatch.setenv("CSAIDX_HOST_ROUND", mode)
+    # host rounding off / on through the default ring / through whole-chunk
+    # slabs / through a 2-piece ring of 96 KiB pieces (many pieces per chunk,
+    # a partial last one)
+    variants = {"0": {"CSAIDX_HOST_ROUND": "0"}, "1": {"CSAIDX_HOST_ROUND": "1"},
+                "slabs": {"CSAIDX_HOST_ROUND": "1", "CSAIDX_HOST_RING": "0"},
+                "small-ring": {"CSAIDX_HOST_ROUND": "1", "CSAIDX_HOST_PIECE_KB": "96", "CSAIDX_HOST_RING_PIECES": "2"}}
+    for mode, env in variants.items():
+        for kname in ("CSAIDX_HOST_RING", "CSAIDX_HOST_PIECE_KB", "CSAIDX_HOST_RING_PIECES"):
+            monkeypatch.delenv(kname, raising=False)
+        for kname, v in env.items():
+            monkeypatch.setenv(kname, v)
         oi = np.empty((B, rows, k), np.int64)
         ov = np.empty((B, rows, k), np.float32)
         api.run_chunked_rows(q4, kcf, w3, dims, cfg, starts, oi, ov)
@@ -399,9 +409,13 @@ def test_host_rounding_matches_device_rounding(orc, monkeypatch):
         api.run_chunked_rows(ql, kcf, wl, dims, cfg, starts, li, lv, local_rows=True)
         assert np.array_equal(oi, li) and np.array_equal(bits(ov), bits(lv))
         outs[mode] = (oi, ov)
-    assert np.array_equal(outs["0"][0], outs["1"][0]) and np.array_equal(bits(outs["0"][1]), bits(outs["1"][1]))
-    for mode in ("0", "1"):
-        monkeypatch.setenv("CSAIDX_HOST_ROUND", mode)
+    for mode in variants:
+        assert np.array_equal(outs["0"][0], outs[mode][0]) and np.array_equal(bits(outs["0"][1]), bits(outs[mode][1]))
+    for mode, env in variants.items():
+        for kname in ("CSAIDX_HOST_RING", "CSAIDX_HOST_PIECE_KB", "CSAIDX_HOST_RING_PIECES"):
+            monkeypatch.delenv(kname, raising=False)
+        for kname, v in env.items():
+            monkeypatch.setenv(kname, v)
         bad = q4.copy()
         bad[1, starts[13] + 5, 7, 3] = np.nan
         oi = np.empty((B, rows, k), np.int64)
