@@ -41,6 +41,16 @@ bool nt_stores() {
     return v;
 }
 
+// bytes ahead of the load the source is prefetched (CSAIDX_HOST_PREFETCH,
+// default one 4 KiB page)
+int prefetch_distance() {
+    static const int v = [] {
+        const char* e = std::getenv("CSAIDX_HOST_PREFETCH");
+        return e != nullptr ? std::clamp(std::atoi(e), 0, 1 << 16) : 4096;
+    }();
+    return v;
+}
+
 __attribute__((target("avx512f,avx512bw"))) void avx512_range(const float* src, uint16_t* dst, size_t n,
                                                                uint32_t& bad_exp, uint32_t& low_bits, bool nt) {
     const __m512i bias = _mm512_set1_epi32(0x7fff), one = _mm512_set1_epi32(1);
@@ -55,7 +65,7 @@ __attribute__((target("avx512f,avx512bw"))) void avx512_range(const float* src, 
     for (; i + 16 <= n; i += 16) {
         // one page ahead: the hardware prefetcher stops at 4 KiB boundaries
         // (pinned caller buffers are 4 KiB pages); +40% measured on the box
-        _mm_prefetch(reinterpret_cast<const char*>(src + i) + 4096, _MM_HINT_T0);
+        _mm_prefetch(reinterpret_cast<const char*>(src + i) + prefetch_distance(), _MM_HINT_T0);
         const __m512i u = _mm512_loadu_si512(reinterpret_cast<const void*>(src + i));
         const __m512i lsb = _mm512_and_si512(_mm512_srli_epi32(u, 16), one);
         const __m512i r = _mm512_srli_epi32(_mm512_add_epi32(u, _mm512_add_epi32(bias, lsb)), 16);
