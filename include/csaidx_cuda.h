@@ -169,6 +169,9 @@ int csaidx_cuda_memset(csaidx_engine* e, void* dst, int value, size_t bytes);
 /* Page-locked host staging memory (cudaHostAlloc) for asynchronous copies. */
 int csaidx_cuda_host_alloc(csaidx_engine* e, size_t bytes, void** ptr);
 int csaidx_cuda_host_free(csaidx_engine* e, void* ptr);
+/* *pinned = 1 when ptr lies in page-locked host memory known to CUDA
+ * (cudaHostAlloc / cudaHostRegister), else 0. */
+int csaidx_cuda_host_is_pinned(const void* ptr, int* pinned);
 
 /* fp32 -> bf16 (RNE) staging of q / kc (IndexerInputs::validated,
  * types.cpp:73-92: rejects non-finite; strict also rejects values that are

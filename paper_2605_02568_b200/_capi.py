@@ -111,6 +111,7 @@ CUDA_SYMBOLS = {
     "csaidx_cuda_memset": (c_int, [c_void_p, c_void_p, c_int, c_size_t]),
     "csaidx_cuda_host_alloc": (c_int, [c_void_p, c_size_t, POINTER(c_void_p)]),
     "csaidx_cuda_host_free": (c_int, [c_void_p, c_void_p]),
+    "csaidx_cuda_host_is_pinned": (c_int, [c_void_p, POINTER(c_int)]),
     "csaidx_cuda_to_bf16": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int]),
     "csaidx_cuda_score": (
         c_int,

@@ -588,6 +588,16 @@ int csaidx_cuda_host_alloc(csaidx_engine* e, size_t bytes, void** ptr) {
     return CSAIDX_OK;
 }
 
+int csaidx_cuda_host_is_pinned(const void* ptr, int* pinned) {
+    if (pinned == nullptr) return fail(CSAIDX_INVALID_ARGUMENT, "host_is_pinned: null out pointer");
+    *pinned = 0;
+    cudaPointerAttributes a{};
+    if (ptr != nullptr && cudaPointerGetAttributes(&a, ptr) == cudaSuccess)
+        *pinned = (a.type == cudaMemoryTypeHost) ? 1 : 0;
+    cudaGetLastError();  // a pageable pointer is not an error worth keeping
+    return CSAIDX_OK;
+}
+
 int csaidx_cuda_host_free(csaidx_engine* e, void* ptr) {
     if (int rc = set_device(e)) return rc;
     if (ptr != nullptr) CSAIDX_CUDA_TRY(cudaFreeHost(ptr), "cudaFreeHost");

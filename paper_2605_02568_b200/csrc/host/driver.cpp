@@ -503,6 +503,22 @@ void run_chunked_rows_impl(const HostView& in, const ProblemDims& dims, const Dr
             host_round = false;  // no pinned staging available: round on the device
         }
     }
+    // fp32 tail: the last chunks of the processing order (the lightest on
+    // the GPU) cross PCIe as fp32 at the start of the call, beside the early
+    // heavy chunks' bf16 pieces, and are rounded on the device when their
+    // turn comes; the rounding thread then finishes that much earlier, which
+    // is what bounds the end of the call on hosts with slower memory.
+    // (pinned q only: pageable copies would block the calling thread)
+    size_t ntail = 0;
+    if (host_round) {
+        int pinned = 0;
+        check(csaidx_cuda_host_is_pinned(in.q, &pinned));
+        if (pinned) ntail = std::min(plan.order.size(), host_fp32_tail(plan.order.size()));
+    }
+    const size_t tail0 = plan.order.size() - ntail;
+    constexpr int kTailSlot0 = 164;  // event slots 164..191: one per tail chunk
+    DeviceBuffer tailbuf;
+    if (ntail > 0) tailbuf = DeviceBuffer(e, ntail * slab_elems * sizeof(float));
     DeviceBuffer slab[kSlabs];
     if (dtype == CSAIDX_DTYPE_BF16 && !host_round) {
         for (auto& sb : slab) sb = DeviceBuffer(e, slab_elems * sizeof(float));
@@ -515,6 +531,14 @@ void run_chunked_rows_impl(const HostView& in, const ProblemDims& dims, const Dr
                 size_t rc = 0;  // ring pieces issued
                 for (size_t o = 0; o < plan.order.size(); ++o) {
                     const double t0 = now_ms();
+                    if (o >= tail0) {  // fp32 tail: rounded on the device
+                        {
+                            std::lock_guard<std::mutex> g(rounder.mu);
+                            rounder.converted = o + 1;
+                        }
+                        rounder.cv.notify_all();
+                        continue;
+                    }
                     if (!ring && o >= static_cast<size_t>(hslabs)) {
                         {
                             std::unique_lock<std::mutex> g(rounder.mu);
@@ -599,7 +623,7 @@ void run_chunked_rows_impl(const HostView& in, const ProblemDims& dims, const Dr
         for (int64_t b = 0; b < B; ++b) {
             const int64_t lrow = b * out_rows + plan.out_row0[c];
             const int64_t hrow = in.local_rows ? lrow : b * dims.seq_len + s0;
-            if (!ring)  // (ring: the rounding thread has enqueued the pieces on this lane)
+            if (!ring && o < tail0)  // (ring: the rounding thread has enqueued the pieces on this lane; tail: fp32 below)
                 check(csaidx_cuda_copy(e, q.as<uint16_t>() + lrow * qrow, hslab[o % hslabs] + b * rows * qrow,
                                        static_cast<size_t>(rows * qrow) * sizeof(uint16_t)));
             check(csaidx_cuda_copy(e, w.as<float>() + lrow * dims.heads, in.w + hrow * dims.heads,
@@ -632,6 +656,18 @@ void run_chunked_rows_impl(const HostView& in, const ProblemDims& dims, const Dr
         check(csaidx_engine_signal(e, static_cast<int>(o % 32)));
     };
     auto convert = [&](size_t o) {  // on the main lane, after chunk o's copy
+        if (host_round && o >= tail0) {  // fp32 tail chunk: its rows arrived early on lane 3
+            const size_t t = o - tail0;
+            const size_t c = plan.order[o];
+            const int64_t rows = std::min(plan.cs, dims.seq_len - plan.starts[c]);
+            check(csaidx_engine_await(e, kTailSlot0 + static_cast<int>(t)));
+            for (int64_t b = 0; b < B; ++b) {
+                const int64_t lrow = b * out_rows + plan.out_row0[c];
+                check(csaidx_cuda_to_bf16(e, tailbuf.as<float>() + t * slab_elems + b * rows * qrow,
+                                          q.as<uint16_t>() + lrow * qrow, rows * qrow, strict ? 1 : 0));
+            }
+            return;
+        }
         if (dtype != CSAIDX_DTYPE_BF16 || host_round) return;
         const size_t c = plan.order[o];
         const int64_t rows = std::min(plan.cs, dims.seq_len - plan.starts[c]);
@@ -667,6 +703,20 @@ void run_chunked_rows_impl(const HostView& in, const ProblemDims& dims, const Dr
                 kc.upload(in.kc, static_cast<size_t>(dims.kc_elems()) * sizeof(float));
             }
             upload_raw(0);
+            if (ntail > 0) {
+                check(csaidx_engine_use_lane(e, 3));
+                for (size_t t = 0; t < ntail; ++t) {
+                    const size_t c = plan.order[tail0 + t];
+                    const int64_t s0 = plan.starts[c], rows = std::min(plan.cs, dims.seq_len - s0);
+                    for (int64_t b = 0; b < B; ++b) {
+                        const int64_t hrow = in.local_rows ? b * out_rows + plan.out_row0[c] : b * dims.seq_len + s0;
+                        check(csaidx_cuda_copy(e, tailbuf.as<float>() + t * slab_elems + b * rows * qrow,
+                                               in.q + hrow * qrow, static_cast<size_t>(rows * qrow) * sizeof(float)));
+                    }
+                    check(csaidx_engine_signal(e, kTailSlot0 + static_cast<int>(t)));
+                }
+                check(csaidx_engine_use_lane(e, kInLane));
+            }
         }
         if (o + 1 < plan.order.size()) upload_raw(o + 1);
         check(csaidx_engine_use_lane(e, kMainLane));
@@ -696,7 +746,7 @@ void run_chunked_rows_impl(const HostView& in, const ProblemDims& dims, const Dr
         csaidx_engine_take_inexact(e, &seen);
         throw;
     }
-    if (dtype == CSAIDX_DTYPE_BF16 && !host_round && !strict) {
+    if (dtype == CSAIDX_DTYPE_BF16 && (!host_round || ntail > 0) && !strict) {
         // the device rounding noted a q value bf16 cannot hold
         int seen = 0;
         check(csaidx_engine_take_inexact(e, &seen));

@@ -210,6 +210,17 @@ int host_ring_pieces() {
     return std::clamp(v != nullptr ? std::atoi(v) : 4, 2, 32);
 }
 
+size_t host_fp32_tail(size_t chunks) {
+    // Off by default: C3 e2e 125 ms with no tail, 133 ms with chunks / 8 and
+    // 150 ms with 24 fp32 chunks on the same box (profiles/r02_host_ring.md):
+    // the extra PCIe bytes beside the first chunks cost more than the
+    // rounding thread saves.
+    (void)chunks;
+    const char* v = std::getenv("CSAIDX_HOST_FP32_TAIL");
+    const long long n = v != nullptr ? std::atoll(v) : 0;
+    return static_cast<size_t>(std::clamp<long long>(n, 0, 27));
+}
+
 uint16_t host_bf16_rne(float x) {
     uint32_t u;
     std::memcpy(&u, &x, 4);

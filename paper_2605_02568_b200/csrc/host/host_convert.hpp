@@ -49,5 +49,9 @@ int64_t host_piece_bytes();
 // still in the host's last-level cache.
 bool host_ring_enabled();
 int host_ring_pieces();
+// Chunks at the end of the processing order sent as fp32 (pinned q) and
+// rounded on the device (CSAIDX_HOST_FP32_TAIL, at most 27; default 0:
+// measured slower).
+size_t host_fp32_tail(size_t chunks);
 
 }  // namespace csaidx::detail

@@ -437,6 +437,44 @@ def test_host_rounding_matches_device_rounding(orc, monkeypatch):
         assert np.array_equal(oi, si) and np.array_equal(bits(ov), bits(sv))
 
 
+@pytest.mark.parametrize("tail", ["0", "4", "27"])
+def test_fp32_tail_chunks_match_host_rounding(orc, monkeypatch, tail):
+    """Pinned q: the last chunks of the processing order cross PCIe as fp32
+    and are rounded on the device (CSAIDX_HOST_FP32_TAIL, opt-in)
+    — the same bytes as rounding every chunk on the host; a non-finite q row
+    in a tail chunk still raises, an inexact one still re-runs exactly."""
+    import torch
+
+    B, S, m, H, D, k = 2, 8192, 4, 64, 128, 64
+    q, kc, w = orc.generate_inputs(B, S, m, H, D, 5, bf16=True)
+    dims = api.ProblemDims.create(B, S, m, H, D, k)
+    cfg = api.DriverConfig(tile=api.TileConfig(256, S // m))
+    starts = list(range(0, S, 256))
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    qp, kcp, wp = pin(np.asarray(q, np.float32).reshape(B, S, H, D)), pin(np.asarray(kc, np.float32)), \
+        pin(np.asarray(w, np.float32).reshape(B, S, H))
+    monkeypatch.setenv("CSAIDX_HOST_FP32_TAIL", "0")
+    ri = torch.empty((B, S, k), dtype=torch.int64).pin_memory()
+    rv = torch.empty((B, S, k), dtype=torch.float32).pin_memory()
+    api.run_chunked_rows(qp, kcp, wp, dims, cfg, starts, ri, rv)
+    monkeypatch.setenv("CSAIDX_HOST_FP32_TAIL", tail)
+    gi, gv = torch.empty_like(ri).pin_memory(), torch.empty_like(rv).pin_memory()
+    api.run_chunked_rows(qp, kcp, wp, dims, cfg, starts, gi, gv)
+    assert torch.equal(gi, ri) and torch.equal(gv.view(torch.int32), rv.view(torch.int32))
+    # chunk 0 is processed last (latest chunk first): it is always in the tail
+    bad = qp.clone().pin_memory()
+    bad[1, 5, 7, 3] = float("nan")
+    with pytest.raises(InvalidArgument):
+        api.run_chunked_rows(bad, kcp, wp, dims, cfg, starts, gi, gv)
+    inexact = qp.clone().pin_memory()
+    inexact[0, 17, 0, 0] = 1.0000001
+    api.run_chunked_rows(inexact, kcp, wp, dims, cfg, starts, gi, gv)
+    scal = api.DriverConfig(tile=api.TileConfig(256, S // m), kernel=api.ScoreKernel.scalar)
+    si, sv = torch.empty_like(ri).pin_memory(), torch.empty_like(rv).pin_memory()
+    api.run_chunked_rows(inexact, kcp, wp, dims, scal, starts, si, sv)
+    assert torch.equal(gi, si) and torch.equal(gv.view(torch.int32), sv.view(torch.int32))
+
+
 def test_auto_detect_on_fp32_inputs_is_bit_exact_like_the_reference(orc):
     """the reference's auto_detect scores arbitrary fp32 operands
     with a kernel bit-identical to its scalar one (score.cpp:18-43). At the
